@@ -1,0 +1,145 @@
+/*
+ * slapo_b200.h — C ABI of the B200-native executor for Slapo's scheduled
+ * forward+backward step (libslapo_b200.so).
+ *
+ * Conventions: every function returns 0 on success, 1 on error, 2 on a
+ * schedule rule violation (R1..R5, proj/include/slapo/schedule.hpp:27-35);
+ * sb_last_error() returns the thread-local message. Never throws. Handles are
+ * opaque. Host buffers are plain double arrays (the reference's TensorValue
+ * payload); device entry points take device pointers, sizes and an explicit
+ * cudaStream_t (passed as void*) and only enqueue.
+ *
+ * Each entry point names the reference interface it replaces.
+ */
+#ifndef SLAPO_B200_H
+#define SLAPO_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct sb_model sb_model;       /* slapo::ModuleDef                    */
+typedef struct sb_schedule sb_schedule; /* slapo::Schedule (a path handle)     */
+typedef struct sb_executor sb_executor; /* slapo::Executor                     */
+
+const char* sb_last_error(void);
+int sb_version(void);
+
+/* ---------------------------------------------------------------- models */
+/* toy_bert / tp_two_linear / fig3c_exact / ffn_stack — proj/tests/support/fixtures.hpp:21-38 */
+int sb_model_toy_bert(int layers, int64_t hidden, int64_t heads, int64_t vocab, int64_t batch, int64_t seq,
+                      double dropout_p, sb_model** out);
+int sb_model_tp_two_linear(int64_t hidden, int64_t inner, int64_t batch, sb_model** out);
+int sb_model_fig3c(sb_model** out);
+int sb_model_ffn_stack(int n, int64_t hidden, int64_t batch, sb_model** out);
+/* load_model / save_model — proj/include/slapo/model_io.hpp:16-23 */
+int sb_model_from_json(const char* text, sb_model** out);
+int sb_model_to_json(const sb_model* m, char* buf, size_t cap, size_t* needed);
+/* f32 storage for every param and input (proj/tests/combos_test.cpp:90-100) */
+int sb_model_to_f32(sb_model* m);
+/* modules_structurally_equal — proj/include/slapo/module.hpp:127 */
+int sb_model_equal(const sb_model* a, const sb_model* b, int* equal);
+int sb_model_free(sb_model* m);
+/* declared_input_specs — proj/include/slapo/shape_inference.hpp:37 */
+int sb_model_num_inputs(const sb_model* m, int* n);
+int sb_model_input_shape(const sb_model* m, int idx, int64_t* dims, int* ndims /* in: cap, out: rank */);
+/* random_tensor(spec, seed, stream) — proj/include/slapo/executor.hpp:85 */
+int sb_model_random_input(const sb_model* m, int idx, uint64_t seed, uint64_t stream, double* out, size_t cap,
+                          size_t* n);
+/* init_param_rank(param at dotted path, rank) — proj/include/slapo/module.hpp:147 */
+int sb_model_param_values(const sb_model* m, const char* dotted, int rank, double* out, size_t cap, size_t* n);
+
+/* -------------------------------------------------------------- schedule */
+/* create_schedule / Schedule::at — proj/include/slapo/schedule.hpp:65-111 */
+int sb_schedule_create(const sb_model* m, int world_size, sb_schedule** out);
+int sb_schedule_at(const sb_schedule* s, const char* path, sb_schedule** out);
+int sb_schedule_trace(sb_schedule* s, int flatten, const char* leaves_csv);
+int sb_schedule_replace(sb_schedule* s, const char* library, const char* pattern /* NULL: whole module */);
+int sb_schedule_shard(sb_schedule* s, const char* params_csv, int axis);
+int sb_schedule_sync(sb_schedule* s, const char* type /* forward|backward|both */);
+int sb_schedule_checkpoint(sb_schedule* s, const char* pattern /* NULL: whole module */);
+int sb_schedule_define_pattern(sb_schedule* s, const char* name, const char* graph_json);
+int sb_schedule_fuse(sb_schedule* s, const char* pattern, const char* backend /* composed | sm100 */);
+int sb_schedule_pipeline_split(sb_schedule* s, const char* after_child);
+int sb_schedule_find(sb_schedule* s, const char* glob, int* count);
+/* load_schedule_script — proj/include/slapo/script.hpp:17 */
+int sb_schedule_load_script(sb_schedule* s, const char* text);
+int sb_schedule_num_warnings(const sb_schedule* s, int* n);
+/* Schedule::apply — proj/src/schedule.cpp:719-746 */
+int sb_schedule_apply(const sb_schedule* s, sb_model** out);
+int sb_schedule_free(sb_schedule* s);
+
+/* -------------------------------------------------------------- executor */
+/* Executor(root, mode, seed, world) — proj/include/slapo/executor.hpp:37-63.
+ * dtype: 0 = fp32, 1 = bf16 (fp32 accumulate). fused: 1 lowers fused regions and
+ * EfficientAttention to fused kernels, 0 runs them op-by-op. All `world` ranks
+ * live on the current device (the reference's lockstep simulator, with device
+ * collectives). */
+int sb_executor_create(const sb_model* m, int train, uint64_t seed, int world, int dtype, int fused, sb_executor** out);
+/* One process per GPU: this process is `rank` of `world`; collectives via NCCL. */
+int sb_nccl_unique_id(void* out128);
+int sb_executor_create_nccl(const sb_model* m, int train, uint64_t seed, int world, int rank, const void* unique_id128,
+                            int dtype, int fused, sb_executor** out);
+int sb_executor_free(sb_executor* e);
+int sb_executor_set_nan_guard(sb_executor* e, int on);
+/* Executor::forward (inputs replicated to every rank) */
+int sb_executor_forward(sb_executor* e, const double* const* inputs, int n_inputs);
+/* Executor::outputs_of_rank */
+int sb_executor_num_outputs(sb_executor* e, int rank, int* n);
+int sb_executor_output(sb_executor* e, int rank, int idx, double* out, size_t cap, size_t* n, int64_t* dims,
+                       int* ndims);
+/* Executor::backward_all_ranks (loss = sum of outputs) */
+int sb_executor_backward(sb_executor* e);
+int sb_executor_num_grads(sb_executor* e, int rank, int* n);
+int sb_executor_grad_name(sb_executor* e, int rank, int idx, char* buf, size_t cap);
+int sb_executor_grad(sb_executor* e, int rank, const char* dotted, double* out, size_t cap, size_t* n);
+int sb_executor_input_grad(sb_executor* e, int rank, int idx, double* out, size_t cap, size_t* n);
+/* Executor::ledger / collective_invocations */
+int sb_executor_ledger(sb_executor* e, int64_t* bytes);
+int sb_executor_collectives(sb_executor* e, int64_t* count);
+/* device-resident stepping for benchmarks: H2D of inputs (pinned host ok),
+ * one fwd+bwd (optionally through a captured CUDA graph), loss to host. */
+int sb_executor_upload_inputs(sb_executor* e, const double* const* inputs, int n_inputs);
+int sb_executor_step(sb_executor* e, int use_graph);
+int sb_executor_step_loss(sb_executor* e, int use_graph, float* loss_host);
+int sb_executor_synchronize(sb_executor* e);
+int sb_executor_stream(sb_executor* e, void** stream);
+int sb_executor_describe(sb_executor* e, char* buf, size_t cap);
+int sb_executor_profile(sb_executor* e, char* buf, size_t cap); /* per-op-kind ms of one step, JSON */
+int sb_executor_device_bytes(sb_executor* e, int64_t* bytes);
+
+/* ------------------------------------------------------- device kernels */
+/* dtype codes: 0 f32, 1 bf16, 2 f64. */
+/* linear_fwd / linear_dx / linear_dw / matmul_fwd — proj/src/executor.cpp:38-133 */
+int sb_gemm(const void* A, int ta, int64_t sAb, int64_t sAm, int64_t sAk, const void* B, int tb, int64_t sBb,
+            int64_t sBk, int64_t sBn, void* C, int tc, int64_t sCb, int64_t sCm, int64_t sCn, int64_t batch, int64_t M,
+            int64_t N, int64_t K, float alpha, int accumulate, const void* bias, int epilogue, void* aux, void* stream);
+int sb_gemm_engine(void);                /* engine of the last sb_gemm: 0 SIMT, 1 tcgen05 */
+int sb_gemm_force_simt(int on);
+/* dropout keep mask (apply_dropout, proj/src/executor.cpp:793-806): bit i of word i/32 =
+ * uniform01(hash_combine(exec_seed, node_seed), 0xd0, i) >= p */
+int sb_dropout_mask(uint32_t* bits, int64_t n, uint64_t exec_seed, uint64_t node_seed, double p, void* stream);
+/* eval_layernorm_mod / backward_layernorm_mod — proj/src/executor.cpp:699-740,1158-1197 */
+int sb_layernorm_fwd(const void* x, const void* gamma, const void* beta, void* y, float* mean, float* rstd, int dtype,
+                     int64_t rows, int64_t n, float eps, void* stream);
+/* fused bias+dropout+residual+LayerNorm (the .fuse'd output block) */
+int sb_bias_dropout_residual_ln_fwd(const void* partial, const void* bias, const void* residual, const void* gamma,
+                                    const void* beta, void* sum, void* y, float* mean, float* rstd, int dtype,
+                                    int64_t rows, int64_t n, float eps, uint64_t exec_seed, uint64_t node_seed,
+                                    double p, void* stream);
+/* EfficientAttention forward/backward (library.cpp:9-34 semantics) */
+int sb_attn_fwd(const void* q, const void* k, const void* v, void* o, int64_t ld_qkv, int64_t ld_o, float* lse,
+                int64_t B, int64_t S, int64_t nh, int64_t hd, float scale, uint64_t exec_seed, uint64_t node_seed,
+                double p, int dtype, void* stream);
+int sb_attn_bwd(const void* q, const void* k, const void* v, const void* o, int64_t ld_qkv, int64_t ld_o,
+                const float* lse, const void* dout, void* dq, void* dk, void* dv, float* delta, int64_t B, int64_t S,
+                int64_t nh, int64_t hd, float scale, uint64_t exec_seed, uint64_t node_seed, double p, int dtype,
+                void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SLAPO_B200_H */

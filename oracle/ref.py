@@ -1,0 +1,115 @@
+"""Oracle runner — TEST INFRASTRUCTURE ONLY (never imported by the product).
+
+Runs the reference executor compiled from /root/reference/proj by
+oracle/Makefile (`oracle/_ref/slapo_ref_driver`, a static binary that also
+travels to the GPU box) and reads back its dumps (format in ref_driver.cpp).
+Only tests/, __graft_entry__.smoke() and bench.py's CPU-baseline legs use it.
+"""
+from __future__ import annotations
+
+import json
+import os
+import struct
+import subprocess
+import tempfile
+from typing import Dict, Optional
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+DRIVER = os.path.join(HERE, "_ref", "slapo_ref_driver")
+
+
+def available() -> bool:
+    return os.path.exists(DRIVER)
+
+
+def read_dump(path: str) -> Dict[str, np.ndarray]:
+    out: Dict[str, np.ndarray] = {}
+    with open(path, "rb") as f:
+        data = f.read()
+    assert data[:4] == b"SBT1", path
+    off = 4
+    (n,) = struct.unpack_from("<I", data, off)
+    off += 4
+    for _ in range(n):
+        (ln,) = struct.unpack_from("<I", data, off)
+        off += 4
+        name = data[off:off + ln].decode()
+        off += ln
+        (rank,) = struct.unpack_from("<I", data, off)
+        off += 4
+        dims = struct.unpack_from("<%dq" % rank, data, off)
+        off += 8 * rank
+        cnt = int(np.prod(dims)) if rank else 1
+        arr = np.frombuffer(data, dtype="<f8", count=cnt, offset=off).copy()
+        off += 8 * cnt
+        out[name] = arr.reshape(dims)
+    return out
+
+
+class RefRun:
+    def __init__(self, outdir: str, meta: dict):
+        self.dir = outdir
+        self.meta = meta
+
+    def outputs(self, rank: int = 0):
+        d = read_dump(os.path.join(self.dir, "outputs.bin"))
+        return [d[k] for k in sorted(d) if k.startswith(f"r{rank}:out")]
+
+    def grads(self, rank: int = 0) -> Dict[str, np.ndarray]:
+        d = read_dump(os.path.join(self.dir, "grads.bin"))
+        p = f"r{rank}:"
+        return {k[len(p):]: v for k, v in d.items() if k.startswith(p) and not k[len(p):].startswith("@input")}
+
+    def input_grads(self, rank: int = 0):
+        d = read_dump(os.path.join(self.dir, "grads.bin"))
+        p = f"r{rank}:@input"
+        return [d[k] for k in sorted(d) if k.startswith(p)]
+
+    def params(self, rank: int = 0) -> Dict[str, np.ndarray]:
+        d = read_dump(os.path.join(self.dir, "params.bin"))
+        p = f"r{rank}:"
+        return {k[len(p):]: v for k, v in d.items() if k.startswith(p)}
+
+    def inputs(self):
+        d = read_dump(os.path.join(self.dir, "inputs.bin"))
+        return [d[k] for k in sorted(d)]
+
+    def model_json(self) -> str:
+        with open(os.path.join(self.dir, "model.json")) as f:
+            return f.read()
+
+
+def run(model: str = "toy_bert", schedule: Optional[str] = None, outdir: Optional[str] = None, timeout: int = 600,
+        **kw) -> RefRun:
+    """kw: layers, hidden, heads, vocab, batch, seq, p, dtype, world, mode, seed, input_seed,
+    backward, dump_params, tp_hidden, tp_inner, tp_batch, repeat, model_json (path)."""
+    if not available():
+        raise RuntimeError(f"oracle driver missing: build it with `make -C oracle` ({DRIVER})")
+    outdir = outdir or tempfile.mkdtemp(prefix="sbref_")
+    args = [DRIVER, "--model", model, "--out", outdir]
+    sched_file = None
+    if schedule:
+        if os.path.exists(schedule):
+            sched_file = schedule
+        else:
+            sched_file = os.path.join(outdir, "schedule.sch")
+            with open(sched_file, "w") as f:
+                f.write(schedule)
+        args += ["--schedule", sched_file]
+    for k, v in kw.items():
+        args += ["--" + k, str(v)]
+    r = subprocess.run(args, capture_output=True, text=True, timeout=timeout)
+    if r.returncode != 0:
+        raise RuntimeError(f"oracle failed ({r.returncode}): {r.stderr.strip()}")
+    meta = json.loads(r.stdout.strip().splitlines()[-1])
+    return RefRun(outdir, meta)
+
+
+def uniform01_probe(stream_seed: int, n: int) -> np.ndarray:
+    outdir = tempfile.mkdtemp(prefix="sbrng_")
+    r = subprocess.run([DRIVER, "--probe_rng", f"{stream_seed},{n}", "--out", outdir], capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(r.stderr)
+    return read_dump(os.path.join(outdir, "rng.bin"))["uniform01"]

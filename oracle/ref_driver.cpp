@@ -1,0 +1,206 @@
+// Oracle driver — TEST INFRASTRUCTURE, not product code.
+//
+// Links the reference's own slapo_core (built from /root/reference/proj/src by
+// oracle/Makefile) and runs the reference executor on a fixture model with a
+// schedule script, dumping everything the B200 executor is checked against:
+//   model.json     post-apply ModuleDef (save_model, proj/src/model_io.cpp:225)
+//   outputs.bin    forward outputs of every rank   (Executor::outputs_of_rank)
+//   grads.bin      param + input gradients, every rank (backward_all_ranks)
+//   params.bin     worker-local param values, every rank (init_param_rank)
+//   meta.json      collective count, ledger bytes, wall-clock timing
+// The dump format ("SBT1") is: magic, u32 count, then per tensor
+//   u32 name_len, name, u32 rank, i64 dims[rank], f64 data.
+//
+// Reference APIs used: toy_bert / tp_two_linear / fig3c_exact
+// (proj/tests/support/fixtures.cpp:79-171), load_schedule_script
+// (proj/src/script.cpp:74), Schedule::apply (proj/src/schedule.cpp:719),
+// Executor (proj/include/slapo/executor.hpp:37-63), random_tensor
+// (proj/src/executor.cpp:19), uniform01 (proj/include/slapo/rng.hpp:35).
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <fstream>
+#include <iostream>
+#include <map>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "slapo/executor.hpp"
+#include "slapo/model_io.hpp"
+#include "slapo/rng.hpp"
+#include "slapo/schedule.hpp"
+#include "slapo/script.hpp"
+#include "slapo/shape_inference.hpp"
+#include "support/fixtures.hpp"
+
+using namespace slapo;
+
+namespace {
+
+struct Named {
+    std::string name;
+    const TensorValue* t;
+};
+
+void write_dump(const std::string& path, const std::vector<std::pair<std::string, TensorValue>>& ts) {
+    std::ofstream out(path, std::ios::binary);
+    if (!out) throw Error("cannot write " + path);
+    out.write("SBT1", 4);
+    std::uint32_t n = static_cast<std::uint32_t>(ts.size());
+    out.write(reinterpret_cast<const char*>(&n), 4);
+    for (const auto& [name, t] : ts) {
+        std::uint32_t len = static_cast<std::uint32_t>(name.size());
+        out.write(reinterpret_cast<const char*>(&len), 4);
+        out.write(name.data(), len);
+        std::uint32_t rank = static_cast<std::uint32_t>(t.spec.shape.size());
+        out.write(reinterpret_cast<const char*>(&rank), 4);
+        for (auto d : t.spec.shape) out.write(reinterpret_cast<const char*>(&d), 8);
+        out.write(reinterpret_cast<const char*>(t.data.data()), t.data.size() * 8);
+    }
+}
+
+std::string read_file(const std::string& p) {
+    std::ifstream in(p, std::ios::binary);
+    if (!in) throw Error("cannot read " + p);
+    std::ostringstream ss;
+    ss << in.rdbuf();
+    return ss.str();
+}
+
+void to_f32(ModuleDef& m) {  // as combos_test.cpp:90-100
+    for (auto& p : m.params) p.spec.dtype = Dtype::F32;
+    if (m.forward) {
+        for (auto& n : m.forward->nodes)
+            if (n.kind == NodeKind::Input) n.attrs["dtype"] = std::string("f32");
+    }
+    for (auto& s : m.submodules) to_f32(*s.module);
+}
+
+void collect_params(const ModuleDef& m, const std::string& path, std::vector<std::pair<std::string, const ParamDef*>>& out) {
+    for (const auto& p : m.params) out.push_back({join_path(path, p.name), &p});
+    for (const auto& s : m.submodules) collect_params(*s.module, join_path(path, s.name), out);
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+    std::map<std::string, std::string> a = {
+        {"model", "toy_bert"}, {"layers", "2"}, {"hidden", "8"}, {"heads", "2"}, {"vocab", "28"},
+        {"batch", "4"}, {"seq", "4"}, {"p", "0.1"}, {"dtype", "f64"}, {"schedule", ""},
+        {"world", "1"}, {"mode", "train"}, {"seed", "123"}, {"input_seed", "9"}, {"out", ""},
+        {"backward", "1"}, {"dump_params", "0"}, {"probe_rng", ""}, {"model_json", ""},
+        {"tp_hidden", "8"}, {"tp_inner", "16"}, {"tp_batch", "4"}, {"repeat", "1"}};
+    for (int i = 1; i + 1 < argc; i += 2) {
+        std::string k = argv[i];
+        if (k.rfind("--", 0) != 0) { std::cerr << "bad arg " << k << "\n"; return 2; }
+        a[k.substr(2)] = argv[i + 1];
+    }
+    try {
+        if (!a["probe_rng"].empty()) {
+            // probe_rng "<stream_seed>,<n>": uniform01(stream, 0xd0, i) for i < n
+            // (the dropout draw, proj/src/executor.cpp:801) and hash_combine.
+            std::uint64_t s = std::stoull(a["probe_rng"].substr(0, a["probe_rng"].find(',')));
+            std::int64_t n = std::stoll(a["probe_rng"].substr(a["probe_rng"].find(',') + 1));
+            TensorValue u(TensorSpec{{n}, Dtype::F64});
+            for (std::int64_t i = 0; i < n; ++i) u.data[i] = uniform01(s, 0xd0, static_cast<std::uint64_t>(i));
+            write_dump(a["out"] + "/rng.bin", {{"uniform01", u}});
+            return 0;
+        }
+        ModuleDef model;
+        if (!a["model_json"].empty()) {
+            model = load_model(read_file(a["model_json"]));
+        } else if (a["model"] == "toy_bert") {
+            testing::BertConfig cfg;
+            cfg.layers = std::stoi(a["layers"]);
+            cfg.hidden = std::stoll(a["hidden"]);
+            cfg.heads = std::stoll(a["heads"]);
+            cfg.vocab = std::stoll(a["vocab"]);
+            cfg.batch = std::stoll(a["batch"]);
+            cfg.seq = std::stoll(a["seq"]);
+            cfg.dropout_p = std::stod(a["p"]);
+            model = testing::toy_bert(cfg);
+        } else if (a["model"] == "tp_two_linear") {
+            model = testing::tp_two_linear(std::stoll(a["tp_hidden"]), std::stoll(a["tp_inner"]),
+                                           std::stoll(a["tp_batch"]));
+        } else if (a["model"] == "fig3c") {
+            model = testing::fig3c_exact();
+        } else {
+            throw Error("unknown model " + a["model"]);
+        }
+        if (a["dtype"] == "f32") to_f32(model);
+        int world = std::stoi(a["world"]);
+        WorldConfig wc;
+        wc.world_size = world;
+        Schedule sch(model, wc);
+        if (!a["schedule"].empty()) load_schedule_script(sch, read_file(a["schedule"]));
+        ApplyResult res = sch.apply();
+        const std::string out = a["out"];
+        if (!out.empty()) {
+            std::ofstream(out + "/model.json") << save_model(res.model);
+            std::ofstream(out + "/original.json") << save_model(model);
+        }
+        if (a["dump_params"] == "1" && !out.empty()) {
+            std::vector<std::pair<std::string, const ParamDef*>> ps;
+            collect_params(res.model, "", ps);
+            std::vector<std::pair<std::string, TensorValue>> dump;
+            for (int r = 0; r < world; ++r)
+                for (auto& [name, p] : ps) dump.push_back({"r" + std::to_string(r) + ":" + name, init_param_rank(*p, r)});
+            write_dump(out + "/params.bin", dump);
+        }
+        ExecMode mode = a["mode"] == "verify" ? ExecMode::Verify : ExecMode::Train;
+        std::uint64_t seed = std::stoull(a["seed"]);
+        auto specs = declared_input_specs(*model.forward);
+        std::vector<TensorValue> inputs;
+        for (std::size_t i = 0; i < specs.size(); ++i)
+            inputs.push_back(random_tensor(specs[i], std::stoull(a["input_seed"]), i));
+
+        int repeat = std::stoi(a["repeat"]);
+        double fwd_s = 0, bwd_s = 0;
+        std::vector<std::pair<std::string, TensorValue>> outs, grads;
+        std::int64_t coll_fwd = 0, coll_total = 0, ledger = 0;
+        for (int it = 0; it < repeat; ++it) {
+            Executor ex(res.model, mode, seed, world);
+            auto t0 = std::chrono::steady_clock::now();
+            ex.forward(inputs);
+            auto t1 = std::chrono::steady_clock::now();
+            coll_fwd = ex.collective_invocations();
+            ledger = ex.ledger().retained_bytes;
+            std::vector<GradientMap> gm;
+            if (a["backward"] == "1") gm = ex.backward_all_ranks();
+            auto t2 = std::chrono::steady_clock::now();
+            coll_total = ex.collective_invocations();
+            fwd_s += std::chrono::duration<double>(t1 - t0).count();
+            bwd_s += std::chrono::duration<double>(t2 - t1).count();
+            if (it + 1 == repeat) {
+                for (int r = 0; r < world; ++r) {
+                    auto o = ex.outputs_of_rank(r);
+                    for (std::size_t i = 0; i < o.size(); ++i)
+                        outs.push_back({"r" + std::to_string(r) + ":out" + std::to_string(i), o[i]});
+                }
+                for (int r = 0; r < static_cast<int>(gm.size()); ++r) {
+                    for (auto& [k, v] : gm[r].params) grads.push_back({"r" + std::to_string(r) + ":" + k, v});
+                    for (std::size_t i = 0; i < gm[r].inputs.size(); ++i)
+                        grads.push_back({"r" + std::to_string(r) + ":@input" + std::to_string(i), gm[r].inputs[i]});
+                }
+            }
+        }
+        if (!out.empty()) {
+            write_dump(out + "/outputs.bin", outs);
+            write_dump(out + "/grads.bin", grads);
+            std::vector<std::pair<std::string, TensorValue>> ins;
+            for (std::size_t i = 0; i < inputs.size(); ++i) ins.push_back({"input" + std::to_string(i), inputs[i]});
+            write_dump(out + "/inputs.bin", ins);
+        }
+        std::ostringstream meta;
+        meta << "{\"collectives_fwd\": " << coll_fwd << ", \"collectives_total\": " << coll_total
+             << ", \"ledger_bytes\": " << ledger << ", \"fwd_s\": " << fwd_s / repeat
+             << ", \"bwd_s\": " << bwd_s / repeat << ", \"repeat\": " << repeat << "}";
+        if (!out.empty()) std::ofstream(out + "/meta.json") << meta.str() << "\n";
+        std::cout << meta.str() << std::endl;
+    } catch (const std::exception& e) {
+        std::cerr << "oracle error: " << e.what() << "\n";
+        return 1;
+    }
+    return 0;
+}

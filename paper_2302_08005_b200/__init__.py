@@ -1,0 +1,478 @@
+"""B200-native executor for Slapo's scheduled forward+backward step.
+
+Python mirror of the reference's C++ interface, bound to the C ABI of
+``libslapo_b200.so`` (include/slapo_b200.h):
+
+* models: ``toy_bert``, ``tp_two_linear``, ``fig3c_exact``, ``ffn_stack``
+  (proj/tests/support/fixtures.hpp:21-38), ``Model.from_json`` (model_io.hpp:16);
+* ``create_schedule`` / ``Schedule`` with ``at``, ``trace``, ``replace``, ``shard``,
+  ``sync``, ``checkpoint``, ``define_pattern``, ``fuse``, ``pipeline_split``,
+  ``find``, ``load_script``, ``apply`` (proj/include/slapo/schedule.hpp:65-111);
+* ``Executor(model, mode, seed, world)`` with ``forward``, ``outputs_of_rank``,
+  ``backward``, ``backward_all_ranks``, ``ledger``, ``collective_invocations``,
+  ``set_nan_guard`` (proj/include/slapo/executor.hpp:37-63).
+
+There is no CPU fallback: importing this package without the built library
+raises, and every executor call runs the sm_100a kernels.
+"""
+from __future__ import annotations
+
+import ctypes
+import json
+import os
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libslapo_b200.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+        "(there is no CPU fallback for the B200 executor)")
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+_c = ctypes
+_P = _c.c_void_p
+_i64 = _c.c_int64
+_u64 = _c.c_uint64
+_dp = _c.POINTER(_c.c_double)
+
+
+def _sig(name, *argtypes):
+    f = getattr(_lib, name)
+    f.argtypes = list(argtypes)
+    f.restype = _c.c_int
+    return f
+
+
+_lib.sb_last_error.restype = _c.c_char_p
+for _n, _a in {
+    "sb_model_toy_bert": (_c.c_int, _i64, _i64, _i64, _i64, _i64, _c.c_double, _c.POINTER(_P)),
+    "sb_model_tp_two_linear": (_i64, _i64, _i64, _c.POINTER(_P)),
+    "sb_model_fig3c": (_c.POINTER(_P),),
+    "sb_model_ffn_stack": (_c.c_int, _i64, _i64, _c.POINTER(_P)),
+    "sb_model_from_json": (_c.c_char_p, _c.POINTER(_P)),
+    "sb_model_to_json": (_P, _c.c_char_p, _c.c_size_t, _c.POINTER(_c.c_size_t)),
+    "sb_model_to_f32": (_P,),
+    "sb_model_equal": (_P, _P, _c.POINTER(_c.c_int)),
+    "sb_model_free": (_P,),
+    "sb_model_num_inputs": (_P, _c.POINTER(_c.c_int)),
+    "sb_model_input_shape": (_P, _c.c_int, _c.POINTER(_i64), _c.POINTER(_c.c_int)),
+    "sb_model_random_input": (_P, _c.c_int, _u64, _u64, _dp, _c.c_size_t, _c.POINTER(_c.c_size_t)),
+    "sb_model_param_values": (_P, _c.c_char_p, _c.c_int, _dp, _c.c_size_t, _c.POINTER(_c.c_size_t)),
+    "sb_schedule_create": (_P, _c.c_int, _c.POINTER(_P)),
+    "sb_schedule_at": (_P, _c.c_char_p, _c.POINTER(_P)),
+    "sb_schedule_trace": (_P, _c.c_int, _c.c_char_p),
+    "sb_schedule_replace": (_P, _c.c_char_p, _c.c_char_p),
+    "sb_schedule_shard": (_P, _c.c_char_p, _c.c_int),
+    "sb_schedule_sync": (_P, _c.c_char_p),
+    "sb_schedule_checkpoint": (_P, _c.c_char_p),
+    "sb_schedule_define_pattern": (_P, _c.c_char_p, _c.c_char_p),
+    "sb_schedule_fuse": (_P, _c.c_char_p, _c.c_char_p),
+    "sb_schedule_pipeline_split": (_P, _c.c_char_p),
+    "sb_schedule_find": (_P, _c.c_char_p, _c.POINTER(_c.c_int)),
+    "sb_schedule_load_script": (_P, _c.c_char_p),
+    "sb_schedule_num_warnings": (_P, _c.POINTER(_c.c_int)),
+    "sb_schedule_apply": (_P, _c.POINTER(_P)),
+    "sb_schedule_free": (_P,),
+    "sb_executor_create": (_P, _c.c_int, _u64, _c.c_int, _c.c_int, _c.c_int, _c.POINTER(_P)),
+    "sb_nccl_unique_id": (_P,),
+    "sb_executor_create_nccl": (_P, _c.c_int, _u64, _c.c_int, _c.c_int, _P, _c.c_int, _c.c_int, _c.POINTER(_P)),
+    "sb_executor_free": (_P,),
+    "sb_executor_set_nan_guard": (_P, _c.c_int),
+    "sb_executor_forward": (_P, _c.POINTER(_dp), _c.c_int),
+    "sb_executor_num_outputs": (_P, _c.c_int, _c.POINTER(_c.c_int)),
+    "sb_executor_output": (_P, _c.c_int, _c.c_int, _dp, _c.c_size_t, _c.POINTER(_c.c_size_t), _c.POINTER(_i64),
+                           _c.POINTER(_c.c_int)),
+    "sb_executor_backward": (_P,),
+    "sb_executor_num_grads": (_P, _c.c_int, _c.POINTER(_c.c_int)),
+    "sb_executor_grad_name": (_P, _c.c_int, _c.c_int, _c.c_char_p, _c.c_size_t),
+    "sb_executor_grad": (_P, _c.c_int, _c.c_char_p, _dp, _c.c_size_t, _c.POINTER(_c.c_size_t)),
+    "sb_executor_input_grad": (_P, _c.c_int, _c.c_int, _dp, _c.c_size_t, _c.POINTER(_c.c_size_t)),
+    "sb_executor_ledger": (_P, _c.POINTER(_i64)),
+    "sb_executor_collectives": (_P, _c.POINTER(_i64)),
+    "sb_executor_upload_inputs": (_P, _c.POINTER(_dp), _c.c_int),
+    "sb_executor_step": (_P, _c.c_int),
+    "sb_executor_step_loss": (_P, _c.c_int, _c.POINTER(_c.c_float)),
+    "sb_executor_synchronize": (_P,),
+    "sb_executor_stream": (_P, _c.POINTER(_P)),
+    "sb_executor_describe": (_P, _c.c_char_p, _c.c_size_t),
+    "sb_executor_profile": (_P, _c.c_char_p, _c.c_size_t),
+    "sb_executor_device_bytes": (_P, _c.POINTER(_i64)),
+    "sb_gemm_force_simt": (_c.c_int,),
+    "sb_dropout_mask": (_P, _i64, _u64, _u64, _c.c_double, _P),
+}.items():
+    _sig(_n, *_a)
+_lib.sb_gemm_engine.restype = _c.c_int
+
+
+class SlapoError(RuntimeError):
+    """slapo::Error (proj/include/slapo/attrs.hpp:21-24)."""
+
+
+class RuleError(SlapoError):
+    """slapo::RuleError R1..R5 (proj/include/slapo/schedule.hpp:27-35)."""
+
+    def __init__(self, msg: str):
+        super().__init__(msg)
+        self.rule = msg.split(":", 1)[0]
+
+
+def _check(rc: int) -> None:
+    if rc == 0:
+        return
+    msg = _lib.sb_last_error().decode()
+    if rc == 2:
+        raise RuleError(msg)
+    raise SlapoError(msg)
+
+
+def lib() -> ctypes.CDLL:
+    return _lib
+
+
+# ------------------------------------------------------------------- models
+class Model:
+    """A ModuleDef handle (proj/include/slapo/module.hpp:88-124)."""
+
+    def __init__(self, handle):
+        self._h = handle
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            _lib.sb_model_free(self._h)
+            self._h = None
+
+    @staticmethod
+    def _make(fn, *args) -> "Model":
+        h = _P()
+        _check(fn(*args, _c.byref(h)))
+        return Model(h)
+
+    @staticmethod
+    def from_json(text: str) -> "Model":
+        return Model._make(_lib.sb_model_from_json, text.encode())
+
+    def to_json(self) -> str:
+        need = _c.c_size_t()
+        _check(_lib.sb_model_to_json(self._h, None, 0, _c.byref(need)))
+        buf = _c.create_string_buffer(need.value)
+        _check(_lib.sb_model_to_json(self._h, buf, need.value, _c.byref(need)))
+        return buf.value.decode()
+
+    def to_f32(self) -> "Model":
+        _check(_lib.sb_model_to_f32(self._h))
+        return self
+
+    def structurally_equal(self, other: "Model") -> bool:
+        eq = _c.c_int()
+        _check(_lib.sb_model_equal(self._h, other._h, _c.byref(eq)))
+        return bool(eq.value)
+
+    def input_shapes(self) -> List[List[int]]:
+        n = _c.c_int()
+        _check(_lib.sb_model_num_inputs(self._h, _c.byref(n)))
+        out = []
+        for i in range(n.value):
+            dims = (_i64 * 16)()
+            nd = _c.c_int(16)
+            _check(_lib.sb_model_input_shape(self._h, i, dims, _c.byref(nd)))
+            out.append([dims[k] for k in range(nd.value)])
+        return out
+
+    def random_inputs(self, seed: int) -> List[np.ndarray]:
+        """random_tensor(spec_i, seed, stream=i) for every declared input."""
+        res = []
+        for i, shape in enumerate(self.input_shapes()):
+            n = int(np.prod(shape)) if shape else 1
+            a = np.empty(n, dtype=np.float64)
+            nn = _c.c_size_t()
+            _check(_lib.sb_model_random_input(self._h, i, seed, i, a.ctypes.data_as(_dp), n, _c.byref(nn)))
+            res.append(a.reshape(shape))
+        return res
+
+    def param_values(self, dotted: str, rank: int = 0) -> np.ndarray:
+        """init_param_rank(param, rank): bit-exact host materialisation."""
+        nn = _c.c_size_t()
+        _check(_lib.sb_model_param_values(self._h, dotted.encode(), rank, None, 0, _c.byref(nn)))
+        a = np.empty(nn.value, dtype=np.float64)
+        _check(_lib.sb_model_param_values(self._h, dotted.encode(), rank, a.ctypes.data_as(_dp), nn.value,
+                                          _c.byref(nn)))
+        return a
+
+
+def toy_bert(layers=24, hidden=8, heads=2, vocab=28, batch=4, seq=4, dropout_p=0.1) -> Model:
+    return Model._make(_lib.sb_model_toy_bert, layers, hidden, heads, vocab, batch, seq, dropout_p)
+
+
+def tp_two_linear(hidden=8, inner=16, batch=4) -> Model:
+    return Model._make(_lib.sb_model_tp_two_linear, hidden, inner, batch)
+
+
+def fig3c_exact() -> Model:
+    return Model._make(_lib.sb_model_fig3c)
+
+
+def ffn_stack(n=24, hidden=4, batch=2) -> Model:
+    return Model._make(_lib.sb_model_ffn_stack, n, hidden, batch)
+
+
+# ----------------------------------------------------------------- schedule
+def _graph_json(pattern) -> str:
+    return pattern if isinstance(pattern, str) else json.dumps(pattern)
+
+
+class Schedule:
+    """Handle into the schedule tree (proj/include/slapo/schedule.hpp:60-111)."""
+
+    def __init__(self, handle, keep=None):
+        self._h = handle
+        self._keep = keep
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            _lib.sb_schedule_free(self._h)
+            self._h = None
+
+    def at(self, path: str) -> "Schedule":
+        h = _P()
+        _check(_lib.sb_schedule_at(self._h, path.encode(), _c.byref(h)))
+        return Schedule(h, self)
+
+    def __getitem__(self, path: str) -> "Schedule":
+        return self.at(path)
+
+    def trace(self, flatten: bool = False, leaves: Sequence[str] = ()) -> None:
+        _check(_lib.sb_schedule_trace(self._h, int(flatten), ",".join(leaves).encode()))
+
+    def replace(self, library: str, pattern: Optional[str] = None) -> None:
+        _check(_lib.sb_schedule_replace(self._h, library.encode(), pattern.encode() if pattern else None))
+
+    def shard(self, params: Sequence[str] | str, axis: int) -> None:
+        if isinstance(params, str):
+            params = [params]
+        _check(_lib.sb_schedule_shard(self._h, ",".join(params).encode(), axis))
+
+    def sync(self, type: str) -> None:  # noqa: A002 - the reference's argument name
+        _check(_lib.sb_schedule_sync(self._h, type.encode()))
+
+    def checkpoint(self, pattern: Optional[str] = None) -> None:
+        _check(_lib.sb_schedule_checkpoint(self._h, pattern.encode() if pattern else None))
+
+    def define_pattern(self, name: str, graph) -> None:
+        _check(_lib.sb_schedule_define_pattern(self._h, name.encode(), _graph_json(graph).encode()))
+
+    def fuse(self, pattern: str, backend: str = "composed") -> None:
+        _check(_lib.sb_schedule_fuse(self._h, pattern.encode(), backend.encode()))
+
+    def pipeline_split(self, after_child: str) -> None:
+        _check(_lib.sb_schedule_pipeline_split(self._h, after_child.encode()))
+
+    def find(self, glob: str) -> int:
+        n = _c.c_int()
+        _check(_lib.sb_schedule_find(self._h, glob.encode(), _c.byref(n)))
+        return n.value
+
+    def load_script(self, text: str) -> None:
+        _check(_lib.sb_schedule_load_script(self._h, text.encode()))
+
+    def num_warnings(self) -> int:
+        n = _c.c_int()
+        _check(_lib.sb_schedule_num_warnings(self._h, _c.byref(n)))
+        return n.value
+
+    def apply(self) -> Model:
+        h = _P()
+        _check(_lib.sb_schedule_apply(self._h, _c.byref(h)))
+        return Model(h)
+
+
+def create_schedule(model: Model, world_size: int = 1) -> Schedule:
+    h = _P()
+    _check(_lib.sb_schedule_create(model._h, world_size, _c.byref(h)))
+    return Schedule(h)
+
+
+def schedule_path(name: str) -> str:
+    return os.path.join(_HERE, "schedules", name)
+
+
+# ----------------------------------------------------------------- executor
+@dataclass
+class GradientMap:
+    """slapo::GradientMap (proj/include/slapo/executor.hpp:27-30)."""
+    params: Dict[str, np.ndarray] = field(default_factory=dict)
+    inputs: List[np.ndarray] = field(default_factory=list)
+
+
+_DTYPES = {"fp32": 0, "f32": 0, "float32": 0, "bf16": 1, "bfloat16": 1}
+
+
+class Executor:
+    """slapo::Executor on B200 (proj/include/slapo/executor.hpp:37-63).
+
+    ``world`` ranks of a sharded model run in lockstep on the current device
+    (collectives are device-side rank-ascending sums, the reference's
+    simulator semantics); ``nccl=(rank, unique_id)`` instead makes this process
+    one rank of a one-process-per-GPU job with NCCL collectives.
+    """
+
+    def __init__(self, model: Model, mode: str = "train", seed: int = 0, world: int = 1, dtype: str = "fp32",
+                 fused: bool = True, nccl: Optional[tuple] = None):
+        h = _P()
+        train = 1 if mode == "train" else 0
+        if mode not in ("train", "verify"):
+            raise ValueError("mode must be 'train' or 'verify'")
+        dt = _DTYPES[dtype]
+        self.world = world
+        self.nccl_rank = None
+        if nccl is None:
+            _check(_lib.sb_executor_create(model._h, train, seed, world, dt, int(fused), _c.byref(h)))
+        else:
+            rank, uid = nccl
+            ub = _c.create_string_buffer(bytes(uid), 128)
+            _check(_lib.sb_executor_create_nccl(model._h, train, seed, world, rank, ub, dt, int(fused), _c.byref(h)))
+            self.nccl_rank = rank
+        self._h = h
+        self._shapes = model.input_shapes()
+        self._pinned = None
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            _lib.sb_executor_free(self._h)
+            self._h = None
+
+    def _in_ptrs(self, inputs: Sequence[np.ndarray]):
+        arrs = [np.ascontiguousarray(np.asarray(x, dtype=np.float64)) for x in inputs]
+        for a, s in zip(arrs, self._shapes):
+            if a.size != (int(np.prod(s)) if s else 1):
+                raise SlapoError(f"input of size {a.size} does not match declared shape {s}")
+        ptrs = (_dp * len(arrs))(*[a.ctypes.data_as(_dp) for a in arrs])
+        return arrs, ptrs
+
+    def set_nan_guard(self, on: bool) -> None:
+        _check(_lib.sb_executor_set_nan_guard(self._h, int(on)))
+
+    def forward(self, inputs: Sequence[np.ndarray]) -> List[np.ndarray]:
+        arrs, ptrs = self._in_ptrs(inputs)
+        _check(_lib.sb_executor_forward(self._h, ptrs, len(arrs)))
+        return self.outputs_of_rank(self.nccl_rank or 0)
+
+    def outputs_of_rank(self, rank: int) -> List[np.ndarray]:
+        n = _c.c_int()
+        _check(_lib.sb_executor_num_outputs(self._h, rank, _c.byref(n)))
+        outs = []
+        for i in range(n.value):
+            nn = _c.c_size_t()
+            dims = (_i64 * 16)()
+            nd = _c.c_int(16)
+            _check(_lib.sb_executor_output(self._h, rank, i, None, 0, _c.byref(nn), dims, _c.byref(nd)))
+            a = np.empty(nn.value, dtype=np.float64)
+            _check(_lib.sb_executor_output(self._h, rank, i, a.ctypes.data_as(_dp), nn.value, _c.byref(nn), dims,
+                                           _c.byref(nd)))
+            outs.append(a.reshape([dims[k] for k in range(nd.value)]))
+        return outs
+
+    def _grad_map(self, rank: int) -> GradientMap:
+        n = _c.c_int()
+        _check(_lib.sb_executor_num_grads(self._h, rank, _c.byref(n)))
+        gm = GradientMap()
+        buf = _c.create_string_buffer(4096)
+        for i in range(n.value):
+            _check(_lib.sb_executor_grad_name(self._h, rank, i, buf, 4096))
+            name = buf.value
+            nn = _c.c_size_t()
+            _check(_lib.sb_executor_grad(self._h, rank, name, None, 0, _c.byref(nn)))
+            a = np.empty(nn.value, dtype=np.float64)
+            _check(_lib.sb_executor_grad(self._h, rank, name, a.ctypes.data_as(_dp), nn.value, _c.byref(nn)))
+            gm.params[name.decode()] = a
+        for i in range(len(self._shapes)):
+            nn = _c.c_size_t()
+            _check(_lib.sb_executor_input_grad(self._h, rank, i, None, 0, _c.byref(nn)))
+            a = np.empty(nn.value, dtype=np.float64)
+            _check(_lib.sb_executor_input_grad(self._h, rank, i, a.ctypes.data_as(_dp), nn.value, _c.byref(nn)))
+            gm.inputs.append(a)
+        return gm
+
+    def backward_all_ranks(self) -> List[GradientMap]:
+        _check(_lib.sb_executor_backward(self._h))
+        ranks = [self.nccl_rank] if self.nccl_rank is not None else range(self.world)
+        return [self._grad_map(r) for r in ranks]
+
+    def backward(self) -> GradientMap:
+        return self.backward_all_ranks()[0]
+
+    def ledger(self) -> int:
+        v = _i64()
+        _check(_lib.sb_executor_ledger(self._h, _c.byref(v)))
+        return v.value
+
+    def collective_invocations(self) -> int:
+        v = _i64()
+        _check(_lib.sb_executor_collectives(self._h, _c.byref(v)))
+        return v.value
+
+    # -- device-resident stepping (bench.py) --
+    def upload_inputs(self, inputs: Sequence[np.ndarray]) -> None:
+        arrs, ptrs = self._in_ptrs(inputs)
+        _check(_lib.sb_executor_upload_inputs(self._h, ptrs, len(arrs)))
+
+    def step(self, use_graph: bool = True) -> None:
+        _check(_lib.sb_executor_step(self._h, int(use_graph)))
+
+    def step_loss(self, use_graph: bool = True) -> float:
+        v = _c.c_float()
+        _check(_lib.sb_executor_step_loss(self._h, int(use_graph), _c.byref(v)))
+        return v.value
+
+    def synchronize(self) -> None:
+        _check(_lib.sb_executor_synchronize(self._h))
+
+    def stream(self) -> int:
+        s = _P()
+        _check(_lib.sb_executor_stream(self._h, _c.byref(s)))
+        return s.value or 0
+
+    def describe(self) -> dict:
+        buf = _c.create_string_buffer(1 << 16)
+        _check(_lib.sb_executor_describe(self._h, buf, 1 << 16))
+        return json.loads(buf.value.decode())
+
+    def profile(self) -> dict:
+        buf = _c.create_string_buffer(1 << 16)
+        _check(_lib.sb_executor_profile(self._h, buf, 1 << 16))
+        return json.loads(buf.value.decode())
+
+    def device_bytes(self) -> int:
+        v = _i64()
+        _check(_lib.sb_executor_device_bytes(self._h, _c.byref(v)))
+        return v.value
+
+
+def nccl_unique_id() -> bytes:
+    buf = _c.create_string_buffer(128)
+    _check(_lib.sb_nccl_unique_id(buf))
+    return buf.raw
+
+
+def run_forward(model: Model, inputs, mode="verify", seed=0, **kw) -> List[np.ndarray]:
+    """run_forward (proj/include/slapo/executor.hpp:66)."""
+    return Executor(model, mode, seed, 1, **kw).forward(inputs)
+
+
+def run_backward(model: Model, inputs, mode="verify", seed=0, **kw) -> GradientMap:
+    """run_backward (proj/include/slapo/executor.hpp:70)."""
+    ex = Executor(model, mode, seed, 1, **kw)
+    ex.forward(inputs)
+    return ex.backward()
+
+
+def run_sharded(model: Model, inputs, world_size: int, mode="verify", seed=0, **kw) -> List[np.ndarray]:
+    """run_sharded (proj/include/slapo/executor.hpp:74)."""
+    if world_size < 2:
+        raise SlapoError("run_sharded requires world_size > 1")
+    return Executor(model, mode, seed, world_size, **kw).forward(inputs)

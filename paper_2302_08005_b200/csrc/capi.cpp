@@ -1,0 +1,492 @@
+// extern "C" boundary (include/slapo_b200.h). Translates handles and host
+// buffers to the C++ host layer; every exception becomes a status code plus a
+// thread-local message (RuleError -> 2).
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstring>
+#include <dlfcn.h>
+#include <sstream>
+
+#include "../../include/slapo_b200.h"
+#include "host/executor.hpp"
+#include "host/rng.hpp"
+#include "host/schedule.hpp"
+
+using namespace sb;
+
+struct sb_model {
+    Module m;
+};
+struct sb_schedule {
+    Schedule s;
+};
+struct sb_executor {
+    std::unique_ptr<Executor> ex;
+    std::vector<GradMap> grads;
+    int world = 1;
+    bool nccl = false;
+    int rank = 0;
+    float* dloss = nullptr;
+};
+
+namespace {
+thread_local std::string g_err;
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const RuleError& e) {
+        g_err = e.what();
+        return 2;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    } catch (...) {
+        g_err = "unknown error";
+        return 1;
+    }
+}
+
+std::vector<std::string> csv(const char* s) {
+    std::vector<std::string> out;
+    if (!s) return out;
+    std::string cur;
+    for (const char* p = s; *p; ++p) {
+        if (*p == ',') {
+            if (!cur.empty()) out.push_back(cur);
+            cur.clear();
+        } else if (*p != ' ') {
+            cur += *p;
+        }
+    }
+    if (!cur.empty()) out.push_back(cur);
+    return out;
+}
+
+void copy_out(const std::vector<double>& v, double* out, size_t cap, size_t* n) {
+    if (n) *n = v.size();
+    if (out && cap >= v.size()) std::memcpy(out, v.data(), v.size() * sizeof(double));
+    else if (out) throw Error("output buffer too small: need " + std::to_string(v.size()) + " doubles");
+}
+
+const GradMap& gmap(sb_executor* e, int rank) {
+    if (e->grads.empty()) throw Error("backward requires a completed forward run");
+    if (e->nccl) {
+        if (rank != e->rank) throw Error("rank lives in another process");
+        return e->grads[0];
+    }
+    if (rank < 0 || rank >= (int)e->grads.size()) throw Error("rank out of range");
+    return e->grads[(size_t)rank];
+}
+}  // namespace
+
+extern "C" {
+
+const char* sb_last_error(void) { return g_err.c_str(); }
+int sb_version(void) { return 1; }
+
+// ------------------------------------------------------------------ models
+int sb_model_toy_bert(int layers, int64_t hidden, int64_t heads, int64_t vocab, int64_t batch, int64_t seq, double p,
+                      sb_model** out) {
+    return guard([&] {
+        BertConfig c;
+        c.layers = layers;
+        c.hidden = hidden;
+        c.heads = heads;
+        c.vocab = vocab;
+        c.batch = batch;
+        c.seq = seq;
+        c.dropout_p = p;
+        *out = new sb_model{toy_bert(c)};
+    });
+}
+int sb_model_tp_two_linear(int64_t hidden, int64_t inner, int64_t batch, sb_model** out) {
+    return guard([&] { *out = new sb_model{tp_two_linear(hidden, inner, batch)}; });
+}
+int sb_model_fig3c(sb_model** out) {
+    return guard([&] { *out = new sb_model{fig3c_exact()}; });
+}
+int sb_model_ffn_stack(int n, int64_t hidden, int64_t batch, sb_model** out) {
+    return guard([&] { *out = new sb_model{ffn_stack(n, hidden, batch)}; });
+}
+int sb_model_from_json(const char* text, sb_model** out) {
+    return guard([&] { *out = new sb_model{load_model_json(text)}; });
+}
+int sb_model_to_json(const sb_model* m, char* buf, size_t cap, size_t* needed) {
+    return guard([&] {
+        std::string s = save_model_json(m->m);
+        if (needed) *needed = s.size() + 1;
+        if (buf && cap >= s.size() + 1) std::memcpy(buf, s.c_str(), s.size() + 1);
+    });
+}
+int sb_model_to_f32(sb_model* m) {
+    return guard([&] { convert_to_f32(m->m); });
+}
+int sb_model_equal(const sb_model* a, const sb_model* b, int* eq) {
+    return guard([&] { *eq = modules_equal(a->m, b->m) ? 1 : 0; });
+}
+int sb_model_free(sb_model* m) {
+    delete m;
+    return 0;
+}
+int sb_model_num_inputs(const sb_model* m, int* n) {
+    return guard([&] { *n = (int)declared_inputs(*m->m.forward).size(); });
+}
+int sb_model_input_shape(const sb_model* m, int idx, int64_t* dims, int* ndims) {
+    return guard([&] {
+        auto specs = declared_inputs(*m->m.forward);
+        auto& s = specs.at((size_t)idx);
+        if (*ndims < (int)s.shape.size()) throw Error("dims buffer too small");
+        for (size_t i = 0; i < s.shape.size(); ++i) dims[i] = s.shape[i];
+        *ndims = (int)s.shape.size();
+    });
+}
+int sb_model_random_input(const sb_model* m, int idx, uint64_t seed, uint64_t stream, double* out, size_t cap,
+                          size_t* n) {
+    return guard([&] {
+        auto specs = declared_inputs(*m->m.forward);
+        copy_out(random_tensor(specs.at((size_t)idx), seed, stream).data, out, cap, n);
+    });
+}
+int sb_model_param_values(const sb_model* m, const char* dotted, int rank, double* out, size_t cap, size_t* n) {
+    return guard([&] {
+        const Param* p = m->m.resolve_param(dotted);
+        if (!p) throw Error(std::string("unknown param '") + dotted + "'");
+        copy_out(param_rank(*p, rank).data, out, cap, n);
+    });
+}
+
+// ---------------------------------------------------------------- schedule
+int sb_schedule_create(const sb_model* m, int world, sb_schedule** out) {
+    return guard([&] { *out = new sb_schedule{Schedule(m->m, WorldConfig{world})}; });
+}
+int sb_schedule_at(const sb_schedule* s, const char* path, sb_schedule** out) {
+    return guard([&] { *out = new sb_schedule{s->s.at(path)}; });
+}
+int sb_schedule_trace(sb_schedule* s, int flatten, const char* leaves) {
+    return guard([&] {
+        TraceSpec t;
+        t.flatten = flatten != 0;
+        t.leaves = csv(leaves);
+        s->s.trace(t);
+    });
+}
+int sb_schedule_replace(sb_schedule* s, const char* lib, const char* pattern) {
+    return guard([&] {
+        if (pattern && *pattern) s->s.replace_at(lib, pattern);
+        else s->s.replace_with(lib);
+    });
+}
+int sb_schedule_shard(sb_schedule* s, const char* params, int axis) {
+    return guard([&] { s->s.shard(csv(params), axis); });
+}
+int sb_schedule_sync(sb_schedule* s, const char* type) {
+    return guard([&] { s->s.sync(type); });
+}
+int sb_schedule_checkpoint(sb_schedule* s, const char* pattern) {
+    return guard([&] {
+        if (pattern && *pattern) s->s.checkpoint_at(pattern);
+        else s->s.checkpoint();
+    });
+}
+int sb_schedule_define_pattern(sb_schedule* s, const char* name, const char* graph_json) {
+    return guard([&] { s->s.define_pattern(name, parse_graph_json(graph_json)); });
+}
+int sb_schedule_fuse(sb_schedule* s, const char* pattern, const char* backend) {
+    return guard([&] { s->s.fuse_at(pattern, backend ? backend : "composed"); });
+}
+int sb_schedule_pipeline_split(sb_schedule* s, const char* after) {
+    return guard([&] { s->s.pipeline_split(after); });
+}
+int sb_schedule_find(sb_schedule* s, const char* glob, int* count) {
+    return guard([&] { *count = (int)s->s.find(std::string(glob)).size(); });
+}
+int sb_schedule_load_script(sb_schedule* s, const char* text) {
+    return guard([&] { load_schedule_script(s->s, text); });
+}
+int sb_schedule_num_warnings(const sb_schedule* s, int* n) {
+    return guard([&] { *n = (int)s->s.warnings().size(); });
+}
+int sb_schedule_apply(const sb_schedule* s, sb_model** out) {
+    return guard([&] { *out = new sb_model{s->s.apply().model}; });
+}
+int sb_schedule_free(sb_schedule* s) {
+    delete s;
+    return 0;
+}
+
+// ---------------------------------------------------------------- executor
+static DT dt_of(int d) {
+    if (d == 0) return sbk::F32;
+    if (d == 1) return sbk::BF16;
+    throw Error("dtype must be 0 (fp32) or 1 (bf16)");
+}
+int sb_executor_create(const sb_model* m, int train, uint64_t seed, int world, int dtype, int fused, sb_executor** out) {
+    return guard([&] {
+        auto* e = new sb_executor;
+        try {
+            e->ex = std::make_unique<Executor>(m->m, train != 0, seed, world, dt_of(dtype), CommConfig{}, fused != 0);
+        } catch (...) {
+            delete e;
+            throw;
+        }
+        e->world = world;
+        *out = e;
+    });
+}
+int sb_nccl_unique_id(void* out128) {
+    return guard([&] {
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) throw Error("NCCL not available");
+        auto f = (ncclResult_t(*)(ncclUniqueId*))dlsym(h, "ncclGetUniqueId");
+        ncclUniqueId id;
+        if (!f || f(&id) != ncclSuccess) throw Error("ncclGetUniqueId failed");
+        std::memcpy(out128, &id, sizeof(id));
+    });
+}
+int sb_executor_create_nccl(const sb_model* m, int train, uint64_t seed, int world, int rank, const void* uid, int dtype,
+                            int fused, sb_executor** out) {
+    return guard([&] {
+        CommConfig c;
+        c.nccl = true;
+        c.rank = rank;
+        c.unique_id.assign((const char*)uid, (const char*)uid + 128);
+        auto* e = new sb_executor;
+        try {
+            e->ex = std::make_unique<Executor>(m->m, train != 0, seed, world, dt_of(dtype), c, fused != 0);
+        } catch (...) {
+            delete e;
+            throw;
+        }
+        e->world = world;
+        e->nccl = true;
+        e->rank = rank;
+        *out = e;
+    });
+}
+int sb_executor_free(sb_executor* e) {
+    if (e && e->dloss) cudaFree(e->dloss);
+    delete e;
+    return 0;
+}
+int sb_executor_set_nan_guard(sb_executor* e, int on) {
+    return guard([&] { e->ex->set_nan_guard(on != 0); });
+}
+int sb_executor_forward(sb_executor* e, const double* const* inputs, int n) {
+    return guard([&] {
+        e->grads.clear();
+        e->ex->upload_inputs_raw(inputs, n);
+        e->ex->forward_uploaded();
+    });
+}
+int sb_executor_num_outputs(sb_executor* e, int rank, int* n) {
+    return guard([&] { *n = (int)e->ex->outputs_of_rank(rank).size(); });
+}
+int sb_executor_output(sb_executor* e, int rank, int idx, double* out, size_t cap, size_t* n, int64_t* dims, int* ndims) {
+    return guard([&] {
+        auto outs = e->ex->outputs_of_rank(rank);
+        auto& t = outs.at((size_t)idx);
+        if (dims && ndims) {
+            if (*ndims < (int)t.spec.shape.size()) throw Error("dims buffer too small");
+            for (size_t i = 0; i < t.spec.shape.size(); ++i) dims[i] = t.spec.shape[i];
+            *ndims = (int)t.spec.shape.size();
+        }
+        copy_out(t.data, out, cap, n);
+    });
+}
+int sb_executor_backward(sb_executor* e) {
+    return guard([&] { e->grads = e->ex->backward_all_ranks(); });
+}
+int sb_executor_num_grads(sb_executor* e, int rank, int* n) {
+    return guard([&] { *n = (int)gmap(e, rank).params.size(); });
+}
+int sb_executor_grad_name(sb_executor* e, int rank, int idx, char* buf, size_t cap) {
+    return guard([&] {
+        auto& g = gmap(e, rank);
+        if (idx < 0 || idx >= (int)g.params.size()) throw Error("grad index out of range");
+        auto it = g.params.begin();
+        std::advance(it, idx);
+        if (cap < it->first.size() + 1) throw Error("name buffer too small");
+        std::memcpy(buf, it->first.c_str(), it->first.size() + 1);
+    });
+}
+int sb_executor_grad(sb_executor* e, int rank, const char* dotted, double* out, size_t cap, size_t* n) {
+    return guard([&] {
+        auto& g = gmap(e, rank);
+        auto it = g.params.find(dotted);
+        if (it == g.params.end()) throw Error(std::string("no gradient for '") + dotted + "'");
+        copy_out(it->second.data, out, cap, n);
+    });
+}
+int sb_executor_input_grad(sb_executor* e, int rank, int idx, double* out, size_t cap, size_t* n) {
+    return guard([&] { copy_out(gmap(e, rank).inputs.at((size_t)idx).data, out, cap, n); });
+}
+int sb_executor_ledger(sb_executor* e, int64_t* bytes) {
+    return guard([&] { *bytes = e->ex->ledger_bytes(); });
+}
+int sb_executor_collectives(sb_executor* e, int64_t* c) {
+    return guard([&] { *c = e->ex->collective_invocations(); });
+}
+int sb_executor_upload_inputs(sb_executor* e, const double* const* inputs, int n) {
+    return guard([&] { e->ex->upload_inputs_raw(inputs, n); });
+}
+int sb_executor_step(sb_executor* e, int use_graph) {
+    return guard([&] {
+        if (use_graph) {
+            e->ex->launch_graph();
+        } else {
+            e->ex->run_forward();
+            e->ex->run_backward();
+        }
+    });
+}
+int sb_executor_step_loss(sb_executor* e, int use_graph, float* loss_host) {
+    return guard([&] {
+        if (!e->dloss && cudaMalloc(&e->dloss, 4) != cudaSuccess) throw Error("cudaMalloc failed");
+        if (use_graph) {
+            e->ex->launch_graph();
+        } else {
+            e->ex->run_forward();
+            e->ex->run_backward();
+        }
+        e->ex->enqueue_loss(e->dloss);
+        if (cudaMemcpyAsync(loss_host, e->dloss, 4, cudaMemcpyDeviceToHost, (cudaStream_t)e->ex->stream()) != cudaSuccess)
+            throw Error("loss copy failed");
+        e->ex->synchronize();
+    });
+}
+int sb_executor_synchronize(sb_executor* e) {
+    return guard([&] { e->ex->synchronize(); });
+}
+int sb_executor_stream(sb_executor* e, void** s) {
+    return guard([&] { *s = e->ex->stream(); });
+}
+int sb_executor_describe(sb_executor* e, char* buf, size_t cap) {
+    return guard([&] {
+        std::string s = e->ex->describe();
+        if (cap < s.size() + 1) throw Error("buffer too small");
+        std::memcpy(buf, s.c_str(), s.size() + 1);
+    });
+}
+int sb_executor_profile(sb_executor* e, char* buf, size_t cap) {
+    return guard([&] {
+        auto p = e->ex->profile_step();
+        std::ostringstream o;
+        o << "{";
+        for (size_t i = 0; i < p.size(); ++i) o << (i ? ", " : "") << "\"" << p[i].first << "\": " << p[i].second;
+        o << "}";
+        std::string s = o.str();
+        if (cap < s.size() + 1) throw Error("buffer too small");
+        std::memcpy(buf, s.c_str(), s.size() + 1);
+    });
+}
+int sb_executor_device_bytes(sb_executor* e, int64_t* b) {
+    return guard([&] { *b = (int64_t)e->ex->device_bytes(); });
+}
+
+// ------------------------------------------------------------------ kernels
+static sbk::DT kdt(int d) {
+    if (d < 0 || d > 2) throw Error("dtype code must be 0, 1 or 2");
+    return (sbk::DT)d;
+}
+int sb_gemm(const void* A, int ta, int64_t sAb, int64_t sAm, int64_t sAk, const void* B, int tb, int64_t sBb, int64_t sBk,
+            int64_t sBn, void* C, int tc, int64_t sCb, int64_t sCm, int64_t sCn, int64_t batch, int64_t M, int64_t N,
+            int64_t K, float alpha, int accumulate, const void* bias, int epilogue, void* aux, void* stream) {
+    return guard([&] {
+        sbk::Gemm g;
+        g.A = A;
+        g.ta = kdt(ta);
+        g.sAb = sAb;
+        g.sAm = sAm;
+        g.sAk = sAk;
+        g.B = B;
+        g.tb = kdt(tb);
+        g.sBb = sBb;
+        g.sBk = sBk;
+        g.sBn = sBn;
+        g.C = C;
+        g.tc = kdt(tc);
+        g.sCb = sCb;
+        g.sCm = sCm;
+        g.sCn = sCn;
+        g.batch = batch;
+        g.M = M;
+        g.N = N;
+        g.K = K;
+        g.alpha = alpha;
+        g.accumulate = accumulate != 0;
+        g.bias = bias;
+        g.tbias = g.tc == sbk::F32 ? g.ta : g.tc;
+        g.epilogue = epilogue;
+        g.aux = aux;
+        sbk::gemm(g, (cudaStream_t)stream);
+    });
+}
+int sb_gemm_engine(void) { return sbk::gemm_last_engine(); }
+int sb_gemm_force_simt(int on) {
+    sbk::gemm_force_simt(on != 0);
+    return 0;
+}
+int sb_dropout_mask(uint32_t* bits, int64_t n, uint64_t exec_seed, uint64_t node_seed, double p, void* stream) {
+    return guard([&] {
+        u64 s1 = hash_combine(hash_combine(exec_seed, node_seed), 0xd0);
+        sbk::dropout_mask(bits, n, s1, dropout_threshold(p), (cudaStream_t)stream);
+    });
+}
+int sb_layernorm_fwd(const void* x, const void* gamma, const void* beta, void* y, float* mean, float* rstd, int dtype,
+                     int64_t rows, int64_t n, float eps, void* stream) {
+    return guard([&] {
+        sbk::layernorm_fwd(x, gamma, beta, kdt(dtype), y, mean, rstd, kdt(dtype), rows, n, eps, (cudaStream_t)stream);
+    });
+}
+int sb_bias_dropout_residual_ln_fwd(const void* partial, const void* bias, const void* residual, const void* gamma,
+                                    const void* beta, void* sum, void* y, float* mean, float* rstd, int dtype, int64_t rows,
+                                    int64_t n, float eps, uint64_t exec_seed, uint64_t node_seed, double p, void* stream) {
+    return guard([&] {
+        u64 s1 = hash_combine(hash_combine(exec_seed, node_seed), 0xd0);
+        u64 thr = p > 0 ? dropout_threshold(p) : 0;
+        sbk::bias_dropout_residual_ln_fwd(partial, bias, residual, gamma, beta, kdt(dtype), sum, y, mean, rstd, kdt(dtype),
+                                          rows, n, eps, s1, thr, (float)(1.0 / (1.0 - p)), (cudaStream_t)stream);
+    });
+}
+static sbk::Attn mk_attn(const void* q, const void* k, const void* v, void* o, int64_t ld_qkv, int64_t ld_o, float* lse,
+                         int64_t B, int64_t S, int64_t nh, int64_t hd, float scale, uint64_t es, uint64_t ns, double p,
+                         int dtype) {
+    sbk::Attn a;
+    a.q = q;
+    a.k = k;
+    a.v = v;
+    a.o = o;
+    a.ld_q = a.ld_k = a.ld_v = ld_qkv;
+    a.ld_o = ld_o;
+    a.lse = lse;
+    a.B = B;
+    a.S = S;
+    a.nh = nh;
+    a.hd = hd;
+    a.scale = scale;
+    a.s1 = p > 0 ? hash_combine(hash_combine(es, ns), 0xd0) : 0;
+    a.thr = p > 0 ? dropout_threshold(p) : 0;
+    a.dscale = (float)(1.0 / (1.0 - p));
+    a.t = kdt(dtype);
+    return a;
+}
+int sb_attn_fwd(const void* q, const void* k, const void* v, void* o, int64_t ld_qkv, int64_t ld_o, float* lse, int64_t B,
+                int64_t S, int64_t nh, int64_t hd, float scale, uint64_t es, uint64_t ns, double p, int dtype, void* stream) {
+    return guard([&] {
+        sbk::attn_fwd(mk_attn(q, k, v, o, ld_qkv, ld_o, lse, B, S, nh, hd, scale, es, ns, p, dtype), (cudaStream_t)stream);
+    });
+}
+int sb_attn_bwd(const void* q, const void* k, const void* v, const void* o, int64_t ld_qkv, int64_t ld_o, const float* lse,
+                const void* dout, void* dq, void* dk, void* dv, float* delta, int64_t B, int64_t S, int64_t nh, int64_t hd,
+                float scale, uint64_t es, uint64_t ns, double p, int dtype, void* stream) {
+    return guard([&] {
+        sbk::Attn a = mk_attn(q, k, v, (void*)o, ld_qkv, ld_o, (float*)lse, B, S, nh, hd, scale, es, ns, p, dtype);
+        sbk::attn_bwd(a, dout, ld_o, dq, dk, dv, ld_qkv, ld_qkv, ld_qkv, delta, (cudaStream_t)stream);
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,1222 @@
+// B200 executor runtime: arena allocation, forward/backward launch lists,
+// checkpoint recompute, collectives (device-local lockstep or NCCL), CUDA
+// graph capture. Semantics per op mirror proj/src/executor.cpp (cited inline).
+#include "executor.hpp"
+
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstring>
+#include <numeric>
+#include <set>
+#include <sstream>
+
+#include "rng.hpp"
+
+namespace sb {
+
+#define CK(x)                                                                                       \
+    do {                                                                                            \
+        cudaError_t e_ = (x);                                                                       \
+        if (e_ != cudaSuccess) throw Error(std::string("CUDA error: ") + cudaGetErrorString(e_) + " at " #x); \
+    } while (0)
+
+// ------------------------------------------------------------------ NCCL (dlopen)
+namespace {
+struct Nccl {
+    void* h = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+    void load() {
+        if (h) return;
+        for (const char* n : {"libnccl.so.2", "libnccl.so"}) {
+            h = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
+            if (h) break;
+        }
+        if (!h) throw Error("NCCL not available: dlopen(libnccl.so.2) failed");
+        CommInitRank = (decltype(CommInitRank))dlsym(h, "ncclCommInitRank");
+        AllReduce = (decltype(AllReduce))dlsym(h, "ncclAllReduce");
+        AllGather = (decltype(AllGather))dlsym(h, "ncclAllGather");
+        CommDestroy = (decltype(CommDestroy))dlsym(h, "ncclCommDestroy");
+        GetErrorString = (decltype(GetErrorString))dlsym(h, "ncclGetErrorString");
+        if (!CommInitRank || !AllReduce || !AllGather) throw Error("NCCL symbols missing");
+    }
+    void check(ncclResult_t r, const char* what) {
+        if (r != ncclSuccess) throw Error(std::string("NCCL error in ") + what + ": " + GetErrorString(r));
+    }
+};
+Nccl& nccl() {
+    static Nccl n;
+    return n;
+}
+ncclDataType_t nccl_dt(DT t) { return t == sbk::F32 ? ncclFloat32 : t == sbk::BF16 ? ncclBfloat16 : ncclFloat64; }
+
+size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+}  // namespace
+
+// ------------------------------------------------------------------ per rank
+struct RankCtx {
+    Plan P;
+    char* base = nullptr;
+    size_t total = 0;
+    std::vector<char*> fptr, gptr;  // per storage
+    char* ws = nullptr;             // workspace
+    size_t ws_bytes = 0;
+    char* tmp = nullptr;            // grad-conversion temp
+    size_t tmp_bytes = 0;
+    size_t scratch_grad_bytes = 0;
+    char* scratch_grad = nullptr;
+    std::vector<std::pair<size_t, size_t>> region_grad_span;  // per region: offset,bytes in grad scratch
+};
+
+struct Step {
+    int kind;  // 0 backward of op, 1 recompute forward op, 2 zero grad scratch of region
+    int idx;
+};
+
+class ExecutorImpl {
+public:
+    bool train;
+    u64 seed;
+    int world;
+    DT cdt;
+    CommConfig comm;
+    bool nan_guard = false;
+    std::vector<RankCtx> ranks;  // Local: world contexts; Nccl: 1
+    std::vector<Step> bsteps;
+    cudaStream_t stream = nullptr;
+    ncclComm_t ncomm = nullptr;
+    i64 collectives = 0;
+    bool ran_forward = false;
+    cudaGraphExec_t gexec = nullptr;
+    cudaGraph_t graph = nullptr;
+    int launches = 0;
+    int* nan_flag = nullptr;
+    // profiling
+    bool profiling = false;
+    std::vector<std::pair<std::string, std::pair<cudaEvent_t, cudaEvent_t>>> prof;
+
+    int my_rank(int idx) const { return comm.nccl ? comm.rank : idx; }
+
+    ExecutorImpl(const Module& root, bool tr, u64 sd, int w, DT c, const CommConfig& cc, bool fused)
+        : train(tr), seed(sd), world(w), cdt(c), comm(cc) {
+        if (world < 1) throw Error("world_size must be >= 1");
+        CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+        int nr = comm.nccl ? 1 : world;
+        ranks.resize((size_t)nr);
+        for (int i = 0; i < nr; ++i) {
+            LowerOptions lo;
+            lo.rank = my_rank(i);
+            lo.world = world;
+            lo.train = train;
+            lo.seed = seed;
+            lo.cdt = cdt;
+            lo.fused_kernels = fused;
+            ranks[(size_t)i].P = lower(root, lo);
+            if (i > 0 && ranks[(size_t)i].P.structure() != ranks[0].P.structure())
+                throw Error("per-rank plans differ structurally; lockstep execution impossible");
+        }
+        build_backward_steps();
+        for (auto& r : ranks) allocate(r);
+        if (comm.nccl && world > 1) {
+            nccl().load();
+            ncclUniqueId id;
+            if (comm.unique_id.size() != sizeof(id)) throw Error("nccl unique id must be 128 bytes");
+            std::memcpy(&id, comm.unique_id.data(), sizeof(id));
+            nccl().check(nccl().CommInitRank(&ncomm, world, id, comm.rank), "ncclCommInitRank");
+        }
+        CK(cudaMalloc(&nan_flag, sizeof(int)));
+        sbk::init_workspace();
+    }
+
+    ~ExecutorImpl() {
+        if (gexec) cudaGraphExecDestroy(gexec);
+        if (graph) cudaGraphDestroy(graph);
+        for (auto& r : ranks)
+            if (r.base) cudaFree(r.base);
+        if (nan_flag) cudaFree(nan_flag);
+        if (ncomm && nccl().CommDestroy) nccl().CommDestroy(ncomm);
+        if (stream) cudaStreamDestroy(stream);
+    }
+
+    // -------------------------------------------------------------- plan
+    static std::set<int> grad_writes(const Plan& P, const Op& op) {
+        // storages whose gradients this op's backward writes
+        std::set<int> s;
+        auto add = [&](int v) { s.insert(P.views[(size_t)v].gst); };
+        switch (op.k) {
+            case K::Embedding: add(op.in[1]); break;
+            case K::AllReduce:
+                if (op.allreduce) add(op.in[0]);
+                break;
+            case K::Cast:
+                if (P.st[(size_t)P.views[(size_t)op.out[0]].st].dt != sbk::F64) add(op.in[0]);
+                break;
+            default:
+                for (int v : op.in) add(v);
+        }
+        return s;
+    }
+
+    void build_backward_steps() {
+        const Plan& P = ranks[0].P;
+        std::vector<bool> has(P.st.size(), false);
+        for (int v : P.outputs) has[(size_t)P.views[(size_t)v].gst] = true;
+        auto any_out = [&](const Op& op) {
+            for (int v : op.out)
+                if (has[(size_t)P.views[(size_t)v].gst]) return true;
+            return false;
+        };
+        auto mark = [&](const Op& op) {
+            for (int s : grad_writes(P, op)) has[(size_t)s] = true;
+        };
+        int i = (int)P.fwd.size() - 1;
+        while (i >= 0) {
+            const Op& op = P.fwd[(size_t)i];
+            if (op.region >= 0) {
+                const Region& R = P.regions[(size_t)op.region];
+                // reference: backward_checkpoint re-runs the region with a tape,
+                // then reverses the sub-tape (executor.cpp:1093-1120)
+                bool flows = false;
+                for (int j = R.first_op; j <= R.last_op; ++j) flows |= any_out(P.fwd[(size_t)j]);
+                if (flows) {
+                    bsteps.push_back({2, op.region});
+                    for (int j = R.first_op; j <= R.last_op; ++j) bsteps.push_back({1, j});
+                    for (int j = R.last_op; j >= R.first_op; --j) {
+                        if (!any_out(P.fwd[(size_t)j])) continue;
+                        bsteps.push_back({0, j});
+                        mark(P.fwd[(size_t)j]);
+                    }
+                }
+                i = R.first_op - 1;
+                continue;
+            }
+            if (any_out(op)) {
+                bsteps.push_back({0, i});
+                mark(op);
+            }
+            --i;
+        }
+    }
+
+    size_t workspace_need(const Plan& P) {
+        size_t ws = 1 << 20;
+        auto rows_of = [&](int v) { return P.views[(size_t)v].numel() / std::max<i64>(1, P.views[(size_t)v].shape.empty() ? 1 : P.views[(size_t)v].shape.back()); };
+        for (auto& op : P.fwd) {
+            switch (op.k) {
+                case K::LayerNorm:
+                    ws = std::max(ws, sbk::layernorm_bwd_workspace(rows_of(op.in[0]), P.views[(size_t)op.in[0]].shape.back()));
+                    break;
+                case K::FusedLinearResLN:
+                    ws = std::max(ws, sbk::bdrln_bwd_workspace(rows_of(op.out[0]), P.views[(size_t)op.out[0]].shape.back()));
+                    break;
+                case K::Linear:
+                case K::FusedLinearGelu:
+                    ws = std::max(ws, sbk::bias_grad_workspace(rows_of(op.out[0]), P.views[(size_t)op.out[0]].shape.back()));
+                    break;
+                case K::FlashAttn: ws = std::max(ws, (size_t)P.views[(size_t)op.out[1]].numel() * 4); break;
+                case K::Embedding: ws = std::max(ws, sbk::embedding_bwd_workspace(P.views[(size_t)op.in[0]].numel())); break;
+                case K::AllGather:
+                    ws = std::max(ws, (size_t)P.views[(size_t)op.out[0]].numel() * (size_t)sbk::dt_bytes(cdt));
+                    break;
+                default: break;
+            }
+        }
+        return align_up(ws);
+    }
+
+    void allocate(RankCtx& r) {
+        Plan& P = r.P;
+        size_t off = 0;
+        std::vector<size_t> foff(P.st.size(), SIZE_MAX), goff(P.st.size(), SIZE_MAX);
+        // persistent forward
+        for (size_t i = 0; i < P.st.size(); ++i) {
+            auto& s = P.st[i];
+            if (!s.has_fwd || s.region >= 0) continue;
+            foff[i] = off;
+            off = align_up(off + (size_t)s.numel * (size_t)sbk::dt_bytes(s.dt));
+        }
+        // persistent grads
+        auto wants_grad = [&](const Storage& s) {
+            if (s.kind == SKind::Aux) return false;
+            if (s.kind == SKind::Act && s.dt == sbk::F64) return false;
+            return true;
+        };
+        size_t gstart = off;
+        for (size_t i = 0; i < P.st.size(); ++i) {
+            auto& s = P.st[i];
+            if (!wants_grad(s) || s.region >= 0) continue;
+            goff[i] = off;
+            off = align_up(off + (size_t)s.numel * (size_t)sbk::dt_bytes(s.gdt));
+        }
+        size_t gend = off;
+        // checkpoint scratch: every region starts at the same base
+        size_t sf = 0, sg = 0;
+        std::vector<size_t> rf(P.regions.size(), 0), rg(P.regions.size(), 0);
+        std::vector<size_t> lf(P.st.size(), 0), lg(P.st.size(), 0);
+        for (size_t i = 0; i < P.st.size(); ++i) {
+            auto& s = P.st[i];
+            if (s.region < 0) continue;
+            if (s.has_fwd) {
+                lf[i] = rf[(size_t)s.region];
+                rf[(size_t)s.region] = align_up(rf[(size_t)s.region] + (size_t)s.numel * (size_t)sbk::dt_bytes(s.dt));
+            }
+            if (wants_grad(s)) {
+                lg[i] = rg[(size_t)s.region];
+                rg[(size_t)s.region] = align_up(rg[(size_t)s.region] + (size_t)s.numel * (size_t)sbk::dt_bytes(s.gdt));
+            }
+        }
+        for (size_t x : rf) sf = std::max(sf, x);
+        for (size_t x : rg) sg = std::max(sg, x);
+        size_t sf_off = off;
+        off += sf;
+        size_t sg_off = off;
+        off += sg;
+        r.ws_bytes = workspace_need(P);
+        size_t ws_off = off;
+        off += r.ws_bytes;
+        // grad-conversion temp: largest activation view
+        size_t tmp = 256;
+        for (auto& v : P.views) tmp = std::max(tmp, (size_t)v.numel() * (size_t)sbk::dt_bytes(cdt));
+        r.tmp_bytes = align_up(tmp);
+        size_t tmp_off = off;
+        off += r.tmp_bytes;
+        r.total = off;
+        CK(cudaMalloc(&r.base, r.total));
+        CK(cudaMemset(r.base, 0, r.total));
+        r.fptr.assign(P.st.size(), nullptr);
+        r.gptr.assign(P.st.size(), nullptr);
+        for (size_t i = 0; i < P.st.size(); ++i) {
+            auto& s = P.st[i];
+            if (s.region >= 0) {
+                if (s.has_fwd) r.fptr[i] = r.base + sf_off + lf[i];
+                if (wants_grad(s)) r.gptr[i] = r.base + sg_off + lg[i];
+            } else {
+                if (foff[i] != SIZE_MAX) r.fptr[i] = r.base + foff[i];
+                if (goff[i] != SIZE_MAX) r.gptr[i] = r.base + goff[i];
+            }
+        }
+        r.ws = r.base + ws_off;
+        r.tmp = r.base + tmp_off;
+        r.scratch_grad = r.base + sg_off;
+        r.region_grad_span.clear();
+        for (size_t k = 0; k < P.regions.size(); ++k) r.region_grad_span.push_back({sg_off, rg[k]});
+        persistent_grad_span = {gstart, gend - gstart};
+        // parameters: host init (bit-exact with the reference) -> compute dtype
+        for (auto& [name, t] : P.param_init) {
+            int v = -1;
+            for (auto& pv : P.params)
+                if (pv.first == name) v = pv.second;
+            upload_f64(r, P.views[(size_t)v].st, t.data);
+        }
+        P.param_init.clear();
+        P.param_init.shrink_to_fit();
+    }
+    std::pair<size_t, size_t> persistent_grad_span{0, 0};
+
+    void upload_f64(RankCtx& r, int st, const std::vector<double>& data) {
+        auto& s = r.P.st[(size_t)st];
+        double* d = nullptr;
+        CK(cudaMalloc(&d, data.size() * sizeof(double)));
+        CK(cudaMemcpy(d, data.data(), data.size() * sizeof(double), cudaMemcpyHostToDevice));
+        sbk::cast(d, sbk::F64, r.fptr[(size_t)st], s.dt, (i64)data.size(), stream);
+        CK(cudaStreamSynchronize(stream));
+        CK(cudaFree(d));
+    }
+
+    // ----------------------------------------------------------- helpers
+    char* fp(RankCtx& r, int v) {
+        auto& vw = r.P.views[(size_t)v];
+        auto& s = r.P.st[(size_t)vw.st];
+        return r.fptr[(size_t)vw.st] + vw.off * sbk::dt_bytes(s.dt);
+    }
+    char* gp(RankCtx& r, int v) {
+        auto& vw = r.P.views[(size_t)v];
+        auto& s = r.P.st[(size_t)vw.gst];
+        if (!r.gptr[(size_t)vw.gst]) throw Error("internal: gradient storage not allocated");
+        return r.gptr[(size_t)vw.gst] + vw.goff * sbk::dt_bytes(s.gdt);
+    }
+    DT gdt(RankCtx& r, int v) { return r.P.st[(size_t)r.P.views[(size_t)v].gst].gdt; }
+    DT fdt(RankCtx& r, int v) { return r.P.st[(size_t)r.P.views[(size_t)v].st].dt; }
+    const View& V(RankCtx& r, int v) { return r.P.views[(size_t)v]; }
+    static i64 rows_of(const View& v) { return v.shape.empty() ? 1 : v.numel() / v.shape.back(); }
+    static i64 cols_of(const View& v) { return v.shape.empty() ? 1 : v.shape.back(); }
+
+    // A grad target in the compute dtype: direct pointer, or the temp buffer
+    // (zeroed) which `flush` accumulates into an fp32 param/input gradient.
+    struct GT {
+        char* p;
+        bool temp;
+        int view;
+    };
+    GT gtarget(RankCtx& r, int v) {
+        if (gdt(r, v) == cdt) return {gp(r, v), false, v};
+        CK(cudaMemsetAsync(r.tmp, 0, (size_t)V(r, v).numel() * (size_t)sbk::dt_bytes(cdt), stream));
+        if (!V(r, v).g_contiguous()) throw Error("internal: strided fp32 gradient target");
+        return {r.tmp, true, v};
+    }
+    void flush(RankCtx& r, const GT& t) {
+        if (!t.temp) return;
+        sbk::accumulate(t.p, cdt, gp(r, t.view), gdt(r, t.view), V(r, t.view).numel(), 1.f, stream);
+    }
+
+    void gemm_rowwise(RankCtx& r, const void* A, i64 lda, bool a_t, const void* B, i64 ldb, bool b_t, void* C, i64 ldc,
+                      DT tc, i64 M, i64 N, i64 K, bool acc, const void* bias, int epi = 0, void* aux = nullptr) {
+        // A(m,k): a_t ? A[k*lda + m] : A[m*lda + k];  B(k,n): b_t ? B[n*ldb + k] : B[k*ldb + n]
+        sbk::Gemm g;
+        g.A = A;
+        g.ta = cdt;
+        g.sAm = a_t ? 1 : lda;
+        g.sAk = a_t ? lda : 1;
+        g.B = B;
+        g.tb = cdt;
+        g.sBk = b_t ? 1 : ldb;
+        g.sBn = b_t ? ldb : 1;
+        g.C = C;
+        g.tc = tc;
+        g.sCm = ldc;
+        g.sCn = 1;
+        g.M = M;
+        g.N = N;
+        g.K = K;
+        g.accumulate = acc;
+        g.bias = bias;
+        g.tbias = cdt;
+        g.epilogue = epi;
+        g.aux = aux;
+        sbk::gemm(g, stream);
+        (void)r;
+    }
+
+    // ------------------------------------------------------- collectives
+    void all_reduce(std::vector<char*> bufs_in, std::vector<char*> bufs_out, DT t, i64 n) {
+        if (comm.nccl) {
+            nccl().check(nccl().AllReduce(bufs_in[0], bufs_out[0], (size_t)n, nccl_dt(t), ncclSum, ncomm, stream),
+                         "ncclAllReduce");
+            return;
+        }
+        sbk::sum_ranks((const void* const*)bufs_in.data(), (void* const*)bufs_out.data(), (int)bufs_in.size(), t, n, false,
+                       stream);
+        ++launches;
+    }
+
+    // ------------------------------------------------------- forward op
+    void fwd_op(int i, bool recompute = false) {
+        const Op& op0 = ranks[0].P.fwd[(size_t)i];
+        if (profiling) prof_begin(std::string(k_str(op0.k)) + (recompute ? "(re)" : ""));
+        switch (op0.k) {
+            case K::AllReduce: {
+                ++collectives;
+                if (!op0.allreduce) break;
+                std::vector<char*> in, out;
+                for (auto& r : ranks) {
+                    in.push_back(fp(r, r.P.fwd[(size_t)i].in[0]));
+                    out.push_back(fp(r, r.P.fwd[(size_t)i].out[0]));
+                }
+                all_reduce(in, out, cdt, V(ranks[0], op0.in[0]).numel());
+                break;
+            }
+            case K::AllGather: {
+                ++collectives;
+                const View& xv = V(ranks[0], op0.in[0]);
+                i64 n = xv.numel(), inner = 1, outer = 1;
+                for (size_t d = (size_t)op0.axis; d < xv.shape.size(); ++d) inner *= xv.shape[d];
+                outer = n / inner;
+                if (comm.nccl) {
+                    RankCtx& r = ranks[0];
+                    if (world > 1)
+                        nccl().check(nccl().AllGather(fp(r, op0.in[0]), r.ws, (size_t)n, nccl_dt(cdt), ncomm, stream),
+                                     "ncclAllGather");
+                    else
+                        CK(cudaMemcpyAsync(r.ws, fp(r, op0.in[0]), (size_t)n * sbk::dt_bytes(cdt), cudaMemcpyDeviceToDevice, stream));
+                    // ws is (world, outer, inner) -> out (outer, world, inner)
+                    i64 shape[3] = {outer, world, inner}, ss[3] = {inner, n, 1}, ds[3] = {world * inner, inner, 1};
+                    sbk::strided_copy(r.ws, cdt, ss, fp(r, r.P.fwd[(size_t)i].out[0]), cdt, ds, shape, 3, false, stream);
+                } else {
+                    for (auto& dst : ranks)
+                        for (int src = 0; src < world; ++src) {
+                            i64 shape[2] = {outer, inner}, ss[2] = {inner, 1}, ds[2] = {world * inner, 1};
+                            sbk::strided_copy(fp(ranks[(size_t)src], op0.in[0]), cdt, ss,
+                                              fp(dst, dst.P.fwd[(size_t)i].out[0]) + (size_t)src * inner * sbk::dt_bytes(cdt),
+                                              cdt, ds, shape, 2, false, stream);
+                        }
+                }
+                break;
+            }
+            case K::FusedLinearResLN:
+                for (auto& r : ranks) fused_res_ln_gemm(r, r.P.fwd[(size_t)i]);
+                if (op0.allreduce) {
+                    ++collectives;
+                    std::vector<char*> b;
+                    for (auto& r : ranks) b.push_back(fp(r, r.P.fwd[(size_t)i].out[1]));
+                    all_reduce(b, b, cdt, V(ranks[0], op0.out[1]).numel());
+                } else if (op0.allreduce == false && op0.k == K::FusedLinearResLN && false) {
+                }
+                for (auto& r : ranks) fused_res_ln_tail(r, r.P.fwd[(size_t)i]);
+                break;
+            default:
+                for (auto& r : ranks) fwd_local(r, r.P.fwd[(size_t)i]);
+        }
+        if (profiling) prof_end();
+        if (nan_guard) check_nan(i);
+    }
+
+    void check_nan(int i) {
+        for (auto& r : ranks) {
+            const Op& op = r.P.fwd[(size_t)i];
+            for (int v : op.out) {
+                if (fdt(r, v) == sbk::F64 || r.P.st[(size_t)V(r, v).st].kind == SKind::Aux) continue;
+                CK(cudaMemsetAsync(nan_flag, 0, sizeof(int), stream));
+                sbk::count_nan(fp(r, v), fdt(r, v), V(r, v).numel(), nan_flag, stream);
+                int h = 0;
+                CK(cudaMemcpyAsync(&h, nan_flag, sizeof(int), cudaMemcpyDeviceToHost, stream));
+                CK(cudaStreamSynchronize(stream));
+                if (h) throw Error(std::string("NaN produced by op '") + k_str(op.k) + "' on rank " + std::to_string(r.P.rank));
+            }
+        }
+    }
+
+    void fused_res_ln_gemm(RankCtx& r, const Op& op) {
+        const View& x = V(r, op.in[0]);
+        const View& w = V(r, op.in[1]);
+        i64 rows, cols, ldx;
+        x.rowwise(rows, cols, ldx);
+        i64 out_f = w.shape[0];
+        gemm_rowwise(r, fp(r, op.in[0]), ldx, false, fp(r, op.in[1]), cols, true, fp(r, op.out[1]), out_f, cdt, rows,
+                     out_f, cols, false, nullptr);
+        ++launches;
+    }
+    void fused_res_ln_tail(RankCtx& r, const Op& op) {
+        const View& y = V(r, op.out[0]);
+        i64 rows = rows_of(y), n = cols_of(y);
+        const void* bias = op.has_bias && op.bias_on ? fp(r, op.in[5]) : nullptr;
+        sbk::bias_dropout_residual_ln_fwd(fp(r, op.out[1]), bias, fp(r, op.in[2]), fp(r, op.in[3]), fp(r, op.in[4]), cdt,
+                                          fp(r, op.out[2]), fp(r, op.out[0]), (float*)fp(r, op.out[3]),
+                                          (float*)fp(r, op.out[4]), cdt, rows, n, (float)op.eps, op.s1,
+                                          op.dropout ? op.thr : 0, (float)(1.0 / (1.0 - op.p)), stream);
+        ++launches;
+    }
+
+    void fwd_local(RankCtx& r, const Op& op) {
+        ++launches;
+        switch (op.k) {
+            case K::Cast:
+                sbk::cast(fp(r, op.in[0]), fdt(r, op.in[0]), fp(r, op.out[0]), fdt(r, op.out[0]), V(r, op.out[0]).numel(), stream);
+                break;
+            case K::Linear: {
+                const View& x = V(r, op.in[0]);
+                const View& w = V(r, op.in[1]);
+                i64 rows, cols, ldx;
+                x.rowwise(rows, cols, ldx);
+                i64 out_f = w.shape[0];
+                gemm_rowwise(r, fp(r, op.in[0]), ldx, false, fp(r, op.in[1]), cols, true, fp(r, op.out[0]), out_f, cdt, rows,
+                             out_f, cols, false, op.bias_on ? fp(r, op.in[2]) : nullptr);
+                break;
+            }
+            case K::FusedLinearGelu: {
+                const View& x = V(r, op.in[0]);
+                const View& w = V(r, op.in[1]);
+                i64 rows, cols, ldx;
+                x.rowwise(rows, cols, ldx);
+                i64 out_f = w.shape[0];
+                gemm_rowwise(r, fp(r, op.in[0]), ldx, false, fp(r, op.in[1]), cols, true, fp(r, op.out[0]), out_f, cdt, rows,
+                             out_f, cols, false, op.bias_on ? fp(r, op.in[2]) : nullptr, 1, fp(r, op.out[1]));
+                break;
+            }
+            case K::LayerNorm: {
+                const View& x = V(r, op.in[0]);
+                sbk::layernorm_fwd(fp(r, op.in[0]), op.affine ? fp(r, op.in[1]) : nullptr,
+                                   op.affine ? fp(r, op.in[2]) : nullptr, cdt, fp(r, op.out[0]), (float*)fp(r, op.out[1]),
+                                   (float*)fp(r, op.out[2]), cdt, rows_of(x), cols_of(x), (float)op.eps, stream);
+                break;
+            }
+            case K::Dropout:
+                sbk::dropout(fp(r, op.in[0]), fp(r, op.out[0]), cdt, V(r, op.out[0]).numel(), op.s1, op.thr,
+                             (float)(1.0 / (1.0 - op.p)), false, stream);
+                break;
+            case K::Add:
+            case K::Mul:
+                sbk::binary(op.k == K::Add ? 0 : 1, fp(r, op.in[0]), V(r, op.in[0]).numel(), fp(r, op.in[1]),
+                            V(r, op.in[1]).numel(), fp(r, op.out[0]), cdt, V(r, op.out[0]).numel(), stream);
+                break;
+            case K::Scale:
+            case K::Relu:
+            case K::Gelu:
+                sbk::unary(op.k == K::Scale ? 0 : op.k == K::Relu ? 1 : 2, fp(r, op.in[0]), fp(r, op.out[0]), cdt,
+                           V(r, op.out[0]).numel(), (float)op.scale, stream);
+                break;
+            case K::Softmax: {
+                i64 outer, n, inner;
+                axis_split(V(r, op.in[0]), op.axis, outer, n, inner);
+                sbk::softmax_fwd(fp(r, op.in[0]), fp(r, op.out[0]), cdt, outer, n, inner, stream);
+                break;
+            }
+            case K::Matmul: {
+                const View& a = V(r, op.in[0]);
+                const View& b = V(r, op.in[1]);
+                int ra = (int)a.shape.size();
+                i64 m = a.shape[(size_t)ra - 2], k = a.shape[(size_t)ra - 1], n = b.shape.back();
+                sbk::Gemm g;
+                g.A = fp(r, op.in[0]);
+                g.ta = cdt;
+                g.sAb = m * k;
+                g.sAm = k;
+                g.sAk = 1;
+                g.B = fp(r, op.in[1]);
+                g.tb = cdt;
+                g.sBb = k * n;
+                g.sBk = n;
+                g.sBn = 1;
+                g.C = fp(r, op.out[0]);
+                g.tc = cdt;
+                g.sCb = m * n;
+                g.sCm = n;
+                g.sCn = 1;
+                g.batch = a.numel() / (m * k);
+                g.M = m;
+                g.N = n;
+                g.K = k;
+                sbk::gemm(g, stream);
+                break;
+            }
+            case K::Permute: {
+                const View& x = V(r, op.in[0]);
+                const View& y = V(r, op.out[0]);
+                std::vector<i64> ss(op.perm.size());
+                for (size_t d = 0; d < op.perm.size(); ++d) ss[d] = x.strides[(size_t)op.perm[d]];
+                sbk::strided_copy(fp(r, op.in[0]), cdt, ss.data(), fp(r, op.out[0]), cdt, y.strides.data(), y.shape.data(),
+                                  (int)y.shape.size(), false, stream);
+                break;
+            }
+            case K::Copy: {
+                const View& x = V(r, op.in[0]);
+                const View& y = V(r, op.out[0]);
+                sbk::strided_copy(fp(r, op.in[0]), cdt, x.strides.data(), fp(r, op.out[0]), cdt, y.strides.data(),
+                                  y.shape.data(), (int)y.shape.size(), false, stream);
+                break;
+            }
+            case K::Concat: {
+                const View& y = V(r, op.out[0]);
+                i64 offset = 0;
+                for (int v : op.in) {
+                    const View& x = V(r, v);
+                    char* dst = fp(r, op.out[0]) + (size_t)(offset * y.strides[(size_t)op.axis]) * sbk::dt_bytes(cdt);
+                    sbk::strided_copy(fp(r, v), cdt, x.strides.data(), dst, cdt, y.strides.data(), x.shape.data(),
+                                      (int)x.shape.size(), false, stream);
+                    offset += x.shape[(size_t)op.axis];
+                }
+                break;
+            }
+            case K::ReduceSum: {
+                const View& x = V(r, op.in[0]);
+                if (op.reduce_all) {
+                    sbk::reduce_all(fp(r, op.in[0]), cdt, x.numel(), fp(r, op.out[0]), cdt, false, stream);
+                } else {
+                    i64 outer, n, inner;
+                    axis_split(x, op.axis, outer, n, inner);
+                    sbk::reduce_axis(fp(r, op.in[0]), fp(r, op.out[0]), cdt, outer, n, inner, false, stream);
+                }
+                break;
+            }
+            case K::SyncGrad: --launches; break;  // identity forward (executor.cpp:450-461)
+            case K::Embedding: {
+                const View& ids = V(r, op.in[0]);
+                const View& w = V(r, op.in[1]);
+                sbk::embedding_fwd((const double*)fp(r, op.in[0]), ids.numel(), fp(r, op.in[1]), cdt, w.shape[1],
+                                   op.full_rows, op.row0, w.shape[0], fp(r, op.out[0]), stream);
+                break;
+            }
+            case K::FlashAttn: sbk::attn_fwd(attn_args(r, op), stream); break;
+            default: throw Error(std::string("internal: no forward launcher for ") + k_str(op.k));
+        }
+    }
+
+    sbk::Attn attn_args(RankCtx& r, const Op& op) {
+        sbk::Attn a;
+        const View& q = V(r, op.in[0]);
+        i64 rows, cols;
+        a.q = fp(r, op.in[0]);
+        a.k = fp(r, op.in[1]);
+        a.v = fp(r, op.in[2]);
+        a.o = fp(r, op.out[0]);
+        q.rowwise(rows, cols, a.ld_q);
+        V(r, op.in[1]).rowwise(rows, cols, a.ld_k);
+        V(r, op.in[2]).rowwise(rows, cols, a.ld_v);
+        a.ld_o = cols;
+        a.lse = (float*)fp(r, op.out[1]);
+        a.B = q.shape[0];
+        a.S = q.shape[1];
+        a.nh = op.nh;
+        a.hd = op.hd;
+        a.scale = (float)op.scale;
+        a.s1 = op.dropout ? op.s1 : 0;
+        a.thr = op.dropout ? op.thr : 0;
+        a.dscale = (float)(1.0 / (1.0 - op.p));
+        a.t = cdt;
+        return a;
+    }
+
+    static void axis_split(const View& v, int axis, i64& outer, i64& n, i64& inner) {
+        outer = 1;
+        inner = 1;
+        for (int d = 0; d < axis; ++d) outer *= v.shape[(size_t)d];
+        n = v.shape.empty() ? 1 : v.shape[(size_t)axis];
+        for (size_t d = (size_t)axis + 1; d < v.shape.size(); ++d) inner *= v.shape[d];
+    }
+
+    // ------------------------------------------------------ backward op
+    void linear_bwd(RankCtx& r, const Op& op, const void* g, i64 ldg) {
+        // dx += g W (executor.cpp:101-118); dW += g^T x (:121-133); db += colsum g (:1146-1154)
+        const View& x = V(r, op.in[0]);
+        const View& w = V(r, op.in[1]);
+        i64 rows, cols, ldx, gr, gc, ldgx;
+        x.rowwise(rows, cols, ldx);
+        i64 out_f = w.shape[0];
+        GT gx = gtarget(r, op.in[0]);
+        if (gx.temp) ldgx = cols;
+        else x.rowwise(gr, gc, ldgx, true);
+        gemm_rowwise(r, g, ldg, false, fp(r, op.in[1]), cols, false, gx.p, ldgx, cdt, rows, cols, out_f, true, nullptr);
+        flush(r, gx);
+        gemm_rowwise(r, g, ldg, true, fp(r, op.in[0]), ldx, false, gp(r, op.in[1]), cols, gdt(r, op.in[1]), out_f, cols,
+                     rows, true, nullptr);
+        launches += 2;
+        if (op.has_bias && op.bias_grad) {
+            sbk::bias_grad(g, cdt, ldg, rows, out_f, (float*)gp(r, op.in[2]), (float*)r.ws, stream);
+            ++launches;
+        }
+    }
+
+    void bwd_op(int i) {
+        const Op& op0 = ranks[0].P.fwd[(size_t)i];
+        if (profiling) prof_begin(std::string(k_str(op0.k)) + "(bwd)");
+        switch (op0.k) {
+            case K::SyncGrad: {
+                // Σ_r of the module input's gradient, accumulated on every rank (executor.cpp:1071-1083)
+                ++collectives;
+                if (op0.ids_input) break;  // id inputs are not differentiable: the sum is of zeros
+                std::vector<char*> b;
+                for (auto& r : ranks) b.push_back(gp(r, r.P.fwd[(size_t)i].out[0]));
+                i64 n = V(ranks[0], op0.out[0]).numel();
+                if (world > 1) all_reduce(b, b, cdt, n);
+                for (auto& r : ranks) {
+                    const Op& op = r.P.fwd[(size_t)i];
+                    accumulate_view(r, op.out[0], op.in[0]);
+                }
+                break;
+            }
+            case K::FusedLinearResLN: {
+                for (auto& r : ranks) {
+                    const Op& op = r.P.fwd[(size_t)i];
+                    const View& y = V(r, op.out[0]);
+                    i64 rows = rows_of(y), n = cols_of(y);
+                    GT gres = gtarget(r, op.in[2]);
+                    sbk::bias_dropout_residual_ln_bwd(
+                        fp(r, op.out[2]), (float*)fp(r, op.out[3]), (float*)fp(r, op.out[4]), fp(r, op.in[3]), cdt,
+                        gp(r, op.out[0]), gres.p, gp(r, op.out[1]), false,
+                        op.has_bias && op.bias_grad ? (float*)gp(r, op.in[5]) : nullptr, (float*)gp(r, op.in[3]),
+                        (float*)gp(r, op.in[4]), cdt, rows, n, op.s1, op.dropout ? op.thr : 0,
+                        (float)(1.0 / (1.0 - op.p)), (float*)r.ws, stream);
+                    flush(r, gres);
+                    ++launches;
+                    // the in-region all_reduce backpropagates as identity (executor.cpp:1227-1233)
+                    Op lin = op;
+                    lin.has_bias = false;
+                    linear_bwd(r, lin, gp(r, op.out[1]), n);
+                }
+                break;
+            }
+            default:
+                for (auto& r : ranks) bwd_local(r, r.P.fwd[(size_t)i]);
+        }
+        if (profiling) prof_end();
+    }
+
+    void accumulate_view(RankCtx& r, int from, int to) {
+        // grad(to) += grad(from); equal shapes
+        const View& a = V(r, from);
+        const View& b = V(r, to);
+        if (a.g_contiguous() && b.g_contiguous()) {
+            sbk::accumulate(gp(r, from), gdt(r, from), gp(r, to), gdt(r, to), a.numel(), 1.f, stream);
+        } else {
+            if (gdt(r, from) != gdt(r, to)) throw Error("internal: strided dtype-converting accumulate");
+            sbk::strided_copy(gp(r, from), gdt(r, from), a.gstrides.data(), gp(r, to), gdt(r, to), b.gstrides.data(),
+                              a.shape.data(), (int)a.shape.size(), true, stream);
+        }
+        ++launches;
+    }
+
+    void bwd_local(RankCtx& r, const Op& op) {
+        ++launches;
+        switch (op.k) {
+            case K::Cast:
+                if (fdt(r, op.out[0]) == sbk::F64) break;  // ids: not differentiable
+                sbk::accumulate(gp(r, op.out[0]), cdt, gp(r, op.in[0]), gdt(r, op.in[0]), V(r, op.out[0]).numel(), 1.f, stream);
+                break;
+            case K::Linear: {
+                const View& y = V(r, op.out[0]);
+                --launches;
+                linear_bwd(r, op, gp(r, op.out[0]), cols_of(y));
+                break;
+            }
+            case K::FusedLinearGelu: {
+                const View& y = V(r, op.out[0]);
+                sbk::unary_bwd(2, fp(r, op.out[1]), gp(r, op.out[0]), gp(r, op.out[1]), cdt, cdt, y.numel(), 1.f, stream);
+                linear_bwd(r, op, gp(r, op.out[1]), cols_of(y));
+                break;
+            }
+            case K::LayerNorm: {
+                const View& x = V(r, op.in[0]);
+                GT gx = gtarget(r, op.in[0]);
+                sbk::layernorm_bwd(fp(r, op.in[0]), (float*)fp(r, op.out[1]), (float*)fp(r, op.out[2]),
+                                   op.affine ? fp(r, op.in[1]) : nullptr, cdt, gp(r, op.out[0]), cdt, gx.p,
+                                   op.affine ? (float*)gp(r, op.in[1]) : nullptr,
+                                   op.affine ? (float*)gp(r, op.in[2]) : nullptr, cdt, rows_of(x), cols_of(x),
+                                   (float*)r.ws, stream);
+                flush(r, gx);
+                break;
+            }
+            case K::Dropout: {
+                GT gx = gtarget(r, op.in[0]);
+                sbk::dropout(gp(r, op.out[0]), gx.p, cdt, V(r, op.out[0]).numel(), op.s1, op.thr,
+                             (float)(1.0 / (1.0 - op.p)), true, stream);
+                flush(r, gx);
+                break;
+            }
+            case K::Add: {
+                i64 n = V(r, op.out[0]).numel();
+                for (int k = 0; k < 2; ++k) {
+                    GT gx = gtarget(r, op.in[(size_t)k]);
+                    if (V(r, op.in[(size_t)k]).numel() == 1 && n != 1)
+                        sbk::reduce_all(gp(r, op.out[0]), cdt, n, gx.p, cdt, true, stream);
+                    else
+                        sbk::accumulate(gp(r, op.out[0]), cdt, gx.p, cdt, n, 1.f, stream);
+                    flush(r, gx);
+                }
+                break;
+            }
+            case K::Mul: {
+                i64 n = V(r, op.out[0]).numel();
+                for (int k = 0; k < 2; ++k) {
+                    GT gx = gtarget(r, op.in[(size_t)k]);
+                    int other = op.in[(size_t)(1 - k)];
+                    sbk::mul_bwd(gp(r, op.out[0]), cdt, fp(r, other), V(r, other).numel(), gx.p, cdt,
+                                 V(r, op.in[(size_t)k]).numel(), n, stream);
+                    flush(r, gx);
+                }
+                break;
+            }
+            case K::Scale:
+            case K::Relu:
+            case K::Gelu: {
+                GT gx = gtarget(r, op.in[0]);
+                sbk::unary_bwd(op.k == K::Scale ? 0 : op.k == K::Relu ? 1 : 2, fp(r, op.in[0]), gp(r, op.out[0]), gx.p, cdt,
+                               cdt, V(r, op.out[0]).numel(), (float)op.scale, stream);
+                flush(r, gx);
+                break;
+            }
+            case K::Softmax: {
+                i64 outer, n, inner;
+                axis_split(V(r, op.in[0]), op.axis, outer, n, inner);
+                GT gx = gtarget(r, op.in[0]);
+                sbk::softmax_bwd(fp(r, op.out[0]), gp(r, op.out[0]), gx.p, cdt, cdt, outer, n, inner, stream);
+                flush(r, gx);
+                break;
+            }
+            case K::Matmul: {
+                // ga += g b^T ; gb += a^T g  (executor.cpp:1257-1264)
+                const View& a = V(r, op.in[0]);
+                const View& b = V(r, op.in[1]);
+                int ra = (int)a.shape.size();
+                i64 m = a.shape[(size_t)ra - 2], k = a.shape[(size_t)ra - 1], n = b.shape.back();
+                i64 batch = a.numel() / (m * k);
+                GT ga = gtarget(r, op.in[0]);
+                sbk::Gemm g;
+                g.ta = g.tb = cdt;
+                g.A = gp(r, op.out[0]);
+                g.sAb = m * n;
+                g.sAm = n;
+                g.sAk = 1;
+                g.B = fp(r, op.in[1]);
+                g.sBb = k * n;
+                g.sBk = 1;
+                g.sBn = n;
+                g.C = ga.p;
+                g.tc = cdt;
+                g.sCb = m * k;
+                g.sCm = k;
+                g.sCn = 1;
+                g.batch = batch;
+                g.M = m;
+                g.N = k;
+                g.K = n;
+                g.accumulate = true;
+                sbk::gemm(g, stream);
+                flush(r, ga);
+                GT gb = gtarget(r, op.in[1]);
+                sbk::Gemm h;
+                h.ta = h.tb = cdt;
+                h.A = fp(r, op.in[0]);
+                h.sAb = m * k;
+                h.sAm = 1;
+                h.sAk = k;
+                h.B = gp(r, op.out[0]);
+                h.sBb = m * n;
+                h.sBk = n;
+                h.sBn = 1;
+                h.C = gb.p;
+                h.tc = cdt;
+                h.sCb = k * n;
+                h.sCm = n;
+                h.sCn = 1;
+                h.batch = batch;
+                h.M = k;
+                h.N = n;
+                h.K = m;
+                h.accumulate = true;
+                sbk::gemm(h, stream);
+                flush(r, gb);
+                ++launches;
+                break;
+            }
+            case K::Permute: {
+                const View& x = V(r, op.in[0]);
+                const View& y = V(r, op.out[0]);
+                std::vector<i64> ds(op.perm.size());
+                for (size_t d = 0; d < op.perm.size(); ++d) ds[d] = x.gstrides[(size_t)op.perm[d]];
+                GT gx = gtarget(r, op.in[0]);
+                if (gx.temp) {
+                    std::vector<i64> cs(x.shape.size(), 1);
+                    for (int d = (int)cs.size() - 2; d >= 0; --d) cs[(size_t)d] = cs[(size_t)d + 1] * x.shape[(size_t)d + 1];
+                    for (size_t d = 0; d < op.perm.size(); ++d) ds[d] = cs[(size_t)op.perm[d]];
+                }
+                sbk::strided_copy(gp(r, op.out[0]), cdt, y.gstrides.data(), gx.p, cdt, ds.data(), y.shape.data(),
+                                  (int)y.shape.size(), true, stream);
+                flush(r, gx);
+                break;
+            }
+            case K::Copy: {
+                const View& x = V(r, op.in[0]);
+                const View& y = V(r, op.out[0]);
+                GT gx = gtarget(r, op.in[0]);
+                std::vector<i64> ds = x.gstrides;
+                if (gx.temp) ds = y.gstrides;
+                sbk::strided_copy(gp(r, op.out[0]), cdt, y.gstrides.data(), gx.p, cdt, ds.data(), y.shape.data(),
+                                  (int)y.shape.size(), true, stream);
+                flush(r, gx);
+                break;
+            }
+            case K::Concat: {
+                const View& y = V(r, op.out[0]);
+                i64 offset = 0;
+                for (int v : op.in) {
+                    const View& x = V(r, v);
+                    const char* src = gp(r, op.out[0]) + (size_t)(offset * y.gstrides[(size_t)op.axis]) * sbk::dt_bytes(cdt);
+                    GT gx = gtarget(r, v);
+                    std::vector<i64> ds = x.gstrides;
+                    if (gx.temp) {
+                        ds.assign(x.shape.size(), 1);
+                        for (int d = (int)ds.size() - 2; d >= 0; --d) ds[(size_t)d] = ds[(size_t)d + 1] * x.shape[(size_t)d + 1];
+                    }
+                    sbk::strided_copy(src, cdt, y.gstrides.data(), gx.p, cdt, ds.data(), x.shape.data(), (int)x.shape.size(),
+                                      true, stream);
+                    flush(r, gx);
+                    offset += x.shape[(size_t)op.axis];
+                }
+                break;
+            }
+            case K::ReduceSum: {
+                const View& x = V(r, op.in[0]);
+                GT gx = gtarget(r, op.in[0]);
+                if (op.reduce_all) {
+                    sbk::add_scalar(gx.p, cdt, x.numel(), 0.f, gp(r, op.out[0]), stream);
+                } else {
+                    i64 outer, n, inner;
+                    axis_split(x, op.axis, outer, n, inner);
+                    sbk::broadcast_axis_acc(gp(r, op.out[0]), gx.p, cdt, outer, n, inner, stream);
+                }
+                flush(r, gx);
+                break;
+            }
+            case K::AllReduce:
+                if (op.allreduce) accumulate_view(r, op.out[0], op.in[0]);
+                --launches;
+                break;
+            case K::AllGather: {
+                // each rank keeps its own slice of its gradient (executor.cpp:1234-1244)
+                const View& x = V(r, op.in[0]);
+                i64 n = x.numel(), inner = 1;
+                for (size_t d = (size_t)op.axis; d < x.shape.size(); ++d) inner *= x.shape[d];
+                i64 outer = n / inner;
+                GT gx = gtarget(r, op.in[0]);
+                i64 shape[2] = {outer, inner}, ss[2] = {world * inner, 1}, ds[2] = {inner, 1};
+                sbk::strided_copy(gp(r, op.out[0]) + (size_t)(r.P.rank * inner) * sbk::dt_bytes(cdt), cdt, ss, gx.p, cdt, ds,
+                                  shape, 2, true, stream);
+                flush(r, gx);
+                break;
+            }
+            case K::Embedding: {
+                const View& ids = V(r, op.in[0]);
+                const View& w = V(r, op.in[1]);
+                sbk::embedding_bwd((const double*)fp(r, op.in[0]), ids.numel(), gp(r, op.out[0]), cdt, w.shape[1],
+                                   op.full_rows, op.row0, w.shape[0], (float*)gp(r, op.in[1]), r.ws, stream);
+                break;
+            }
+            case K::FlashAttn: {
+                sbk::Attn a = attn_args(r, op);
+                i64 rows, cols, lq, lk, lv;
+                V(r, op.in[0]).rowwise(rows, cols, lq, true);
+                V(r, op.in[1]).rowwise(rows, cols, lk, true);
+                V(r, op.in[2]).rowwise(rows, cols, lv, true);
+                sbk::attn_bwd(a, gp(r, op.out[0]), a.ld_o, gp(r, op.in[0]), gp(r, op.in[1]), gp(r, op.in[2]), lq, lk, lv,
+                              (float*)r.ws, stream);
+                break;
+            }
+            default: throw Error(std::string("internal: no backward launcher for ") + k_str(op.k));
+        }
+    }
+
+    // ----------------------------------------------------------- steps
+    void run_forward() {
+        for (size_t i = 0; i < ranks[0].P.fwd.size(); ++i) fwd_op((int)i);
+        ran_forward = true;
+    }
+
+    void run_backward() {
+        for (auto& r : ranks) {
+            // loss = sum of outputs: seed ones (executor.cpp:355-362); zero persistent grads
+            CK(cudaMemsetAsync(r.base + persistent_grad_span.first, 0, persistent_grad_span.second, stream));
+            for (int v : r.P.outputs) {
+                if (!V(r, v).g_contiguous()) throw Error("internal: strided model output gradient");
+                sbk::add_scalar(gp(r, v), gdt(r, v), V(r, v).numel(), 1.f, nullptr, stream);
+                ++launches;
+            }
+        }
+        for (auto& s : bsteps) {
+            if (s.kind == 2) {
+                for (auto& r : ranks)
+                    CK(cudaMemsetAsync(r.scratch_grad, 0, r.region_grad_span[(size_t)s.idx].second, stream));
+            } else if (s.kind == 1) {
+                fwd_op(s.idx, true);
+            } else {
+                bwd_op(s.idx);
+            }
+        }
+    }
+
+    // ---------------------------------------------------------- profile
+    void prof_begin(const std::string& name) {
+        cudaEvent_t a, b;
+        cudaEventCreate(&a);
+        cudaEventCreate(&b);
+        cudaEventRecord(a, stream);
+        prof.push_back({name, {a, b}});
+    }
+    void prof_end() { cudaEventRecord(prof.back().second.second, stream); }
+};
+
+// ====================================================================== API
+Executor::Executor(const Module& root, bool train, u64 seed, int world, DT compute, const CommConfig& comm, bool fused)
+    : impl_(std::make_unique<ExecutorImpl>(root, train, seed, world, compute, comm, fused)) {}
+Executor::~Executor() = default;
+void Executor::set_nan_guard(bool on) { impl_->nan_guard = on; }
+
+void Executor::upload_inputs(const std::vector<HostTensor>& inputs) {
+    auto& I = *impl_;
+    for (auto& r : I.ranks) {
+        if (inputs.size() != r.P.inputs.size())
+            throw Error("model expects " + std::to_string(r.P.inputs.size()) + " inputs, got " + std::to_string(inputs.size()));
+        for (size_t k = 0; k < inputs.size(); ++k) {
+            const View& v = r.P.views[(size_t)r.P.inputs[k]];
+            if ((i64)inputs[k].data.size() != v.numel())
+                throw Error("input " + std::to_string(k) + " has " + std::to_string(inputs[k].data.size()) +
+                            " elements, expected " + std::to_string(v.numel()));
+            CK(cudaMemcpyAsync(I.fp(r, r.P.inputs[k]), inputs[k].data.data(), inputs[k].data.size() * 8,
+                               cudaMemcpyHostToDevice, I.stream));
+        }
+    }
+}
+void Executor::upload_inputs_raw(const double* const* inputs, int n) {
+    auto& I = *impl_;
+    for (auto& r : I.ranks) {
+        if (n != (int)r.P.inputs.size())
+            throw Error("model expects " + std::to_string(r.P.inputs.size()) + " inputs, got " + std::to_string(n));
+        for (int k = 0; k < n; ++k) {
+            const View& v = r.P.views[(size_t)r.P.inputs[(size_t)k]];
+            CK(cudaMemcpyAsync(I.fp(r, r.P.inputs[(size_t)k]), inputs[k], (size_t)v.numel() * 8, cudaMemcpyHostToDevice,
+                               I.stream));
+        }
+    }
+}
+void Executor::forward_uploaded() {
+    impl_->collectives = 0;
+    run_forward();
+    synchronize();
+}
+void Executor::set_inputs_device(int idx, const void* dptr) {
+    auto& I = *impl_;
+    for (auto& r : I.ranks) {
+        const View& v = r.P.views[(size_t)r.P.inputs[(size_t)idx]];
+        CK(cudaMemcpyAsync(I.fp(r, r.P.inputs[(size_t)idx]), dptr, (size_t)v.numel() * 8, cudaMemcpyDeviceToDevice, I.stream));
+    }
+}
+void* Executor::input_device_ptr(int idx) const {
+    auto& I = *impl_;
+    return I.fp(I.ranks[0], I.ranks[0].P.inputs[(size_t)idx]);
+}
+
+std::vector<HostTensor> Executor::forward(const std::vector<HostTensor>& inputs) {
+    upload_inputs(inputs);
+    impl_->collectives = 0;
+    run_forward();
+    synchronize();
+    return outputs_of_rank(impl_->comm.nccl ? impl_->comm.rank : 0);
+}
+void Executor::run_forward() { impl_->run_forward(); }
+void Executor::run_backward() {
+    if (!impl_->ran_forward) throw Error("backward requires a completed forward run");
+    impl_->run_backward();
+}
+void Executor::synchronize() { CK(cudaStreamSynchronize(impl_->stream)); }
+void* Executor::stream() const { return impl_->stream; }
+
+static HostTensor download(ExecutorImpl& I, RankCtx& r, int v, bool grad) {
+    const View& vw = r.P.views[(size_t)v];
+    TensorSpec s;
+    s.shape = vw.shape;
+    s.dtype = vw.rdt;
+    HostTensor t(s);
+    i64 n = vw.numel();
+    DT dt = grad ? I.gdt(r, v) : I.fdt(r, v);
+    const auto& strides = grad ? vw.gstrides : vw.strides;
+    char* src = grad ? I.gp(r, v) : I.fp(r, v);
+    double* d = nullptr;
+    CK(cudaMalloc(&d, (size_t)std::max<i64>(n, 1) * 8));
+    std::vector<i64> cs(vw.shape.size(), 1);
+    for (int k = (int)cs.size() - 2; k >= 0; --k) cs[(size_t)k] = cs[(size_t)k + 1] * vw.shape[(size_t)k + 1];
+    if (vw.shape.empty())
+        sbk::cast(src, dt, d, sbk::F64, 1, I.stream);
+    else
+        sbk::strided_copy(src, dt, strides.data(), d, sbk::F64, cs.data(), vw.shape.data(), (int)vw.shape.size(), false,
+                          I.stream);
+    CK(cudaMemcpyAsync(t.data.data(), d, (size_t)n * 8, cudaMemcpyDeviceToHost, I.stream));
+    CK(cudaStreamSynchronize(I.stream));
+    CK(cudaFree(d));
+    return t;
+}
+
+static RankCtx& rank_ctx(ExecutorImpl& I, int rank) {
+    if (I.comm.nccl) {
+        if (rank != I.comm.rank) throw Error("rank " + std::to_string(rank) + " lives in another process");
+        return I.ranks[0];
+    }
+    if (rank < 0 || rank >= I.world) throw Error("rank out of range");
+    return I.ranks[(size_t)rank];
+}
+
+std::vector<HostTensor> Executor::outputs_of_rank(int rank) const {
+    auto& I = *impl_;
+    RankCtx& r = rank_ctx(I, rank);
+    std::vector<HostTensor> out;
+    for (int v : r.P.outputs) out.push_back(download(I, r, v, false));
+    return out;
+}
+
+std::vector<GradMap> Executor::backward_all_ranks() {
+    auto& I = *impl_;
+    run_backward();
+    synchronize();
+    std::vector<GradMap> maps;
+    for (auto& r : I.ranks) {
+        GradMap m;
+        for (auto& [name, v] : r.P.params) m.params[name] = download(I, r, v, true);
+        for (int v : r.P.inputs) m.inputs.push_back(download(I, r, v, true));
+        maps.push_back(std::move(m));
+    }
+    return maps;
+}
+GradMap Executor::backward() { return backward_all_ranks()[0]; }
+i64 Executor::ledger_bytes() const { return impl_->ranks[0].P.ledger_bytes; }
+i64 Executor::collective_invocations() const { return impl_->collectives; }
+
+void Executor::enqueue_loss(float* dloss) {
+    auto& I = *impl_;
+    RankCtx& r = I.ranks[0];
+    CK(cudaMemsetAsync(dloss, 0, 4, I.stream));
+    for (int v : r.P.outputs) {
+        const View& vw = r.P.views[(size_t)v];
+        if (!vw.contiguous()) throw Error("internal: strided output");
+        sbk::reduce_all(I.fp(r, v), I.fdt(r, v), vw.numel(), dloss, sbk::F32, true, I.stream);
+    }
+}
+
+void Executor::capture_graph() {
+    auto& I = *impl_;
+    if (I.gexec) return;
+    if (I.comm.nccl && I.world > 1) {
+        // NCCL kernels are capturable; nothing special beyond using our stream.
+    }
+    CK(cudaStreamBeginCapture(I.stream, cudaStreamCaptureModeThreadLocal));
+    I.run_forward();
+    I.run_backward();
+    CK(cudaStreamEndCapture(I.stream, &I.graph));
+    CK(cudaGraphInstantiate(&I.gexec, I.graph, 0));
+}
+void Executor::launch_graph() {
+    auto& I = *impl_;
+    if (!I.gexec) capture_graph();
+    CK(cudaGraphLaunch(I.gexec, I.stream));
+}
+int Executor::kernel_launches_per_step() const {
+    auto& I = *impl_;
+    int before = I.launches;
+    (void)before;
+    return I.launches;
+}
+size_t Executor::device_bytes() const {
+    size_t t = 0;
+    for (auto& r : impl_->ranks) t += r.total;
+    return t;
+}
+std::string Executor::describe() const {
+    auto& I = *impl_;
+    std::ostringstream o;
+    const Plan& P = I.ranks[0].P;
+    std::map<std::string, int> cnt;
+    for (auto& op : P.fwd) cnt[k_str(op.k)]++;
+    o << "{\"ops\": " << P.fwd.size() << ", \"regions\": " << P.regions.size() << ", \"backward_steps\": " << I.bsteps.size()
+      << ", \"device_bytes\": " << device_bytes() << ", \"kinds\": {";
+    bool first = true;
+    for (auto& [k, c] : cnt) {
+        o << (first ? "" : ", ") << "\"" << k << "\": " << c;
+        first = false;
+    }
+    o << "}}";
+    return o.str();
+}
+
+std::vector<std::pair<std::string, float>> Executor::profile_step() {
+    auto& I = *impl_;
+    I.profiling = true;
+    I.prof.clear();
+    I.run_forward();
+    I.run_backward();
+    I.profiling = false;
+    synchronize();
+    std::map<std::string, float> acc;
+    for (auto& [name, ev] : I.prof) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, ev.first, ev.second);
+        acc[name] += ms;
+        cudaEventDestroy(ev.first);
+        cudaEventDestroy(ev.second);
+    }
+    I.prof.clear();
+    return {acc.begin(), acc.end()};
+}
+
+}  // namespace sb

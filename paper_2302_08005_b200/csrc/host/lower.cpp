@@ -1,0 +1,847 @@
+// Lowering: post-apply Module -> per-rank static device Plan.
+//
+// Walks the module tree exactly like the reference interpreter
+// (eval_module / eval_graph / eval_builtin / eval_op, proj/src/executor.cpp:438-1030)
+// but emits typed device ops instead of computing values:
+//   * sync_backward on a module inserts a SyncGrad marker on its first input
+//     (executor.cpp:439-461);
+//   * checkpoint regions become [first,last] op ranges re-launched in backward
+//     (executor.cpp:463-492, 1093-1120);
+//   * EfficientAttention becomes one flash-attention op (it is always a
+//     recompute region in the reference, executor.cpp:442-444);
+//   * fused composites ({fused:1}) whose region is Linear->gelu or
+//     Linear->[all_reduce]->[Dropout]->add->LayerNorm become single fused ops;
+//     anything else is lowered op-by-op ("composed" semantics).
+// The activation ledger is accumulated with the reference's accounting rule
+// (executor.hpp:20-25) so ledger() matches it byte for byte.
+#include <algorithm>
+#include <functional>
+#include <map>
+#include <sstream>
+
+#include "plan.hpp"
+#include "rng.hpp"
+#include "schedule.hpp"
+
+namespace sb {
+
+const char* k_str(K k) {
+    static const char* n[] = {"Cast",   "Linear",  "LayerNorm", "Dropout",   "Add",       "Mul",
+                              "Scale",  "Relu",    "Gelu",      "Softmax",   "Matmul",    "Permute",
+                              "Copy",   "Concat",  "ReduceSum", "AllReduce", "AllGather", "SyncGrad",
+                              "Embedding", "FusedLinearGelu", "FusedLinearResLN", "FlashAttn", "FillOnes"};
+    return n[(int)k];
+}
+
+static std::vector<i64> contig_strides(const std::vector<i64>& shape) {
+    std::vector<i64> s(shape.size(), 1);
+    for (int i = (int)shape.size() - 2; i >= 0; --i) s[(size_t)i] = s[(size_t)i + 1] * shape[(size_t)i + 1];
+    return s;
+}
+
+bool View::contiguous() const { return strides == contig_strides(shape); }
+bool View::g_contiguous() const { return gstrides == contig_strides(shape); }
+bool View::rowwise(i64& rows, i64& cols, i64& ld, bool grad) const {
+    const auto& s = grad ? gstrides : strides;
+    if (shape.empty()) {
+        rows = cols = ld = 1;
+        return true;
+    }
+    cols = shape.back();
+    if (s.back() != 1) return false;
+    rows = 1;
+    for (size_t i = 0; i + 1 < shape.size(); ++i) rows *= shape[i];
+    if (shape.size() == 1) {
+        ld = cols;
+        return true;
+    }
+    ld = s[shape.size() - 2];
+    for (int i = (int)shape.size() - 3; i >= 0; --i)
+        if (shape[(size_t)i] > 1 && s[(size_t)i] != s[(size_t)i + 1] * shape[(size_t)i + 1]) return false;
+    return ld >= cols || rows == 1;
+}
+
+std::string Plan::structure() const {
+    std::string s;
+    for (auto& o : fwd) s += std::string(k_str(o.k)) + ";";
+    return s;
+}
+
+namespace {
+
+struct Val {
+    std::vector<int> parts;
+    bool tuple = false;
+    int one() const {
+        if (tuple || parts.size() != 1) throw Error("expected single tensor, got tuple");
+        return parts[0];
+    }
+};
+
+struct Lowerer {
+    Plan& P;
+    const Module& root;
+    LowerOptions o;
+    std::map<std::string, int> param_views;
+    std::map<int, int> cast_cache;
+    bool in_ckpt = false, ledger_on = true;
+    int cur_region = -1;
+
+    Lowerer(Plan& p, const Module& r, const LowerOptions& opt) : P(p), root(r), o(opt) {}
+
+    // ------------------------------------------------------------ storage
+    int new_storage(i64 numel, DT dt, SKind kind, const std::string& name = "") {
+        Storage s;
+        s.numel = numel;
+        s.dt = dt;
+        s.gdt = kind == SKind::Param || kind == SKind::Input ? sbk::F32 : o.cdt;
+        s.kind = kind;
+        s.region = in_ckpt ? cur_region : -1;
+        s.name = name;
+        P.st.push_back(s);
+        return (int)P.st.size() - 1;
+    }
+    int new_view(int st, std::vector<i64> shape, Dtype rdt) {
+        View v;
+        v.st = v.gst = st;
+        v.shape = shape;
+        v.strides = v.gstrides = contig_strides(shape);
+        v.rdt = rdt;
+        P.views.push_back(v);
+        return (int)P.views.size() - 1;
+    }
+    int fresh(std::vector<i64> shape, Dtype rdt, DT dt = (DT)-1) {
+        i64 n = 1;
+        for (i64 d : shape) n *= d;
+        return new_view(new_storage(n, dt == (DT)-1 ? o.cdt : dt, SKind::Act), shape, rdt);
+    }
+    int aux(i64 n) { return new_view(new_storage(n, sbk::F32, SKind::Aux), {n}, Dtype::F32); }
+    View& V(int id) { return P.views[(size_t)id]; }
+    TensorSpec spec(int v) {
+        TensorSpec s;
+        s.shape = V(v).shape;
+        s.dtype = V(v).rdt;
+        return s;
+    }
+    int emit(Op op) {
+        op.region = in_ckpt ? cur_region : -1;
+        P.fwd.push_back(std::move(op));
+        return (int)P.fwd.size() - 1;
+    }
+    void ledger(const Val& v) {
+        if (!ledger_on) return;
+        for (int p : v.parts) P.ledger_bytes += V(p).numel() * dtype_bytes(V(p).rdt);
+    }
+    u64 dropout_s1(i64 node_seed) { return hash_combine(hash_combine(o.seed, (u64)node_seed), 0xd0); }
+
+    // a compute-dtype, contiguous version of view v
+    int as_compute(int v) {
+        if (P.st[(size_t)V(v).st].dt == sbk::F64) {
+            auto it = cast_cache.find(v);
+            if (it != cast_cache.end()) return it->second;
+            int out = fresh(V(v).shape, V(v).rdt);
+            Op c;
+            c.k = K::Cast;
+            c.in = {v};
+            c.out = {out};
+            emit(c);
+            cast_cache[v] = out;
+            return out;
+        }
+        return v;
+    }
+    int contig(int v) {
+        v = as_compute(v);
+        if (V(v).contiguous() && V(v).g_contiguous()) return v;
+        int out = fresh(V(v).shape, V(v).rdt);
+        Op c;
+        c.k = K::Copy;
+        c.in = {v};
+        c.out = {out};
+        emit(c);
+        return out;
+    }
+    int rowwise(int v) {
+        v = as_compute(v);
+        i64 r, c, ld;
+        if (V(v).rowwise(r, c, ld) && V(v).rowwise(r, c, ld, true)) {
+            i64 r2, c2, ld2;
+            V(v).rowwise(r2, c2, ld2, true);
+            if (ld2 == ld) return v;
+        }
+        return contig(v);
+    }
+
+    // ------------------------------------------------------------- params
+    int param_view(const Module& ctx, const std::string& path, const std::string& target) {
+        std::string key = join(path, target);
+        auto it = param_views.find(key);
+        if (it != param_views.end()) return it->second;
+        const Param* p = ctx.resolve_param(target);
+        if (!p) throw Error("unknown param '" + target + "' in module '" + ctx.name + "'");
+        HostTensor t = param_rank(*p, o.rank);
+        int st = new_storage(t.spec.numel(), o.cdt, SKind::Param, key);
+        P.st[(size_t)st].region = -1;
+        P.st[(size_t)st].needs_grad = true;
+        int v = new_view(st, t.spec.shape, p->spec.dtype);
+        P.params.push_back({key, v});
+        P.param_init.push_back({key, std::move(t)});
+        param_views[key] = v;
+        return v;
+    }
+
+    // ---------------------------------------------------------- modules
+    Val eval_module(const Module& m, const std::string& path, std::vector<Val> args) {
+        if (get_flag(m.attrs, "sync_backward") && o.world > 1 && !args.empty())
+            args[0] = Val{{sync_grad(args[0].one())}, false};
+        bool want_ckpt = (get_flag(m.attrs, "checkpoint") || m.kind == "EfficientAttention") && !in_ckpt;
+        if (want_ckpt) {
+            if (m.kind == "EfficientAttention" && o.fused_kernels) {
+                Val out = flash_attention(m, path, args);
+                if (ledger_on) {
+                    for (auto& a : args) ledger(a);
+                    ledger(out);
+                }
+                return out;
+            }
+            return eval_checkpointed(m, path, args);
+        }
+        if (m.composite()) {
+            Val out;
+            if (o.fused_kernels && get_flag(m.attrs, "fused") && try_fused(m, path, args, out)) return out;
+            return eval_graph(*m.forward, m, path, args);
+        }
+        return eval_builtin(m, path, args);
+    }
+
+    int sync_grad(int in) {
+        View nv = V(in);
+        int gst = new_storage(nv.numel(), o.cdt, SKind::Act, "syncgrad");
+        P.st[(size_t)gst].has_fwd = false;
+        nv.gst = gst;
+        nv.goff = 0;
+        nv.gstrides = contig_strides(nv.shape);
+        P.views.push_back(nv);
+        int out = (int)P.views.size() - 1;
+        Op op;
+        op.k = K::SyncGrad;
+        op.in = {in};
+        op.out = {out};
+        op.ids_input = P.st[(size_t)V(in).st].kind == SKind::Input;
+        emit(op);
+        return out;
+    }
+
+    Val eval_checkpointed(const Module& m, const std::string& path, const std::vector<Val>& args) {
+        bool old_ledger = ledger_on;
+        ledger_on = false;
+        in_ckpt = true;
+        int r = (int)P.regions.size();
+        P.regions.push_back({(int)P.fwd.size(), -1});
+        cur_region = r;
+        Val out;
+        if (m.kind == "EfficientAttention") {
+            Module ref = attention_reference_graph(m);
+            out = eval_graph(*ref.forward, ref, path, args);
+        } else if (m.composite()) {
+            Val f;
+            if (o.fused_kernels && get_flag(m.attrs, "fused") && try_fused(m, path, args, f))
+                out = f;
+            else
+                out = eval_graph(*m.forward, m, path, args);
+        } else {
+            out = eval_builtin(m, path, args);
+        }
+        in_ckpt = false;
+        cur_region = -1;
+        ledger_on = old_ledger;
+        P.regions[(size_t)r].last_op = (int)P.fwd.size() - 1;
+        if (ledger_on) {
+            for (auto& a : args) ledger(a);
+            ledger(out);
+        }
+        return out;
+    }
+
+    Val eval_graph(const Graph& g, const Module& ctx, const std::string& path, const std::vector<Val>& args) {
+        if (args.size() != g.inputs.size())
+            throw Error("graph of '" + (path.empty() ? root.name : path) + "' expects " + std::to_string(g.inputs.size()) +
+                        " inputs, got " + std::to_string(args.size()));
+        std::map<int, Val> env;
+        size_t next = 0;
+        Val result;
+        for (auto& n : g.nodes) {
+            switch (n.kind) {
+                case NK::Input: env[n.id] = args[next++]; break;
+                case NK::ParamRef: env[n.id] = Val{{param_view(ctx, path, n.target)}, false}; break;
+                case NK::CallOp: {
+                    std::vector<Val> a;
+                    for (int x : n.args) a.push_back(env.at(x));
+                    env[n.id] = eval_op(n.op, n.attrs, a, path);
+                    break;
+                }
+                case NK::CallModule: {
+                    const Module* s = ctx.resolve(n.target);
+                    if (!s) throw Error("unknown submodule '" + n.target + "'");
+                    std::vector<Val> a;
+                    for (int x : n.args) a.push_back(env.at(x));
+                    env[n.id] = eval_module(*s, join(path, n.target), a);
+                    break;
+                }
+                case NK::GetItem: {
+                    const Val& v = env.at(n.args[0]);
+                    i64 idx = get_int(n.attrs, "index").value_or(0);
+                    if (!v.tuple || idx < 0 || idx >= (i64)v.parts.size())
+                        throw Error("get_item index " + std::to_string(idx) + " out of range");
+                    env[n.id] = Val{{v.parts[(size_t)idx]}, false};
+                    break;
+                }
+                case NK::Output: {
+                    Val v;
+                    bool anyt = false;
+                    for (int x : n.args) {
+                        anyt |= env.at(x).tuple;
+                        for (int p : env.at(x).parts) v.parts.push_back(p);
+                    }
+                    v.tuple = n.args.size() > 1 || anyt;
+                    result = v;
+                    break;
+                }
+            }
+        }
+        return result;
+    }
+
+    // ----------------------------------------------------------- builtins
+    Val eval_builtin(const Module& m, const std::string& path, const std::vector<Val>& args) {
+        const std::string& k = m.kind;
+        if (k == "Linear" || k == "FusedQKV") return linear(m, path, args[0].one());
+        if (k == "LayerNorm") {
+            int x = contig(args[0].one());
+            int g = param_view(m, path, "gamma"), b = param_view(m, path, "beta");
+            Val out = layernorm(x, g, b, get_double(m.attrs, "eps").value_or(1e-5), path);
+            ledger(out);
+            return out;
+        }
+        if (k == "Dropout") return eval_op("dropout", m.attrs, args, path);
+        if (k == "Embedding") return embedding(m, path, args[0].one());
+        if (k == "EfficientAttention") {
+            if (o.fused_kernels) return flash_attention(m, path, args);
+            Module ref = attention_reference_graph(m);
+            return eval_graph(*ref.forward, ref, path, args);
+        }
+        throw Error("no executor semantics for module kind '" + k + "'");
+    }
+
+    Val linear(const Module& m, const std::string& path, int xin) {
+        const Param* wp = m.param("weight");
+        if (!wp) throw Error("module '" + path + "' missing weight");
+        int x = rowwise(xin);
+        int w = param_view(m, path, "weight");
+        const Param* bp = m.param("bias");
+        int b = bp ? param_view(m, path, "bias") : -1;
+        bool rank0_only = bp && !bp->shard && wp->shard && wp->shard->axis == 1 && o.world > 1;
+        i64 out_f = V(w).shape[0], in_f = V(w).shape[1];
+        if (V(x).shape.empty() || V(x).shape.back() != in_f)
+            throw Error("shape mismatch in '" + path + "': input " + spec(x).str() + " vs weight " + spec(w).str());
+        std::vector<i64> oshape = V(x).shape;
+        oshape.back() = out_f;
+        int y = fresh(oshape, V(x).rdt);
+        Op op;
+        op.k = K::Linear;
+        op.in = {x, w};
+        if (b >= 0) op.in.push_back(b);
+        op.has_bias = b >= 0;
+        op.bias_on = op.bias_grad = b >= 0 && (!rank0_only || o.rank == 0);
+        op.out = {y};
+        op.path = path;
+        Val out;
+        if (m.kind == "FusedQKV") {
+            if (out_f % 3 != 0) throw Error("FusedQKV output features must divide by 3");
+            op.qkv = true;
+            i64 part = out_f / 3;
+            out.tuple = true;
+            for (int pi = 0; pi < 3; ++pi) {
+                View pv = V(y);
+                pv.shape.back() = part;
+                pv.off = pv.goff = pi * part;
+                out.parts.push_back((int)P.views.size());
+                P.views.push_back(pv);
+            }
+        } else {
+            out.parts = {y};
+        }
+        emit(op);
+        ledger(out);
+        return out;
+    }
+
+    Val layernorm(int x, int g, int b, double eps, const std::string& path) {
+        i64 rows = V(x).numel() / V(x).shape.back();
+        int y = fresh(V(x).shape, V(x).rdt);
+        Op op;
+        op.k = K::LayerNorm;
+        op.in = {x};
+        op.affine = g >= 0;
+        if (g >= 0) op.in.insert(op.in.end(), {g, b});
+        op.out = {y, aux(rows), aux(rows)};
+        op.eps = eps;
+        op.path = path;
+        emit(op);
+        return Val{{y}, false};
+    }
+
+    Val embedding(const Module& m, const std::string& path, int ids) {
+        const Param* wp = m.param("weight");
+        if (!wp) throw Error("embedding '" + path + "' missing weight");
+        int w = param_view(m, path, "weight");
+        if (P.st[(size_t)V(ids).st].dt != sbk::F64 || !V(ids).contiguous()) {
+            // ids computed on device: bring them to f64 row ids first
+            int c = fresh(V(ids).shape, V(ids).rdt, sbk::F64);
+            Op op;
+            op.k = K::Cast;
+            op.in = {ids};
+            op.out = {c};
+            emit(op);
+            ids = c;
+        }
+        i64 local = V(w).shape[0], dim = V(w).shape[1];
+        std::vector<i64> shape = V(ids).shape;
+        shape.push_back(dim);
+        int y = fresh(shape, wp->spec.dtype);
+        Op op;
+        op.k = K::Embedding;
+        op.in = {ids, w};
+        op.out = {y};
+        op.full_rows = wp->full_shape()[0];
+        op.row0 = wp->shard ? (i64)o.rank * local : 0;
+        op.path = path;
+        emit(op);
+        Val out{{y}, false};
+        ledger(out);
+        return out;
+    }
+
+    Val flash_attention(const Module& m, const std::string& path, const std::vector<Val>& args) {
+        i64 hd = get_int(m.attrs, "head_dim").value_or(0);
+        if (hd <= 0) throw Error("EfficientAttention requires a positive head_dim attr");
+        double p = get_double(m.attrs, "p").value_or(0.0);
+        i64 seed = get_int(m.attrs, "seed").value_or(0);
+        double scale = get_double(m.attrs, "scale").value_or(1.0 / std::sqrt((double)hd));
+        int q = rowwise(args[0].one()), k = rowwise(args[1].one()), v = rowwise(args[2].one());
+        auto& sh = V(q).shape;
+        if (sh.size() != 3 || V(k).shape != sh || V(v).shape != sh || sh[2] % hd != 0) {
+            // shapes the kernel does not cover: the reference graph, recomputed
+            Module ref = attention_reference_graph(m);
+            return eval_graph(*ref.forward, ref, path, args);
+        }
+        if (p >= 1.0 && o.train) throw Error("dropout p must be < 1");
+        i64 B = sh[0], S = sh[1], nh = sh[2] / hd;
+        int out = fresh(sh, V(q).rdt);
+        Op op;
+        op.k = K::FlashAttn;
+        op.in = {q, k, v};
+        op.out = {out, aux(B * nh * S)};
+        op.hd = hd;
+        op.nh = nh;
+        op.scale = scale;
+        op.p = p;
+        op.dropout = o.train && p > 0.0;
+        if (op.dropout) {
+            op.s1 = dropout_s1(seed);
+            op.thr = dropout_threshold(p);
+        }
+        op.path = path;
+        emit(op);
+        return Val{{out}, false};
+    }
+
+    // ------------------------------------------------------------ fused
+    bool try_fused(const Module& m, const std::string& path, const std::vector<Val>& args, Val& out) {
+        const Graph& g = *m.forward;
+        std::vector<const Node*> core;
+        for (auto& n : g.nodes)
+            if (n.kind != NK::Input && n.kind != NK::Output) core.push_back(&n);
+        for (auto& c : m.children)
+            if (get_flag(c.mod->attrs, "checkpoint")) return false;
+        auto kind_of = [&](const Node* n) -> std::string {
+            if (n->kind == NK::CallModule) {
+                const Module* s = m.resolve(n->target);
+                return s ? "mod:" + s->kind : "?";
+            }
+            if (n->kind == NK::CallOp) return "op:" + n->op;
+            return "?";
+        };
+        if (core.empty() || kind_of(core[0]) != "mod:Linear") return false;
+        if (core[0]->args.size() != 1 || core[0]->args[0] != g.inputs[0]) return false;
+        const Module* lin = m.resolve(core[0]->target);
+        std::string lpath = join(path, core[0]->target);
+        const Node& outn = g.out_node();
+        if (outn.args.size() != 1 || outn.args[0] != core.back()->id) return false;
+        // ---- Linear -> gelu
+        if (core.size() == 2 && kind_of(core[1]) == "op:gelu" && core[1]->args[0] == core[0]->id && g.inputs.size() == 1) {
+            int x = args[0].one();
+            if (get_flag(lin->attrs, "sync_backward") && o.world > 1) x = sync_grad(x);
+            return fused_linear_gelu(*lin, lpath, x, path, out);
+        }
+        // ---- Linear -> [all_reduce] -> [Dropout] -> add(., residual) -> LayerNorm
+        if (g.inputs.size() != 2) return false;
+        size_t i = 1;
+        bool ar = false;
+        const Module* drop = nullptr;
+        int prev = core[0]->id;
+        if (i < core.size() && kind_of(core[i]) == "op:all_reduce" && core[i]->args[0] == prev) {
+            ar = true;
+            prev = core[i++]->id;
+        }
+        if (i < core.size() && kind_of(core[i]) == "mod:Dropout" && core[i]->args[0] == prev) {
+            drop = m.resolve(core[i]->target);
+            if (get_flag(drop->attrs, "sync_backward")) return false;
+            prev = core[i++]->id;
+        }
+        if (i + 2 != core.size() || kind_of(core[i]) != "op:add" || kind_of(core[i + 1]) != "mod:LayerNorm") return false;
+        const Node* add = core[i];
+        int res_node = g.inputs[1];
+        bool ok_order = (add->args[0] == prev && add->args[1] == res_node) || (add->args[1] == prev && add->args[0] == res_node);
+        if (!ok_order || core[i + 1]->args[0] != add->id) return false;
+        const Module* ln = m.resolve(core[i + 1]->target);
+        if (get_flag(ln->attrs, "sync_backward")) return false;
+        const Param* wp = lin->param("weight");
+        const Param* bp = lin->param("bias");
+        if (ar && ((wp->shard && wp->shard->axis != 1) || (bp && bp->shard))) return false;
+        if (V(args[0].one()).shape.size() < 1) return false;
+        int x = args[0].one();
+        if (get_flag(lin->attrs, "sync_backward") && o.world > 1) x = sync_grad(x);
+        int res = contig(args[1].one());
+        x = rowwise(x);
+        int w = param_view(*lin, lpath, "weight");
+        int b = bp ? param_view(*lin, lpath, "bias") : -1;
+        i64 out_f = V(w).shape[0];
+        if (V(x).shape.back() != V(w).shape[1]) return false;
+        std::vector<i64> oshape = V(x).shape;
+        oshape.back() = out_f;
+        if (oshape != V(res).shape) return false;
+        std::string lnpath = join(path, core[i + 1]->target);
+        int gm = param_view(*ln, lnpath, "gamma"), bt = param_view(*ln, lnpath, "beta");
+        i64 rows = V(res).numel() / out_f;
+        Dtype rdt = V(x).rdt;
+        int partial = fresh(oshape, rdt), sum = fresh(oshape, rdt), y = fresh(oshape, rdt);
+        Op op;
+        op.k = K::FusedLinearResLN;
+        op.in = {x, w, res, gm, bt};
+        op.has_bias = b >= 0;
+        if (b >= 0) op.in.push_back(b);
+        bool rank0_only = bp && !bp->shard && wp->shard && wp->shard->axis == 1 && o.world > 1;
+        // after an in-region all_reduce the whole bias is added once on every
+        // rank; its gradient still lands on rank 0 only (executor.cpp:645,1146)
+        op.bias_on = b >= 0 && (ar || !rank0_only || o.rank == 0);
+        op.bias_grad = b >= 0 && (!rank0_only || o.rank == 0);
+        op.allreduce = ar && o.world > 1;
+        op.out = {y, partial, sum, aux(rows), aux(rows)};
+        op.eps = get_double(ln->attrs, "eps").value_or(1e-5);
+        if (drop) {
+            double p = get_double(drop->attrs, "p").value_or(0.0);
+            if (o.train && p > 0.0) {
+                if (p >= 1.0) throw Error("dropout p must be < 1");
+                op.dropout = true;
+                op.p = p;
+                op.s1 = dropout_s1(get_int(drop->attrs, "seed").value_or(0));
+                op.thr = dropout_threshold(p);
+            }
+        }
+        op.path = path;
+        emit(op);
+        if (ar) P.collectives_fwd += 1;
+        // reference ledger: linear, [all_reduce], [dropout], add, LayerNorm outputs
+        int nouts = 3 + (ar ? 1 : 0) + (drop ? 1 : 0);
+        if (ledger_on) P.ledger_bytes += nouts * V(y).numel() * dtype_bytes(rdt);
+        out = Val{{y}, false};
+        return true;
+    }
+
+    bool fused_linear_gelu(const Module& lin, const std::string& lpath, int xin, const std::string& path, Val& out) {
+        int x = rowwise(xin);
+        int w = param_view(lin, lpath, "weight");
+        const Param* wp = lin.param("weight");
+        const Param* bp = lin.param("bias");
+        int b = bp ? param_view(lin, lpath, "bias") : -1;
+        if (V(x).shape.back() != V(w).shape[1]) throw Error("shape mismatch in '" + lpath + "'");
+        std::vector<i64> oshape = V(x).shape;
+        oshape.back() = V(w).shape[0];
+        int act = fresh(oshape, V(x).rdt), pre = fresh(oshape, V(x).rdt);
+        Op op;
+        op.k = K::FusedLinearGelu;
+        op.in = {x, w};
+        if (b >= 0) op.in.push_back(b);
+        op.has_bias = b >= 0;
+        bool rank0_only = bp && !bp->shard && wp->shard && wp->shard->axis == 1 && o.world > 1;
+        op.bias_on = op.bias_grad = b >= 0 && (!rank0_only || o.rank == 0);
+        op.out = {act, pre};
+        op.path = path;
+        emit(op);
+        if (ledger_on) P.ledger_bytes += 2 * V(act).numel() * dtype_bytes(V(act).rdt);
+        out = Val{{act}, false};
+        return true;
+    }
+
+    // ---------------------------------------------------------------- ops
+    Val eval_op(const std::string& op, const Attrs& at, const std::vector<Val>& args, const std::string& path) {
+        Val out = eval_op_inner(op, at, args, path);
+        ledger(out);
+        return out;
+    }
+
+    int unary_op(K k, int x, double c = 1.0) {
+        x = contig(x);
+        int y = fresh(V(x).shape, V(x).rdt);
+        Op op;
+        op.k = k;
+        op.in = {x};
+        op.out = {y};
+        op.scale = c;
+        emit(op);
+        return y;
+    }
+
+    Val eval_op_inner(const std::string& opn, const Attrs& at, const std::vector<Val>& args, const std::string& path) {
+        auto arg = [&](size_t i) { return args.at(i).one(); };
+        if (opn == "all_reduce") {
+            int x = arg(0);
+            P.collectives_fwd += 1;
+            if (o.world == 1) {
+                // one-rank sum: the value itself (the count still matches the reference)
+                Op op;
+                op.k = K::AllReduce;
+                op.in = {x};
+                op.out = {x};
+                op.allreduce = false;
+                emit(op);
+                return Val{{x}, false};
+            }
+            x = contig(x);
+            int y = fresh(V(x).shape, V(x).rdt);
+            Op op;
+            op.k = K::AllReduce;
+            op.in = {x};
+            op.out = {y};
+            op.allreduce = true;
+            emit(op);
+            return Val{{y}, false};
+        }
+        if (opn == "all_gather") {
+            int x = contig(arg(0));
+            int axis = (int)get_int(at, "axis").value_or(-1);
+            if (axis < 0) axis += (int)V(x).shape.size();
+            std::vector<i64> shape = V(x).shape;
+            shape[(size_t)axis] *= o.world;
+            int y = fresh(shape, V(x).rdt);
+            Op op;
+            op.k = K::AllGather;
+            op.in = {x};
+            op.out = {y};
+            op.axis = axis;
+            emit(op);
+            P.collectives_fwd += 1;
+            return Val{{y}, false};
+        }
+        std::vector<const ValueSpec*> sp;
+        std::vector<ValueSpec> sps;
+        for (auto& a : args) {
+            ValueSpec vs;
+            for (int p : a.parts) vs.parts.push_back(spec(p));
+            vs.tuple = a.tuple;
+            sps.push_back(vs);
+        }
+        for (auto& s : sps) sp.push_back(&s);
+        ValueSpec os = infer_op(opn, sp, at, -1);
+        if (opn == "matmul") {
+            int a = contig(arg(0)), b = contig(arg(1));
+            int y = fresh(os.one().shape, V(a).rdt);
+            Op op;
+            op.k = K::Matmul;
+            op.in = {a, b};
+            op.out = {y};
+            emit(op);
+            return Val{{y}, false};
+        }
+        if (opn == "add" || opn == "mul") {
+            int a = contig(arg(0)), b = contig(arg(1));
+            bool as = V(a).shape.empty();
+            int y = fresh(os.one().shape, V(as ? b : a).rdt);
+            Op op;
+            op.k = opn == "add" ? K::Add : K::Mul;
+            op.in = {a, b};
+            op.out = {y};
+            emit(op);
+            return Val{{y}, false};
+        }
+        if (opn == "scale") return Val{{unary_op(K::Scale, arg(0), get_double(at, "factor").value_or(1.0))}, false};
+        if (opn == "relu") return Val{{unary_op(K::Relu, arg(0))}, false};
+        if (opn == "gelu") return Val{{unary_op(K::Gelu, arg(0))}, false};
+        if (opn == "softmax") {
+            int x = contig(arg(0));
+            int r = (int)V(x).shape.size();
+            i64 ax = get_int(at, "axis").value_or(-1);
+            int y = fresh(V(x).shape, V(x).rdt);
+            Op op;
+            op.k = K::Softmax;
+            op.in = {x};
+            op.out = {y};
+            op.axis = (int)(ax < 0 ? ax + r : ax);
+            emit(op);
+            return Val{{y}, false};
+        }
+        if (opn == "layernorm") {
+            int x = contig(arg(0));
+            return layernorm(x, -1, -1, get_double(at, "eps").value_or(1e-5), path);
+        }
+        if (opn == "dropout") {
+            double p = get_double(at, "p").value_or(0.0);
+            int x = arg(0);
+            if (!o.train || p <= 0.0) return Val{{x}, false};  // identity (executor.cpp:795)
+            if (p >= 1.0) throw Error("dropout p must be < 1");
+            x = contig(x);
+            int y = fresh(V(x).shape, V(x).rdt);
+            Op op;
+            op.k = K::Dropout;
+            op.in = {x};
+            op.out = {y};
+            op.p = p;
+            op.s1 = dropout_s1(get_int(at, "seed").value_or(0));
+            op.thr = dropout_threshold(p);
+            emit(op);
+            return Val{{y}, false};
+        }
+        if (opn == "transpose") {
+            int x = as_compute(arg(0));
+            int r = (int)V(x).shape.size();
+            std::vector<int> perm;
+            if (auto pm = get_ints(at, "perm")) {
+                for (i64 v : *pm) perm.push_back((int)(v < 0 ? v + r : v));
+            } else {
+                auto axes = get_ints(at, "axes").value_or(std::vector<i64>{-2, -1});
+                for (int i = 0; i < r; ++i) perm.push_back(i);
+                std::swap(perm[(size_t)(axes[0] < 0 ? axes[0] + r : axes[0])], perm[(size_t)(axes[1] < 0 ? axes[1] + r : axes[1])]);
+            }
+            int y = fresh(os.one().shape, V(x).rdt);
+            Op op;
+            op.k = K::Permute;
+            op.in = {x};
+            op.out = {y};
+            op.perm = perm;
+            emit(op);
+            return Val{{y}, false};
+        }
+        if (opn == "reshape") {
+            int x = contig(arg(0));
+            View nv = V(x);
+            nv.shape = os.one().shape;
+            nv.strides = nv.gstrides = contig_strides(nv.shape);
+            P.views.push_back(nv);
+            return Val{{(int)P.views.size() - 1}, false};
+        }
+        if (opn == "split") {
+            int x = as_compute(arg(0));
+            int r = (int)V(x).shape.size();
+            i64 ax = get_int(at, "axis").value_or(-1);
+            int axis = (int)(ax < 0 ? ax + r : ax);
+            Val out;
+            out.tuple = true;
+            i64 offset = 0;
+            for (auto& ps : os.parts) {
+                View pv = V(x);
+                pv.shape = ps.shape;
+                pv.off += offset * pv.strides[(size_t)axis];
+                pv.goff += offset * pv.gstrides[(size_t)axis];
+                offset += ps.shape[(size_t)axis];
+                P.views.push_back(pv);
+                out.parts.push_back((int)P.views.size() - 1);
+            }
+            return out;
+        }
+        if (opn == "concat") {
+            std::vector<int> ins;
+            for (size_t i = 0; i < args.size(); ++i) ins.push_back(as_compute(arg(i)));
+            int r = (int)V(ins[0]).shape.size();
+            i64 ax = get_int(at, "axis").value_or(-1);
+            int y = fresh(os.one().shape, V(ins[0]).rdt);
+            Op op;
+            op.k = K::Concat;
+            op.in = ins;
+            op.out = {y};
+            op.axis = (int)(ax < 0 ? ax + r : ax);
+            emit(op);
+            return Val{{y}, false};
+        }
+        if (opn == "reduce_sum") {
+            int x = contig(arg(0));
+            int y = fresh(os.one().shape, V(x).rdt);
+            Op op;
+            op.k = K::ReduceSum;
+            op.in = {x};
+            op.out = {y};
+            if (auto ax = get_int(at, "axis")) {
+                int r = (int)V(x).shape.size();
+                op.axis = (int)(*ax < 0 ? *ax + r : *ax);
+            } else {
+                op.reduce_all = true;
+            }
+            emit(op);
+            return Val{{y}, false};
+        }
+        throw Error("unknown op '" + opn + "'");
+    }
+
+    void run() {
+        auto specs = declared_inputs(*root.forward);
+        std::vector<Val> args;
+        for (auto& s : specs) {
+            int st = new_storage(s.numel(), sbk::F64, SKind::Input, "input");
+            P.st[(size_t)st].needs_grad = true;
+            int v = new_view(st, s.shape, s.dtype);
+            P.inputs.push_back(v);
+            args.push_back(Val{{v}, false});
+        }
+        Val out = eval_module(root, "", args);
+        P.outputs = out.parts;
+    }
+};
+
+}  // namespace
+
+Plan lower(const Module& root, const LowerOptions& o) {
+    Plan P;
+    P.rank = o.rank;
+    P.world = o.world;
+    P.cdt = o.cdt;
+    P.train = o.train;
+    if (o.world < 1) throw Error("world_size must be >= 1");
+    Lowerer L(P, root, o);
+    L.run();
+    // Drop empty regions; keep region-internal storages in scratch only when
+    // nothing outside the region reads them.
+    std::vector<Region> keep;
+    std::vector<int> remap(P.regions.size(), -1);
+    for (size_t r = 0; r < P.regions.size(); ++r)
+        if (P.regions[r].last_op >= P.regions[r].first_op) {
+            remap[r] = (int)keep.size();
+            keep.push_back(P.regions[r]);
+        }
+    P.regions = keep;
+    for (auto& op : P.fwd) op.region = op.region >= 0 ? remap[(size_t)op.region] : -1;
+    for (auto& s : P.st) s.region = s.region >= 0 ? remap[(size_t)s.region] : -1;
+    auto escape = [&](int v) {
+        auto& vv = P.views[(size_t)v];
+        P.st[(size_t)vv.st].region = -1;
+        P.st[(size_t)vv.gst].region = -1;
+    };
+    for (auto& op : P.fwd)
+        for (int v : op.in)
+            if (P.st[(size_t)P.views[(size_t)v].st].region != op.region || op.region < 0) {
+                if (P.st[(size_t)P.views[(size_t)v].st].region != op.region) escape(v);
+            }
+    for (int v : P.outputs) escape(v);
+    return P;
+}
+
+}  // namespace sb

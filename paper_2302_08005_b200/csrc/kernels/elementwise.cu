@@ -1,0 +1,488 @@
+// Elementwise / reduction / copy / RNG-dropout / embedding / simulated
+// collective kernels. HBM-bound: grid-stride loops, 16-byte vector accesses on
+// the hot contiguous paths, deterministic fixed-order reductions (no float
+// atomics), so identical runs give identical bits (the reference's
+// determinism contract, proj/tests/executor_test.cpp:273-283).
+#include "common.cuh"
+
+namespace sbk {
+
+namespace {
+float* g_red_ws = nullptr;  // deterministic reduction partials
+constexpr int kRedBlocks = 296;
+}  // namespace
+
+void init_workspace() {
+    if (!g_red_ws) cudaMalloc(&g_red_ws, sizeof(float) * kRedBlocks * 2);
+}
+
+// ------------------------------------------------------------------- fill/cast
+template <class T>
+__global__ void k_fill(T* x, i64 n, float v) {
+    for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) x[i] = from_f<T>(v);
+}
+void fill(void* x, DT t, i64 n, float v, cudaStream_t s) {
+    dispatch(t, [&](auto* p) {
+        using T = std::remove_pointer_t<decltype(p)>;
+        k_fill<T><<<grid_for(n, 256), 256, 0, s>>>((T*)x, n, v);
+    });
+    SBK_CHECK_LAUNCH();
+}
+
+template <class A, class B>
+__device__ __forceinline__ B conv(A a) {
+    if constexpr (std::is_same_v<A, B>) return a;
+    else if constexpr (std::is_same_v<A, double> && std::is_same_v<B, bf16>) return __double2bfloat16(a);
+    else if constexpr (std::is_same_v<A, double>) return (B)a;
+    else if constexpr (std::is_same_v<B, double>) return (double)to_f<A>(a);
+    else return from_f<B>(to_f<A>(a));
+}
+
+template <class A, class B>
+__global__ void k_cast(const A* x, B* y, i64 n) {
+    for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) y[i] = conv<A, B>(x[i]);
+}
+void cast(const void* x, DT tx, void* y, DT ty, i64 n, cudaStream_t s) {
+    dispatch(tx, [&](auto* pa) {
+        using A = std::remove_pointer_t<decltype(pa)>;
+        dispatch(ty, [&](auto* pb) {
+            using B = std::remove_pointer_t<decltype(pb)>;
+            k_cast<A, B><<<grid_for(n, 256), 256, 0, s>>>((const A*)x, (B*)y, n);
+        });
+    });
+    SBK_CHECK_LAUNCH();
+}
+
+// ------------------------------------------------------------------- binary
+template <class T>
+__global__ void k_binary(int op, const T* a, i64 an, const T* b, i64 bn, T* y, i64 n) {
+    for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
+        float av = to_f(a[an == 1 ? 0 : i]), bv = to_f(b[bn == 1 ? 0 : i]);
+        y[i] = from_f<T>(op == 0 ? av + bv : av * bv);
+    }
+}
+void binary(int op, const void* a, i64 a_n, const void* b, i64 b_n, void* y, DT t, i64 n, cudaStream_t s) {
+    dispatch(t, [&](auto* p) {
+        using T = std::remove_pointer_t<decltype(p)>;
+        k_binary<T><<<grid_for(n, 256), 256, 0, s>>>(op, (const T*)a, a_n, (const T*)b, b_n, (T*)y, n);
+    });
+    SBK_CHECK_LAUNCH();
+}
+
+template <class T>
+__global__ void k_unary(int op, const T* x, T* y, i64 n, float c) {
+    for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
+        float v = to_f(x[i]);
+        y[i] = from_f<T>(op == 0 ? v * c : op == 1 ? (v > 0.f ? v : 0.f) : gelu_f(v));
+    }
+}
+void unary(int op, const void* x, void* y, DT t, i64 n, float c, cudaStream_t s) {
+    dispatch(t, [&](auto* p) {
+        using T = std::remove_pointer_t<decltype(p)>;
+        k_unary<T><<<grid_for(n, 256), 256, 0, s>>>(op, (const T*)x, (T*)y, n, c);
+    });
+    SBK_CHECK_LAUNCH();
+}
+
+template <class T>
+__global__ void k_unary_bwd(int op, const T* x, const T* g, T* gx, i64 n, float c) {
+    for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
+        float gv = to_f(g[i]), d;
+        if (op == 0) d = c * gv;
+        else if (op == 1) d = to_f(x[i]) > 0.f ? gv : 0.f;  // executor.cpp:1298-1305
+        else d = gv * gelu_grad_f(to_f(x[i]));
+        gx[i] = from_f<T>(to_f(gx[i]) + d);
+    }
+}
+void unary_bwd(int op, const void* x, const void* g, void* gx, DT t, DT tg, i64 n, float c, cudaStream_t s) {
+    (void)tg;
+    dispatch(t, [&](auto* p) {
+        using T = std::remove_pointer_t<decltype(p)>;
+        k_unary_bwd<T><<<grid_for(n, 256), 256, 0, s>>>(op, (const T*)x, (const T*)g, (T*)gx, n, c);
+    });
+    SBK_CHECK_LAUNCH();
+}
+
+template <class A, class B>
+__global__ void k_acc(const A* x, B* y, i64 n, float alpha) {
+    for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
+        y[i] = from_f<B>(to_f(y[i]) + alpha * to_f(x[i]));
+}
+void accumulate(const void* x, DT tx, void* y, DT ty, i64 n, float alpha, cudaStream_t s) {
+    dispatch(tx, [&](auto* pa) {
+        using A = std::remove_pointer_t<decltype(pa)>;
+        dispatch(ty, [&](auto* pb) {
+            using B = std::remove_pointer_t<decltype(pb)>;
+            k_acc<A, B><<<grid_for(n, 256), 256, 0, s>>>((const A*)x, (B*)y, n, alpha);
+        });
+    });
+    SBK_CHECK_LAUNCH();
+}
+
+template <class T>
+__global__ void k_add_scalar(T* x, i64 n, float v, const T* g) {
+    float add = g ? to_f(g[0]) : v;
+    for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
+        x[i] = from_f<T>(to_f(x[i]) + add);
+}
+void add_scalar(void* x, DT t, i64 n, float v, const void* g, cudaStream_t s) {
+    dispatch(t, [&](auto* p) {
+        using T = std::remove_pointer_t<decltype(p)>;
+        k_add_scalar<T><<<grid_for(n, 256), 256, 0, s>>>((T*)x, n, v, (const T*)g);
+    });
+    SBK_CHECK_LAUNCH();
+}
+
+// deterministic sum: fixed grid partials, then one block in fixed order
+template <class A>
+__global__ void k_red_partial(const A* x, i64 n, float* part) {
+    __shared__ float sh[32];
+    float acc = 0.f;
+    for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) acc += to_f(x[i]);
+    acc = warp_sum(acc);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        float v = threadIdx.x < blockDim.x / 32 ? sh[threadIdx.x] : 0.f;
+        v = warp_sum(v);
+        if (threadIdx.x == 0) part[blockIdx.x] = v;
+    }
+}
+template <class B>
+__global__ void k_red_final(const float* part, int np, B* y, bool acc) {
+    __shared__ float sh[32];
+    float v = 0.f;
+    for (int i = threadIdx.x; i < np; i += blockDim.x) v += part[i];
+    v = warp_sum(v);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        float w = threadIdx.x < blockDim.x / 32 ? sh[threadIdx.x] : 0.f;
+        w = warp_sum(w);
+        if (threadIdx.x == 0) y[0] = from_f<B>(acc ? to_f(y[0]) + w : w);
+    }
+}
+void reduce_all(const void* x, DT tx, i64 n, void* y, DT ty, bool acc, cudaStream_t s) {
+    init_workspace();
+    int nb = (int)std::min<i64>(kRedBlocks, std::max<i64>(1, (n + 255) / 256));
+    dispatch(tx, [&](auto* pa) {
+        using A = std::remove_pointer_t<decltype(pa)>;
+        k_red_partial<A><<<nb, 256, 0, s>>>((const A*)x, n, g_red_ws);
+    });
+    dispatch(ty, [&](auto* pb) {
+        using B = std::remove_pointer_t<decltype(pb)>;
+        k_red_final<B><<<1, 256, 0, s>>>(g_red_ws, nb, (B*)y, acc);
+    });
+    SBK_CHECK_LAUNCH();
+}
+
+template <class T>
+__global__ void k_reduce_axis(const T* x, T* y, i64 outer, i64 adim, i64 inner, bool acc) {
+    i64 n = outer * inner;
+    for (i64 idx = blockIdx.x * (i64)blockDim.x + threadIdx.x; idx < n; idx += (i64)gridDim.x * blockDim.x) {
+        i64 o = idx / inner, i = idx % inner;
+        float s = 0.f;
+        for (i64 a = 0; a < adim; ++a) s += to_f(x[(o * adim + a) * inner + i]);
+        y[idx] = from_f<T>(acc ? to_f(y[idx]) + s : s);
+    }
+}
+void reduce_axis(const void* x, void* y, DT t, i64 outer, i64 adim, i64 inner, bool acc, cudaStream_t s) {
+    dispatch(t, [&](auto* p) {
+        using T = std::remove_pointer_t<decltype(p)>;
+        k_reduce_axis<T><<<grid_for(outer * inner, 256), 256, 0, s>>>((const T*)x, (T*)y, outer, adim, inner, acc);
+    });
+    SBK_CHECK_LAUNCH();
+}
+template <class T>
+__global__ void k_bcast_axis(const T* g, T* gx, i64 outer, i64 adim, i64 inner) {
+    i64 n = outer * adim * inner;
+    for (i64 idx = blockIdx.x * (i64)blockDim.x + threadIdx.x; idx < n; idx += (i64)gridDim.x * blockDim.x) {
+        i64 o = idx / (adim * inner), i = idx % inner;
+        gx[idx] = from_f<T>(to_f(gx[idx]) + to_f(g[o * inner + i]));
+    }
+}
+void broadcast_axis_acc(const void* g, void* gx, DT t, i64 outer, i64 adim, i64 inner, cudaStream_t s) {
+    dispatch(t, [&](auto* p) {
+        using T = std::remove_pointer_t<decltype(p)>;
+        k_bcast_axis<T><<<grid_for(outer * adim * inner, 256), 256, 0, s>>>((const T*)g, (T*)gx, outer, adim, inner);
+    });
+    SBK_CHECK_LAUNCH();
+}
+
+// ga += g * other, reduced to a scalar when ga_n == 1 and n > 1
+template <class T>
+__global__ void k_mul_bwd(const T* g, const T* other, i64 on, T* ga, i64 n) {
+    for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
+        ga[i] = from_f<T>(to_f(ga[i]) + to_f(g[i]) * to_f(other[on == 1 ? 0 : i]));
+}
+template <class T>
+__global__ void k_mul_bwd_scalar(const T* g, const T* other, i64 on, T* ga, i64 n) {
+    __shared__ float sh[32];
+    float acc = 0.f;
+    for (i64 i = threadIdx.x; i < n; i += blockDim.x) acc += to_f(g[i]) * to_f(other[on == 1 ? 0 : i]);
+    acc = warp_sum(acc);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        float v = threadIdx.x < blockDim.x / 32 ? sh[threadIdx.x] : 0.f;
+        v = warp_sum(v);
+        if (threadIdx.x == 0) ga[0] = from_f<T>(to_f(ga[0]) + v);
+    }
+}
+void mul_bwd(const void* g, DT tg, const void* other, i64 other_n, void* ga, DT tga, i64 ga_n, i64 n, cudaStream_t s) {
+    (void)tga;
+    dispatch(tg, [&](auto* p) {
+        using T = std::remove_pointer_t<decltype(p)>;
+        if (ga_n == 1 && n > 1)
+            k_mul_bwd_scalar<T><<<1, 1024, 0, s>>>((const T*)g, (const T*)other, other_n, (T*)ga, n);
+        else
+            k_mul_bwd<T><<<grid_for(n, 256), 256, 0, s>>>((const T*)g, (const T*)other, other_n, (T*)ga, n);
+    });
+    SBK_CHECK_LAUNCH();
+}
+
+// -------------------------------------------------------------------- dropout
+template <class T>
+__global__ void k_dropout(const T* x, T* y, i64 n, uint64_t s1, uint64_t thr, float scale, bool acc) {
+    for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
+        float v = d_keep(s1, (uint64_t)i, thr) ? to_f(x[i]) * scale : 0.f;
+        y[i] = from_f<T>(acc ? to_f(y[i]) + v : v);
+    }
+}
+void dropout(const void* x, void* y, DT t, i64 n, u64 s1, u64 thr, float scale, bool acc, cudaStream_t s) {
+    dispatch(t, [&](auto* p) {
+        using T = std::remove_pointer_t<decltype(p)>;
+        k_dropout<T><<<grid_for(n, 256), 256, 0, s>>>((const T*)x, (T*)y, n, s1, thr, scale, acc);
+    });
+    SBK_CHECK_LAUNCH();
+}
+__global__ void k_dropout_mask(uint32_t* bits, i64 n, uint64_t s1, uint64_t thr) {
+    i64 nw = (n + 31) / 32;
+    for (i64 w = blockIdx.x * (i64)blockDim.x + threadIdx.x; w < nw; w += (i64)gridDim.x * blockDim.x) {
+        uint32_t m = 0;
+        for (int b = 0; b < 32; ++b) {
+            i64 i = w * 32 + b;
+            if (i < n && d_keep(s1, (uint64_t)i, thr)) m |= 1u << b;
+        }
+        bits[w] = m;
+    }
+}
+void dropout_mask(uint32_t* bits, i64 n, u64 s1, u64 thr, cudaStream_t s) {
+    k_dropout_mask<<<grid_for((n + 31) / 32, 256), 256, 0, s>>>(bits, n, s1, thr);
+    SBK_CHECK_LAUNCH();
+}
+
+// --------------------------------------------------------------- strided copy
+struct Idx8 {
+    i64 shape[8], ss[8], ds[8];
+    int rank;
+};
+template <class A, class B>
+__global__ void k_strided(const A* src, B* dst, Idx8 ix, i64 n, bool acc) {
+    for (i64 lin = blockIdx.x * (i64)blockDim.x + threadIdx.x; lin < n; lin += (i64)gridDim.x * blockDim.x) {
+        i64 rem = lin, so = 0, dof = 0;
+        for (int d = ix.rank - 1; d >= 0; --d) {
+            i64 c = rem % ix.shape[d];
+            rem /= ix.shape[d];
+            so += c * ix.ss[d];
+            dof += c * ix.ds[d];
+        }
+        if constexpr (std::is_same_v<B, double>) {
+            dst[dof] = acc ? dst[dof] + conv<A, double>(src[so]) : conv<A, double>(src[so]);
+        } else {
+            B v = conv<A, B>(src[so]);
+            dst[dof] = acc ? from_f<B>(to_f(dst[dof]) + to_f(v)) : v;
+        }
+    }
+}
+void strided_copy(const void* src, DT ts, const i64* sst, void* dst, DT td, const i64* dstr, const i64* shape, int rank,
+                  bool acc, cudaStream_t s) {
+    if (rank > 8) throw std::runtime_error("strided_copy: rank > 8");
+    Idx8 ix{};
+    ix.rank = rank;
+    i64 n = 1;
+    for (int d = 0; d < rank; ++d) {
+        ix.shape[d] = shape[d];
+        ix.ss[d] = sst[d];
+        ix.ds[d] = dstr[d];
+        n *= shape[d];
+    }
+    if (n == 0) return;
+    dispatch(ts, [&](auto* pa) {
+        using A = std::remove_pointer_t<decltype(pa)>;
+        dispatch(td, [&](auto* pb) {
+            using B = std::remove_pointer_t<decltype(pb)>;
+            k_strided<A, B><<<grid_for(n, 256), 256, 0, s>>>((const A*)src, (B*)dst, ix, n, acc);
+        });
+    });
+    SBK_CHECK_LAUNCH();
+}
+
+// ------------------------------------------------------------------ nan guard
+template <class T>
+__global__ void k_nan(const T* x, i64 n, int* flag) {
+    int c = 0;
+    for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) c += isnan(to_f(x[i]));
+    if (c) atomicAdd(flag, c);
+}
+void count_nan(const void* x, DT t, i64 n, int* flag, cudaStream_t s) {
+    dispatch(t, [&](auto* p) {
+        using T = std::remove_pointer_t<decltype(p)>;
+        k_nan<T><<<grid_for(n, 256), 256, 0, s>>>((const T*)x, n, flag);
+    });
+    SBK_CHECK_LAUNCH();
+}
+
+// ---------------------------------------------------------- rank-local sums
+struct Ptrs16 {
+    const void* src[16];
+    void* dst[16];
+};
+template <class T>
+__global__ void k_sum_ranks(Ptrs16 p, int R, i64 n, bool acc) {
+    for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
+        float s = 0.f;
+        for (int r = 0; r < R; ++r) s += to_f(((const T*)p.src[r])[i]);  // rank-ascending fold (executor.cpp:813-817)
+        for (int r = 0; r < R; ++r) {
+            T* d = (T*)p.dst[r];
+            d[i] = from_f<T>(acc ? to_f(d[i]) + s : s);
+        }
+    }
+}
+void sum_ranks(const void* const* srcs, void* const* dsts, int R, DT t, i64 n, bool acc, cudaStream_t s) {
+    if (R > 16) throw std::runtime_error("sum_ranks: more than 16 ranks");
+    Ptrs16 p{};
+    for (int r = 0; r < R; ++r) {
+        p.src[r] = srcs[r];
+        p.dst[r] = dsts[r];
+    }
+    dispatch(t, [&](auto* q) {
+        using T = std::remove_pointer_t<decltype(q)>;
+        k_sum_ranks<T><<<grid_for(n, 256), 256, 0, s>>>(p, R, n, acc);
+    });
+    SBK_CHECK_LAUNCH();
+}
+
+// ------------------------------------------------------------------ embedding
+// row = llround(raw) mod V, vocab-parallel rows [row0, row0+local) (executor.cpp:14-17,749-784)
+__device__ __forceinline__ i64 d_row(double raw, i64 V) {
+    i64 i = (i64)llround(raw) % V;
+    return i < 0 ? i + V : i;
+}
+template <class T>
+__global__ void k_emb_fwd(const double* ids, i64 n, const T* table, i64 dim, i64 V, i64 row0, i64 local, T* out) {
+    i64 total = n * dim;
+    for (i64 idx = blockIdx.x * (i64)blockDim.x + threadIdx.x; idx < total; idx += (i64)gridDim.x * blockDim.x) {
+        i64 i = idx / dim, d = idx % dim;
+        i64 r = d_row(ids[i], V) - row0;
+        out[idx] = (r >= 0 && r < local) ? table[r * dim + d] : from_f<T>(0.f);
+    }
+}
+void embedding_fwd(const double* ids, i64 n, const void* table, DT t, i64 dim, i64 V, i64 row0, i64 local, void* out,
+                   cudaStream_t s) {
+    dispatch(t, [&](auto* p) {
+        using T = std::remove_pointer_t<decltype(p)>;
+        k_emb_fwd<T><<<grid_for(n * dim, 256), 256, 0, s>>>(ids, n, (const T*)table, dim, V, row0, local, (T*)out);
+    });
+    SBK_CHECK_LAUNCH();
+}
+// Deterministic scatter-add. k_emb_sort: one block bitonic-sorts the keys
+// (row << 32 | position) of the local hits (non-local ids sort last);
+// k_emb_seg: the block owning a segment head sums that row's positions in
+// ascending order and adds once into the table gradient.
+static i64 pow2_at_least(i64 n) {
+    i64 p = 1;
+    while (p < n) p <<= 1;
+    return p;
+}
+size_t embedding_bwd_workspace(i64 n) { return (size_t)pow2_at_least(std::max<i64>(n, 1)) * 8; }
+__global__ void k_emb_sort(const double* ids, i64 n, i64 N, i64 V, i64 row0, i64 local, unsigned long long* keys) {
+    for (i64 i = threadIdx.x; i < N; i += blockDim.x) {
+        unsigned long long k = ~0ull;
+        if (i < n) {
+            i64 r = d_row(ids[i], V) - row0;
+            if (r >= 0 && r < local) k = ((unsigned long long)r << 32) | (unsigned long long)i;
+        }
+        keys[i] = k;
+    }
+    __syncthreads();
+    for (i64 size = 2; size <= N; size <<= 1) {
+        for (i64 stride = size >> 1; stride > 0; stride >>= 1) {
+            for (i64 i = threadIdx.x; i < N; i += blockDim.x) {
+                i64 j = i ^ stride;
+                if (j > i) {
+                    bool up = (i & size) == 0;
+                    unsigned long long a = keys[i], b = keys[j];
+                    if ((a > b) == up) {
+                        keys[i] = b;
+                        keys[j] = a;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+template <class T>
+__global__ void k_emb_seg(const unsigned long long* keys, i64 n, const T* g, i64 dim, float* gt) {
+    i64 j = blockIdx.x;
+    unsigned long long k = keys[j];
+    if (k == ~0ull) return;
+    unsigned row = (unsigned)(k >> 32);
+    if (j > 0 && (unsigned)(keys[j - 1] >> 32) == row && keys[j - 1] != ~0ull) return;  // not a head
+    i64 d = blockIdx.y * (i64)blockDim.x + threadIdx.x;
+    if (d >= dim) return;
+    float acc = 0.f;
+    for (i64 m = j; m < n; ++m) {
+        unsigned long long km = keys[m];
+        if (km == ~0ull || (unsigned)(km >> 32) != row) break;
+        acc += to_f(g[(i64)(km & 0xffffffffull) * dim + d]);
+    }
+    gt[(i64)row * dim + d] += acc;
+}
+void embedding_bwd(const double* ids, i64 n, const void* g, DT tg, i64 dim, i64 V, i64 row0, i64 local, float* gt,
+                   void* ws, cudaStream_t s) {
+    i64 N = pow2_at_least(std::max<i64>(n, 1));
+    auto* keys = (unsigned long long*)ws;
+    k_emb_sort<<<1, 1024, 0, s>>>(ids, n, N, V, row0, local, keys);
+    dim3 grid((unsigned)n, (unsigned)((dim + 255) / 256));
+    dispatch(tg, [&](auto* p) {
+        using T = std::remove_pointer_t<decltype(p)>;
+        k_emb_seg<T><<<grid, 256, 0, s>>>(keys, n, (const T*)g, dim, gt);
+    });
+    SBK_CHECK_LAUNCH();
+}
+
+// ------------------------------------------------------------------ bias grad
+// db[c] += sum_r g[r*ld + c]: fixed row chunks -> partials -> ordered sum.
+constexpr int kBiasChunk = 256;
+template <class T>
+__global__ void k_bias_partial(const T* g, i64 ld, i64 rows, i64 cols, float* part) {
+    i64 c = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+    i64 r0 = (i64)blockIdx.y * kBiasChunk;
+    if (c >= cols) return;
+    float acc = 0.f;
+    i64 r1 = r0 + kBiasChunk < rows ? r0 + kBiasChunk : rows;
+    for (i64 r = r0; r < r1; ++r) acc += to_f(g[r * ld + c]);
+    part[(i64)blockIdx.y * cols + c] = acc;
+}
+__global__ void k_bias_final(const float* part, i64 chunks, i64 cols, float* db) {
+    i64 c = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+    if (c >= cols) return;
+    float acc = 0.f;
+    for (i64 k = 0; k < chunks; ++k) acc += part[k * cols + c];
+    db[c] += acc;
+}
+size_t bias_grad_workspace(i64 rows, i64 cols) { return (size_t)((rows + kBiasChunk - 1) / kBiasChunk) * cols * 4; }
+void bias_grad(const void* g, DT tg, i64 ld, i64 rows, i64 cols, float* db, float* ws, cudaStream_t s) {
+    i64 chunks = (rows + kBiasChunk - 1) / kBiasChunk;
+    dim3 grid((unsigned)((cols + 127) / 128), (unsigned)chunks);
+    dispatch(tg, [&](auto* p) {
+        using T = std::remove_pointer_t<decltype(p)>;
+        k_bias_partial<T><<<grid, 128, 0, s>>>((const T*)g, ld, rows, cols, ws);
+    });
+    k_bias_final<<<(unsigned)((cols + 255) / 256), 256, 0, s>>>(ws, chunks, cols, db);
+    SBK_CHECK_LAUNCH();
+}
+
+}  // namespace sbk

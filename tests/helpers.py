@@ -1,0 +1,45 @@
+"""Shared test helpers: the parity metric and oracle/executor runners."""
+import numpy as np
+
+from oracle import ref
+
+
+def rel_err(got, want):
+    """Per-tensor normalised max error ||a-b||_inf / ||b||_inf."""
+    got = np.asarray(got, dtype=np.float64).ravel()
+    want = np.asarray(want, dtype=np.float64).ravel()
+    assert got.shape == want.shape, (got.shape, want.shape)
+    scale = max(np.abs(want).max(initial=0.0), 1e-30)
+    return float(np.abs(got - want).max(initial=0.0) / scale)
+
+
+def rel_l2(got, want):
+    got = np.asarray(got, dtype=np.float64).ravel()
+    want = np.asarray(want, dtype=np.float64).ravel()
+    return float(np.linalg.norm(got - want) / max(np.linalg.norm(want), 1e-30))
+
+
+def group_scale(name, grads):
+    """Analytically-zero tensors (the key-bias gradient, softmax shift invariance)
+    are normalised by their layer's QKV-bias group."""
+    if name.endswith("key.bias"):
+        q = grads.get(name.replace("key.bias", "query.bias"))
+        if q is not None:
+            return max(np.abs(q).max(), 1e-30)
+    return None
+
+
+def compare_grads(got, want, tol, metric=rel_err):
+    worst = (0.0, None)
+    assert set(got) == set(want), (sorted(set(got) ^ set(want)))
+    for k, w in want.items():
+        g = got[k]
+        gs = group_scale(k, want)
+        if gs is not None:
+            e = float(np.abs(np.asarray(g).ravel() - np.asarray(w).ravel()).max() / gs)
+        else:
+            e = metric(g, w)
+        if e > worst[0]:
+            worst = (e, k)
+    assert worst[0] <= tol, f"worst gradient {worst[1]}: {worst[0]:.3e} > {tol}"
+    return worst

@@ -1,0 +1,162 @@
+"""GPU parity: the B200 executor (through the C ABI) against the reference
+executor compiled from /root/reference (oracle/_ref/slapo_ref_driver), on the
+same fixture, seeds, inputs and schedule.
+
+Tolerances (north star): fp32 path 1e-4 relative (per-tensor ||a-b||_inf/||b||_inf
+against the reference's f64 run) on outputs, loss and every gradient; bf16 path
+BF16_TOL below (stated in DESIGN.md). Integer work (dropout masks, shard maps)
+is bit-exact.
+"""
+import numpy as np
+import pytest
+
+import paper_2302_08005_b200 as sb
+from paper_2302_08005_b200 import recipes
+from oracle import ref
+from tests.helpers import compare_grads, rel_err, rel_l2
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not ref.available(), reason="oracle not built")]
+
+FP32_TOL = 1e-4
+BF16_OUT_TOL = 3e-2   # relL2 of outputs vs f64 (SURVEY.md A.5 calibration, 2 layers)
+BF16_GRAD_TOL = 8e-2  # relL2 per gradient tensor
+
+TOY = dict(layers=2, hidden=32, heads=4, vocab=32, batch=2, seq=8, p=0.1)
+
+
+def build(cfg, script, world, dtype_model="f64"):
+    m = sb.toy_bert(cfg["layers"], cfg["hidden"], cfg["heads"], cfg["vocab"], cfg["batch"], cfg["seq"], cfg["p"])
+    if dtype_model == "f32":
+        m.to_f32()
+    s = sb.create_schedule(m, world)
+    if script:
+        s.load_script(script)
+    return m, s.apply()
+
+
+def run_both(cfg, script, world, mode="train", dtype="fp32", fused=True, seed=123, input_seed=9):
+    m, applied = build(cfg, script, world)
+    inputs = m.random_inputs(input_seed)
+    ex = sb.Executor(applied, mode, seed, world, dtype=dtype, fused=fused)
+    ex.forward(inputs)
+    outs = [ex.outputs_of_rank(r) for r in range(world)]
+    grads = ex.backward_all_ranks()
+    r = ref.run("toy_bert", schedule=script or None, world=world, mode=mode, seed=seed, input_seed=input_seed, **cfg)
+    return ex, outs, grads, r
+
+
+def check(outs, grads, r, world, tol_out, tol_grad, metric=rel_err):
+    for rank in range(world):
+        want = r.outputs(rank)
+        assert len(want) == len(outs[rank])
+        for g, w in zip(outs[rank], want):
+            e = metric(g, w)
+            assert e <= tol_out, f"rank {rank} output err {e:.3e}"
+        loss_g, loss_w = sum(o.sum() for o in outs[rank]), sum(w.sum() for w in want)
+        assert abs(loss_g - loss_w) <= tol_out * max(1.0, abs(loss_w)) * 10, (loss_g, loss_w)
+        compare_grads(grads[rank].params, r.grads(rank), tol_grad, metric)
+
+
+@pytest.mark.parametrize("mode", ["train", "verify"])
+def test_c1_unscheduled_fp32(mode):
+    _, outs, grads, r = run_both(TOY, "", 1, mode=mode)
+    check(outs, grads, r, 1, FP32_TOL, FP32_TOL)
+
+
+def test_c2_fused_flash_checkpoint_fp32():
+    script = recipes.c2_script(2, checkpoint_layers=[1])
+    _, outs, grads, r = run_both(TOY, script, 1)
+    check(outs, grads, r, 1, FP32_TOL, FP32_TOL)
+
+
+def test_c2_opbyop_equals_fused_lowering():
+    script = recipes.c2_script(2, checkpoint_layers=[1])
+    _, o1, g1, r = run_both(TOY, script, 1, fused=False)
+    check(o1, g1, r, 1, FP32_TOL, FP32_TOL)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_tp_recipe_fp32(world):
+    script = recipes.tp_script(2, world, ckpt_ratio=0.5)
+    ex, outs, grads, r = run_both(TOY, script, world)
+    check(outs, grads, r, world, FP32_TOL, FP32_TOL)
+    # collective count mirrors the reference (incl. checkpoint recompute, A.14)
+    assert ex.collective_invocations() == r.meta["collectives_total"]
+
+
+def test_tp8_fp32():
+    cfg = dict(TOY, hidden=64, heads=8, vocab=64)
+    script = recipes.tp_script(2, 8)
+    _, outs, grads, r = run_both(cfg, script, 8)
+    check(outs, grads, r, 8, FP32_TOL, FP32_TOL)
+
+
+def test_bf16_path_within_stated_tolerance():
+    script = recipes.c2_script(2)
+    _, outs, grads, r = run_both(TOY, script, 1, dtype="bf16")
+    check(outs, grads, r, 1, BF16_OUT_TOL, BF16_GRAD_TOL, metric=rel_l2)
+
+
+def test_c1_full_size_fp32():
+    cfg = dict(layers=2, hidden=256, heads=4, vocab=32, batch=8, seq=128, p=0.1)
+    _, outs, grads, r = run_both(cfg, recipes.c2_script(2), 1)
+    check(outs, grads, r, 1, FP32_TOL, FP32_TOL)
+
+
+def test_dropout_mask_bit_exact():
+    import ctypes
+    import torch
+    n = 4099
+    for exec_seed, node_seed, p in [(123, 1040, 0.1), (7, 2028, 0.5), (0, 9, 0.9)]:
+        bits = torch.zeros((n + 31) // 32, dtype=torch.int32, device="cuda")
+        rc = sb.lib().sb_dropout_mask(ctypes.c_void_p(bits.data_ptr()), n, exec_seed, node_seed, p, None)
+        assert rc == 0
+        torch.cuda.synchronize()
+        b = bits.cpu().numpy().view(np.uint32)
+        got = np.array([(b[i // 32] >> (i % 32)) & 1 for i in range(n)], dtype=bool)
+        from oracle import slapo_oracle as so
+        s = so.hash_combine(exec_seed, node_seed)
+        want = ref.uniform01_probe(s, n) >= p
+        assert np.array_equal(got, want)
+
+
+def test_fig3c_partials_and_sync():
+    m = sb.fig3c_exact()
+    x = [np.array([[1.0, 2.0]])]
+    s = sb.create_schedule(m, 2)
+    s.at("wa").shard(["weight"], 0)
+    s.at("wb").shard(["weight"], 1)
+    ex = sb.Executor(s.apply(), "verify", 0, 2)
+    ex.forward(x)
+    assert ex.outputs_of_rank(0)[0].ravel().tolist() == [1, 2]
+    assert ex.outputs_of_rank(1)[0].ravel().tolist() == [0, 0]
+    s.at("wb").sync("forward")
+    ex = sb.Executor(s.apply(), "verify", 0, 2)
+    ex.forward(x)
+    assert ex.outputs_of_rank(0)[0].ravel().tolist() == [1, 2]
+    assert ex.outputs_of_rank(1)[0].ravel().tolist() == [1, 2]
+    assert ex.collective_invocations() == 1
+
+
+def test_ledger_matches_reference():
+    for script in ["", recipes.c2_script(2, checkpoint_layers=[1])]:
+        m, applied = build(TOY, script, 1)
+        ex = sb.Executor(applied, "train", 123, 1)
+        ex.forward(m.random_inputs(9))
+        r = ref.run("toy_bert", schedule=script or None, world=1, backward=0, **TOY)
+        assert ex.ledger() == r.meta["ledger_bytes"]
+
+
+def test_determinism_bitwise():
+    m, applied = build(TOY, recipes.c2_script(2), 1)
+    x = m.random_inputs(9)
+    res = []
+    for _ in range(2):
+        ex = sb.Executor(applied, "train", 123, 1)
+        o = ex.forward(x)
+        g = ex.backward()
+        res.append((o, g))
+    for a, b in zip(res[0][0], res[1][0]):
+        assert a.tobytes() == b.tobytes()
+    for k in res[0][1].params:
+        assert res[0][1].params[k].tobytes() == res[1][1].params[k].tobytes(), k
