@@ -150,7 +150,12 @@ public:
         std::set<int> s;
         auto add = [&](int v) { s.insert(P.views[(size_t)v].gst); };
         switch (op.k) {
-            case K::Embedding: add(op.in[1]); break;
+            case K::Embedding:
+                // the id input receives a (zero) gradient too (executor.cpp:1216-1217),
+                // which is what lets a SyncGrad on it run (and count) in backward
+                add(op.in[0]);
+                add(op.in[1]);
+                break;
             case K::AllReduce:
                 if (op.allreduce) add(op.in[0]);
                 break;
@@ -288,7 +293,10 @@ public:
         off += r.tmp_bytes;
         r.total = off;
         CK(cudaMalloc(&r.base, r.total));
-        CK(cudaMemset(r.base, 0, r.total));
+        // on our (non-blocking) stream: a legacy-stream memset would race the
+        // parameter uploads enqueued below
+        CK(cudaMemsetAsync(r.base, 0, r.total, stream));
+        CK(cudaStreamSynchronize(stream));
         r.fptr.assign(P.st.size(), nullptr);
         r.gptr.assign(P.st.size(), nullptr);
         for (size_t i = 0; i < P.st.size(); ++i) {
@@ -323,7 +331,9 @@ public:
         auto& s = r.P.st[(size_t)st];
         double* d = nullptr;
         CK(cudaMalloc(&d, data.size() * sizeof(double)));
-        CK(cudaMemcpy(d, data.data(), data.size() * sizeof(double), cudaMemcpyHostToDevice));
+        // same stream as the cast: a legacy-stream pageable cudaMemcpy may return
+        // before its DMA lands, which a non-blocking stream would not wait for
+        CK(cudaMemcpyAsync(d, data.data(), data.size() * sizeof(double), cudaMemcpyHostToDevice, stream));
         sbk::cast(d, sbk::F64, r.fptr[(size_t)st], s.dt, (i64)data.size(), stream);
         CK(cudaStreamSynchronize(stream));
         CK(cudaFree(d));
