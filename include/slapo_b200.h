@@ -106,6 +106,13 @@ int sb_executor_upload_inputs(sb_executor* e, const double* const* inputs, int n
 int sb_executor_step(sb_executor* e, int use_graph);
 int sb_executor_step_loss(sb_executor* e, int use_graph, float* loss_host);
 int sb_executor_synchronize(sb_executor* e);
+/* device time (CUDA events on the executor stream) of `steps` back-to-back steps */
+int sb_executor_time_steps(sb_executor* e, int steps, int use_graph, float* ms);
+/* end-to-end: per step H2D of the host inputs, fwd+bwd, D2H of the loss (sum of outputs) */
+int sb_executor_time_e2e(sb_executor* e, int steps, const double* const* inputs, int n_inputs, int use_graph,
+                         float* ms, float* loss);
+/* kernel nodes in the captured fwd+bwd CUDA graph (after a graph step) */
+int sb_executor_kernels_per_step(sb_executor* e, int* n);
 int sb_executor_stream(sb_executor* e, void** stream);
 int sb_executor_describe(sb_executor* e, char* buf, size_t cap);
 int sb_executor_profile(sb_executor* e, char* buf, size_t cap); /* per-op-kind ms of one step, JSON */
@@ -119,6 +126,8 @@ int sb_gemm(const void* A, int ta, int64_t sAb, int64_t sAm, int64_t sAk, const 
             int64_t N, int64_t K, float alpha, int accumulate, const void* bias, int epilogue, void* aux, void* stream);
 int sb_gemm_engine(void);                /* engine of the last sb_gemm: 0 SIMT, 1 tcgen05 */
 int sb_gemm_force_simt(int on);
+/* scratch the tcgen05 path may use for deterministic split-K (wgrad) */
+int sb_gemm_set_workspace(void* ws, size_t bytes);
 /* dropout keep mask (apply_dropout, proj/src/executor.cpp:793-806): bit i of word i/32 =
  * uniform01(hash_combine(exec_seed, node_seed), 0xd0, i) >= p */
 int sb_dropout_mask(uint32_t* bits, int64_t n, uint64_t exec_seed, uint64_t node_seed, double p, void* stream);

@@ -103,6 +103,10 @@ for _n, _a in {
     "sb_executor_describe": (_P, _c.c_char_p, _c.c_size_t),
     "sb_executor_profile": (_P, _c.c_char_p, _c.c_size_t),
     "sb_executor_device_bytes": (_P, _c.POINTER(_i64)),
+    "sb_executor_time_steps": (_P, _c.c_int, _c.c_int, _c.POINTER(_c.c_float)),
+    "sb_executor_kernels_per_step": (_P, _c.POINTER(_c.c_int)),
+    "sb_executor_time_e2e": (_P, _c.c_int, _c.POINTER(_dp), _c.c_int, _c.c_int, _c.POINTER(_c.c_float),
+                             _c.POINTER(_c.c_float)),
     "sb_gemm_force_simt": (_c.c_int,),
     "sb_dropout_mask": (_P, _i64, _u64, _u64, _c.c_double, _P),
 }.items():
@@ -431,6 +435,29 @@ class Executor:
 
     def synchronize(self) -> None:
         _check(_lib.sb_executor_synchronize(self._h))
+
+    def time_steps(self, steps: int, use_graph: bool = True) -> float:
+        """Device milliseconds of `steps` back-to-back fwd+bwd steps (CUDA events)."""
+        v = _c.c_float()
+        _check(_lib.sb_executor_time_steps(self._h, steps, int(use_graph), _c.byref(v)))
+        return v.value
+
+    def time_e2e(self, steps: int, inputs: Sequence[np.ndarray], use_graph: bool = True):
+        """(device ms, last loss) of `steps` end-to-end steps: H2D of `inputs`
+        (pass pinned host arrays for async DMA), fwd+bwd, D2H of the loss."""
+        arrs = [np.asarray(x) for x in inputs]
+        for a in arrs:
+            assert a.dtype == np.float64 and a.flags["C_CONTIGUOUS"]
+        ptrs = (_dp * len(arrs))(*[a.ctypes.data_as(_dp) for a in arrs])
+        ms, loss = _c.c_float(), _c.c_float()
+        _check(_lib.sb_executor_time_e2e(self._h, steps, ptrs, len(arrs), int(use_graph), _c.byref(ms),
+                                         _c.byref(loss)))
+        return ms.value, loss.value
+
+    def kernels_per_step(self) -> int:
+        v = _c.c_int()
+        _check(_lib.sb_executor_kernels_per_step(self._h, _c.byref(v)))
+        return v.value
 
     def stream(self) -> int:
         s = _P()

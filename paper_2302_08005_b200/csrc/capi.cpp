@@ -358,6 +358,16 @@ int sb_executor_step_loss(sb_executor* e, int use_graph, float* loss_host) {
         e->ex->synchronize();
     });
 }
+int sb_executor_time_steps(sb_executor* e, int steps, int use_graph, float* ms) {
+    return guard([&] { *ms = e->ex->time_steps(steps, use_graph != 0); });
+}
+int sb_executor_time_e2e(sb_executor* e, int steps, const double* const* inputs, int n_inputs, int use_graph,
+                         float* ms, float* loss) {
+    return guard([&] { *ms = e->ex->time_e2e(steps, inputs, n_inputs, use_graph != 0, loss); });
+}
+int sb_executor_kernels_per_step(sb_executor* e, int* n) {
+    return guard([&] { *n = e->ex->kernel_launches_per_step(); });
+}
 int sb_executor_synchronize(sb_executor* e) {
     return guard([&] { e->ex->synchronize(); });
 }
@@ -388,6 +398,8 @@ int sb_executor_device_bytes(sb_executor* e, int64_t* b) {
 }
 
 // ------------------------------------------------------------------ kernels
+static void* g_gemm_ws = nullptr;
+static size_t g_gemm_ws_bytes = 0;
 static sbk::DT kdt(int d) {
     if (d < 0 || d > 2) throw Error("dtype code must be 0, 1 or 2");
     return (sbk::DT)d;
@@ -422,10 +434,17 @@ int sb_gemm(const void* A, int ta, int64_t sAb, int64_t sAm, int64_t sAk, const 
         g.tbias = g.tc == sbk::F32 ? g.ta : g.tc;
         g.epilogue = epilogue;
         g.aux = aux;
+        g.ws = g_gemm_ws;
+        g.ws_bytes = g_gemm_ws_bytes;
         sbk::gemm(g, (cudaStream_t)stream);
     });
 }
 int sb_gemm_engine(void) { return sbk::gemm_last_engine(); }
+int sb_gemm_set_workspace(void* ws, size_t bytes) {
+    g_gemm_ws = ws;
+    g_gemm_ws_bytes = bytes;
+    return 0;
+}
 int sb_gemm_force_simt(int on) {
     sbk::gemm_force_simt(on != 0);
     return 0;

@@ -217,13 +217,16 @@ public:
                 case K::LayerNorm:
                     ws = std::max(ws, sbk::layernorm_bwd_workspace(rows_of(op.in[0]), P.views[(size_t)op.in[0]].shape.back()));
                     break;
-                case K::FusedLinearResLN:
-                    ws = std::max(ws, sbk::bdrln_bwd_workspace(rows_of(op.out[0]), P.views[(size_t)op.out[0]].shape.back()));
-                    break;
                 case K::Linear:
                 case K::FusedLinearGelu:
+                case K::FusedLinearResLN: {
+                    const View& w = P.views[(size_t)op.in[1]];
                     ws = std::max(ws, sbk::bias_grad_workspace(rows_of(op.out[0]), P.views[(size_t)op.out[0]].shape.back()));
+                    ws = std::max(ws, sbk::gemm_splitk_workspace(w.shape[0], w.shape[1]));
+                    if (op.k == K::FusedLinearResLN)
+                        ws = std::max(ws, sbk::bdrln_bwd_workspace(rows_of(op.out[0]), P.views[(size_t)op.out[0]].shape.back()));
                     break;
+                }
                 case K::FlashAttn: ws = std::max(ws, (size_t)P.views[(size_t)op.out[1]].numel() * 4); break;
                 case K::Embedding: ws = std::max(ws, sbk::embedding_bwd_workspace(P.views[(size_t)op.in[0]].numel())); break;
                 case K::AllGather:
@@ -375,6 +378,19 @@ public:
         sbk::accumulate(t.p, cdt, gp(r, t.view), gdt(r, t.view), V(r, t.view).numel(), 1.f, stream);
     }
 
+    // every GEMM of the step goes through here: profiling tags them "gemm" and
+    // counts their flops (the roofline of the dominant kernel in bench.py)
+    double gemm_flops = 0;
+    void run_gemm(const sbk::Gemm& g) {
+        if (profiling) {
+            prof_begin("gemm");
+            gemm_flops += 2.0 * (double)g.M * (double)g.N * (double)g.K * (double)g.batch;
+        }
+        sbk::gemm(g, stream);
+        if (profiling) prof_end();
+        ++launches;
+    }
+
     void gemm_rowwise(RankCtx& r, const void* A, i64 lda, bool a_t, const void* B, i64 ldb, bool b_t, void* C, i64 ldc,
                       DT tc, i64 M, i64 N, i64 K, bool acc, const void* bias, int epi = 0, void* aux = nullptr) {
         // A(m,k): a_t ? A[k*lda + m] : A[m*lda + k];  B(k,n): b_t ? B[n*ldb + k] : B[k*ldb + n]
@@ -399,8 +415,9 @@ public:
         g.tbias = cdt;
         g.epilogue = epi;
         g.aux = aux;
-        sbk::gemm(g, stream);
-        (void)r;
+        g.ws = r.ws;
+        g.ws_bytes = r.ws_bytes;
+        run_gemm(g);
     }
 
     // ------------------------------------------------------- collectives
@@ -591,7 +608,7 @@ public:
                 g.M = m;
                 g.N = n;
                 g.K = k;
-                sbk::gemm(g, stream);
+                run_gemm(g);
                 break;
             }
             case K::Permute: {
@@ -865,7 +882,7 @@ public:
                 g.N = k;
                 g.K = n;
                 g.accumulate = true;
-                sbk::gemm(g, stream);
+                run_gemm(g);
                 flush(r, ga);
                 GT gb = gtarget(r, op.in[1]);
                 sbk::Gemm h;
@@ -888,7 +905,7 @@ public:
                 h.N = n;
                 h.K = m;
                 h.accumulate = true;
-                sbk::gemm(h, stream);
+                run_gemm(h);
                 flush(r, gb);
                 ++launches;
                 break;
@@ -1019,14 +1036,19 @@ public:
     }
 
     // ---------------------------------------------------------- profile
+    std::vector<size_t> prof_open;
     void prof_begin(const std::string& name) {
         cudaEvent_t a, b;
         cudaEventCreate(&a);
         cudaEventCreate(&b);
         cudaEventRecord(a, stream);
+        prof_open.push_back(prof.size());
         prof.push_back({name, {a, b}});
     }
-    void prof_end() { cudaEventRecord(prof.back().second.second, stream); }
+    void prof_end() {
+        cudaEventRecord(prof[prof_open.back()].second.second, stream);
+        prof_open.pop_back();
+    }
 };
 
 // ====================================================================== API
@@ -1182,10 +1204,81 @@ void Executor::launch_graph() {
     CK(cudaGraphLaunch(I.gexec, I.stream));
 }
 int Executor::kernel_launches_per_step() const {
+    // exact: the kernel nodes of the captured fwd+bwd graph
     auto& I = *impl_;
-    int before = I.launches;
-    (void)before;
-    return I.launches;
+    if (!I.graph) return -1;
+    size_t n = 0;
+    CK(cudaGraphGetNodes(I.graph, nullptr, &n));
+    std::vector<cudaGraphNode_t> nodes(n);
+    CK(cudaGraphGetNodes(I.graph, nodes.data(), &n));
+    int k = 0;
+    for (auto nd : nodes) {
+        cudaGraphNodeType t;
+        CK(cudaGraphNodeGetType(nd, &t));
+        k += t == cudaGraphNodeTypeKernel;
+    }
+    return k;
+}
+// End-to-end steps through the public API: every step copies its inputs from
+// host memory (pinned by the caller for async DMA), runs fwd+bwd and reads the
+// loss (sum of outputs) back to the host.
+float Executor::time_e2e(int steps, const double* const* inputs, int n, bool use_graph, float* last_loss) {
+    auto& I = *impl_;
+    float* dloss = nullptr;
+    float* hloss = nullptr;
+    CK(cudaMalloc(&dloss, 4));
+    CK(cudaMallocHost(&hloss, 4));
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    CK(cudaStreamSynchronize(I.stream));
+    CK(cudaEventRecord(a, I.stream));
+    for (int i = 0; i < steps; ++i) {
+        upload_inputs_raw(inputs, n);
+        if (use_graph) {
+            launch_graph();
+        } else {
+            I.run_forward();
+            I.run_backward();
+        }
+        enqueue_loss(dloss);
+        CK(cudaMemcpyAsync(hloss, dloss, 4, cudaMemcpyDeviceToHost, I.stream));
+        CK(cudaStreamSynchronize(I.stream));
+    }
+    CK(cudaEventRecord(b, I.stream));
+    CK(cudaEventSynchronize(b));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, a, b));
+    if (last_loss) *last_loss = *hloss;
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(dloss);
+    cudaFreeHost(hloss);
+    return ms;
+}
+
+float Executor::time_steps(int steps, bool use_graph) {
+    auto& I = *impl_;
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    CK(cudaStreamSynchronize(I.stream));
+    CK(cudaEventRecord(a, I.stream));
+    for (int i = 0; i < steps; ++i) {
+        if (use_graph) {
+            launch_graph();
+        } else {
+            I.run_forward();
+            I.run_backward();
+        }
+    }
+    CK(cudaEventRecord(b, I.stream));
+    CK(cudaEventSynchronize(b));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    return ms;
 }
 size_t Executor::device_bytes() const {
     size_t t = 0;
@@ -1213,11 +1306,23 @@ std::vector<std::pair<std::string, float>> Executor::profile_step() {
     auto& I = *impl_;
     I.profiling = true;
     I.prof.clear();
+    I.gemm_flops = 0;
+    cudaEvent_t s0, s1;
+    cudaEventCreate(&s0);
+    cudaEventCreate(&s1);
+    cudaEventRecord(s0, I.stream);
     I.run_forward();
     I.run_backward();
+    cudaEventRecord(s1, I.stream);
     I.profiling = false;
     synchronize();
     std::map<std::string, float> acc;
+    float total = 0;
+    cudaEventElapsedTime(&total, s0, s1);
+    cudaEventDestroy(s0);
+    cudaEventDestroy(s1);
+    acc["@step_ms"] = total;
+    acc["@gemm_gflop"] = (float)(I.gemm_flops * 1e-9);
     for (auto& [name, ev] : I.prof) {
         float ms = 0;
         cudaEventElapsedTime(&ms, ev.first, ev.second);

@@ -60,7 +60,9 @@ public:
     void launch_graph();
     void synchronize();
     void* stream() const;
-    int kernel_launches_per_step() const;
+    int kernel_launches_per_step() const;  // kernel nodes of the captured step graph
+    float time_steps(int steps, bool use_graph);  // device ms of `steps` fwd+bwd, CUDA events on our stream
+    float time_e2e(int steps, const double* const* inputs, int n, bool use_graph, float* last_loss);
     std::string describe() const;  // plan summary (ops, bytes)
     size_t device_bytes() const;
     void* input_device_ptr(int idx) const;

@@ -36,12 +36,19 @@ struct Gemm {
     DT tbias = F32;
     int epilogue = 0;
     void* aux = nullptr;  // pre-activation (same layout as C) when epilogue == gelu
+    void* ws = nullptr;   // scratch for deterministic split-K partials (optional)
+    size_t ws_bytes = 0;
 };
 void gemm(const Gemm& g, cudaStream_t s);
 // Which engine the last gemm() call used: 0 SIMT, 1 tcgen05 (for tests/bench).
 int gemm_last_engine();
 // Force the SIMT engine (tests compare the tcgen05 kernel against it).
 void gemm_force_simt(bool on);
+// workspace the tcgen05 split-K path may use for an (M x N) fp32 output
+inline size_t gemm_splitk_workspace(i64 M, i64 N) {
+    size_t w = (size_t)16 * M * N * 4, cap = (size_t)48 << 20;
+    return w < cap ? w : cap;
+}
 
 // ----------------------------------------------------------- elementwise
 void fill(void* x, DT t, i64 n, float v, cudaStream_t s);

