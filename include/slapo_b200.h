@@ -139,14 +139,16 @@ int sb_bias_dropout_residual_ln_fwd(const void* partial, const void* bias, const
                                     const void* beta, void* sum, void* y, float* mean, float* rstd, int dtype,
                                     int64_t rows, int64_t n, float eps, uint64_t exec_seed, uint64_t node_seed,
                                     double p, void* stream);
-/* EfficientAttention forward/backward (library.cpp:9-34 semantics) */
+/* EfficientAttention forward/backward (library.cpp:9-34 semantics). keep_bits: the
+ * sb_dropout_mask bits of the (B, nh, S, S) probabilities (required by the
+ * tensor-core kernels when p > 0; NULL makes the portable kernel hash in place). */
 int sb_attn_fwd(const void* q, const void* k, const void* v, void* o, int64_t ld_qkv, int64_t ld_o, float* lse,
                 int64_t B, int64_t S, int64_t nh, int64_t hd, float scale, uint64_t exec_seed, uint64_t node_seed,
-                double p, int dtype, void* stream);
+                double p, int dtype, const uint32_t* keep_bits, void* stream);
 int sb_attn_bwd(const void* q, const void* k, const void* v, const void* o, int64_t ld_qkv, int64_t ld_o,
                 const float* lse, const void* dout, void* dq, void* dk, void* dv, float* delta, int64_t B, int64_t S,
                 int64_t nh, int64_t hd, float scale, uint64_t exec_seed, uint64_t node_seed, double p, int dtype,
-                void* stream);
+                const uint32_t* keep_bits, void* stream);
 
 #ifdef __cplusplus
 }

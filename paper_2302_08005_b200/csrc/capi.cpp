@@ -494,16 +494,20 @@ static sbk::Attn mk_attn(const void* q, const void* k, const void* v, void* o, i
     return a;
 }
 int sb_attn_fwd(const void* q, const void* k, const void* v, void* o, int64_t ld_qkv, int64_t ld_o, float* lse, int64_t B,
-                int64_t S, int64_t nh, int64_t hd, float scale, uint64_t es, uint64_t ns, double p, int dtype, void* stream) {
+                int64_t S, int64_t nh, int64_t hd, float scale, uint64_t es, uint64_t ns, double p, int dtype,
+                const uint32_t* keep_bits, void* stream) {
     return guard([&] {
-        sbk::attn_fwd(mk_attn(q, k, v, o, ld_qkv, ld_o, lse, B, S, nh, hd, scale, es, ns, p, dtype), (cudaStream_t)stream);
+        sbk::Attn a = mk_attn(q, k, v, o, ld_qkv, ld_o, lse, B, S, nh, hd, scale, es, ns, p, dtype);
+        a.mask = keep_bits;
+        sbk::attn_fwd(a, (cudaStream_t)stream);
     });
 }
 int sb_attn_bwd(const void* q, const void* k, const void* v, const void* o, int64_t ld_qkv, int64_t ld_o, const float* lse,
                 const void* dout, void* dq, void* dk, void* dv, float* delta, int64_t B, int64_t S, int64_t nh, int64_t hd,
-                float scale, uint64_t es, uint64_t ns, double p, int dtype, void* stream) {
+                float scale, uint64_t es, uint64_t ns, double p, int dtype, const uint32_t* keep_bits, void* stream) {
     return guard([&] {
         sbk::Attn a = mk_attn(q, k, v, (void*)o, ld_qkv, ld_o, (float*)lse, B, S, nh, hd, scale, es, ns, p, dtype);
+        a.mask = keep_bits;
         sbk::attn_bwd(a, dout, ld_o, dq, dk, dv, ld_qkv, ld_qkv, ld_qkv, delta, (cudaStream_t)stream);
     });
 }

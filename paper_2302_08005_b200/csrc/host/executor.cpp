@@ -658,7 +658,13 @@ public:
                                    op.full_rows, op.row0, w.shape[0], fp(r, op.out[0]), stream);
                 break;
             }
-            case K::FlashAttn: sbk::attn_fwd(attn_args(r, op), stream); break;
+            case K::FlashAttn: {
+                sbk::Attn a = attn_args(r, op);
+                if (op.dropout)  // keep bits once per forward (and per recompute); backward re-reads them
+                    sbk::dropout_mask((uint32_t*)fp(r, op.out[2]), a.B * a.nh * a.S * a.S, op.s1, op.thr, stream);
+                sbk::attn_fwd(a, stream);
+                break;
+            }
             default: throw Error(std::string("internal: no forward launcher for ") + k_str(op.k));
         }
     }
@@ -685,6 +691,7 @@ public:
         a.thr = op.dropout ? op.thr : 0;
         a.dscale = (float)(1.0 / (1.0 - op.p));
         a.t = cdt;
+        a.mask = op.dropout ? (const uint32_t*)fp(r, op.out[2]) : nullptr;
         return a;
     }
 

@@ -442,6 +442,7 @@ struct Lowerer {
         op.k = K::FlashAttn;
         op.in = {q, k, v};
         op.out = {out, aux(B * nh * S)};
+        if (o.train && p > 0.0) op.out.push_back(aux((B * nh * S * S + 31) / 32));  // 1-bit keep mask
         op.hd = hd;
         op.nh = nh;
         op.scale = scale;

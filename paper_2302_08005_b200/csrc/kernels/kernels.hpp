@@ -149,6 +149,7 @@ struct Attn {
     u64 s1 = 0, thr = 0;
     float dscale = 1.f;
     DT t;
+    const uint32_t* mask = nullptr;  // precomputed keep bits (dropout_mask); required by the tensor-core path
 };
 void attn_fwd(const Attn& a, cudaStream_t s);
 // dq/dk/dv accumulate (+=) with their own row strides; `delta` scratch (B,nh,S) fp32.

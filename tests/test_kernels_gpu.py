@@ -102,3 +102,54 @@ def test_tc_matches_simt_engine():
     finally:
         L.sb_gemm_force_simt(0)
     assert (y1 - y2).abs().max().item() < 1e-3 * y2.abs().max().item()
+
+
+# ------------------------------------------------------------------ attention
+L.sb_attn_fwd.argtypes = [ctypes.c_void_p] * 4 + [ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p] + \
+    [ctypes.c_int64] * 4 + [ctypes.c_float, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_double, ctypes.c_int,
+                            ctypes.c_void_p, ctypes.c_void_p]
+L.sb_attn_bwd.argtypes = [ctypes.c_void_p] * 4 + [ctypes.c_int64, ctypes.c_int64] + [ctypes.c_void_p] * 6 + \
+    [ctypes.c_int64] * 4 + [ctypes.c_float, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_double, ctypes.c_int,
+                            ctypes.c_void_p, ctypes.c_void_p]
+L.sb_dropout_mask.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_double,
+                              ctypes.c_void_p]
+
+
+@pytest.mark.parametrize("B,S,nh,hd,p", [(2, 128, 4, 64, 0.0), (2, 256, 2, 64, 0.1), (1, 128, 2, 128, 0.1)])
+def test_flash_attention_tensor_core(B, S, nh, hd, p):
+    H = nh * hd
+    torch.manual_seed(0)
+    qkv = (torch.randn(B, S, 3 * H, device="cuda") * 0.5).bfloat16()  # FusedQKV layout, consumed in place
+    q, k, v = qkv[..., :H], qkv[..., H:2 * H], qkv[..., 2 * H:]
+    o = torch.zeros(B, S, H, device="cuda", dtype=torch.bfloat16)
+    lse = torch.zeros(B * nh * S, device="cuda")
+    n = B * nh * S * S
+    bits = torch.zeros((n + 31) // 32, dtype=torch.int32, device="cuda")
+    es, ns = 123, 1040
+    if p > 0:
+        assert L.sb_dropout_mask(P(bits), n, es, ns, p, None) == 0
+    scale = hd ** -0.5
+    rc = L.sb_attn_fwd(P(q), P(k), P(v), P(o), 3 * H, H, P(lse), B, S, nh, hd, scale, es, ns, p, 1,
+                       P(bits) if p > 0 else None, None)
+    assert rc == 0, L.sb_last_error()
+    torch.cuda.synchronize()
+    # torch fp32 reference of the same math
+    qf, kf, vf = (t.float().reshape(B, S, nh, hd).transpose(1, 2).requires_grad_() for t in (q, k, v))
+    pr = torch.softmax(qf @ kf.transpose(-1, -2) * scale, dim=-1)
+    if p > 0:
+        idx = torch.arange(n, device="cuda")
+        keep = ((bits.view(torch.int32)[idx // 32] >> (idx % 32)) & 1).bool().reshape(B, nh, S, S)
+        pr = torch.where(keep, pr / (1 - p), torch.zeros_like(pr))
+    ref = (pr @ vf).transpose(1, 2).reshape(B, S, H)
+    close(o, ref)
+    # backward
+    do = (torch.randn(B, S, H, device="cuda") * 0.5).bfloat16()
+    ref.backward(do.float())
+    g = torch.zeros_like(qkv)
+    delta = torch.zeros(B * nh * S, device="cuda")
+    rc = L.sb_attn_bwd(P(q), P(k), P(v), P(o), 3 * H, H, P(lse), P(do), P(g[..., :H]), P(g[..., H:2 * H]),
+                       P(g[..., 2 * H:]), P(delta), B, S, nh, hd, scale, es, ns, p, 1, P(bits) if p > 0 else None, None)
+    assert rc == 0, L.sb_last_error()
+    torch.cuda.synchronize()
+    for got, want in ((g[..., :H], qf.grad), (g[..., H:2 * H], kf.grad), (g[..., 2 * H:], vf.grad)):
+        close(got, want.transpose(1, 2).reshape(B, S, H), 3e-2)
