@@ -123,6 +123,7 @@ public:
         }
         build_backward_steps();
         for (auto& r : ranks) allocate(r);
+        init_mask_stream();
         if (comm.nccl && world > 1) {
             nccl().load();
             ncclUniqueId id;
@@ -141,6 +142,10 @@ public:
             if (r.base) cudaFree(r.base);
         if (nan_flag) cudaFree(nan_flag);
         if (ncomm && nccl().CommDestroy) nccl().CommDestroy(ncomm);
+        for (auto e : mask_ev)
+            if (e) cudaEventDestroy(e);
+        if (fork_ev) cudaEventDestroy(fork_ev);
+        if (mstream) cudaStreamDestroy(mstream);
         if (stream) cudaStreamDestroy(stream);
     }
 
@@ -228,7 +233,10 @@ public:
                     break;
                 }
                 case K::FlashAttn: ws = std::max(ws, (size_t)P.views[(size_t)op.out[1]].numel() * 4); break;
-                case K::Embedding: ws = std::max(ws, sbk::embedding_bwd_workspace(P.views[(size_t)op.in[0]].numel())); break;
+                case K::Embedding:
+                    ws = std::max(ws, sbk::embedding_bwd_workspace(P.views[(size_t)op.in[0]].numel(),
+                                                                   P.views[(size_t)op.in[1]].shape[1]));
+                    break;
                 case K::AllGather:
                     ws = std::max(ws, (size_t)P.views[(size_t)op.out[0]].numel() * (size_t)sbk::dt_bytes(cdt));
                     break;
@@ -658,13 +666,7 @@ public:
                                    op.full_rows, op.row0, w.shape[0], fp(r, op.out[0]), stream);
                 break;
             }
-            case K::FlashAttn: {
-                sbk::Attn a = attn_args(r, op);
-                if (op.dropout)  // keep bits once per forward (and per recompute); backward re-reads them
-                    sbk::dropout_mask((uint32_t*)fp(r, op.out[2]), a.B * a.nh * a.S * a.S, op.s1, op.thr, stream);
-                sbk::attn_fwd(a, stream);
-                break;
-            }
+            case K::FlashAttn: sbk::attn_fwd(attn_args(r, op), stream); break;  // keep bits: launch_masks()
             default: throw Error(std::string("internal: no forward launcher for ") + k_str(op.k));
         }
     }
@@ -1015,8 +1017,56 @@ public:
     }
 
     // ----------------------------------------------------------- steps
+    // Dropout keep bits of every attention op are a pure function of (seed,
+    // node seed, index): they are generated on a low-priority side stream at the
+    // start of the forward, overlapping the GEMMs (whose integer pipes idle),
+    // and each attention op waits only for its own mask.
+    cudaStream_t mstream = nullptr;
+    cudaEvent_t fork_ev = nullptr;
+    std::vector<cudaEvent_t> mask_ev;  // per forward op index (null when none)
+
+    void init_mask_stream() {
+        const Plan& P = ranks[0].P;
+        mask_ev.assign(P.fwd.size(), nullptr);
+        bool any = false;
+        for (size_t i = 0; i < P.fwd.size(); ++i)
+            if (P.fwd[i].k == K::FlashAttn && P.fwd[i].dropout) {
+                CK(cudaEventCreateWithFlags(&mask_ev[i], cudaEventDisableTiming));
+                any = true;
+            }
+        if (!any) return;
+        int lo, hi;
+        CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        CK(cudaStreamCreateWithPriority(&mstream, cudaStreamNonBlocking, lo));  // lo = least priority
+        CK(cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming));
+    }
+
+    void launch_masks() {
+        if (!mstream) return;
+        CK(cudaEventRecord(fork_ev, stream));
+        CK(cudaStreamWaitEvent(mstream, fork_ev, 0));
+        for (size_t i = 0; i < mask_ev.size(); ++i) {
+            if (!mask_ev[i]) continue;
+            for (auto& r : ranks) {
+                const Op& op = r.P.fwd[i];
+                sbk::Attn a = attn_args(r, op);
+                sbk::dropout_mask((uint32_t*)fp(r, op.out[2]), a.B * a.nh * a.S * a.S, op.s1, op.thr, mstream);
+            }
+            CK(cudaEventRecord(mask_ev[i], mstream));
+        }
+    }
+
     void run_forward() {
-        for (size_t i = 0; i < ranks[0].P.fwd.size(); ++i) fwd_op((int)i);
+        launch_masks();
+        cudaEvent_t last = nullptr;
+        for (size_t i = 0; i < ranks[0].P.fwd.size(); ++i) {
+            if (mask_ev.size() > i && mask_ev[i]) {
+                CK(cudaStreamWaitEvent(stream, mask_ev[i], 0));
+                last = mask_ev[i];
+            }
+            fwd_op((int)i);
+        }
+        if (last) CK(cudaStreamWaitEvent(stream, last, 0));  // join (graph capture needs it)
         ran_forward = true;
     }
 

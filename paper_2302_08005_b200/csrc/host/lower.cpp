@@ -442,7 +442,13 @@ struct Lowerer {
         op.k = K::FlashAttn;
         op.in = {q, k, v};
         op.out = {out, aux(B * nh * S)};
-        if (o.train && p > 0.0) op.out.push_back(aux((B * nh * S * S + 31) / 32));  // 1-bit keep mask
+        if (o.train && p > 0.0) {
+            // 1-bit keep mask, persistent even inside a checkpoint region: it is a
+            // pure function of the seeds, so recompute re-reads it
+            int mv = aux((B * nh * S * S + 31) / 32);
+            P.st[(size_t)V(mv).st].region = -1;
+            op.out.push_back(mv);
+        }
         op.hd = hd;
         op.nh = nh;
         op.scale = scale;

@@ -386,73 +386,6 @@ void embedding_fwd(const double* ids, i64 n, const void* table, DT t, i64 dim, i
     });
     SBK_CHECK_LAUNCH();
 }
-// Deterministic scatter-add. k_emb_sort: one block bitonic-sorts the keys
-// (row << 32 | position) of the local hits (non-local ids sort last);
-// k_emb_seg: the block owning a segment head sums that row's positions in
-// ascending order and adds once into the table gradient.
-static i64 pow2_at_least(i64 n) {
-    i64 p = 1;
-    while (p < n) p <<= 1;
-    return p;
-}
-size_t embedding_bwd_workspace(i64 n) { return (size_t)pow2_at_least(std::max<i64>(n, 1)) * 8; }
-__global__ void k_emb_sort(const double* ids, i64 n, i64 N, i64 V, i64 row0, i64 local, unsigned long long* keys) {
-    for (i64 i = threadIdx.x; i < N; i += blockDim.x) {
-        unsigned long long k = ~0ull;
-        if (i < n) {
-            i64 r = d_row(ids[i], V) - row0;
-            if (r >= 0 && r < local) k = ((unsigned long long)r << 32) | (unsigned long long)i;
-        }
-        keys[i] = k;
-    }
-    __syncthreads();
-    for (i64 size = 2; size <= N; size <<= 1) {
-        for (i64 stride = size >> 1; stride > 0; stride >>= 1) {
-            for (i64 i = threadIdx.x; i < N; i += blockDim.x) {
-                i64 j = i ^ stride;
-                if (j > i) {
-                    bool up = (i & size) == 0;
-                    unsigned long long a = keys[i], b = keys[j];
-                    if ((a > b) == up) {
-                        keys[i] = b;
-                        keys[j] = a;
-                    }
-                }
-            }
-            __syncthreads();
-        }
-    }
-}
-template <class T>
-__global__ void k_emb_seg(const unsigned long long* keys, i64 n, const T* g, i64 dim, float* gt) {
-    i64 j = blockIdx.x;
-    unsigned long long k = keys[j];
-    if (k == ~0ull) return;
-    unsigned row = (unsigned)(k >> 32);
-    if (j > 0 && (unsigned)(keys[j - 1] >> 32) == row && keys[j - 1] != ~0ull) return;  // not a head
-    i64 d = blockIdx.y * (i64)blockDim.x + threadIdx.x;
-    if (d >= dim) return;
-    float acc = 0.f;
-    for (i64 m = j; m < n; ++m) {
-        unsigned long long km = keys[m];
-        if (km == ~0ull || (unsigned)(km >> 32) != row) break;
-        acc += to_f(g[(i64)(km & 0xffffffffull) * dim + d]);
-    }
-    gt[(i64)row * dim + d] += acc;
-}
-void embedding_bwd(const double* ids, i64 n, const void* g, DT tg, i64 dim, i64 V, i64 row0, i64 local, float* gt,
-                   void* ws, cudaStream_t s) {
-    i64 N = pow2_at_least(std::max<i64>(n, 1));
-    auto* keys = (unsigned long long*)ws;
-    k_emb_sort<<<1, 1024, 0, s>>>(ids, n, N, V, row0, local, keys);
-    dim3 grid((unsigned)n, (unsigned)((dim + 255) / 256));
-    dispatch(tg, [&](auto* p) {
-        using T = std::remove_pointer_t<decltype(p)>;
-        k_emb_seg<T><<<grid, 256, 0, s>>>(keys, n, (const T*)g, dim, gt);
-    });
-    SBK_CHECK_LAUNCH();
-}
-
 // ------------------------------------------------------------------ bias grad
 // db[c] += sum_r g[r*ld + c]: fixed row chunks -> partials -> ordered sum.
 constexpr int kBiasChunk = 256;

@@ -125,7 +125,7 @@ void embedding_fwd(const double* ids, i64 n_ids, const void* table, DT t, i64 di
 // positions are summed in ascending order by one owner (no float atomics).
 void embedding_bwd(const double* ids, i64 n_ids, const void* g, DT tg, i64 dim, i64 full_rows, i64 row0,
                    i64 local_rows, float* gtable, void* workspace, cudaStream_t s);
-size_t embedding_bwd_workspace(i64 n_ids);
+size_t embedding_bwd_workspace(i64 n_ids, i64 dim);
 
 // ---------------------------------------------- simulated collectives
 // dst_r = sum_{r'} src_{r'} in rank-ascending order (fp32 accumulation), for

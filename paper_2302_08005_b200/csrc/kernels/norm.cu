@@ -13,6 +13,17 @@ constexpr int kWarps = 8;           // rows in flight per block
 constexpr int kRowBlocks = 296;     // fixed grid for the backward column partials
 }  // namespace
 
+// vectorised register-resident variants (norm_vec.cu); false = shape not covered
+bool ln_fwd_vec(const void* x, const void* gamma, const void* beta, void* y, float* mean, float* rstd, DT t, i64 rows,
+                i64 n, float eps, cudaStream_t s);
+bool bdrln_fwd_vec(const void* partial, const void* bias, const void* res, const void* gamma, const void* beta, void* sum,
+                   void* y, float* mean, float* rstd, DT t, i64 rows, i64 n, float eps, u64 s1, u64 thr, float dscale,
+                   cudaStream_t s);
+bool ln_bwd_vec(int mode, const void* x, const float* mean, const float* rstd, const void* gamma, const void* g, void* gx,
+                void* gres, bool gx_acc, DT t, i64 rows, i64 n, u64 s1, u64 thr, float dscale, float* ws, int ncol,
+                int nblocks, cudaStream_t s);
+static int vec_blocks(i64 rows) { return (int)std::min<i64>(148, std::max<i64>(1, (rows + kWarps - 1) / kWarps)); }
+
 // ------------------------------------------------------------------ softmax
 template <class T>
 __global__ void k_softmax_rows(const T* x, T* y, i64 rows, i64 n) {
@@ -117,6 +128,10 @@ __global__ void k_ln_fwd(const T* x, const P* gamma, const P* beta, T* y, float*
 void layernorm_fwd(const void* x, const void* gamma, const void* beta, DT tp, void* y, float* mean, float* rstd, DT t,
                    i64 rows, i64 n, float eps, cudaStream_t s) {
     (void)tp;
+    if (ln_fwd_vec(x, gamma, beta, y, mean, rstd, t, rows, n, eps, s)) {
+        SBK_CHECK_LAUNCH();
+        return;
+    }
     dispatch(t, [&](auto* p) {
         using T = std::remove_pointer_t<decltype(p)>;
         k_ln_fwd<T, T><<<(unsigned)((rows + kWarps - 1) / kWarps), 32 * kWarps, 0, s>>>(
@@ -200,8 +215,14 @@ void layernorm_bwd(const void* x, const float* mean, const float* rstd, const vo
                    void* gx, float* dgamma, float* dbeta, DT t, i64 rows, i64 n, float* ws, cudaStream_t s) {
     (void)tp;
     (void)tg;
-    int nb = row_blocks(rows);
     int ncol = (dgamma || dbeta) ? 2 : 0;
+    int vb = vec_blocks(rows);
+    if (ln_bwd_vec(0, x, mean, rstd, gamma, g, gx, nullptr, true, t, rows, n, 0, 0, 1.f, ws, ncol, vb, s)) {
+        if (ncol) k_col_final<<<grid_for(2 * n, 256), 256, 0, s>>>(ws, vb, 2 * n, dgamma, dbeta, nullptr, n);
+        SBK_CHECK_LAUNCH();
+        return;
+    }
+    int nb = row_blocks(rows);
     size_t smem = (size_t)kWarps * ncol * n * 4;
     dispatch(t, [&](auto* p) {
         using T = std::remove_pointer_t<decltype(p)>;
@@ -245,6 +266,10 @@ void bias_dropout_residual_ln_fwd(const void* partial, const void* bias, const v
                                   const void* beta, DT tp, void* sum, void* y, float* mean, float* rstd, DT t, i64 rows,
                                   i64 n, float eps, u64 s1, u64 thr, float dscale, cudaStream_t s) {
     (void)tp;
+    if (bdrln_fwd_vec(partial, bias, residual, gamma, beta, sum, y, mean, rstd, t, rows, n, eps, s1, thr, dscale, s)) {
+        SBK_CHECK_LAUNCH();
+        return;
+    }
     dispatch(t, [&](auto* p) {
         using T = std::remove_pointer_t<decltype(p)>;
         k_bdrln_fwd<T><<<(unsigned)((rows + kWarps - 1) / kWarps), 32 * kWarps, 0, s>>>(
@@ -258,8 +283,15 @@ void bias_dropout_residual_ln_bwd(const void* sum, const float* mean, const floa
                                   float* dgamma, float* dbeta, DT t, i64 rows, i64 n, u64 s1, u64 thr, float dscale,
                                   float* ws, cudaStream_t s) {
     (void)tp;
-    int nb = row_blocks(rows);
     int ncol = 3;
+    int vb = vec_blocks(rows);
+    if (ln_bwd_vec(1, sum, mean, rstd, gamma, g, g_partial, g_res, g_partial_acc, t, rows, n, s1, thr, dscale, ws, ncol,
+                   vb, s)) {
+        k_col_final<<<grid_for(3 * n, 256), 256, 0, s>>>(ws, vb, 3 * n, dgamma, dbeta, dbias, n);
+        SBK_CHECK_LAUNCH();
+        return;
+    }
+    int nb = row_blocks(rows);
     size_t smem = (size_t)kWarps * ncol * n * 4;
     dispatch(t, [&](auto* p) {
         using T = std::remove_pointer_t<decltype(p)>;

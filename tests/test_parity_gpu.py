@@ -162,11 +162,13 @@ def test_determinism_bitwise():
         assert res[0][1].params[k].tobytes() == res[1][1].params[k].tobytes(), k
 
 
-@pytest.mark.parametrize("world", [1, 2])
-def test_bf16_tensor_core_path_vs_reference(world):
-    """Shapes that route every GEMM to tcgen05 and attention to the tensor-core
-    kernels (T=256, hd=64): the full TP recipe in bf16 against the f64 reference."""
-    cfg = dict(layers=2, hidden=128, heads=2, vocab=64, batch=2, seq=128, p=0.1)
+@pytest.mark.parametrize("world,hidden,heads,seq", [(1, 128, 2, 128), (2, 128, 2, 128), (1, 256, 4, 64),
+                                                    (2, 512, 8, 64)])
+def test_bf16_tensor_core_path_vs_reference(world, hidden, heads, seq):
+    """Shapes that route every GEMM to tcgen05, attention to the tensor-core
+    kernels (hd=64) and LayerNorm to the vectorised kernels: the full TP recipe
+    in bf16 against the f64 reference."""
+    cfg = dict(layers=2, hidden=hidden, heads=heads, vocab=64, batch=2, seq=seq, p=0.1)
     script = recipes.tp_script(2, world, ckpt_ratio=0.5)
     _, outs, grads, r = run_both(cfg, script, world, dtype="bf16")
     check(outs, grads, r, world, BF16_OUT_TOL, BF16_GRAD_TOL, metric=rel_l2)
