@@ -118,14 +118,20 @@ struct MaskRef {
     long long S;
     float scale;  // 1/(1-p)
 };
-__device__ __forceinline__ float keep_f(const MaskRef& m, long long bh, long long i, long long j) {
-    long long e = (bh * m.S + i) * m.S + j;
-    return ((m.bits[e >> 5] >> (e & 31)) & 1u) ? m.scale : 0.f;
+// keep bits of keys [j0, j0+64) for query row i (j0 % 64 == 0, S % 64 == 0: one aligned 64-bit word)
+__device__ __forceinline__ uint64_t row_bits(const MaskRef& m, long long bh, long long i, long long j0) {
+    long long e = (bh * m.S + i) * m.S + j0;
+    return __ldg((const unsigned long long*)(m.bits + (e >> 5)));
+}
+__device__ __forceinline__ float ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
 }
 
 // ------------------------------------------------------------------- forward
 template <int D>
-__global__ void __launch_bounds__(128) k_fa_fwd(Attn a, MaskRef mk) {
+__global__ void __launch_bounds__(128, 4) k_fa_fwd(Attn a, MaskRef mk) {
     extern __shared__ __align__(128) bf16 fsm[];
     bf16* Qs = fsm;
     bf16* Ks = Qs + TB * D;     // 2 stages
@@ -172,19 +178,24 @@ __global__ void __launch_bounds__(128) k_fa_fwd(Attn a, MaskRef mk) {
             mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 1));
             mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 2));
         }
-        float corr[2] = {exp2f(m[0] - mx[0]), exp2f(m[1] - mx[1])};
+        float corr[2] = {ex2(m[0] - mx[0]), ex2(m[1] - mx[1])};
         m[0] = mx[0];
         m[1] = mx[1];
         float rs[2] = {0.f, 0.f};
         const long long i0 = q0 + warp * 16 + g;
+        uint64_t mb[2] = {~0ull, ~0ull};
+        if (mk.bits) {
+            mb[0] = row_bits(mk, bh, i0, (long long)jb * TB);
+            mb[1] = row_bits(mk, bh, i0 + 8, (long long)jb * TB);
+        }
 #pragma unroll
         for (int n = 0; n < TB / 8; ++n) {
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
                 int r = e >> 1;
-                float pv = exp2f(s[n][e] * sl2 - m[r]);
+                float pv = ex2(s[n][e] * sl2 - m[r]);
                 rs[r] += pv;  // the normaliser counts every probability (dropout acts after softmax)
-                if (mk.bits) pv *= keep_f(mk, bh, i0 + 8 * r, (long long)jb * TB + n * 8 + 2 * t + (e & 1));
+                if (mk.bits) pv = ((mb[r] >> (n * 8 + 2 * t + (e & 1))) & 1) ? pv * mk.scale : 0.f;
                 s[n][e] = pv;
             }
         }
@@ -235,6 +246,7 @@ __global__ void __launch_bounds__(128) k_fa_dkdv(Attn a, MaskRef mk, const bf16*
     bf16* Ds = Qs + 2 * TB * D;   // dO, 2 stages
     float* Ls = (float*)(Ds + 2 * TB * D);  // lse, 2 stages
     float* Es = Ls + 2 * TB;                // delta, 2 stages
+    uint64_t* Ms = (uint64_t*)(Es + 2 * TB);  // keep bits of (query, this key block), 2 stages
     const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
     const int g = lane >> 2, t = lane & 3;
     const long long b = blockIdx.z, h = blockIdx.y, k0 = (long long)blockIdx.x * TB;
@@ -249,8 +261,9 @@ __global__ void __launch_bounds__(128) k_fa_dkdv(Attn a, MaskRef mk, const bf16*
         load_tile<D>(Qs + st * TB * D, Qg + (long long)ib * TB * a.ld_q, a.ld_q, tid, 128);
         load_tile<D>(Ds + st * TB * D, Og + (long long)ib * TB * ld_do, ld_do, tid, 128);
         if (tid < TB) {
-            Ls[st * TB + tid] = a.lse[bh * a.S + ib * TB + tid];
+            Ls[st * TB + tid] = a.lse[bh * a.S + ib * TB + tid] * 1.4426950408889634f;
             Es[st * TB + tid] = delta[bh * a.S + ib * TB + tid];
+            Ms[st * TB + tid] = mk.bits ? row_bits(mk, bh, (long long)ib * TB + tid, k0) : ~0ull;
         }
     };
     load_q(0, 0);
@@ -285,8 +298,8 @@ __global__ void __launch_bounds__(128) k_fa_dkdv(Attn a, MaskRef mk, const bf16*
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
                 int qi = n * 8 + 2 * t + (e & 1);  // query within the block
-                float p = exp2f(s[n][e] * sl2 - Ls[st * TB + qi] * 1.4426950408889634f);
-                float c = mk.bits ? keep_f(mk, bh, (long long)ib * TB + qi, j0 + 8 * (e >> 1)) : 1.f;
+                float p = ex2(s[n][e] * sl2 - Ls[st * TB + qi]);
+                float c = mk.bits ? (((Ms[st * TB + qi] >> (warp * 16 + g + 8 * (e >> 1))) & 1) ? mk.scale : 0.f) : 1.f;
                 float dsv = p * (c * dp[n][e] - Es[st * TB + qi]);
                 s[n][e] = p * c;   // dropped probabilities for dV
                 dp[n][e] = dsv;    // dS^T
@@ -356,13 +369,18 @@ __global__ void __launch_bounds__(128) k_fa_dq(Attn a, MaskRef mk, const bf16* d
         float s[TB / 8][4] = {}, dp[TB / 8][4] = {};
         mma_abt<D, TB / 8>(s, qa, k, lane);
         mma_abt<D, TB / 8>(dp, da, Vs + st * TB * D, lane);
+        uint64_t mb[2] = {~0ull, ~0ull};
+        if (mk.bits) {
+            mb[0] = row_bits(mk, bh, i0, (long long)jb * TB);
+            mb[1] = row_bits(mk, bh, i0 + 8, (long long)jb * TB);
+        }
 #pragma unroll
         for (int n = 0; n < TB / 8; ++n) {
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
                 int r = e >> 1;
-                float p = exp2f(s[n][e] * sl2 - L2[r]);
-                float c = mk.bits ? keep_f(mk, bh, i0 + 8 * r, (long long)jb * TB + n * 8 + 2 * t + (e & 1)) : 1.f;
+                float p = ex2(s[n][e] * sl2 - L2[r]);
+                float c = mk.bits ? (((mb[r] >> (n * 8 + 2 * t + (e & 1))) & 1) ? mk.scale : 0.f) : 1.f;
                 s[n][e] = p * (c * dp[n][e] - E[r]);  // dS
             }
         }
@@ -441,7 +459,7 @@ bool attn_bwd_tc_try(const Attn& a, const void* dout, i64 ld_do, void* dq, void*
     dim3 grid((unsigned)(a.S / TB), (unsigned)a.nh, (unsigned)a.B);
     auto go = [&](auto dc) {
         constexpr int D = decltype(dc)::value;
-        int s1 = 6 * TB * D * 2 + 4 * TB * 4, s2 = 6 * TB * D * 2;
+        int s1 = 6 * TB * D * 2 + 4 * TB * 4 + 2 * TB * 8, s2 = 6 * TB * D * 2;
         smem_attr(k_fa_dkdv<D>, s1);
         smem_attr(k_fa_dq<D>, s2);
         k_fa_dkdv<D><<<grid, 128, s1, s>>>(a, mk, (const bf16*)dout, ld_do, (bf16*)dk, (bf16*)dv, ld_dk, ld_dv, delta);

@@ -260,9 +260,11 @@ __global__ void k_dropout_mask(uint32_t* bits, i64 n, uint64_t s1, uint64_t thr)
     i64 nw = (n + 31) / 32;
     for (i64 w = blockIdx.x * (i64)blockDim.x + threadIdx.x; w < nw; w += (i64)gridDim.x * blockDim.x) {
         uint32_t m = 0;
+        // 32 independent hash chains per thread: fully unrolled so they interleave
+#pragma unroll
         for (int b = 0; b < 32; ++b) {
             i64 i = w * 32 + b;
-            if (i < n && d_keep(s1, (uint64_t)i, thr)) m |= 1u << b;
+            if (d_keep(s1, (uint64_t)i, thr) && i < n) m |= 1u << b;
         }
         bits[w] = m;
     }

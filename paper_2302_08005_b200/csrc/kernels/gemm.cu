@@ -68,6 +68,8 @@ __global__ void __launch_bounds__(256) k_gemm_simt(Gemm g) {
             if (g.epilogue == 1) {
                 if (X) X[ci] = from_f<TC>(v);
                 v = gelu_f(v);
+            } else if (g.epilogue == 2) {
+                v *= gelu_grad_f(to_f(X[ci]));  // dgrad straight into a GeLU input's gradient
             }
             if (g.accumulate) v += to_f(C[ci]);
             C[ci] = from_f<TC>(v);

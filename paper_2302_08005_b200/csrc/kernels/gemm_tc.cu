@@ -7,10 +7,12 @@
 //   forward  y  = x W^T : A K-major, B K-major
 //   dgrad    dx = g W   : A K-major, B MN-major
 //   wgrad    dW = g^T x : A MN-major, B MN-major, long K -> deterministic split-K
-// Warp roles (192 threads, 1 CTA/SM): warp 0 TMA producer, warp 1 TMEM
-// allocator + single-thread MMA issuer, warps 2-5 epilogue (TMEM lane quarter
-// = warp % 4). mbarrier ring of STAGES {full, empty} pairs between TMA and MMA,
-// one tcgen05.commit barrier between MMA and the epilogue.
+// Persistent: one CTA per SM walks a static tile schedule. Warp roles (192
+// threads): warp 0 TMA producer, warp 1 TMEM allocator + single-thread MMA
+// issuer, warps 2-5 epilogue (TMEM lane quarter = warp % 4). Two TMEM
+// accumulators (2 x BN columns) let the epilogue of tile i overlap the MMAs of
+// tile i+1. mbarrier rings: STAGES {full, empty} between TMA and MMA, and
+// {tmem_full, tmem_empty} x 2 between MMA and epilogue.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -31,6 +33,9 @@ __device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
 }
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
     asm volatile(
@@ -81,7 +86,7 @@ struct Epi {
     long long ldc;
     int c_f32;
     const bf16* bias;
-    int gelu;
+    int gelu;        // 1: C = gelu(v), aux = v (forward);  2: C = gelu'(aux) * v (dgrad of a GeLU input)
     bf16* aux;
     int accumulate;
     float alpha;
@@ -89,19 +94,110 @@ struct Epi {
     long long M, N;
 };
 
+struct Sched {
+    int m_blks, n_blks, splits, kblocks;  // kblocks per split
+    __host__ __device__ int tiles() const { return m_blks * n_blks * splits; }
+};
+
+__device__ __forceinline__ void tile_coords(const Sched& sc, int tile, int BN, int& m0, int& n0, int& z) {
+    int per = sc.m_blks * sc.n_blks;
+    z = tile / per;
+    int r = tile % per;
+    m0 = (r / sc.n_blks) * BM;  // consecutive tiles share the A row block (L2 reuse)
+    n0 = (r % sc.n_blks) * BN;
+}
+
+template <int BN>
+__device__ __forceinline__ void epilogue_chunk(const Epi& ep, int z, long long row, long long col, const uint32_t (&r)[32]) {
+    float v[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * ep.alpha;
+    if (ep.partial) {
+        float4* dst = (float4*)(ep.partial + ((long long)z * ep.M + row) * ep.N + col);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) dst[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+        return;
+    }
+    if (ep.bias) {
+        const uint4* bp = (const uint4*)(ep.bias + col);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            uint4 w = bp[j];
+            const bf16* e = (const bf16*)&w;
+#pragma unroll
+            for (int t = 0; t < 8; ++t) v[8 * j + t] += __bfloat162float(e[t]);
+        }
+    }
+    if (ep.gelu == 1) {
+        uint4* ax = (uint4*)(ep.aux + row * ep.ldc + col);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            uint4 w;
+            bf16* e = (bf16*)&w;
+#pragma unroll
+            for (int t = 0; t < 8; ++t) e[t] = __float2bfloat16_rn(v[8 * j + t]);
+            ax[j] = w;
+        }
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = gelu_f(v[j]);
+    } else if (ep.gelu == 2) {
+        const uint4* ax = (const uint4*)(ep.aux + row * ep.ldc + col);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            uint4 w = ax[j];
+            const bf16* e = (const bf16*)&w;
+#pragma unroll
+            for (int t = 0; t < 8; ++t) v[8 * j + t] *= gelu_grad_f(__bfloat162float(e[t]));
+        }
+    }
+    if (ep.c_f32) {
+        float4* dst = (float4*)((float*)ep.C + row * ep.ldc + col);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            float4 o = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+            if (ep.accumulate) {
+                float4 p = dst[j];
+                o.x += p.x;
+                o.y += p.y;
+                o.z += p.z;
+                o.w += p.w;
+            }
+            dst[j] = o;
+        }
+    } else {
+        uint4* dst = (uint4*)((bf16*)ep.C + row * ep.ldc + col);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            uint4 w;
+            bf16* e = (bf16*)&w;
+            if (ep.accumulate) {
+                uint4 p = dst[j];
+                const bf16* pe = (const bf16*)&p;
+#pragma unroll
+                for (int t = 0; t < 8; ++t) e[t] = __float2bfloat16_rn(v[8 * j + t] + __bfloat162float(pe[t]));
+            } else {
+#pragma unroll
+                for (int t = 0; t < 8; ++t) e[t] = __float2bfloat16_rn(v[8 * j + t]);
+            }
+            dst[j] = w;
+        }
+    }
+}
+
 template <int BN, int STAGES, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(192, 1)
-    k_gemm_tc(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB, Epi ep, int kblocks) {
+    k_gemm_tc(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB, Epi ep, Sched sc) {
     constexpr int A_BYTES = BM * BK * 2, B_BYTES = BN * BK * 2, STAGE = A_BYTES + B_BYTES;
+    constexpr uint32_t TCOLS = 2 * BN;  // two accumulators
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint64_t* full = (uint64_t*)(smem + STAGES * STAGE);
     uint64_t* empty = full + STAGES;
-    uint64_t* tfull = empty + STAGES;
-    uint32_t* tslot = (uint32_t*)(tfull + 1);
+    uint64_t* tfull = empty + STAGES;  // [2]
+    uint64_t* tempty = tfull + 2;      // [2]
+    uint32_t* tslot = (uint32_t*)(tempty + 2);
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    const int n0 = blockIdx.x * BN, m0 = blockIdx.y * BM;
-    const int kb0 = blockIdx.z * kblocks;
+    const int ntiles = sc.tiles();
 
     if (warp == 0 && lane == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tA) : "memory");
@@ -110,11 +206,15 @@ __global__ void __launch_bounds__(192, 1)
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
-        mbar_init(tfull, 1);
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 4);  // one arrival per epilogue warp
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)), "r"(BN));
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
+                     "r"(TCOLS));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -124,25 +224,30 @@ __global__ void __launch_bounds__(192, 1)
 
     if (warp == 0) {
         if (lane == 0) {
-            // ---------------- TMA producer
-            for (int it = 0; it < kblocks; ++it) {
-                int s = it % STAGES;
-                mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
-                uint8_t* sa = smem + s * STAGE;
-                uint8_t* sbp = sa + A_BYTES;
-                mbar_expect_tx(&full[s], STAGE);
-                int kc = (kb0 + it) * BK;
-                if (A_MN) {
+            // ---------------- TMA producer: all k-blocks of all this CTA's tiles
+            int it = 0;
+            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+                int m0, n0, z;
+                tile_coords(sc, tile, BN, m0, n0, z);
+                for (int kb = 0; kb < sc.kblocks; ++kb, ++it) {
+                    int s = it % STAGES;
+                    mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
+                    uint8_t* sa = smem + s * STAGE;
+                    uint8_t* sbp = sa + A_BYTES;
+                    mbar_expect_tx(&full[s], STAGE);
+                    int kc = (z * sc.kblocks + kb) * BK;
+                    if (A_MN) {
 #pragma unroll
-                    for (int c = 0; c < BM / 64; ++c) tma_load_2d(sa + c * 8192, &tA, &full[s], m0 + 64 * c, kc);
-                } else {
-                    tma_load_2d(sa, &tA, &full[s], kc, m0);
-                }
-                if (B_MN) {
+                        for (int c = 0; c < BM / 64; ++c) tma_load_2d(sa + c * 8192, &tA, &full[s], m0 + 64 * c, kc);
+                    } else {
+                        tma_load_2d(sa, &tA, &full[s], kc, m0);
+                    }
+                    if (B_MN) {
 #pragma unroll
-                    for (int c = 0; c < BN / 64; ++c) tma_load_2d(sbp + c * 8192, &tB, &full[s], n0 + 64 * c, kc);
-                } else {
-                    tma_load_2d(sbp, &tB, &full[s], kc, n0);
+                        for (int c = 0; c < BN / 64; ++c) tma_load_2d(sbp + c * 8192, &tB, &full[s], n0 + 64 * c, kc);
+                    } else {
+                        tma_load_2d(sbp, &tB, &full[s], kc, n0);
+                    }
                 }
             }
         }
@@ -151,103 +256,57 @@ __global__ void __launch_bounds__(192, 1)
             // ---------------- MMA issuer (one thread for the whole CTA)
             constexpr uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((A_MN ? 1u : 0u) << 15) |
                                        ((B_MN ? 1u : 0u) << 16) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
-            for (int it = 0; it < kblocks; ++it) {
-                int s = it % STAGES;
-                mbar_wait(&full[s], (it / STAGES) & 1);
+            int it = 0, lt = 0;
+            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++lt) {
+                const int acc = lt & 1;
+                mbar_wait(&tempty[acc], ((lt >> 1) & 1) ^ 1);  // epilogue drained this accumulator
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                uint32_t a_base = smem_u32(smem + s * STAGE), b_base = a_base + A_BYTES;
+                const uint32_t d = tmem + (uint32_t)(acc * BN);
+                for (int kb = 0; kb < sc.kblocks; ++kb, ++it) {
+                    int s = it % STAGES;
+                    mbar_wait(&full[s], (it / STAGES) & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    uint32_t a_base = smem_u32(smem + s * STAGE), b_base = a_base + A_BYTES;
 #pragma unroll
-                for (int k = 0; k < BK / 16; ++k) {
-                    uint64_t da = A_MN ? sdesc(a_base + k * 2048, 8192 >> 4, 1024 >> 4) : sdesc(a_base + k * 32, 1, 1024 >> 4);
-                    uint64_t db = B_MN ? sdesc(b_base + k * 2048, 8192 >> 4, 1024 >> 4) : sdesc(b_base + k * 32, 1, 1024 >> 4);
-                    mma_bf16(tmem, da, db, idesc, (it | k) != 0);
+                    for (int k = 0; k < BK / 16; ++k) {
+                        uint64_t da = A_MN ? sdesc(a_base + k * 2048, 8192 >> 4, 1024 >> 4)
+                                           : sdesc(a_base + k * 32, 1, 1024 >> 4);
+                        uint64_t db = B_MN ? sdesc(b_base + k * 2048, 8192 >> 4, 1024 >> 4)
+                                           : sdesc(b_base + k * 32, 1, 1024 >> 4);
+                        mma_bf16(d, da, db, idesc, (kb | k) != 0);
+                    }
+                    mma_commit(&empty[s]);  // frees the smem slot once these MMAs have read it
                 }
-                mma_commit(&empty[s]);  // frees the smem slot once these MMAs have read it
+                mma_commit(&tfull[acc]);  // accumulator complete
             }
-            mma_commit(tfull);  // accumulator complete
         }
     } else {
         // ---------------- epilogue: TMEM -> registers -> global
         const int q = warp & 3;  // TMEM lane quarter this warp may access
-        const long long row = m0 + q * 32 + lane;
-        mbar_wait(tfull, 0);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        int lt = 0;
+        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++lt) {
+            const int acc = lt & 1;
+            int m0, n0, z;
+            tile_coords(sc, tile, BN, m0, n0, z);
+            const long long row = m0 + q * 32 + lane;
+            mbar_wait(&tfull[acc], (lt >> 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
-            uint32_t r[32];
-            tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(c * 32), r);
-            const long long col = n0 + c * 32;
-            float v[32];
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * ep.alpha;
-            if (ep.partial) {
-                float4* dst = (float4*)(ep.partial + ((long long)blockIdx.z * ep.M + row) * ep.N + col);
-#pragma unroll
-                for (int j = 0; j < 8; ++j) dst[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-                continue;
+            for (int c = 0; c < BN / 32; ++c) {
+                uint32_t r[32];
+                tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c * 32), r);
+                epilogue_chunk<BN>(ep, z, row, n0 + c * 32, r);
             }
-            if (ep.bias) {
-                const uint4* bp = (const uint4*)(ep.bias + col);
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    uint4 w = bp[j];
-                    const bf16* e = (const bf16*)&w;
-#pragma unroll
-                    for (int t = 0; t < 8; ++t) v[8 * j + t] += __bfloat162float(e[t]);
-                }
-            }
-            if (ep.gelu) {
-                uint4* ax = (uint4*)(ep.aux + row * ep.ldc + col);
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    uint4 w;
-                    bf16* e = (bf16*)&w;
-#pragma unroll
-                    for (int t = 0; t < 8; ++t) e[t] = __float2bfloat16_rn(v[8 * j + t]);
-                    ax[j] = w;
-                }
-#pragma unroll
-                for (int j = 0; j < 32; ++j) v[j] = gelu_f(v[j]);
-            }
-            if (ep.c_f32) {
-                float4* dst = (float4*)((float*)ep.C + row * ep.ldc + col);
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    float4 o = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-                    if (ep.accumulate) {
-                        float4 p = dst[j];
-                        o.x += p.x;
-                        o.y += p.y;
-                        o.z += p.z;
-                        o.w += p.w;
-                    }
-                    dst[j] = o;
-                }
-            } else {
-                uint4* dst = (uint4*)((bf16*)ep.C + row * ep.ldc + col);
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    uint4 w;
-                    bf16* e = (bf16*)&w;
-                    if (ep.accumulate) {
-                        uint4 p = dst[j];
-                        const bf16* pe = (const bf16*)&p;
-#pragma unroll
-                        for (int t = 0; t < 8; ++t) e[t] = __float2bfloat16_rn(v[8 * j + t] + __bfloat162float(pe[t]));
-                    } else {
-#pragma unroll
-                        for (int t = 0; t < 8; ++t) e[t] = __float2bfloat16_rn(v[8 * j + t]);
-                    }
-                    dst[j] = w;
-                }
-            }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     if (warp == 1) {
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TCOLS));
     }
 }
 
@@ -303,9 +362,10 @@ bool make_map(CUtensorMap* m, const void* base, long long inner, long long outer
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+int g_num_sms = 0;
+
 template <int BN, int STAGES, bool A_MN, bool B_MN>
-void launch(const CUtensorMap& ta, const CUtensorMap& tb, const Epi& ep, long long M, long long N, int kblocks, int splits,
-            cudaStream_t s) {
+void launch(const CUtensorMap& ta, const CUtensorMap& tb, const Epi& ep, const Sched& sc, cudaStream_t s) {
     constexpr int smem = STAGES * (BM * BK * 2 + BN * BK * 2) + 1024 + 256;
     auto k = k_gemm_tc<BN, STAGES, A_MN, B_MN>;
     static bool attr = false;
@@ -313,8 +373,9 @@ void launch(const CUtensorMap& ta, const CUtensorMap& tb, const Epi& ep, long lo
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         attr = true;
     }
-    dim3 grid((unsigned)(N / BN), (unsigned)(M / BM), (unsigned)splits);
-    k<<<grid, 192, smem, s>>>(ta, tb, ep, kblocks);
+    if (!g_num_sms) cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, 0);
+    int grid = std::min(sc.tiles(), g_num_sms);
+    k<<<grid, 192, smem, s>>>(ta, tb, ep, sc);
 }
 
 bool g_tc_disabled = false;
@@ -327,7 +388,7 @@ bool gemm_tc_try(const Gemm& g, cudaStream_t s) {
     if (g_tc_disabled) return false;
     if (g.ta != BF16 || g.tb != BF16 || g.batch != 1 || g.sCn != 1) return false;
     if (g.tc != BF16 && g.tc != F32) return false;
-    if (g.epilogue == 1 && (g.tc != BF16 || !g.aux)) return false;
+    if (g.epilogue && (g.tc != BF16 || !g.aux)) return false;
     if (g.bias && g.tbias != BF16) return false;
     const bool a_mn = g.sAm == 1 && g.sAk != 1, b_mn = g.sBn == 1 && g.sBk != 1;
     const bool a_k = g.sAk == 1 && !a_mn, b_k = g.sBk == 1 && !b_mn;
@@ -360,24 +421,24 @@ bool gemm_tc_try(const Gemm& g, cudaStream_t s) {
     ep.ldc = ldc;
     ep.c_f32 = g.tc == F32;
     ep.bias = (const bf16*)g.bias;
-    ep.gelu = g.epilogue == 1;
+    ep.gelu = g.epilogue;
     ep.aux = (bf16*)g.aux;
     ep.accumulate = g.accumulate;
     ep.alpha = g.alpha;
     ep.partial = splits > 1 ? (float*)g.ws : nullptr;
     ep.M = M;
     ep.N = N;
-    int kb = kblocks / splits;
+    Sched sc{(int)(M / BM), (int)(N / BNs), splits, kblocks / splits};
     if (BNs == 256) {
-        if (!a_mn && !b_mn) launch<256, 4, false, false>(ta, tb, ep, M, N, kb, splits, s);
-        else if (!a_mn && b_mn) launch<256, 4, false, true>(ta, tb, ep, M, N, kb, splits, s);
-        else if (a_mn && b_mn) launch<256, 4, true, true>(ta, tb, ep, M, N, kb, splits, s);
-        else launch<256, 4, true, false>(ta, tb, ep, M, N, kb, splits, s);
+        if (!a_mn && !b_mn) launch<256, 4, false, false>(ta, tb, ep, sc, s);
+        else if (!a_mn && b_mn) launch<256, 4, false, true>(ta, tb, ep, sc, s);
+        else if (a_mn && b_mn) launch<256, 4, true, true>(ta, tb, ep, sc, s);
+        else launch<256, 4, true, false>(ta, tb, ep, sc, s);
     } else {
-        if (!a_mn && !b_mn) launch<128, 6, false, false>(ta, tb, ep, M, N, kb, splits, s);
-        else if (!a_mn && b_mn) launch<128, 6, false, true>(ta, tb, ep, M, N, kb, splits, s);
-        else if (a_mn && b_mn) launch<128, 6, true, true>(ta, tb, ep, M, N, kb, splits, s);
-        else launch<128, 6, true, false>(ta, tb, ep, M, N, kb, splits, s);
+        if (!a_mn && !b_mn) launch<128, 6, false, false>(ta, tb, ep, sc, s);
+        else if (!a_mn && b_mn) launch<128, 6, false, true>(ta, tb, ep, sc, s);
+        else if (a_mn && b_mn) launch<128, 6, true, true>(ta, tb, ep, sc, s);
+        else launch<128, 6, true, false>(ta, tb, ep, sc, s);
     }
     SBK_CHECK_LAUNCH();
     if (splits > 1) {

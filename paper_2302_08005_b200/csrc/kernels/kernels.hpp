@@ -18,7 +18,8 @@ inline int dt_bytes(DT d) { return d == F32 ? 4 : d == BF16 ? 2 : 8; }
 // ------------------------------------------------------------------ GEMM
 // C[b](m,n) = alpha * sum_k A[b](m,k) B[b](k,n)  (+ bias[n]) (+ C if accumulate)
 // with arbitrary element strides; fp32 accumulation. epilogue: 0 none,
-// 1 gelu (then `aux`, if set, receives the pre-activation in C's dtype).
+// 1 gelu (then `aux`, if set, receives the pre-activation in C's dtype),
+// 2 dgelu: C (+)= gelu'(aux) * (A B) — a dgrad written as the gradient of a GeLU's input.
 struct Gemm {
     const void* A = nullptr;
     DT ta = F32;
