@@ -122,6 +122,7 @@ public:
                 throw Error("per-rank plans differ structurally; lockstep execution impossible");
         }
         build_backward_steps();
+        analyze_writes();
         for (auto& r : ranks) allocate(r);
         init_mask_stream();
         if (comm.nccl && world > 1) {
@@ -170,6 +171,7 @@ public:
             default:
                 for (int v : op.in) add(v);
         }
+        if (op.dgelu_pre >= 0) add(op.dgelu_pre);
         return s;
     }
 
@@ -211,6 +213,166 @@ public:
                 mark(op);
             }
             --i;
+        }
+    }
+
+    // ------------------------------------------------ first-writer analysis
+    // Instead of zeroing every gradient and accumulating, each gradient write of
+    // the (static) backward order is classified: the first write to a region
+    // overwrites, later ones accumulate. Only storages that are read or
+    // accumulated before being fully written are zeroed, once, at backward start.
+    std::vector<std::map<int, bool>> step_ow;  // per backward step: view -> overwrite
+    std::map<int, bool> seed_ow;               // output-gradient seeds
+    std::vector<int> zero_gst;                 // persistent grad storages to zero
+    std::vector<char> region_zero;             // region scratch needs zeroing
+    const std::map<int, bool>* cur_ow = nullptr;
+    bool OW(int v) const {
+        if (!cur_ow) return false;
+        auto it = cur_ow->find(v);
+        return it != cur_ow->end() && it->second;
+    }
+
+    // (view, kernel can overwrite) in the order the backward writes them
+    std::vector<std::pair<int, bool>> grad_slots(const Plan& P, const Op& op) const {
+        std::vector<std::pair<int, bool>> s;
+        auto direct = [&](int v) { return P.st[(size_t)P.views[(size_t)v].gst].gdt == P.cdt; };
+        auto linear = [&](bool bias) {
+            if (op.dgelu_pre >= 0) s.push_back({op.dgelu_pre, true});
+            else s.push_back({op.in[0], direct(op.in[0])});
+            s.push_back({op.in[1], true});
+            if (bias && op.has_bias && op.bias_grad) s.push_back({op.in[2], true});
+        };
+        switch (op.k) {
+            case K::Linear: linear(true); break;
+            case K::FusedLinearGelu:
+                if (!op.dgelu_fused) s.push_back({op.out[1], false});
+                linear(true);
+                break;
+            case K::FusedLinearResLN:
+                s.push_back({op.in[2], direct(op.in[2])});
+                s.push_back({op.out[1], true});
+                if (op.has_bias && op.bias_grad) s.push_back({op.in[5], true});
+                s.push_back({op.in[3], true});
+                s.push_back({op.in[4], true});
+                linear(false);
+                break;
+            case K::LayerNorm:
+                s.push_back({op.in[0], direct(op.in[0])});
+                if (op.affine) {
+                    s.push_back({op.in[1], true});
+                    s.push_back({op.in[2], true});
+                }
+                break;
+            case K::FlashAttn:
+                for (int k = 0; k < 3; ++k) s.push_back({op.in[(size_t)k], true});
+                break;
+            case K::Embedding: s.push_back({op.in[1], false}); break;  // scatter-add: partial rows
+            case K::SyncGrad:
+                if (!op.ids_input) s.push_back({op.in[0], true});
+                break;
+            case K::Cast:
+                if (P.st[(size_t)P.views[(size_t)op.out[0]].st].dt != sbk::F64) s.push_back({op.in[0], true});
+                break;
+            case K::Dropout: s.push_back({op.in[0], direct(op.in[0])}); break;
+            case K::AllReduce:
+                if (op.allreduce) s.push_back({op.in[0], true});
+                break;
+            case K::Add:
+                s.push_back({op.in[0], direct(op.in[0])});
+                s.push_back({op.in[1], direct(op.in[1])});
+                break;
+            default:
+                for (int v : op.in) s.push_back({v, false});
+        }
+        return s;
+    }
+    std::vector<int> grad_reads(const Op& op) const {
+        if (op.k == K::FusedLinearGelu && op.dgelu_fused) return {op.out[1]};
+        if (op.k == K::SyncGrad && op.ids_input) return {};
+        return {op.out[0]};
+    }
+
+    struct Span {
+        i64 lo, hi, ld, c0, c1;
+        bool rowwise;
+        i64 n;
+    };
+    static Span span_of(const View& v) {
+        Span s{};
+        s.lo = v.goff;
+        s.hi = v.goff + 1;
+        for (size_t d = 0; d < v.shape.size(); ++d) s.hi += (v.shape[d] - 1) * v.gstrides[d];
+        i64 rows, cols, ld;
+        s.rowwise = v.rowwise(rows, cols, ld, true);
+        s.ld = s.rowwise ? ld : 0;
+        s.c0 = s.rowwise && ld ? v.goff % ld : 0;
+        s.c1 = s.c0 + (s.rowwise ? cols : 0);
+        s.n = v.numel();
+        return s;
+    }
+    static bool overlap(const Span& a, const Span& b) {
+        if (a.hi <= b.lo || b.hi <= a.lo) return false;
+        if (a.rowwise && b.rowwise && a.ld == b.ld && a.ld > 0 && (a.c1 <= b.c0 || b.c1 <= a.c0)) return false;
+        return true;
+    }
+    static bool same(const Span& a, const Span& b) {
+        return a.lo == b.lo && a.hi == b.hi && a.n == b.n && a.c0 == b.c0 && a.c1 == b.c1;
+    }
+
+    void analyze_writes() {
+        const Plan& P = ranks[0].P;
+        std::map<int, std::vector<Span>> written;
+        std::vector<char> need(P.st.size(), 0);
+        auto covered = [&](int gst, const Span& r) {
+            auto& w = written[gst];
+            for (auto& s : w)
+                if (same(s, r)) return true;
+            i64 tot = 0;
+            for (size_t i = 0; i < w.size(); ++i) {
+                for (size_t j = i + 1; j < w.size(); ++j)
+                    if (overlap(w[i], w[j])) return false;
+                tot += w[i].n;
+            }
+            return r.lo == 0 && r.n == P.st[(size_t)gst].numel && tot >= r.n;
+        };
+        auto write = [&](std::map<int, bool>& modes, int v, bool ok) {
+            int gst = P.views[(size_t)v].gst;
+            Span sp = span_of(P.views[(size_t)v]);
+            bool fresh = true;
+            for (auto& s : written[gst]) fresh = fresh && !overlap(s, sp);
+            if (modes.count(v)) {  // the same view twice in one op: both writes accumulate
+                if (modes[v]) need[(size_t)gst] = 1;
+                modes[v] = false;
+            } else {
+                bool ow = fresh && ok;
+                if (!ow && fresh) need[(size_t)gst] = 1;  // accumulating onto never-written memory
+                modes[v] = ow;
+            }
+            written[gst].push_back(sp);
+        };
+        for (int v : P.outputs) write(seed_ow, v, true);
+        step_ow.assign(bsteps.size(), {});
+        for (size_t si = 0; si < bsteps.size(); ++si) {
+            if (bsteps[si].kind != 0) continue;
+            const Op& op = P.fwd[(size_t)bsteps[si].idx];
+            for (int v : grad_reads(op)) {
+                int gst = P.views[(size_t)v].gst;
+                if (!covered(gst, span_of(P.views[(size_t)v]))) need[(size_t)gst] = 1;
+            }
+            for (auto& [v, ok] : grad_slots(P, op)) write(step_ow[si], v, ok);
+        }
+        auto final_read = [&](int v) {
+            int gst = P.views[(size_t)v].gst;
+            if (!covered(gst, span_of(P.views[(size_t)v]))) need[(size_t)gst] = 1;
+        };
+        for (auto& pv : P.params) final_read(pv.second);
+        for (int v : P.inputs) final_read(v);
+        zero_gst.clear();
+        region_zero.assign(P.regions.size(), 0);
+        for (size_t g = 0; g < P.st.size(); ++g) {
+            if (!need[g]) continue;
+            if (P.st[g].region >= 0) region_zero[(size_t)P.st[g].region] = 1;
+            else zero_gst.push_back((int)g);
         }
     }
 
@@ -713,16 +875,23 @@ public:
         i64 rows, cols, ldx, gr, gc, ldgx;
         x.rowwise(rows, cols, ldx);
         i64 out_f = w.shape[0];
-        GT gx = gtarget(r, op.in[0]);
-        if (gx.temp) ldgx = cols;
-        else x.rowwise(gr, gc, ldgx, true);
-        gemm_rowwise(r, g, ldg, false, fp(r, op.in[1]), cols, false, gx.p, ldgx, cdt, rows, cols, out_f, true, nullptr);
-        flush(r, gx);
+        if (op.dgelu_pre >= 0) {
+            // dx lands directly as the producing GeLU's input gradient: gelu'(pre) * (g W)
+            gemm_rowwise(r, g, ldg, false, fp(r, op.in[1]), cols, false, gp(r, op.dgelu_pre), cols, cdt, rows, cols,
+                         out_f, !OW(op.dgelu_pre), nullptr, 2, fp(r, op.dgelu_pre));
+        } else {
+            GT gx = gtarget(r, op.in[0]);
+            if (gx.temp) ldgx = cols;
+            else x.rowwise(gr, gc, ldgx, true);
+            gemm_rowwise(r, g, ldg, false, fp(r, op.in[1]), cols, false, gx.p, ldgx, cdt, rows, cols, out_f,
+                         gx.temp || !OW(op.in[0]), nullptr);
+            flush(r, gx);
+        }
         gemm_rowwise(r, g, ldg, true, fp(r, op.in[0]), ldx, false, gp(r, op.in[1]), cols, gdt(r, op.in[1]), out_f, cols,
-                     rows, true, nullptr);
+                     rows, !OW(op.in[1]), nullptr);
         launches += 2;
         if (op.has_bias && op.bias_grad) {
-            sbk::bias_grad(g, cdt, ldg, rows, out_f, (float*)gp(r, op.in[2]), (float*)r.ws, stream);
+            sbk::bias_grad(g, cdt, ldg, rows, out_f, (float*)gp(r, op.in[2]), (float*)r.ws, stream, !OW(op.in[2]));
             ++launches;
         }
     }
@@ -741,7 +910,7 @@ public:
                 if (world > 1) all_reduce(b, b, cdt, n);
                 for (auto& r : ranks) {
                     const Op& op = r.P.fwd[(size_t)i];
-                    accumulate_view(r, op.out[0], op.in[0]);
+                    accumulate_view(r, op.out[0], op.in[0], !OW(op.in[0]));
                 }
                 break;
             }
@@ -756,7 +925,7 @@ public:
                         gp(r, op.out[0]), gres.p, gp(r, op.out[1]), false,
                         op.has_bias && op.bias_grad ? (float*)gp(r, op.in[5]) : nullptr, (float*)gp(r, op.in[3]),
                         (float*)gp(r, op.in[4]), cdt, rows, n, op.s1, op.dropout ? op.thr : 0,
-                        (float)(1.0 / (1.0 - op.p)), (float*)r.ws, stream);
+                        (float)(1.0 / (1.0 - op.p)), (float*)r.ws, stream, gres.temp || !OW(op.in[2]), !OW(op.in[3]));
                     flush(r, gres);
                     ++launches;
                     // the in-region all_reduce backpropagates as identity (executor.cpp:1227-1233)
@@ -772,16 +941,17 @@ public:
         if (profiling) prof_end();
     }
 
-    void accumulate_view(RankCtx& r, int from, int to) {
-        // grad(to) += grad(from); equal shapes
+    void accumulate_view(RankCtx& r, int from, int to, bool acc = true) {
+        // grad(to) (+)= grad(from); equal shapes
         const View& a = V(r, from);
         const View& b = V(r, to);
         if (a.g_contiguous() && b.g_contiguous()) {
-            sbk::accumulate(gp(r, from), gdt(r, from), gp(r, to), gdt(r, to), a.numel(), 1.f, stream);
+            if (acc) sbk::accumulate(gp(r, from), gdt(r, from), gp(r, to), gdt(r, to), a.numel(), 1.f, stream);
+            else sbk::cast(gp(r, from), gdt(r, from), gp(r, to), gdt(r, to), a.numel(), stream);
         } else {
             if (gdt(r, from) != gdt(r, to)) throw Error("internal: strided dtype-converting accumulate");
             sbk::strided_copy(gp(r, from), gdt(r, from), a.gstrides.data(), gp(r, to), gdt(r, to), b.gstrides.data(),
-                              a.shape.data(), (int)a.shape.size(), true, stream);
+                              a.shape.data(), (int)a.shape.size(), acc, stream);
         }
         ++launches;
     }
@@ -791,7 +961,11 @@ public:
         switch (op.k) {
             case K::Cast:
                 if (fdt(r, op.out[0]) == sbk::F64) break;  // ids: not differentiable
-                sbk::accumulate(gp(r, op.out[0]), cdt, gp(r, op.in[0]), gdt(r, op.in[0]), V(r, op.out[0]).numel(), 1.f, stream);
+                if (OW(op.in[0]))
+                    sbk::cast(gp(r, op.out[0]), cdt, gp(r, op.in[0]), gdt(r, op.in[0]), V(r, op.out[0]).numel(), stream);
+                else
+                    sbk::accumulate(gp(r, op.out[0]), cdt, gp(r, op.in[0]), gdt(r, op.in[0]), V(r, op.out[0]).numel(), 1.f,
+                                    stream);
                 break;
             case K::Linear: {
                 const View& y = V(r, op.out[0]);
@@ -801,7 +975,9 @@ public:
             }
             case K::FusedLinearGelu: {
                 const View& y = V(r, op.out[0]);
-                sbk::unary_bwd(2, fp(r, op.out[1]), gp(r, op.out[0]), gp(r, op.out[1]), cdt, cdt, y.numel(), 1.f, stream);
+                if (!op.dgelu_fused)  // else the consumer's dgrad already wrote gelu'(pre) * g
+                    sbk::unary_bwd(2, fp(r, op.out[1]), gp(r, op.out[0]), gp(r, op.out[1]), cdt, cdt, y.numel(), 1.f,
+                                   stream);
                 linear_bwd(r, op, gp(r, op.out[1]), cols_of(y));
                 break;
             }
@@ -812,14 +988,14 @@ public:
                                    op.affine ? fp(r, op.in[1]) : nullptr, cdt, gp(r, op.out[0]), cdt, gx.p,
                                    op.affine ? (float*)gp(r, op.in[1]) : nullptr,
                                    op.affine ? (float*)gp(r, op.in[2]) : nullptr, cdt, rows_of(x), cols_of(x),
-                                   (float*)r.ws, stream);
+                                   (float*)r.ws, stream, gx.temp || !OW(op.in[0]), !op.affine || !OW(op.in[1]));
                 flush(r, gx);
                 break;
             }
             case K::Dropout: {
                 GT gx = gtarget(r, op.in[0]);
                 sbk::dropout(gp(r, op.out[0]), gx.p, cdt, V(r, op.out[0]).numel(), op.s1, op.thr,
-                             (float)(1.0 / (1.0 - op.p)), true, stream);
+                             (float)(1.0 / (1.0 - op.p)), gx.temp || !OW(op.in[0]), stream);
                 flush(r, gx);
                 break;
             }
@@ -827,10 +1003,13 @@ public:
                 i64 n = V(r, op.out[0]).numel();
                 for (int k = 0; k < 2; ++k) {
                     GT gx = gtarget(r, op.in[(size_t)k]);
+                    bool acc = gx.temp || !OW(op.in[(size_t)k]);
                     if (V(r, op.in[(size_t)k]).numel() == 1 && n != 1)
-                        sbk::reduce_all(gp(r, op.out[0]), cdt, n, gx.p, cdt, true, stream);
-                    else
+                        sbk::reduce_all(gp(r, op.out[0]), cdt, n, gx.p, cdt, acc, stream);
+                    else if (acc)
                         sbk::accumulate(gp(r, op.out[0]), cdt, gx.p, cdt, n, 1.f, stream);
+                    else
+                        sbk::cast(gp(r, op.out[0]), cdt, gx.p, cdt, n, stream);
                     flush(r, gx);
                 }
                 break;
@@ -979,7 +1158,7 @@ public:
                 break;
             }
             case K::AllReduce:
-                if (op.allreduce) accumulate_view(r, op.out[0], op.in[0]);
+                if (op.allreduce) accumulate_view(r, op.out[0], op.in[0], !OW(op.in[0]));
                 --launches;
                 break;
             case K::AllGather: {
@@ -1004,6 +1183,7 @@ public:
             }
             case K::FlashAttn: {
                 sbk::Attn a = attn_args(r, op);
+                a.acc_mask = (OW(op.in[0]) ? 0 : 1) | (OW(op.in[1]) ? 0 : 2) | (OW(op.in[2]) ? 0 : 4);
                 i64 rows, cols, lq, lk, lv;
                 V(r, op.in[0]).rowwise(rows, cols, lq, true);
                 V(r, op.in[1]).rowwise(rows, cols, lk, true);
@@ -1072,24 +1252,50 @@ public:
 
     void run_backward() {
         for (auto& r : ranks) {
-            // loss = sum of outputs: seed ones (executor.cpp:355-362); zero persistent grads
-            CK(cudaMemsetAsync(r.base + persistent_grad_span.first, 0, persistent_grad_span.second, stream));
+            // zero only what is read/accumulated before being fully written (analyze_writes)
+            for (auto& [off, bytes] : zero_ranges(r)) CK(cudaMemsetAsync(r.base + off, 0, bytes, stream));
+            // loss = sum of outputs: seed ones (executor.cpp:355-362)
             for (int v : r.P.outputs) {
                 if (!V(r, v).g_contiguous()) throw Error("internal: strided model output gradient");
-                sbk::add_scalar(gp(r, v), gdt(r, v), V(r, v).numel(), 1.f, nullptr, stream);
+                if (seed_ow.count(v) && seed_ow[v]) sbk::fill(gp(r, v), gdt(r, v), V(r, v).numel(), 1.f, stream);
+                else sbk::add_scalar(gp(r, v), gdt(r, v), V(r, v).numel(), 1.f, nullptr, stream);
                 ++launches;
             }
         }
-        for (auto& s : bsteps) {
+        for (size_t si = 0; si < bsteps.size(); ++si) {
+            const Step& s = bsteps[si];
             if (s.kind == 2) {
-                for (auto& r : ranks)
-                    CK(cudaMemsetAsync(r.scratch_grad, 0, r.region_grad_span[(size_t)s.idx].second, stream));
+                if (region_zero[(size_t)s.idx])
+                    for (auto& r : ranks)
+                        CK(cudaMemsetAsync(r.scratch_grad, 0, r.region_grad_span[(size_t)s.idx].second, stream));
             } else if (s.kind == 1) {
                 fwd_op(s.idx, true);
             } else {
+                cur_ow = &step_ow[si];
                 bwd_op(s.idx);
+                cur_ow = nullptr;
             }
         }
+    }
+
+    // merged [offset, bytes) ranges of the persistent gradient storages to zero
+    std::vector<std::pair<size_t, size_t>> zero_ranges(RankCtx& r) {
+        std::vector<std::pair<size_t, size_t>> v;
+        for (int g : zero_gst) {
+            if (!r.gptr[(size_t)g]) continue;
+            size_t off = (size_t)(r.gptr[(size_t)g] - r.base);
+            size_t bytes = (size_t)r.P.st[(size_t)g].numel * (size_t)sbk::dt_bytes(r.P.st[(size_t)g].gdt);
+            v.push_back({off, (bytes + 255) / 256 * 256});
+        }
+        std::sort(v.begin(), v.end());
+        std::vector<std::pair<size_t, size_t>> m;
+        for (auto& x : v) {
+            if (!m.empty() && m.back().first + m.back().second >= x.first)
+                m.back().second = std::max(m.back().second, x.first + x.second - m.back().first);
+            else
+                m.push_back(x);
+        }
+        return m;
     }
 
     // ---------------------------------------------------------- profile

@@ -848,6 +848,27 @@ Plan lower(const Module& root, const LowerOptions& o) {
                 if (P.st[(size_t)P.views[(size_t)v].st].region != op.region) escape(v);
             }
     for (int v : P.outputs) escape(v);
+
+    // Fold a FusedLinearGelu's GeLU backward into the dgrad epilogue of the one
+    // Linear-like op consuming its activation (dense1 -> dense2 in an FFN).
+    std::map<int, int> consumers;  // activation storage -> number of reading ops
+    for (auto& op : P.fwd)
+        for (int v : op.in) consumers[P.views[(size_t)v].st]++;
+    for (int v : P.outputs) consumers[P.views[(size_t)v].st] += 2;
+    std::map<int, int> producer;  // act storage -> FusedLinearGelu op index
+    for (size_t i = 0; i < P.fwd.size(); ++i)
+        if (P.fwd[i].k == K::FusedLinearGelu) producer[P.views[(size_t)P.fwd[i].out[0]].st] = (int)i;
+    for (auto& op : P.fwd) {
+        if (op.k != K::Linear && op.k != K::FusedLinearGelu && op.k != K::FusedLinearResLN) continue;
+        const View& x = P.views[(size_t)op.in[0]];
+        auto it = producer.find(x.st);
+        if (it == producer.end() || consumers[x.st] != 1) continue;
+        Op& g = P.fwd[(size_t)it->second];
+        const View& act = P.views[(size_t)g.out[0]];
+        if (g.region != op.region || x.gst != act.gst || !x.contiguous() || !x.g_contiguous() || x.off || act.off) continue;
+        op.dgelu_pre = g.out[1];
+        g.dgelu_fused = true;
+    }
     return P;
 }
 

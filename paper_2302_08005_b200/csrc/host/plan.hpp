@@ -92,6 +92,10 @@ struct Op {
     i64 full_rows = 0, row0 = 0;
     bool reduce_all = false;
     bool ids_input = false;  // SyncGrad over a non-differentiable id input (zero grad)
+    // dgrad of this Linear-like op writes gelu'(pre) * (g W) straight into the
+    // gradient of view `dgelu_pre` (the producing FusedLinearGelu's pre-activation)
+    int dgelu_pre = -1;
+    bool dgelu_fused = false;  // FusedLinearGelu whose GeLU backward was folded into its consumer
 };
 
 struct Region {

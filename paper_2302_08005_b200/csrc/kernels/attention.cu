@@ -158,8 +158,8 @@ __global__ void __launch_bounds__(kT) k_attn_dkdv(Attn a, const T* dout, i64 ld_
     if (!valid) return;
     for (int d = 0; d < hd; ++d) {
         i64 ik = (b * a.S + j) * ld_dk + h * hd + d, iv = (b * a.S + j) * ld_dv + h * hd + d;
-        dk[ik] = from_f<T>(to_f(dk[ik]) + a.scale * gk[d]);
-        dv[iv] = from_f<T>(to_f(dv[iv]) + gv[d]);
+        dk[ik] = from_f<T>(((a.acc_mask & 2) ? to_f(dk[ik]) : 0.f) + a.scale * gk[d]);
+        dv[iv] = from_f<T>(((a.acc_mask & 4) ? to_f(dv[iv]) : 0.f) + gv[d]);
     }
 }
 
@@ -210,7 +210,7 @@ __global__ void __launch_bounds__(kT) k_attn_dq(Attn a, const T* dout, i64 ld_do
     if (!valid) return;
     for (int d = 0; d < hd; ++d) {
         i64 k = (b * a.S + i) * ld_dq + h * hd + d;
-        dq[k] = from_f<T>(to_f(dq[k]) + a.scale * gq[d]);
+        dq[k] = from_f<T>(((a.acc_mask & 1) ? to_f(dq[k]) : 0.f) + a.scale * gq[d]);
     }
 }
 

@@ -316,7 +316,8 @@ __global__ void __launch_bounds__(128) k_fa_dkdv(Attn a, MaskRef mk, const bf16*
             long long row = b * a.S + j0 + 8 * r;
             __nv_bfloat162* pk = (__nv_bfloat162*)(dk + row * ld_dk + h * D + n * 8 + 2 * t);
             __nv_bfloat162* pv = (__nv_bfloat162*)(dv + row * ld_dv + h * D + n * 8 + 2 * t);
-            float2 ok = __bfloat1622float2(*pk), ov = __bfloat1622float2(*pv);
+            float2 ok = (a.acc_mask & 2) ? __bfloat1622float2(*pk) : make_float2(0.f, 0.f);
+            float2 ov = (a.acc_mask & 4) ? __bfloat1622float2(*pv) : make_float2(0.f, 0.f);
             *pk = __floats2bfloat162_rn(ok.x + a.scale * gk[n][2 * r], ok.y + a.scale * gk[n][2 * r + 1]);
             *pv = __floats2bfloat162_rn(ov.x + gv[n][2 * r], ov.y + gv[n][2 * r + 1]);
         }
@@ -392,7 +393,7 @@ __global__ void __launch_bounds__(128) k_fa_dq(Attn a, MaskRef mk, const bf16* d
 #pragma unroll
         for (int r = 0; r < 2; ++r) {
             __nv_bfloat162* p = (__nv_bfloat162*)(dq + (b * a.S + i0 + 8 * r) * ld_dq + h * D + n * 8 + 2 * t);
-            float2 ov = __bfloat1622float2(*p);
+            float2 ov = (a.acc_mask & 1) ? __bfloat1622float2(*p) : make_float2(0.f, 0.f);
             *p = __floats2bfloat162_rn(ov.x + a.scale * gq[n][2 * r], ov.y + a.scale * gq[n][2 * r + 1]);
         }
     }

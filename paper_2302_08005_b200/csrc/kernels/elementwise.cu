@@ -401,22 +401,22 @@ __global__ void k_bias_partial(const T* g, i64 ld, i64 rows, i64 cols, float* pa
     for (i64 r = r0; r < r1; ++r) acc += to_f(g[r * ld + c]);
     part[(i64)blockIdx.y * cols + c] = acc;
 }
-__global__ void k_bias_final(const float* part, i64 chunks, i64 cols, float* db) {
+__global__ void k_bias_final(const float* part, i64 chunks, i64 cols, float* db, bool accum) {
     i64 c = blockIdx.x * (i64)blockDim.x + threadIdx.x;
     if (c >= cols) return;
     float acc = 0.f;
     for (i64 k = 0; k < chunks; ++k) acc += part[k * cols + c];
-    db[c] += acc;
+    db[c] = accum ? db[c] + acc : acc;
 }
 size_t bias_grad_workspace(i64 rows, i64 cols) { return (size_t)((rows + kBiasChunk - 1) / kBiasChunk) * cols * 4; }
-void bias_grad(const void* g, DT tg, i64 ld, i64 rows, i64 cols, float* db, float* ws, cudaStream_t s) {
+void bias_grad(const void* g, DT tg, i64 ld, i64 rows, i64 cols, float* db, float* ws, cudaStream_t s, bool accum) {
     i64 chunks = (rows + kBiasChunk - 1) / kBiasChunk;
     dim3 grid((unsigned)((cols + 127) / 128), (unsigned)chunks);
     dispatch(tg, [&](auto* p) {
         using T = std::remove_pointer_t<decltype(p)>;
         k_bias_partial<T><<<grid, 128, 0, s>>>((const T*)g, ld, rows, cols, ws);
     });
-    k_bias_final<<<(unsigned)((cols + 255) / 256), 256, 0, s>>>(ws, chunks, cols, db);
+    k_bias_final<<<(unsigned)((cols + 255) / 256), 256, 0, s>>>(ws, chunks, cols, db, accum);
     SBK_CHECK_LAUNCH();
 }
 

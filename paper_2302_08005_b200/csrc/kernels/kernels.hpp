@@ -99,7 +99,7 @@ void layernorm_fwd(const void* x, const void* gamma, const void* beta, DT tp, vo
 // gx += ...; dgamma/dbeta (+)= column sums (fp32) when non-null.
 void layernorm_bwd(const void* x, const float* mean, const float* rstd, const void* gamma, DT tp, const void* g,
                    DT tg, void* gx, float* dgamma, float* dbeta, DT t, i64 rows, i64 n, float* workspace,
-                   cudaStream_t s);
+                   cudaStream_t s, bool gx_acc = true, bool col_acc = true);
 size_t layernorm_bwd_workspace(i64 rows, i64 n);
 
 // Fused bias + dropout + residual + LayerNorm (the .fuse'd BERT output block):
@@ -112,11 +112,13 @@ void bias_dropout_residual_ln_fwd(const void* partial, const void* bias, const v
 void bias_dropout_residual_ln_bwd(const void* sum, const float* mean, const float* rstd, const void* gamma, DT tp,
                                   const void* g, void* g_res, void* g_partial, bool g_partial_accumulate,
                                   float* dbias, float* dgamma, float* dbeta, DT t, i64 rows, i64 n, u64 s1,
-                                  u64 thr, float dscale, float* workspace, cudaStream_t s);
+                                  u64 thr, float dscale, float* workspace, cudaStream_t s, bool gres_acc = true,
+                                  bool col_acc = true);
 size_t bdrln_bwd_workspace(i64 rows, i64 n);
 
 // column sums of g (rows x cols) into fp32 db (+=)
-void bias_grad(const void* g, DT tg, i64 ld, i64 rows, i64 cols, float* db, float* workspace, cudaStream_t s);
+void bias_grad(const void* g, DT tg, i64 ld, i64 rows, i64 cols, float* db, float* workspace, cudaStream_t s,
+               bool acc = true);
 size_t bias_grad_workspace(i64 rows, i64 cols);
 
 // ---------------------------------------------------------- embedding
@@ -151,6 +153,7 @@ struct Attn {
     float dscale = 1.f;
     DT t;
     const uint32_t* mask = nullptr;  // precomputed keep bits (dropout_mask); required by the tensor-core path
+    int acc_mask = 7;                // backward: bit0/1/2 = dq/dk/dv accumulate (else overwrite)
 };
 void attn_fwd(const Attn& a, cudaStream_t s);
 // dq/dk/dv accumulate (+=) with their own row strides; `delta` scratch (B,nh,S) fp32.

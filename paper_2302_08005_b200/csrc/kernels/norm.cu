@@ -20,7 +20,7 @@ bool bdrln_fwd_vec(const void* partial, const void* bias, const void* res, const
                    void* y, float* mean, float* rstd, DT t, i64 rows, i64 n, float eps, u64 s1, u64 thr, float dscale,
                    cudaStream_t s);
 bool ln_bwd_vec(int mode, const void* x, const float* mean, const float* rstd, const void* gamma, const void* g, void* gx,
-                void* gres, bool gx_acc, DT t, i64 rows, i64 n, u64 s1, u64 thr, float dscale, float* ws, int ncol,
+                void* gres, bool gx_acc, bool gres_acc, DT t, i64 rows, i64 n, u64 s1, u64 thr, float dscale, float* ws, int ncol,
                 int nblocks, cudaStream_t s);
 static int vec_blocks(i64 rows) { return (int)std::min<i64>(148, std::max<i64>(1, (rows + kWarps - 1) / kWarps)); }
 
@@ -145,7 +145,8 @@ void layernorm_fwd(const void* x, const void* gamma, const void* beta, DT tp, vo
 // 1 dbeta, 2 dbias) and are summed in block order by k_col_final.
 template <class T, class P, int MODE>  // MODE 0: LayerNorm, 1: bias+dropout+residual+LN
 __global__ void k_ln_bwd(const T* x, const float* mean, const float* rstd, const P* gamma, const T* g, T* gx, T* gres,
-                         bool gx_acc, i64 rows, i64 n, uint64_t s1, uint64_t thr, float dscale, float* ws, int ncol) {
+                         bool gx_acc, i64 rows, i64 n, uint64_t s1, uint64_t thr, float dscale, float* ws, int ncol,
+                         bool gres_acc) {
     extern __shared__ float sh[];  // [kWarps][ncol][n]
     int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
     float* mine = sh + (size_t)warp * ncol * n;
@@ -175,10 +176,10 @@ __global__ void k_ln_bwd(const T* x, const float* mean, const float* rstd, const
             float d = rs * (gh - a - xh * b);
             i64 k = row * n + i;
             if (MODE == 0) {
-                gx[k] = from_f<T>(to_f(gx[k]) + d);
+                gx[k] = from_f<T>(gx_acc ? to_f(gx[k]) + d : d);
             } else {
                 // residual branch gets g_sum; the dense branch gets dropout_bwd(g_sum)
-                gres[k] = from_f<T>(to_f(gres[k]) + d);
+                gres[k] = from_f<T>(gres_acc ? to_f(gres[k]) + d : d);
                 float gp = thr == 0 ? d : (d_keep(s1, (uint64_t)k, thr) ? d * dscale : 0.f);
                 gx[k] = from_f<T>(gx_acc ? to_f(gx[k]) + gp : gp);
                 if (ncol == 3) mine[2 * n + i] += gp;  // dbias
@@ -193,13 +194,13 @@ __global__ void k_ln_bwd(const T* x, const float* mean, const float* rstd, const
         ws[(i64)blockIdx.x * ncol * n + i] = acc;
     }
 }
-__global__ void k_col_final(const float* ws, int blocks, i64 ncoln, float* o0, float* o1, float* o2, i64 n) {
+__global__ void k_col_final(const float* ws, int blocks, i64 ncoln, float* o0, float* o1, float* o2, i64 n, bool accum) {
     for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < ncoln; i += (i64)gridDim.x * blockDim.x) {
         float acc = 0.f;
         for (int b = 0; b < blocks; ++b) acc += ws[(i64)b * ncoln + i];
         int k = (int)(i / n);
         float* o = k == 0 ? o0 : k == 1 ? o1 : o2;
-        if (o) o[i % n] += acc;
+        if (o) o[i % n] = accum ? o[i % n] + acc : acc;
     }
 }
 static int row_blocks(i64 rows) { return (int)std::min<i64>(kRowBlocks, std::max<i64>(1, (rows + kWarps - 1) / kWarps)); }
@@ -212,13 +213,14 @@ static void set_smem(K k, size_t bytes) {
 }
 
 void layernorm_bwd(const void* x, const float* mean, const float* rstd, const void* gamma, DT tp, const void* g, DT tg,
-                   void* gx, float* dgamma, float* dbeta, DT t, i64 rows, i64 n, float* ws, cudaStream_t s) {
+                   void* gx, float* dgamma, float* dbeta, DT t, i64 rows, i64 n, float* ws, cudaStream_t s, bool gx_acc,
+                   bool col_acc) {
     (void)tp;
     (void)tg;
     int ncol = (dgamma || dbeta) ? 2 : 0;
     int vb = vec_blocks(rows);
-    if (ln_bwd_vec(0, x, mean, rstd, gamma, g, gx, nullptr, true, t, rows, n, 0, 0, 1.f, ws, ncol, vb, s)) {
-        if (ncol) k_col_final<<<grid_for(2 * n, 256), 256, 0, s>>>(ws, vb, 2 * n, dgamma, dbeta, nullptr, n);
+    if (ln_bwd_vec(0, x, mean, rstd, gamma, g, gx, nullptr, gx_acc, true, t, rows, n, 0, 0, 1.f, ws, ncol, vb, s)) {
+        if (ncol) k_col_final<<<grid_for(2 * n, 256), 256, 0, s>>>(ws, vb, 2 * n, dgamma, dbeta, nullptr, n, col_acc);
         SBK_CHECK_LAUNCH();
         return;
     }
@@ -228,10 +230,10 @@ void layernorm_bwd(const void* x, const float* mean, const float* rstd, const vo
         using T = std::remove_pointer_t<decltype(p)>;
         auto k = k_ln_bwd<T, T, 0>;
         set_smem(k, smem);
-        k<<<nb, 32 * kWarps, smem, s>>>((const T*)x, mean, rstd, (const T*)gamma, (const T*)g, (T*)gx, nullptr, true, rows,
-                                        n, 0, 0, 1.f, ws, ncol);
+        k<<<nb, 32 * kWarps, smem, s>>>((const T*)x, mean, rstd, (const T*)gamma, (const T*)g, (T*)gx, nullptr, gx_acc,
+                                        rows, n, 0, 0, 1.f, ws, ncol, true);
     });
-    if (ncol) k_col_final<<<grid_for(2 * n, 256), 256, 0, s>>>(ws, nb, 2 * n, dgamma, dbeta, nullptr, n);
+    if (ncol) k_col_final<<<grid_for(2 * n, 256), 256, 0, s>>>(ws, nb, 2 * n, dgamma, dbeta, nullptr, n, col_acc);
     SBK_CHECK_LAUNCH();
 }
 
@@ -281,13 +283,13 @@ void bias_dropout_residual_ln_fwd(const void* partial, const void* bias, const v
 void bias_dropout_residual_ln_bwd(const void* sum, const float* mean, const float* rstd, const void* gamma, DT tp,
                                   const void* g, void* g_res, void* g_partial, bool g_partial_acc, float* dbias,
                                   float* dgamma, float* dbeta, DT t, i64 rows, i64 n, u64 s1, u64 thr, float dscale,
-                                  float* ws, cudaStream_t s) {
+                                  float* ws, cudaStream_t s, bool gres_acc, bool col_acc) {
     (void)tp;
     int ncol = 3;
     int vb = vec_blocks(rows);
-    if (ln_bwd_vec(1, sum, mean, rstd, gamma, g, g_partial, g_res, g_partial_acc, t, rows, n, s1, thr, dscale, ws, ncol,
-                   vb, s)) {
-        k_col_final<<<grid_for(3 * n, 256), 256, 0, s>>>(ws, vb, 3 * n, dgamma, dbeta, dbias, n);
+    if (ln_bwd_vec(1, sum, mean, rstd, gamma, g, g_partial, g_res, g_partial_acc, gres_acc, t, rows, n, s1, thr, dscale,
+                   ws, ncol, vb, s)) {
+        k_col_final<<<grid_for(3 * n, 256), 256, 0, s>>>(ws, vb, 3 * n, dgamma, dbeta, dbias, n, col_acc);
         SBK_CHECK_LAUNCH();
         return;
     }
@@ -298,9 +300,9 @@ void bias_dropout_residual_ln_bwd(const void* sum, const float* mean, const floa
         auto k = k_ln_bwd<T, T, 1>;
         set_smem(k, smem);
         k<<<nb, 32 * kWarps, smem, s>>>((const T*)sum, mean, rstd, (const T*)gamma, (const T*)g, (T*)g_partial, (T*)g_res,
-                                        g_partial_acc, rows, n, s1, thr, dscale, ws, ncol);
+                                        g_partial_acc, rows, n, s1, thr, dscale, ws, ncol, gres_acc);
     });
-    k_col_final<<<grid_for(3 * n, 256), 256, 0, s>>>(ws, nb, 3 * n, dgamma, dbeta, dbias, n);
+    k_col_final<<<grid_for(3 * n, 256), 256, 0, s>>>(ws, nb, 3 * n, dgamma, dbeta, dbias, n, col_acc);
     SBK_CHECK_LAUNCH();
 }
 

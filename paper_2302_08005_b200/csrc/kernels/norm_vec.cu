@@ -159,7 +159,7 @@ __global__ void __launch_bounds__(32 * kW) k_bdrln_fwd_v(const T* partial, const
 template <class T, int CPL, int MODE>
 __global__ void __launch_bounds__(32 * kW, 1)
     k_ln_bwd_v(const T* x, const float* mean, const float* rstd, const T* gamma, const T* g, T* gx, T* gres, bool gx_acc,
-               i64 rows, int n, uint64_t s1, uint64_t thr, float dscale, float* ws, int ncol) {
+               i64 rows, int n, uint64_t s1, uint64_t thr, float dscale, float* ws, int ncol, bool gres_acc) {
     constexpr int VN = Vec<T>::N;
     extern __shared__ float sh[];  // [kW][ncol][n]
     int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
@@ -194,16 +194,16 @@ __global__ void __launch_bounds__(32 * kW, 1)
                 gv[c][e] = rs * (gh - a - xv[c][e] * b);  // d(sum) / dx
             }
         if (MODE == 0) {
-            float o[CPL][VN];
-            load_row<T, CPL>(gx + row * n, lane, o);
+            float o[CPL][VN] = {};
+            if (gx_acc) load_row<T, CPL>(gx + row * n, lane, o);
 #pragma unroll
             for (int c = 0; c < CPL; ++c)
 #pragma unroll
                 for (int e = 0; e < VN; ++e) o[c][e] += gv[c][e];
             store_row<T, CPL>(gx + row * n, lane, o);
         } else {
-            float o[CPL][VN];
-            load_row<T, CPL>(gres + row * n, lane, o);
+            float o[CPL][VN] = {};
+            if (gres_acc) load_row<T, CPL>(gres + row * n, lane, o);
 #pragma unroll
             for (int c = 0; c < CPL; ++c)
 #pragma unroll
@@ -307,7 +307,7 @@ bool bdrln_fwd_vec(const void* partial, const void* bias, const void* res, const
 // mode 0: LN backward into gx (+=); mode 1: bdrln backward. Writes ncol column
 // partials per block to ws (the caller finishes with the fixed-order column sum).
 bool ln_bwd_vec(int mode, const void* x, const float* mean, const float* rstd, const void* gamma, const void* g, void* gx,
-                void* gres, bool gx_acc, DT t, i64 rows, i64 n, u64 s1, u64 thr, float dscale, float* ws, int ncol,
+                void* gres, bool gx_acc, bool gres_acc, DT t, i64 rows, i64 n, u64 s1, u64 thr, float dscale, float* ws, int ncol,
                 int nblocks, cudaStream_t s) {
     for (const void* p : {x, g, (const void*)gx})
         if (!aligned16(p)) return false;
@@ -323,7 +323,8 @@ bool ln_bwd_vec(int mode, const void* x, const float* mean, const float* rstd, c
                 auto launch = [&](auto k) {
                     if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
                     k<<<nblocks, 32 * kW, smem, s>>>((const T*)x, mean, rstd, (const T*)gamma, (const T*)g, (T*)gx,
-                                                     (T*)gres, gx_acc, rows, (int)n, s1, thr, dscale, ws, ncol);
+                                                     (T*)gres, gx_acc, rows, (int)n, s1, thr, dscale, ws, ncol,
+                                                     gres_acc);
                 };
                 if (mode == 0) launch(k_ln_bwd_v<T, CPL, 0>);
                 else launch(k_ln_bwd_v<T, CPL, 1>);
