@@ -7,9 +7,10 @@
 //   forward  y  = x W^T : A K-major, B K-major
 //   dgrad    dx = g W   : A K-major, B MN-major
 //   wgrad    dW = g^T x : A MN-major, B MN-major, long K -> deterministic split-K
-// Persistent: one CTA per SM walks a static tile schedule. Warp roles (192
+// Persistent: one CTA per SM walks a static tile schedule. Warp roles (320
 // threads): warp 0 TMA producer, warp 1 TMEM allocator + single-thread MMA
-// issuer, warps 2-5 epilogue (TMEM lane quarter = warp % 4). Two TMEM
+// issuer, warps 2-9 epilogue (TMEM lane quarter = warp % 4, two warps per
+// quarter splitting the columns). Two TMEM
 // accumulators (2 x BN columns) let the epilogue of tile i overlap the MMAs of
 // tile i+1. mbarrier rings: STAGES {full, empty} between TMA and MMA, and
 // {tmem_full, tmem_empty} x 2 between MMA and epilogue.
@@ -81,6 +82,22 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// tanh.approx (one MUFU op): the bf16 epilogues do not need tanhf's accuracy
+__device__ __forceinline__ float tanh_fast(float x) {
+    float y;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float gelu_fast(float x) {
+    const float c = 0.7978845608028654f, a = 0.044715f;
+    return 0.5f * x * (1.f + tanh_fast(c * (x + a * x * x * x)));
+}
+__device__ __forceinline__ float gelu_grad_fast(float x) {
+    const float c = 0.7978845608028654f, a = 0.044715f;
+    float t = tanh_fast(c * (x + a * x * x * x));
+    return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * c * (1.f + 3.f * a * x * x);
+}
+
 struct Epi {
     void* C;
     long long ldc;
@@ -139,7 +156,7 @@ __device__ __forceinline__ void epilogue_chunk(const Epi& ep, int z, long long r
             ax[j] = w;
         }
 #pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = gelu_f(v[j]);
+        for (int j = 0; j < 32; ++j) v[j] = gelu_fast(v[j]);
     } else if (ep.gelu == 2) {
         const uint4* ax = (const uint4*)(ep.aux + row * ep.ldc + col);
 #pragma unroll
@@ -147,7 +164,7 @@ __device__ __forceinline__ void epilogue_chunk(const Epi& ep, int z, long long r
             uint4 w = ax[j];
             const bf16* e = (const bf16*)&w;
 #pragma unroll
-            for (int t = 0; t < 8; ++t) v[8 * j + t] *= gelu_grad_f(__bfloat162float(e[t]));
+            for (int t = 0; t < 8; ++t) v[8 * j + t] *= gelu_grad_fast(__bfloat162float(e[t]));
         }
     }
     if (ep.c_f32) {
@@ -185,7 +202,7 @@ __device__ __forceinline__ void epilogue_chunk(const Epi& ep, int z, long long r
 }
 
 template <int BN, int STAGES, bool A_MN, bool B_MN>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(320, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB, Epi ep, Sched sc) {
     constexpr int A_BYTES = BM * BK * 2, B_BYTES = BN * BK * 2, STAGE = A_BYTES + B_BYTES;
     constexpr uint32_t TCOLS = 2 * BN;  // two accumulators
@@ -208,7 +225,7 @@ __global__ void __launch_bounds__(192, 1)
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], 4);  // one arrival per epilogue warp
+            mbar_init(&tempty[a], 8);  // one arrival per epilogue warp
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -281,8 +298,10 @@ __global__ void __launch_bounds__(192, 1)
             }
         }
     } else {
-        // ---------------- epilogue: TMEM -> registers -> global
-        const int q = warp & 3;  // TMEM lane quarter this warp may access
+        // ---------------- epilogue: TMEM -> registers -> global. 8 warps: two per
+        // TMEM lane quarter (= warp % 4), splitting the 32-column chunks
+        const int q = warp & 3;
+        const int half = (warp - 2) / 4;
         int lt = 0;
         for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++lt) {
             const int acc = lt & 1;
@@ -292,7 +311,7 @@ __global__ void __launch_bounds__(192, 1)
             mbar_wait(&tfull[acc], (lt >> 1) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll 1
-            for (int c = 0; c < BN / 32; ++c) {
+            for (int c = half; c < BN / 32; c += 2) {
                 uint32_t r[32];
                 tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c * 32), r);
                 epilogue_chunk<BN>(ep, z, row, n0 + c * 32, r);
@@ -375,7 +394,7 @@ void launch(const CUtensorMap& ta, const CUtensorMap& tb, const Epi& ep, const S
     }
     if (!g_num_sms) cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, 0);
     int grid = std::min(sc.tiles(), g_num_sms);
-    k<<<grid, 192, smem, s>>>(ta, tb, ep, sc);
+    k<<<grid, 320, smem, s>>>(ta, tb, ep, sc);
 }
 
 bool g_tc_disabled = false;
