@@ -84,6 +84,11 @@ int sb_nccl_unique_id(void* out128);
 int sb_executor_create_nccl(const sb_model* m, int train, uint64_t seed, int world, int rank, const void* unique_id128,
                             int dtype, int fused, sb_executor** out);
 int sb_executor_free(sb_executor* e);
+/* Host-only lowering of `rank`'s device plan (no GPU needed): JSON with op
+ * kinds, checkpoint regions, the activation ledger (ActivationLedger rule,
+ * proj/include/slapo/executor.hpp:20-25) and forward collective count. */
+int sb_plan_describe(const sb_model* m, int train, uint64_t seed, int world, int rank, int dtype, int fused, char* buf,
+                     size_t cap);
 int sb_executor_set_nan_guard(sb_executor* e, int on);
 /* Executor::forward (inputs replicated to every rank) */
 int sb_executor_forward(sb_executor* e, const double* const* inputs, int n_inputs);

@@ -480,6 +480,20 @@ class Executor:
         return v.value
 
 
+_lib.sb_plan_describe.argtypes = [_P, _c.c_int, _u64, _c.c_int, _c.c_int, _c.c_int, _c.c_int, _c.c_char_p, _c.c_size_t]
+_lib.sb_plan_describe.restype = _c.c_int
+
+
+def plan_summary(model: Model, mode: str = "train", seed: int = 0, world: int = 1, rank: int = 0,
+                 dtype: str = "fp32", fused: bool = True) -> dict:
+    """Host-only lowering of one rank's device plan (no GPU): op kinds,
+    checkpoint regions, activation ledger, forward collective count."""
+    buf = _c.create_string_buffer(1 << 20)
+    _check(_lib.sb_plan_describe(model._h, 1 if mode == "train" else 0, seed, world, rank, _DTYPES[dtype], int(fused),
+                                 buf, 1 << 20))
+    return json.loads(buf.value.decode())
+
+
 def nccl_unique_id() -> bytes:
     buf = _c.create_string_buffer(128)
     _check(_lib.sb_nccl_unique_id(buf))

@@ -267,6 +267,41 @@ int sb_executor_create_nccl(const sb_model* m, int train, uint64_t seed, int wor
         *out = e;
     });
 }
+// Host-only lowering (no device): the per-rank plan summary as JSON.
+int sb_plan_describe(const sb_model* m, int train, uint64_t seed, int world, int rank, int dtype, int fused, char* buf,
+                     size_t cap) {
+    return guard([&] {
+        LowerOptions lo;
+        lo.rank = rank;
+        lo.world = world;
+        lo.train = train != 0;
+        lo.seed = seed;
+        lo.cdt = dt_of(dtype);
+        lo.fused_kernels = fused != 0;
+        Plan P = lower(m->m, lo);
+        std::map<std::string, int> kinds;
+        int folded = 0, bias_on = 0;
+        for (auto& op : P.fwd) {
+            kinds[k_str(op.k)]++;
+            folded += op.dgelu_fused;
+            bias_on += op.has_bias && op.bias_on;
+        }
+        std::ostringstream o;
+        o << "{\"ops\": " << P.fwd.size() << ", \"regions\": " << P.regions.size() << ", \"ledger_bytes\": "
+          << P.ledger_bytes << ", \"collectives_fwd\": " << P.collectives_fwd << ", \"gelu_folded\": " << folded
+          << ", \"bias_added\": " << bias_on << ", \"params\": " << P.params.size() << ", \"structure\": \""
+          << P.structure() << "\", \"kinds\": {";
+        bool first = true;
+        for (auto& [k, c] : kinds) {
+            o << (first ? "" : ", ") << "\"" << k << "\": " << c;
+            first = false;
+        }
+        o << "}}";
+        std::string s = o.str();
+        if (cap < s.size() + 1) throw Error("buffer too small");
+        std::memcpy(buf, s.c_str(), s.size() + 1);
+    });
+}
 int sb_executor_free(sb_executor* e) {
     if (e && e->dloss) cudaFree(e->dloss);
     delete e;
