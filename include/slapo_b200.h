@@ -131,6 +131,10 @@ int sb_gemm(const void* A, int ta, int64_t sAb, int64_t sAm, int64_t sAk, const 
             int64_t N, int64_t K, float alpha, int accumulate, const void* bias, int epilogue, void* aux, void* stream);
 int sb_gemm_engine(void);                /* engine of the last sb_gemm: 0 SIMT, 1 tcgen05 */
 int sb_gemm_force_simt(int on);
+/* attention engine cap: 0 best available (tcgen05 > mma.sync > SIMT), 1 at most mma.sync, 2 SIMT;
+ * sb_attn_engine(bwd) = engine of the last forward (0) / backward (1) call: 3 tcgen05, 2 mma.sync, 1 SIMT */
+int sb_attn_set_engine(int max_engine);
+int sb_attn_engine(int bwd);
 /* scratch the tcgen05 path may use for deterministic split-K (wgrad) */
 int sb_gemm_set_workspace(void* ws, size_t bytes);
 /* dropout keep mask (apply_dropout, proj/src/executor.cpp:793-806): bit i of word i/32 =

@@ -484,6 +484,11 @@ int sb_gemm_force_simt(int on) {
     sbk::gemm_force_simt(on != 0);
     return 0;
 }
+int sb_attn_set_engine(int max_engine) {
+    sbk::attn_set_engine(max_engine);
+    return 0;
+}
+int sb_attn_engine(int bwd) { return sbk::attn_last_engine(bwd); }
 int sb_dropout_mask(uint32_t* bits, int64_t n, uint64_t exec_seed, uint64_t node_seed, double p, void* stream) {
     return guard([&] {
         u64 s1 = hash_combine(hash_combine(exec_seed, node_seed), 0xd0);

@@ -14,7 +14,8 @@
 
 namespace sbk {
 
-bool attn_fwd_tc_try(const Attn& a, cudaStream_t s);  // attention_tc.cu
+bool attn_fwd_tc_try(const Attn& a, cudaStream_t s);  // attention_tc.cu (mma.sync)
+bool attn_fwd_sm100_try(const Attn& a, cudaStream_t s);  // attention_sm100.cu (tcgen05)
 bool attn_bwd_tc_try(const Attn& a, const void* dout, i64 ld_do, void* dq, void* dk, void* dv, i64 ld_dq, i64 ld_dk,
                      i64 ld_dv, float* delta, cudaStream_t s);
 
@@ -229,10 +230,23 @@ void smem_attr(K k, size_t bytes) {
 }
 }  // namespace
 
-bool g_attn_force_simt = false;
+// engine selection: 0 = best available, 1 = at most mma.sync, 2 = SIMT only
+int g_attn_max_engine = 0;
+int g_attn_last_fwd = -1, g_attn_last_bwd = -1;  // 3 tcgen05, 2 mma.sync, 1 SIMT
+
+void attn_set_engine(int e) { g_attn_max_engine = e; }
+int attn_last_engine(int bwd) { return bwd ? g_attn_last_bwd : g_attn_last_fwd; }
 
 void attn_fwd(const Attn& a, cudaStream_t s) {
-    if (!g_attn_force_simt && attn_fwd_tc_try(a, s)) return;
+    if (g_attn_max_engine == 0 && attn_fwd_sm100_try(a, s)) {
+        g_attn_last_fwd = 3;
+        return;
+    }
+    if (g_attn_max_engine <= 1 && attn_fwd_tc_try(a, s)) {
+        g_attn_last_fwd = 2;
+        return;
+    }
+    g_attn_last_fwd = 1;
     dim3 grid((unsigned)((a.S + kT - 1) / kT), (unsigned)a.nh, (unsigned)a.B);
     dispatch(a.t, [&](auto* p) {
         using T = std::remove_pointer_t<decltype(p)>;
@@ -253,7 +267,11 @@ void attn_fwd(const Attn& a, cudaStream_t s) {
 
 void attn_bwd(const Attn& a, const void* dout, i64 ld_do, void* dq, void* dk, void* dv, i64 ld_dq, i64 ld_dk, i64 ld_dv,
               float* delta, cudaStream_t s) {
-    if (!g_attn_force_simt && attn_bwd_tc_try(a, dout, ld_do, dq, dk, dv, ld_dq, ld_dk, ld_dv, delta, s)) return;
+    if (g_attn_max_engine <= 1 && attn_bwd_tc_try(a, dout, ld_do, dq, dk, dv, ld_dq, ld_dk, ld_dv, delta, s)) {
+        g_attn_last_bwd = 2;
+        return;
+    }
+    g_attn_last_bwd = 1;
     dim3 grid((unsigned)((a.S + kT - 1) / kT), (unsigned)a.nh, (unsigned)a.B);
     dispatch(a.t, [&](auto* p) {
         using T = std::remove_pointer_t<decltype(p)>;

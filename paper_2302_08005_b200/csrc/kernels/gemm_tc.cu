@@ -19,7 +19,7 @@
 
 #include <mutex>
 
-#include "common.cuh"
+#include "tc5.cuh"
 
 namespace sbk {
 
@@ -402,6 +402,10 @@ bool g_tc_disabled = false;
 }  // namespace
 
 void gemm_tc_disable(bool off) { g_tc_disabled = off; }
+
+bool tc5::make_map_bf16(CUtensorMap* m, const void* base, long long inner, long long outer, long long ld, int box_outer) {
+    return make_map(m, base, inner, outer, ld, box_outer);
+}
 
 bool gemm_tc_try(const Gemm& g, cudaStream_t s) {
     if (g_tc_disabled) return false;

@@ -156,6 +156,9 @@ struct Attn {
     int acc_mask = 7;                // backward: bit0/1/2 = dq/dk/dv accumulate (else overwrite)
 };
 void attn_fwd(const Attn& a, cudaStream_t s);
+// 0 = best available (tcgen05 > mma.sync > SIMT), 1 = at most mma.sync, 2 = SIMT only
+void attn_set_engine(int e);
+int attn_last_engine(int bwd);  // engine of the last fwd/bwd call: 3 tcgen05, 2 mma.sync, 1 SIMT
 // dq/dk/dv accumulate (+=) with their own row strides; `delta` scratch (B,nh,S) fp32.
 void attn_bwd(const Attn& a, const void* dout, i64 ld_do, void* dq, void* dk, void* dv, i64 ld_dq, i64 ld_dk,
               i64 ld_dv, float* delta, cudaStream_t s);

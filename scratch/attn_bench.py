@@ -24,3 +24,8 @@ def t(f, it=10):
 unit = 2 * B * nh * S * S * hd / 1e12  # one S-sized GEMM in TFLOP
 tm, tf, tb = t(mask), t(fwd), t(bwd)
 print(f"mask {tm:.3f} ms  fwd {tf:.3f} ms ({2*unit/tf*1e3:.0f} TF/s)  bwd {tb:.3f} ms ({7*unit/tb*1e3:.0f} TF/s executed, {5*unit/tb*1e3:.0f} model)")
+for eng in (0, 1):
+    L.sb_attn_set_engine(eng)
+    tf = t(fwd)
+    print(f"engine cap {eng}: used {L.sb_attn_engine(0)} fwd {tf:.3f} ms ({2*unit/tf*1e3:.0f} TF/s)")
+L.sb_attn_set_engine(0)

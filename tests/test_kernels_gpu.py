@@ -153,3 +153,66 @@ def test_flash_attention_tensor_core(B, S, nh, hd, p):
     torch.cuda.synchronize()
     for got, want in ((g[..., :H], qf.grad), (g[..., H:2 * H], kf.grad), (g[..., 2 * H:], vf.grad)):
         close(got, want.transpose(1, 2).reshape(B, S, H), 3e-2)
+
+
+L.sb_attn_set_engine.argtypes = [ctypes.c_int]
+L.sb_attn_engine.argtypes = [ctypes.c_int]
+
+
+def _attn_case(B, S, nh, hd, p, qscale=0.5, seed=0):
+    H = nh * hd
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    qkv = (torch.randn(B, S, 3 * H, device="cuda", generator=g) * 0.5).bfloat16()
+    qkv[..., :H] = (qkv[..., :H].float() * (qscale / 0.5)).bfloat16()
+    n = B * nh * S * S
+    bits = torch.zeros((n + 31) // 32, dtype=torch.int32, device="cuda")
+    if p > 0:
+        assert L.sb_dropout_mask(P(bits), n, 123, 1040, p, None) == 0
+    return qkv, bits
+
+
+def _attn_fwd(qkv, bits, B, S, nh, hd, p, engine):
+    H = nh * hd
+    o = torch.full((B, S, H), float("nan"), device="cuda", dtype=torch.bfloat16)
+    lse = torch.full((B * nh * S,), float("nan"), device="cuda")
+    L.sb_attn_set_engine(engine)
+    try:
+        rc = L.sb_attn_fwd(P(qkv[..., :H]), P(qkv[..., H:2 * H]), P(qkv[..., 2 * H:]), P(o), 3 * H, H, P(lse), B, S, nh,
+                           hd, hd ** -0.5, 123, 1040, p, 1, P(bits) if p > 0 else None, None)
+        assert rc == 0, L.sb_last_error()
+        torch.cuda.synchronize()
+        used = L.sb_attn_engine(0)
+    finally:
+        L.sb_attn_set_engine(0)
+    return o, lse, used
+
+
+def _attn_ref(qkv, bits, B, S, nh, hd, p):
+    H = nh * hd
+    q, k, v = (qkv[..., i * H:(i + 1) * H].float().reshape(B, S, nh, hd).transpose(1, 2) for i in range(3))
+    s = q @ k.transpose(-1, -2) * hd ** -0.5
+    lse = torch.logsumexp(s, -1).reshape(-1)
+    pr = torch.softmax(s, -1)
+    if p > 0:
+        n = B * nh * S * S
+        idx = torch.arange(n, device="cuda")
+        keep = ((bits[idx // 32] >> (idx % 32)) & 1).bool().reshape(B, nh, S, S)
+        pr = torch.where(keep, pr / (1 - p), torch.zeros_like(pr))
+    return (pr @ v).transpose(1, 2).reshape(B, S, H), lse
+
+
+@pytest.mark.parametrize("B,S,nh,hd,p,qscale", [(2, 128, 4, 64, 0.0, 0.5), (2, 256, 2, 64, 0.1, 0.5),
+                                                 (1, 384, 2, 64, 0.1, 0.5), (2, 512, 16, 64, 0.1, 0.5),
+                                                 (1, 512, 2, 64, 0.1, 4.0), (1, 1024, 2, 64, 0.0, 3.0)])
+def test_flash_attention_tcgen05_forward(B, S, nh, hd, p, qscale):
+    """tcgen05/TMEM forward (engine 3) vs a torch fp32 reference and vs the mma.sync kernel;
+    qscale > 1 makes logits large enough to exercise the lazy running-max rescale."""
+    qkv, bits = _attn_case(B, S, nh, hd, p, qscale)
+    o5, lse5, used = _attn_fwd(qkv, bits, B, S, nh, hd, p, 0)
+    assert used == 3, "tcgen05 attention path not taken"
+    ref, lse_ref = _attn_ref(qkv, bits, B, S, nh, hd, p)
+    close(o5, ref)
+    assert (lse5 - lse_ref).abs().max().item() < 2e-3 * max(1.0, lse_ref.abs().max().item())
+    o2, lse2, used2 = _attn_fwd(qkv, bits, B, S, nh, hd, p, 1)
+    assert used2 == 2
+    close(o5, o2.float(), 1e-2)
