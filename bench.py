@@ -161,6 +161,7 @@ def main():
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile", action="store_true", help="print the per-op-kind breakdown to stderr")
+    ap.add_argument("--p", type=float, default=CFG["p"], help="dropout probability (experiments only; the metric uses 0.1)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -176,7 +177,7 @@ def main():
     import paper_2302_08005_b200 as sb
     from paper_2302_08005_b200 import recipes
 
-    cfg = dict(CFG, layers=args.layers, batch=args.batch)
+    cfg = dict(CFG, layers=args.layers, batch=args.batch, p=args.p)
     dist = None
     uid = None
     if world > 1:

@@ -148,16 +148,25 @@ int sb_bias_dropout_residual_ln_fwd(const void* partial, const void* bias, const
                                     const void* beta, void* sum, void* y, float* mean, float* rstd, int dtype,
                                     int64_t rows, int64_t n, float eps, uint64_t exec_seed, uint64_t node_seed,
                                     double p, void* stream);
+/* attention keep bits in both layouts (S % 32 == 0): words [0, W) natural (bit e%32 of word e/32
+ * for element e = ((b*nh + h)*S + i)*S + j, exactly sb_dropout_mask's bits), words [W, 2W)
+ * transposed (element ((b*nh + h)*S + j)*S + i), W = B*nh*S*S/32 */
+int sb_attn_dropout_mask(uint32_t* bits, int64_t B, int64_t S, int64_t nh, uint64_t exec_seed, uint64_t node_seed,
+                         double p, void* stream);
 /* EfficientAttention forward/backward (library.cpp:9-34 semantics). keep_bits: the
- * sb_dropout_mask bits of the (B, nh, S, S) probabilities (required by the
- * tensor-core kernels when p > 0; NULL makes the portable kernel hash in place). */
+ * sb_attn_dropout_mask bits of the (B, nh, S, S) probabilities (required by the
+ * tensor-core kernels when p > 0; the forward and the mma.sync backward read the
+ * natural half, the tcgen05 backward the transposed half; NULL makes the portable
+ * kernel hash in place). workspace: sb_attn_bwd_workspace() bytes of device scratch. acc_mask:
+ * bit 0/1/2 = dq/dk/dv are accumulated into (+=), else overwritten. */
 int sb_attn_fwd(const void* q, const void* k, const void* v, void* o, int64_t ld_qkv, int64_t ld_o, float* lse,
                 int64_t B, int64_t S, int64_t nh, int64_t hd, float scale, uint64_t exec_seed, uint64_t node_seed,
                 double p, int dtype, const uint32_t* keep_bits, void* stream);
+size_t sb_attn_bwd_workspace(int64_t B, int64_t S, int64_t nh, int64_t hd);
 int sb_attn_bwd(const void* q, const void* k, const void* v, const void* o, int64_t ld_qkv, int64_t ld_o,
-                const float* lse, const void* dout, void* dq, void* dk, void* dv, float* delta, int64_t B, int64_t S,
+                const float* lse, const void* dout, void* dq, void* dk, void* dv, void* workspace, int64_t B, int64_t S,
                 int64_t nh, int64_t hd, float scale, uint64_t exec_seed, uint64_t node_seed, double p, int dtype,
-                const uint32_t* keep_bits, void* stream);
+                const uint32_t* keep_bits, int acc_mask, void* stream);
 
 #ifdef __cplusplus
 }

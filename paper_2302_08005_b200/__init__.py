@@ -109,9 +109,15 @@ for _n, _a in {
                              _c.POINTER(_c.c_float)),
     "sb_gemm_force_simt": (_c.c_int,),
     "sb_dropout_mask": (_P, _i64, _u64, _u64, _c.c_double, _P),
+    "sb_attn_dropout_mask": (_P, _i64, _i64, _i64, _u64, _u64, _c.c_double, _P),
+    "sb_attn_set_engine": (_c.c_int,),
+    "sb_attn_engine": (_c.c_int,),
+    "sb_attn_bwd_workspace": (_i64, _i64, _i64, _i64),
 }.items():
     _sig(_n, *_a)
 _lib.sb_gemm_engine.restype = _c.c_int
+_lib.sb_attn_engine.restype = _c.c_int
+_lib.sb_attn_bwd_workspace.restype = _c.c_size_t
 
 
 class SlapoError(RuntimeError):

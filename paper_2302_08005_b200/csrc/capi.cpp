@@ -489,6 +489,14 @@ int sb_attn_set_engine(int max_engine) {
     return 0;
 }
 int sb_attn_engine(int bwd) { return sbk::attn_last_engine(bwd); }
+int sb_attn_dropout_mask(uint32_t* bits, int64_t B, int64_t S, int64_t nh, uint64_t exec_seed, uint64_t node_seed,
+                         double p, void* stream) {
+    return guard([&] {
+        u64 s1 = hash_combine(hash_combine(exec_seed, node_seed), 0xd0);
+        sbk::dropout_mask_dual(bits, B * nh, S, s1, dropout_threshold(p), (cudaStream_t)stream);
+    });
+}
+size_t sb_attn_bwd_workspace(int64_t B, int64_t S, int64_t nh, int64_t hd) { return sbk::attn_bwd_workspace(B, S, nh, hd); }
 int sb_dropout_mask(uint32_t* bits, int64_t n, uint64_t exec_seed, uint64_t node_seed, double p, void* stream) {
     return guard([&] {
         u64 s1 = hash_combine(hash_combine(exec_seed, node_seed), 0xd0);
@@ -543,12 +551,15 @@ int sb_attn_fwd(const void* q, const void* k, const void* v, void* o, int64_t ld
     });
 }
 int sb_attn_bwd(const void* q, const void* k, const void* v, const void* o, int64_t ld_qkv, int64_t ld_o, const float* lse,
-                const void* dout, void* dq, void* dk, void* dv, float* delta, int64_t B, int64_t S, int64_t nh, int64_t hd,
-                float scale, uint64_t es, uint64_t ns, double p, int dtype, const uint32_t* keep_bits, void* stream) {
+                const void* dout, void* dq, void* dk, void* dv, void* workspace, int64_t B, int64_t S, int64_t nh, int64_t hd,
+                float scale, uint64_t es, uint64_t ns, double p, int dtype, const uint32_t* keep_bits, int acc_mask,
+                void* stream) {
     return guard([&] {
         sbk::Attn a = mk_attn(q, k, v, (void*)o, ld_qkv, ld_o, (float*)lse, B, S, nh, hd, scale, es, ns, p, dtype);
+        a.acc_mask = acc_mask;
         a.mask = keep_bits;
-        sbk::attn_bwd(a, dout, ld_o, dq, dk, dv, ld_qkv, ld_qkv, ld_qkv, delta, (cudaStream_t)stream);
+        a.mask_t = keep_bits && S % 32 == 0 ? keep_bits + (B * nh * S * S) / 32 : nullptr;
+        sbk::attn_bwd(a, dout, ld_o, dq, dk, dv, ld_qkv, ld_qkv, ld_qkv, workspace, (cudaStream_t)stream);
     });
 }
 

@@ -394,7 +394,11 @@ public:
                         ws = std::max(ws, sbk::bdrln_bwd_workspace(rows_of(op.out[0]), P.views[(size_t)op.out[0]].shape.back()));
                     break;
                 }
-                case K::FlashAttn: ws = std::max(ws, (size_t)P.views[(size_t)op.out[1]].numel() * 4); break;
+                case K::FlashAttn: {
+                    const auto& q = P.views[(size_t)op.in[0]];
+                    ws = std::max(ws, sbk::attn_bwd_workspace(q.shape[0], q.shape[1], op.nh, op.hd));
+                    break;
+                }
                 case K::Embedding:
                     ws = std::max(ws, sbk::embedding_bwd_workspace(P.views[(size_t)op.in[0]].numel(),
                                                                    P.views[(size_t)op.in[1]].shape[1]));
@@ -856,6 +860,7 @@ public:
         a.dscale = (float)(1.0 / (1.0 - op.p));
         a.t = cdt;
         a.mask = op.dropout ? (const uint32_t*)fp(r, op.out[2]) : nullptr;
+        if (a.mask && a.S % 32 == 0) a.mask_t = a.mask + (a.B * a.nh * a.S * a.S) / 32;
         return a;
     }
 
@@ -1189,7 +1194,7 @@ public:
                 V(r, op.in[1]).rowwise(rows, cols, lk, true);
                 V(r, op.in[2]).rowwise(rows, cols, lv, true);
                 sbk::attn_bwd(a, gp(r, op.out[0]), a.ld_o, gp(r, op.in[0]), gp(r, op.in[1]), gp(r, op.in[2]), lq, lk, lv,
-                              (float*)r.ws, stream);
+                              r.ws, stream);
                 break;
             }
             default: throw Error(std::string("internal: no backward launcher for ") + k_str(op.k));
@@ -1230,7 +1235,10 @@ public:
             for (auto& r : ranks) {
                 const Op& op = r.P.fwd[i];
                 sbk::Attn a = attn_args(r, op);
-                sbk::dropout_mask((uint32_t*)fp(r, op.out[2]), a.B * a.nh * a.S * a.S, op.s1, op.thr, mstream);
+                if (a.S % 32 == 0)
+                    sbk::dropout_mask_dual((uint32_t*)fp(r, op.out[2]), a.B * a.nh, a.S, op.s1, op.thr, mstream);
+                else
+                    sbk::dropout_mask((uint32_t*)fp(r, op.out[2]), a.B * a.nh * a.S * a.S, op.s1, op.thr, mstream);
             }
             CK(cudaEventRecord(mask_ev[i], mstream));
         }

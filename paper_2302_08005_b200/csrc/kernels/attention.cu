@@ -16,6 +16,9 @@ namespace sbk {
 
 bool attn_fwd_tc_try(const Attn& a, cudaStream_t s);  // attention_tc.cu (mma.sync)
 bool attn_fwd_sm100_try(const Attn& a, cudaStream_t s);  // attention_sm100.cu (tcgen05)
+bool attn_bwd_sm100_try(const Attn& a, const void* dout, i64 ld_do, void* dq, void* dk, void* dv, i64 ld_dq, i64 ld_dk,
+                        i64 ld_dv, void* ws, cudaStream_t s);
+size_t attn_bwd_sm100_workspace(i64 B, i64 S, i64 nh, i64 hd);
 bool attn_bwd_tc_try(const Attn& a, const void* dout, i64 ld_do, void* dq, void* dk, void* dv, i64 ld_dq, i64 ld_dk,
                      i64 ld_dv, float* delta, cudaStream_t s);
 
@@ -235,6 +238,10 @@ int g_attn_max_engine = 0;
 int g_attn_last_fwd = -1, g_attn_last_bwd = -1;  // 3 tcgen05, 2 mma.sync, 1 SIMT
 
 void attn_set_engine(int e) { g_attn_max_engine = e; }
+
+size_t attn_bwd_workspace(i64 B, i64 S, i64 nh, i64 hd) {
+    return std::max((size_t)(B * nh * S) * 4, attn_bwd_sm100_workspace(B, S, nh, hd));
+}
 int attn_last_engine(int bwd) { return bwd ? g_attn_last_bwd : g_attn_last_fwd; }
 
 void attn_fwd(const Attn& a, cudaStream_t s) {
@@ -266,7 +273,12 @@ void attn_fwd(const Attn& a, cudaStream_t s) {
 }
 
 void attn_bwd(const Attn& a, const void* dout, i64 ld_do, void* dq, void* dk, void* dv, i64 ld_dq, i64 ld_dk, i64 ld_dv,
-              float* delta, cudaStream_t s) {
+              void* ws, cudaStream_t s) {
+    float* delta = (float*)ws;
+    if (g_attn_max_engine == 0 && attn_bwd_sm100_try(a, dout, ld_do, dq, dk, dv, ld_dq, ld_dk, ld_dv, ws, s)) {
+        g_attn_last_bwd = 3;
+        return;
+    }
     if (g_attn_max_engine <= 1 && attn_bwd_tc_try(a, dout, ld_do, dq, dk, dv, ld_dq, ld_dk, ld_dv, delta, s)) {
         g_attn_last_bwd = 2;
         return;

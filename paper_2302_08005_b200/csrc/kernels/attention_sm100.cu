@@ -18,6 +18,10 @@
 // other tile's softmax runs. The running max is rescaled lazily (only when it
 // grows by more than 2^8), and O is touched only then; S(j+1)'s completion
 // implies PV(j)'s (tcgen05.commit tracks every earlier MMA), so no extra wait.
+#include <cstdlib>
+#include <cstdio>
+#include <cstring>
+
 #include "tc5.cuh"
 
 namespace sbk {
@@ -30,7 +34,7 @@ constexpr int FD = 64;    // head dim
 constexpr int FT = 128;   // rows per tile (queries / keys)
 constexpr int FNS = 3;    // K/V ring stages
 constexpr int F_TILE_BYTES = FT * FD * 2;  // 16 KB
-constexpr int F_SMEM = 1024 + 2 * F_TILE_BYTES + FNS * 2 * F_TILE_BYTES + 256;
+constexpr int F_SMEM = 1024 + 2 * F_TILE_BYTES + FNS * 2 * F_TILE_BYTES + FNS * 2 * 2048 + 256;
 
 struct FwdArgs {
     bf16* o;
@@ -44,13 +48,14 @@ struct FwdArgs {
 
 __global__ void __launch_bounds__(384, 1)
     k_fa5_fwd(const __grid_constant__ CUtensorMap tQ, const __grid_constant__ CUtensorMap tK,
-              const __grid_constant__ CUtensorMap tV, FwdArgs fa) {
+              const __grid_constant__ CUtensorMap tV, const __grid_constant__ CUtensorMap tM, FwdArgs fa) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint8_t* sQ = smem;                        // [2][FT][FD]
     uint8_t* sK = sQ + 2 * F_TILE_BYTES;       // [FNS][FT][FD]
     uint8_t* sV = sK + FNS * F_TILE_BYTES;     // [FNS][FT][FD]
-    uint64_t* bars = (uint64_t*)(sV + FNS * F_TILE_BYTES);
+    uint8_t* sM = sV + FNS * F_TILE_BYTES;      // [FNS][2 tiles][128 rows][4 words] keep bits
+    uint64_t* bars = (uint64_t*)(sM + FNS * 2 * 2048);
     uint64_t* q_full = bars;
     uint64_t* kv_full = q_full + 1;
     uint64_t* kv_empty = kv_full + FNS;
@@ -70,6 +75,7 @@ __global__ void __launch_bounds__(384, 1)
         tma_prefetch(&tQ);
         tma_prefetch(&tK);
         tma_prefetch(&tV);
+        if (fa.mask) tma_prefetch(&tM);
         mbar_init(q_full, 1);
         for (int s = 0; s < FNS; ++s) {
             mbar_init(&kv_full[s], 1);
@@ -97,9 +103,13 @@ __global__ void __launch_bounds__(384, 1)
             for (int j = 0; j < nj; ++j) {
                 const int s = j % FNS;
                 mbar_wait(&kv_empty[s], ((j / FNS) & 1) ^ 1);
-                mbar_expect_tx(&kv_full[s], 2 * F_TILE_BYTES);
+                mbar_expect_tx(&kv_full[s], 2 * F_TILE_BYTES + (fa.mask ? ntile * 2048 : 0));
                 tma_load_2d(sK + s * F_TILE_BYTES, &tK, &kv_full[s], h * FD, row_base + j * FT);
                 tma_load_2d(sV + s * F_TILE_BYTES, &tV, &kv_full[s], h * FD, row_base + j * FT);
+                if (fa.mask)  // keep bits of (query rows of each tile, key chunk j)
+                    for (int g = 0; g < ntile; ++g)
+                        tma_load_2d(sM + (s * 2 + g) * 2048, &tM, &kv_full[s], j * (FT / 32),
+                                    (b * fa.nh + h) * S + (tile0 + g) * FT);
             }
         }
     } else if (warp == 1) {
@@ -150,13 +160,13 @@ __global__ void __launch_bounds__(384, 1)
             const long long qi = (long long)(tile0 + g) * FT + row;
             const long long bh = (long long)b * fa.nh + h;
             const uint32_t t_row = tmem + ((uint32_t)(q * 32) << 16) + g * 256;
-            const uint4* mrow = fa.mask ? (const uint4*)(fa.mask + ((bh * S + qi) * S >> 5)) : nullptr;
             float m_used = 0.f, l = 0.f;
             for (int j = 0; j < nj; ++j) {
-                uint4 mw = make_uint4(~0u, ~0u, ~0u, ~0u);
-                if (mrow) mw = __ldg(mrow + j);
+                mbar_wait(&kv_full[j % FNS], (j / FNS) & 1);  // keep bits of chunk j landed
                 mbar_wait(&s_full[g], j & 1);
                 fence_after();
+                const uint4 mw = fa.mask ? *(const uint4*)(sM + ((j % FNS) * 2 + g) * 2048 + row * 16)
+                                         : make_uint4(~0u, ~0u, ~0u, ~0u);
                 if (j == 0) {  // first chunk: exact row max (one extra TMEM read of S)
                     float mx = -INFINITY;
 #pragma unroll
@@ -264,15 +274,496 @@ bool fwd_fits(const Attn& a) {
     return true;
 }
 
+// ------------------------------------------------------------------ backward
+// One CTA per (batch, head), sweeping key blocks j (outer) and query blocks i
+// (inner) — the reference's attention backward (executor.cpp:1257-1378) as the
+// flash-attention recurrence. Per (j, i):
+//   S^T  = K_j Q_i^T            (SS MMA, TMEM [0,128))
+//   dP^T = V_j dO_i^T           (SS MMA, TMEM [128,256))
+//   8 softmax warps (thread = key row, half the query columns each):
+//     P^T = exp2(S^T c - lse2_q), Z^T = keep/(1-p) P^T -> TMEM [448,512) (bf16 pairs),
+//     dS^T = P^T (keep/(1-p) dP^T - delta_q) -> shared memory (bf16, 128B swizzle, 2 buffers)
+//   dV_j += Z^T dO_i            (TS MMA, A from TMEM, TMEM [256,320))
+//   dK_j += dS^T Q_i            (SS MMA, dS^T read K-major, TMEM [320,384))
+//   dQ_ij = dS K_j              (SS MMA, the same dS^T bytes read MN-major, TMEM [384,448))
+// The MMA issue order per step is dV, dK, S/dP of the next step, dQ, so the
+// next softmax starts while dQ is computed. 4 dQ warps (thread = query row)
+// drain dQ_ij from TMEM and add it into this CTA's private fp32 accumulator
+// (j = 0 stores, the last j writes bf16): dQ needs no cross-CTA reduction, so
+// the backward is deterministic without atomics or inter-CTA waits. dK_j / dV_j
+// are drained by the softmax warps while block j+1 starts.
+// delta_q = dO_q . O_q and lse2 = lse * log2(e) come from k_fa5_prep.
+constexpr int B_STAGE = 2 * F_TILE_BYTES + 1024 + 2048;  // Q, dO, lse2[128], delta[128], keep bits [128][4]
+constexpr int B_SMEM = 1024 + 4 * F_TILE_BYTES + 2 * B_STAGE + 4 * F_TILE_BYTES + 12 * 2048 + 256;
+
+struct BwdArgs {
+    const float* lse2;
+    const float* delta;
+    float* dqacc;
+    const uint32_t* mask_t;
+    float dscale, c, scale;
+    bf16* dq;
+    bf16* dk;
+    bf16* dv;
+    long long ld_dq, ld_dk, ld_dv;
+    int S, nh, acc;
+    int dbg;  // debugging switches (SB_ATTN_DBG): 1 skip softmax math, 2 skip dQ accumulation, 4 skip MMAs
+    unsigned long long* ts;  // debugging timeline (SB_ATTN_TS): [role][event], CTA (0,0) only
+};
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+// delta = rowsum(dO * O) and lse2 = lse * log2(e); 8 threads per (b, h, query) row
+__global__ void k_fa5_prep(const bf16* dout, long long ld_do, const bf16* o, long long ld_o, const float* lse,
+                           float* lse2, float* delta, long long BH, int S, int nh) {
+    const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    const long long idx = tid >> 3;
+    const int part = (int)(tid & 7);
+    const bool ok = idx < BH * S;
+    float acc = 0.f;
+    if (ok) {
+        const long long bh = idx / S, q = idx % S, b = bh / nh, h = bh % nh;
+        const uint4 a = *((const uint4*)(dout + (b * S + q) * ld_do + h * FD) + part);
+        const uint4 c = *((const uint4*)(o + (b * S + q) * ld_o + h * FD) + part);
+        const __nv_bfloat162* pa = (const __nv_bfloat162*)&a;
+        const __nv_bfloat162* pc = (const __nv_bfloat162*)&c;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            float2 fa = __bfloat1622float2(pa[t]), fc = __bfloat1622float2(pc[t]);
+            acc = fmaf(fa.x, fc.x, fmaf(fa.y, fc.y, acc));
+        }
+    }
+    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+    if (ok && part == 0) {
+        delta[idx] = acc;
+        lse2[idx] = lse[idx] * 1.4426950408889634f;
+    }
+}
+
+__device__ __forceinline__ uint64_t desc_kmajor_2blk(uint32_t base, int kk) {
+    // K-major tile of 128 rows x 128 bf16 stored as two 64-column blocks of 16 KB
+    return sdesc(base + (kk >> 2) * 16384 + (kk & 3) * 32, 1, 1024 >> 4);
+}
+
+__device__ __forceinline__ void store_bf16x8(bf16* dst, const float (&f)[8], bool acc) {
+    float g[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) g[t] = f[t];
+    uint4* d = (uint4*)dst;
+    if (acc) {
+        uint4 old = *d;
+        const __nv_bfloat162* po = (const __nv_bfloat162*)&old;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            float2 x = __bfloat1622float2(po[t]);
+            g[2 * t] += x.x;
+            g[2 * t + 1] += x.y;
+        }
+    }
+    *d = make_uint4(pack_bf16(g[0], g[1]), pack_bf16(g[2], g[3]), pack_bf16(g[4], g[5]), pack_bf16(g[6], g[7]));
+}
+
+// A warp writes 32 rows (thread = row, 64 fp32 values each) as bf16 (x scale,
+// += the existing values when acc) with coalesced 128-byte rows: 8 rows at a
+// time go through a 2 KB fp32 staging buffer (16-byte units XOR-swizzled by
+// row), then each store instruction covers 4 full rows.
+__device__ __forceinline__ void warp_rows_out(float* stage, bf16* dst0, long long ld, const float (&f)[64], float sc,
+                                              bool acc, int lane) {
+    uint4* st4 = (uint4*)stage;
+    const int c = lane & 7;
+    // accumulate mode: the 8 old 16-byte chunks this lane will update, loaded up front (one latency)
+    uint4 old[8];
+    if (acc) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) old[q] = *(const uint4*)(dst0 + (long long)(q * 4 + (lane >> 3)) * ld + c * 8);
+    }
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+        if ((lane >> 3) == p) {
+            const int rr = lane & 7;
+#pragma unroll
+            for (int u = 0; u < 16; ++u)
+                st4[rr * 16 + (u ^ rr)] = make_uint4(__float_as_uint(f[4 * u]), __float_as_uint(f[4 * u + 1]),
+                                                     __float_as_uint(f[4 * u + 2]), __float_as_uint(f[4 * u + 3]));
+        }
+        __syncwarp();
+#pragma unroll
+        for (int it = 0; it < 2; ++it) {
+            const int rr = it * 4 + (lane >> 3);
+            const uint4 a = st4[rr * 16 + ((2 * c) ^ rr)], b = st4[rr * 16 + ((2 * c + 1) ^ rr)];
+            float g[8] = {__uint_as_float(a.x) * sc, __uint_as_float(a.y) * sc, __uint_as_float(a.z) * sc,
+                          __uint_as_float(a.w) * sc, __uint_as_float(b.x) * sc, __uint_as_float(b.y) * sc,
+                          __uint_as_float(b.z) * sc, __uint_as_float(b.w) * sc};
+            if (acc) {
+                const __nv_bfloat162* po = (const __nv_bfloat162*)&old[p * 2 + it];
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    float2 x = __bfloat1622float2(po[t]);
+                    g[2 * t] += x.x;
+                    g[2 * t + 1] += x.y;
+                }
+            }
+            *(uint4*)(dst0 + (long long)(p * 8 + rr) * ld + c * 8) =
+                make_uint4(pack_bf16(g[0], g[1]), pack_bf16(g[2], g[3]), pack_bf16(g[4], g[5]), pack_bf16(g[6], g[7]));
+        }
+        __syncwarp();
+    }
+}
+
+__global__ void __launch_bounds__(512, 1)
+    k_fa5_bwd(const __grid_constant__ CUtensorMap tK, const __grid_constant__ CUtensorMap tV,
+              const __grid_constant__ CUtensorMap tQ, const __grid_constant__ CUtensorMap tdO,
+              const __grid_constant__ CUtensorMap tM, BwdArgs ba) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint8_t* sKV = smem;                        // [2] x {K, V}
+    uint8_t* sStage = sKV + 4 * F_TILE_BYTES;   // [2][B_STAGE]
+    uint8_t* sDS = sStage + 2 * B_STAGE;        // [2] x dS^T [2 q-blocks][128 keys][64 q] bf16, swizzled
+    float* sOut = (float*)(sDS + 4 * F_TILE_BYTES);  // [12 warps][2 KB] output staging
+    uint64_t* bars = (uint64_t*)(sDS + 4 * F_TILE_BYTES + 12 * 2048);
+    uint64_t* kv_full = bars;        // [2]
+    uint64_t* kv_empty = bars + 2;   // [2]
+    uint64_t* st_full = bars + 4;    // [2]
+    uint64_t* st_empty = bars + 6;   // [2]
+    uint64_t* sdp_full = bars + 8;   // [2 query halves]
+    uint64_t* sm_done = bars + 10;   // [2 query halves]
+    uint64_t* dq_full = bars + 12;
+    uint64_t* dq_free = bars + 13;
+    uint64_t* acc_full = bars + 14;  // dK_j / dV_j complete
+    uint64_t* acc_free = bars + 15;  // dK_j / dV_j read out of TMEM
+    uint32_t* tslot = (uint32_t*)(bars + 16);
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int S = ba.S, nj = S / FT, nsteps = nj * nj;
+    const int h = blockIdx.x, b = blockIdx.y;
+    const long long bh = (long long)b * ba.nh + h;
+    const int row_base = b * S;
+
+    if (threadIdx.x == 0) {
+        tma_prefetch(&tK);
+        tma_prefetch(&tV);
+        tma_prefetch(&tQ);
+        tma_prefetch(&tdO);
+        if (ba.mask_t) tma_prefetch(&tM);
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&kv_full[s], 1);
+            mbar_init(&kv_empty[s], 1);
+            mbar_init(&st_full[s], 1);
+            mbar_init(&st_empty[s], 1);
+        }
+        for (int hh = 0; hh < 2; ++hh) {
+            mbar_init(&sdp_full[hh], 1);
+            mbar_init(&sm_done[hh], 8);
+        }
+        mbar_init(dq_full, 1);
+        mbar_init(dq_free, 4);
+        mbar_init(acc_full, 1);
+        mbar_init(acc_free, 8);
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc<512>(tslot);
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem = *tslot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ------------------------------------------------ TMA producer
+            for (int u = 0; u < nsteps; ++u) {
+                const int j = u / nj, i = u % nj;
+                if (i == 0) {
+                    const int kb = j & 1;
+                    mbar_wait(&kv_empty[kb], ((j >> 1) & 1) ^ 1);
+                    mbar_expect_tx(&kv_full[kb], 2 * F_TILE_BYTES);
+                    tma_load_2d(sKV + kb * 2 * F_TILE_BYTES, &tK, &kv_full[kb], h * FD, row_base + j * FT);
+                    tma_load_2d(sKV + kb * 2 * F_TILE_BYTES + F_TILE_BYTES, &tV, &kv_full[kb], h * FD,
+                                row_base + j * FT);
+                }
+                const int s = u & 1;
+                uint8_t* st = sStage + s * B_STAGE;
+                mbar_wait(&st_empty[s], ((u >> 1) & 1) ^ 1);
+                if (ba.ts && blockIdx.x == 0 && blockIdx.y == 0) ba.ts[0 * 64 + u] = gtime();
+                mbar_expect_tx(&st_full[s], 2 * F_TILE_BYTES + 1024 + (ba.mask_t ? 2048 : 0));
+                tma_load_2d(st, &tQ, &st_full[s], h * FD, row_base + i * FT);
+                tma_load_2d(st + F_TILE_BYTES, &tdO, &st_full[s], h * FD, row_base + i * FT);
+                bulk_load(st + 2 * F_TILE_BYTES, ba.lse2 + bh * S + i * FT, 512, &st_full[s]);
+                bulk_load(st + 2 * F_TILE_BYTES + 512, ba.delta + bh * S + i * FT, 512, &st_full[s]);
+                // transposed keep bits of (key rows of block j, query block i): [128 keys][4 words]
+                if (ba.mask_t)
+                    tma_load_2d(st + 2 * F_TILE_BYTES + 1024, &tM, &st_full[s], i * (FT / 32), (int)(bh * S) + j * FT);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            // ------------------------------------------------ MMA issuer
+            // Each step's 128 query columns are two halves: while the softmax
+            // warps work on half b of step u, the tensor pipe runs dV/dK of half
+            // a and S/dP of half a of step u+1, and vice versa.
+            constexpr uint32_t id_s = idesc_bf16(FT, FT / 2, false, false);
+            constexpr uint32_t id_kv = idesc_bf16(FT, FD, false, true);
+            constexpr uint32_t id_q = idesc_bf16(FT, FD, true, true);
+            const bool mm = !(ba.dbg & 4);
+            auto issue_sdp = [&](int u, int hh) {
+                const int j = u / nj, i = u % nj, s = u & 1, kb = j & 1;
+                const uint32_t aK = smem_u32(sKV + kb * 2 * F_TILE_BYTES), aV = aK + F_TILE_BYTES;
+                const uint32_t aQ = smem_u32(sStage + s * B_STAGE) + hh * (F_TILE_BYTES / 2), adO = aQ + F_TILE_BYTES;
+                if (hh == 0) {
+                    if (i == 0) mbar_wait(&kv_full[kb], (j >> 1) & 1);
+                    mbar_wait(&st_full[s], (u >> 1) & 1);
+                    fence_after();
+                }
+                if (mm) {
+#pragma unroll
+                    for (int kk = 0; kk < FD / 16; ++kk)  // S^T half = K Q_half^T
+                        mma_ss(tmem + hh * 64, desc_kmajor(aK, kk), desc_kmajor(aQ, kk), id_s, kk > 0);
+#pragma unroll
+                    for (int kk = 0; kk < FD / 16; ++kk)  // dP^T half = V dO_half^T
+                        mma_ss(tmem + 128 + hh * 64, desc_kmajor(aV, kk), desc_kmajor(adO, kk), id_s, kk > 0);
+                }
+                mma_commit(&sdp_full[hh]);
+            };
+            issue_sdp(0, 0);
+            issue_sdp(0, 1);
+            for (int u = 0; u < nsteps; ++u) {
+                const int j = u / nj, i = u % nj, s = u & 1, kb = j & 1;
+                const uint32_t aK = smem_u32(sKV + kb * 2 * F_TILE_BYTES);
+                const uint32_t aQ = smem_u32(sStage + s * B_STAGE), adO = aQ + F_TILE_BYTES;
+                const uint32_t aDS = smem_u32(sDS + (u & 1) * 2 * F_TILE_BYTES);
+#pragma unroll 1
+                for (int hh = 0; hh < 2; ++hh) {
+                    mbar_wait(&sm_done[hh], u & 1);
+                    if (hh == 0 && i == 0 && j > 0) mbar_wait(acc_free, (j - 1) & 1);  // dK/dV of block j-1 drained
+                    if (ba.ts && blockIdx.x == 0 && blockIdx.y == 0 && hh == 1) ba.ts[1 * 64 + u] = gtime();
+                    fence_after();
+                    if (mm) {
+#pragma unroll
+                        for (int k4 = 0; k4 < 4; ++k4) {  // dV += Z^T_half dO_half
+                            const int kk = hh * 4 + k4;
+                            mma_ts(tmem + 256, tmem + 448 + kk * 8, desc_mnmajor(adO, kk), id_kv, (i | kk) != 0);
+                        }
+#pragma unroll
+                        for (int k4 = 0; k4 < 4; ++k4) {  // dK += dS^T_half Q_half
+                            const int kk = hh * 4 + k4;
+                            mma_ss(tmem + 320, desc_kmajor_2blk(aDS, kk), desc_mnmajor(aQ, kk), id_kv, (i | kk) != 0);
+                        }
+                    }
+                    if (hh == 1) {
+                        mma_commit(&st_empty[s]);  // Q, dO, lse, delta, keep bits of this step are no longer read
+                        if (i == nj - 1) mma_commit(acc_full);
+                    }
+                    if (u + 1 < nsteps) issue_sdp(u + 1, hh);
+                }
+                if (ba.ts && blockIdx.x == 0 && blockIdx.y == 0) ba.ts[2 * 64 + u] = gtime();
+                if (u > 0) {
+                    mbar_wait(dq_free, (u - 1) & 1);  // dQ of the previous step has left TMEM
+                    fence_after();
+                }
+                if (ba.ts && blockIdx.x == 0 && blockIdx.y == 0) ba.ts[3 * 64 + u] = gtime();
+                if (mm) {
+#pragma unroll
+                    for (int kk = 0; kk < FT / 16; ++kk)  // dQ_ij = dS K
+                        mma_ss(tmem + 384, sdesc(aDS + kk * 2048, 16384 >> 4, 1024 >> 4), desc_mnmajor(aK, kk), id_q,
+                               kk > 0);
+                }
+                mma_commit(dq_full);
+                if (i == nj - 1) mma_commit(&kv_empty[kb]);  // K_j, V_j no longer read
+            }
+        }
+    } else if (warp >= 4 && warp < 12) {
+        // ------------------------------------------------------------------
+        // 8 softmax warps: quarter q4 = TMEM lanes (key rows), half hf = 64 of
+        // the 128 query columns
+        const int q4 = warp & 3, hf = (warp - 4) >> 2, k = q4 * 32 + lane;
+        const uint32_t t_lane = tmem + ((uint32_t)(q4 * 32) << 16);
+        // dK_j (hf 1) / dV_j (hf 0) -> global
+        float* my_stage = sOut + (warp - 4) * 512;
+        auto drain_kv = [&](int j) {
+            mbar_wait(acc_full, j & 1);
+            fence_after();
+            float f[64];
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+                uint32_t r[32];
+                tmem_ld32_nowait(t_lane + 256 + hf * 64 + hh * 32, r);
+                tmem_ld_wait();
+#pragma unroll
+                for (int e = 0; e < 32; ++e) f[hh * 32 + e] = __uint_as_float(r[e]);
+            }
+            fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(acc_free);
+            const long long kg0 = (long long)j * FT + q4 * 32;  // first key row of this warp
+            if (hf)
+                warp_rows_out(my_stage, ba.dk + (row_base + kg0) * ba.ld_dk + (long long)h * FD, ba.ld_dk, f, ba.scale,
+                              ba.acc & 2, lane);
+            else
+                warp_rows_out(my_stage, ba.dv + (row_base + kg0) * ba.ld_dv + (long long)h * FD, ba.ld_dv, f, 1.f,
+                              ba.acc & 4, lane);
+        };
+        const int g = hf;  // 32-column group of each query half
+        for (int u = 0; u < nsteps; ++u) {
+            const int j = u / nj, i = u % nj, s = u & 1;
+            if (i == 0 && j > 0) drain_kv(j - 1);  // TMEM dK/dV free before dV/dK of block j start
+            const float* lse_s = (const float*)(sStage + s * B_STAGE + 2 * F_TILE_BYTES);
+            const float* dl_s = lse_s + FT;
+            uint8_t* ds_buf = sDS + (u & 1) * 2 * F_TILE_BYTES;
+            mbar_wait(&st_full[s], (u >> 1) & 1);
+            const uint4 mw = ba.mask_t ? *(const uint4*)(sStage + s * B_STAGE + 2 * F_TILE_BYTES + 1024 + k * 16)
+                                       : make_uint4(~0u, ~0u, ~0u, ~0u);
+#pragma unroll 1
+            for (int hh = 0; hh < 2; ++hh) {
+                const int c = hh * 2 + g;  // 32-query chunk
+                mbar_wait(&sdp_full[hh], u & 1);
+                fence_after();
+                if (ba.ts && blockIdx.x == 0 && blockIdx.y == 0 && warp == 4 && lane == 0 && hh == 0)
+                    ba.ts[4 * 64 + u] = gtime();
+                if (!(ba.dbg & 1)) {
+                    uint32_t sv[32], dp[32];
+                    tmem_ld32_nowait(t_lane + c * 32, sv);
+                    tmem_ld32_nowait(t_lane + 128 + c * 32, dp);
+                    tmem_ld_wait();
+                    const uint32_t mword = c == 0 ? mw.x : c == 1 ? mw.y : c == 2 ? mw.z : mw.w;
+                    uint32_t zk[16], dk[16];
+#pragma unroll
+                    for (int e4 = 0; e4 < 8; ++e4) {
+                        const float4 l4 = *(const float4*)(lse_s + c * 32 + e4 * 4);
+                        const float4 d4 = *(const float4*)(dl_s + c * 32 + e4 * 4);
+                        const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dv[4] = {d4.x, d4.y, d4.z, d4.w};
+                        float z[4], ds[4];
+#pragma unroll
+                        for (int e1 = 0; e1 < 4; ++e1) {
+                            const int e = e4 * 4 + e1;
+                            const float p = ex2f(fmaf(__uint_as_float(sv[e]), ba.c, -lv[e1]));
+                            const float kd = ((mword >> e) & 1) ? ba.dscale : 0.f;
+                            z[e1] = p * kd;
+                            ds[e1] = p * fmaf(kd, __uint_as_float(dp[e]), -dv[e1]);
+                        }
+                        zk[2 * e4] = pack_bf16(z[0], z[1]);
+                        zk[2 * e4 + 1] = pack_bf16(z[2], z[3]);
+                        dk[2 * e4] = pack_bf16(ds[0], ds[1]);
+                        dk[2 * e4 + 1] = pack_bf16(ds[2], ds[3]);
+                    }
+                    tmem_st16(t_lane + 448 + c * 16, zk);
+                    // dS^T row k, queries c*32..c*32+31: q-block c/2 (= hh), 16-byte chunks (c%2)*4 + v
+                    uint8_t* rowp = ds_buf + hh * 16384 + k * 128;
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) {
+                        const int ch = ((c & 1) * 4 + v) ^ (k & 7);
+                        *(uint4*)(rowp + ch * 16) = make_uint4(dk[4 * v], dk[4 * v + 1], dk[4 * v + 2], dk[4 * v + 3]);
+                    }
+                    tmem_st_wait();
+                }
+                fence_proxy_async();
+                fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&sm_done[hh]);
+            }
+            if (ba.ts && blockIdx.x == 0 && blockIdx.y == 0 && warp == 4 && lane == 0) ba.ts[5 * 64 + u] = gtime();
+        }
+        drain_kv(nj - 1);
+    } else if (warp >= 12) {
+        // ---------------------------------------------------- dQ warps (thread = query row)
+        const int q4 = warp & 3, r = q4 * 32 + lane;
+        const uint32_t t_row = tmem + ((uint32_t)(q4 * 32) << 16) + 384;
+        for (int u = 0; u < nsteps; ++u) {
+            const int j = u / nj, i = u % nj;
+            // private fp32 accumulator, thread-major: float4 v of query row r of
+            // block i at ((bh*nj + i)*16 + v)*128 + r, so a warp's accesses coalesce
+            float4* acc = (float4*)ba.dqacc + ((bh * nj + i) * 16) * FT + r;
+            float f[64];
+            if (j > 0 && !(ba.dbg & 2)) {  // this thread's own partial sum (written by it at step u - nj)
+#pragma unroll
+                for (int v = 0; v < 16; ++v) {
+                    const float4 a4 = __ldcg(acc + v * FT);
+                    f[4 * v] = a4.x;
+                    f[4 * v + 1] = a4.y;
+                    f[4 * v + 2] = a4.z;
+                    f[4 * v + 3] = a4.w;
+                }
+            } else {
+#pragma unroll
+                for (int e = 0; e < 64; ++e) f[e] = 0.f;
+            }
+            mbar_wait(dq_full, u & 1);
+            fence_after();
+            if (ba.ts && blockIdx.x == 0 && blockIdx.y == 0 && warp == 12 && lane == 0) ba.ts[6 * 64 + u] = gtime();
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+                uint32_t d[32];
+                tmem_ld32_nowait(t_row + hh * 32, d);
+                tmem_ld_wait();
+#pragma unroll
+                for (int e = 0; e < 32; ++e) f[hh * 32 + e] += __uint_as_float(d[e]);
+            }
+            fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(dq_free);
+            if (ba.dbg & 2) continue;
+            if (j == nj - 1) {
+                const long long q0 = (long long)i * FT + q4 * 32;  // first query row of this warp
+                warp_rows_out(sOut + (8 + q4) * 512, ba.dq + (row_base + q0) * ba.ld_dq + (long long)h * FD, ba.ld_dq,
+                              f, ba.scale, ba.acc & 1, lane);
+            } else {
+#pragma unroll
+                for (int v = 0; v < 16; ++v)
+                    __stcg(acc + v * FT, make_float4(f[4 * v], f[4 * v + 1], f[4 * v + 2], f[4 * v + 3]));
+            }
+        }
+    }
+    fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        fence_after();
+        tmem_dealloc<512>(tmem);
+    }
+}
+
+bool bwd_fits(const Attn& a, const void* dout, i64 ld_do, i64 ld_dq, i64 ld_dk, i64 ld_dv) {
+    if (!fwd_fits(a)) return false;
+    if (a.thr && !a.mask_t) return false;
+    auto al = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
+    if (!al(dout) || ld_do % 8 || ld_dq % 8 || ld_dk % 8 || ld_dv % 8) return false;
+    return true;
+}
+
+struct BwdWs {
+    float* lse2;
+    float* delta;
+    float* dqacc;
+};
+size_t carve(const Attn& a, void* base, BwdWs* w) {
+    const size_t rows = (size_t)(a.B * a.nh * a.S);
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        size_t o = off;
+        off += (bytes + 255) & ~(size_t)255;
+        return o;
+    };
+    size_t o_l = take(rows * 4), o_d = take(rows * 4), o_q = take(rows * FD * 4);
+    if (w) {
+        char* c = (char*)base;
+        *w = BwdWs{(float*)(c + o_l), (float*)(c + o_d), (float*)(c + o_q)};
+    }
+    return off;
+}
+
 }  // namespace
 
 bool attn_fwd_sm100_try(const Attn& a, cudaStream_t s) {
     if (!fwd_fits(a)) return false;
-    CUtensorMap tq, tk, tv;
+    CUtensorMap tq, tk, tv, tm;
     const long long rows = a.B * a.S, cols = a.nh * FD;
     if (!make_map_bf16(&tq, a.q, cols, rows, a.ld_q, FT) || !make_map_bf16(&tk, a.k, cols, rows, a.ld_k, FT) ||
         !make_map_bf16(&tv, a.v, cols, rows, a.ld_v, FT))
         return false;
+    memset(&tm, 0, sizeof(tm));
+    if (a.thr && !make_map_u32(&tm, a.mask, a.S / 32, a.B * a.nh * a.S, a.S / 32, FT / 32, FT)) return false;
     FwdArgs fa{(bf16*)a.o, a.ld_o, a.lse, a.thr ? a.mask : nullptr, a.thr ? a.dscale : 1.f,
                a.scale * 1.4426950408889634f, (int)a.S, (int)a.nh};
     static bool attr = false;
@@ -281,8 +772,73 @@ bool attn_fwd_sm100_try(const Attn& a, cudaStream_t s) {
         attr = true;
     }
     dim3 grid((unsigned)((a.S / FT + 1) / 2), (unsigned)a.nh, (unsigned)a.B);
-    k_fa5_fwd<<<grid, 384, F_SMEM, s>>>(tq, tk, tv, fa);
+    k_fa5_fwd<<<grid, 384, F_SMEM, s>>>(tq, tk, tv, tm, fa);
     SBK_CHECK_LAUNCH();
+    return true;
+}
+
+}  // namespace sbk
+
+namespace sbk {
+
+size_t attn_bwd_sm100_workspace(i64 B, i64 S, i64 nh, i64 hd) {
+    Attn a;
+    a.B = B;
+    a.S = S;
+    a.nh = nh;
+    a.hd = hd;
+    return carve(a, nullptr, nullptr);
+}
+
+bool attn_bwd_sm100_try(const Attn& a, const void* dout, i64 ld_do, void* dq, void* dk, void* dv, i64 ld_dq, i64 ld_dk,
+                        i64 ld_dv, void* ws, cudaStream_t s) {
+    if (!bwd_fits(a, dout, ld_do, ld_dq, ld_dk, ld_dv)) return false;
+    CUtensorMap tq, tk, tv, tdo, tm;
+    const long long rows = a.B * a.S, cols = a.nh * FD;
+    if (!make_map_bf16(&tq, a.q, cols, rows, a.ld_q, FT) || !make_map_bf16(&tk, a.k, cols, rows, a.ld_k, FT) ||
+        !make_map_bf16(&tv, a.v, cols, rows, a.ld_v, FT) || !make_map_bf16(&tdo, dout, cols, rows, ld_do, FT))
+        return false;
+    memset(&tm, 0, sizeof(tm));
+    if (a.thr && !make_map_u32(&tm, a.mask_t, a.S / 32, a.B * a.nh * a.S, a.S / 32, FT / 32, FT)) return false;
+    BwdWs w;
+    carve(a, ws, &w);
+    const long long BH = a.B * a.nh;
+    const long long n = BH * a.S;
+    k_fa5_prep<<<(unsigned)((n * 8 + 255) / 256), 256, 0, s>>>((const bf16*)dout, ld_do, (const bf16*)a.o, a.ld_o, a.lse,
+                                                              w.lse2, w.delta, BH, (int)a.S, (int)a.nh);
+    SBK_CHECK_LAUNCH();
+    BwdArgs ba{w.lse2, w.delta, w.dqacc, a.thr ? a.mask_t : nullptr, a.thr ? a.dscale : 1.f,
+               a.scale * 1.4426950408889634f, a.scale, (bf16*)dq, (bf16*)dk, (bf16*)dv, ld_dq, ld_dk, ld_dv,
+               (int)a.S, (int)a.nh, a.acc_mask, 0};
+    if (const char* e = getenv("SB_ATTN_DBG")) ba.dbg = atoi(e);
+    ba.ts = nullptr;
+    static unsigned long long* ts_buf = nullptr;
+    if (getenv("SB_ATTN_TS")) {
+        if (!ts_buf) cudaMalloc(&ts_buf, 8 * 64 * 8);
+        cudaMemsetAsync(ts_buf, 0, 8 * 64 * 8, s);
+        ba.ts = ts_buf;
+    }
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_fa5_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, B_SMEM);
+        attr = true;
+    }
+    dim3 grid((unsigned)a.nh, (unsigned)a.B);
+    k_fa5_bwd<<<grid, 512, B_SMEM, s>>>(tk, tv, tq, tdo, tm, ba);
+    SBK_CHECK_LAUNCH();
+    if (ba.ts) {
+        unsigned long long h_ts[8 * 64];
+        cudaMemcpyAsync(h_ts, ba.ts, sizeof(h_ts), cudaMemcpyDeviceToHost, s);
+        cudaStreamSynchronize(s);
+        unsigned long long t0 = h_ts[0];
+        const char* names[7] = {"prod st_empty ok", "mma sm_done_b ok", "mma sdp(u+1) issued", "mma dq_free ok",
+                                "smax sdp ok", "smax done", "dq dq_full ok"};
+        for (int r = 0; r < 7; ++r) {
+            fprintf(stderr, "%-22s", names[r]);
+            for (int u = 0; u < 16; ++u) fprintf(stderr, " %6lld", h_ts[r * 64 + u] ? (long long)(h_ts[r * 64 + u] - t0) : -1);
+            fprintf(stderr, "\n");
+        }
+    }
     return true;
 }
 

@@ -274,6 +274,39 @@ void dropout_mask(uint32_t* bits, i64 n, u64 s1, u64 thr, cudaStream_t s) {
     SBK_CHECK_LAUNCH();
 }
 
+// Attention keep bits in two layouts from one set of hashes: natural (bit j of
+// query row i: element ((bh*S + i)*S + j), read by the forward, one row per
+// thread) and transposed (bit i of key row j, read by the backward, one key per
+// thread). A warp owns a 32x32 (query, key) block: lane = query row computes
+// its 32 keep bits, and 32 ballots transpose the block.
+__global__ void k_dropout_mask_dual(uint32_t* bits, uint32_t* bits_t, i64 BH, int S, uint64_t s1, uint64_t thr) {
+    const int lane = threadIdx.x & 31;
+    const i64 nb = (i64)S / 32, blocks = BH * nb * nb;
+    for (i64 w = (blockIdx.x * (i64)blockDim.x + threadIdx.x) / 32; w < blocks; w += (i64)gridDim.x * blockDim.x / 32) {
+        const i64 kb = w % nb, qb = (w / nb) % nb, bh = w / (nb * nb);
+        const i64 e0 = (bh * S + qb * 32 + lane) * S + kb * 32;  // flat index of (query qb*32+lane, key kb*32)
+        uint32_t m = 0;
+#pragma unroll
+        for (int b = 0; b < 32; ++b)
+            if (d_keep(s1, (uint64_t)(e0 + b), thr)) m |= 1u << b;
+        bits[e0 >> 5] = m;
+        uint32_t t = 0;
+#pragma unroll
+        for (int b = 0; b < 32; ++b) {
+            uint32_t v = __ballot_sync(0xffffffffu, (m >> b) & 1);
+            if (lane == b) t = v;
+        }
+        bits_t[((bh * S + kb * 32 + lane) * S + qb * 32) >> 5] = t;
+    }
+}
+void dropout_mask_dual(uint32_t* bits, i64 BH, i64 S, u64 s1, u64 thr, cudaStream_t s) {
+    if (S % 32) throw std::runtime_error("dropout_mask_dual: S % 32 != 0");
+    const i64 words = BH * S * S / 32;
+    const i64 warps = BH * (S / 32) * (S / 32);
+    k_dropout_mask_dual<<<grid_for(warps * 32, 256), 256, 0, s>>>(bits, bits + words, BH, (int)S, s1, thr);
+    SBK_CHECK_LAUNCH();
+}
+
 // --------------------------------------------------------------- strided copy
 struct Idx8 {
     i64 shape[8], ss[8], ds[8];

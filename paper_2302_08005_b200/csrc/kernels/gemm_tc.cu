@@ -407,6 +407,19 @@ bool tc5::make_map_bf16(CUtensorMap* m, const void* base, long long inner, long 
     return make_map(m, base, inner, outer, ld, box_outer);
 }
 
+bool tc5::make_map_u32(CUtensorMap* m, const void* base, long long inner, long long outer, long long ld, int box_inner,
+                       int box_outer) {
+    auto fn = encode_fn();
+    if (!fn || (ld * 4) % 16 || ((uintptr_t)base & 15)) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+    cuuint64_t strides[1] = {(cuuint64_t)(ld * 4)};
+    cuuint32_t box[2] = {(cuuint32_t)box_inner, (cuuint32_t)box_outer};
+    cuuint32_t es[2] = {1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<void*>(base), dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 bool gemm_tc_try(const Gemm& g, cudaStream_t s) {
     if (g_tc_disabled) return false;
     if (g.ta != BF16 || g.tb != BF16 || g.batch != 1 || g.sCn != 1) return false;

@@ -83,6 +83,10 @@ void mul_bwd(const void* g, DT tg, const void* other, i64 other_n, void* ga, DT 
 void dropout(const void* x, void* y, DT t, i64 n, u64 s1, u64 thr, float scale, bool accumulate, cudaStream_t s);
 // Packed keep mask (bit i of word i/32) for tests / the attention kernels.
 void dropout_mask(uint32_t* bits, i64 n, u64 s1, u64 thr, cudaStream_t s);
+// attention keep bits, both layouts: bits[0, W) natural (element ((bh*S+i)*S+j)
+// at bit e%32 of word e/32), bits[W, 2W) transposed (element ((bh*S+j)*S+i)),
+// W = BH*S*S/32; S % 32 == 0
+void dropout_mask_dual(uint32_t* bits, i64 BH, i64 S, u64 s1, u64 thr, cudaStream_t s);
 
 // --------------------------------------------------------- strided copy
 // dst[idx] (+)= src[idx] over a rank<=8 index space with per-tensor strides.
@@ -152,15 +156,18 @@ struct Attn {
     u64 s1 = 0, thr = 0;
     float dscale = 1.f;
     DT t;
-    const uint32_t* mask = nullptr;  // precomputed keep bits (dropout_mask); required by the tensor-core path
+    const uint32_t* mask = nullptr;    // precomputed keep bits (dropout_mask); required by the tensor-core paths
+    const uint32_t* mask_t = nullptr;  // transposed keep bits (dropout_mask_dual); required by the tcgen05 backward
     int acc_mask = 7;                // backward: bit0/1/2 = dq/dk/dv accumulate (else overwrite)
 };
 void attn_fwd(const Attn& a, cudaStream_t s);
 // 0 = best available (tcgen05 > mma.sync > SIMT), 1 = at most mma.sync, 2 = SIMT only
 void attn_set_engine(int e);
 int attn_last_engine(int bwd);  // engine of the last fwd/bwd call: 3 tcgen05, 2 mma.sync, 1 SIMT
-// dq/dk/dv accumulate (+=) with their own row strides; `delta` scratch (B,nh,S) fp32.
+// dq/dk/dv accumulate (+=) or overwrite per acc_mask, with their own row
+// strides; `ws` scratch of attn_bwd_workspace() bytes.
 void attn_bwd(const Attn& a, const void* dout, i64 ld_do, void* dq, void* dk, void* dv, i64 ld_dq, i64 ld_dk,
-              i64 ld_dv, float* delta, cudaStream_t s);
+              i64 ld_dv, void* ws, cudaStream_t s);
+size_t attn_bwd_workspace(i64 B, i64 S, i64 nh, i64 hd);
 
 }  // namespace sbk

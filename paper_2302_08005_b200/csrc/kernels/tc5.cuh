@@ -33,6 +33,27 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
 }
 __device__ __forceinline__ void fence_barrier_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 
+// 1D bulk copy global -> shared (bytes % 16 == 0, 16-byte aligned), completes on `bar`
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"((uint64_t)src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+// generic-proxy shared-memory writes -> visible to the async proxy (tcgen05.mma operand reads)
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void named_bar(int id, int threads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+__device__ __forceinline__ int ld_acquire(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 __device__ __forceinline__ void tma_prefetch(const CUtensorMap* m) {
     asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)m) : "memory");
 }
@@ -143,6 +164,9 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 // stride `ld` elements), box {64, box_outer}, 128B swizzle. false if the
 // driver entry point is unavailable or the encoding is rejected.
 bool make_map_bf16(CUtensorMap* m, const void* base, long long inner, long long outer, long long ld, int box_outer);
+// host: 2D uint32 tensor map, no swizzle, box {box_inner, box_outer} (row-major in shared memory)
+bool make_map_u32(CUtensorMap* m, const void* base, long long inner, long long outer, long long ld, int box_inner,
+                  int box_outer);
 
 }  // namespace tc5
 }  // namespace sbk

@@ -26,15 +26,15 @@ qkv = torch.randn(B, S, 3 * H, device="cuda").bfloat16()
 q, k, v = qkv[..., :H], qkv[..., H:2 * H], qkv[..., 2 * H:]
 o = torch.empty(B, S, H, device="cuda", dtype=torch.bfloat16)
 lse = torch.empty(B * nh * S, device="cuda")
-delta = torch.empty_like(lse)
+delta = torch.empty(L.sb_attn_bwd_workspace(B, S, nh, hd), dtype=torch.uint8, device="cuda")
 n = B * nh * S * S
-bits = torch.empty((n + 31) // 32, dtype=torch.int32, device="cuda")
-L.sb_dropout_mask(P(bits), n, 123, 1040, p, None)
+bits = torch.empty(2 * ((n + 31) // 32), dtype=torch.int32, device="cuda")
+L.sb_attn_dropout_mask(P(bits), B, S, nh, 123, 1040, p, None)
 do = torch.randn(B, S, H, device="cuda").bfloat16()
 g = torch.zeros_like(qkv)
 for _ in range(2):
     L.sb_attn_fwd(P(q), P(k), P(v), P(o), 3 * H, H, P(lse), B, S, nh, hd, hd ** -0.5, 123, 1040, p, 1, P(bits), None)
     L.sb_attn_bwd(P(q), P(k), P(v), P(o), 3 * H, H, P(lse), P(do), P(g[..., :H]), P(g[..., H:2 * H]), P(g[..., 2 * H:]),
-                  P(delta), B, S, nh, hd, hd ** -0.5, 123, 1040, p, 1, P(bits), None)
+                  P(delta), B, S, nh, hd, hd ** -0.5, 123, 1040, p, 1, P(bits), 0, None)
 torch.cuda.synchronize()
 print("ok")

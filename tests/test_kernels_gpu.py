@@ -110,65 +110,29 @@ L.sb_attn_fwd.argtypes = [ctypes.c_void_p] * 4 + [ctypes.c_int64, ctypes.c_int64
                             ctypes.c_void_p, ctypes.c_void_p]
 L.sb_attn_bwd.argtypes = [ctypes.c_void_p] * 4 + [ctypes.c_int64, ctypes.c_int64] + [ctypes.c_void_p] * 6 + \
     [ctypes.c_int64] * 4 + [ctypes.c_float, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_double, ctypes.c_int,
-                            ctypes.c_void_p, ctypes.c_void_p]
+                            ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]
 L.sb_dropout_mask.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_double,
                               ctypes.c_void_p]
-
-
-@pytest.mark.parametrize("B,S,nh,hd,p", [(2, 128, 4, 64, 0.0), (2, 256, 2, 64, 0.1), (1, 128, 2, 128, 0.1)])
-def test_flash_attention_tensor_core(B, S, nh, hd, p):
-    H = nh * hd
-    torch.manual_seed(0)
-    qkv = (torch.randn(B, S, 3 * H, device="cuda") * 0.5).bfloat16()  # FusedQKV layout, consumed in place
-    q, k, v = qkv[..., :H], qkv[..., H:2 * H], qkv[..., 2 * H:]
-    o = torch.zeros(B, S, H, device="cuda", dtype=torch.bfloat16)
-    lse = torch.zeros(B * nh * S, device="cuda")
-    n = B * nh * S * S
-    bits = torch.zeros((n + 31) // 32, dtype=torch.int32, device="cuda")
-    es, ns = 123, 1040
-    if p > 0:
-        assert L.sb_dropout_mask(P(bits), n, es, ns, p, None) == 0
-    scale = hd ** -0.5
-    rc = L.sb_attn_fwd(P(q), P(k), P(v), P(o), 3 * H, H, P(lse), B, S, nh, hd, scale, es, ns, p, 1,
-                       P(bits) if p > 0 else None, None)
-    assert rc == 0, L.sb_last_error()
-    torch.cuda.synchronize()
-    # torch fp32 reference of the same math
-    qf, kf, vf = (t.float().reshape(B, S, nh, hd).transpose(1, 2).requires_grad_() for t in (q, k, v))
-    pr = torch.softmax(qf @ kf.transpose(-1, -2) * scale, dim=-1)
-    if p > 0:
-        idx = torch.arange(n, device="cuda")
-        keep = ((bits.view(torch.int32)[idx // 32] >> (idx % 32)) & 1).bool().reshape(B, nh, S, S)
-        pr = torch.where(keep, pr / (1 - p), torch.zeros_like(pr))
-    ref = (pr @ vf).transpose(1, 2).reshape(B, S, H)
-    close(o, ref)
-    # backward
-    do = (torch.randn(B, S, H, device="cuda") * 0.5).bfloat16()
-    ref.backward(do.float())
-    g = torch.zeros_like(qkv)
-    delta = torch.zeros(B * nh * S, device="cuda")
-    rc = L.sb_attn_bwd(P(q), P(k), P(v), P(o), 3 * H, H, P(lse), P(do), P(g[..., :H]), P(g[..., H:2 * H]),
-                       P(g[..., 2 * H:]), P(delta), B, S, nh, hd, scale, es, ns, p, 1, P(bits) if p > 0 else None, None)
-    assert rc == 0, L.sb_last_error()
-    torch.cuda.synchronize()
-    for got, want in ((g[..., :H], qf.grad), (g[..., H:2 * H], kf.grad), (g[..., 2 * H:], vf.grad)):
-        close(got, want.transpose(1, 2).reshape(B, S, H), 3e-2)
-
-
-L.sb_attn_set_engine.argtypes = [ctypes.c_int]
-L.sb_attn_engine.argtypes = [ctypes.c_int]
+ES, NS = 123, 1040
 
 
 def _attn_case(B, S, nh, hd, p, qscale=0.5, seed=0):
+    """FusedQKV-layout (B, S, 3H) input consumed in place + dual-layout keep bits."""
     H = nh * hd
     g = torch.Generator(device="cuda").manual_seed(seed)
     qkv = (torch.randn(B, S, 3 * H, device="cuda", generator=g) * 0.5).bfloat16()
     qkv[..., :H] = (qkv[..., :H].float() * (qscale / 0.5)).bfloat16()
     n = B * nh * S * S
-    bits = torch.zeros((n + 31) // 32, dtype=torch.int32, device="cuda")
+    bits = torch.zeros(2 * ((n + 31) // 32), dtype=torch.int32, device="cuda")
     if p > 0:
-        assert L.sb_dropout_mask(P(bits), n, 123, 1040, p, None) == 0
+        assert L.sb_attn_dropout_mask(P(bits), B, S, nh, ES, NS, p, None) == 0
     return qkv, bits
+
+
+def _keep(bits, B, S, nh):
+    n = B * nh * S * S
+    idx = torch.arange(n, device="cuda")
+    return ((bits[idx // 32] >> (idx % 32)) & 1).bool().reshape(B, nh, S, S)
 
 
 def _attn_fwd(qkv, bits, B, S, nh, hd, p, engine):
@@ -178,7 +142,7 @@ def _attn_fwd(qkv, bits, B, S, nh, hd, p, engine):
     L.sb_attn_set_engine(engine)
     try:
         rc = L.sb_attn_fwd(P(qkv[..., :H]), P(qkv[..., H:2 * H]), P(qkv[..., 2 * H:]), P(o), 3 * H, H, P(lse), B, S, nh,
-                           hd, hd ** -0.5, 123, 1040, p, 1, P(bits) if p > 0 else None, None)
+                           hd, hd ** -0.5, ES, NS, p, 1, P(bits) if p > 0 else None, None)
         assert rc == 0, L.sb_last_error()
         torch.cuda.synchronize()
         used = L.sb_attn_engine(0)
@@ -187,18 +151,71 @@ def _attn_fwd(qkv, bits, B, S, nh, hd, p, engine):
     return o, lse, used
 
 
-def _attn_ref(qkv, bits, B, S, nh, hd, p):
+def _attn_bwd(qkv, o, lse, do, bits, B, S, nh, hd, p, engine, g=None):
+    """g given: accumulate into it (acc_mask 7); else overwrite a garbage-filled buffer (acc_mask 0)."""
     H = nh * hd
-    q, k, v = (qkv[..., i * H:(i + 1) * H].float().reshape(B, S, nh, hd).transpose(1, 2) for i in range(3))
+    acc = 7 if g is not None else 0
+    g = torch.full_like(qkv, 1e4) if g is None else g
+    ws = torch.empty(L.sb_attn_bwd_workspace(B, S, nh, hd), dtype=torch.uint8, device="cuda")
+    L.sb_attn_set_engine(engine)
+    try:
+        rc = L.sb_attn_bwd(P(qkv[..., :H]), P(qkv[..., H:2 * H]), P(qkv[..., 2 * H:]), P(o), 3 * H, H, P(lse), P(do),
+                           P(g[..., :H]), P(g[..., H:2 * H]), P(g[..., 2 * H:]), P(ws), B, S, nh, hd, hd ** -0.5, ES,
+                           NS, p, 1, P(bits) if p > 0 else None, acc, None)
+        assert rc == 0, L.sb_last_error()
+        torch.cuda.synchronize()
+        used = L.sb_attn_engine(1)
+    finally:
+        L.sb_attn_set_engine(0)
+    return g, used
+
+
+def _attn_ref(qkv, bits, B, S, nh, hd, p, do=None):
+    """torch fp32 reference of the same math (+ autograd gradients of q, k, v when do is given)."""
+    H = nh * hd
+    q, k, v = (qkv[..., i * H:(i + 1) * H].float().reshape(B, S, nh, hd).transpose(1, 2).requires_grad_()
+               for i in range(3))
     s = q @ k.transpose(-1, -2) * hd ** -0.5
     lse = torch.logsumexp(s, -1).reshape(-1)
     pr = torch.softmax(s, -1)
     if p > 0:
-        n = B * nh * S * S
-        idx = torch.arange(n, device="cuda")
-        keep = ((bits[idx // 32] >> (idx % 32)) & 1).bool().reshape(B, nh, S, S)
-        pr = torch.where(keep, pr / (1 - p), torch.zeros_like(pr))
-    return (pr @ v).transpose(1, 2).reshape(B, S, H), lse
+        pr = torch.where(_keep(bits, B, S, nh), pr / (1 - p), torch.zeros_like(pr))
+    o = (pr @ v).transpose(1, 2).reshape(B, S, H)
+    grads = None
+    if do is not None:
+        o.backward(do.float())
+        grads = [t.grad.transpose(1, 2).reshape(B, S, H) for t in (q, k, v)]
+    return o.detach(), lse.detach(), grads
+
+
+def test_attention_dropout_mask_dual_layout():
+    B, S, nh, p = 2, 256, 3, 0.1
+    n = B * nh * S * S
+    dual = torch.zeros(2 * n // 32, dtype=torch.int32, device="cuda")
+    nat = torch.zeros(n // 32, dtype=torch.int32, device="cuda")
+    assert L.sb_attn_dropout_mask(P(dual), B, S, nh, ES, NS, p, None) == 0
+    assert L.sb_dropout_mask(P(nat), n, ES, NS, p, None) == 0
+    torch.cuda.synchronize()
+    assert torch.equal(dual[:n // 32], nat)  # natural half: the reference's bits exactly
+    keep = _keep(dual, B, S, nh)
+    keep_t = _keep(dual[n // 32:], B, S, nh)
+    assert torch.equal(keep_t, keep.transpose(-1, -2))
+
+
+@pytest.mark.parametrize("B,S,nh,hd,p", [(2, 128, 4, 64, 0.0), (2, 256, 2, 64, 0.1), (1, 128, 2, 128, 0.1)])
+def test_flash_attention_tensor_core(B, S, nh, hd, p):
+    """mma.sync kernels (engine 2) vs a torch fp32 reference."""
+    H = nh * hd
+    qkv, bits = _attn_case(B, S, nh, hd, p)
+    o, lse, used = _attn_fwd(qkv, bits, B, S, nh, hd, p, 1)
+    assert used == 2
+    do = (torch.randn(B, S, H, device="cuda") * 0.5).bfloat16()
+    ref, _, grads = _attn_ref(qkv, bits, B, S, nh, hd, p, do)
+    close(o, ref)
+    g, used = _attn_bwd(qkv, o, lse, do, bits, B, S, nh, hd, p, 1)
+    assert used == 2
+    for i in range(3):
+        close(g[..., i * H:(i + 1) * H], grads[i], 3e-2)
 
 
 @pytest.mark.parametrize("B,S,nh,hd,p,qscale", [(2, 128, 4, 64, 0.0, 0.5), (2, 256, 2, 64, 0.1, 0.5),
@@ -210,9 +227,35 @@ def test_flash_attention_tcgen05_forward(B, S, nh, hd, p, qscale):
     qkv, bits = _attn_case(B, S, nh, hd, p, qscale)
     o5, lse5, used = _attn_fwd(qkv, bits, B, S, nh, hd, p, 0)
     assert used == 3, "tcgen05 attention path not taken"
-    ref, lse_ref = _attn_ref(qkv, bits, B, S, nh, hd, p)
+    ref, lse_ref, _ = _attn_ref(qkv, bits, B, S, nh, hd, p)
     close(o5, ref)
     assert (lse5 - lse_ref).abs().max().item() < 2e-3 * max(1.0, lse_ref.abs().max().item())
     o2, lse2, used2 = _attn_fwd(qkv, bits, B, S, nh, hd, p, 1)
     assert used2 == 2
     close(o5, o2.float(), 1e-2)
+
+
+@pytest.mark.parametrize("B,S,nh,hd,p,qscale", [(2, 128, 4, 64, 0.0, 0.5), (2, 256, 2, 64, 0.1, 0.5),
+                                                 (1, 384, 2, 64, 0.1, 0.5), (2, 512, 16, 64, 0.1, 0.5),
+                                                 (1, 512, 2, 64, 0.1, 3.0)])
+def test_flash_attention_tcgen05_backward(B, S, nh, hd, p, qscale):
+    """tcgen05 backward (engine 3: TS/SS MMAs, ordered fp32 dQ accumulation) vs torch autograd
+    of the fp32 reference, vs the mma.sync backward, accumulate mode, and run-to-run bitwise equality."""
+    H = nh * hd
+    qkv, bits = _attn_case(B, S, nh, hd, p, qscale)
+    o, lse, _ = _attn_fwd(qkv, bits, B, S, nh, hd, p, 0)
+    do = (torch.randn(B, S, H, device="cuda", generator=torch.Generator(device="cuda").manual_seed(1)) * 0.5).bfloat16()
+    _, _, grads = _attn_ref(qkv, bits, B, S, nh, hd, p, do)
+    g5, used = _attn_bwd(qkv, o, lse, do, bits, B, S, nh, hd, p, 0)
+    assert used == 3, "tcgen05 attention backward not taken"
+    for i in range(3):
+        close(g5[..., i * H:(i + 1) * H], grads[i], 3e-2)
+    g2, used2 = _attn_bwd(qkv, o, lse, do, bits, B, S, nh, hd, p, 1)
+    assert used2 == 2
+    for i in range(3):
+        close(g5[..., i * H:(i + 1) * H], g2[..., i * H:(i + 1) * H].float(), 2e-2)
+    g5b, _ = _attn_bwd(qkv, o, lse, do, bits, B, S, nh, hd, p, 0)
+    assert torch.equal(g5, g5b)  # deterministic (no float atomics)
+    base = (torch.randn_like(qkv.float()) * 0.1).bfloat16()
+    gacc, _ = _attn_bwd(qkv, o, lse, do, bits, B, S, nh, hd, p, 0, g=base.clone())
+    close(gacc, base.float() + g5.float(), 2e-2)
