@@ -145,6 +145,8 @@ public:
         if (ncomm && nccl().CommDestroy) nccl().CommDestroy(ncomm);
         for (auto e : mask_ev)
             if (e) cudaEventDestroy(e);
+        for (auto e : bwd_ev)
+            if (e) cudaEventDestroy(e);
         if (fork_ev) cudaEventDestroy(fork_ev);
         if (mstream) cudaStreamDestroy(mstream);
         if (stream) cudaStreamDestroy(stream);
@@ -699,7 +701,8 @@ public:
         sbk::bias_dropout_residual_ln_fwd(fp(r, op.out[1]), bias, fp(r, op.in[2]), fp(r, op.in[3]), fp(r, op.in[4]), cdt,
                                           fp(r, op.out[2]), fp(r, op.out[0]), (float*)fp(r, op.out[3]),
                                           (float*)fp(r, op.out[4]), cdt, rows, n, (float)op.eps, op.s1,
-                                          op.dropout ? op.thr : 0, (float)(1.0 / (1.0 - op.p)), stream);
+                                          op.dropout ? op.thr : 0, (float)(1.0 / (1.0 - op.p)), stream,
+                                          op.dropout ? (const uint32_t*)fp(r, op.out[5]) : nullptr);
         ++launches;
     }
 
@@ -930,7 +933,8 @@ public:
                         gp(r, op.out[0]), gres.p, gp(r, op.out[1]), false,
                         op.has_bias && op.bias_grad ? (float*)gp(r, op.in[5]) : nullptr, (float*)gp(r, op.in[3]),
                         (float*)gp(r, op.in[4]), cdt, rows, n, op.s1, op.dropout ? op.thr : 0,
-                        (float)(1.0 / (1.0 - op.p)), (float*)r.ws, stream, gres.temp || !OW(op.in[2]), !OW(op.in[3]));
+                        (float)(1.0 / (1.0 - op.p)), (float*)r.ws, stream, gres.temp || !OW(op.in[2]), !OW(op.in[3]),
+                        op.dropout ? (const uint32_t*)fp(r, op.out[5]) : nullptr);
                     flush(r, gres);
                     ++launches;
                     // the in-region all_reduce backpropagates as identity (executor.cpp:1227-1233)
@@ -1215,46 +1219,78 @@ public:
         mask_ev.assign(P.fwd.size(), nullptr);
         bool any = false;
         for (size_t i = 0; i < P.fwd.size(); ++i)
-            if (P.fwd[i].k == K::FlashAttn && P.fwd[i].dropout) {
+            if ((P.fwd[i].k == K::FlashAttn || P.fwd[i].k == K::FusedLinearResLN) && P.fwd[i].dropout) {
                 CK(cudaEventCreateWithFlags(&mask_ev[i], cudaEventDisableTiming));
                 any = true;
             }
         if (!any) return;
+        bwd_ev.assign(P.fwd.size(), nullptr);
+        for (size_t i = 0; i < P.fwd.size(); ++i)
+            if (mask_ev[i]) CK(cudaEventCreateWithFlags(&bwd_ev[i], cudaEventDisableTiming));
         int lo, hi;
         CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
         CK(cudaStreamCreateWithPriority(&mstream, cudaStreamNonBlocking, lo));  // lo = least priority
         CK(cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming));
     }
 
+    // Keep bits depend only on (executor seed, node seed, index) (rng.hpp,
+    // executor.cpp:788-806), so every forward of this executor uses the same
+    // bits. They are generated on the side stream: all of them before the first
+    // forward, then each step regenerates mask i right after its last reader
+    // (op i's backward), overlapping the rest of the backward; the forward
+    // waits per op on mask_ev[i].
+    bool masks_valid = false;
+    std::vector<cudaEvent_t> bwd_ev;  // per forward op index: its backward was enqueued
+    std::vector<char> ev_real;        // mask_ev[i] last recorded outside a graph capture (waitable)
+
+    void gen_mask(size_t i) {
+        for (auto& r : ranks) {
+            const Op& op = r.P.fwd[i];
+            if (op.k == K::FusedLinearResLN) {
+                const View& y = V(r, op.out[0]);
+                sbk::dropout_mask((uint32_t*)fp(r, op.out[5]), rows_of(y) * cols_of(y), op.s1, op.thr, mstream);
+                continue;
+            }
+            sbk::Attn a = attn_args(r, op);
+            if (a.S % 32 == 0)
+                sbk::dropout_mask_dual((uint32_t*)fp(r, op.out[2]), a.B * a.nh, a.S, op.s1, op.thr, mstream);
+            else
+                sbk::dropout_mask((uint32_t*)fp(r, op.out[2]), a.B * a.nh * a.S * a.S, op.s1, op.thr, mstream);
+        }
+        CK(cudaEventRecord(mask_ev[i], mstream));
+        if (ev_real.size() != mask_ev.size()) ev_real.assign(mask_ev.size(), 0);
+        ev_real[i] = !capturing();
+    }
+
     void launch_masks() {
         if (!mstream) return;
         CK(cudaEventRecord(fork_ev, stream));
         CK(cudaStreamWaitEvent(mstream, fork_ev, 0));
-        for (size_t i = 0; i < mask_ev.size(); ++i) {
-            if (!mask_ev[i]) continue;
-            for (auto& r : ranks) {
-                const Op& op = r.P.fwd[i];
-                sbk::Attn a = attn_args(r, op);
-                if (a.S % 32 == 0)
-                    sbk::dropout_mask_dual((uint32_t*)fp(r, op.out[2]), a.B * a.nh, a.S, op.s1, op.thr, mstream);
-                else
-                    sbk::dropout_mask((uint32_t*)fp(r, op.out[2]), a.B * a.nh * a.S * a.S, op.s1, op.thr, mstream);
-            }
-            CK(cudaEventRecord(mask_ev[i], mstream));
-        }
+        for (size_t i = 0; i < mask_ev.size(); ++i)
+            if (mask_ev[i]) gen_mask(i);
+        masks_valid = true;
+    }
+
+    bool capturing() {
+        cudaStreamCaptureStatus st;
+        CK(cudaStreamIsCapturing(stream, &st));
+        return st != cudaStreamCaptureStatusNone;
     }
 
     void run_forward() {
-        launch_masks();
+        if (!masks_valid) launch_masks();
+        const bool cap = capturing();
         cudaEvent_t last = nullptr;
         for (size_t i = 0; i < ranks[0].P.fwd.size(); ++i) {
-            if (mask_ev.size() > i && mask_ev[i]) {
+            // (inside a graph capture the masks were made before the capture or
+            // by the previous replay's backward, which the stream order covers)
+            if (!cap && mask_ev.size() > i && mask_ev[i] && ev_real[i]) {
                 CK(cudaStreamWaitEvent(stream, mask_ev[i], 0));
                 last = mask_ev[i];
             }
             fwd_op((int)i);
         }
-        if (last) CK(cudaStreamWaitEvent(stream, last, 0));  // join (graph capture needs it)
+        if (last) CK(cudaStreamWaitEvent(stream, last, 0));
         ran_forward = true;
     }
 
@@ -1270,6 +1306,8 @@ public:
                 ++launches;
             }
         }
+        const bool cap = capturing();
+        cudaEvent_t last = nullptr;
         for (size_t si = 0; si < bsteps.size(); ++si) {
             const Step& s = bsteps[si];
             if (s.kind == 2) {
@@ -1282,8 +1320,17 @@ public:
                 cur_ow = &step_ow[si];
                 bwd_op(s.idx);
                 cur_ow = nullptr;
+                const size_t i = (size_t)s.idx;
+                if (masks_valid && mstream && mask_ev.size() > i && mask_ev[i]) {
+                    // last reader of mask i done: regenerate it for the next step
+                    CK(cudaEventRecord(bwd_ev[i], stream));
+                    CK(cudaStreamWaitEvent(mstream, bwd_ev[i], 0));
+                    gen_mask(i);
+                    last = mask_ev[i];
+                }
             }
         }
+        if (cap && last) CK(cudaStreamWaitEvent(stream, last, 0));  // join the side stream into the graph
     }
 
     // merged [offset, bytes) ranges of the persistent gradient storages to zero
@@ -1462,6 +1509,10 @@ void Executor::capture_graph() {
     if (I.gexec) return;
     if (I.comm.nccl && I.world > 1) {
         // NCCL kernels are capturable; nothing special beyond using our stream.
+    }
+    if (!I.masks_valid && I.mstream) {  // the graph regenerates masks in its backward; prime them once here
+        I.launch_masks();
+        CK(cudaStreamSynchronize(I.mstream));
     }
     CK(cudaStreamBeginCapture(I.stream, cudaStreamCaptureModeThreadLocal));
     I.run_forward();

@@ -556,6 +556,11 @@ struct Lowerer {
                 op.p = p;
                 op.s1 = dropout_s1(get_int(drop->attrs, "seed").value_or(0));
                 op.thr = dropout_threshold(p);
+                // keep bits (bit row*n + col), generated off the critical path and
+                // persistent like the attention masks (checkpoint recompute re-reads them)
+                int kb = aux((rows * out_f + 31) / 32);
+                P.st[(size_t)V(kb).st].region = -1;
+                op.out.push_back(kb);
             }
         }
         op.path = path;

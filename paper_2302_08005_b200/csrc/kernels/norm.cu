@@ -18,10 +18,10 @@ bool ln_fwd_vec(const void* x, const void* gamma, const void* beta, void* y, flo
                 i64 n, float eps, cudaStream_t s);
 bool bdrln_fwd_vec(const void* partial, const void* bias, const void* res, const void* gamma, const void* beta, void* sum,
                    void* y, float* mean, float* rstd, DT t, i64 rows, i64 n, float eps, u64 s1, u64 thr, float dscale,
-                   cudaStream_t s);
+                   const uint32_t* keep, cudaStream_t s);
 bool ln_bwd_vec(int mode, const void* x, const float* mean, const float* rstd, const void* gamma, const void* g, void* gx,
-                void* gres, bool gx_acc, bool gres_acc, DT t, i64 rows, i64 n, u64 s1, u64 thr, float dscale, float* ws, int ncol,
-                int nblocks, cudaStream_t s);
+                void* gres, bool gx_acc, bool gres_acc, DT t, i64 rows, i64 n, u64 s1, u64 thr, float dscale,
+                const uint32_t* keep, float* ws, int ncol, int nblocks, cudaStream_t s);
 static int vec_blocks(i64 rows) { return (int)std::min<i64>(148, std::max<i64>(1, (rows + kWarps - 1) / kWarps)); }
 
 // ------------------------------------------------------------------ softmax
@@ -219,7 +219,7 @@ void layernorm_bwd(const void* x, const float* mean, const float* rstd, const vo
     (void)tg;
     int ncol = (dgamma || dbeta) ? 2 : 0;
     int vb = vec_blocks(rows);
-    if (ln_bwd_vec(0, x, mean, rstd, gamma, g, gx, nullptr, gx_acc, true, t, rows, n, 0, 0, 1.f, ws, ncol, vb, s)) {
+    if (ln_bwd_vec(0, x, mean, rstd, gamma, g, gx, nullptr, gx_acc, true, t, rows, n, 0, 0, 1.f, nullptr, ws, ncol, vb, s)) {
         if (ncol) k_col_final<<<grid_for(2 * n, 256), 256, 0, s>>>(ws, vb, 2 * n, dgamma, dbeta, nullptr, n, col_acc);
         SBK_CHECK_LAUNCH();
         return;
@@ -266,9 +266,9 @@ __global__ void k_bdrln_fwd(const T* partial, const T* bias, const T* res, const
 }
 void bias_dropout_residual_ln_fwd(const void* partial, const void* bias, const void* residual, const void* gamma,
                                   const void* beta, DT tp, void* sum, void* y, float* mean, float* rstd, DT t, i64 rows,
-                                  i64 n, float eps, u64 s1, u64 thr, float dscale, cudaStream_t s) {
+                                  i64 n, float eps, u64 s1, u64 thr, float dscale, cudaStream_t s, const uint32_t* keep) {
     (void)tp;
-    if (bdrln_fwd_vec(partial, bias, residual, gamma, beta, sum, y, mean, rstd, t, rows, n, eps, s1, thr, dscale, s)) {
+    if (bdrln_fwd_vec(partial, bias, residual, gamma, beta, sum, y, mean, rstd, t, rows, n, eps, s1, thr, dscale, keep, s)) {
         SBK_CHECK_LAUNCH();
         return;
     }
@@ -283,12 +283,12 @@ void bias_dropout_residual_ln_fwd(const void* partial, const void* bias, const v
 void bias_dropout_residual_ln_bwd(const void* sum, const float* mean, const float* rstd, const void* gamma, DT tp,
                                   const void* g, void* g_res, void* g_partial, bool g_partial_acc, float* dbias,
                                   float* dgamma, float* dbeta, DT t, i64 rows, i64 n, u64 s1, u64 thr, float dscale,
-                                  float* ws, cudaStream_t s, bool gres_acc, bool col_acc) {
+                                  float* ws, cudaStream_t s, bool gres_acc, bool col_acc, const uint32_t* keep) {
     (void)tp;
     int ncol = 3;
     int vb = vec_blocks(rows);
     if (ln_bwd_vec(1, sum, mean, rstd, gamma, g, g_partial, g_res, g_partial_acc, gres_acc, t, rows, n, s1, thr, dscale,
-                   ws, ncol, vb, s)) {
+                   keep, ws, ncol, vb, s)) {
         k_col_final<<<grid_for(3 * n, 256), 256, 0, s>>>(ws, vb, 3 * n, dgamma, dbeta, dbias, n, col_acc);
         SBK_CHECK_LAUNCH();
         return;

@@ -79,6 +79,13 @@ __device__ __forceinline__ void stats(const float (&v)[CPL][VN], float n, float 
     rs = rsqrtf(warp_sum(q) / n + eps);
 }
 __device__ __forceinline__ int col_of(int c, int lane, int e, int VN) { return (c * 32 + lane) * VN + e; }
+// the VN keep bits of elements idx0 .. idx0+VN-1 (idx0 % VN == 0, VN <= 8) from a
+// dropout_mask bit array (bit i of word w = element 32w + i, i.e. byte idx/8, bit idx%8)
+template <int VN>
+__device__ __forceinline__ uint32_t keep_bits(const uint32_t* keep, i64 idx0) {
+    const uint32_t byte = ((const uint8_t*)keep)[idx0 >> 3];
+    return VN == 8 ? byte : (byte >> (idx0 & 7)) & ((1u << VN) - 1);
+}
 
 template <class T, int CPL>
 __global__ void __launch_bounds__(32 * kW) k_ln_fwd_v(const T* x, const T* gamma, const T* beta, T* y, float* mean,
@@ -113,7 +120,8 @@ __global__ void __launch_bounds__(32 * kW) k_ln_fwd_v(const T* x, const T* gamma
 template <class T, int CPL>
 __global__ void __launch_bounds__(32 * kW) k_bdrln_fwd_v(const T* partial, const T* bias, const T* res, const T* gamma,
                                                          const T* beta, T* sum, T* y, float* mean, float* rstd, i64 rows,
-                                                         int n, float eps, uint64_t s1, uint64_t thr, float dscale) {
+                                                         int n, float eps, uint64_t s1, uint64_t thr, float dscale,
+                                                         const uint32_t* keep) {
     constexpr int VN = Vec<T>::N;
     i64 row = blockIdx.x * (i64)kW + threadIdx.x / 32;
     int lane = threadIdx.x & 31;
@@ -123,12 +131,20 @@ __global__ void __launch_bounds__(32 * kW) k_bdrln_fwd_v(const T* partial, const
     load_row<T, CPL>(res + row * n, lane, r);
     float bb[CPL][VN];
     if (bias) load_row<T, CPL>(bias, lane, bb);
+    uint32_t kb[CPL];
+    if (thr && keep) {
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) kb[c] = keep_bits<VN>(keep, row * n + col_of(c, lane, 0, VN));
+    }
 #pragma unroll
     for (int c = 0; c < CPL; ++c)
 #pragma unroll
         for (int e = 0; e < VN; ++e) {
             float t = v[c][e] + (bias ? bb[c][e] : 0.f);
-            if (thr) t = d_keep(s1, (uint64_t)(row * n + col_of(c, lane, e, VN)), thr) ? t * dscale : 0.f;
+            if (thr) {
+                const bool kept = keep ? ((kb[c] >> e) & 1) : d_keep(s1, (uint64_t)(row * n + col_of(c, lane, e, VN)), thr);
+                t = kept ? t * dscale : 0.f;
+            }
             v[c][e] = t + r[c][e];
         }
     // `sum` is rounded to the storage dtype before the statistics, exactly as
@@ -159,7 +175,8 @@ __global__ void __launch_bounds__(32 * kW) k_bdrln_fwd_v(const T* partial, const
 template <class T, int CPL, int MODE>
 __global__ void __launch_bounds__(32 * kW, 1)
     k_ln_bwd_v(const T* x, const float* mean, const float* rstd, const T* gamma, const T* g, T* gx, T* gres, bool gx_acc,
-               i64 rows, int n, uint64_t s1, uint64_t thr, float dscale, float* ws, int ncol, bool gres_acc) {
+               i64 rows, int n, uint64_t s1, uint64_t thr, float dscale, const uint32_t* keep, float* ws, int ncol,
+               bool gres_acc) {
     constexpr int VN = Vec<T>::N;
     extern __shared__ float sh[];  // [kW][ncol][n]
     int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
@@ -209,12 +226,21 @@ __global__ void __launch_bounds__(32 * kW, 1)
 #pragma unroll
                 for (int e = 0; e < VN; ++e) o[c][e] += gv[c][e];
             store_row<T, CPL>(gres + row * n, lane, o);
+            uint32_t kb[CPL];
+            if (thr && keep) {
+#pragma unroll
+                for (int c = 0; c < CPL; ++c) kb[c] = keep_bits<VN>(keep, row * n + col_of(c, lane, 0, VN));
+            }
 #pragma unroll
             for (int c = 0; c < CPL; ++c)
 #pragma unroll
                 for (int e = 0; e < VN; ++e) {
                     float d = gv[c][e];
-                    if (thr) d = d_keep(s1, (uint64_t)(row * n + col_of(c, lane, e, VN)), thr) ? d * dscale : 0.f;
+                    if (thr) {
+                        const bool kept =
+                            keep ? ((kb[c] >> e) & 1) : d_keep(s1, (uint64_t)(row * n + col_of(c, lane, e, VN)), thr);
+                        d = kept ? d * dscale : 0.f;
+                    }
                     gv[c][e] = d;
                     pd[c][e] += d;
                 }
@@ -286,7 +312,7 @@ bool ln_fwd_vec(const void* x, const void* gamma, const void* beta, void* y, flo
 
 bool bdrln_fwd_vec(const void* partial, const void* bias, const void* res, const void* gamma, const void* beta, void* sum,
                    void* y, float* mean, float* rstd, DT t, i64 rows, i64 n, float eps, u64 s1, u64 thr, float dscale,
-                   cudaStream_t s) {
+                   const uint32_t* keep, cudaStream_t s) {
     for (const void* p : {partial, res, gamma, beta, (const void*)sum, (const void*)y})
         if (!aligned16(p)) return false;
     if (t == F64 || (bias && !aligned16(bias))) return false;
@@ -297,7 +323,7 @@ bool bdrln_fwd_vec(const void* partial, const void* bias, const void* res, const
             ok = with_cpl<T>((int)n, [&](auto cc) {
                 k_bdrln_fwd_v<T, decltype(cc)::value><<<(unsigned)((rows + kW - 1) / kW), 32 * kW, 0, s>>>(
                     (const T*)partial, (const T*)bias, (const T*)res, (const T*)gamma, (const T*)beta, (T*)sum, (T*)y,
-                    mean, rstd, rows, (int)n, eps, s1, thr, dscale);
+                    mean, rstd, rows, (int)n, eps, s1, thr, dscale, keep);
             });
         }
     });
@@ -307,8 +333,8 @@ bool bdrln_fwd_vec(const void* partial, const void* bias, const void* res, const
 // mode 0: LN backward into gx (+=); mode 1: bdrln backward. Writes ncol column
 // partials per block to ws (the caller finishes with the fixed-order column sum).
 bool ln_bwd_vec(int mode, const void* x, const float* mean, const float* rstd, const void* gamma, const void* g, void* gx,
-                void* gres, bool gx_acc, bool gres_acc, DT t, i64 rows, i64 n, u64 s1, u64 thr, float dscale, float* ws, int ncol,
-                int nblocks, cudaStream_t s) {
+                void* gres, bool gx_acc, bool gres_acc, DT t, i64 rows, i64 n, u64 s1, u64 thr, float dscale,
+                const uint32_t* keep, float* ws, int ncol, int nblocks, cudaStream_t s) {
     for (const void* p : {x, g, (const void*)gx})
         if (!aligned16(p)) return false;
     if (t == F64 || (gamma && !aligned16(gamma)) || (gres && !aligned16(gres))) return false;
@@ -323,8 +349,8 @@ bool ln_bwd_vec(int mode, const void* x, const float* mean, const float* rstd, c
                 auto launch = [&](auto k) {
                     if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
                     k<<<nblocks, 32 * kW, smem, s>>>((const T*)x, mean, rstd, (const T*)gamma, (const T*)g, (T*)gx,
-                                                     (T*)gres, gx_acc, rows, (int)n, s1, thr, dscale, ws, ncol,
-                                                     gres_acc);
+                                                     (T*)gres, gx_acc, rows, (int)n, s1, thr, dscale, keep, ws,
+                                                     ncol, gres_acc);
                 };
                 if (mode == 0) launch(k_ln_bwd_v<T, CPL, 0>);
                 else launch(k_ln_bwd_v<T, CPL, 1>);

@@ -1,6 +1,3 @@
 cd $GRAFT_REPO_ROOT
 timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-timeout 600 python bench.py --no-cpu-baseline > gpurun_out/bench.json 2> gpurun_out/bench.err
-timeout 600 python bench.py --no-cpu-baseline --profile --steps 5 > gpurun_out/bench_prof.json 2> gpurun_out/bench_prof.err
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 1200 --csv --log-file gpurun_out/launches.csv \
-    python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-graph > gpurun_out/ncu_list.log 2>&1
+timeout 600 python bench.py --no-cpu-baseline --profile > gpurun_out/bench.json 2> gpurun_out/bench.err
