@@ -129,8 +129,10 @@ int sb_executor_device_bytes(sb_executor* e, int64_t* bytes);
 int sb_gemm(const void* A, int ta, int64_t sAb, int64_t sAm, int64_t sAk, const void* B, int tb, int64_t sBb,
             int64_t sBk, int64_t sBn, void* C, int tc, int64_t sCb, int64_t sCm, int64_t sCn, int64_t batch, int64_t M,
             int64_t N, int64_t K, float alpha, int accumulate, const void* bias, int epilogue, void* aux, void* stream);
-int sb_gemm_engine(void);                /* engine of the last sb_gemm: 0 SIMT, 1 tcgen05 */
+int sb_gemm_engine(void);                /* engine of the last sb_gemm: 0 SIMT, 1 tcgen05 1-SM, 2 tcgen05 2-SM */
 int sb_gemm_force_simt(int on);
+/* engine cap: 0 best available (2-SM > 1-SM tcgen05 > SIMT), 1 at most the 1-SM kernel, 2 SIMT */
+int sb_gemm_set_engine(int max_engine);
 /* attention engine cap: 0 best available (tcgen05 > mma.sync > SIMT), 1 at most mma.sync, 2 SIMT;
  * sb_attn_engine(bwd) = engine of the last forward (0) / backward (1) call: 3 tcgen05, 2 mma.sync, 1 SIMT */
 int sb_attn_set_engine(int max_engine);

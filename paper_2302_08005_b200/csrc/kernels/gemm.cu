@@ -8,7 +8,8 @@
 
 namespace sbk {
 
-bool gemm_tc_try(const Gemm& g, cudaStream_t s);  // gemm_tc.cu
+bool gemm_tc_try(const Gemm& g, cudaStream_t s);   // gemm_tc.cu  (1-SM tcgen05)
+bool gemm_tc2_try(const Gemm& g, cudaStream_t s);  // gemm_tc2.cu (2-SM tcgen05)
 
 namespace {
 int g_last_engine = 0;
@@ -78,12 +79,18 @@ __global__ void __launch_bounds__(256) k_gemm_simt(Gemm g) {
 }
 }  // namespace
 
+int g_gemm_max_engine = 0;  // 0 best available, 1 at most the 1-SM tcgen05 kernel, 2 SIMT
 int gemm_last_engine() { return g_last_engine; }
 void gemm_force_simt(bool on) { g_force_simt = on; }
+void gemm_set_engine(int e) { g_gemm_max_engine = e; }
 
 void gemm(const Gemm& g, cudaStream_t s) {
     if (g.M == 0 || g.N == 0) return;
-    if (!g_force_simt && gemm_tc_try(g, s)) {
+    if (!g_force_simt && g_gemm_max_engine == 0 && gemm_tc2_try(g, s)) {
+        g_last_engine = 2;
+        return;
+    }
+    if (!g_force_simt && g_gemm_max_engine <= 1 && gemm_tc_try(g, s)) {
         g_last_engine = 1;
         return;
     }

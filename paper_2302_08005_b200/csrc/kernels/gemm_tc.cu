@@ -403,6 +403,17 @@ bool g_tc_disabled = false;
 
 void gemm_tc_disable(bool off) { g_tc_disabled = off; }
 
+void splitk_reduce_launch(const float* partial, int splits, i64 M, i64 N, void* C, DT tc, i64 ldc, const void* bias,
+                          bool accumulate, cudaStream_t s) {
+    unsigned blocks = grid_for(M * N / 4, 256);
+    if (tc == F32)
+        k_splitk_reduce<float><<<blocks, 256, 0, s>>>(partial, splits, M, N, (float*)C, ldc, (const bf16*)bias,
+                                                      accumulate);
+    else
+        k_splitk_reduce<bf16><<<blocks, 256, 0, s>>>(partial, splits, M, N, (bf16*)C, ldc, (const bf16*)bias, accumulate);
+    SBK_CHECK_LAUNCH();
+}
+
 bool tc5::make_map_bf16(CUtensorMap* m, const void* base, long long inner, long long outer, long long ld, int box_outer) {
     return make_map(m, base, inner, outer, ld, box_outer);
 }

@@ -41,8 +41,10 @@ struct Gemm {
     size_t ws_bytes = 0;
 };
 void gemm(const Gemm& g, cudaStream_t s);
-// Which engine the last gemm() call used: 0 SIMT, 1 tcgen05 (for tests/bench).
+// Which engine the last gemm() call used: 0 SIMT, 1 tcgen05 1-SM, 2 tcgen05 2-SM (tests/bench).
 int gemm_last_engine();
+// engine cap: 0 best available, 1 at most the 1-SM tcgen05 kernel, 2 SIMT only
+void gemm_set_engine(int e);
 // Force the SIMT engine (tests compare the tcgen05 kernel against it).
 void gemm_force_simt(bool on);
 // workspace the tcgen05 split-K path may use for an (M x N) fp32 output

@@ -1,2 +1,2 @@
 cd $GRAFT_REPO_ROOT
-for p in 0.1 0.0; do timeout 600 python bench.py --no-cpu-baseline --steps 5 --p $p --profile > gpurun_out/bench_p$p.json 2> gpurun_out/bench_p$p.err; done
+for c in 0 1; do timeout 600 python bench.py --no-cpu-baseline --steps 5 --gemm-cap $c --profile > gpurun_out/bench_c$c.json 2> gpurun_out/bench_c$c.err; done

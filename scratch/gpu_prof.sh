@@ -1,2 +1,2 @@
 cd $GRAFT_REPO_ROOT
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_fa5_bwd" -c 1 -o gpurun_out/prof_bwd3 python profiles/ncu_targets.py > gpurun_out/ncu_attn.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_gemm" -c 4 -o gpurun_out/prof_gemm2 python scratch/gemm_one.py > gpurun_out/ncu_gemm.log 2>&1

@@ -18,13 +18,20 @@ L.sb_gemm.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_in
                       ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_float, ctypes.c_int,
                       ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]
 L.sb_gemm_set_workspace.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
+L.sb_gemm_set_engine.argtypes = [ctypes.c_int]
 P = lambda t: ctypes.c_void_p(t.data_ptr()) if t is not None else None  # noqa: E731
 DT = {torch.float32: 0, torch.bfloat16: 1}
 
 
-def gemm(A, sA, B, sB, C, M, N, K, acc=False, bias=None, gelu=False, aux=None):
-    rc = L.sb_gemm(P(A), DT[A.dtype], 0, sA[0], sA[1], P(B), DT[B.dtype], 0, sB[0], sB[1], P(C), DT[C.dtype], 0,
-                   C.stride(0), 1, 1, M, N, K, 1.0, int(acc), P(bias), 1 if gelu else 0, P(aux), None)
+def gemm(A, sA, B, sB, C, M, N, K, acc=False, bias=None, gelu=False, aux=None, epi=None, cap=0):
+    """C (+)= A B through the C ABI; epi: 0 none, 1 gelu (+aux pre-activation), 2 dgelu(aux); cap: engine cap."""
+    L.sb_gemm_set_engine(cap)
+    try:
+        rc = L.sb_gemm(P(A), DT[A.dtype], 0, sA[0], sA[1], P(B), DT[B.dtype], 0, sB[0], sB[1], P(C), DT[C.dtype], 0,
+                       C.stride(0), 1, 1, M, N, K, 1.0, int(acc), P(bias), (1 if gelu else 0) if epi is None else epi,
+                       P(aux), None)
+    finally:
+        L.sb_gemm_set_engine(0)
     assert rc == 0, L.sb_last_error()
     torch.cuda.synchronize()
     return L.sb_gemm_engine()
@@ -51,7 +58,7 @@ def test_forward_tn(M, N, K):
     b = torch.randn(N, device="cuda", generator=g).bfloat16()
     y = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
     eng = gemm(x, (K, 1), w, (1, K), y, M, N, K, bias=b)
-    assert eng == 1, "tcgen05 path not taken"
+    assert eng in (1, 2), "tcgen05 path not taken"
     close(y, x.float() @ w.float().T + b.float())
 
 
@@ -62,7 +69,7 @@ def test_forward_gelu_epilogue_and_aux():
     b = torch.randn(N, device="cuda").bfloat16()
     y = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
     pre = torch.empty_like(y)
-    assert gemm(x, (K, 1), w, (1, K), y, M, N, K, bias=b, gelu=True, aux=pre) == 1
+    assert gemm(x, (K, 1), w, (1, K), y, M, N, K, bias=b, gelu=True, aux=pre) in (1, 2)
     ref = x.float() @ w.float().T + b.float()
     close(pre, ref)
     close(y, torch.nn.functional.gelu(ref, approximate="tanh"))
@@ -74,7 +81,7 @@ def test_dgrad_nn_accumulate(M, N, K):
     w = torch.randn(K, N, device="cuda").bfloat16()  # W is (out=K, in=N)
     dx = torch.randn(M, N, device="cuda").bfloat16()
     want = dx.float() + g.float() @ w.float()
-    assert gemm(g, (K, 1), w, (N, 1), dx, M, N, K, acc=True) == 1  # B(k,n) = W[k][n]: sBk=N, sBn=1
+    assert gemm(g, (K, 1), w, (N, 1), dx, M, N, K, acc=True) in (1, 2)  # B(k,n) = W[k][n]: sBk=N, sBn=1
     close(dx, want)
 
 
@@ -85,7 +92,7 @@ def test_wgrad_nt_fp32_splitk(O, I, T):
     dw = torch.randn(O, I, device="cuda", dtype=torch.float32)
     want = dw + gy.float().T @ x.float()
     # A(m=o, k=t) = gy[t][o]: sAm=1, sAk=O ; B(k=t, n=i) = x[t][i]: sBk=I, sBn=1
-    assert gemm(gy, (1, O), x, (I, 1), dw, O, I, T, acc=True) == 1
+    assert gemm(gy, (1, O), x, (I, 1), dw, O, I, T, acc=True) in (1, 2)
     close(dw, want, 1e-2)
 
 
@@ -95,13 +102,66 @@ def test_tc_matches_simt_engine():
     w = torch.randn(N, K, device="cuda").bfloat16()
     y1 = torch.empty(M, N, device="cuda", dtype=torch.float32)
     y2 = torch.empty_like(y1)
-    assert gemm(x, (K, 1), w, (1, K), y1, M, N, K) == 1
+    assert gemm(x, (K, 1), w, (1, K), y1, M, N, K) in (1, 2)
     L.sb_gemm_force_simt(1)
     try:
         assert gemm(x, (K, 1), w, (1, K), y2, M, N, K) == 0
     finally:
         L.sb_gemm_force_simt(0)
     assert (y1 - y2).abs().max().item() < 1e-3 * y2.abs().max().item()
+
+
+def _gemm_engine(cap, *a, **k):
+    return gemm(*a, cap=cap, **k)
+
+
+@pytest.mark.parametrize("layout", ["tn", "tn_bias", "tn_gelu", "nn", "nn_acc", "nn_dgelu", "nt_f32", "nt_f32_acc",
+                                    "nt_splitk"])
+def test_gemm_2sm_vs_1sm(layout):
+    """The 2-SM cta_group::2 kernel (engine 2, TMA-store epilogue) against the 1-SM kernel and fp32 torch,
+    every operand layout / epilogue the executor uses, at shapes that need several tiles per cluster."""
+    M, N, K = 1024, 768, 512
+    outs = {}
+    for cap in (0, 1):
+        g = torch.Generator(device="cuda").manual_seed(3)  # same inputs for both engines
+        rnd = lambda *sh: torch.randn(*sh, device="cuda", generator=g)  # noqa: E731
+        if layout.startswith("tn"):
+            x, w, b = rnd(M, K).bfloat16(), rnd(N, K).bfloat16(), rnd(N).bfloat16()
+            y = torch.zeros(M, N, device="cuda", dtype=torch.bfloat16)
+            pre = torch.zeros_like(y) if layout == "tn_gelu" else None
+            e = _gemm_engine(cap, x, (K, 1), w, (1, K), y, M, N, K, bias=b if layout != "tn" else None,
+                             gelu=layout == "tn_gelu", aux=pre)
+            ref = x.float() @ w.float().T + (b.float() if layout != "tn" else 0)
+            outs[cap] = (y, pre)
+            if layout == "tn_gelu":
+                close(pre, ref)
+                ref = torch.nn.functional.gelu(ref, approximate="tanh")
+            close(y, ref)
+        elif layout.startswith("nn"):
+            gy, w = rnd(M, K).bfloat16(), rnd(K, N).bfloat16()
+            base = rnd(M, N).bfloat16()
+            dx = base.clone() if layout == "nn_acc" else torch.zeros(M, N, device="cuda", dtype=torch.bfloat16)
+            aux = rnd(M, N).bfloat16() if layout == "nn_dgelu" else None
+            if aux is not None:
+                e = _gemm_engine(cap, gy, (K, 1), w, (N, 1), dx, M, N, K, epi=2, aux=aux)
+                a = aux.float()
+                t = torch.tanh(0.7978845608028654 * (a + 0.044715 * a ** 3))
+                dg = 0.5 * (1 + t) + 0.5 * a * (1 - t * t) * 0.7978845608028654 * (1 + 3 * 0.044715 * a * a)
+                close(dx, (gy.float() @ w.float()) * dg)
+            else:
+                e = _gemm_engine(cap, gy, (K, 1), w, (N, 1), dx, M, N, K, acc=layout == "nn_acc")
+                close(dx, (base.float() if layout == "nn_acc" else 0) + gy.float() @ w.float())
+            outs[cap] = (dx, None)
+        else:
+            T = 4096 if layout == "nt_splitk" else K
+            gy, x = rnd(T, M).bfloat16(), rnd(T, N).bfloat16()
+            base = rnd(M, N)
+            dw = base.clone() if layout.endswith("acc") else torch.zeros(M, N, device="cuda")
+            e = _gemm_engine(cap, gy, (1, M), x, (N, 1), dw, M, N, T, acc=layout.endswith("acc"))
+            close(dw, (base if layout.endswith("acc") else 0) + gy.float().T @ x.float(), 1e-2)
+            outs[cap] = (dw, None)
+        assert e == (2 if cap == 0 else 1), (layout, cap, e)
+    assert (outs[0][0].float() - outs[1][0].float()).abs().max().item() <= 2e-2 * outs[1][0].float().abs().max().item()
 
 
 # ------------------------------------------------------------------ attention
