@@ -150,7 +150,7 @@ int sb_bias_dropout_residual_ln_fwd(const void* partial, const void* bias, const
                                     const void* beta, void* sum, void* y, float* mean, float* rstd, int dtype,
                                     int64_t rows, int64_t n, float eps, uint64_t exec_seed, uint64_t node_seed,
                                     double p, void* stream);
-/* attention keep bits in both layouts (S % 32 == 0): words [0, W) natural (bit e%32 of word e/32
+/* attention keep bits in both layouts (S % 128 == 0): words [0, W) natural (bit e%32 of word e/32
  * for element e = ((b*nh + h)*S + i)*S + j, exactly sb_dropout_mask's bits), words [W, 2W)
  * transposed (element ((b*nh + h)*S + j)*S + i), W = B*nh*S*S/32 */
 int sb_attn_dropout_mask(uint32_t* bits, int64_t B, int64_t S, int64_t nh, uint64_t exec_seed, uint64_t node_seed,

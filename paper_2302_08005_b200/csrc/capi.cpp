@@ -562,7 +562,7 @@ int sb_attn_bwd(const void* q, const void* k, const void* v, const void* o, int6
         sbk::Attn a = mk_attn(q, k, v, (void*)o, ld_qkv, ld_o, (float*)lse, B, S, nh, hd, scale, es, ns, p, dtype);
         a.acc_mask = acc_mask;
         a.mask = keep_bits;
-        a.mask_t = keep_bits && S % 32 == 0 ? keep_bits + (B * nh * S * S) / 32 : nullptr;
+        a.mask_t = keep_bits && S % 128 == 0 ? keep_bits + (B * nh * S * S) / 32 : nullptr;
         sbk::attn_bwd(a, dout, ld_o, dq, dk, dv, ld_qkv, ld_qkv, ld_qkv, workspace, (cudaStream_t)stream);
     });
 }

@@ -863,7 +863,7 @@ public:
         a.dscale = (float)(1.0 / (1.0 - op.p));
         a.t = cdt;
         a.mask = op.dropout ? (const uint32_t*)fp(r, op.out[2]) : nullptr;
-        if (a.mask && a.S % 32 == 0) a.mask_t = a.mask + (a.B * a.nh * a.S * a.S) / 32;
+        if (a.mask && a.S % 128 == 0) a.mask_t = a.mask + (a.B * a.nh * a.S * a.S) / 32;
         return a;
     }
 
@@ -1252,7 +1252,7 @@ public:
                 continue;
             }
             sbk::Attn a = attn_args(r, op);
-            if (a.S % 32 == 0)
+            if (a.S % 128 == 0)
                 sbk::dropout_mask_dual((uint32_t*)fp(r, op.out[2]), a.B * a.nh, a.S, op.s1, op.thr, mstream);
             else
                 sbk::dropout_mask((uint32_t*)fp(r, op.out[2]), a.B * a.nh * a.S * a.S, op.s1, op.thr, mstream);

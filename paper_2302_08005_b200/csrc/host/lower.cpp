@@ -445,9 +445,9 @@ struct Lowerer {
         if (o.train && p > 0.0) {
             // 1-bit keep mask, persistent even inside a checkpoint region: it is a
             // pure function of the seeds, so recompute re-reads it
-            // (both layouts when S % 32 == 0: natural for the forward, transposed for the backward)
+            // (both layouts when S % 128 == 0: natural for the forward, transposed for the backward)
             const i64 words = (B * nh * S * S + 31) / 32;
-            int mv = aux(S % 32 == 0 ? 2 * words : words);
+            int mv = aux(S % 128 == 0 ? 2 * words : words);
             P.st[(size_t)V(mv).st].region = -1;
             op.out.push_back(mv);
         }

@@ -89,6 +89,30 @@ __device__ __forceinline__ bool d_keep_k(uint64_t s1, uint64_t key, uint64_t i, 
 __device__ __forceinline__ bool d_keep(uint64_t s1, uint64_t i, uint64_t thr) {
     return d_keep_k(s1, d_keep_key(s1), i, thr);
 }
+// keep bits of the 32 elements e0 .. e0+31 (bit b = element e0 + b); bk = e0 + d_keep_key(s1),
+// T = thr << 11. The index add is one 64-bit mad and the >= T test a borrow chain, so the
+// hash (integer-ALU bound) carries no extra compare/select work per element.
+__device__ __forceinline__ uint32_t d_keep_word(uint64_t s1, uint64_t bk, uint64_t T) {
+    const uint32_t tlo = (uint32_t)T, thi = (uint32_t)(T >> 32);
+    uint32_t m = 0;
+#pragma unroll
+    for (int b = 0; b < 32; ++b) {
+        unsigned long long d;
+        asm("mad.wide.u32 %0, %1, 1, %2;" : "=l"(d) : "r"((uint32_t)b), "l"(bk));
+        d ^= s1;
+        uint32_t lo = (uint32_t)d, hi = (uint32_t)(d >> 32);
+        sm64_body(lo, hi);
+        sm64_xs(lo, hi, 31);
+        sm64_body(lo, hi);
+        sm64_xs(lo, hi, 31);
+        uint32_t bit;
+        asm("{\n\t.reg .u32 t;\n\tsub.cc.u32 t, %1, %3;\n\tsubc.cc.u32 t, %2, %4;\n\taddc.u32 %0, 0, 0;\n\t}"
+            : "=r"(bit)
+            : "r"(lo), "r"(hi), "r"(tlo), "r"(thi));
+        m |= bit << b;
+    }
+    return m;
+}
 
 __device__ __forceinline__ float gelu_f(float x) {
     const float c = 0.7978845608028654f, a = 0.044715f;

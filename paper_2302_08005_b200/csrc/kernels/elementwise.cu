@@ -257,15 +257,12 @@ void dropout(const void* x, void* y, DT t, i64 n, u64 s1, u64 thr, float scale, 
     SBK_CHECK_LAUNCH();
 }
 __global__ void k_dropout_mask(uint32_t* bits, i64 n, uint64_t s1, uint64_t thr) {
-    i64 nw = (n + 31) / 32;
+    const i64 nw = (n + 31) / 32;
+    const uint64_t key = d_keep_key(s1), T = thr << 11;
     for (i64 w = blockIdx.x * (i64)blockDim.x + threadIdx.x; w < nw; w += (i64)gridDim.x * blockDim.x) {
-        uint32_t m = 0;
         // 32 independent hash chains per thread: fully unrolled so they interleave
-#pragma unroll
-        for (int b = 0; b < 32; ++b) {
-            i64 i = w * 32 + b;
-            if (d_keep(s1, (uint64_t)i, thr) && i < n) m |= 1u << b;
-        }
+        uint32_t m = d_keep_word(s1, (uint64_t)w * 32 + key, T);
+        if (w == nw - 1 && (n & 31)) m &= (1u << (n & 31)) - 1;
         bits[w] = m;
     }
 }
@@ -279,31 +276,33 @@ void dropout_mask(uint32_t* bits, i64 n, u64 s1, u64 thr, cudaStream_t s) {
 // thread) and transposed (bit i of key row j, read by the backward, one key per
 // thread). A warp owns a 32x32 (query, key) block: lane = query row computes
 // its 32 keep bits, and 32 ballots transpose the block.
-__global__ void k_dropout_mask_dual(uint32_t* bits, uint32_t* bits_t, i64 BH, int S, uint64_t s1, uint64_t thr) {
-    const int lane = threadIdx.x & 31;
-    const i64 nb = (i64)S / 32, blocks = BH * nb * nb;
-    for (i64 w = (blockIdx.x * (i64)blockDim.x + threadIdx.x) / 32; w < blocks; w += (i64)gridDim.x * blockDim.x / 32) {
-        const i64 kb = w % nb, qb = (w / nb) % nb, bh = w / (nb * nb);
-        const i64 e0 = (bh * S + qb * 32 + lane) * S + kb * 32;  // flat index of (query qb*32+lane, key kb*32)
-        uint32_t m = 0;
+__global__ void k_dropout_mask_dual(uint32_t* bits, uint32_t* bits_t, int S, uint64_t s1, uint64_t thr) {
+    // block = (bh, 32-query block qb, 4 x 32-key blocks); warp = 32-key block kb. Small blocks
+    // (128 threads, few registers) so the hashing co-resides with the GEMM / attention CTAs
+    // and uses their idle issue slots
+    const int lane = threadIdx.x & 31, kb = blockIdx.z * 4 + (threadIdx.x >> 5);
+    const long long bh = blockIdx.x;
+    const int qb = blockIdx.y;
+    const long long e0 = (bh * S + qb * 32 + lane) * S + kb * 32;  // flat index of (query qb*32+lane, key kb*32)
+    const uint32_t m = d_keep_word(s1, (uint64_t)e0 + d_keep_key(s1), thr << 11);
+    bits[e0 >> 5] = m;
+    // 32x32 bit-matrix transpose across the warp (lane = row -> lane = column):
+    // swap the off-diagonal blocks of width 16, 8, 4, 2, 1
+    uint32_t t = m;
 #pragma unroll
-        for (int b = 0; b < 32; ++b)
-            if (d_keep(s1, (uint64_t)(e0 + b), thr)) m |= 1u << b;
-        bits[e0 >> 5] = m;
-        uint32_t t = 0;
-#pragma unroll
-        for (int b = 0; b < 32; ++b) {
-            uint32_t v = __ballot_sync(0xffffffffu, (m >> b) & 1);
-            if (lane == b) t = v;
-        }
-        bits_t[((bh * S + kb * 32 + lane) * S + qb * 32) >> 5] = t;
+    for (int j = 16; j > 0; j >>= 1) {
+        const uint32_t msk = j == 16 ? 0x0000FFFFu : j == 8 ? 0x00FF00FFu : j == 4 ? 0x0F0F0F0Fu
+                             : j == 2 ? 0x33333333u : 0x55555555u;
+        const uint32_t y = __shfl_xor_sync(0xffffffffu, t, j);
+        t = (lane & j) ? (t & ~msk) | ((y >> j) & msk) : (t & msk) | ((y & msk) << j);
     }
+    bits_t[((bh * S + kb * 32 + lane) * S + qb * 32) >> 5] = t;
 }
 void dropout_mask_dual(uint32_t* bits, i64 BH, i64 S, u64 s1, u64 thr, cudaStream_t s) {
-    if (S % 32) throw std::runtime_error("dropout_mask_dual: S % 32 != 0");
+    if (S % 128) throw std::runtime_error("dropout_mask_dual: S % 128 != 0");
     const i64 words = BH * S * S / 32;
-    const i64 warps = BH * (S / 32) * (S / 32);
-    k_dropout_mask_dual<<<grid_for(warps * 32, 256), 256, 0, s>>>(bits, bits + words, BH, (int)S, s1, thr);
+    dim3 grid((unsigned)BH, (unsigned)(S / 32), (unsigned)(S / 128));
+    k_dropout_mask_dual<<<grid, 128, 0, s>>>(bits, bits + words, (int)S, s1, thr);
     SBK_CHECK_LAUNCH();
 }
 

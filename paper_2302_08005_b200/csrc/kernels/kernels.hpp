@@ -87,7 +87,7 @@ void dropout(const void* x, void* y, DT t, i64 n, u64 s1, u64 thr, float scale, 
 void dropout_mask(uint32_t* bits, i64 n, u64 s1, u64 thr, cudaStream_t s);
 // attention keep bits, both layouts: bits[0, W) natural (element ((bh*S+i)*S+j)
 // at bit e%32 of word e/32), bits[W, 2W) transposed (element ((bh*S+j)*S+i)),
-// W = BH*S*S/32; S % 32 == 0
+// W = BH*S*S/32; S % 128 == 0
 void dropout_mask_dual(uint32_t* bits, i64 BH, i64 S, u64 s1, u64 thr, cudaStream_t s);
 
 // --------------------------------------------------------- strided copy

@@ -12,8 +12,12 @@ __device__ __forceinline__ bool ref_keep(uint64_t s1, uint64_t i, uint64_t thr) 
     return (h >> 11) >= thr;
 }
 // xorshift right by k: ALU form or FMA form (mul.hi by 2^(32-k) held in a register)
-template <bool F> __device__ __forceinline__ void xs(uint32_t& lo, uint32_t& hi, int k, uint32_t m) {
-    if (F) {
+template <bool F, bool H = false> __device__ __forceinline__ void xs(uint32_t& lo, uint32_t& hi, int k, uint32_t m) {
+    if (H) {  // lo on the ALU (funnel shift), hi >> k as mul.hi on the FMA pipe
+        uint32_t c;
+        asm("mul.hi.u32 %0, %1, %2;" : "=r"(c) : "r"(hi), "r"(m));
+        lo ^= __funnelshift_r(lo, hi, k); hi ^= c;
+    } else if (F) {
         uint32_t a, b, c;
         asm("mul.hi.u32 %0, %1, %2;" : "=r"(a) : "r"(lo), "r"(m));
         asm("mul.lo.u32 %0, %1, %2;" : "=r"(b) : "r"(hi), "r"(m));
@@ -47,13 +51,14 @@ template <int V> __device__ __forceinline__ uint32_t keep_word(uint64_t s1, uint
         d ^= s1;
         uint32_t lo = (uint32_t)d, hi = (uint32_t)(d >> 32);
         addg<(V >> 6) & 1>(lo, hi, kc.one);
-        xs<(V >> 0) & 1>(lo, hi, 30, kc.c4); mul(lo, hi, 0x1ce4e5b9u, 0xbf58476du);
-        xs<(V >> 1) & 1>(lo, hi, 27, kc.c32); mul(lo, hi, 0x133111ebu, 0x94d049bbu);
-        xs<(V >> 2) & 1>(lo, hi, 31, kc.c2);
+        constexpr int HM = (V >> 8) & 63;
+        xs<(V >> 0) & 1, (HM >> 0) & 1>(lo, hi, 30, kc.c4); mul(lo, hi, 0x1ce4e5b9u, 0xbf58476du);
+        xs<(V >> 1) & 1, (HM >> 1) & 1>(lo, hi, 27, kc.c32); mul(lo, hi, 0x133111ebu, 0x94d049bbu);
+        xs<(V >> 2) & 1, (HM >> 2) & 1>(lo, hi, 31, kc.c2);
         addg<(V >> 7) & 1>(lo, hi, kc.one);
-        xs<(V >> 3) & 1>(lo, hi, 30, kc.c4); mul(lo, hi, 0x1ce4e5b9u, 0xbf58476du);
-        xs<(V >> 4) & 1>(lo, hi, 27, kc.c32); mul(lo, hi, 0x133111ebu, 0x94d049bbu);
-        xs<(V >> 5) & 1>(lo, hi, 31, kc.c2);
+        xs<(V >> 3) & 1, (HM >> 3) & 1>(lo, hi, 30, kc.c4); mul(lo, hi, 0x1ce4e5b9u, 0xbf58476du);
+        xs<(V >> 4) & 1, (HM >> 4) & 1>(lo, hi, 27, kc.c32); mul(lo, hi, 0x133111ebu, 0x94d049bbu);
+        xs<(V >> 5) & 1, (HM >> 5) & 1>(lo, hi, 31, kc.c2);
         uint32_t bit;
         asm("{\n\t.reg .u32 t;\n\tsub.cc.u32 t, %1, %3;\n\tsubc.cc.u32 t, %2, %4;\n\taddc.u32 %0, 0, 0;\n\t}"
             : "=r"(bit) : "r"(lo), "r"(hi), "r"(tlo), "r"(thi));
@@ -98,6 +103,6 @@ int main() {
     float ms; cudaEventElapsedTime(&ms, a, b); printf("ref 64-bit C: %.1f us\n", ms * 1000);
     int bad;
 #define R(V) { float t = run<V>(d, r, nw, s1, thr, kc, &bad); printf("V=%3d (xsF=%d%d%d%d%d%d addF=%d%d): %.1f us bad=%d\n", V, V&1,(V>>1)&1,(V>>2)&1,(V>>3)&1,(V>>4)&1,(V>>5)&1,(V>>6)&1,(V>>7)&1, t*1000, bad); }
-    R(0) R(1) R(3) R(7) R(9) R(27) R(63) R(64+128) R(9+64+128) R(27+64+128) R(7+64) R(18) R(45)
+    R(0) R(63*256) R(9*256) R(27*256) R(18*256) R(45*256) R(7*256) R(56*256) R(21*256)
     return 0;
 }
