@@ -162,6 +162,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile", action="store_true", help="print the per-op-kind breakdown to stderr")
     ap.add_argument("--gemm-cap", type=int, default=0, help="GEMM engine cap (experiments: 1 = 1-SM tcgen05 only)")
+    ap.add_argument("--mask-blocks", type=int, default=-1, help="keep-bit kernel grid (experiments)")
     ap.add_argument("--p", type=float, default=CFG["p"], help="dropout probability (experiments only; the metric uses 0.1)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -181,6 +182,8 @@ def main():
     cfg = dict(CFG, layers=args.layers, batch=args.batch, p=args.p)
     if args.gemm_cap:
         sb.lib().sb_gemm_set_engine(args.gemm_cap)
+    if args.mask_blocks != -1:
+        sb.lib().sb_set_mask_blocks(args.mask_blocks)
     dist = None
     uid = None
     if world > 1:

@@ -484,6 +484,10 @@ int sb_gemm_force_simt(int on) {
     sbk::gemm_force_simt(on != 0);
     return 0;
 }
+int sb_set_mask_blocks(int n) {
+    sbk::set_mask_blocks(n);
+    return 0;
+}
 int sb_gemm_set_engine(int max_engine) {
     sbk::gemm_set_engine(max_engine);
     return 0;

@@ -1227,6 +1227,7 @@ public:
         bwd_ev.assign(P.fwd.size(), nullptr);
         for (size_t i = 0; i < P.fwd.size(); ++i)
             if (mask_ev[i]) CK(cudaEventCreateWithFlags(&bwd_ev[i], cudaEventDisableTiming));
+        if (const char* e = getenv("SB_MASK_PHASE")) regen_bwd = std::string(e) != "fwd";
         int lo, hi;
         CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
         CK(cudaStreamCreateWithPriority(&mstream, cudaStreamNonBlocking, lo));  // lo = least priority
@@ -1234,14 +1235,24 @@ public:
     }
 
     // Keep bits depend only on (executor seed, node seed, index) (rng.hpp,
-    // executor.cpp:788-806), so every forward of this executor uses the same
-    // bits. They are generated on the side stream: all of them before the first
-    // forward, then each step regenerates mask i right after its last reader
-    // (op i's backward), overlapping the rest of the backward; the forward
-    // waits per op on mask_ev[i].
+    // executor.cpp:788-806), so every forward of this executor reads the same bits.
+    // They are regenerated every step on a low-priority side stream (small
+    // co-residing blocks, kernels/elementwise.cu). Placement (SB_MASK_PHASE):
+    //   "bwd" (default): all masks before the first forward, then each step
+    //     regenerates mask i right after its last reader (op i's backward),
+    //     overlapping the rest of the backward;
+    //   "fwd": at the start of every forward, layer by layer ahead of the readers.
+    // Readers wait on mask_ev[i] only.
     bool masks_valid = false;
+    bool regen_bwd = true;
     std::vector<cudaEvent_t> bwd_ev;  // per forward op index: its backward was enqueued
     std::vector<char> ev_real;        // mask_ev[i] last recorded outside a graph capture (waitable)
+
+    bool capturing() {
+        cudaStreamCaptureStatus st;
+        CK(cudaStreamIsCapturing(stream, &st));
+        return st != cudaStreamCaptureStatusNone;
+    }
 
     void gen_mask(size_t i) {
         for (auto& r : ranks) {
@@ -1271,26 +1282,21 @@ public:
         masks_valid = true;
     }
 
-    bool capturing() {
-        cudaStreamCaptureStatus st;
-        CK(cudaStreamIsCapturing(stream, &st));
-        return st != cudaStreamCaptureStatusNone;
-    }
-
     void run_forward() {
-        if (!masks_valid) launch_masks();
+        if (!regen_bwd || !masks_valid) launch_masks();
         const bool cap = capturing();
         cudaEvent_t last = nullptr;
         for (size_t i = 0; i < ranks[0].P.fwd.size(); ++i) {
-            // (inside a graph capture the masks were made before the capture or
-            // by the previous replay's backward, which the stream order covers)
-            if (!cap && mask_ev.size() > i && mask_ev[i] && ev_real[i]) {
+            // (in bwd placement inside a graph capture the masks were made before the
+            // capture or by the previous replay's backward, which the stream order covers)
+            const bool wait = regen_bwd ? (!cap && ev_real[i]) : true;
+            if (mask_ev.size() > i && mask_ev[i] && wait) {
                 CK(cudaStreamWaitEvent(stream, mask_ev[i], 0));
                 last = mask_ev[i];
             }
             fwd_op((int)i);
         }
-        if (last) CK(cudaStreamWaitEvent(stream, last, 0));
+        if (last && !regen_bwd) CK(cudaStreamWaitEvent(stream, last, 0));  // join (graph capture needs it)
         ran_forward = true;
     }
 
@@ -1321,7 +1327,7 @@ public:
                 bwd_op(s.idx);
                 cur_ow = nullptr;
                 const size_t i = (size_t)s.idx;
-                if (masks_valid && mstream && mask_ev.size() > i && mask_ev[i]) {
+                if (regen_bwd && masks_valid && mstream && mask_ev.size() > i && mask_ev[i]) {
                     // last reader of mask i done: regenerate it for the next step
                     CK(cudaEventRecord(bwd_ev[i], stream));
                     CK(cudaStreamWaitEvent(mstream, bwd_ev[i], 0));
@@ -1510,7 +1516,7 @@ void Executor::capture_graph() {
     if (I.comm.nccl && I.world > 1) {
         // NCCL kernels are capturable; nothing special beyond using our stream.
     }
-    if (!I.masks_valid && I.mstream) {  // the graph regenerates masks in its backward; prime them once here
+    if (I.regen_bwd && !I.masks_valid && I.mstream) {  // the graph regenerates masks in its backward; prime once
         I.launch_masks();
         CK(cudaStreamSynchronize(I.mstream));
     }

@@ -266,43 +266,70 @@ __global__ void k_dropout_mask(uint32_t* bits, i64 n, uint64_t s1, uint64_t thr)
         bits[w] = m;
     }
 }
-void dropout_mask(uint32_t* bits, i64 n, u64 s1, u64 thr, cudaStream_t s) {
-    k_dropout_mask<<<grid_for((n + 31) / 32, 256), 256, 0, s>>>(bits, n, s1, thr);
-    SBK_CHECK_LAUNCH();
-}
+
 
 // Attention keep bits in two layouts from one set of hashes: natural (bit j of
 // query row i: element ((bh*S + i)*S + j), read by the forward, one row per
 // thread) and transposed (bit i of key row j, read by the backward, one key per
 // thread). A warp owns a 32x32 (query, key) block: lane = query row computes
 // its 32 keep bits, and 32 ballots transpose the block.
-__global__ void k_dropout_mask_dual(uint32_t* bits, uint32_t* bits_t, int S, uint64_t s1, uint64_t thr) {
-    // block = (bh, 32-query block qb, 4 x 32-key blocks); warp = 32-key block kb. Small blocks
-    // (128 threads, few registers) so the hashing co-resides with the GEMM / attention CTAs
-    // and uses their idle issue slots
-    const int lane = threadIdx.x & 31, kb = blockIdx.z * 4 + (threadIdx.x >> 5);
-    const long long bh = blockIdx.x;
-    const int qb = blockIdx.y;
-    const long long e0 = (bh * S + qb * 32 + lane) * S + kb * 32;  // flat index of (query qb*32+lane, key kb*32)
-    const uint32_t m = d_keep_word(s1, (uint64_t)e0 + d_keep_key(s1), thr << 11);
-    bits[e0 >> 5] = m;
-    // 32x32 bit-matrix transpose across the warp (lane = row -> lane = column):
-    // swap the off-diagonal blocks of width 16, 8, 4, 2, 1
-    uint32_t t = m;
+__global__ void k_dropout_mask_dual(uint32_t* bits, uint32_t* bits_t, int S, long long BH, uint64_t s1, uint64_t thr) {
+    // grid-stride over 32x32 (query, key) blocks, one per warp: a small persistent grid
+    // (g_mask_blocks blocks of 4 warps) co-resides with the GEMM / attention CTAs and
+    // uses their idle issue slots without crowding out their producer / MMA warps
+    const int lane = threadIdx.x & 31;
+    const int nb = S / 32;
+    const long long nblk = BH * nb * nb;
+    for (long long w = (long long)blockIdx.x * 4 + (threadIdx.x >> 5); w < nblk; w += (long long)gridDim.x * 4) {
+        const int kb = (int)(w % nb), qb = (int)((w / nb) % nb);
+        const long long bh = w / ((long long)nb * nb);
+        const long long e0 = (bh * S + qb * 32 + lane) * S + kb * 32;  // flat index of (query qb*32+lane, key kb*32)
+        const uint32_t m = d_keep_word(s1, (uint64_t)e0 + d_keep_key(s1), thr << 11);
+        bits[e0 >> 5] = m;
+        // 32x32 bit-matrix transpose across the warp (lane = row -> lane = column):
+        // swap the off-diagonal blocks of width 16, 8, 4, 2, 1
+        uint32_t t = m;
 #pragma unroll
-    for (int j = 16; j > 0; j >>= 1) {
-        const uint32_t msk = j == 16 ? 0x0000FFFFu : j == 8 ? 0x00FF00FFu : j == 4 ? 0x0F0F0F0Fu
-                             : j == 2 ? 0x33333333u : 0x55555555u;
-        const uint32_t y = __shfl_xor_sync(0xffffffffu, t, j);
-        t = (lane & j) ? (t & ~msk) | ((y >> j) & msk) : (t & msk) | ((y & msk) << j);
+        for (int j = 16; j > 0; j >>= 1) {
+            const uint32_t msk = j == 16 ? 0x0000FFFFu : j == 8 ? 0x00FF00FFu : j == 4 ? 0x0F0F0F0Fu
+                                 : j == 2 ? 0x33333333u : 0x55555555u;
+            const uint32_t y = __shfl_xor_sync(0xffffffffu, t, j);
+            t = (lane & j) ? (t & ~msk) | ((y >> j) & msk) : (t & msk) | ((y & msk) << j);
+        }
+        bits_t[((bh * S + kb * 32 + lane) * S + qb * 32) >> 5] = t;
     }
-    bits_t[((bh * S + kb * 32 + lane) * S + qb * 32) >> 5] = t;
+}
+int g_mask_blocks = 0;  // grid of the keep-bit kernels: 0 full grid (measured best), -1 one block per SM, n > 0 n blocks
+void set_mask_blocks(int n) { g_mask_blocks = n; }
+static unsigned mask_grid(long long work_blocks) {
+    if (g_mask_blocks == 0) return (unsigned)std::max(1ll, work_blocks);
+    if (g_mask_blocks > 0) return (unsigned)g_mask_blocks;
+    static int sms = 0;
+    if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    return (unsigned)sms;
 }
 void dropout_mask_dual(uint32_t* bits, i64 BH, i64 S, u64 s1, u64 thr, cudaStream_t s) {
-    if (S % 128) throw std::runtime_error("dropout_mask_dual: S % 128 != 0");
+    if (S % 32) throw std::runtime_error("dropout_mask_dual: S % 32 != 0");
     const i64 words = BH * S * S / 32;
-    dim3 grid((unsigned)BH, (unsigned)(S / 32), (unsigned)(S / 128));
-    k_dropout_mask_dual<<<grid, 128, 0, s>>>(bits, bits + words, (int)S, s1, thr);
+    const i64 nblk = BH * (S / 32) * (S / 32);
+    const unsigned grid = mask_grid((nblk + 3) / 4);
+    static bool attr = false;
+    if (!attr) {
+        // same shared-memory carveout as the GEMM / attention kernels, so an SM never has to
+        // drain to reconfigure between them and the side-stream hashing can co-reside
+        cudaFuncSetAttribute(k_dropout_mask_dual, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        attr = true;
+    }
+    k_dropout_mask_dual<<<grid, 128, 0, s>>>(bits, bits + words, (int)S, BH, s1, thr);
+    SBK_CHECK_LAUNCH();
+}
+void dropout_mask(uint32_t* bits, i64 n, u64 s1, u64 thr, cudaStream_t s) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_dropout_mask, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        attr = true;
+    }
+    k_dropout_mask<<<mask_grid(((n + 31) / 32 + 127) / 128), 128, 0, s>>>(bits, n, s1, thr);
     SBK_CHECK_LAUNCH();
 }
 

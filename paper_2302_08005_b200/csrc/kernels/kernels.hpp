@@ -89,6 +89,7 @@ void dropout_mask(uint32_t* bits, i64 n, u64 s1, u64 thr, cudaStream_t s);
 // at bit e%32 of word e/32), bits[W, 2W) transposed (element ((bh*S+j)*S+i)),
 // W = BH*S*S/32; S % 128 == 0
 void dropout_mask_dual(uint32_t* bits, i64 BH, i64 S, u64 s1, u64 thr, cudaStream_t s);
+void set_mask_blocks(int n);  // experiments: persistent grid size of the keep-bit kernel (0 = full grid)
 
 // --------------------------------------------------------- strided copy
 // dst[idx] (+)= src[idx] over a rank<=8 index space with per-tensor strides.

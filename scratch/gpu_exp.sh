@@ -1,2 +1,4 @@
 cd $GRAFT_REPO_ROOT
-for c in 0 1; do timeout 600 python bench.py --no-cpu-baseline --steps 5 --gemm-cap $c --profile > gpurun_out/bench_c$c.json 2> gpurun_out/bench_c$c.err; done
+for ph in bwd fwd; do for mb in 0 148 296; do
+SB_MASK_PHASE=$ph timeout 600 python bench.py --no-cpu-baseline --steps 5 --mask-blocks $mb > gpurun_out/b_${ph}_$mb.json 2>/dev/null
+done; done
