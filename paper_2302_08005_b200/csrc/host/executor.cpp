@@ -1289,8 +1289,9 @@ public:
         for (size_t i = 0; i < ranks[0].P.fwd.size(); ++i) {
             // (in bwd placement inside a graph capture the masks were made before the
             // capture or by the previous replay's backward, which the stream order covers)
-            const bool wait = regen_bwd ? (!cap && ev_real[i]) : true;
-            if (mask_ev.size() > i && mask_ev[i] && wait) {
+            const bool has = mask_ev.size() > i && mask_ev[i];
+            const bool wait = has && (regen_bwd ? (!cap && ev_real.size() > i && ev_real[i]) : true);
+            if (wait) {
                 CK(cudaStreamWaitEvent(stream, mask_ev[i], 0));
                 last = mask_ev[i];
             }

@@ -22,7 +22,7 @@ bool bdrln_fwd_vec(const void* partial, const void* bias, const void* res, const
 bool ln_bwd_vec(int mode, const void* x, const float* mean, const float* rstd, const void* gamma, const void* g, void* gx,
                 void* gres, bool gx_acc, bool gres_acc, DT t, i64 rows, i64 n, u64 s1, u64 thr, float dscale,
                 const uint32_t* keep, float* ws, int ncol, int nblocks, cudaStream_t s);
-static int vec_blocks(i64 rows) { return (int)std::min<i64>(148, std::max<i64>(1, (rows + kWarps - 1) / kWarps)); }
+static int vec_blocks(i64 rows) { return (int)std::min<i64>(296, std::max<i64>(1, (rows + kWarps - 1) / kWarps)); }
 
 // ------------------------------------------------------------------ softmax
 template <class T>
@@ -194,15 +194,27 @@ __global__ void k_ln_bwd(const T* x, const float* mean, const float* rstd, const
         ws[(i64)blockIdx.x * ncol * n + i] = acc;
     }
 }
+// block = 32 columns x 8 warps: warp w sums partial rows w, w+8, ... of its lane's
+// column, then warp 0 adds the 8 sums in warp order (fixed order: deterministic)
 __global__ void k_col_final(const float* ws, int blocks, i64 ncoln, float* o0, float* o1, float* o2, i64 n, bool accum) {
-    for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < ncoln; i += (i64)gridDim.x * blockDim.x) {
-        float acc = 0.f;
-        for (int b = 0; b < blocks; ++b) acc += ws[(i64)b * ncoln + i];
+    __shared__ float part[8][32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const i64 i = blockIdx.x * 32ll + lane;
+    float acc = 0.f;
+    if (i < ncoln)
+        for (int b = warp; b < blocks; b += 8) acc += ws[(i64)b * ncoln + i];
+    part[warp][lane] = acc;
+    __syncthreads();
+    if (warp == 0 && i < ncoln) {
+        float t = 0.f;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) t += part[w][lane];
         int k = (int)(i / n);
         float* o = k == 0 ? o0 : k == 1 ? o1 : o2;
-        if (o) o[i % n] = accum ? o[i % n] + acc : acc;
+        if (o) o[i % n] = accum ? o[i % n] + t : t;
     }
 }
+static unsigned col_final_grid(i64 ncoln) { return (unsigned)((ncoln + 31) / 32); }
 static int row_blocks(i64 rows) { return (int)std::min<i64>(kRowBlocks, std::max<i64>(1, (rows + kWarps - 1) / kWarps)); }
 size_t layernorm_bwd_workspace(i64 rows, i64 n) { return (size_t)row_blocks(rows) * 2 * n * 4; }
 size_t bdrln_bwd_workspace(i64 rows, i64 n) { return (size_t)row_blocks(rows) * 3 * n * 4; }
@@ -220,7 +232,7 @@ void layernorm_bwd(const void* x, const float* mean, const float* rstd, const vo
     int ncol = (dgamma || dbeta) ? 2 : 0;
     int vb = vec_blocks(rows);
     if (ln_bwd_vec(0, x, mean, rstd, gamma, g, gx, nullptr, gx_acc, true, t, rows, n, 0, 0, 1.f, nullptr, ws, ncol, vb, s)) {
-        if (ncol) k_col_final<<<grid_for(2 * n, 256), 256, 0, s>>>(ws, vb, 2 * n, dgamma, dbeta, nullptr, n, col_acc);
+        if (ncol) k_col_final<<<col_final_grid(2 * n), 256, 0, s>>>(ws, vb, 2 * n, dgamma, dbeta, nullptr, n, col_acc);
         SBK_CHECK_LAUNCH();
         return;
     }
@@ -233,7 +245,7 @@ void layernorm_bwd(const void* x, const float* mean, const float* rstd, const vo
         k<<<nb, 32 * kWarps, smem, s>>>((const T*)x, mean, rstd, (const T*)gamma, (const T*)g, (T*)gx, nullptr, gx_acc,
                                         rows, n, 0, 0, 1.f, ws, ncol, true);
     });
-    if (ncol) k_col_final<<<grid_for(2 * n, 256), 256, 0, s>>>(ws, nb, 2 * n, dgamma, dbeta, nullptr, n, col_acc);
+    if (ncol) k_col_final<<<col_final_grid(2 * n), 256, 0, s>>>(ws, nb, 2 * n, dgamma, dbeta, nullptr, n, col_acc);
     SBK_CHECK_LAUNCH();
 }
 
@@ -289,7 +301,7 @@ void bias_dropout_residual_ln_bwd(const void* sum, const float* mean, const floa
     int vb = vec_blocks(rows);
     if (ln_bwd_vec(1, sum, mean, rstd, gamma, g, g_partial, g_res, g_partial_acc, gres_acc, t, rows, n, s1, thr, dscale,
                    keep, ws, ncol, vb, s)) {
-        k_col_final<<<grid_for(3 * n, 256), 256, 0, s>>>(ws, vb, 3 * n, dgamma, dbeta, dbias, n, col_acc);
+        k_col_final<<<col_final_grid(3 * n), 256, 0, s>>>(ws, vb, 3 * n, dgamma, dbeta, dbias, n, col_acc);
         SBK_CHECK_LAUNCH();
         return;
     }
@@ -302,7 +314,7 @@ void bias_dropout_residual_ln_bwd(const void* sum, const float* mean, const floa
         k<<<nb, 32 * kWarps, smem, s>>>((const T*)sum, mean, rstd, (const T*)gamma, (const T*)g, (T*)g_partial, (T*)g_res,
                                         g_partial_acc, rows, n, s1, thr, dscale, ws, ncol, gres_acc);
     });
-    k_col_final<<<grid_for(3 * n, 256), 256, 0, s>>>(ws, nb, 3 * n, dgamma, dbeta, dbias, n, col_acc);
+    k_col_final<<<col_final_grid(3 * n), 256, 0, s>>>(ws, nb, 3 * n, dgamma, dbeta, dbias, n, col_acc);
     SBK_CHECK_LAUNCH();
 }
 

@@ -81,6 +81,15 @@ __device__ __forceinline__ void stats(const float (&v)[CPL][VN], float n, float 
 __device__ __forceinline__ int col_of(int c, int lane, int e, int VN) { return (c * 32 + lane) * VN + e; }
 // the VN keep bits of elements idx0 .. idx0+VN-1 (idx0 % VN == 0, VN <= 8) from a
 // dropout_mask bit array (bit i of word w = element 32w + i, i.e. byte idx/8, bit idx%8)
+// keep bits of VN consecutive elements hashed in place (no precomputed bits);
+// out of line so the hash does not inflate the register budget of the caller
+template <int VN>
+__device__ __noinline__ uint32_t hash_keep_bits(uint64_t s1, uint64_t thr, i64 idx0) {
+    uint32_t m = 0;
+    for (int e = 0; e < VN; ++e)
+        if (d_keep(s1, (uint64_t)(idx0 + e), thr)) m |= 1u << e;
+    return m;
+}
 template <int VN>
 __device__ __forceinline__ uint32_t keep_bits(const uint32_t* keep, i64 idx0) {
     const uint32_t byte = ((const uint8_t*)keep)[idx0 >> 3];
@@ -273,6 +282,141 @@ __global__ void __launch_bounds__(32 * kW, 1)
     }
 }
 
+// The same backward with WPR warps per row (each warp owns CPL/WPR 16-byte
+// column chunks): a quarter of the registers of the warp-per-row kernel (the
+// per-column dgamma/dbeta/dbias partials dominate), so 16-warp blocks fit and
+// co-reside with other work. The two row sums are combined across the WPR warps
+// through shared memory in a fixed order (deterministic).
+template <class T, int CPL, int MODE, int WPR>
+__global__ void __launch_bounds__(512, 1)
+    k_ln_bwd_w(const T* x, const float* mean, const float* rstd, const T* gamma, const T* g, T* gx, T* gres, bool gx_acc,
+               i64 rows, int n, uint64_t s1, uint64_t thr, float dscale, const uint32_t* keep, float* ws, int ncol,
+               bool gres_acc) {
+    constexpr int VN = Vec<T>::N, CW = CPL / WPR, RPB = 16 / WPR;  // chunks per warp, rows per block pass
+    extern __shared__ float sh[];  // [16 warps][ncol][CW*32*VN] column partials | red[2][16][2]
+    float* red = sh + (size_t)16 * ncol * (CW * 32 * VN);
+    const int warp = threadIdx.x / 32, lane = threadIdx.x & 31, slot = warp / WPR, part = warp % WPR;
+    using V = Vec<T>;
+    float gm[CW][VN];
+    if (gamma) {
+#pragma unroll
+        for (int c = 0; c < CW; ++c) V::unpack(((const typename V::R*)gamma)[(part * CW + c) * 32 + lane], gm[c]);
+    }
+    float pg[CW][VN] = {}, pb[CW][VN] = {}, pd[CW][VN] = {};
+    int it = 0;
+    for (i64 row = (i64)blockIdx.x * RPB + slot; row < rows; row += (i64)gridDim.x * RPB, ++it) {
+        float xv[CW][VN], gv[CW][VN];
+        const typename V::R* xr = (const typename V::R*)(x + row * n);
+        const typename V::R* gr = (const typename V::R*)(g + row * n);
+#pragma unroll
+        for (int c = 0; c < CW; ++c) {
+            V::unpack(xr[(part * CW + c) * 32 + lane], xv[c]);
+            V::unpack(gr[(part * CW + c) * 32 + lane], gv[c]);
+        }
+        const float mu = mean[row], rs = rstd[row];
+        float a = 0.f, b = 0.f;
+#pragma unroll
+        for (int c = 0; c < CW; ++c)
+#pragma unroll
+            for (int e = 0; e < VN; ++e) {
+                const float xh = (xv[c][e] - mu) * rs;
+                const float gh = gamma ? gv[c][e] * gm[c][e] : gv[c][e];
+                a += gh;
+                b += gh * xh;
+                pg[c][e] += gv[c][e] * xh;
+                pb[c][e] += gv[c][e];
+                xv[c][e] = xh;
+            }
+        a = warp_sum(a);
+        b = warp_sum(b);
+        if (WPR > 1) {
+            float* rr = red + ((it & 1) * 16 + warp) * 2;
+            if (lane == 0) {
+                rr[0] = a;
+                rr[1] = b;
+            }
+            asm volatile("bar.sync %0, %1;" ::"r"(1 + slot), "r"(32 * WPR) : "memory");
+            const float* r0 = red + ((it & 1) * 16 + slot * WPR) * 2;
+            a = 0.f;
+            b = 0.f;
+#pragma unroll
+            for (int w = 0; w < WPR; ++w) {
+                a += r0[2 * w];
+                b += r0[2 * w + 1];
+            }
+        }
+        a /= (float)n;
+        b /= (float)n;
+#pragma unroll
+        for (int c = 0; c < CW; ++c)
+#pragma unroll
+            for (int e = 0; e < VN; ++e) {
+                const float gh = gamma ? gv[c][e] * gm[c][e] : gv[c][e];
+                gv[c][e] = rs * (gh - a - xv[c][e] * b);  // d(sum) / dx
+            }
+        typename V::R* gxr = (typename V::R*)(gx + row * n);
+        if (MODE == 0) {
+#pragma unroll
+            for (int c = 0; c < CW; ++c) {
+                float o[VN];
+                if (gx_acc) V::unpack(gxr[(part * CW + c) * 32 + lane], o);
+#pragma unroll
+                for (int e = 0; e < VN; ++e) o[e] = (gx_acc ? o[e] : 0.f) + gv[c][e];
+                gxr[(part * CW + c) * 32 + lane] = V::pack(o);
+            }
+        } else {
+            typename V::R* grr = (typename V::R*)(gres + row * n);
+#pragma unroll
+            for (int c = 0; c < CW; ++c) {
+                const int ch = (part * CW + c) * 32 + lane;
+                float o[VN];
+                if (gres_acc) V::unpack(grr[ch], o);
+#pragma unroll
+                for (int e = 0; e < VN; ++e) o[e] = (gres_acc ? o[e] : 0.f) + gv[c][e];
+                grr[ch] = V::pack(o);
+                uint32_t kb = 0;
+                if (thr) kb = keep ? keep_bits<VN>(keep, row * n + (i64)ch * VN)
+                                   : hash_keep_bits<VN>(s1, thr, row * n + (i64)ch * VN);
+#pragma unroll
+                for (int e = 0; e < VN; ++e) {
+                    float d = gv[c][e];
+                    if (thr) d = ((kb >> e) & 1) ? d * dscale : 0.f;
+                    gv[c][e] = d;
+                    pd[c][e] += d;
+                }
+                if (gx_acc) {
+                    V::unpack(gxr[ch], o);
+#pragma unroll
+                    for (int e = 0; e < VN; ++e) gv[c][e] += o[e];
+                }
+                gxr[ch] = V::pack(gv[c]);
+            }
+        }
+    }
+    if (ncol == 0) return;
+    // column partials: warp's own segment, then a fixed-order sum over the row slots
+    constexpr int SEG = CW * 32 * VN;
+    float* mine = sh + (size_t)warp * ncol * SEG;
+#pragma unroll
+    for (int c = 0; c < CW; ++c)
+#pragma unroll
+        for (int e = 0; e < VN; ++e) {
+            const int lc = (c * 32 + lane) * VN + e;
+            mine[lc] = pg[c][e];
+            mine[SEG + lc] = pb[c][e];
+            if (ncol == 3) mine[2 * SEG + lc] = pd[c][e];
+        }
+    __syncthreads();
+    for (int i = threadIdx.x; i < ncol * n; i += blockDim.x) {
+        const int k = i / n, col = i % n;
+        // column col: chunk col / VN -> owning part = (chunk / 32) / CW, local = col - part * SEG
+        const int prt = (col / VN / 32) / CW, lc = col - prt * SEG;
+        float acc = 0.f;
+        for (int sl = 0; sl < RPB; ++sl) acc += sh[(size_t)(sl * WPR + prt) * ncol * SEG + (size_t)k * SEG + lc];
+        ws[(i64)blockIdx.x * ncol * n + i] = acc;
+    }
+}
+
 template <class T, class F>
 bool with_cpl(int n, F&& f) {
     constexpr int VN = Vec<T>::N;
@@ -352,8 +496,19 @@ bool ln_bwd_vec(int mode, const void* x, const float* mean, const float* rstd, c
                                                      (T*)gres, gx_acc, rows, (int)n, s1, thr, dscale, keep, ws,
                                                      ncol, gres_acc);
                 };
-                if (mode == 0) launch(k_ln_bwd_v<T, CPL, 0>);
-                else launch(k_ln_bwd_v<T, CPL, 1>);
+                if constexpr (CPL % 4 == 0) {
+                    // 4 warps per row, 16-warp blocks, two blocks per SM
+                    constexpr int WPR = 4;
+                    const size_t sm2 = (size_t)16 * ncol * (n / WPR) * 4 + 2 * 16 * 2 * 4;
+                    auto k = mode == 0 ? k_ln_bwd_w<T, CPL, 0, WPR> : k_ln_bwd_w<T, CPL, 1, WPR>;
+                    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+                    k<<<nblocks, 512, sm2, s>>>((const T*)x, mean, rstd, (const T*)gamma, (const T*)g, (T*)gx, (T*)gres,
+                                                 gx_acc, rows, (int)n, s1, thr, dscale, keep, ws, ncol, gres_acc);
+                } else if (mode == 0) {
+                    launch(k_ln_bwd_v<T, CPL, 0>);
+                } else {
+                    launch(k_ln_bwd_v<T, CPL, 1>);
+                }
             });
         }
     });

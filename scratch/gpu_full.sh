@@ -1,5 +1,3 @@
 cd $GRAFT_REPO_ROOT
 timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
 timeout 600 python bench.py --no-cpu-baseline > gpurun_out/bench.json 2> gpurun_out/bench.err
-timeout 600 python bench.py --no-cpu-baseline --profile --steps 5 > gpurun_out/bench_prof.json 2> gpurun_out/bench_prof.err
-timeout 600 python bench.py --no-cpu-baseline --steps 5 --p 0.0 > gpurun_out/bench_p0.json 2> gpurun_out/bench_p0.err
