@@ -236,6 +236,14 @@ def main():
     if rank != 0:
         return
     burst, sustained, hbm, src = peaks()
+    traffic = None
+    try:  # DRAM bytes of the step's GEMM launches from the committed ncu capture (profiles/README.md)
+        with open(os.path.join(ROOT, "profiles", "r1_gemm_traffic.json")) as f:
+            tr = json.load(f)
+        if world == 1 and cfg["layers"] == CFG["layers"] and cfg["batch"] == CFG["batch"]:
+            traffic = tr["dram_read_bytes_per_step"] + tr["dram_write_bytes_per_step"]
+    except Exception:
+        traffic = None
     gemm_ms = prof.get("gemm", 0.0)
     gemm_tflop = prof.get("@gemm_gflop", 0.0) / 1000.0
     achieved = gemm_tflop / (gemm_ms / 1000.0) if gemm_ms > 0 else 0.0
@@ -251,7 +259,9 @@ def main():
                    "cuda_graph": use_graph},
         "roofline": {"bound": "tensor", "kernel": "tcgen05 GEMMs (all Linear fwd/dgrad/wgrad of the step)",
                      "achieved": achieved, "peak": sustained, "unit": "TFLOP/s", "frac": achieved / sustained,
-                     "peak_source": f"bf16_tflops_sustained ({src})", "traffic": None,
+                     "peak_source": f"bf16_tflops_sustained ({src})", "traffic": traffic,
+                     "traffic_unit": "DRAM bytes per step of all GEMM launches (ncu, profiles/r1_gemm_traffic.json)",
+                     "algorithmic_flop_per_byte": (gemm_tflop * 1e12 / traffic) if traffic else None,
                      "gemm_ms_per_step": gemm_ms, "gemm_tflop_per_step": gemm_tflop},
         "model_tflops": model_tflops, "model_flops_frac": model_tflops / sustained,
         "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": int(host_ids.nbytes),

@@ -1,2 +1,3 @@
 cd $GRAFT_REPO_ROOT
-timeout 600 ncu --metrics smsp__inst_executed_pipe_alu.sum,smsp__inst_executed_pipe_fma.sum,smsp__inst_executed_pipe_fmaheavy.sum,smsp__inst_executed_pipe_fmalite.sum,smsp__inst_executed.sum,sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active,sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active,sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_active,sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active,sm__issue_active.avg.pct_of_peak_sustained_active,gpu__time_duration.sum -k regex:"kmask" -c 2 ./scratch/hashbench/hb > gpurun_out/hb_ncu.log 2>&1
+timeout 1200 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none -k regex:"k_gemm2|k_gemm_tc|k_splitk" --csv --log-file gpurun_out/gemm_traffic.csv \
+    python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-graph > gpurun_out/gemm_traffic.log 2>&1
