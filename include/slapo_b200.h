@@ -133,6 +133,8 @@ int sb_gemm_engine(void);                /* engine of the last sb_gemm: 0 SIMT, 
 int sb_gemm_force_simt(int on);
 /* engine cap: 0 best available (2-SM > 1-SM tcgen05 > SIMT), 1 at most the 1-SM kernel, 2 SIMT */
 int sb_gemm_set_engine(int max_engine);
+/* 2-SM kernel cluster tile N: 0 default (256), 128 or 256 forced (tests) */
+int sb_gemm_set_tile_n(int bn);
 /* experiments: grid size of the keep-bit generator (0 = one warp per 32x32 block) */
 int sb_set_mask_blocks(int n);
 /* attention engine cap: 0 best available (tcgen05 > mma.sync > SIMT), 1 at most mma.sync, 2 SIMT;

@@ -488,6 +488,10 @@ int sb_set_mask_blocks(int n) {
     sbk::set_mask_blocks(n);
     return 0;
 }
+int sb_gemm_set_tile_n(int bn) {
+    sbk::gemm2_set_tile_n(bn);
+    return 0;
+}
 int sb_gemm_set_engine(int max_engine) {
     sbk::gemm_set_engine(max_engine);
     return 0;

@@ -25,6 +25,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <type_traits>
 
 #include "tc5.cuh"
 
@@ -35,14 +36,18 @@ using namespace tc5;
 namespace {
 
 constexpr int G_BM = 128;  // rows of A per CTA (cluster tile M = 256)
-constexpr int G_BN = 256;  // cluster tile N (each CTA loads 128 rows of B)
 constexpr int G_BK = 64;
-constexpr int G_ST = 6;
-constexpr int G_A = G_BM * G_BK * 2;         // 16 KB
-constexpr int G_B = (G_BN / 2) * G_BK * 2;   // 16 KB
-constexpr int G_STAGE = G_A + G_B;
-constexpr int G_EPI_BUF = 4096;              // one staging slot: 32 rows x 128 B
-constexpr int G_SMEM = 1024 + G_ST * G_STAGE + 8 * G_EPI_BUF + 256;
+constexpr int G_A = G_BM * G_BK * 2;  // 16 KB
+constexpr int G_EPI_BUF = 4096;       // one staging slot per epilogue warp: 32 rows x 128 B
+// cluster tile N = BN (256 or 128: the narrower tile evens out the last wave of
+// N = 1024 problems); each CTA loads BN/2 rows of B per stage
+template <int BN>
+struct Cfg {
+    static constexpr int B_BYTES = (BN / 2) * G_BK * 2;
+    static constexpr int STAGE = G_A + B_BYTES;
+    static constexpr int ST = BN == 256 ? 6 : 8;
+    static constexpr int SMEM = 1024 + ST * STAGE + 8 * G_EPI_BUF + 256;
+};
 
 __device__ __forceinline__ uint32_t cluster_rank() {
     uint32_t r;
@@ -145,10 +150,11 @@ struct Sched2 {
     __host__ __device__ int tiles() const { return m_blks * n_blks * splits; }
 };
 
-template <bool A_MN, bool B_MN>
+template <int G_BN, bool A_MN, bool B_MN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
     k_gemm2(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB,
             const __grid_constant__ CUtensorMap tC, const __grid_constant__ CUtensorMap tX, Epi2 ep, Sched2 sc) {
+    constexpr int G_ST = Cfg<G_BN>::ST, G_STAGE = Cfg<G_BN>::STAGE;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint8_t* epi = smem + G_ST * G_STAGE;  // [8 warps][4 KB staging]
@@ -224,7 +230,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
                     }
                     if (B_MN) {
                         tma_load_2sm(sb, &tB, fb, nb, kc);
-                        tma_load_2sm(sb + 8192, &tB, fb, nb + 64, kc);
+                        if (G_BN == 256) tma_load_2sm(sb + 8192, &tB, fb, nb + 64, kc);
                     } else {
                         tma_load_2sm(sb, &tB, fb, kc, nb);
                     }
@@ -434,23 +440,25 @@ bool make_store_map(CUtensorMap* m, const void* base, bool f32, long long cols, 
 
 int g_sms2 = 0;
 
-template <bool A_MN, bool B_MN>
+template <int BN, bool A_MN, bool B_MN>
 void launch2(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const CUtensorMap& tx, const Epi2& ep,
              const Sched2& sc, cudaStream_t s) {
-    auto k = k_gemm2<A_MN, B_MN>;
+    auto k = k_gemm2<BN, A_MN, B_MN>;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, G_SMEM);
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM);
         attr = true;
     }
     if (!g_sms2) cudaDeviceGetAttribute(&g_sms2, cudaDevAttrMultiProcessorCount, 0);
     const int clusters = std::min(sc.tiles(), g_sms2 / 2);
-    k<<<clusters * 2, 320, G_SMEM, s>>>(ta, tb, tc, tx, ep, sc);
+    k<<<clusters * 2, 320, Cfg<BN>::SMEM, s>>>(ta, tb, tc, tx, ep, sc);
 }
 
 }  // namespace
 
 bool g_tc2_disabled = false;
+int g_tc2_bn = 0;  // cluster tile N: 0 default (256), 128 or 256 forced (tests)
+void gemm2_set_tile_n(int bn) { g_tc2_bn = bn; }
 
 // splitk reduce kernel of gemm_tc.cu
 void splitk_reduce_launch(const float* partial, int splits, i64 M, i64 N, void* C, DT tc, i64 ldc, const void* bias,
@@ -475,13 +483,16 @@ bool gemm_tc2_try(const Gemm& g, cudaStream_t s) {
     memset(&tc, 0, sizeof(tc));
     memset(&tx, 0, sizeof(tx));
     if (!(a_mn ? make_map_bf16(&ta, g.A, M, K, lda, 64) : make_map_bf16(&ta, g.A, K, M, lda, G_BM))) return false;
+    if (!g_sms2) cudaDeviceGetAttribute(&g_sms2, cudaDevAttrMultiProcessorCount, 0);
+    const int clusters = g_sms2 / 2;
+    // tile N 256 (measured: the 256x128 tile, though it evens out the last wave of
+    // N = 1024 problems, runs 30-40% slower on the BERT-large shapes)
+    const int G_BN = g_tc2_bn ? g_tc2_bn : 256;
     if (!(b_mn ? make_map_bf16(&tb, g.B, N, K, ldb, 64) : make_map_bf16(&tb, g.B, K, N, ldb, G_BN / 2))) return false;
     const int kblocks = (int)(K / G_BK);
     const long long tiles = (M / 256) * (N / G_BN);
     int splits = 1;
     // long-K, few-tile problems (the weight gradients) -> deterministic split-K
-    if (!g_sms2) cudaDeviceGetAttribute(&g_sms2, cudaDevAttrMultiProcessorCount, 0);
-    const int clusters = g_sms2 / 2;
     if (tiles < clusters && kblocks >= 32 && g.ws && !g.epilogue) {
         const int want = (int)((clusters + tiles - 1) / tiles);
         for (int sp = std::min(want, 16); sp > 1; --sp)
@@ -516,10 +527,15 @@ bool gemm_tc2_try(const Gemm& g, cudaStream_t s) {
         cudaMemsetAsync(ts_buf, 0, 3 * 128 * 8, s);
         ep.ts = ts_buf;
     }
-    if (!a_mn && !b_mn) launch2<false, false>(ta, tb, tc, tx, ep, sc, s);
-    else if (!a_mn && b_mn) launch2<false, true>(ta, tb, tc, tx, ep, sc, s);
-    else if (a_mn && b_mn) launch2<true, true>(ta, tb, tc, tx, ep, sc, s);
-    else launch2<true, false>(ta, tb, tc, tx, ep, sc, s);
+    auto go = [&](auto bn) {
+        constexpr int BN = decltype(bn)::value;
+        if (!a_mn && !b_mn) launch2<BN, false, false>(ta, tb, tc, tx, ep, sc, s);
+        else if (!a_mn && b_mn) launch2<BN, false, true>(ta, tb, tc, tx, ep, sc, s);
+        else if (a_mn && b_mn) launch2<BN, true, true>(ta, tb, tc, tx, ep, sc, s);
+        else launch2<BN, true, false>(ta, tb, tc, tx, ep, sc, s);
+    };
+    if (G_BN == 256) go(std::integral_constant<int, 256>{});
+    else go(std::integral_constant<int, 128>{});
     SBK_CHECK_LAUNCH();
     if (ep.ts) {
         unsigned long long h[3 * 128];

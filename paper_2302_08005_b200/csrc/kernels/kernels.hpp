@@ -45,6 +45,8 @@ void gemm(const Gemm& g, cudaStream_t s);
 int gemm_last_engine();
 // engine cap: 0 best available, 1 at most the 1-SM tcgen05 kernel, 2 SIMT only
 void gemm_set_engine(int e);
+// 2-SM kernel cluster tile N: 0 default (256), 128 or 256 forced
+void gemm2_set_tile_n(int bn);
 // Force the SIMT engine (tests compare the tcgen05 kernel against it).
 void gemm_force_simt(bool on);
 // workspace the tcgen05 split-K path may use for an (M x N) fp32 output

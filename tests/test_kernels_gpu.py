@@ -115,9 +115,17 @@ def _gemm_engine(cap, *a, **k):
     return gemm(*a, cap=cap, **k)
 
 
+@pytest.fixture(params=[0, 128, 256], ids=["tileN-auto", "tileN-128", "tileN-256"])
+def tile_n(request):
+    L.sb_gemm_set_tile_n.argtypes = [ctypes.c_int]
+    L.sb_gemm_set_tile_n(request.param)
+    yield request.param
+    L.sb_gemm_set_tile_n(0)
+
+
 @pytest.mark.parametrize("layout", ["tn", "tn_bias", "tn_gelu", "nn", "nn_acc", "nn_dgelu", "nt_f32", "nt_f32_acc",
                                     "nt_splitk"])
-def test_gemm_2sm_vs_1sm(layout):
+def test_gemm_2sm_vs_1sm(layout, tile_n):
     """The 2-SM cta_group::2 kernel (engine 2, TMA-store epilogue) against the 1-SM kernel and fp32 torch,
     every operand layout / epilogue the executor uses, at shapes that need several tiles per cluster."""
     M, N, K = 1024, 768, 512
