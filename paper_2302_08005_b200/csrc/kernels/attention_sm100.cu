@@ -50,7 +50,8 @@ __global__ void __launch_bounds__(384, 1)
     k_fa5_fwd(const __grid_constant__ CUtensorMap tQ, const __grid_constant__ CUtensorMap tK,
               const __grid_constant__ CUtensorMap tV, const __grid_constant__ CUtensorMap tM, FwdArgs fa) {
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    // 1024-aligned, derived from smem_raw by pointer arithmetic so accesses stay ld/st.shared
+    uint8_t* smem = smem_raw + ((1024 - (tc5::smem_u32(smem_raw) & 1023)) & 1023);
     uint8_t* sQ = smem;                        // [2][FT][FD]
     uint8_t* sK = sQ + 2 * F_TILE_BYTES;       // [FNS][FT][FD]
     uint8_t* sV = sK + FNS * F_TILE_BYTES;     // [FNS][FT][FD]
@@ -420,7 +421,8 @@ __global__ void __launch_bounds__(512, 1)
               const __grid_constant__ CUtensorMap tQ, const __grid_constant__ CUtensorMap tdO,
               const __grid_constant__ CUtensorMap tM, BwdArgs ba) {
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    // 1024-aligned, derived from smem_raw by pointer arithmetic so accesses stay ld/st.shared
+    uint8_t* smem = smem_raw + ((1024 - (tc5::smem_u32(smem_raw) & 1023)) & 1023);
     uint8_t* sKV = smem;                        // [2] x {K, V}
     uint8_t* sStage = sKV + 4 * F_TILE_BYTES;   // [2][B_STAGE]
     uint8_t* sDS = sStage + 2 * B_STAGE;        // [2] x dS^T [2 q-blocks][128 keys][64 q] bf16, swizzled

@@ -156,7 +156,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
             const __grid_constant__ CUtensorMap tC, const __grid_constant__ CUtensorMap tX, Epi2 ep, Sched2 sc) {
     constexpr int G_ST = Cfg<G_BN>::ST, G_STAGE = Cfg<G_BN>::STAGE;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    // 1024-aligned, derived from smem_raw by pointer arithmetic so accesses stay ld/st.shared
+    uint8_t* smem = smem_raw + ((1024 - (tc5::smem_u32(smem_raw) & 1023)) & 1023);
     uint8_t* epi = smem + G_ST * G_STAGE;  // [8 warps][4 KB staging]
     uint64_t* full = (uint64_t*)(epi + 8 * G_EPI_BUF);
     uint64_t* empty = full + G_ST;
