@@ -460,22 +460,88 @@ __global__ void k_bias_partial(const T* g, i64 ld, i64 rows, i64 cols, float* pa
     for (i64 r = r0; r < r1; ++r) acc += to_f(g[r * ld + c]);
     part[(i64)blockIdx.y * cols + c] = acc;
 }
-__global__ void k_bias_final(const float* part, i64 chunks, i64 cols, float* db, bool accum) {
-    i64 c = blockIdx.x * (i64)blockDim.x + threadIdx.x;
-    if (c >= cols) return;
-    float acc = 0.f;
-    for (i64 k = 0; k < chunks; ++k) acc += part[k * cols + c];
-    db[c] = accum ? db[c] + acc : acc;
+// bf16, cols % 8 == 0, 16-byte aligned rows: thread = 8 columns (one 16-byte load per
+// row), 8 rows of loads in flight; row chunks of kBiasChunkV summed in row order
+constexpr int kBiasChunkV = 32;
+__global__ void k_bias_partial_v(const bf16* g, i64 ld, i64 rows, i64 cols, float* part) {
+    const i64 c8 = blockIdx.x * (i64)blockDim.x + threadIdx.x;  // 8-column group
+    if (c8 * 8 >= cols) return;
+    const i64 r0 = (i64)blockIdx.y * kBiasChunkV;
+    const i64 r1 = r0 + kBiasChunkV < rows ? r0 + kBiasChunkV : rows;
+    float acc[8] = {};
+    i64 r = r0;
+    for (; r + 8 <= r1; r += 8) {
+        uint4 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = __ldcs((const uint4*)(g + (r + u) * ld) + c8);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const __nv_bfloat162* h = (const __nv_bfloat162*)&v[u];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                float2 f = __bfloat1622float2(h[t]);
+                acc[2 * t] += f.x;
+                acc[2 * t + 1] += f.y;
+            }
+        }
+    }
+    for (; r < r1; ++r) {
+        uint4 v = *((const uint4*)(g + r * ld) + c8);
+        const __nv_bfloat162* h = (const __nv_bfloat162*)&v;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            float2 f = __bfloat1622float2(h[t]);
+            acc[2 * t] += f.x;
+            acc[2 * t + 1] += f.y;
+        }
+    }
+    float4* o = (float4*)(part + (i64)blockIdx.y * cols + c8 * 8);
+    o[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+    o[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
 }
-size_t bias_grad_workspace(i64 rows, i64 cols) { return (size_t)((rows + kBiasChunk - 1) / kBiasChunk) * cols * 4; }
+// block = 32 columns x 32 warps: warp w sums chunks w, w+32, ... (4 loads in flight);
+// then the 32 sums in warp order (fixed order: deterministic)
+__global__ void __launch_bounds__(1024) k_bias_final(const float* part, i64 chunks, i64 cols, float* db, bool accum) {
+    __shared__ float s[32][33];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const i64 c = blockIdx.x * 32ll + lane;
+    float acc = 0.f;
+    if (c < cols) {
+        i64 k = warp;
+        for (; k + 96 < chunks; k += 128) {
+            const float a0 = part[k * cols + c], a1 = part[(k + 32) * cols + c], a2 = part[(k + 64) * cols + c],
+                        a3 = part[(k + 96) * cols + c];
+            acc += a0;
+            acc += a1;
+            acc += a2;
+            acc += a3;
+        }
+        for (; k < chunks; k += 32) acc += part[k * cols + c];
+    }
+    s[warp][lane] = acc;
+    __syncthreads();
+    if (warp == 0 && c < cols) {
+        float t = 0.f;
+#pragma unroll
+        for (int w = 0; w < 32; ++w) t += s[w][lane];
+        db[c] = accum ? db[c] + t : t;
+    }
+}
+size_t bias_grad_workspace(i64 rows, i64 cols) { return (size_t)((rows + kBiasChunkV - 1) / kBiasChunkV) * cols * 4; }
 void bias_grad(const void* g, DT tg, i64 ld, i64 rows, i64 cols, float* db, float* ws, cudaStream_t s, bool accum) {
     i64 chunks = (rows + kBiasChunk - 1) / kBiasChunk;
-    dim3 grid((unsigned)((cols + 127) / 128), (unsigned)chunks);
-    dispatch(tg, [&](auto* p) {
-        using T = std::remove_pointer_t<decltype(p)>;
-        k_bias_partial<T><<<grid, 128, 0, s>>>((const T*)g, ld, rows, cols, ws);
-    });
-    k_bias_final<<<(unsigned)((cols + 255) / 256), 256, 0, s>>>(ws, chunks, cols, db, accum);
+    if (tg == BF16 && cols % 8 == 0 && ld % 8 == 0 && ((uintptr_t)g & 15) == 0) {
+        chunks = (rows + kBiasChunkV - 1) / kBiasChunkV;
+        dim3 grid((unsigned)((cols / 8 + 127) / 128), (unsigned)chunks);
+        k_bias_partial_v<<<grid, 128, 0, s>>>((const bf16*)g, ld, rows, cols, ws);
+    } else {
+        dim3 grid((unsigned)((cols + 127) / 128), (unsigned)chunks);
+        dispatch(tg, [&](auto* p) {
+            using T = std::remove_pointer_t<decltype(p)>;
+            k_bias_partial<T><<<grid, 128, 0, s>>>((const T*)g, ld, rows, cols, ws);
+        });
+    }
+    k_bias_final<<<(unsigned)((cols + 31) / 32), 1024, 0, s>>>(ws, chunks, cols, db, accum);
     SBK_CHECK_LAUNCH();
 }
 
