@@ -1227,7 +1227,10 @@ public:
         bwd_ev.assign(P.fwd.size(), nullptr);
         for (size_t i = 0; i < P.fwd.size(); ++i)
             if (mask_ev[i]) CK(cudaEventCreateWithFlags(&bwd_ev[i], cudaEventDisableTiming));
-        if (const char* e = getenv("SB_MASK_PHASE")) regen_bwd = std::string(e) != "fwd";
+        if (const char* e = getenv("SB_MASK_PHASE")) {
+            regen_bwd = std::string(e) == "bwd";  // anything else: "fwd" or "inline"
+            mask_inline = std::string(e) == "inline";
+        }
         int lo, hi;
         CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
         CK(cudaStreamCreateWithPriority(&mstream, cudaStreamNonBlocking, lo));  // lo = least priority
@@ -1238,13 +1241,16 @@ public:
     // executor.cpp:788-806), so every forward of this executor reads the same bits.
     // They are regenerated every step on a low-priority side stream (small
     // co-residing blocks, kernels/elementwise.cu). Placement (SB_MASK_PHASE):
-    //   "bwd" (default): all masks before the first forward, then each step
-    //     regenerates mask i right after its last reader (op i's backward),
-    //     overlapping the rest of the backward;
-    //   "fwd": at the start of every forward, layer by layer ahead of the readers.
-    // Readers wait on mask_ev[i] only.
+    //   "fwd" (default): at the start of every forward, layer by layer ahead of
+    //     the readers (each reader waits on mask_ev[i] only);
+    //   "bwd": all masks before the first forward, then each step regenerates
+    //     mask i right after its last reader (op i's backward);
+    //   "inline": on the executor stream right before each reader.
+    // The three measure within 2% of each other at C3: the hashing is integer-ALU
+    // bound and costs its full duration wherever it runs.
     bool masks_valid = false;
-    bool regen_bwd = true;
+    bool regen_bwd = false;  // default "fwd" placement (measured best of fwd / bwd / inline)
+    bool mask_inline = false;  // "inline": on the executor stream right before each reader (no overlap)
     std::vector<cudaEvent_t> bwd_ev;  // per forward op index: its backward was enqueued
     std::vector<char> ev_real;        // mask_ev[i] last recorded outside a graph capture (waitable)
 
@@ -1254,20 +1260,23 @@ public:
         return st != cudaStreamCaptureStatusNone;
     }
 
-    void gen_mask(size_t i) {
+    void gen_mask(size_t i, cudaStream_t ms = nullptr) {
+        const bool side = ms == nullptr;
+        if (side) ms = mstream;
         for (auto& r : ranks) {
             const Op& op = r.P.fwd[i];
             if (op.k == K::FusedLinearResLN) {
                 const View& y = V(r, op.out[0]);
-                sbk::dropout_mask((uint32_t*)fp(r, op.out[5]), rows_of(y) * cols_of(y), op.s1, op.thr, mstream);
+                sbk::dropout_mask((uint32_t*)fp(r, op.out[5]), rows_of(y) * cols_of(y), op.s1, op.thr, ms);
                 continue;
             }
             sbk::Attn a = attn_args(r, op);
             if (a.S % 128 == 0)
-                sbk::dropout_mask_dual((uint32_t*)fp(r, op.out[2]), a.B * a.nh, a.S, op.s1, op.thr, mstream);
+                sbk::dropout_mask_dual((uint32_t*)fp(r, op.out[2]), a.B * a.nh, a.S, op.s1, op.thr, ms);
             else
-                sbk::dropout_mask((uint32_t*)fp(r, op.out[2]), a.B * a.nh * a.S * a.S, op.s1, op.thr, mstream);
+                sbk::dropout_mask((uint32_t*)fp(r, op.out[2]), a.B * a.nh * a.S * a.S, op.s1, op.thr, ms);
         }
+        if (!side) return;
         CK(cudaEventRecord(mask_ev[i], mstream));
         if (ev_real.size() != mask_ev.size()) ev_real.assign(mask_ev.size(), 0);
         ev_real[i] = !capturing();
@@ -1283,6 +1292,14 @@ public:
     }
 
     void run_forward() {
+        if (mask_inline) {
+            for (size_t i = 0; i < ranks[0].P.fwd.size(); ++i) {
+                if (mask_ev.size() > i && mask_ev[i]) gen_mask(i, stream);
+                fwd_op((int)i);
+            }
+            ran_forward = true;
+            return;
+        }
         if (!regen_bwd || !masks_valid) launch_masks();
         const bool cap = capturing();
         cudaEvent_t last = nullptr;
@@ -1328,7 +1345,7 @@ public:
                 bwd_op(s.idx);
                 cur_ow = nullptr;
                 const size_t i = (size_t)s.idx;
-                if (regen_bwd && masks_valid && mstream && mask_ev.size() > i && mask_ev[i]) {
+                if (regen_bwd && !mask_inline && masks_valid && mstream && mask_ev.size() > i && mask_ev[i]) {
                     // last reader of mask i done: regenerate it for the next step
                     CK(cudaEventRecord(bwd_ev[i], stream));
                     CK(cudaStreamWaitEvent(mstream, bwd_ev[i], 0));
@@ -1517,7 +1534,7 @@ void Executor::capture_graph() {
     if (I.comm.nccl && I.world > 1) {
         // NCCL kernels are capturable; nothing special beyond using our stream.
     }
-    if (I.regen_bwd && !I.masks_valid && I.mstream) {  // the graph regenerates masks in its backward; prime once
+    if (I.regen_bwd && !I.mask_inline && !I.masks_valid && I.mstream) {  // the graph regenerates masks in its backward; prime once
         I.launch_masks();
         CK(cudaStreamSynchronize(I.mstream));
     }

@@ -179,65 +179,87 @@ __global__ void __launch_bounds__(32 * kW) k_bdrln_fwd_v(const T* partial, const
 }
 
 // bias+dropout+residual+LayerNorm forward with WPR warps per row (each warp owns
-// CPL/WPR 16-byte column chunks): few registers, 16-warp blocks; the row mean and
-// variance are combined across the WPR warps through shared memory in a fixed order.
-template <class T, int CPL, int WPR>
+// CPL/WPR 16-byte column chunks) and NR rows per warp group in flight (all their
+// loads issued before any math: bytes in flight for HBM): few registers, 16-warp
+// blocks; the row mean and variance are combined across the WPR warps through
+// shared memory in a fixed order.
+template <class T, int CPL, int WPR, int NR>
 __global__ void __launch_bounds__(512) k_bdrln_fwd_w(const T* partial, const T* bias, const T* res, const T* gamma,
                                                      const T* beta, T* sum, T* y, float* mean, float* rstd, i64 rows,
                                                      int n, float eps, uint64_t s1, uint64_t thr, float dscale,
                                                      const uint32_t* keep) {
     using V = Vec<T>;
     constexpr int VN = V::N, CW = CPL / WPR, RPB = 16 / WPR;
-    __shared__ float red[2][16];
+    __shared__ float red[2][16][NR];
     const int warp = threadIdx.x / 32, lane = threadIdx.x & 31, slot = warp / WPR, part = warp % WPR;
-    const i64 row = (i64)blockIdx.x * RPB + slot;
-    if (row >= rows) return;  // whole row groups exit together (RPB rows per block)
-    float v[CW][VN];
-    const typename V::R* pr = (const typename V::R*)(partial + row * n);
-    const typename V::R* rr = (const typename V::R*)(res + row * n);
+    const i64 row0 = ((i64)blockIdx.x * RPB + slot) * NR;  // NR consecutive rows of this group
+    if (row0 >= rows) return;  // rows % (RPB * NR) == 0: whole groups exit together
+    typename V::R pv[NR][CW], rv[NR][CW];
 #pragma unroll
-    for (int c = 0; c < CW; ++c) {
-        const int ch = (part * CW + c) * 32 + lane;
-        float r[VN], bb[VN];
-        V::unpack(pr[ch], v[c]);
-        V::unpack(rr[ch], r);
-        if (bias) V::unpack(((const typename V::R*)bias)[ch], bb);
-        uint32_t kb = 0;
-        if (thr) kb = keep ? keep_bits<VN>(keep, row * n + (i64)ch * VN) : hash_keep_bits<VN>(s1, thr, row * n + (i64)ch * VN);
+    for (int k = 0; k < NR; ++k)
 #pragma unroll
-        for (int e = 0; e < VN; ++e) {
-            float t = v[c][e] + (bias ? bb[e] : 0.f);
-            if (thr) t = ((kb >> e) & 1) ? t * dscale : 0.f;
-            v[c][e] = to_f(from_f<T>(t + r[e]));  // `sum` is rounded to the storage dtype before the statistics
+        for (int c = 0; c < CW; ++c) {
+            const int ch = (part * CW + c) * 32 + lane;
+            pv[k][c] = __ldcs((const typename V::R*)(partial + (row0 + k) * n) + ch);
+            rv[k][c] = __ldcs((const typename V::R*)(res + (row0 + k) * n) + ch);
         }
-        ((typename V::R*)(sum + row * n))[ch] = V::pack(v[c]);
+    float v[NR][CW][VN];
+    float sm[NR];
+#pragma unroll
+    for (int k = 0; k < NR; ++k) {
+        sm[k] = 0.f;
+#pragma unroll
+        for (int c = 0; c < CW; ++c) {
+            const int ch = (part * CW + c) * 32 + lane;
+            float r[VN], bb[VN];
+            V::unpack(pv[k][c], v[k][c]);
+            V::unpack(rv[k][c], r);
+            if (bias) V::unpack(((const typename V::R*)bias)[ch], bb);
+            uint32_t kb = 0;
+            if (thr)
+                kb = keep ? keep_bits<VN>(keep, (row0 + k) * n + (i64)ch * VN)
+                          : hash_keep_bits<VN>(s1, thr, (row0 + k) * n + (i64)ch * VN);
+#pragma unroll
+            for (int e = 0; e < VN; ++e) {
+                float t = v[k][c][e] + (bias ? bb[e] : 0.f);
+                if (thr) t = ((kb >> e) & 1) ? t * dscale : 0.f;
+                v[k][c][e] = to_f(from_f<T>(t + r[e]));  // `sum` is rounded to the storage dtype before the statistics
+                sm[k] += v[k][c][e];
+            }
+            ((typename V::R*)(sum + (row0 + k) * n))[ch] = V::pack(v[k][c]);
+        }
     }
-    auto row_sum = [&](float x, int which) {
-        x = warp_sum(x);
+    auto row_sums = [&](float (&x)[NR], int which) {
+#pragma unroll
+        for (int k = 0; k < NR; ++k) x[k] = warp_sum(x[k]);
         if (WPR > 1) {
-            if (lane == 0) red[which][warp] = x;
+            if (lane == 0)
+#pragma unroll
+                for (int k = 0; k < NR; ++k) red[which][warp][k] = x[k];
             asm volatile("bar.sync %0, %1;" ::"r"(1 + slot), "r"(32 * WPR) : "memory");
-            x = 0.f;
 #pragma unroll
-            for (int w = 0; w < WPR; ++w) x += red[which][slot * WPR + w];
+            for (int k = 0; k < NR; ++k) {
+                x[k] = 0.f;
+#pragma unroll
+                for (int w = 0; w < WPR; ++w) x[k] += red[which][slot * WPR + w][k];
+            }
         }
-        return x;
     };
-    float s = 0.f;
+    row_sums(sm, 0);
+    float mu[NR], q[NR];
 #pragma unroll
-    for (int c = 0; c < CW; ++c)
+    for (int k = 0; k < NR; ++k) {
+        mu[k] = sm[k] / (float)n;
+        q[k] = 0.f;
 #pragma unroll
-        for (int e = 0; e < VN; ++e) s += v[c][e];
-    const float mu = row_sum(s, 0) / (float)n;
-    float q = 0.f;
+        for (int c = 0; c < CW; ++c)
 #pragma unroll
-    for (int c = 0; c < CW; ++c)
-#pragma unroll
-        for (int e = 0; e < VN; ++e) {
-            const float d = v[c][e] - mu;
-            q += d * d;
-        }
-    const float rs = rsqrtf(row_sum(q, 1) / (float)n + eps);
+            for (int e = 0; e < VN; ++e) {
+                const float d = v[k][c][e] - mu[k];
+                q[k] += d * d;
+            }
+    }
+    row_sums(q, 1);
 #pragma unroll
     for (int c = 0; c < CW; ++c) {
         const int ch = (part * CW + c) * 32 + lane;
@@ -245,13 +267,20 @@ __global__ void __launch_bounds__(512) k_bdrln_fwd_w(const T* partial, const T* 
         V::unpack(((const typename V::R*)gamma)[ch], gm);
         V::unpack(((const typename V::R*)beta)[ch], bt);
 #pragma unroll
-        for (int e = 0; e < VN; ++e) v[c][e] = gm[e] * ((v[c][e] - mu) * rs) + bt[e];
-        ((typename V::R*)(y + row * n))[ch] = V::pack(v[c]);
+        for (int k = 0; k < NR; ++k) {
+            const float rs = rsqrtf(q[k] / (float)n + eps);
+            float o[VN];
+#pragma unroll
+            for (int e = 0; e < VN; ++e) o[e] = gm[e] * ((v[k][c][e] - mu[k]) * rs) + bt[e];
+            ((typename V::R*)(y + (row0 + k) * n))[ch] = V::pack(o);
+        }
     }
-    if (lane == 0 && part == 0) {
-        mean[row] = mu;
-        rstd[row] = rs;
-    }
+    if (lane == 0 && part == 0)
+#pragma unroll
+        for (int k = 0; k < NR; ++k) {
+            mean[row0 + k] = mu[k];
+            rstd[row0 + k] = rsqrtf(q[k] / (float)n + eps);
+        }
 }
 
 // MODE 0: LayerNorm backward (gx += ...). MODE 1: fused bias+dropout+residual+LN
@@ -544,8 +573,8 @@ bool bdrln_fwd_vec(const void* partial, const void* bias, const void* res, const
                 constexpr int CPL = decltype(cc)::value;
                 if constexpr (CPL % 4 == 0) {
                     // 4 warps per row, 16-warp blocks (4 rows per block)
-                    if (rows % 4 == 0) {
-                        k_bdrln_fwd_w<T, CPL, 4><<<(unsigned)(rows / 4), 512, 0, s>>>(
+                    if (rows % 16 == 0) {
+                        k_bdrln_fwd_w<T, CPL, 4, 4><<<(unsigned)(rows / 16), 512, 0, s>>>(
                             (const T*)partial, (const T*)bias, (const T*)res, (const T*)gamma, (const T*)beta, (T*)sum,
                             (T*)y, mean, rstd, rows, (int)n, eps, s1, thr, dscale, keep);
                         return;
