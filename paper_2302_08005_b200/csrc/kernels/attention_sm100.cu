@@ -295,7 +295,8 @@ bool fwd_fits(const Attn& a) {
 // are drained by the softmax warps while block j+1 starts.
 // delta_q = dO_q . O_q and lse2 = lse * log2(e) come from k_fa5_prep.
 constexpr int B_STAGE = 2 * F_TILE_BYTES + 1024 + 2048;  // Q, dO, lse2[128], delta[128], keep bits [128][4]
-constexpr int B_SMEM = 1024 + 4 * F_TILE_BYTES + 2 * B_STAGE + 4 * F_TILE_BYTES + 12 * 2048 + 256;
+constexpr int B_NST = 3;  // Q / dO / lse / delta / keep-bit stages
+constexpr int B_SMEM = 1024 + 2 * F_TILE_BYTES + B_NST * B_STAGE + 4 * F_TILE_BYTES + 12 * 2048 + 256;
 
 struct BwdArgs {
     const float* lse2;
@@ -423,22 +424,22 @@ __global__ void __launch_bounds__(512, 1)
     extern __shared__ uint8_t smem_raw[];
     // 1024-aligned, derived from smem_raw by pointer arithmetic so accesses stay ld/st.shared
     uint8_t* smem = smem_raw + ((1024 - (tc5::smem_u32(smem_raw) & 1023)) & 1023);
-    uint8_t* sKV = smem;                        // [2] x {K, V}
-    uint8_t* sStage = sKV + 4 * F_TILE_BYTES;   // [2][B_STAGE]
-    uint8_t* sDS = sStage + 2 * B_STAGE;        // [2] x dS^T [2 q-blocks][128 keys][64 q] bf16, swizzled
+    uint8_t* sKV = smem;                        // {K, V} of the current key block
+    uint8_t* sStage = sKV + 2 * F_TILE_BYTES;   // [B_NST][B_STAGE]
+    uint8_t* sDS = sStage + B_NST * B_STAGE;    // [2] x dS^T [2 q-blocks][128 keys][64 q] bf16, swizzled
     float* sOut = (float*)(sDS + 4 * F_TILE_BYTES);  // [12 warps][2 KB] output staging
     uint64_t* bars = (uint64_t*)(sDS + 4 * F_TILE_BYTES + 12 * 2048);
-    uint64_t* kv_full = bars;        // [2]
-    uint64_t* kv_empty = bars + 2;   // [2]
-    uint64_t* st_full = bars + 4;    // [2]
-    uint64_t* st_empty = bars + 6;   // [2]
-    uint64_t* sdp_full = bars + 8;   // [2 query halves]
-    uint64_t* sm_done = bars + 10;   // [2 query halves]
-    uint64_t* dq_full = bars + 12;
-    uint64_t* dq_free = bars + 13;
-    uint64_t* acc_full = bars + 14;  // dK_j / dV_j complete
-    uint64_t* acc_free = bars + 15;  // dK_j / dV_j read out of TMEM
-    uint32_t* tslot = (uint32_t*)(bars + 16);
+    uint64_t* kv_full = bars;
+    uint64_t* kv_empty = bars + 1;
+    uint64_t* st_full = bars + 2;              // [B_NST]
+    uint64_t* st_empty = st_full + B_NST;      // [B_NST]
+    uint64_t* sdp_full = st_empty + B_NST;     // [2 query halves]
+    uint64_t* sm_done = sdp_full + 2;          // [2 query halves]
+    uint64_t* dq_full = sm_done + 2;
+    uint64_t* dq_free = dq_full + 1;
+    uint64_t* acc_full = dq_free + 1;  // dK_j / dV_j complete
+    uint64_t* acc_free = acc_full + 1;  // dK_j / dV_j read out of TMEM
+    uint32_t* tslot = (uint32_t*)(acc_free + 1);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int S = ba.S, nj = S / FT, nsteps = nj * nj;
@@ -452,9 +453,9 @@ __global__ void __launch_bounds__(512, 1)
         tma_prefetch(&tQ);
         tma_prefetch(&tdO);
         if (ba.mask_t) tma_prefetch(&tM);
-        for (int s = 0; s < 2; ++s) {
-            mbar_init(&kv_full[s], 1);
-            mbar_init(&kv_empty[s], 1);
+        mbar_init(kv_full, 1);
+        mbar_init(kv_empty, 1);
+        for (int s = 0; s < B_NST; ++s) {
             mbar_init(&st_full[s], 1);
             mbar_init(&st_empty[s], 1);
         }
@@ -479,17 +480,15 @@ __global__ void __launch_bounds__(512, 1)
             // ------------------------------------------------ TMA producer
             for (int u = 0; u < nsteps; ++u) {
                 const int j = u / nj, i = u % nj;
-                if (i == 0) {
-                    const int kb = j & 1;
-                    mbar_wait(&kv_empty[kb], ((j >> 1) & 1) ^ 1);
-                    mbar_expect_tx(&kv_full[kb], 2 * F_TILE_BYTES);
-                    tma_load_2d(sKV + kb * 2 * F_TILE_BYTES, &tK, &kv_full[kb], h * FD, row_base + j * FT);
-                    tma_load_2d(sKV + kb * 2 * F_TILE_BYTES + F_TILE_BYTES, &tV, &kv_full[kb], h * FD,
-                                row_base + j * FT);
+                if (i == 0) {  // single K/V buffer: block j after the last reader of block j-1
+                    mbar_wait(kv_empty, (j & 1) ^ 1);
+                    mbar_expect_tx(kv_full, 2 * F_TILE_BYTES);
+                    tma_load_2d(sKV, &tK, kv_full, h * FD, row_base + j * FT);
+                    tma_load_2d(sKV + F_TILE_BYTES, &tV, kv_full, h * FD, row_base + j * FT);
                 }
-                const int s = u & 1;
+                const int s = u % B_NST;
                 uint8_t* st = sStage + s * B_STAGE;
-                mbar_wait(&st_empty[s], ((u >> 1) & 1) ^ 1);
+                mbar_wait(&st_empty[s], ((u / B_NST) & 1) ^ 1);
                 if (ba.ts && blockIdx.x == 0 && blockIdx.y == 0) ba.ts[0 * 64 + u] = gtime();
                 mbar_expect_tx(&st_full[s], 2 * F_TILE_BYTES + 1024 + (ba.mask_t ? 2048 : 0));
                 tma_load_2d(st, &tQ, &st_full[s], h * FD, row_base + i * FT);
@@ -512,12 +511,12 @@ __global__ void __launch_bounds__(512, 1)
             constexpr uint32_t id_q = idesc_bf16(FT, FD, true, true);
             const bool mm = !(ba.dbg & 4);
             auto issue_sdp = [&](int u, int hh) {
-                const int j = u / nj, i = u % nj, s = u & 1, kb = j & 1;
-                const uint32_t aK = smem_u32(sKV + kb * 2 * F_TILE_BYTES), aV = aK + F_TILE_BYTES;
+                const int j = u / nj, i = u % nj, s = u % B_NST;
+                const uint32_t aK = smem_u32(sKV), aV = aK + F_TILE_BYTES;
                 const uint32_t aQ = smem_u32(sStage + s * B_STAGE) + hh * (F_TILE_BYTES / 2), adO = aQ + F_TILE_BYTES;
                 if (hh == 0) {
-                    if (i == 0) mbar_wait(&kv_full[kb], (j >> 1) & 1);
-                    mbar_wait(&st_full[s], (u >> 1) & 1);
+                    if (i == 0) mbar_wait(kv_full, j & 1);
+                    mbar_wait(&st_full[s], (u / B_NST) & 1);
                     fence_after();
                 }
                 if (mm) {
@@ -533,8 +532,8 @@ __global__ void __launch_bounds__(512, 1)
             issue_sdp(0, 0);
             issue_sdp(0, 1);
             for (int u = 0; u < nsteps; ++u) {
-                const int j = u / nj, i = u % nj, s = u & 1, kb = j & 1;
-                const uint32_t aK = smem_u32(sKV + kb * 2 * F_TILE_BYTES);
+                const int j = u / nj, i = u % nj, s = u % B_NST;
+                const uint32_t aK = smem_u32(sKV);
                 const uint32_t aQ = smem_u32(sStage + s * B_STAGE), adO = aQ + F_TILE_BYTES;
                 const uint32_t aDS = smem_u32(sDS + (u & 1) * 2 * F_TILE_BYTES);
 #pragma unroll 1
@@ -559,7 +558,9 @@ __global__ void __launch_bounds__(512, 1)
                         mma_commit(&st_empty[s]);  // Q, dO, lse, delta, keep bits of this step are no longer read
                         if (i == nj - 1) mma_commit(acc_full);
                     }
-                    if (u + 1 < nsteps) issue_sdp(u + 1, hh);
+                    // (at the last query block of key block j, S/dP of block j+1 need its
+                    // K/V, loaded into the single K/V buffer only after dQ below releases K_j)
+                    if (u + 1 < nsteps && i != nj - 1) issue_sdp(u + 1, hh);
                 }
                 if (ba.ts && blockIdx.x == 0 && blockIdx.y == 0) ba.ts[2 * 64 + u] = gtime();
                 if (u > 0) {
@@ -574,7 +575,13 @@ __global__ void __launch_bounds__(512, 1)
                                kk > 0);
                 }
                 mma_commit(dq_full);
-                if (i == nj - 1) mma_commit(&kv_empty[kb]);  // K_j, V_j no longer read
+                if (i == nj - 1) {
+                    mma_commit(kv_empty);  // K_j, V_j no longer read
+                    if (u + 1 < nsteps) {
+                        issue_sdp(u + 1, 0);
+                        issue_sdp(u + 1, 1);
+                    }
+                }
             }
         }
     } else if (warp >= 4 && warp < 12) {
@@ -610,12 +617,12 @@ __global__ void __launch_bounds__(512, 1)
         };
         const int g = hf;  // 32-column group of each query half
         for (int u = 0; u < nsteps; ++u) {
-            const int j = u / nj, i = u % nj, s = u & 1;
+            const int j = u / nj, i = u % nj, s = u % B_NST;
             if (i == 0 && j > 0) drain_kv(j - 1);  // TMEM dK/dV free before dV/dK of block j start
             const float* lse_s = (const float*)(sStage + s * B_STAGE + 2 * F_TILE_BYTES);
             const float* dl_s = lse_s + FT;
             uint8_t* ds_buf = sDS + (u & 1) * 2 * F_TILE_BYTES;
-            mbar_wait(&st_full[s], (u >> 1) & 1);
+            mbar_wait(&st_full[s], (u / B_NST) & 1);
             const uint4 mw = ba.mask_t ? *(const uint4*)(sStage + s * B_STAGE + 2 * F_TILE_BYTES + 1024 + k * 16)
                                        : make_uint4(~0u, ~0u, ~0u, ~0u);
 #pragma unroll 1
