@@ -21,6 +21,7 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <type_traits>
 
 #include "tc5.cuh"
 
@@ -32,9 +33,16 @@ namespace {
 
 constexpr int FD = 64;    // head dim
 constexpr int FT = 128;   // rows per tile (queries / keys)
-constexpr int FNS = 3;    // K/V ring stages
 constexpr int F_TILE_BYTES = FT * FD * 2;  // 16 KB
-constexpr int F_SMEM = 1024 + 2 * F_TILE_BYTES + FNS * 2 * F_TILE_BYTES + FNS * 2 * 2048 + 256;
+// NT query tiles per CTA: 2 (one CTA per SM, the tiles ping-pong) or 1 (two CTAs
+// per SM, each with half the TMEM, overlapping each other's prologue/epilogue)
+template <int NT>
+struct FCfg {
+    static constexpr int NS = NT == 2 ? 3 : 2;  // K/V ring stages
+    static constexpr int THREADS = (4 + 4 * NT) * 32;
+    static constexpr uint32_t TCOLS = NT == 2 ? 512 : 256;
+    static constexpr int SMEM = 1024 + NT * F_TILE_BYTES + NS * 2 * F_TILE_BYTES + NS * NT * 2048 + 256;
+};
 
 struct FwdArgs {
     bf16* o;
@@ -46,17 +54,19 @@ struct FwdArgs {
     int S, nh;
 };
 
-__global__ void __launch_bounds__(384, 1)
+template <int NT>
+__global__ void __launch_bounds__(FCfg<NT>::THREADS, NT == 1 ? 2 : 1)
     k_fa5_fwd(const __grid_constant__ CUtensorMap tQ, const __grid_constant__ CUtensorMap tK,
               const __grid_constant__ CUtensorMap tV, const __grid_constant__ CUtensorMap tM, FwdArgs fa) {
     extern __shared__ uint8_t smem_raw[];
     // 1024-aligned, derived from smem_raw by pointer arithmetic so accesses stay ld/st.shared
     uint8_t* smem = smem_raw + ((1024 - (tc5::smem_u32(smem_raw) & 1023)) & 1023);
-    uint8_t* sQ = smem;                        // [2][FT][FD]
-    uint8_t* sK = sQ + 2 * F_TILE_BYTES;       // [FNS][FT][FD]
+    constexpr int FNS = FCfg<NT>::NS;
+    uint8_t* sQ = smem;                        // [NT][FT][FD]
+    uint8_t* sK = sQ + NT * F_TILE_BYTES;      // [FNS][FT][FD]
     uint8_t* sV = sK + FNS * F_TILE_BYTES;     // [FNS][FT][FD]
-    uint8_t* sM = sV + FNS * F_TILE_BYTES;      // [FNS][2 tiles][128 rows][4 words] keep bits
-    uint64_t* bars = (uint64_t*)(sM + FNS * 2 * 2048);
+    uint8_t* sM = sV + FNS * F_TILE_BYTES;     // [FNS][NT tiles][128 rows][4 words] keep bits
+    uint64_t* bars = (uint64_t*)(sM + FNS * NT * 2048);
     uint64_t* q_full = bars;
     uint64_t* kv_full = q_full + 1;
     uint64_t* kv_empty = kv_full + FNS;
@@ -68,8 +78,8 @@ __global__ void __launch_bounds__(384, 1)
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int S = fa.S, nj = S / FT;
     const int b = blockIdx.z, h = blockIdx.y;
-    const int tile0 = blockIdx.x * 2;
-    const int ntile = (tile0 + 1 < nj) ? 2 : 1;  // query tiles in this CTA
+    const int tile0 = blockIdx.x * NT;
+    const int ntile = (NT == 2 && tile0 + 1 < nj) ? 2 : 1;  // query tiles in this CTA
     const int row_base = b * S;                  // first token row of this sequence
 
     if (threadIdx.x == 0) {
@@ -89,7 +99,7 @@ __global__ void __launch_bounds__(384, 1)
         }
         fence_barrier_init();
     }
-    if (warp == 1) tmem_alloc<512>(tslot);
+    if (warp == 1) tmem_alloc<FCfg<NT>::TCOLS>(tslot);
     fence_before();
     __syncthreads();
     fence_after();
@@ -109,7 +119,7 @@ __global__ void __launch_bounds__(384, 1)
                 tma_load_2d(sV + s * F_TILE_BYTES, &tV, &kv_full[s], h * FD, row_base + j * FT);
                 if (fa.mask)  // keep bits of (query rows of each tile, key chunk j)
                     for (int g = 0; g < ntile; ++g)
-                        tma_load_2d(sM + (s * 2 + g) * 2048, &tM, &kv_full[s], j * (FT / 32),
+                        tma_load_2d(sM + (s * NT + g) * 2048, &tM, &kv_full[s], j * (FT / 32),
                                     (b * fa.nh + h) * S + (tile0 + g) * FT);
             }
         }
@@ -166,7 +176,7 @@ __global__ void __launch_bounds__(384, 1)
                 mbar_wait(&kv_full[j % FNS], (j / FNS) & 1);  // keep bits of chunk j landed
                 mbar_wait(&s_full[g], j & 1);
                 fence_after();
-                const uint4 mw = fa.mask ? *(const uint4*)(sM + ((j % FNS) * 2 + g) * 2048 + row * 16)
+                const uint4 mw = fa.mask ? *(const uint4*)(sM + ((j % FNS) * NT + g) * 2048 + row * 16)
                                          : make_uint4(~0u, ~0u, ~0u, ~0u);
                 if (j == 0) {  // first chunk: exact row max (one extra TMEM read of S)
                     float mx = -INFINITY;
@@ -261,7 +271,7 @@ __global__ void __launch_bounds__(384, 1)
     __syncthreads();
     if (warp == 1) {
         fence_after();
-        tmem_dealloc<512>(tmem);
+        tmem_dealloc<FCfg<NT>::TCOLS>(tmem);
     }
 }
 
@@ -775,13 +785,19 @@ bool attn_fwd_sm100_try(const Attn& a, cudaStream_t s) {
     if (a.thr && !make_map_u32(&tm, a.mask, a.S / 32, a.B * a.nh * a.S, a.S / 32, FT / 32, FT)) return false;
     FwdArgs fa{(bf16*)a.o, a.ld_o, a.lse, a.thr ? a.mask : nullptr, a.thr ? a.dscale : 1.f,
                a.scale * 1.4426950408889634f, (int)a.S, (int)a.nh};
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_fa5_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, F_SMEM);
-        attr = true;
-    }
-    dim3 grid((unsigned)((a.S / FT + 1) / 2), (unsigned)a.nh, (unsigned)a.B);
-    k_fa5_fwd<<<grid, 384, F_SMEM, s>>>(tq, tk, tv, tm, fa);
+    static int nt_env = getenv("SB_ATTN_FWD_NT") ? atoi(getenv("SB_ATTN_FWD_NT")) : 1;
+    auto go = [&](auto ntc) {
+        constexpr int NT = decltype(ntc)::value;
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(k_fa5_fwd<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, FCfg<NT>::SMEM);
+            attr = true;
+        }
+        dim3 grid((unsigned)((a.S / FT + NT - 1) / NT), (unsigned)a.nh, (unsigned)a.B);
+        k_fa5_fwd<NT><<<grid, FCfg<NT>::THREADS, FCfg<NT>::SMEM, s>>>(tq, tk, tv, tm, fa);
+    };
+    if (nt_env == 2) go(std::integral_constant<int, 2>{});
+    else go(std::integral_constant<int, 1>{});
     SBK_CHECK_LAUNCH();
     return true;
 }
