@@ -125,6 +125,7 @@ public:
         analyze_writes();
         for (auto& r : ranks) allocate(r);
         init_mask_stream();
+        init_early_allreduce();
         if (comm.nccl && world > 1) {
             nccl().load();
             ncclUniqueId id;
@@ -147,6 +148,11 @@ public:
             if (e) cudaEventDestroy(e);
         for (auto e : bwd_ev)
             if (e) cudaEventDestroy(e);
+        for (auto e : ar_ev)
+            if (e) cudaEventDestroy(e);
+        for (auto e : dgrad_ev)
+            if (e) cudaEventDestroy(e);
+        if (cstream) cudaStreamDestroy(cstream);
         if (fork_ev) cudaEventDestroy(fork_ev);
         if (mstream) cudaStreamDestroy(mstream);
         if (stream) cudaStreamDestroy(stream);
@@ -597,15 +603,110 @@ public:
     }
 
     // ------------------------------------------------------- collectives
-    void all_reduce(std::vector<char*> bufs_in, std::vector<char*> bufs_out, DT t, i64 n) {
+    void all_reduce(std::vector<char*> bufs_in, std::vector<char*> bufs_out, DT t, i64 n, cudaStream_t st = nullptr) {
+        if (!st) st = stream;
         if (comm.nccl) {
-            nccl().check(nccl().AllReduce(bufs_in[0], bufs_out[0], (size_t)n, nccl_dt(t), ncclSum, ncomm, stream),
+            nccl().check(nccl().AllReduce(bufs_in[0], bufs_out[0], (size_t)n, nccl_dt(t), ncclSum, ncomm, st),
                          "ncclAllReduce");
             return;
         }
         sbk::sum_ranks((const void* const*)bufs_in.data(), (void* const*)bufs_out.data(), (int)bufs_in.size(), t, n, false,
-                       stream);
+                       st);
         ++launches;
+    }
+
+    // ---------------------------------------- backward all-reduce overlap
+    // A Linear whose input is a SyncGrad output (Megatron column-parallel layer,
+    // sync_backward): its dgrad completes that gradient, so the SyncGrad's
+    // all-reduce is issued on a communication stream right after the dgrad and
+    // runs while the weight gradient GEMM runs on the executor stream; the
+    // SyncGrad backward step then only waits for it (semantics unchanged:
+    // executor.cpp:1071-1083).
+    cudaStream_t cstream = nullptr;
+    std::vector<int> early_ar;           // per forward op: SyncGrad op whose all-reduce follows its dgrad, or -1
+    std::vector<cudaEvent_t> ar_ev;      // per SyncGrad op: its all-reduce completed (on cstream)
+    std::vector<cudaEvent_t> dgrad_ev;   // per Linear op with early_ar: its dgrads are enqueued
+    std::vector<char> ar_pending;
+
+    void init_early_allreduce() {
+        const Plan& P = ranks[0].P;
+        early_ar.assign(P.fwd.size(), -1);
+        if (world <= 1) return;
+        std::vector<int> pos(P.fwd.size(), -1);
+        for (size_t k = 0; k < bsteps.size(); ++k)
+            if (bsteps[k].kind == 0) pos[(size_t)bsteps[k].idx] = (int)k;
+        for (size_t sidx = 0; sidx < P.fwd.size(); ++sidx) {
+            const Op& sg = P.fwd[sidx];
+            if (sg.k != K::SyncGrad || sg.ids_input || pos[sidx] < 0) continue;
+            const int gst = P.views[(size_t)sg.out[0]].gst;
+            // the last backward writer of the SyncGrad output's gradient before the SyncGrad step
+            int last = -1;
+            bool clean = true;
+            for (int k = pos[sidx] - 1; k >= 0; --k) {
+                const Step& st = bsteps[(size_t)k];
+                if (st.kind == 2) {
+                    clean = false;
+                    break;
+                }
+                if (st.kind != 0) continue;
+                if (grad_writes(P, P.fwd[(size_t)st.idx]).count(gst)) {
+                    last = st.idx;
+                    break;
+                }
+            }
+            if (!clean || last < 0) continue;
+            const Op& l = P.fwd[(size_t)last];
+            if (l.k != K::Linear && l.k != K::FusedLinearGelu) continue;
+            if (l.dgelu_pre >= 0 || P.views[(size_t)l.in[0]].gst != gst) continue;
+            if (gdt(ranks[0], l.in[0]) != cdt) continue;  // dgrad through an fp32 temp: keep the plain order
+            early_ar[(size_t)last] = (int)sidx;
+        }
+        bool any = false;
+        ar_ev.assign(P.fwd.size(), nullptr);
+        dgrad_ev.assign(P.fwd.size(), nullptr);
+        ar_pending.assign(P.fwd.size(), 0);
+        for (size_t k = 0; k < P.fwd.size(); ++k)
+            if (early_ar[k] >= 0) {
+                CK(cudaEventCreateWithFlags(&dgrad_ev[k], cudaEventDisableTiming));
+                CK(cudaEventCreateWithFlags(&ar_ev[(size_t)early_ar[k]], cudaEventDisableTiming));
+                any = true;
+            }
+        if (any) {
+            int lo, hi;
+            CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+            CK(cudaStreamCreateWithPriority(&cstream, cudaStreamNonBlocking, hi));  // communication first
+        }
+    }
+
+    // backward of a Linear / FusedLinearGelu whose dgrad feeds an early all-reduce
+    void linear_bwd_overlapped(int i) {
+        const int sidx = early_ar[(size_t)i];
+        auto gin = [&](RankCtx& r, const Op& op) {
+            if (op.k == K::FusedLinearGelu) {
+                const View& y = V(r, op.out[0]);
+                if (!op.dgelu_fused)
+                    sbk::unary_bwd(2, fp(r, op.out[1]), gp(r, op.out[0]), gp(r, op.out[1]), cdt, cdt, y.numel(), 1.f,
+                                   stream);
+                return std::make_pair((const void*)gp(r, op.out[1]), cols_of(y));
+            }
+            const View& y = V(r, op.out[0]);
+            return std::make_pair((const void*)gp(r, op.out[0]), cols_of(y));
+        };
+        std::vector<std::pair<const void*, i64>> g(ranks.size());
+        for (size_t k = 0; k < ranks.size(); ++k) {
+            const Op& op = ranks[k].P.fwd[(size_t)i];
+            g[k] = gin(ranks[k], op);
+            linear_bwd(ranks[k], op, g[k].first, g[k].second, 1);
+        }
+        // all-reduce of the SyncGrad output gradient on the communication stream
+        CK(cudaEventRecord(dgrad_ev[(size_t)i], stream));
+        CK(cudaStreamWaitEvent(cstream, dgrad_ev[(size_t)i], 0));
+        std::vector<char*> b;
+        for (auto& r : ranks) b.push_back(gp(r, r.P.fwd[(size_t)sidx].out[0]));
+        all_reduce(b, b, cdt, V(ranks[0], ranks[0].P.fwd[(size_t)sidx].out[0]).numel(), cstream);
+        CK(cudaEventRecord(ar_ev[(size_t)sidx], cstream));
+        ar_pending[(size_t)sidx] = 1;
+        for (size_t k = 0; k < ranks.size(); ++k) linear_bwd(ranks[k], ranks[k].P.fwd[(size_t)i], g[k].first, g[k].second, 2);
     }
 
     // ------------------------------------------------------- forward op
@@ -876,14 +977,16 @@ public:
     }
 
     // ------------------------------------------------------ backward op
-    void linear_bwd(RankCtx& r, const Op& op, const void* g, i64 ldg) {
+    // part: 1 dgrad only, 2 weight/bias gradients only, 3 both
+    void linear_bwd(RankCtx& r, const Op& op, const void* g, i64 ldg, int part = 3) {
         // dx += g W (executor.cpp:101-118); dW += g^T x (:121-133); db += colsum g (:1146-1154)
         const View& x = V(r, op.in[0]);
         const View& w = V(r, op.in[1]);
         i64 rows, cols, ldx, gr, gc, ldgx;
         x.rowwise(rows, cols, ldx);
         i64 out_f = w.shape[0];
-        if (op.dgelu_pre >= 0) {
+        if (!(part & 1)) {
+        } else if (op.dgelu_pre >= 0) {
             // dx lands directly as the producing GeLU's input gradient: gelu'(pre) * (g W)
             gemm_rowwise(r, g, ldg, false, fp(r, op.in[1]), cols, false, gp(r, op.dgelu_pre), cols, cdt, rows, cols,
                          out_f, !OW(op.dgelu_pre), nullptr, 2, fp(r, op.dgelu_pre));
@@ -895,9 +998,13 @@ public:
                          gx.temp || !OW(op.in[0]), nullptr);
             flush(r, gx);
         }
+        if (!(part & 2)) {
+            ++launches;
+            return;
+        }
         gemm_rowwise(r, g, ldg, true, fp(r, op.in[0]), ldx, false, gp(r, op.in[1]), cols, gdt(r, op.in[1]), out_f, cols,
                      rows, !OW(op.in[1]), nullptr);
-        launches += 2;
+        launches += (part & 1) ? 2 : 1;
         if (op.has_bias && op.bias_grad) {
             sbk::bias_grad(g, cdt, ldg, rows, out_f, (float*)gp(r, op.in[2]), (float*)r.ws, stream, !OW(op.in[2]));
             ++launches;
@@ -907,6 +1014,11 @@ public:
     void bwd_op(int i) {
         const Op& op0 = ranks[0].P.fwd[(size_t)i];
         if (profiling) prof_begin(std::string(k_str(op0.k)) + "(bwd)");
+        if (early_ar.size() > (size_t)i && early_ar[(size_t)i] >= 0) {
+            linear_bwd_overlapped(i);
+            if (profiling) prof_end();
+            return;
+        }
         switch (op0.k) {
             case K::SyncGrad: {
                 // Σ_r of the module input's gradient, accumulated on every rank (executor.cpp:1071-1083)
@@ -915,7 +1027,12 @@ public:
                 std::vector<char*> b;
                 for (auto& r : ranks) b.push_back(gp(r, r.P.fwd[(size_t)i].out[0]));
                 i64 n = V(ranks[0], op0.out[0]).numel();
-                if (world > 1) all_reduce(b, b, cdt, n);
+                if (ar_pending.size() > (size_t)i && ar_pending[(size_t)i]) {
+                    CK(cudaStreamWaitEvent(stream, ar_ev[(size_t)i], 0));  // issued right after the dgrad
+                    ar_pending[(size_t)i] = 0;
+                } else if (world > 1) {
+                    all_reduce(b, b, cdt, n);
+                }
                 for (auto& r : ranks) {
                     const Op& op = r.P.fwd[(size_t)i];
                     accumulate_view(r, op.out[0], op.in[0], !OW(op.in[0]));
@@ -1637,8 +1754,11 @@ std::string Executor::describe() const {
     const Plan& P = I.ranks[0].P;
     std::map<std::string, int> cnt;
     for (auto& op : P.fwd) cnt[k_str(op.k)]++;
+    int early = 0;
+    for (int e : I.early_ar) early += e >= 0;
     o << "{\"ops\": " << P.fwd.size() << ", \"regions\": " << P.regions.size() << ", \"backward_steps\": " << I.bsteps.size()
-      << ", \"device_bytes\": " << device_bytes() << ", \"kinds\": {";
+      << ", \"device_bytes\": " << device_bytes() << ", \"overlapped_backward_allreduces\": " << early
+      << ", \"kinds\": {";
     bool first = true;
     for (auto& [k, c] : cnt) {
         o << (first ? "" : ", ") << "\"" << k << "\": " << c;

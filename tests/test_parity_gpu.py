@@ -80,6 +80,9 @@ def test_tp_recipe_fp32(world):
     script = recipes.tp_script(2, world, ckpt_ratio=0.5)
     ex, outs, grads, r = run_both(TOY, script, world)
     check(outs, grads, r, world, FP32_TOL, FP32_TOL)
+    # the SyncGrad all-reduces of the column-parallel qkv / dense1 inputs run on the
+    # communication stream overlapping their weight-gradient GEMMs (2 per layer)
+    assert ex.describe()["overlapped_backward_allreduces"] == 2 * 2
     # collective count mirrors the reference (incl. checkpoint recompute, A.14)
     assert ex.collective_invocations() == r.meta["collectives_total"]
 
