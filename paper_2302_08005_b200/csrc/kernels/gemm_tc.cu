@@ -88,14 +88,22 @@ __device__ __forceinline__ float tanh_fast(float x) {
     asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
+// tanh-GeLU and its derivative with the polynomial folded (5 FP ops + one MUFU):
+//   u = x (c + c a x^2);  gelu = 0.5 x (1 + tanh u)
+//   gelu' = 0.5 (1 + t) + 0.5 x (1 - t^2) (c + 3 c a x^2)
 __device__ __forceinline__ float gelu_fast(float x) {
-    const float c = 0.7978845608028654f, a = 0.044715f;
-    return 0.5f * x * (1.f + tanh_fast(c * (x + a * x * x * x)));
+    const float c = 0.7978845608028654f, ca = 0.7978845608028654f * 0.044715f;
+    const float x2 = x * x;
+    const float t = tanh_fast(x * fmaf(ca, x2, c));
+    const float hx = 0.5f * x;
+    return fmaf(hx, t, hx);
 }
 __device__ __forceinline__ float gelu_grad_fast(float x) {
-    const float c = 0.7978845608028654f, a = 0.044715f;
-    float t = tanh_fast(c * (x + a * x * x * x));
-    return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * c * (1.f + 3.f * a * x * x);
+    const float c = 0.7978845608028654f, ca = 0.7978845608028654f * 0.044715f;
+    const float x2 = x * x;
+    const float t = tanh_fast(x * fmaf(ca, x2, c));
+    const float hx = 0.5f * x;
+    return fmaf(0.5f, t, 0.5f) + hx * fmaf(-t, t, 1.f) * fmaf(3.f * ca, x2, c);
 }
 
 struct Epi {

@@ -117,14 +117,22 @@ __device__ __forceinline__ float tanh_fast(float x) {
     asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
+// tanh-GeLU and its derivative with the polynomial folded (5 FP ops + one MUFU):
+//   u = x (c + c a x^2);  gelu = 0.5 x (1 + tanh u)
+//   gelu' = 0.5 (1 + t) + 0.5 x (1 - t^2) (c + 3 c a x^2)
 __device__ __forceinline__ float gelu_fast(float x) {
-    const float c = 0.7978845608028654f, a = 0.044715f;
-    return 0.5f * x * (1.f + tanh_fast(c * (x + a * x * x * x)));
+    const float c = 0.7978845608028654f, ca = 0.7978845608028654f * 0.044715f;
+    const float x2 = x * x;
+    const float t = tanh_fast(x * fmaf(ca, x2, c));
+    const float hx = 0.5f * x;
+    return fmaf(hx, t, hx);
 }
 __device__ __forceinline__ float gelu_grad_fast(float x) {
-    const float c = 0.7978845608028654f, a = 0.044715f;
-    float t = tanh_fast(c * (x + a * x * x * x));
-    return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * c * (1.f + 3.f * a * x * x);
+    const float c = 0.7978845608028654f, ca = 0.7978845608028654f * 0.044715f;
+    const float x2 = x * x;
+    const float t = tanh_fast(x * fmaf(ca, x2, c));
+    const float hx = 0.5f * x;
+    return fmaf(0.5f, t, 0.5f) + hx * fmaf(-t, t, 1.f) * fmaf(3.f * ca, x2, c);
 }
 
 struct Epi2 {
@@ -163,7 +171,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
     uint64_t* empty = full + G_ST;
     uint64_t* tfull = empty + G_ST;   // [2]
     uint64_t* tempty = tfull + 2;     // [2]
-    uint32_t* tslot = (uint32_t*)(tempty + 2);
+    uint64_t* auxbar = tempty + 2;    // [8] per epilogue warp: its dGeLU pre-activation chunk landed
+    uint32_t* tslot = (uint32_t*)(auxbar + 8);
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const uint32_t rank = cluster_rank();
     const bool leader = rank == 0;
@@ -173,10 +182,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
     if (threadIdx.x == 0) {
         tma_prefetch(&tA);
         tma_prefetch(&tB);
-        if (!ep.accumulate) {
-            tma_prefetch(&tC);
-            if (ep.gelu == 1) tma_prefetch(&tX);
-        }
+        if (!ep.accumulate) tma_prefetch(&tC);
+        if (ep.gelu) tma_prefetch(&tX);
         for (int s = 0; s < G_ST; ++s) {
             mbar_init(&full[s], 2);
             mbar_init(&empty[s], 1);
@@ -185,6 +192,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
             mbar_init(&tfull[a], 1);
             mbar_init(&tempty[a], 16);
         }
+        for (int w = 0; w < 8; ++w) mbar_init(&auxbar[w], 1);
         fence_barrier_init();
     }
     if (warp == 1) {
@@ -273,12 +281,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
         const int q = warp & 3, half = (warp - 2) / 4;
         uint8_t* mybuf = epi + (warp - 2) * G_EPI_BUF;
         const uint32_t tempty0 = mapa_shared(smem_u32(&tempty[0]), 0);
-        int lt = 0, nst = 0;
+        int lt = 0, nst = 0, naux = 0;
+        uint64_t* abar = &auxbar[warp - 2];
+        // dGeLU epilogue: the pre-activation chunk (32 x 32 bf16) is TMA-loaded into the
+        // upper half of the staging slot ahead of its use
+        auto aux_load = [&](int col, long long row) {
+            if (lane == 0) {
+                mbar_expect_tx(abar, 2048);
+                tma_load_2d(mybuf + 2048, &tX, abar, col, (int)row);
+            }
+        };
         for (int tile = cluster; tile < ntiles; tile += nclusters, ++lt) {
             const int acc = lt & 1;
             int m0, n0, z;
             tile_coords(tile, m0, n0, z);
             const long long row0 = m0 + (long long)rank * G_BM + q * 32;  // first row of this warp
+            if (ep.gelu == 2) aux_load((int)(n0 + half * 32), row0);
             mbar_wait(&tfull[acc], (lt >> 1) & 1);
             fence_after();
 #pragma unroll 1
@@ -331,11 +349,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
 #pragma unroll
                     for (int j = 0; j < 32; ++j) v[j] = gelu_fast(v[j]);
                 } else if (ep.gelu == 2) {
-                    const uint4* ax = (const uint4*)(ep.aux + row * ep.ldc + col);
+                    mbar_wait(abar, naux & 1);
+                    ++naux;
+                    uint4 w[4];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) w[j] = *(const uint4*)(mybuf + 2048 + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4));
+                    __syncwarp();
+                    if (c + 2 < G_BN / 32) aux_load((int)(col + 64), row0);  // next chunk of this warp
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {
-                        uint4 w = ax[j];
-                        const bf16* e = (const bf16*)&w;
+                        const bf16* e = (const bf16*)&w[j];
 #pragma unroll
                         for (int t = 0; t < 8; ++t) v[8 * j + t] *= gelu_grad_fast(__bfloat162float(e[t]));
                     }
@@ -518,7 +541,9 @@ bool gemm_tc2_try(const Gemm& g, cudaStream_t s) {
         if (!make_store_map(&tc, g.ws, true, N, (long long)splits * M, N)) return false;
     } else if (!ep.accumulate) {
         if (!make_store_map(&tc, g.C, ep.c_f32, N, M, ldc)) return false;
-        if (g.epilogue == 1 && !make_store_map(&tx, g.aux, false, N, M, ldc)) return false;
+    }
+    if (g.epilogue && splits == 1) {  // GeLU: pre-activation store map; dGeLU: pre-activation load map
+        if (!make_store_map(&tx, g.aux, false, N, M, ldc)) return false;
     }
     Sched2 sc{(int)(M / 256), (int)(N / G_BN), splits, kblocks / splits};
     static unsigned long long* ts_buf = nullptr;
