@@ -190,97 +190,116 @@ __global__ void __launch_bounds__(512) k_bdrln_fwd_w(const T* partial, const T* 
                                                      const uint32_t* keep) {
     using V = Vec<T>;
     constexpr int VN = V::N, CW = CPL / WPR, RPB = 16 / WPR;
-    __shared__ float red[2][16][NR];
+    __shared__ float red[2][2][16][NR];
     const int warp = threadIdx.x / 32, lane = threadIdx.x & 31, slot = warp / WPR, part = warp % WPR;
-    const i64 row0 = ((i64)blockIdx.x * RPB + slot) * NR;  // NR consecutive rows of this group
-    if (row0 >= rows) return;  // rows % (RPB * NR) == 0: whole groups exit together
-    typename V::R pv[NR][CW], rv[NR][CW];
+    // row groups of NR consecutive rows, grid-strided; the next group's inputs are loaded
+    // while the current one is processed (rows % (RPB * NR) == 0)
+    const i64 gstep = (i64)gridDim.x * RPB;
+    i64 grp = (i64)blockIdx.x * RPB + slot;
+    const i64 ngrp = rows / NR;
+    typename V::R pn[NR][CW], rn[NR][CW];
+    auto prefetch = [&](i64 gi) {
+        if (gi >= ngrp) return;
 #pragma unroll
-    for (int k = 0; k < NR; ++k)
+        for (int k = 0; k < NR; ++k)
 #pragma unroll
-        for (int c = 0; c < CW; ++c) {
-            const int ch = (part * CW + c) * 32 + lane;
-            pv[k][c] = __ldcs((const typename V::R*)(partial + (row0 + k) * n) + ch);
-            rv[k][c] = __ldcs((const typename V::R*)(res + (row0 + k) * n) + ch);
-        }
-    float v[NR][CW][VN];
-    float sm[NR];
-#pragma unroll
-    for (int k = 0; k < NR; ++k) {
-        sm[k] = 0.f;
-#pragma unroll
-        for (int c = 0; c < CW; ++c) {
-            const int ch = (part * CW + c) * 32 + lane;
-            float r[VN], bb[VN];
-            V::unpack(pv[k][c], v[k][c]);
-            V::unpack(rv[k][c], r);
-            if (bias) V::unpack(((const typename V::R*)bias)[ch], bb);
-            uint32_t kb = 0;
-            if (thr)
-                kb = keep ? keep_bits<VN>(keep, (row0 + k) * n + (i64)ch * VN)
-                          : hash_keep_bits<VN>(s1, thr, (row0 + k) * n + (i64)ch * VN);
-#pragma unroll
-            for (int e = 0; e < VN; ++e) {
-                float t = v[k][c][e] + (bias ? bb[e] : 0.f);
-                if (thr) t = ((kb >> e) & 1) ? t * dscale : 0.f;
-                v[k][c][e] = to_f(from_f<T>(t + r[e]));  // `sum` is rounded to the storage dtype before the statistics
-                sm[k] += v[k][c][e];
+            for (int c = 0; c < CW; ++c) {
+                const int ch = (part * CW + c) * 32 + lane;
+                pn[k][c] = __ldcs((const typename V::R*)(partial + (gi * NR + k) * n) + ch);
+                rn[k][c] = __ldcs((const typename V::R*)(res + (gi * NR + k) * n) + ch);
             }
-            ((typename V::R*)(sum + (row0 + k) * n))[ch] = V::pack(v[k][c]);
+    };
+    prefetch(grp);
+    for (int it = 0; grp < ngrp; grp += gstep, ++it) {
+        const i64 row0 = grp * NR;
+        float v[NR][CW][VN];
+        float sm[NR];
+#pragma unroll
+        for (int k = 0; k < NR; ++k) {
+            sm[k] = 0.f;
+#pragma unroll
+            for (int c = 0; c < CW; ++c) V::unpack(pn[k][c], v[k][c]);
         }
-    }
-    auto row_sums = [&](float (&x)[NR], int which) {
+        float rv[NR][CW][VN];
 #pragma unroll
-        for (int k = 0; k < NR; ++k) x[k] = warp_sum(x[k]);
-        if (WPR > 1) {
-            if (lane == 0)
+        for (int k = 0; k < NR; ++k)
 #pragma unroll
-                for (int k = 0; k < NR; ++k) red[which][warp][k] = x[k];
-            asm volatile("bar.sync %0, %1;" ::"r"(1 + slot), "r"(32 * WPR) : "memory");
+            for (int c = 0; c < CW; ++c) V::unpack(rn[k][c], rv[k][c]);
+        prefetch(grp + gstep);
+#pragma unroll
+        for (int k = 0; k < NR; ++k) {
+#pragma unroll
+            for (int c = 0; c < CW; ++c) {
+                const int ch = (part * CW + c) * 32 + lane;
+                float bb[VN];
+                if (bias) V::unpack(((const typename V::R*)bias)[ch], bb);
+                uint32_t kb = 0;
+                if (thr)
+                    kb = keep ? keep_bits<VN>(keep, (row0 + k) * n + (i64)ch * VN)
+                              : hash_keep_bits<VN>(s1, thr, (row0 + k) * n + (i64)ch * VN);
+#pragma unroll
+                for (int e = 0; e < VN; ++e) {
+                    float t = v[k][c][e] + (bias ? bb[e] : 0.f);
+                    if (thr) t = ((kb >> e) & 1) ? t * dscale : 0.f;
+                    v[k][c][e] = to_f(from_f<T>(t + rv[k][c][e]));  // `sum` rounded to the storage dtype first
+                    sm[k] += v[k][c][e];
+                }
+                ((typename V::R*)(sum + (row0 + k) * n))[ch] = V::pack(v[k][c]);
+            }
+        }
+        auto row_sums = [&](float (&xx)[NR], int which) {
+#pragma unroll
+            for (int k = 0; k < NR; ++k) xx[k] = warp_sum(xx[k]);
+            if (WPR > 1) {
+                if (lane == 0)
+#pragma unroll
+                    for (int k = 0; k < NR; ++k) red[it & 1][which][warp][k] = xx[k];
+                asm volatile("bar.sync %0, %1;" ::"r"(1 + slot), "r"(32 * WPR) : "memory");
+#pragma unroll
+                for (int k = 0; k < NR; ++k) {
+                    xx[k] = 0.f;
+#pragma unroll
+                    for (int w = 0; w < WPR; ++w) xx[k] += red[it & 1][which][slot * WPR + w][k];
+                }
+            }
+        };
+        row_sums(sm, 0);
+        float mu[NR], q[NR];
+#pragma unroll
+        for (int k = 0; k < NR; ++k) {
+            mu[k] = sm[k] / (float)n;
+            q[k] = 0.f;
+#pragma unroll
+            for (int c = 0; c < CW; ++c)
+#pragma unroll
+                for (int e = 0; e < VN; ++e) {
+                    const float d = v[k][c][e] - mu[k];
+                    q[k] += d * d;
+                }
+        }
+        row_sums(q, 1);
+#pragma unroll
+        for (int c = 0; c < CW; ++c) {
+            const int ch = (part * CW + c) * 32 + lane;
+            float gm[VN], bt[VN];
+            V::unpack(((const typename V::R*)gamma)[ch], gm);
+            V::unpack(((const typename V::R*)beta)[ch], bt);
 #pragma unroll
             for (int k = 0; k < NR; ++k) {
-                x[k] = 0.f;
+                const float rs = rsqrtf(q[k] / (float)n + eps);
+                float o[VN];
 #pragma unroll
-                for (int w = 0; w < WPR; ++w) x[k] += red[which][slot * WPR + w][k];
+                for (int e = 0; e < VN; ++e) o[e] = gm[e] * ((v[k][c][e] - mu[k]) * rs) + bt[e];
+                ((typename V::R*)(y + (row0 + k) * n))[ch] = V::pack(o);
             }
         }
-    };
-    row_sums(sm, 0);
-    float mu[NR], q[NR];
+        if (lane == 0 && part == 0)
 #pragma unroll
-    for (int k = 0; k < NR; ++k) {
-        mu[k] = sm[k] / (float)n;
-        q[k] = 0.f;
-#pragma unroll
-        for (int c = 0; c < CW; ++c)
-#pragma unroll
-            for (int e = 0; e < VN; ++e) {
-                const float d = v[k][c][e] - mu[k];
-                q[k] += d * d;
+            for (int k = 0; k < NR; ++k) {
+                mean[row0 + k] = mu[k];
+                rstd[row0 + k] = rsqrtf(q[k] / (float)n + eps);
             }
     }
-    row_sums(q, 1);
-#pragma unroll
-    for (int c = 0; c < CW; ++c) {
-        const int ch = (part * CW + c) * 32 + lane;
-        float gm[VN], bt[VN];
-        V::unpack(((const typename V::R*)gamma)[ch], gm);
-        V::unpack(((const typename V::R*)beta)[ch], bt);
-#pragma unroll
-        for (int k = 0; k < NR; ++k) {
-            const float rs = rsqrtf(q[k] / (float)n + eps);
-            float o[VN];
-#pragma unroll
-            for (int e = 0; e < VN; ++e) o[e] = gm[e] * ((v[k][c][e] - mu[k]) * rs) + bt[e];
-            ((typename V::R*)(y + (row0 + k) * n))[ch] = V::pack(o);
-        }
-    }
-    if (lane == 0 && part == 0)
-#pragma unroll
-        for (int k = 0; k < NR; ++k) {
-            mean[row0 + k] = mu[k];
-            rstd[row0 + k] = rsqrtf(q[k] / (float)n + eps);
-        }
 }
 
 // MODE 0: LayerNorm backward (gx += ...). MODE 1: fused bias+dropout+residual+LN
@@ -409,16 +428,31 @@ __global__ void __launch_bounds__(512, 1)
     }
     float pg[CW][VN] = {}, pb[CW][VN] = {}, pd[CW][VN] = {};
     int it = 0;
-    for (i64 row = (i64)blockIdx.x * RPB + slot; row < rows; row += (i64)gridDim.x * RPB, ++it) {
-        float xv[CW][VN], gv[CW][VN];
-        const typename V::R* xr = (const typename V::R*)(x + row * n);
-        const typename V::R* gr = (const typename V::R*)(g + row * n);
+    // software pipeline: the next row's x / g / statistics are loaded while this row is processed
+    const i64 rstep = (i64)gridDim.x * RPB;
+    i64 row = (i64)blockIdx.x * RPB + slot;
+    typename V::R xn[CW], gn[CW];
+    float mun = 0.f, rsn = 0.f;
+    auto prefetch = [&](i64 r) {
+        if (r >= rows) return;
 #pragma unroll
         for (int c = 0; c < CW; ++c) {
-            V::unpack(xr[(part * CW + c) * 32 + lane], xv[c]);
-            V::unpack(gr[(part * CW + c) * 32 + lane], gv[c]);
+            xn[c] = __ldcs((const typename V::R*)(x + r * n) + (part * CW + c) * 32 + lane);
+            gn[c] = __ldcs((const typename V::R*)(g + r * n) + (part * CW + c) * 32 + lane);
         }
-        const float mu = mean[row], rs = rstd[row];
+        mun = mean[r];
+        rsn = rstd[r];
+    };
+    prefetch(row);
+    for (; row < rows; row += rstep, ++it) {
+        float xv[CW][VN], gv[CW][VN];
+#pragma unroll
+        for (int c = 0; c < CW; ++c) {
+            V::unpack(xn[c], xv[c]);
+            V::unpack(gn[c], gv[c]);
+        }
+        const float mu = mun, rs = rsn;
+        prefetch(row + rstep);
         float a = 0.f, b = 0.f;
 #pragma unroll
         for (int c = 0; c < CW; ++c)
@@ -573,8 +607,10 @@ bool bdrln_fwd_vec(const void* partial, const void* bias, const void* res, const
                 constexpr int CPL = decltype(cc)::value;
                 if constexpr (CPL % 4 == 0) {
                     // 4 warps per row, 16-warp blocks (4 rows per block)
-                    if (rows % 16 == 0) {
-                        k_bdrln_fwd_w<T, CPL, 4, 4><<<(unsigned)(rows / 16), 512, 0, s>>>(
+                    if (rows % 2 == 0) {
+                        // 4 warps per row, 2-row groups, persistent grid (2 blocks per SM)
+                        const unsigned blocks = (unsigned)std::min<i64>(296, (rows / 2 + 3) / 4);
+                        k_bdrln_fwd_w<T, CPL, 4, 2><<<blocks, 512, 0, s>>>(
                             (const T*)partial, (const T*)bias, (const T*)res, (const T*)gamma, (const T*)beta, (T*)sum,
                             (T*)y, mean, rstd, rows, (int)n, eps, s1, thr, dscale, keep);
                         return;
