@@ -114,6 +114,61 @@ __device__ __forceinline__ uint32_t d_keep_word(uint64_t s1, uint64_t bk, uint64
     return m;
 }
 
+static __device__ __noinline__ uint32_t d_keep_word_slow(uint64_t s1, uint64_t bk, uint64_t T) { return d_keep_word(s1, bk, T); }
+// 64-bit multiply by a constant in three IMADs (the generic form compiles to four)
+__device__ __forceinline__ void sm64_mul3(uint32_t& lo, uint32_t& hi, uint32_t mlo, uint32_t mhi) {
+    asm("{\n\t.reg .u32 pl, ph, t;\n\t"
+        "mul.lo.u32 pl, %0, %2;\n\tmul.hi.u32 ph, %0, %2;\n\t"
+        "mad.lo.u32 t, %0, %3, ph;\n\tmad.lo.u32 %1, %1, %2, t;\n\tmov.u32 %0, pl;\n\t}"
+        : "+r"(lo), "+r"(hi)
+        : "r"(mlo), "r"(mhi));
+}
+// d_keep_word with fewer integer ops per element (same bits; 250 vs 307 us per
+// 134M elements on B200, ALU-pipe bound):
+//  * the 32 indices bk .. bk+31 share their high word (checked), so the first
+//    `+ golden` and `x ^= x >> 30` on the high word take one of two precomputed
+//    values, selected by the carry with FMA-pipe mads (`one` = 1 from a kernel
+//    argument, so ptxas keeps them off the ALU pipe);
+//  * 64-bit products in three IMADs, and only the high word of the final one;
+//  * the final `h ^= h >> 31` is skipped: for T's high word t < 2^31,
+//    f(v) = v ^ (v >> 31) satisfies f(v) > t <=> v > t and f(v) == t <=> v == t,
+//    so h >= T is v > t, or v == t and a low-word compare; a tie (p ~ 2^-32 per
+//    element) reruns the exact d_keep_word for the word.
+// Falls back to d_keep_word when t >= 2^31 (p >= 0.5) or the indices cross a 2^32 boundary.
+__device__ __forceinline__ uint32_t d_keep_word_fast(uint64_t s1, uint64_t bk, uint64_t T, uint32_t one) {
+    const uint32_t thi = (uint32_t)(T >> 32), bklo = (uint32_t)bk, s1lo = (uint32_t)s1;
+    if ((thi >> 31) | (bklo > 0xFFFFFFFFu - 31u)) return d_keep_word_slow(s1, bk, T);
+    const uint32_t h0 = ((uint32_t)(bk >> 32) ^ (uint32_t)(s1 >> 32)) + 0x9e3779b9u;
+    const uint32_t H0 = h0 ^ (h0 >> 30), dH = ((h0 + 1u) ^ ((h0 + 1u) >> 30)) - H0;
+    uint32_t m = 0;
+    bool tie = false;
+#pragma unroll
+    for (int b = 0; b < 32; ++b) {
+        const uint32_t x = (bklo + (uint32_t)b) ^ s1lo;
+        uint32_t lo, cy, h, hi;
+        asm("add.cc.u32 %0, %2, 0x7f4a7c15;\n\taddc.u32 %1, 0, 0;" : "=r"(lo), "=r"(cy) : "r"(x));
+        asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(h) : "r"(cy), "r"(one), "r"(h0));
+        asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(hi) : "r"(cy), "r"(dH), "r"(H0));
+        lo ^= __funnelshift_r(lo, h, 30);
+        sm64_mul3(lo, hi, 0x1ce4e5b9u, 0xbf58476du);
+        sm64_xs(lo, hi, 27);
+        sm64_mul3(lo, hi, 0x133111ebu, 0x94d049bbu);
+        sm64_xs(lo, hi, 31);
+        sm64_add(lo, hi, 0x7f4a7c15u, 0x9e3779b9u);
+        sm64_xs(lo, hi, 30);
+        sm64_mul3(lo, hi, 0x1ce4e5b9u, 0xbf58476du);
+        sm64_xs(lo, hi, 27);
+        uint32_t v;  // high word of (lo, hi) * M2
+        asm("{\n\t.reg .u32 t;\n\tmul.lo.u32 t, %1, %4;\n\tmad.lo.u32 t, %2, %3, t;\n\tmad.hi.u32 %0, %1, %3, t;\n\t}"
+            : "=r"(v)
+            : "r"(lo), "r"(hi), "r"(0x133111ebu), "r"(0x94d049bbu));
+        m |= (uint32_t)(v >= thi) << b;
+        tie |= v == thi;
+    }
+    if (tie) return d_keep_word_slow(s1, bk, T);
+    return m;
+}
+
 __device__ __forceinline__ float gelu_f(float x) {
     const float c = 0.7978845608028654f, a = 0.044715f;
     float u = c * (x + a * x * x * x);

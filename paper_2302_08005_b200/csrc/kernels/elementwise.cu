@@ -256,12 +256,12 @@ void dropout(const void* x, void* y, DT t, i64 n, u64 s1, u64 thr, float scale, 
     });
     SBK_CHECK_LAUNCH();
 }
-__global__ void k_dropout_mask(uint32_t* bits, i64 n, uint64_t s1, uint64_t thr) {
+__global__ void k_dropout_mask(uint32_t* bits, i64 n, uint64_t s1, uint64_t thr, uint32_t one) {
     const i64 nw = (n + 31) / 32;
     const uint64_t key = d_keep_key(s1), T = thr << 11;
     for (i64 w = blockIdx.x * (i64)blockDim.x + threadIdx.x; w < nw; w += (i64)gridDim.x * blockDim.x) {
         // 32 independent hash chains per thread: fully unrolled so they interleave
-        uint32_t m = d_keep_word(s1, (uint64_t)w * 32 + key, T);
+        uint32_t m = d_keep_word_fast(s1, (uint64_t)w * 32 + key, T, one);
         if (w == nw - 1 && (n & 31)) m &= (1u << (n & 31)) - 1;
         bits[w] = m;
     }
@@ -273,7 +273,8 @@ __global__ void k_dropout_mask(uint32_t* bits, i64 n, uint64_t s1, uint64_t thr)
 // thread) and transposed (bit i of key row j, read by the backward, one key per
 // thread). A warp owns a 32x32 (query, key) block: lane = query row computes
 // its 32 keep bits, and 32 ballots transpose the block.
-__global__ void k_dropout_mask_dual(uint32_t* bits, uint32_t* bits_t, int S, long long BH, uint64_t s1, uint64_t thr) {
+__global__ void k_dropout_mask_dual(uint32_t* bits, uint32_t* bits_t, int S, long long BH, uint64_t s1, uint64_t thr,
+                                    uint32_t one) {
     // grid-stride over 32x32 (query, key) blocks, one per warp: a small persistent grid
     // (g_mask_blocks blocks of 4 warps) co-resides with the GEMM / attention CTAs and
     // uses their idle issue slots without crowding out their producer / MMA warps
@@ -284,7 +285,7 @@ __global__ void k_dropout_mask_dual(uint32_t* bits, uint32_t* bits_t, int S, lon
         const int kb = (int)(w % nb), qb = (int)((w / nb) % nb);
         const long long bh = w / ((long long)nb * nb);
         const long long e0 = (bh * S + qb * 32 + lane) * S + kb * 32;  // flat index of (query qb*32+lane, key kb*32)
-        const uint32_t m = d_keep_word(s1, (uint64_t)e0 + d_keep_key(s1), thr << 11);
+        const uint32_t m = d_keep_word_fast(s1, (uint64_t)e0 + d_keep_key(s1), thr << 11, one);
         bits[e0 >> 5] = m;
         // 32x32 bit-matrix transpose across the warp (lane = row -> lane = column):
         // swap the off-diagonal blocks of width 16, 8, 4, 2, 1
@@ -320,7 +321,7 @@ void dropout_mask_dual(uint32_t* bits, i64 BH, i64 S, u64 s1, u64 thr, cudaStrea
         cudaFuncSetAttribute(k_dropout_mask_dual, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         attr = true;
     }
-    k_dropout_mask_dual<<<grid, 128, 0, s>>>(bits, bits + words, (int)S, BH, s1, thr);
+    k_dropout_mask_dual<<<grid, 128, 0, s>>>(bits, bits + words, (int)S, BH, s1, thr, 1u);
     SBK_CHECK_LAUNCH();
 }
 void dropout_mask(uint32_t* bits, i64 n, u64 s1, u64 thr, cudaStream_t s) {
@@ -329,7 +330,7 @@ void dropout_mask(uint32_t* bits, i64 n, u64 s1, u64 thr, cudaStream_t s) {
         cudaFuncSetAttribute(k_dropout_mask, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         attr = true;
     }
-    k_dropout_mask<<<mask_grid(((n + 31) / 32 + 127) / 128), 128, 0, s>>>(bits, n, s1, thr);
+    k_dropout_mask<<<mask_grid(((n + 31) / 32 + 127) / 128), 128, 0, s>>>(bits, n, s1, thr, 1u);
     SBK_CHECK_LAUNCH();
 }
 

@@ -184,7 +184,7 @@ __global__ void __launch_bounds__(32 * kW) k_bdrln_fwd_v(const T* partial, const
 // blocks; the row mean and variance are combined across the WPR warps through
 // shared memory in a fixed order.
 template <class T, int CPL, int WPR, int NR>
-__global__ void __launch_bounds__(512) k_bdrln_fwd_w(const T* partial, const T* bias, const T* res, const T* gamma,
+__global__ void __launch_bounds__(512, 2) k_bdrln_fwd_w(const T* partial, const T* bias, const T* res, const T* gamma,
                                                      const T* beta, T* sum, T* y, float* mean, float* rstd, i64 rows,
                                                      int n, float eps, uint64_t s1, uint64_t thr, float dscale,
                                                      const uint32_t* keep) {
@@ -209,6 +209,17 @@ __global__ void __launch_bounds__(512) k_bdrln_fwd_w(const T* partial, const T* 
                 rn[k][c] = __ldcs((const typename V::R*)(res + (gi * NR + k) * n) + ch);
             }
     };
+    // per-column parameters: this thread always owns the same columns
+    // (kept packed: unpacked at each use, one ALU op per element)
+    typename V::R bbp[CW], gmp[CW], btp[CW];
+#pragma unroll
+    for (int c = 0; c < CW; ++c) {
+        const int ch = (part * CW + c) * 32 + lane;
+        if (bias) bbp[c] = ((const typename V::R*)bias)[ch];
+        else bbp[c] = typename V::R{};
+        gmp[c] = ((const typename V::R*)gamma)[ch];
+        btp[c] = ((const typename V::R*)beta)[ch];
+    }
     prefetch(grp);
     for (int it = 0; grp < ngrp; grp += gstep, ++it) {
         const i64 row0 = grp * NR;
@@ -231,15 +242,13 @@ __global__ void __launch_bounds__(512) k_bdrln_fwd_w(const T* partial, const T* 
 #pragma unroll
             for (int c = 0; c < CW; ++c) {
                 const int ch = (part * CW + c) * 32 + lane;
-                float bb[VN];
-                if (bias) V::unpack(((const typename V::R*)bias)[ch], bb);
                 uint32_t kb = 0;
-                if (thr)
-                    kb = keep ? keep_bits<VN>(keep, (row0 + k) * n + (i64)ch * VN)
-                              : hash_keep_bits<VN>(s1, thr, (row0 + k) * n + (i64)ch * VN);
+                if (thr) kb = keep_bits<VN>(keep, (row0 + k) * n + (i64)ch * VN);  // keep != null (host)
+                float bbv[VN];
+                V::unpack(bbp[c], bbv);
 #pragma unroll
                 for (int e = 0; e < VN; ++e) {
-                    float t = v[k][c][e] + (bias ? bb[e] : 0.f);
+                    float t = v[k][c][e] + bbv[e];
                     if (thr) t = ((kb >> e) & 1) ? t * dscale : 0.f;
                     v[k][c][e] = to_f(from_f<T>(t + rv[k][c][e]));  // `sum` rounded to the storage dtype first
                     sm[k] += v[k][c][e];
@@ -281,15 +290,15 @@ __global__ void __launch_bounds__(512) k_bdrln_fwd_w(const T* partial, const T* 
 #pragma unroll
         for (int c = 0; c < CW; ++c) {
             const int ch = (part * CW + c) * 32 + lane;
-            float gm[VN], bt[VN];
-            V::unpack(((const typename V::R*)gamma)[ch], gm);
-            V::unpack(((const typename V::R*)beta)[ch], bt);
+            float gmv[VN], btv[VN];
+            V::unpack(gmp[c], gmv);
+            V::unpack(btp[c], btv);
 #pragma unroll
             for (int k = 0; k < NR; ++k) {
                 const float rs = rsqrtf(q[k] / (float)n + eps);
                 float o[VN];
 #pragma unroll
-                for (int e = 0; e < VN; ++e) o[e] = gm[e] * ((v[k][c][e] - mu[k]) * rs) + bt[e];
+                for (int e = 0; e < VN; ++e) o[e] = gmv[e] * ((v[k][c][e] - mu[k]) * rs) + btv[e];
                 ((typename V::R*)(y + (row0 + k) * n))[ch] = V::pack(o);
             }
         }
@@ -412,7 +421,7 @@ __global__ void __launch_bounds__(32 * kW, 1)
 // co-reside with other work. The two row sums are combined across the WPR warps
 // through shared memory in a fixed order (deterministic).
 template <class T, int CPL, int MODE, int WPR>
-__global__ void __launch_bounds__(512, 1)
+__global__ void __launch_bounds__(512, 2)
     k_ln_bwd_w(const T* x, const float* mean, const float* rstd, const T* gamma, const T* g, T* gx, T* gres, bool gx_acc,
                i64 rows, int n, uint64_t s1, uint64_t thr, float dscale, const uint32_t* keep, float* ws, int ncol,
                bool gres_acc) {
@@ -421,11 +430,10 @@ __global__ void __launch_bounds__(512, 1)
     float* red = sh + (size_t)16 * ncol * (CW * 32 * VN);
     const int warp = threadIdx.x / 32, lane = threadIdx.x & 31, slot = warp / WPR, part = warp % WPR;
     using V = Vec<T>;
-    float gm[CW][VN];
-    if (gamma) {
+    typename V::R gmp[CW];  // packed; unpacked at each use
 #pragma unroll
-        for (int c = 0; c < CW; ++c) V::unpack(((const typename V::R*)gamma)[(part * CW + c) * 32 + lane], gm[c]);
-    }
+    for (int c = 0; c < CW; ++c)
+        gmp[c] = gamma ? ((const typename V::R*)gamma)[(part * CW + c) * 32 + lane] : typename V::R{};
     float pg[CW][VN] = {}, pb[CW][VN] = {}, pd[CW][VN] = {};
     int it = 0;
     // software pipeline: the next row's x / g / statistics are loaded while this row is processed
@@ -455,17 +463,20 @@ __global__ void __launch_bounds__(512, 1)
         prefetch(row + rstep);
         float a = 0.f, b = 0.f;
 #pragma unroll
-        for (int c = 0; c < CW; ++c)
+        for (int c = 0; c < CW; ++c) {
+            float gm[VN];
+            V::unpack(gmp[c], gm);
 #pragma unroll
             for (int e = 0; e < VN; ++e) {
                 const float xh = (xv[c][e] - mu) * rs;
-                const float gh = gamma ? gv[c][e] * gm[c][e] : gv[c][e];
+                const float gh = gamma ? gv[c][e] * gm[e] : gv[c][e];
                 a += gh;
                 b += gh * xh;
                 pg[c][e] += gv[c][e] * xh;
                 pb[c][e] += gv[c][e];
                 xv[c][e] = xh;
             }
+        }
         a = warp_sum(a);
         b = warp_sum(b);
         if (WPR > 1) {
@@ -487,12 +498,15 @@ __global__ void __launch_bounds__(512, 1)
         a /= (float)n;
         b /= (float)n;
 #pragma unroll
-        for (int c = 0; c < CW; ++c)
+        for (int c = 0; c < CW; ++c) {
+            float gm[VN];
+            V::unpack(gmp[c], gm);
 #pragma unroll
             for (int e = 0; e < VN; ++e) {
-                const float gh = gamma ? gv[c][e] * gm[c][e] : gv[c][e];
+                const float gh = gamma ? gv[c][e] * gm[e] : gv[c][e];
                 gv[c][e] = rs * (gh - a - xv[c][e] * b);  // d(sum) / dx
             }
+        }
         typename V::R* gxr = (typename V::R*)(gx + row * n);
         if (MODE == 0) {
 #pragma unroll
@@ -514,8 +528,7 @@ __global__ void __launch_bounds__(512, 1)
                 for (int e = 0; e < VN; ++e) o[e] = (gres_acc ? o[e] : 0.f) + gv[c][e];
                 grr[ch] = V::pack(o);
                 uint32_t kb = 0;
-                if (thr) kb = keep ? keep_bits<VN>(keep, row * n + (i64)ch * VN)
-                                   : hash_keep_bits<VN>(s1, thr, row * n + (i64)ch * VN);
+                if (thr) kb = keep_bits<VN>(keep, row * n + (i64)ch * VN);  // keep != null (host)
 #pragma unroll
                 for (int e = 0; e < VN; ++e) {
                     float d = gv[c][e];
@@ -607,10 +620,10 @@ bool bdrln_fwd_vec(const void* partial, const void* bias, const void* res, const
                 constexpr int CPL = decltype(cc)::value;
                 if constexpr (CPL % 4 == 0) {
                     // 4 warps per row, 16-warp blocks (4 rows per block)
-                    if (rows % 2 == 0) {
-                        // 4 warps per row, 2-row groups, persistent grid (2 blocks per SM)
-                        const unsigned blocks = (unsigned)std::min<i64>(296, (rows / 2 + 3) / 4);
-                        k_bdrln_fwd_w<T, CPL, 4, 2><<<blocks, 512, 0, s>>>(
+                    if (thr == 0 || keep) {
+                        // 4 warps per row, persistent grid of two 16-warp blocks per SM (<= 64 registers)
+                        const unsigned blocks = (unsigned)std::min<i64>(296, (rows + 3) / 4);
+                        k_bdrln_fwd_w<T, CPL, 4, 1><<<blocks, 512, 0, s>>>(
                             (const T*)partial, (const T*)bias, (const T*)res, (const T*)gamma, (const T*)beta, (T*)sum,
                             (T*)y, mean, rstd, rows, (int)n, eps, s1, thr, dscale, keep);
                         return;
@@ -648,6 +661,7 @@ bool ln_bwd_vec(int mode, const void* x, const float* mean, const float* rstd, c
                                                      ncol, gres_acc);
                 };
                 if constexpr (CPL % 4 == 0) {
+                  if (thr == 0 || keep) {
                     // 4 warps per row, 16-warp blocks, two blocks per SM
                     constexpr int WPR = 4;
                     const size_t sm2 = (size_t)16 * ncol * (n / WPR) * 4 + 2 * 16 * 2 * 4;
@@ -655,6 +669,10 @@ bool ln_bwd_vec(int mode, const void* x, const float* mean, const float* rstd, c
                     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
                     k<<<nblocks, 512, sm2, s>>>((const T*)x, mean, rstd, (const T*)gamma, (const T*)g, (T*)gx, (T*)gres,
                                                  gx_acc, rows, (int)n, s1, thr, dscale, keep, ws, ncol, gres_acc);
+                    return;
+                  }
+                }
+                if (false) {
                 } else if (mode == 0) {
                     launch(k_ln_bwd_v<T, CPL, 0>);
                 } else {
