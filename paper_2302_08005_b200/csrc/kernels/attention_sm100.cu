@@ -275,6 +275,201 @@ __global__ void __launch_bounds__(FCfg<NT>::THREADS, NT == 1 ? 2 : 1)
     }
 }
 
+// Forward with 64-key chunks, four CTAs per SM (one 128-query tile each):
+//   warps 0-3   softmax (thread = query row = TMEM lane)
+//   warp 4      TMA producer (Q once; K/V chunks of 64 keys, 2 stages)
+//   warp 5      TMEM allocator (128 columns) + tcgen05.mma issuer
+// TMEM: S [0,64) fp32, overwritten in place by P (bf16 pairs, [0,32)) as the
+// softmax consumes it; O [64,128). Per chunk: S = Q K^T -> softmax -> O += P V.
+// S(j+1) is issued right after PV(j), which reads P(j) from the same columns
+// (in-order tcgen05.mma execution). Four resident CTAs per SM overlap each
+// other's chains, prologues and epilogues. Keep bits are read per row from the
+// natural-layout mask one chunk ahead (8 bytes per row and chunk).
+constexpr int KC6 = 64;                      // keys per chunk
+constexpr int F6_KV_BYTES = KC6 * FD * 2;    // 8 KB
+constexpr int F6_NS = 2;                     // K/V stages
+constexpr int F6_THREADS = 192;
+constexpr int F6_SMEM = 1024 + F_TILE_BYTES + F6_NS * 2 * F6_KV_BYTES + 128;
+constexpr float kLazy6 = 8.f;                // lazy rescale threshold (log2 units)
+
+__global__ void __launch_bounds__(F6_THREADS, 4)
+    k_fa6_fwd(const __grid_constant__ CUtensorMap tQ, const __grid_constant__ CUtensorMap tK,
+              const __grid_constant__ CUtensorMap tV, FwdArgs fa) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024 - (tc5::smem_u32(smem_raw) & 1023)) & 1023);
+    uint8_t* sQ = smem;                          // [FT][FD]
+    uint8_t* sK = sQ + F_TILE_BYTES;             // [F6_NS][KC6][FD]
+    uint8_t* sV = sK + F6_NS * F6_KV_BYTES;      // [F6_NS][KC6][FD]
+    uint64_t* bars = (uint64_t*)(sV + F6_NS * F6_KV_BYTES);
+    uint64_t* q_full = bars;
+    uint64_t* kv_full = q_full + 1;         // [F6_NS]
+    uint64_t* kv_empty = kv_full + F6_NS;   // [F6_NS]
+    uint64_t* s_full = kv_empty + F6_NS;
+    uint64_t* p_full = s_full + 1;
+    uint64_t* o_done = p_full + 1;
+    uint32_t* tslot = (uint32_t*)(o_done + 1);
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int S = fa.S, nj = S / KC6;
+    const int b = blockIdx.z, h = blockIdx.y, tile = blockIdx.x;
+    const int row_base = b * S;
+
+    if (threadIdx.x == 0) {
+        mbar_init(q_full, 1);
+        for (int s = 0; s < F6_NS; ++s) {
+            mbar_init(&kv_full[s], 1);
+            mbar_init(&kv_empty[s], 1);
+        }
+        mbar_init(s_full, 1);
+        mbar_init(p_full, 4);
+        mbar_init(o_done, 1);
+        fence_barrier_init();
+    }
+    if (warp == 5) tmem_alloc<128>(tslot);
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem = *tslot;
+
+    if (warp == 4) {
+        if (lane == 0) {
+            // ------------------------------------------------ TMA producer
+            mbar_expect_tx(q_full, F_TILE_BYTES);
+            tma_load_2d(sQ, &tQ, q_full, h * FD, row_base + tile * FT);
+            for (int j = 0; j < nj; ++j) {
+                const int s = j % F6_NS;
+                mbar_wait(&kv_empty[s], ((j / F6_NS) & 1) ^ 1);
+                mbar_expect_tx(&kv_full[s], 2 * F6_KV_BYTES);
+                tma_load_2d(sK + s * F6_KV_BYTES, &tK, &kv_full[s], h * FD, row_base + j * KC6);
+                tma_load_2d(sV + s * F6_KV_BYTES, &tV, &kv_full[s], h * FD, row_base + j * KC6);
+            }
+        }
+    } else if (warp == 5) {
+        if (lane == 0) {
+            // ------------------------------------------------ MMA issuer
+            constexpr uint32_t id_s = idesc_bf16(FT, KC6, false, false);  // S = Q K^T
+            constexpr uint32_t id_o = idesc_bf16(FT, FD, false, true);    // O += P V (V MN-major)
+            const uint32_t a = smem_u32(sQ);
+            mbar_wait(q_full, 0);
+            for (int j = 0; j < nj; ++j) {
+                const int s = j % F6_NS;
+                mbar_wait(&kv_full[s], (j / F6_NS) & 1);
+                fence_after();
+                const uint32_t bk = smem_u32(sK + s * F6_KV_BYTES);
+#pragma unroll
+                for (int kk = 0; kk < FD / 16; ++kk)
+                    mma_ss(tmem, desc_kmajor(a, kk), desc_kmajor(bk, kk), id_s, kk > 0);
+                mma_commit(s_full);
+                mbar_wait(p_full, j & 1);
+                fence_after();
+                const uint32_t bv = smem_u32(sV + s * F6_KV_BYTES);
+#pragma unroll
+                for (int kk = 0; kk < KC6 / 16; ++kk)
+                    mma_ts(tmem + 64, tmem + kk * 8, desc_mnmajor(bv, kk), id_o, (j | kk) != 0);
+                mma_commit(o_done);
+                mma_commit(&kv_empty[s]);
+            }
+        }
+    } else {
+        // ---------------------------------------------------- softmax (warps 0-3)
+        const int row = warp * 32 + lane;
+        const long long qi = (long long)tile * FT + row;
+        const long long bh = (long long)b * fa.nh + h;
+        const uint32_t t_row = tmem + ((uint32_t)(warp * 32) << 16);
+        float m_used = 0.f, l = 0.f;
+        // keep bits of this row (natural layout: S/32 words per row), one chunk ahead
+        const uint2* mrow = fa.mask ? (const uint2*)(fa.mask + (bh * S + qi) * (S / 32)) : nullptr;
+        uint2 mw_next = mrow ? __ldg(mrow) : make_uint2(~0u, ~0u);
+        for (int j = 0; j < nj; ++j) {
+            const uint2 mw = mw_next;
+            if (mrow && j + 1 < nj) mw_next = __ldg(mrow + j + 1);
+            mbar_wait(s_full, j & 1);
+            fence_after();
+            // pass 1: row max of S (P overwrites S in place, so the max comes first)
+            float mx = -INFINITY;
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                uint32_t sv[32];
+                tmem_ld32_nowait(t_row + c * 32, sv);
+                tmem_ld_wait();
+#pragma unroll
+                for (int e = 0; e < 32; ++e) mx = fmaxf(mx, __uint_as_float(sv[e]));
+            }
+            mx *= fa.c;
+            if (j == 0) m_used = mx;
+            if (__any_sync(0xffffffffu, mx > m_used + kLazy6)) {
+                // rare: the running max grew by > 2^kLazy6 -> rescale O (after PV(j-1)) and l
+                const float m_new = fmaxf(m_used, mx);
+                const float f = ex2f(m_used - m_new);
+                l *= f;
+                m_used = m_new;
+                mbar_wait(o_done, (j - 1) & 1);
+                fence_after();
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    uint32_t o[32];
+                    tmem_ld32_nowait(t_row + 64 + c * 32, o);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * f);
+                    tmem_st32(t_row + 64 + c * 32, o);
+                }
+            }
+            // pass 2: P = exp2(S*c - m_used) * keep -> TMEM (bf16 pairs over S's first 32 columns)
+            float lc = 0.f;
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                const uint32_t mword = c == 0 ? mw.x : mw.y;
+                uint32_t sv[32], pk[16];
+                tmem_ld32_nowait(t_row + c * 32, sv);
+                tmem_ld_wait();
+#pragma unroll
+                for (int e = 0; e < 16; ++e) {
+                    float p0 = ex2f(fmaf(__uint_as_float(sv[2 * e]), fa.c, -m_used));
+                    float p1 = ex2f(fmaf(__uint_as_float(sv[2 * e + 1]), fa.c, -m_used));
+                    lc += p0 + p1;  // the normaliser counts every probability (dropout acts after softmax)
+                    p0 = ((mword >> (2 * e)) & 1) ? p0 : 0.f;
+                    p1 = ((mword >> (2 * e + 1)) & 1) ? p1 : 0.f;
+                    pk[e] = pack_bf16(p0, p1);
+                }
+                tmem_st16(t_row + c * 16, pk);
+            }
+            l += lc;
+            tmem_st_wait();
+            fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(p_full);
+        }
+        // ---------------------------------------------------- epilogue
+        mbar_wait(o_done, (nj - 1) & 1);
+        fence_after();
+        const float inv = fa.dscale / l;
+        bf16* orow = fa.o + (long long)(row_base + qi) * fa.ld_o + (long long)h * FD;
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            uint32_t o[32];
+            tmem_ld32_nowait(t_row + 64 + c * 32, o);
+            tmem_ld_wait();
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                uint4 w;
+                w.x = pack_bf16(__uint_as_float(o[8 * v + 0]) * inv, __uint_as_float(o[8 * v + 1]) * inv);
+                w.y = pack_bf16(__uint_as_float(o[8 * v + 2]) * inv, __uint_as_float(o[8 * v + 3]) * inv);
+                w.z = pack_bf16(__uint_as_float(o[8 * v + 4]) * inv, __uint_as_float(o[8 * v + 5]) * inv);
+                w.w = pack_bf16(__uint_as_float(o[8 * v + 6]) * inv, __uint_as_float(o[8 * v + 7]) * inv);
+                *(uint4*)(orow + c * 32 + v * 8) = w;
+            }
+        }
+        fa.lse[bh * S + qi] = (m_used + __log2f(l)) * 0.6931471805599453f;  // natural log
+    }
+    fence_before();
+    __syncthreads();
+    if (warp == 5) {
+        fence_after();
+        tmem_dealloc<128>(tmem);
+    }
+}
+
 bool fwd_fits(const Attn& a) {
     if (a.t != BF16 || a.hd != FD || a.S % FT || a.S < FT) return false;
     if (a.thr && !a.mask) return false;
@@ -796,7 +991,18 @@ bool attn_fwd_sm100_try(const Attn& a, cudaStream_t s) {
         dim3 grid((unsigned)((a.S / FT + NT - 1) / NT), (unsigned)a.nh, (unsigned)a.B);
         k_fa5_fwd<NT><<<grid, FCfg<NT>::THREADS, FCfg<NT>::SMEM, s>>>(tq, tk, tv, tm, fa);
     };
-    if (nt_env == 2) go(std::integral_constant<int, 2>{});
+    if (nt_env == 6) {
+        CUtensorMap tk6, tv6;
+        if (!make_map_bf16(&tk6, a.k, cols, rows, a.ld_k, KC6) || !make_map_bf16(&tv6, a.v, cols, rows, a.ld_v, KC6))
+            return false;
+        static bool attr6 = false;
+        if (!attr6) {
+            cudaFuncSetAttribute(k_fa6_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, F6_SMEM);
+            attr6 = true;
+        }
+        dim3 grid((unsigned)(a.S / FT), (unsigned)a.nh, (unsigned)a.B);
+        k_fa6_fwd<<<grid, F6_THREADS, F6_SMEM, s>>>(tq, tk6, tv6, fa);
+    } else if (nt_env == 2) go(std::integral_constant<int, 2>{});
     else go(std::integral_constant<int, 1>{});
     SBK_CHECK_LAUNCH();
     return true;

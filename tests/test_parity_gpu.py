@@ -123,6 +123,30 @@ def test_dropout_mask_bit_exact():
         assert np.array_equal(got, want)
 
 
+def test_dropout_mask_threshold_ties():
+    """Thresholds equal to an element's hash in the high word: the keep-bit kernels
+    take their exact tie path (the fast test compares high words only)."""
+    import ctypes
+    import torch
+    from oracle import slapo_oracle as so
+    n = 4099
+    exec_seed, node_seed = 99, 1040
+    s = so.hash_combine(exec_seed, node_seed)
+    u = so.uniform01_array(s, 0xD0, n)
+    k = (u * 2.0 ** 53).astype(np.uint64)  # = h >> 11 per element
+    picks = [i for i in range(0, n, 37) if k[i] < (1 << 52)][:12]
+    assert picks
+    for i in picks:
+        for kk in (int(k[i]), int(k[i]) + 1, int(k[i]) - 1):
+            p = kk * 2.0 ** -53
+            bits = torch.zeros((n + 31) // 32, dtype=torch.int32, device="cuda")
+            assert sb.lib().sb_dropout_mask(ctypes.c_void_p(bits.data_ptr()), n, exec_seed, node_seed, p, None) == 0
+            torch.cuda.synchronize()
+            b = bits.cpu().numpy().view(np.uint32)
+            got = np.array([(b[j // 32] >> (j % 32)) & 1 for j in range(n)], dtype=bool)
+            assert np.array_equal(got, u >= p), (i, kk)
+
+
 def test_fig3c_partials_and_sync():
     m = sb.fig3c_exact()
     x = [np.array([[1.0, 2.0]])]
