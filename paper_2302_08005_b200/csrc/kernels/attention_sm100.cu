@@ -18,6 +18,7 @@
 // other tile's softmax runs. The running max is rescaled lazily (only when it
 // grows by more than 2^8), and O is touched only then; S(j+1)'s completion
 // implies PV(j)'s (tcgen05.commit tracks every earlier MMA), so no extra wait.
+#include <algorithm>
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
@@ -52,6 +53,7 @@ struct FwdArgs {
     float dscale;          // 1/(1-p)
     float c;               // scale * log2(e)
     int S, nh;
+    int dbg;               // debugging switches (SB_ATTN_DBG): 1 skip softmax math, 4 skip MMAs
 };
 
 template <int NT>
@@ -275,16 +277,18 @@ __global__ void __launch_bounds__(FCfg<NT>::THREADS, NT == 1 ? 2 : 1)
     }
 }
 
-// Forward with 64-key chunks, four CTAs per SM (one 128-query tile each):
-//   warps 0-3   softmax (thread = query row = TMEM lane)
-//   warp 4      TMA producer (Q once; K/V chunks of 64 keys, 2 stages)
+// Forward with 64-key chunks, four persistent CTAs per SM, each walking 128-query
+// tiles (tile t = (b*nh + h)*S/128 + q-tile, grid-strided):
+//   warps 0-3   softmax (thread = query row = TMEM lane) + the tile epilogue
+//   warp 4      TMA producer: Q per tile (Q buffer released by the tile's last
+//               S MMA), K/V chunks of 64 keys through a 2-stage ring
 //   warp 5      TMEM allocator (128 columns) + tcgen05.mma issuer
 // TMEM: S [0,64) fp32, overwritten in place by P (bf16 pairs, [0,32)) as the
 // softmax consumes it; O [64,128). Per chunk: S = Q K^T -> softmax -> O += P V.
 // S(j+1) is issued right after PV(j), which reads P(j) from the same columns
-// (in-order tcgen05.mma execution). Four resident CTAs per SM overlap each
-// other's chains, prologues and epilogues. Keep bits are read per row from the
-// natural-layout mask one chunk ahead (8 bytes per row and chunk).
+// (in-order tcgen05.mma execution); the next tile's first S overlaps this
+// tile's epilogue, and its first PV waits until the epilogue has read O.
+// Keep bits are read per row from the natural-layout mask one chunk ahead.
 constexpr int KC6 = 64;                      // keys per chunk
 constexpr int F6_KV_BYTES = KC6 * FD * 2;    // 8 KB
 constexpr int F6_NS = 2;                     // K/V stages
@@ -294,7 +298,7 @@ constexpr float kLazy6 = 8.f;                // lazy rescale threshold (log2 uni
 
 __global__ void __launch_bounds__(F6_THREADS, 4)
     k_fa6_fwd(const __grid_constant__ CUtensorMap tQ, const __grid_constant__ CUtensorMap tK,
-              const __grid_constant__ CUtensorMap tV, FwdArgs fa) {
+              const __grid_constant__ CUtensorMap tV, FwdArgs fa, int ntiles) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024 - (tc5::smem_u32(smem_raw) & 1023)) & 1023);
     uint8_t* sQ = smem;                          // [FT][FD]
@@ -302,20 +306,21 @@ __global__ void __launch_bounds__(F6_THREADS, 4)
     uint8_t* sV = sK + F6_NS * F6_KV_BYTES;      // [F6_NS][KC6][FD]
     uint64_t* bars = (uint64_t*)(sV + F6_NS * F6_KV_BYTES);
     uint64_t* q_full = bars;
-    uint64_t* kv_full = q_full + 1;         // [F6_NS]
+    uint64_t* q_empty = q_full + 1;
+    uint64_t* kv_full = q_empty + 1;        // [F6_NS]
     uint64_t* kv_empty = kv_full + F6_NS;   // [F6_NS]
     uint64_t* s_full = kv_empty + F6_NS;
     uint64_t* p_full = s_full + 1;
     uint64_t* o_done = p_full + 1;
-    uint32_t* tslot = (uint32_t*)(o_done + 1);
+    uint64_t* o_free = o_done + 1;          // epilogue has read O (4 softmax warps)
+    uint32_t* tslot = (uint32_t*)(o_free + 1);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    const int S = fa.S, nj = S / KC6;
-    const int b = blockIdx.z, h = blockIdx.y, tile = blockIdx.x;
-    const int row_base = b * S;
+    const int S = fa.S, nj = S / KC6, nq = S / FT;
 
     if (threadIdx.x == 0) {
         mbar_init(q_full, 1);
+        mbar_init(q_empty, 1);
         for (int s = 0; s < F6_NS; ++s) {
             mbar_init(&kv_full[s], 1);
             mbar_init(&kv_empty[s], 1);
@@ -323,6 +328,7 @@ __global__ void __launch_bounds__(F6_THREADS, 4)
         mbar_init(s_full, 1);
         mbar_init(p_full, 4);
         mbar_init(o_done, 1);
+        mbar_init(o_free, 4);
         fence_barrier_init();
     }
     if (warp == 5) tmem_alloc<128>(tslot);
@@ -334,14 +340,24 @@ __global__ void __launch_bounds__(F6_THREADS, 4)
     if (warp == 4) {
         if (lane == 0) {
             // ------------------------------------------------ TMA producer
-            mbar_expect_tx(q_full, F_TILE_BYTES);
-            tma_load_2d(sQ, &tQ, q_full, h * FD, row_base + tile * FT);
-            for (int j = 0; j < nj; ++j) {
-                const int s = j % F6_NS;
-                mbar_wait(&kv_empty[s], ((j / F6_NS) & 1) ^ 1);
-                mbar_expect_tx(&kv_full[s], 2 * F6_KV_BYTES);
-                tma_load_2d(sK + s * F6_KV_BYTES, &tK, &kv_full[s], h * FD, row_base + j * KC6);
-                tma_load_2d(sV + s * F6_KV_BYTES, &tV, &kv_full[s], h * FD, row_base + j * KC6);
+            int u = 0, n = 0;  // chunks / tiles loaded by this CTA
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++n) {
+                const int bh = t / nq, b = bh / fa.nh, h = bh % fa.nh;
+                const int row_base = b * S;
+                mbar_wait(q_empty, (n & 1) ^ 1);
+                mbar_expect_tx(q_full, F_TILE_BYTES);
+                tma_load_2d(sQ, &tQ, q_full, h * FD, row_base + (t % nq) * FT);
+                for (int j = 0; j < nj; ++j, ++u) {
+                    const int s = u % F6_NS;
+                    mbar_wait(&kv_empty[s], ((u / F6_NS) & 1) ^ 1);
+                    if (fa.dbg & 8) {  // debugging: no K/V traffic
+                        mbar_arrive(&kv_full[s]);
+                        continue;
+                    }
+                    mbar_expect_tx(&kv_full[s], 2 * F6_KV_BYTES);
+                    tma_load_2d(sK + s * F6_KV_BYTES, &tK, &kv_full[s], h * FD, row_base + j * KC6);
+                    tma_load_2d(sV + s * F6_KV_BYTES, &tV, &kv_full[s], h * FD, row_base + j * KC6);
+                }
             }
         }
     } else if (warp == 5) {
@@ -350,117 +366,139 @@ __global__ void __launch_bounds__(F6_THREADS, 4)
             constexpr uint32_t id_s = idesc_bf16(FT, KC6, false, false);  // S = Q K^T
             constexpr uint32_t id_o = idesc_bf16(FT, FD, false, true);    // O += P V (V MN-major)
             const uint32_t a = smem_u32(sQ);
-            mbar_wait(q_full, 0);
-            for (int j = 0; j < nj; ++j) {
-                const int s = j % F6_NS;
-                mbar_wait(&kv_full[s], (j / F6_NS) & 1);
-                fence_after();
-                const uint32_t bk = smem_u32(sK + s * F6_KV_BYTES);
+            int u = 0, n = 0;
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++n) {
+                mbar_wait(q_full, n & 1);
+                for (int j = 0; j < nj; ++j, ++u) {
+                    const int s = u % F6_NS;
+                    mbar_wait(&kv_full[s], (u / F6_NS) & 1);
+                    fence_after();
+                    // S(j) overwrites P(j-1) in TMEM: tcgen05.mma executes in issue order, so
+                    // PV(j-1) (issued first) has read it (the CUTLASS Blackwell FMHA relies on the same)
+                    const uint32_t bk = smem_u32(sK + s * F6_KV_BYTES);
+                    if (!(fa.dbg & 4))
 #pragma unroll
-                for (int kk = 0; kk < FD / 16; ++kk)
-                    mma_ss(tmem, desc_kmajor(a, kk), desc_kmajor(bk, kk), id_s, kk > 0);
-                mma_commit(s_full);
-                mbar_wait(p_full, j & 1);
-                fence_after();
-                const uint32_t bv = smem_u32(sV + s * F6_KV_BYTES);
+                        for (int kk = 0; kk < FD / 16; ++kk)
+                            mma_ss(tmem, desc_kmajor(a, kk), desc_kmajor(bk, kk), id_s, kk > 0);
+                    mma_commit(s_full);
+                    if (j == nj - 1) mma_commit(q_empty);  // last read of this tile's Q
+                    if (j == 0 && n > 0) mbar_wait(o_free, (n - 1) & 1);  // previous epilogue read O
+                    mbar_wait(p_full, u & 1);
+                    fence_after();
+                    const uint32_t bv = smem_u32(sV + s * F6_KV_BYTES);
+                    if (!(fa.dbg & 4))
 #pragma unroll
-                for (int kk = 0; kk < KC6 / 16; ++kk)
-                    mma_ts(tmem + 64, tmem + kk * 8, desc_mnmajor(bv, kk), id_o, (j | kk) != 0);
-                mma_commit(o_done);
-                mma_commit(&kv_empty[s]);
+                        for (int kk = 0; kk < KC6 / 16; ++kk)
+                            mma_ts(tmem + 64, tmem + kk * 8, desc_mnmajor(bv, kk), id_o, (j | kk) != 0);
+                    mma_commit(o_done);
+                    mma_commit(&kv_empty[s]);
+                }
             }
         }
     } else {
         // ---------------------------------------------------- softmax (warps 0-3)
         const int row = warp * 32 + lane;
-        const long long qi = (long long)tile * FT + row;
-        const long long bh = (long long)b * fa.nh + h;
         const uint32_t t_row = tmem + ((uint32_t)(warp * 32) << 16);
-        float m_used = 0.f, l = 0.f;
-        // keep bits of this row (natural layout: S/32 words per row), one chunk ahead
-        const uint2* mrow = fa.mask ? (const uint2*)(fa.mask + (bh * S + qi) * (S / 32)) : nullptr;
-        uint2 mw_next = mrow ? __ldg(mrow) : make_uint2(~0u, ~0u);
-        for (int j = 0; j < nj; ++j) {
-            const uint2 mw = mw_next;
-            if (mrow && j + 1 < nj) mw_next = __ldg(mrow + j + 1);
-            mbar_wait(s_full, j & 1);
-            fence_after();
-            // pass 1: row max of S (P overwrites S in place, so the max comes first)
-            float mx = -INFINITY;
-#pragma unroll
-            for (int c = 0; c < 2; ++c) {
-                uint32_t sv[32];
-                tmem_ld32_nowait(t_row + c * 32, sv);
-                tmem_ld_wait();
-#pragma unroll
-                for (int e = 0; e < 32; ++e) mx = fmaxf(mx, __uint_as_float(sv[e]));
-            }
-            mx *= fa.c;
-            if (j == 0) m_used = mx;
-            if (__any_sync(0xffffffffu, mx > m_used + kLazy6)) {
-                // rare: the running max grew by > 2^kLazy6 -> rescale O (after PV(j-1)) and l
-                const float m_new = fmaxf(m_used, mx);
-                const float f = ex2f(m_used - m_new);
-                l *= f;
-                m_used = m_new;
-                mbar_wait(o_done, (j - 1) & 1);
+        int u = 0;
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            const long long bh = t / nq;
+            const long long qi = (long long)(t % nq) * FT + row;
+            const int b = (int)(bh / fa.nh), h = (int)(bh % fa.nh);
+            float m_used = 0.f, l = 0.f;
+            // keep bits of this row (natural layout: S/32 words per row), one chunk ahead
+            const uint2* mrow = fa.mask ? (const uint2*)(fa.mask + (bh * S + qi) * (S / 32)) : nullptr;
+            uint2 mw_next = mrow ? __ldg(mrow) : make_uint2(~0u, ~0u);
+            for (int j = 0; j < nj; ++j, ++u) {
+                const uint2 mw = mw_next;
+                if (mrow && j + 1 < nj) mw_next = __ldg(mrow + j + 1);
+                mbar_wait(s_full, u & 1);
                 fence_after();
+                if (fa.dbg & 1) {
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(p_full);
+                    l = 1.f;
+                    continue;
+                }
+                // pass 1: row max of S (P overwrites S in place, so the max comes first)
+                float mx = -INFINITY;
 #pragma unroll
                 for (int c = 0; c < 2; ++c) {
-                    uint32_t o[32];
-                    tmem_ld32_nowait(t_row + 64 + c * 32, o);
+                    uint32_t sv[32];
+                    tmem_ld32_nowait(t_row + c * 32, sv);
                     tmem_ld_wait();
 #pragma unroll
-                    for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * f);
-                    tmem_st32(t_row + 64 + c * 32, o);
+                    for (int e = 0; e < 32; ++e) mx = fmaxf(mx, __uint_as_float(sv[e]));
                 }
-            }
-            // pass 2: P = exp2(S*c - m_used) * keep -> TMEM (bf16 pairs over S's first 32 columns)
-            float lc = 0.f;
+                mx *= fa.c;
+                if (j == 0) m_used = mx;
+                if (__any_sync(0xffffffffu, mx > m_used + kLazy6)) {
+                    // rare: the running max grew by > 2^kLazy6 -> rescale O (after PV(j-1)) and l
+                    const float m_new = fmaxf(m_used, mx);
+                    const float f = ex2f(m_used - m_new);
+                    l *= f;
+                    m_used = m_new;
+                    mbar_wait(o_done, (u - 1) & 1);
+                    fence_after();
 #pragma unroll
-            for (int c = 0; c < 2; ++c) {
-                const uint32_t mword = c == 0 ? mw.x : mw.y;
-                uint32_t sv[32], pk[16];
-                tmem_ld32_nowait(t_row + c * 32, sv);
-                tmem_ld_wait();
+                    for (int c = 0; c < 2; ++c) {
+                        uint32_t o[32];
+                        tmem_ld32_nowait(t_row + 64 + c * 32, o);
+                        tmem_ld_wait();
 #pragma unroll
-                for (int e = 0; e < 16; ++e) {
-                    float p0 = ex2f(fmaf(__uint_as_float(sv[2 * e]), fa.c, -m_used));
-                    float p1 = ex2f(fmaf(__uint_as_float(sv[2 * e + 1]), fa.c, -m_used));
-                    lc += p0 + p1;  // the normaliser counts every probability (dropout acts after softmax)
-                    p0 = ((mword >> (2 * e)) & 1) ? p0 : 0.f;
-                    p1 = ((mword >> (2 * e + 1)) & 1) ? p1 : 0.f;
-                    pk[e] = pack_bf16(p0, p1);
+                        for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * f);
+                        tmem_st32(t_row + 64 + c * 32, o);
+                    }
                 }
-                tmem_st16(t_row + c * 16, pk);
+                // pass 2: P = exp2(S*c - m_used) * keep -> TMEM (bf16 pairs over S's first 32 columns)
+                float lc = 0.f;
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    const uint32_t mword = c == 0 ? mw.x : mw.y;
+                    uint32_t sv[32], pk[16];
+                    tmem_ld32_nowait(t_row + c * 32, sv);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) {
+                        float p0 = ex2f(fmaf(__uint_as_float(sv[2 * e]), fa.c, -m_used));
+                        float p1 = ex2f(fmaf(__uint_as_float(sv[2 * e + 1]), fa.c, -m_used));
+                        lc += p0 + p1;  // the normaliser counts every probability (dropout acts after softmax)
+                        p0 = ((mword >> (2 * e)) & 1) ? p0 : 0.f;
+                        p1 = ((mword >> (2 * e + 1)) & 1) ? p1 : 0.f;
+                        pk[e] = pack_bf16(p0, p1);
+                    }
+                    tmem_st16(t_row + c * 16, pk);
+                }
+                l += lc;
+                tmem_st_wait();
+                fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(p_full);
             }
-            l += lc;
-            tmem_st_wait();
+            // ------------------------------------------------ epilogue
+            mbar_wait(o_done, (u - 1) & 1);
+            fence_after();
+            uint32_t o[2][32];
+            tmem_ld32_nowait(t_row + 64, o[0]);
+            tmem_ld32_nowait(t_row + 96, o[1]);
+            tmem_ld_wait();
             fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(p_full);
-        }
-        // ---------------------------------------------------- epilogue
-        mbar_wait(o_done, (nj - 1) & 1);
-        fence_after();
-        const float inv = fa.dscale / l;
-        bf16* orow = fa.o + (long long)(row_base + qi) * fa.ld_o + (long long)h * FD;
+            if (lane == 0) mbar_arrive(o_free);  // O may be overwritten by the next tile's PV
+            const float inv = fa.dscale / l;
+            bf16* orow = fa.o + (long long)(b * S + qi) * fa.ld_o + (long long)h * FD;
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
-            uint32_t o[32];
-            tmem_ld32_nowait(t_row + 64 + c * 32, o);
-            tmem_ld_wait();
+            for (int c = 0; c < 2; ++c)
 #pragma unroll
-            for (int v = 0; v < 4; ++v) {
-                uint4 w;
-                w.x = pack_bf16(__uint_as_float(o[8 * v + 0]) * inv, __uint_as_float(o[8 * v + 1]) * inv);
-                w.y = pack_bf16(__uint_as_float(o[8 * v + 2]) * inv, __uint_as_float(o[8 * v + 3]) * inv);
-                w.z = pack_bf16(__uint_as_float(o[8 * v + 4]) * inv, __uint_as_float(o[8 * v + 5]) * inv);
-                w.w = pack_bf16(__uint_as_float(o[8 * v + 6]) * inv, __uint_as_float(o[8 * v + 7]) * inv);
-                *(uint4*)(orow + c * 32 + v * 8) = w;
-            }
+                for (int v = 0; v < 4; ++v) {
+                    uint4 w;
+                    w.x = pack_bf16(__uint_as_float(o[c][8 * v + 0]) * inv, __uint_as_float(o[c][8 * v + 1]) * inv);
+                    w.y = pack_bf16(__uint_as_float(o[c][8 * v + 2]) * inv, __uint_as_float(o[c][8 * v + 3]) * inv);
+                    w.z = pack_bf16(__uint_as_float(o[c][8 * v + 4]) * inv, __uint_as_float(o[c][8 * v + 5]) * inv);
+                    w.w = pack_bf16(__uint_as_float(o[c][8 * v + 6]) * inv, __uint_as_float(o[c][8 * v + 7]) * inv);
+                    *(uint4*)(orow + c * 32 + v * 8) = w;
+                }
+            fa.lse[bh * S + qi] = (m_used + __log2f(l)) * 0.6931471805599453f;  // natural log
         }
-        fa.lse[bh * S + qi] = (m_used + __log2f(l)) * 0.6931471805599453f;  // natural log
     }
     fence_before();
     __syncthreads();
@@ -979,8 +1017,9 @@ bool attn_fwd_sm100_try(const Attn& a, cudaStream_t s) {
     memset(&tm, 0, sizeof(tm));
     if (a.thr && !make_map_u32(&tm, a.mask, a.S / 32, a.B * a.nh * a.S, a.S / 32, FT / 32, FT)) return false;
     FwdArgs fa{(bf16*)a.o, a.ld_o, a.lse, a.thr ? a.mask : nullptr, a.thr ? a.dscale : 1.f,
-               a.scale * 1.4426950408889634f, (int)a.S, (int)a.nh};
-    static int nt_env = getenv("SB_ATTN_FWD_NT") ? atoi(getenv("SB_ATTN_FWD_NT")) : 1;
+               a.scale * 1.4426950408889634f, (int)a.S, (int)a.nh, 0};
+    if (const char* e = getenv("SB_ATTN_DBG")) fa.dbg = atoi(e);
+    static int nt_env = getenv("SB_ATTN_FWD_NT") ? atoi(getenv("SB_ATTN_FWD_NT")) : 6;
     auto go = [&](auto ntc) {
         constexpr int NT = decltype(ntc)::value;
         static bool attr = false;
@@ -1000,8 +1039,11 @@ bool attn_fwd_sm100_try(const Attn& a, cudaStream_t s) {
             cudaFuncSetAttribute(k_fa6_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, F6_SMEM);
             attr6 = true;
         }
-        dim3 grid((unsigned)(a.S / FT), (unsigned)a.nh, (unsigned)a.B);
-        k_fa6_fwd<<<grid, F6_THREADS, F6_SMEM, s>>>(tq, tk6, tv6, fa);
+        static int sms = 0;
+        if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+        const long long ntiles = a.B * a.nh * (a.S / FT);
+        const int grid = (int)std::min<long long>(ntiles, 4ll * sms);
+        k_fa6_fwd<<<grid, F6_THREADS, F6_SMEM, s>>>(tq, tk6, tv6, fa, (int)ntiles);
     } else if (nt_env == 2) go(std::integral_constant<int, 2>{});
     else go(std::integral_constant<int, 1>{});
     SBK_CHECK_LAUNCH();
