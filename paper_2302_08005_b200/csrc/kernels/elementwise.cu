@@ -462,7 +462,7 @@ __global__ void k_bias_partial(const T* g, i64 ld, i64 rows, i64 cols, float* pa
     part[(i64)blockIdx.y * cols + c] = acc;
 }
 // bf16, cols % 8 == 0, 16-byte aligned rows: thread = 8 columns (one 16-byte load per
-// row), 8 rows of loads in flight; row chunks of kBiasChunkV summed in row order
+// row), 16 rows of loads in flight; row chunks of kBiasChunkV summed in row order
 constexpr int kBiasChunkV = 32;
 __global__ void k_bias_partial_v(const bf16* g, i64 ld, i64 rows, i64 cols, float* part) {
     const i64 c8 = blockIdx.x * (i64)blockDim.x + threadIdx.x;  // 8-column group
@@ -471,12 +471,12 @@ __global__ void k_bias_partial_v(const bf16* g, i64 ld, i64 rows, i64 cols, floa
     const i64 r1 = r0 + kBiasChunkV < rows ? r0 + kBiasChunkV : rows;
     float acc[8] = {};
     i64 r = r0;
-    for (; r + 8 <= r1; r += 8) {
-        uint4 v[8];
+    for (; r + 16 <= r1; r += 16) {
+        uint4 v[16];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = __ldcs((const uint4*)(g + (r + u) * ld) + c8);
+        for (int u = 0; u < 16; ++u) v[u] = __ldcs((const uint4*)(g + (r + u) * ld) + c8);
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < 16; ++u) {
             const __nv_bfloat162* h = (const __nv_bfloat162*)&v[u];
 #pragma unroll
             for (int t = 0; t < 4; ++t) {
@@ -500,7 +500,7 @@ __global__ void k_bias_partial_v(const bf16* g, i64 ld, i64 rows, i64 cols, floa
     o[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
     o[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
 }
-// block = 32 columns x 32 warps: warp w sums chunks w, w+32, ... (4 loads in flight);
+// block = 32 columns x 32 warps: warp w sums chunks w, w+32, ... (8 loads in flight);
 // then the 32 sums in warp order (fixed order: deterministic)
 __global__ void __launch_bounds__(1024) k_bias_final(const float* part, i64 chunks, i64 cols, float* db, bool accum) {
     __shared__ float s[32][33];
@@ -509,13 +509,12 @@ __global__ void __launch_bounds__(1024) k_bias_final(const float* part, i64 chun
     float acc = 0.f;
     if (c < cols) {
         i64 k = warp;
-        for (; k + 96 < chunks; k += 128) {
-            const float a0 = part[k * cols + c], a1 = part[(k + 32) * cols + c], a2 = part[(k + 64) * cols + c],
-                        a3 = part[(k + 96) * cols + c];
-            acc += a0;
-            acc += a1;
-            acc += a2;
-            acc += a3;
+        for (; k + 7 * 32 < chunks; k += 8 * 32) {  // 8 loads in flight, summed in chunk order
+            float a[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) a[u] = part[(k + u * 32) * cols + c];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) acc += a[u];
         }
         for (; k < chunks; k += 32) acc += part[k * cols + c];
     }
