@@ -26,6 +26,7 @@
 #include <string>
 #include <vector>
 
+#include "slapo/dump.hpp"
 #include "slapo/executor.hpp"
 #include "slapo/model_io.hpp"
 #include "slapo/rng.hpp"
@@ -90,7 +91,7 @@ int main(int argc, char** argv) {
         {"batch", "4"}, {"seq", "4"}, {"p", "0.1"}, {"dtype", "f64"}, {"schedule", ""},
         {"world", "1"}, {"mode", "train"}, {"seed", "123"}, {"input_seed", "9"}, {"out", ""},
         {"backward", "1"}, {"dump_params", "0"}, {"probe_rng", ""}, {"model_json", ""},
-        {"tp_hidden", "8"}, {"tp_inner", "16"}, {"tp_batch", "4"}, {"repeat", "1"}};
+        {"tp_hidden", "8"}, {"tp_inner", "16"}, {"tp_batch", "4"}, {"repeat", "1"}, {"cli_run", ""}};
     for (int i = 1; i + 1 < argc; i += 2) {
         std::string k = argv[i];
         if (k.rfind("--", 0) != 0) { std::cerr << "bad arg " << k << "\n"; return 2; }
@@ -150,6 +151,21 @@ int main(int argc, char** argv) {
         }
         ExecMode mode = a["mode"] == "verify" ? ExecMode::Verify : ExecMode::Train;
         std::uint64_t seed = std::stoull(a["seed"]);
+        if (!a["cli_run"].empty()) {
+            // `slapo run MODEL [SCRIPT] --seed --mode --dump` (proj/tools/slapo_main.cpp:168-199):
+            // default_inputs (:69-76), run_forward / run_sharded, write_tensor_dump (dump.cpp:29)
+            auto specs = declared_input_specs(*model.forward);
+            std::vector<TensorValue> ins;
+            for (std::size_t i = 0; i < specs.size(); ++i)
+                ins.push_back(random_tensor(specs[i], derive_seed(seed, "cli-input"), static_cast<std::uint64_t>(i)));
+            std::vector<TensorValue> outs;
+            if (a["schedule"].empty()) outs = run_forward(model, ins, mode, derive_seed(seed, "run"));
+            else if (world > 1) outs = run_sharded(res.model, ins, world, mode, derive_seed(seed, "run"));
+            else outs = run_forward(res.model, ins, mode, derive_seed(seed, "run"));
+            write_tensor_dump(a["cli_run"], outs);
+            for (const auto& t : outs) std::cout << format_tensor_text(t) << "\n";
+            return 0;
+        }
         auto specs = declared_input_specs(*model.forward);
         std::vector<TensorValue> inputs;
         for (std::size_t i = 0; i < specs.size(); ++i)
