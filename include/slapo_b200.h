@@ -42,6 +42,16 @@ int sb_model_to_json(const sb_model* m, char* buf, size_t cap, size_t* needed);
 int sb_model_to_f32(sb_model* m);
 /* modules_structurally_equal — proj/include/slapo/module.hpp:127 */
 int sb_model_equal(const sb_model* a, const sb_model* b, int* equal);
+/* Analytical step-time / memory estimate (slapo::estimate, proj/include/slapo/costmodel.hpp:52;
+ * proj/src/costmodel.cpp:258-266). constants: {device_flops_per_s, link_bytes_per_s,
+ * kernel_launch_overhead_s, optimizer_state_multiplier} or NULL for the reference defaults.
+ * ints[8]: flops, recompute_flops, launches, collective_bytes, param_bytes, activation_bytes,
+ * peak_memory_bytes, oom; reals[2]: step_time_s, throughput_samples_per_s; text: CostReport::to_text. */
+int sb_estimate(const sb_model* m, int64_t batch, int world_size, int64_t device_memory_bytes, const double* constants,
+                int64_t* ints, double* reals, char* text, size_t cap, size_t* needed);
+/* Flag the first floor(ratio * L) children of `container` as checkpointed
+ * (slapo::apply_checkpoint_ratio, costmodel.hpp:59; costmodel.cpp:310-324). */
+int sb_model_apply_checkpoint_ratio(sb_model* m, const char* container, double ratio, int* count);
 int sb_model_free(sb_model* m);
 /* declared_input_specs — proj/include/slapo/shape_inference.hpp:37 */
 int sb_model_num_inputs(const sb_model* m, int* n);

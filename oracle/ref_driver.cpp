@@ -26,7 +26,9 @@
 #include <string>
 #include <vector>
 
+#include "slapo/costmodel.hpp"
 #include "slapo/dump.hpp"
+#include "slapo/tuner.hpp"
 #include "slapo/executor.hpp"
 #include "slapo/model_io.hpp"
 #include "slapo/rng.hpp"
@@ -91,7 +93,9 @@ int main(int argc, char** argv) {
         {"batch", "4"}, {"seq", "4"}, {"p", "0.1"}, {"dtype", "f64"}, {"schedule", ""},
         {"world", "1"}, {"mode", "train"}, {"seed", "123"}, {"input_seed", "9"}, {"out", ""},
         {"backward", "1"}, {"dump_params", "0"}, {"probe_rng", ""}, {"model_json", ""},
-        {"tp_hidden", "8"}, {"tp_inner", "16"}, {"tp_batch", "4"}, {"repeat", "1"}, {"cli_run", ""}};
+        {"tp_hidden", "8"}, {"tp_inner", "16"}, {"tp_batch", "4"}, {"repeat", "1"}, {"cli_run", ""},
+        {"estimate", ""}, {"est_batch", "0"}, {"est_mem", "17179869184"}, {"est_consts", ""}, {"ckpt_container", ""},
+        {"ckpt_ratio", "0"}, {"tune", ""}, {"tune_seed", "0"}, {"tune_restarts", "3"}};
     for (int i = 1; i + 1 < argc; i += 2) {
         std::string k = argv[i];
         if (k.rfind("--", 0) != 0) { std::cerr << "bad arg " << k << "\n"; return 2; }
@@ -148,6 +152,68 @@ int main(int argc, char** argv) {
             for (int r = 0; r < world; ++r)
                 for (auto& [name, p] : ps) dump.push_back({"r" + std::to_string(r) + ":" + name, init_param_rank(*p, r)});
             write_dump(out + "/params.bin", dump);
+        }
+        auto est_opts = [&](std::int64_t batch) {
+            // EstimateOptions (costmodel.hpp:37-43); est_consts "flops,link,launch,optmult"
+            EstimateOptions eo;
+            eo.batch = batch;
+            eo.world_size = world;
+            eo.device_memory_bytes = std::stoll(a["est_mem"]);
+            if (!a["est_consts"].empty()) {
+                std::stringstream ss(a["est_consts"]);
+                std::string t;
+                std::vector<double> v;
+                while (std::getline(ss, t, ',')) v.push_back(std::stod(t));
+                eo.constants = CostConstants{v.at(0), v.at(1), v.at(2), v.at(3)};
+            }
+            return eo;
+        };
+        auto est_json = [](const CostReport& r) {
+            char buf[512];
+            std::snprintf(buf, sizeof(buf),
+                          "{\"step_time_s\": %.17g, \"flops\": %lld, \"recompute_flops\": %lld, \"launches\": %lld, "
+                          "\"collective_bytes\": %lld, \"param_bytes\": %lld, \"activation_bytes\": %lld, "
+                          "\"peak_memory_bytes\": %lld, \"oom\": %d, \"throughput_samples_per_s\": %.17g}",
+                          r.step_time_s, (long long)r.flops, (long long)r.recompute_flops, (long long)r.launches,
+                          (long long)r.collective_bytes, (long long)r.param_bytes, (long long)r.activation_bytes,
+                          (long long)r.peak_memory_bytes, r.oom ? 1 : 0, r.throughput_samples_per_s);
+            return std::string(buf);
+        };
+        if (!a["estimate"].empty()) {
+            // slapo::estimate (costmodel.cpp:258) of the post-apply model, optionally after
+            // apply_checkpoint_ratio (costmodel.cpp:310); prints to_text then a JSON line
+            ModuleDef m = res.model;
+            if (!a["ckpt_container"].empty()) apply_checkpoint_ratio(m, a["ckpt_container"], std::stod(a["ckpt_ratio"]));
+            CostReport r = estimate(m, est_opts(std::stoll(a["est_batch"])));
+            std::cout << r.to_text() << est_json(r) << std::endl;
+            return 0;
+        }
+        if (!a["tune"].empty()) {
+            // slapo::exhaustive / coordinate_descent (tuner.cpp:98-180) over batch x checkpoint
+            // ratio with the cost-model objective of cmd_tune (slapo_main.cpp:218-252):
+            // batch in {est_batch/4, /2, x1, x2, x4}, ratio in {0, .25, .5, .75, 1}; prints the trials
+            const std::int64_t b0 = std::stoll(a["est_batch"]);
+            SearchSpace sp;
+            SymbolicVar vb, vr;
+            vb.name = "batch";
+            for (std::int64_t f : {1, 2, 4, 8, 16}) vb.candidates.push_back(Expr::parse(std::to_string(b0 * f / 4)));
+            vr.name = "ckpt";
+            for (const char* r : {"0", "0.25", "0.5", "0.75", "1"}) vr.candidates.push_back(Expr::parse(r));
+            sp.vars = {vb, vr};
+            Objective obj = [&](const Assignment& as) -> TrialEval {
+                ModuleDef m = res.model;
+                apply_checkpoint_ratio(m, a["ckpt_container"], as.at("ckpt"));
+                CostReport r = estimate(m, est_opts(static_cast<std::int64_t>(as.at("batch"))));
+                return {r.oom ? 0.0 : r.throughput_samples_per_s, r};
+            };
+            TunerResult tr = a["tune"] == "cd" ? coordinate_descent(sp, obj, std::stoull(a["tune_seed"]),
+                                                                    std::stoi(a["tune_restarts"]))
+                                               : exhaustive(sp, obj);
+            for (const auto& t : tr.trials)
+                std::printf("trial %.17g %.17g %.17g\n", t.assignment.at("batch"), t.assignment.at("ckpt"), t.objective);
+            std::printf("best %.17g %.17g %.17g all_zero %d\n", tr.best.assignment.at("batch"), tr.best.assignment.at("ckpt"),
+                        tr.best.objective, tr.all_zero ? 1 : 0);
+            return 0;
         }
         ExecMode mode = a["mode"] == "verify" ? ExecMode::Verify : ExecMode::Train;
         std::uint64_t seed = std::stoull(a["seed"]);

@@ -60,6 +60,9 @@ for _n, _a in {
     "sb_model_to_f32": (_P,),
     "sb_model_equal": (_P, _P, _c.POINTER(_c.c_int)),
     "sb_model_free": (_P,),
+    "sb_estimate": (_P, _i64, _c.c_int, _i64, _dp, _c.POINTER(_i64), _dp, _c.c_char_p, _c.c_size_t,
+                    _c.POINTER(_c.c_size_t)),
+    "sb_model_apply_checkpoint_ratio": (_P, _c.c_char_p, _c.c_double, _c.POINTER(_c.c_int)),
     "sb_model_num_inputs": (_P, _c.POINTER(_c.c_int)),
     "sb_model_input_shape": (_P, _c.c_int, _c.POINTER(_i64), _c.POINTER(_c.c_int)),
     "sb_model_random_input": (_P, _c.c_int, _u64, _u64, _dp, _c.c_size_t, _c.POINTER(_c.c_size_t)),
@@ -204,6 +207,12 @@ class Model:
             _check(_lib.sb_model_random_input(self._h, i, seed, i, a.ctypes.data_as(_dp), n, _c.byref(nn)))
             res.append(a.reshape(shape))
         return res
+
+    def apply_checkpoint_ratio(self, container: str, ratio: float) -> int:
+        """Flag the first floor(ratio * L) children of `container` as checkpointed (costmodel.cpp:310-324)."""
+        n = _c.c_int()
+        _check(_lib.sb_model_apply_checkpoint_ratio(self._h, container.encode(), ratio, _c.byref(n)))
+        return n.value
 
     def param_values(self, dotted: str, rank: int = 0) -> np.ndarray:
         """init_param_rank(param, rank): bit-exact host materialisation."""

@@ -12,6 +12,7 @@
 #include "host/executor.hpp"
 #include "host/rng.hpp"
 #include "host/schedule.hpp"
+#include "host/step_model.hpp"
 
 using namespace sb;
 
@@ -127,6 +128,36 @@ int sb_model_to_f32(sb_model* m) {
 }
 int sb_model_equal(const sb_model* a, const sb_model* b, int* eq) {
     return guard([&] { *eq = modules_equal(a->m, b->m) ? 1 : 0; });
+}
+int sb_estimate(const sb_model* m, int64_t batch, int world_size, int64_t device_memory_bytes, const double* constants,
+                int64_t* ints, double* reals, char* text, size_t cap, size_t* needed) {
+    return guard([&] {
+        EstimateOptions o;
+        o.batch = batch;
+        o.world_size = world_size;
+        o.device_memory_bytes = device_memory_bytes;
+        if (constants)
+            o.constants = CostConstants{constants[0], constants[1], constants[2], constants[3]};
+        CostReport r = estimate(m->m, o);
+        if (ints) {
+            const int64_t v[8] = {r.flops, r.recompute_flops, r.launches, r.collective_bytes,
+                                  r.param_bytes, r.activation_bytes, r.peak_memory_bytes, r.oom ? 1 : 0};
+            std::memcpy(ints, v, sizeof(v));
+        }
+        if (reals) {
+            reals[0] = r.step_time_s;
+            reals[1] = r.throughput_samples_per_s;
+        }
+        std::string t = r.to_text();
+        if (needed) *needed = t.size() + 1;
+        if (text && cap >= t.size() + 1) std::memcpy(text, t.c_str(), t.size() + 1);
+    });
+}
+int sb_model_apply_checkpoint_ratio(sb_model* m, const char* container, double ratio, int* count) {
+    return guard([&] {
+        int c = apply_checkpoint_ratio(m->m, container ? container : "", ratio);
+        if (count) *count = c;
+    });
 }
 int sb_model_free(sb_model* m) {
     delete m;
