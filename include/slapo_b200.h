@@ -23,6 +23,7 @@ extern "C" {
 
 typedef struct sb_model sb_model;       /* slapo::ModuleDef                    */
 typedef struct sb_schedule sb_schedule; /* slapo::Schedule (a path handle)     */
+typedef struct sb_pipeline sb_pipeline; /* slapo::PipelineStagePlan             */
 typedef struct sb_executor sb_executor; /* slapo::Executor                     */
 
 const char* sb_last_error(void);
@@ -80,6 +81,16 @@ int sb_schedule_load_script(sb_schedule* s, const char* text);
 int sb_schedule_num_warnings(const sb_schedule* s, int* n);
 /* Schedule::apply — proj/src/schedule.cpp:719-746 */
 int sb_schedule_apply(const sb_schedule* s, sb_model** out);
+/* Schedule::apply with pipeline_split annotations: the stage plan
+ * (ApplyResult::stages, proj/include/slapo/schedule.hpp:54-57; build_pipeline_plan,
+ * proj/src/pipeline.cpp:343-420). Stage i's module is returned as a fresh sb_model;
+ * stage_io: which 0 = consumes, 1 = produces (i < 0: the plan's model inputs / outputs),
+ * newline-terminated names. */
+int sb_schedule_apply_pipeline(const sb_schedule* s, sb_pipeline** out);
+int sb_pipeline_num_stages(const sb_pipeline* p, int* n);
+int sb_pipeline_stage(const sb_pipeline* p, int i, sb_model** out);
+int sb_pipeline_stage_io(const sb_pipeline* p, int i, int which, char* buf, size_t cap, size_t* needed);
+int sb_pipeline_free(sb_pipeline* p);
 int sb_schedule_free(sb_schedule* s);
 
 /* -------------------------------------------------------------- executor */

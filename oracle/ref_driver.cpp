@@ -95,7 +95,7 @@ int main(int argc, char** argv) {
         {"backward", "1"}, {"dump_params", "0"}, {"probe_rng", ""}, {"model_json", ""},
         {"tp_hidden", "8"}, {"tp_inner", "16"}, {"tp_batch", "4"}, {"repeat", "1"}, {"cli_run", ""},
         {"estimate", ""}, {"est_batch", "0"}, {"est_mem", "17179869184"}, {"est_consts", ""}, {"ckpt_container", ""},
-        {"ckpt_ratio", "0"}, {"tune", ""}, {"tune_seed", "0"}, {"tune_restarts", "3"}};
+        {"ckpt_ratio", "0"}, {"tune", ""}, {"tune_seed", "0"}, {"tune_restarts", "3"}, {"micro", "1"}};
     for (int i = 1; i + 1 < argc; i += 2) {
         std::string k = argv[i];
         if (k.rfind("--", 0) != 0) { std::cerr << "bad arg " << k << "\n"; return 2; }
@@ -144,6 +144,23 @@ int main(int argc, char** argv) {
         if (!out.empty()) {
             std::ofstream(out + "/model.json") << save_model(res.model);
             std::ofstream(out + "/original.json") << save_model(model);
+            if (res.stages) {  // the stage plan (ApplyResult::stages, schedule.hpp:54-57)
+                std::ofstream io(out + "/stages.txt");
+                io << "inputs";
+                for (auto& x : res.stages->model_inputs) io << " " << x;
+                io << "\noutputs";
+                for (auto& x : res.stages->model_outputs) io << " " << x;
+                io << "\n";
+                for (std::size_t i = 0; i < res.stages->stages.size(); ++i) {
+                    const auto& st = res.stages->stages[i];
+                    std::ofstream(out + "/stage" + std::to_string(i) + ".json") << save_model(st.module);
+                    io << "stage" << i << " consumes";
+                    for (auto& x : st.consumes) io << " " << x;
+                    io << " produces";
+                    for (auto& x : st.produces) io << " " << x;
+                    io << "\n";
+                }
+            }
         }
         if (a["dump_params"] == "1" && !out.empty()) {
             std::vector<std::pair<std::string, const ParamDef*>> ps;
@@ -226,6 +243,8 @@ int main(int argc, char** argv) {
                 ins.push_back(random_tensor(specs[i], derive_seed(seed, "cli-input"), static_cast<std::uint64_t>(i)));
             std::vector<TensorValue> outs;
             if (a["schedule"].empty()) outs = run_forward(model, ins, mode, derive_seed(seed, "run"));
+            else if (res.stages)
+                outs = run_pipeline(*res.stages, ins, std::stoi(a["micro"]), mode, derive_seed(seed, "run"));
             else if (world > 1) outs = run_sharded(res.model, ins, world, mode, derive_seed(seed, "run"));
             else outs = run_forward(res.model, ins, mode, derive_seed(seed, "run"));
             write_tensor_dump(a["cli_run"], outs);

@@ -82,6 +82,11 @@ for _n, _a in {
     "sb_schedule_num_warnings": (_P, _c.POINTER(_c.c_int)),
     "sb_schedule_apply": (_P, _c.POINTER(_P)),
     "sb_schedule_free": (_P,),
+    "sb_schedule_apply_pipeline": (_P, _c.POINTER(_P)),
+    "sb_pipeline_num_stages": (_P, _c.POINTER(_c.c_int)),
+    "sb_pipeline_stage": (_P, _c.c_int, _c.POINTER(_P)),
+    "sb_pipeline_stage_io": (_P, _c.c_int, _c.c_int, _c.c_char_p, _c.c_size_t, _c.POINTER(_c.c_size_t)),
+    "sb_pipeline_free": (_P,),
     "sb_executor_create": (_P, _c.c_int, _u64, _c.c_int, _c.c_int, _c.c_int, _c.POINTER(_P)),
     "sb_nccl_unique_id": (_P,),
     "sb_executor_create_nccl": (_P, _c.c_int, _u64, _c.c_int, _c.c_int, _P, _c.c_int, _c.c_int, _c.POINTER(_P)),
@@ -304,10 +309,48 @@ class Schedule:
         _check(_lib.sb_schedule_num_warnings(self._h, _c.byref(n)))
         return n.value
 
+    def apply_pipeline(self) -> "PipelinePlan":
+        """apply() with pipeline_split annotations: the stage plan (ApplyResult::stages)."""
+        h = _P()
+        _check(_lib.sb_schedule_apply_pipeline(self._h, _c.byref(h)))
+        try:
+            n = _c.c_int()
+            _check(_lib.sb_pipeline_num_stages(h, _c.byref(n)))
+
+            def names(i, which):
+                need = _c.c_size_t()
+                _check(_lib.sb_pipeline_stage_io(h, i, which, None, 0, _c.byref(need)))
+                buf = _c.create_string_buffer(need.value)
+                _check(_lib.sb_pipeline_stage_io(h, i, which, buf, need.value, _c.byref(need)))
+                return [x for x in buf.value.decode().split("\n") if x]
+            stages = []
+            for i in range(n.value):
+                mh = _P()
+                _check(_lib.sb_pipeline_stage(h, i, _c.byref(mh)))
+                stages.append(PipelineStage(Model(mh), names(i, 0), names(i, 1)))
+            return PipelinePlan(stages, names(-1, 0), names(-1, 1))
+        finally:
+            _lib.sb_pipeline_free(h)
+
     def apply(self) -> Model:
         h = _P()
         _check(_lib.sb_schedule_apply(self._h, _c.byref(h)))
         return Model(h)
+
+
+@dataclass
+class PipelineStage:
+    module: Model
+    consumes: List[str]
+    produces: List[str]
+
+
+@dataclass
+class PipelinePlan:
+    """slapo::PipelineStagePlan (proj/include/slapo/pipeline.hpp:14-27)."""
+    stages: List[PipelineStage]
+    model_inputs: List[str]
+    model_outputs: List[str]
 
 
 def create_schedule(model: Model, world_size: int = 1) -> Schedule:
@@ -532,3 +575,53 @@ def run_sharded(model: Model, inputs, world_size: int, mode="verify", seed=0, **
     if world_size < 2:
         raise SlapoError("run_sharded requires world_size > 1")
     return Executor(model, mode, seed, world_size, **kw).forward(inputs)
+
+
+def run_pipeline(plan: PipelinePlan, inputs, micro_batches: int = 1, mode: str = "verify", seed: int = 0,
+                 dtype: str = "fp32") -> List[np.ndarray]:
+    """GPipe forward of a stage plan on the GPU (run_pipeline, proj/src/executor.cpp:1531-1579):
+    the batch is cut into `micro_batches` slices along dim 0; for each micro-batch
+    the stages run in order, every stage on the device through its own executor,
+    its inputs bound by name from the model inputs and earlier stages' outputs;
+    the model outputs are concatenated along dim 0 in micro-batch order."""
+    if micro_batches < 1:
+        raise SlapoError("micro_batches must be >= 1")
+    if len(inputs) != len(plan.model_inputs):
+        raise SlapoError(f"pipeline expects {len(plan.model_inputs)} inputs")
+    def micro_module(m: Model) -> Model:
+        # the executor plans from declared input shapes: a stage runs on 1/micro of the batch
+        if micro_batches == 1:
+            return m
+        d = json.loads(m.to_json())
+        for node in d["modules"].get("forward", []):
+            if node.get("kind") == "input":
+                shape = node["attrs"]["shape"]
+                if shape[0] % micro_batches:
+                    raise SlapoError(f"batch dimension {shape[0]} not divisible into {micro_batches} micro-batches")
+                shape[0] //= micro_batches
+        return Model.from_json(json.dumps(d))
+
+    execs = [Executor(micro_module(st.module), mode=mode, seed=seed, dtype=dtype) for st in plan.stages]
+    chunks = []
+    for c in range(micro_batches):
+        env = {}
+        for name, x in zip(plan.model_inputs, inputs):
+            x = np.asarray(x)
+            if micro_batches > 1:
+                if x.shape[0] % micro_batches:
+                    raise SlapoError(f"batch dimension {x.shape[0]} not divisible into {micro_batches} micro-batches")
+                per = x.shape[0] // micro_batches
+                x = x[c * per:(c + 1) * per]
+            env[name] = x
+        for st, ex in zip(plan.stages, execs):
+            missing = [n for n in st.consumes if n not in env]
+            if missing:
+                raise SlapoError(f"pipeline stage consumes unknown value '{missing[0]}'")
+            outs = ex.forward([env[n] for n in st.consumes])
+            if len(outs) != len(st.produces):
+                raise SlapoError(f"pipeline stage produced {len(outs)} values, expected {len(st.produces)}")
+            env.update(zip(st.produces, outs))
+        chunks.append([env[n] for n in plan.model_outputs])
+    if micro_batches == 1:
+        return chunks[0]
+    return [np.concatenate([ch[o] for ch in chunks], axis=0) for o in range(len(plan.model_outputs))]

@@ -5,7 +5,7 @@ dumps (e.g. one written by the reference's `slapo run --dump`).
 
     python -m paper_2302_08005_b200 inspect MODEL.json
     python -m paper_2302_08005_b200 apply   MODEL.json SCRIPT [--world-size N] [--out OUT.json]
-    python -m paper_2302_08005_b200 run     MODEL.json [SCRIPT] [--seed S] [--world-size N]
+    python -m paper_2302_08005_b200 run     MODEL.json [SCRIPT] [--seed S] [--world-size N] [--micro-batches M]
                                             [--mode verify|train] [--dump OUT.sld] [--dtype fp32|bf16]
     python -m paper_2302_08005_b200 verify  MODEL.json SCRIPT [--world-size N] [--seed S]
                                             [--trials T] [--atol A] [--rtol R]
@@ -136,12 +136,24 @@ def _run_outputs(model, inputs, world: int, mode: str, seed: int, dtype: str) ->
     return ex.forward(inputs)
 
 
+def _has_stages(script_path: Optional[str]) -> bool:
+    return bool(script_path) and any(ln.split()[:1] == ["pipeline_split"] for ln in _read(script_path).splitlines())
+
+
 def cmd_run(a) -> int:
+    from . import create_schedule, run_pipeline
     model = _load_model(a.model)
     dt = _input_dtype(json.loads(_read(a.model)))
     inputs = cli_inputs(model, a.seed)
-    target = _apply(model, a.script, a.world_size) if a.script else model
-    outs = _run_outputs(target, inputs, a.world_size if a.script else 1, a.mode, derive_seed(a.seed, "run"), a.dtype)
+    if _has_stages(a.script):  # cmd_run's run_pipeline branch (slapo_main.cpp:180-182)
+        sch = create_schedule(model, a.world_size)
+        sch.load_script(_read(a.script))
+        outs = run_pipeline(sch.apply_pipeline(), inputs, max(a.micro_batches, 1), a.mode, derive_seed(a.seed, "run"),
+                            a.dtype)
+    else:
+        target = _apply(model, a.script, a.world_size) if a.script else model
+        outs = _run_outputs(target, inputs, a.world_size if a.script else 1, a.mode, derive_seed(a.seed, "run"),
+                            a.dtype)
     for o in outs:
         print(_dump.format_tensor_text(o, dt))
     if a.dump:
@@ -241,6 +253,7 @@ def main(argv: Optional[List[str]] = None) -> int:
     q.add_argument("--world-size", type=int, default=1)
     q.add_argument("--mode", choices=["verify", "train"], default="verify")
     q.add_argument("--dump", default="")
+    q.add_argument("--micro-batches", type=int, default=1)
     q.add_argument("--dtype", choices=["fp32", "bf16"], default="fp32")
     q = sp.add_parser("verify")
     q.add_argument("model")

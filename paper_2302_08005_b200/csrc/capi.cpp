@@ -12,6 +12,7 @@
 #include "host/executor.hpp"
 #include "host/rng.hpp"
 #include "host/schedule.hpp"
+#include "host/stages.hpp"
 #include "host/step_model.hpp"
 
 using namespace sb;
@@ -21,6 +22,9 @@ struct sb_model {
 };
 struct sb_schedule {
     Schedule s;
+};
+struct sb_pipeline {
+    StagePlan p;
 };
 struct sb_executor {
     std::unique_ptr<Executor> ex;
@@ -243,6 +247,34 @@ int sb_schedule_num_warnings(const sb_schedule* s, int* n) {
 }
 int sb_schedule_apply(const sb_schedule* s, sb_model** out) {
     return guard([&] { *out = new sb_model{s->s.apply().model}; });
+}
+static void put_names(const std::vector<std::string>& v, char* buf, size_t cap, size_t* needed) {
+    std::string t;
+    for (auto& x : v) t += x + "\n";
+    if (needed) *needed = t.size() + 1;
+    if (buf && cap >= t.size() + 1) std::memcpy(buf, t.c_str(), t.size() + 1);
+}
+int sb_schedule_apply_pipeline(const sb_schedule* s, sb_pipeline** out) {
+    return guard([&] {
+        ApplyResult r = s->s.apply();
+        *out = new sb_pipeline{build_stage_plan(r.model, r.pipeline_splits)};
+    });
+}
+int sb_pipeline_num_stages(const sb_pipeline* p, int* n) {
+    return guard([&] { *n = (int)p->p.stages.size(); });
+}
+int sb_pipeline_stage(const sb_pipeline* p, int i, sb_model** out) {
+    return guard([&] { *out = new sb_model{p->p.stages.at((size_t)i).module}; });
+}
+int sb_pipeline_stage_io(const sb_pipeline* p, int i, int which, char* buf, size_t cap, size_t* needed) {
+    return guard([&] {
+        if (i < 0) put_names(which ? p->p.model_outputs : p->p.model_inputs, buf, cap, needed);
+        else put_names(which ? p->p.stages.at((size_t)i).produces : p->p.stages.at((size_t)i).consumes, buf, cap, needed);
+    });
+}
+int sb_pipeline_free(sb_pipeline* p) {
+    delete p;
+    return 0;
 }
 int sb_schedule_free(sb_schedule* s) {
     delete s;

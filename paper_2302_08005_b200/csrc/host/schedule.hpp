@@ -66,7 +66,7 @@ struct SplitAnnotation {
 
 struct ApplyResult {
     Module model;
-    std::vector<SplitAnnotation> pipeline_splits;  // stage materialisation is §8(f1), not built
+    std::vector<SplitAnnotation> pipeline_splits;  // materialised by build_stage_plan (stages.hpp)
 };
 
 struct ScheduleState;
