@@ -1,5 +1,5 @@
 """Command-line surface of the reference's `slapo` tool for the B200 executor
-(proj/tools/slapo_main.cpp): `inspect`, `apply`, `run` and `verify` with the
+(proj/tools/slapo_main.cpp): `inspect`, `apply`, `run`, `verify` and `estimate` with the
 reference's arguments, outputs and exit codes, plus `diff` to compare two SLD1
 dumps (e.g. one written by the reference's `slapo run --dump`).
 
@@ -9,6 +9,7 @@ dumps (e.g. one written by the reference's `slapo run --dump`).
                                             [--mode verify|train] [--dump OUT.sld] [--dtype fp32|bf16]
     python -m paper_2302_08005_b200 verify  MODEL.json SCRIPT [--world-size N] [--seed S]
                                             [--trials T] [--atol A] [--rtol R]
+    python -m paper_2302_08005_b200 estimate MODEL.json [SCRIPT] [--world-size N] [--batch B] [--b200]
     python -m paper_2302_08005_b200 diff    A.sld B.sld [--atol A] [--rtol R]
 
 `run` and `verify` execute on the GPU through the C ABI (there is no CPU
@@ -111,6 +112,20 @@ def cmd_apply(a) -> int:
     with open(out, "w") as f:
         f.write(res.to_json())
     print("wrote " + out)
+    return EXIT_OK
+
+
+def cmd_estimate(a) -> int:
+    """cmd_estimate (slapo_main.cpp:146-166): the cost model of the (scheduled) model."""
+    from . import costmodel
+    model = _load_model(a.model)
+    if a.script and _has_stages(a.script):
+        raise NotImplementedError("estimate_pipeline is not built (pipeline stages: DESIGN.md §8)")
+    target = _apply(model, a.script, a.world_size) if a.script else model
+    c = costmodel.B200_CONSTANTS if a.b200 else costmodel.CostConstants()
+    mem = costmodel.B200_MEMORY_BYTES if a.b200 else 16 * 1024 ** 3
+    r = costmodel.estimate(target, batch=a.batch, world_size=a.world_size, device_memory_bytes=mem, constants=c)
+    print(r.to_text(), end="")
     return EXIT_OK
 
 
@@ -264,6 +279,12 @@ def main(argv: Optional[List[str]] = None) -> int:
     q.add_argument("--atol", type=float, default=1e-4)
     q.add_argument("--rtol", type=float, default=1e-3)
     q.add_argument("--dtype", choices=["fp32", "bf16"], default="fp32")
+    q = sp.add_parser("estimate")
+    q.add_argument("model")
+    q.add_argument("script", nargs="?", default="")
+    q.add_argument("--world-size", type=int, default=1)
+    q.add_argument("--batch", type=int, default=0)
+    q.add_argument("--b200", action="store_true", help="B200-calibrated constants and 180 GB instead of the defaults")
     q = sp.add_parser("diff")
     q.add_argument("a")
     q.add_argument("b")
@@ -275,7 +296,7 @@ def main(argv: Optional[List[str]] = None) -> int:
         return EXIT_USAGE if e.code else EXIT_OK
     try:
         return {"inspect": cmd_inspect, "apply": cmd_apply, "run": cmd_run, "verify": cmd_verify,
-                "diff": cmd_diff}[a.cmd](a)
+                "estimate": cmd_estimate, "diff": cmd_diff}[a.cmd](a)
     except SystemExit:
         raise
     except Exception as e:  # noqa: BLE001 - the CLI's internal-error exit

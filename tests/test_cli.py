@@ -158,3 +158,17 @@ def test_cli_verify_tp_recipe(tmp_path):
     lines = r.stdout.splitlines()
     assert lines[0].split() == ["trials", "3"] and lines[5].startswith("pass          true")
     assert float(lines[1].split()[1]) < 1e-4
+
+
+@needs_ref
+def test_cli_estimate_matches_reference(tmp_path):
+    """`estimate MODEL SCRIPT --batch B`: CostReport::to_text of the reference's estimate."""
+    tmp = str(tmp_path)
+    model_json, sch = _ref_model(tmp, world=2)
+    r = subprocess.run([ref.DRIVER, "--model_json", model_json, "--schedule", sch, "--world", "2", "--est_batch", "8",
+                        "--estimate", "1"], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    want = "\n".join(r.stdout.strip().splitlines()[:-1]) + "\n"
+    got = _cli("estimate", model_json, sch, "--world-size", 2, "--batch", 8)
+    assert got.returncode == 0, got.stderr
+    assert got.stdout == want
