@@ -354,14 +354,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
                     uint4 w[4];
 #pragma unroll
                     for (int j = 0; j < 4; ++j) w[j] = *(const uint4*)(mybuf + 2048 + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4));
-                    __syncwarp();
-                    if (c + 2 < G_BN / 32) aux_load((int)(col + 64), row0);  // next chunk of this warp
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {
                         const bf16* e = (const bf16*)&w[j];
 #pragma unroll
                         for (int t = 0; t < 8; ++t) v[8 * j + t] *= gelu_grad_fast(__bfloat162float(e[t]));
                     }
+                    // every lane's generic reads of the aux slot are ordered before the next
+                    // chunk's TMA (async-proxy) write into it
+                    fence_proxy_async();
+                    __syncwarp();
+                    if (c + 2 < G_BN / 32) aux_load((int)(col + 64), row0);  // next chunk of this warp
                 }
                 if (ep.accumulate) {
                     // C += v, direct read-modify-write of this thread's row
@@ -516,14 +519,25 @@ bool gemm_tc2_try(const Gemm& g, cudaStream_t s) {
     const int kblocks = (int)(K / G_BK);
     const long long tiles = (M / 256) * (N / G_BN);
     int splits = 1;
-    // long-K, few-tile problems (the weight gradients) -> deterministic split-K
+    // long-K, few-tile problems (the weight gradients) -> deterministic split-K, with the
+    // split count from a wave model: ceil(tiles * s / clusters) waves of kblocks / s
+    // k-blocks each (~0.33 us per k-block per tile, measured), plus the fp32 partials'
+    // reduce ((s + 1) * M * N * 4 bytes at ~5 TB/s) and its launch (~3 us)
+    static const int force = getenv("SB_GEMM_SPLITS") ? atoi(getenv("SB_GEMM_SPLITS")) : 0;
     if (tiles < clusters && kblocks >= 32 && g.ws && !g.epilogue) {
-        const int want = (int)((clusters + tiles - 1) / tiles);
-        for (int sp = std::min(want, 16); sp > 1; --sp)
-            if (kblocks % sp == 0 && kblocks / sp >= 8 && (size_t)sp * M * N * 4 <= g.ws_bytes) {
+        auto cost = [&](int sp) {
+            const double waves = (double)((tiles * sp + clusters - 1) / clusters);
+            const double t = waves * (double)kblocks / sp * 0.33e-6;
+            return sp == 1 ? t : t + (double)(sp + 1) * M * N * 4 / 5e12 + 3e-6;
+        };
+        double best = cost(1);
+        for (int sp = 2; sp <= 16; ++sp)
+            if (kblocks % sp == 0 && kblocks / sp >= 8 && (size_t)sp * M * N * 4 <= g.ws_bytes &&
+                (force ? sp == force : cost(sp) < best)) {
+                best = cost(sp);
                 splits = sp;
-                break;
             }
+        if (force == 1) splits = 1;
     }
     Epi2 ep{};
     ep.C = g.C;
