@@ -161,7 +161,7 @@ class Model:
         self._h = handle
 
     def __del__(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and _lib is not None:  # (at interpreter exit the module may be gone)
             _lib.sb_model_free(self._h)
             self._h = None
 
@@ -258,7 +258,7 @@ class Schedule:
         self._keep = keep
 
     def __del__(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and _lib is not None:  # (at interpreter exit the module may be gone)
             _lib.sb_schedule_free(self._h)
             self._h = None
 
@@ -404,7 +404,7 @@ class Executor:
         self._pinned = None
 
     def __del__(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and _lib is not None:  # (at interpreter exit the module may be gone)
             _lib.sb_executor_free(self._h)
             self._h = None
 
