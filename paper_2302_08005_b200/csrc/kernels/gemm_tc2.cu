@@ -78,6 +78,16 @@ __device__ __forceinline__ void mbar_wait_u32(uint32_t addr, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+// TMA load multicast to the CTAs in `mask` (same smem offset in each), completion
+// signalled on each destination pair's leader mbarrier
+__device__ __forceinline__ void tma_load_2sm_mc(uint32_t dst, const CUtensorMap* map, uint32_t bar_cluster, int c0, int c1,
+                                                uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster "
+        "[%0], [%1, {%4, %5}], [%2], %3;" ::"r"(dst),
+        "l"((uint64_t)map), "r"(bar_cluster), "h"(mask), "r"(c0), "r"(c1)
+        : "memory");
+}
 // TMA load whose completion is signalled on the leader CTA's mbarrier
 __device__ __forceinline__ void tma_load_2sm(uint32_t dst, const CUtensorMap* map, uint32_t bar_cluster, int c0, int c1) {
     asm volatile(
@@ -154,12 +164,17 @@ __device__ __forceinline__ unsigned long long gtime2() {
     return t;
 }
 struct Sched2 {
-    int m_blks, n_blks, splits, kblocks;  // cluster tiles of 256 x 256, k-blocks per split
-    __host__ __device__ int tiles() const { return m_blks * n_blks * splits; }
+    int m_blks, n_blks, splits, kblocks;  // pair tiles of 256 x BN, k-blocks per split
+    int pairs;                            // CTA pairs per cluster (N-adjacent tiles)
+    __host__ __device__ int tiles() const { return m_blks * (n_blks / pairs) * splits; }  // cluster tiles
 };
 
-template <int G_BN, bool A_MN, bool B_MN>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
+// PAIRS = 2: a cluster of two CTA pairs computes two N-adjacent 256 x BN tiles that
+// share their A rows; each pair loads half of the A block and multicasts it to both
+// pairs (a quarter less L2->SM traffic per stage), so every stage is freed only
+// when both pairs' MMAs have consumed it.
+template <int G_BN, bool A_MN, bool B_MN, int PAIRS>
+__global__ void __cluster_dims__(2 * PAIRS, 1, 1) __launch_bounds__(320, 1)
     k_gemm2(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB,
             const __grid_constant__ CUtensorMap tC, const __grid_constant__ CUtensorMap tX, Epi2 ep, Sched2 sc) {
     constexpr int G_ST = Cfg<G_BN>::ST, G_STAGE = Cfg<G_BN>::STAGE;
@@ -174,9 +189,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
     uint64_t* auxbar = tempty + 2;    // [8] per epilogue warp: its dGeLU pre-activation chunk landed
     uint32_t* tslot = (uint32_t*)(auxbar + 8);
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    const uint32_t rank = cluster_rank();
+    const uint32_t crank = cluster_rank();
+    const uint32_t rank = crank & 1u, pair = crank >> 1, lead_rank = crank & ~1u;  // rank in the pair
     const bool leader = rank == 0;
-    const int cluster = blockIdx.x / 2, nclusters = gridDim.x / 2;
+    const int cluster = blockIdx.x / (2 * PAIRS), nclusters = gridDim.x / (2 * PAIRS);
     const int ntiles = sc.tiles();
 
     if (threadIdx.x == 0) {
@@ -186,7 +202,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
         if (ep.gelu) tma_prefetch(&tX);
         for (int s = 0; s < G_ST; ++s) {
             mbar_init(&full[s], 2);
-            mbar_init(&empty[s], 1);
+            mbar_init(&empty[s], PAIRS);  // freed by every pair's MMA commit
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
@@ -204,12 +220,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
     fence_after();
     const uint32_t tmem = *tslot;
 
-    auto tile_coords = [&](int tile, int& m0, int& n0, int& z) {
-        const int per = sc.m_blks * sc.n_blks;
+    auto tile_coords = [&](int tile, int& m0, int& n0, int& z) {  // this pair's tile of the cluster tile
+        const int ncl = sc.n_blks / PAIRS, per = sc.m_blks * ncl;
         z = tile / per;
         const int r = tile % per;
-        m0 = (r / sc.n_blks) * 256;  // consecutive tiles share the A row block (L2 reuse)
-        n0 = (r % sc.n_blks) * G_BN;
+        m0 = (r / ncl) * 256;  // consecutive tiles share the A row block (L2 reuse)
+        n0 = ((r % ncl) * PAIRS + (int)pair) * G_BN;
     };
 
     if (warp == 0) {
@@ -226,12 +242,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
                     mbar_wait(&empty[s], ((it / G_ST) & 1) ^ 1);
                     if (ep.ts && cluster == 0 && it < 128) ep.ts[rank * 128 + it] = gtime2();
                     const uint32_t fb_local = smem_u32(&full[s]);
-                    const uint32_t fb = mapa_shared(fb_local, 0);
+                    const uint32_t fb = mapa_shared(fb_local, lead_rank);
                     if (leader) mbar_expect_tx_u32(fb_local, 2 * G_STAGE);
                     else mbar_arrive_cluster(fb);
                     const uint32_t sa = sbase + s * G_STAGE, sb = sa + G_A;
                     const int kc = (z * sc.kblocks + kb) * G_BK;
-                    if (A_MN) {
+                    if (PAIRS == 2) {  // this pair's 64-row share of the A block, to both pairs
+                        const uint16_t mc = (uint16_t)((1u << rank) | (1u << (rank + 2)));
+                        if (A_MN) tma_load_2sm_mc(sa + pair * 8192, &tA, fb, ma + (int)pair * 64, kc, mc);
+                        else tma_load_2sm_mc(sa + pair * 8192, &tA, fb, kc, ma + (int)pair * 64, mc);
+                    } else if (A_MN) {
                         tma_load_2sm(sa, &tA, fb, ma, kc);
                         tma_load_2sm(sa + 8192, &tA, fb, ma + 64, kc);
                     } else {
@@ -271,16 +291,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
                                                  : sdesc(b_base + k * 32, 1, 1024 >> 4);
                         mma_cta2(d, da, db, idesc, (kb | k) != 0);
                     }
-                    commit_mc(smem_u32(&empty[s]), 0x3);  // frees this stage in both CTAs
+                    commit_mc(smem_u32(&empty[s]), PAIRS == 2 ? 0xF : 0x3);  // frees this stage in every CTA
                 }
-                commit_mc(smem_u32(&tfull[acc]), 0x3);  // accumulator complete in both CTAs
+                commit_mc(smem_u32(&tfull[acc]), (uint16_t)(0x3u << (2 * pair)));  // accumulator complete in the pair
             }
         }
     } else {
         // ---------------- epilogue: TMEM -> registers -> smem -> TMA store
         const int q = warp & 3, half = (warp - 2) / 4;
         uint8_t* mybuf = epi + (warp - 2) * G_EPI_BUF;
-        const uint32_t tempty0 = mapa_shared(smem_u32(&tempty[0]), 0);
+        const uint32_t tempty0 = mapa_shared(smem_u32(&tempty[0]), lead_rank);
         int lt = 0, nst = 0, naux = 0;
         uint64_t* abar = &auxbar[warp - 2];
         // dGeLU epilogue: the pre-activation chunk (32 x 32 bf16) is TMA-loaded into the
@@ -467,18 +487,44 @@ bool make_store_map(CUtensorMap* m, const void* base, bool f32, long long cols, 
 
 int g_sms2 = 0;
 
-template <int BN, bool A_MN, bool B_MN>
+// co-resident clusters of the persistent kernel (GPCs need not split into whole 4-CTA clusters)
+template <int BN, bool A_MN, bool B_MN, int PAIRS>
+int max_clusters2() {
+    static int mc = 0;
+    if (!mc) {
+        if (!g_sms2) cudaDeviceGetAttribute(&g_sms2, cudaDevAttrMultiProcessorCount, 0);
+        auto k = k_gemm2<BN, A_MN, B_MN, PAIRS>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM);
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2 * PAIRS;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.gridDim = dim3(2 * PAIRS * (g_sms2 / (2 * PAIRS)));
+        cfg.blockDim = dim3(320);
+        cfg.dynamicSmemBytes = Cfg<BN>::SMEM;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        if (cudaOccupancyMaxActiveClusters(&mc, k, &cfg) != cudaSuccess || mc <= 0) mc = g_sms2 / (2 * PAIRS);
+        mc = std::min(mc, g_sms2 / (2 * PAIRS));
+    }
+    return mc;
+}
+
+template <int BN, bool A_MN, bool B_MN, int PAIRS>
 void launch2(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const CUtensorMap& tx, const Epi2& ep,
              const Sched2& sc, cudaStream_t s) {
-    auto k = k_gemm2<BN, A_MN, B_MN>;
+    auto k = k_gemm2<BN, A_MN, B_MN, PAIRS>;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM);
         attr = true;
     }
     if (!g_sms2) cudaDeviceGetAttribute(&g_sms2, cudaDevAttrMultiProcessorCount, 0);
-    const int clusters = std::min(sc.tiles(), g_sms2 / 2);
-    k<<<clusters * 2, 320, Cfg<BN>::SMEM, s>>>(ta, tb, tc, tx, ep, sc);
+    const int max_clusters = max_clusters2<BN, A_MN, B_MN, PAIRS>();
+    const int clusters = std::min(sc.tiles(), max_clusters);
+    k<<<clusters * 2 * PAIRS, 320, Cfg<BN>::SMEM, s>>>(ta, tb, tc, tx, ep, sc);
 }
 
 }  // namespace
@@ -509,15 +555,25 @@ bool gemm_tc2_try(const Gemm& g, cudaStream_t s) {
     CUtensorMap ta, tb, tc, tx;
     memset(&tc, 0, sizeof(tc));
     memset(&tx, 0, sizeof(tx));
-    if (!(a_mn ? make_map_bf16(&ta, g.A, M, K, lda, 64) : make_map_bf16(&ta, g.A, K, M, lda, G_BM))) return false;
     if (!g_sms2) cudaDeviceGetAttribute(&g_sms2, cudaDevAttrMultiProcessorCount, 0);
-    const int clusters = g_sms2 / 2;
     // tile N 256 (measured: the 256x128 tile, though it evens out the last wave of
     // N = 1024 problems, runs 30-40% slower on the BERT-large shapes)
     const int G_BN = g_tc2_bn ? g_tc2_bn : 256;
+    // two CTA pairs per cluster sharing A (multicast) for mainloop-dominated problems
+    // (K >= 4096) when N holds an even number of tiles: a quarter less L2->SM traffic per
+    // stage, but 4-CTA clusters fit only 33 per chip (132 SMs): measured +2-3% on
+    // K = 4096 / 16384, -3-6% on the K = 1024 GEMMs with GeLU / dGeLU / bias epilogues
+    static const int pairs_env = getenv("SB_GEMM_PAIRS") ? atoi(getenv("SB_GEMM_PAIRS")) : 0;
+    const int pairs = (N / G_BN) % 2 ? 1 : pairs_env ? pairs_env : (K >= 4096 ? 2 : 1);
+    // pair slots of the persistent grid (the split-K model below counts waves in them)
+    const int clusters = pairs == 2 ? 2 * (G_BN == 256 ? max_clusters2<256, false, false, 2>()
+                                                       : max_clusters2<128, false, false, 2>())
+                                    : g_sms2 / 2;
+    if (!(a_mn ? make_map_bf16(&ta, g.A, M, K, lda, 64) : make_map_bf16(&ta, g.A, K, M, lda, pairs == 2 ? 64 : G_BM)))
+        return false;
     if (!(b_mn ? make_map_bf16(&tb, g.B, N, K, ldb, 64) : make_map_bf16(&tb, g.B, K, N, ldb, G_BN / 2))) return false;
     const int kblocks = (int)(K / G_BK);
-    const long long tiles = (M / 256) * (N / G_BN);
+    const long long tiles = (M / 256) * (N / G_BN);  // pair tiles
     int splits = 1;
     // long-K, few-tile problems (the weight gradients) -> deterministic split-K, with the
     // split count from a wave model: ceil(tiles * s / clusters) waves of kblocks / s
@@ -559,7 +615,7 @@ bool gemm_tc2_try(const Gemm& g, cudaStream_t s) {
     if (g.epilogue && splits == 1) {  // GeLU: pre-activation store map; dGeLU: pre-activation load map
         if (!make_store_map(&tx, g.aux, false, N, M, ldc)) return false;
     }
-    Sched2 sc{(int)(M / 256), (int)(N / G_BN), splits, kblocks / splits};
+    Sched2 sc{(int)(M / 256), (int)(N / G_BN), splits, kblocks / splits, pairs};
     static unsigned long long* ts_buf = nullptr;
     ep.ts = nullptr;
     if (getenv("SB_GEMM_TS")) {
@@ -569,10 +625,15 @@ bool gemm_tc2_try(const Gemm& g, cudaStream_t s) {
     }
     auto go = [&](auto bn) {
         constexpr int BN = decltype(bn)::value;
-        if (!a_mn && !b_mn) launch2<BN, false, false>(ta, tb, tc, tx, ep, sc, s);
-        else if (!a_mn && b_mn) launch2<BN, false, true>(ta, tb, tc, tx, ep, sc, s);
-        else if (a_mn && b_mn) launch2<BN, true, true>(ta, tb, tc, tx, ep, sc, s);
-        else launch2<BN, true, false>(ta, tb, tc, tx, ep, sc, s);
+        auto go2 = [&](auto pc) {
+            constexpr int PR = decltype(pc)::value;
+            if (!a_mn && !b_mn) launch2<BN, false, false, PR>(ta, tb, tc, tx, ep, sc, s);
+            else if (!a_mn && b_mn) launch2<BN, false, true, PR>(ta, tb, tc, tx, ep, sc, s);
+            else if (a_mn && b_mn) launch2<BN, true, true, PR>(ta, tb, tc, tx, ep, sc, s);
+            else launch2<BN, true, false, PR>(ta, tb, tc, tx, ep, sc, s);
+        };
+        if (pairs == 2) go2(std::integral_constant<int, 2>{});
+        else go2(std::integral_constant<int, 1>{});
     };
     if (G_BN == 256) go(std::integral_constant<int, 256>{});
     else go(std::integral_constant<int, 128>{});
