@@ -3,6 +3,8 @@
 // the hot contiguous paths, deterministic fixed-order reductions (no float
 // atomics), so identical runs give identical bits (the reference's
 // determinism contract, proj/tests/executor_test.cpp:273-283).
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace sbk {
@@ -440,8 +442,26 @@ __global__ void k_emb_fwd(const double* ids, i64 n, const T* table, i64 dim, i64
         out[idx] = (r >= 0 && r < local) ? table[r * dim + d] : from_f<T>(0.f);
     }
 }
+// 16-byte vectors (bf16, dim % 8 == 0): one row-slice per thread, the id read once per vector
+__global__ void k_emb_fwd_v(const double* ids, int n, const uint4* table, int vdim, i64 V, i64 row0, i64 local,
+                            uint4* out) {
+    const int total = n * vdim;
+    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
+        const int i = idx / vdim, d = idx - i * vdim;
+        const i64 r = d_row(ids[i], V) - row0;
+        out[idx] = (r >= 0 && r < local) ? __ldg(table + r * vdim + d) : make_uint4(0, 0, 0, 0);
+    }
+}
 void embedding_fwd(const double* ids, i64 n, const void* table, DT t, i64 dim, i64 V, i64 row0, i64 local, void* out,
                    cudaStream_t s) {
+    if (t == BF16 && dim % 8 == 0 && n * (dim / 8) < (1ll << 31) && ((uintptr_t)table & 15) == 0 &&
+        ((uintptr_t)out & 15) == 0) {
+        const i64 total = n * (dim / 8);
+        k_emb_fwd_v<<<(unsigned)std::min<i64>((total + 255) / 256, 148 * 16), 256, 0, s>>>(
+            ids, (int)n, (const uint4*)table, (int)(dim / 8), V, row0, local, (uint4*)out);
+        SBK_CHECK_LAUNCH();
+        return;
+    }
     dispatch(t, [&](auto* p) {
         using T = std::remove_pointer_t<decltype(p)>;
         k_emb_fwd<T><<<grid_for(n * dim, 256), 256, 0, s>>>(ids, n, (const T*)table, dim, V, row0, local, (T*)out);

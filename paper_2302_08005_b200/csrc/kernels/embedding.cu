@@ -3,8 +3,9 @@
 // outside this rank's vocab slice skipped. Deterministic (no float atomics)
 // and parallel even when the ids are heavily repeated (the reference's
 // synthetic ids hit ~9 rows):
-//   1. one block sorts keys (row << 32 | position) in shared memory and cuts
-//      the sorted order into "pieces": maximal runs of one row inside an
+//   1. keys (row << 32 | position) are sorted — by one block in shared memory, or for
+//      N >= 4096 as 1024-key runs (one block each) merged by rank — and one block
+//      cuts the sorted order into "pieces": maximal runs of one row inside an
 //      aligned 64-position chunk (piece starts, rows, segment-head flags);
 //   2. one block per (piece, 256 dims) sums its <= 64 gradient rows in order;
 //   3. the first piece of each row-segment adds its segment's piece sums, in
@@ -29,7 +30,8 @@ i64 pow2_ge(i64 n) {
 }
 
 struct Layout {
-    unsigned long long* keys;  // N (global fallback sort)
+    unsigned long long* keys;    // N (global fallback sort; sorted 1024-key runs)
+    unsigned long long* sorted;  // N (merged runs)
     int* piece_start;          // npieces + 1
     int* piece_row;
     int* piece_head;
@@ -43,6 +45,8 @@ Layout carve(void* ws, i64 n, i64 dim) {
     Layout L;
     i64 N = pow2_ge(std::max<i64>(n, 1));
     L.keys = (unsigned long long*)p;
+    p += N * 8;
+    L.sorted = (unsigned long long*)p;
     p += N * 8;
     i64 pmax = n / kChunk + n + 2;
     L.piece_start = (int*)p;
@@ -60,19 +64,70 @@ Layout carve(void* ws, i64 n, i64 dim) {
     return L;
 }
 
+// key of position i: (row << 32 | i); positions outside this rank's rows (and the
+// padding up to N) get row 0xFFFFFFFF: unique keys that sort last
+__device__ __forceinline__ unsigned long long e_key(const double* ids, i64 i, i64 n, i64 V, i64 row0, i64 local) {
+    unsigned long long k = (0xFFFFFFFFull << 32) | (unsigned long long)i;
+    if (i < n) {
+        i64 r = e_row(ids[i], V) - row0;
+        if (r >= 0 && r < local) k = ((unsigned long long)r << 32) | (unsigned long long)i;
+    }
+    return k;
+}
+__device__ __forceinline__ bool e_invalid(unsigned long long k) { return (k >> 32) == 0xFFFFFFFFull; }
+
+// large N: every block sorts one 1024-key run in shared memory ...
+__global__ void __launch_bounds__(1024) k_emb_runs(const double* ids, i64 n, i64 V, i64 row0, i64 local, Layout L) {
+    __shared__ unsigned long long k[1024];
+    const int t = threadIdx.x;
+    const i64 base = (i64)blockIdx.x * 1024;
+    k[t] = e_key(ids, base + t, n, V, row0, local);
+    __syncthreads();
+    for (int size = 2; size <= 1024; size <<= 1)
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            const int j = t ^ stride;
+            if (j > t) {
+                const bool up = (t & size) == 0;
+                const unsigned long long a = k[t], b = k[j];
+                if ((a > b) == up) {
+                    k[t] = b;
+                    k[j] = a;
+                }
+            }
+            __syncthreads();
+        }
+    L.keys[base + t] = k[t];
+}
+// ... then each key's final position is its position in its run plus, per other run,
+// the number of (unique) keys below it (binary search)
+__global__ void k_emb_merge(i64 N, Layout L) {
+    const i64 g = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+    if (g >= N) return;
+    const unsigned long long key = L.keys[g];
+    const i64 run = g / 1024, nruns = N / 1024;
+    i64 rank = g % 1024;
+    for (i64 r = 0; r < nruns; ++r) {
+        if (r == run) continue;
+        const unsigned long long* a = L.keys + r * 1024;
+        int lo = 0, hi = 1024;  // first element >= key
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (a[mid] < key) lo = mid + 1;
+            else hi = mid;
+        }
+        rank += lo;
+    }
+    L.sorted[rank] = key;
+}
+
 __global__ void __launch_bounds__(1024) k_emb_pieces(const double* ids, i64 n, i64 N, i64 V, i64 row0, i64 local,
                                                      Layout L, int use_smem) {
     extern __shared__ unsigned long long skeys[];
-    unsigned long long* keys = use_smem ? skeys : L.keys;
+    // use_smem 2: keys already sorted in L.sorted (k_emb_runs + k_emb_merge)
+    unsigned long long* keys = use_smem == 2 ? L.sorted : use_smem ? skeys : L.keys;
     __shared__ int warp_tot[32];
-    for (i64 i = threadIdx.x; i < N; i += blockDim.x) {
-        unsigned long long k = ~0ull;
-        if (i < n) {
-            i64 r = e_row(ids[i], V) - row0;
-            if (r >= 0 && r < local) k = ((unsigned long long)r << 32) | (unsigned long long)i;
-        }
-        keys[i] = k;
-    }
+    if (use_smem != 2) {
+    for (i64 i = threadIdx.x; i < N; i += blockDim.x) keys[i] = e_key(ids, i, n, V, row0, local);
     __syncthreads();
     for (i64 size = 2; size <= N; size <<= 1)
         for (i64 stride = size >> 1; stride > 0; stride >>= 1) {
@@ -89,16 +144,22 @@ __global__ void __launch_bounds__(1024) k_emb_pieces(const double* ids, i64 n, i
             }
             __syncthreads();
         }
+    }
     // piece flags over the valid prefix, block-wide exclusive scan (ordered)
     const int per = (int)((n + blockDim.x - 1) / blockDim.x);
     const i64 lo = (i64)threadIdx.x * per, hi = min(lo + per, n);
-    int cnt = 0;
+    __shared__ int s_nvalid;
+    if (threadIdx.x == 0) s_nvalid = 0;
+    __syncthreads();
+    int cnt = 0, nv = 0;  // pieces starting in / valid keys of [lo, hi) (valid keys are a prefix)
     for (i64 m = lo; m < hi; ++m) {
         unsigned long long k = keys[m];
-        if (k == ~0ull) break;
+        if (e_invalid(k)) break;
         bool flag = (m % kChunk == 0) || (keys[m - 1] >> 32) != (k >> 32);
         cnt += flag;
+        ++nv;
     }
+    if (nv) atomicAdd(&s_nvalid, nv);  // integer count: order-independent
     // scan of cnt across the block
     int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     int x = cnt;
@@ -121,7 +182,7 @@ __global__ void __launch_bounds__(1024) k_emb_pieces(const double* ids, i64 n, i
     int total = warp_tot[(blockDim.x / 32) - 1];
     for (i64 m = lo; m < hi; ++m) {
         unsigned long long k = keys[m];
-        if (k == ~0ull) break;
+        if (e_invalid(k)) break;
         L.perm[m] = (int)(k & 0xffffffffull);
         bool rowchg = m == 0 || (keys[m - 1] >> 32) != (k >> 32);
         if ((m % kChunk == 0) || rowchg) {
@@ -133,14 +194,7 @@ __global__ void __launch_bounds__(1024) k_emb_pieces(const double* ids, i64 n, i
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        // end of the valid region closes the last piece
-        i64 nvalid = 0;
-        for (i64 m = n; m > 0; --m)
-            if (keys[m - 1] != ~0ull) {
-                nvalid = m;
-                break;
-            }
-        L.piece_start[total] = (int)nvalid;
+        L.piece_start[total] = s_nvalid;  // end of the valid region closes the last piece
         *L.npieces = total;
     }
 }
@@ -164,8 +218,18 @@ __global__ void k_emb_combine(Layout L, i64 dim, float* gt) {
     i64 d = blockIdx.y * (i64)blockDim.x + threadIdx.x;
     if (d >= dim) return;
     int row = L.piece_row[p];
+    int q1 = p + 1;  // end of this row's segment
+    while (q1 < np && L.piece_row[q1] == row && !L.piece_head[q1]) ++q1;
     float acc = 0.f;
-    for (int q = p; q < np && L.piece_row[q] == row && (q == p || !L.piece_head[q]); ++q) acc += L.piece_sum[(i64)q * dim + d];
+    int q = p;
+    for (; q + 8 <= q1; q += 8) {  // 8 loads in flight, summed in piece order
+        float a[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) a[u] = L.piece_sum[(i64)(q + u) * dim + d];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc += a[u];
+    }
+    for (; q < q1; ++q) acc += L.piece_sum[(i64)q * dim + d];
     gt[(i64)row * dim + d] += acc;
 }
 }  // namespace
@@ -173,7 +237,7 @@ __global__ void k_emb_combine(Layout L, i64 dim, float* gt) {
 size_t embedding_bwd_workspace(i64 n, i64 dim) {
     i64 N = pow2_ge(std::max<i64>(n, 1));
     i64 pmax = n / kChunk + n + 2;
-    return (size_t)(N * 8 + (pmax + 1) * 4 + 2 * pmax * 4 + 16 + n * 4 + 256 + pmax * dim * 4);
+    return (size_t)(2 * N * 8 + (pmax + 1) * 4 + 2 * pmax * 4 + 16 + n * 4 + 256 + pmax * dim * 4);
 }
 
 void embedding_bwd(const double* ids, i64 n, const void* g, DT tg, i64 dim, i64 V, i64 row0, i64 local, float* gt,
@@ -183,6 +247,12 @@ void embedding_bwd(const double* ids, i64 n, const void* g, DT tg, i64 dim, i64 
     i64 N = pow2_ge(n);
     int use_smem = N <= kSortMax;
     size_t smem = use_smem ? (size_t)N * 8 : 0;
+    if (N >= 4096) {  // parallel: sorted 1024-key runs, merged by rank
+        k_emb_runs<<<(unsigned)(N / 1024), 1024, 0, s>>>(ids, n, V, row0, local, L);
+        k_emb_merge<<<(unsigned)(N / 256), 256, 0, s>>>(N, L);
+        use_smem = 2;
+        smem = 0;
+    }
     if (smem > 48 * 1024) cudaFuncSetAttribute(k_emb_pieces, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_emb_pieces<<<1, 1024, smem, s>>>(ids, n, N, V, row0, local, L, use_smem);
     i64 pmax = n / kChunk + std::min(n, local) + 2;
