@@ -18,12 +18,78 @@ void init_workspace() {
     if (!g_red_ws) cudaMalloc(&g_red_ws, sizeof(float) * kRedBlocks * 2);
 }
 
+// --------------------------------------------------- 16-byte bf16 elementwise
+// contiguous bf16 with n % 8 == 0 and 16-byte aligned operands: 8 elements per
+// thread and access (same per-element math as the scalar kernels: same bits)
+__device__ __forceinline__ void bf8_unpack(const uint4& r, float* f) {
+    const __nv_bfloat162* h = (const __nv_bfloat162*)&r;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        float2 v = __bfloat1622float2(h[i]);
+        f[2 * i] = v.x;
+        f[2 * i + 1] = v.y;
+    }
+}
+__device__ __forceinline__ uint4 bf8_pack(const float* f) {
+    uint4 r;
+    __nv_bfloat162* h = (__nv_bfloat162*)&r;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+    return r;
+}
+static bool vec8_ok(i64 n, std::initializer_list<const void*> ps) {
+    if (n % 8 || n / 8 >= (1ll << 31)) return false;
+    for (const void* p : ps)
+        if (((uintptr_t)p & 15) != 0) return false;
+    return true;
+}
+static unsigned vec8_grid(i64 n) { return (unsigned)std::min<i64>((n / 8 + 255) / 256, 148 * 16); }
+// kind: 0 fill(c) | 1 unary(op, c) | 2 unary_bwd(op, c) | 3 binary add / mul (op) | 4 y += c x
+__global__ void k_vec8(int kind, int op, const uint4* x, const uint4* g, uint4* y, int n8, float c) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += gridDim.x * blockDim.x) {
+        float a[8], b[8], o[8];
+        if (kind == 0) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) o[e] = c;
+        } else if (kind == 1) {
+            bf8_unpack(x[i], a);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) o[e] = op == 0 ? a[e] * c : op == 1 ? (a[e] > 0.f ? a[e] : 0.f) : gelu_f(a[e]);
+        } else if (kind == 2) {  // gx += d(x, g)
+            bf8_unpack(g[i], b);
+            bf8_unpack(y[i], o);
+            if (op != 0) bf8_unpack(x[i], a);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                const float d = op == 0 ? c * b[e] : op == 1 ? (a[e] > 0.f ? b[e] : 0.f) : b[e] * gelu_grad_f(a[e]);
+                o[e] = o[e] + d;
+            }
+        } else if (kind == 3) {
+            bf8_unpack(x[i], a);
+            bf8_unpack(g[i], b);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) o[e] = op == 0 ? a[e] + b[e] : a[e] * b[e];
+        } else {
+            bf8_unpack(x[i], a);
+            bf8_unpack(y[i], o);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) o[e] = o[e] + c * a[e];
+        }
+        y[i] = bf8_pack(o);
+    }
+}
+
 // ------------------------------------------------------------------- fill/cast
 template <class T>
 __global__ void k_fill(T* x, i64 n, float v) {
     for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) x[i] = from_f<T>(v);
 }
 void fill(void* x, DT t, i64 n, float v, cudaStream_t s) {
+    if (t == BF16 && vec8_ok(n, {x})) {
+        k_vec8<<<vec8_grid(n), 256, 0, s>>>(0, 0, nullptr, nullptr, (uint4*)x, (int)(n / 8), v);
+        SBK_CHECK_LAUNCH();
+        return;
+    }
     dispatch(t, [&](auto* p) {
         using T = std::remove_pointer_t<decltype(p)>;
         k_fill<T><<<grid_for(n, 256), 256, 0, s>>>((T*)x, n, v);
@@ -45,6 +111,11 @@ __global__ void k_cast(const A* x, B* y, i64 n) {
     for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) y[i] = conv<A, B>(x[i]);
 }
 void cast(const void* x, DT tx, void* y, DT ty, i64 n, cudaStream_t s) {
+    if (tx == ty) {  // same type: a device copy
+        if (n > 0 && cudaMemcpyAsync(y, x, (size_t)n * dt_bytes(tx), cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+            throw std::runtime_error("cast: device copy failed");
+        return;
+    }
     dispatch(tx, [&](auto* pa) {
         using A = std::remove_pointer_t<decltype(pa)>;
         dispatch(ty, [&](auto* pb) {
@@ -64,6 +135,11 @@ __global__ void k_binary(int op, const T* a, i64 an, const T* b, i64 bn, T* y, i
     }
 }
 void binary(int op, const void* a, i64 a_n, const void* b, i64 b_n, void* y, DT t, i64 n, cudaStream_t s) {
+    if (t == BF16 && a_n == n && b_n == n && vec8_ok(n, {a, b, y})) {
+        k_vec8<<<vec8_grid(n), 256, 0, s>>>(3, op, (const uint4*)a, (const uint4*)b, (uint4*)y, (int)(n / 8), 0.f);
+        SBK_CHECK_LAUNCH();
+        return;
+    }
     dispatch(t, [&](auto* p) {
         using T = std::remove_pointer_t<decltype(p)>;
         k_binary<T><<<grid_for(n, 256), 256, 0, s>>>(op, (const T*)a, a_n, (const T*)b, b_n, (T*)y, n);
@@ -79,6 +155,11 @@ __global__ void k_unary(int op, const T* x, T* y, i64 n, float c) {
     }
 }
 void unary(int op, const void* x, void* y, DT t, i64 n, float c, cudaStream_t s) {
+    if (t == BF16 && vec8_ok(n, {x, y})) {
+        k_vec8<<<vec8_grid(n), 256, 0, s>>>(1, op, (const uint4*)x, nullptr, (uint4*)y, (int)(n / 8), c);
+        SBK_CHECK_LAUNCH();
+        return;
+    }
     dispatch(t, [&](auto* p) {
         using T = std::remove_pointer_t<decltype(p)>;
         k_unary<T><<<grid_for(n, 256), 256, 0, s>>>(op, (const T*)x, (T*)y, n, c);
@@ -98,6 +179,11 @@ __global__ void k_unary_bwd(int op, const T* x, const T* g, T* gx, i64 n, float 
 }
 void unary_bwd(int op, const void* x, const void* g, void* gx, DT t, DT tg, i64 n, float c, cudaStream_t s) {
     (void)tg;
+    if (t == BF16 && vec8_ok(n, {x, g, gx})) {
+        k_vec8<<<vec8_grid(n), 256, 0, s>>>(2, op, (const uint4*)x, (const uint4*)g, (uint4*)gx, (int)(n / 8), c);
+        SBK_CHECK_LAUNCH();
+        return;
+    }
     dispatch(t, [&](auto* p) {
         using T = std::remove_pointer_t<decltype(p)>;
         k_unary_bwd<T><<<grid_for(n, 256), 256, 0, s>>>(op, (const T*)x, (const T*)g, (T*)gx, n, c);
