@@ -220,6 +220,7 @@ __global__ void __launch_bounds__(512, 2) k_bdrln_fwd_w(const T* partial, const 
         gmp[c] = ((const typename V::R*)gamma)[ch];
         btp[c] = ((const typename V::R*)beta)[ch];
     }
+    const float inv_n = 1.f / (float)n;
     prefetch(grp);
     for (int it = 0; grp < ngrp; grp += gstep, ++it) {
         const i64 row0 = grp * NR;
@@ -250,10 +251,15 @@ __global__ void __launch_bounds__(512, 2) k_bdrln_fwd_w(const T* partial, const 
                 for (int e = 0; e < VN; ++e) {
                     float t = v[k][c][e] + bbv[e];
                     if (thr) t = ((kb >> e) & 1) ? t * dscale : 0.f;
-                    v[k][c][e] = to_f(from_f<T>(t + rv[k][c][e]));  // `sum` rounded to the storage dtype first
-                    sm[k] += v[k][c][e];
+                    v[k][c][e] = t + rv[k][c][e];
                 }
-                ((typename V::R*)(sum + (row0 + k) * n))[ch] = V::pack(v[k][c]);
+                // `sum` rounded to the storage dtype first: pack once, and the statistics
+                // read the rounded values back from the packed vector
+                const typename V::R packed = V::pack(v[k][c]);
+                ((typename V::R*)(sum + (row0 + k) * n))[ch] = packed;
+                V::unpack(packed, v[k][c]);
+#pragma unroll
+                for (int e = 0; e < VN; ++e) sm[k] += v[k][c][e];
             }
         }
         auto row_sums = [&](float (&xx)[NR], int which) {
@@ -276,7 +282,7 @@ __global__ void __launch_bounds__(512, 2) k_bdrln_fwd_w(const T* partial, const 
         float mu[NR], q[NR];
 #pragma unroll
         for (int k = 0; k < NR; ++k) {
-            mu[k] = sm[k] / (float)n;
+            mu[k] = sm[k] * inv_n;  // (n a power of two: the same bits as / n)
             q[k] = 0.f;
 #pragma unroll
             for (int c = 0; c < CW; ++c)
@@ -295,7 +301,7 @@ __global__ void __launch_bounds__(512, 2) k_bdrln_fwd_w(const T* partial, const 
             V::unpack(btp[c], btv);
 #pragma unroll
             for (int k = 0; k < NR; ++k) {
-                const float rs = rsqrtf(q[k] / (float)n + eps);
+                const float rs = rsqrtf(q[k] * inv_n + eps);
                 float o[VN];
 #pragma unroll
                 for (int e = 0; e < VN; ++e) o[e] = gmv[e] * ((v[k][c][e] - mu[k]) * rs) + btv[e];
