@@ -293,18 +293,21 @@ constexpr int KC6 = 64;                      // keys per chunk
 constexpr int F6_KV_BYTES = KC6 * FD * 2;    // 8 KB
 constexpr int F6_NS = 2;                     // K/V stages
 constexpr int F6_THREADS = 192;
-constexpr int F6_SMEM = 1024 + F_TILE_BYTES + F6_NS * 2 * F6_KV_BYTES + 128;
+constexpr int F6_MASK_BYTES = 2048;         // keep bits of 128 query rows x 128 keys (two chunks)
+constexpr int F6_SMEM = 1024 + F_TILE_BYTES + F6_NS * 2 * F6_KV_BYTES + 2 * F6_MASK_BYTES + 160;
 constexpr float kLazy6 = 8.f;                // lazy rescale threshold (log2 units)
 
 __global__ void __launch_bounds__(F6_THREADS, 4)
     k_fa6_fwd(const __grid_constant__ CUtensorMap tQ, const __grid_constant__ CUtensorMap tK,
-              const __grid_constant__ CUtensorMap tV, FwdArgs fa, int ntiles) {
+              const __grid_constant__ CUtensorMap tV, const __grid_constant__ CUtensorMap tM, FwdArgs fa,
+              int ntiles) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024 - (tc5::smem_u32(smem_raw) & 1023)) & 1023);
     uint8_t* sQ = smem;                          // [FT][FD]
     uint8_t* sK = sQ + F_TILE_BYTES;             // [F6_NS][KC6][FD]
     uint8_t* sV = sK + F6_NS * F6_KV_BYTES;      // [F6_NS][KC6][FD]
-    uint64_t* bars = (uint64_t*)(sV + F6_NS * F6_KV_BYTES);
+    uint8_t* sMk = sV + F6_NS * F6_KV_BYTES;     // [2][128 rows][4 words]: keep bits of a chunk pair
+    uint64_t* bars = (uint64_t*)(sMk + 2 * F6_MASK_BYTES);
     uint64_t* q_full = bars;
     uint64_t* q_empty = q_full + 1;
     uint64_t* kv_full = q_empty + 1;        // [F6_NS]
@@ -313,7 +316,9 @@ __global__ void __launch_bounds__(F6_THREADS, 4)
     uint64_t* p_full = s_full + 1;
     uint64_t* o_done = p_full + 1;
     uint64_t* o_free = o_done + 1;          // epilogue has read O (4 softmax warps)
-    uint32_t* tslot = (uint32_t*)(o_free + 1);
+    uint64_t* m_full = o_free + 1;          // [2] keep bits of a chunk pair landed
+    uint64_t* m_empty = m_full + 2;         // [2] the 4 softmax warps have read them
+    uint32_t* tslot = (uint32_t*)(m_empty + 2);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int S = fa.S, nj = S / KC6, nq = S / FT;
@@ -329,6 +334,10 @@ __global__ void __launch_bounds__(F6_THREADS, 4)
         mbar_init(p_full, 4);
         mbar_init(o_done, 1);
         mbar_init(o_free, 4);
+        for (int x = 0; x < 2; ++x) {
+            mbar_init(&m_full[x], 1);
+            mbar_init(&m_empty[x], 4);
+        }
         fence_barrier_init();
     }
     if (warp == 5) tmem_alloc<128>(tslot);
@@ -340,7 +349,7 @@ __global__ void __launch_bounds__(F6_THREADS, 4)
     if (warp == 4) {
         if (lane == 0) {
             // ------------------------------------------------ TMA producer
-            int u = 0, n = 0;  // chunks / tiles loaded by this CTA
+            int u = 0, n = 0, pp = 0;  // chunks / tiles / keep-bit chunk pairs loaded by this CTA
             for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++n) {
                 const int bh = t / nq, b = bh / fa.nh, h = bh % fa.nh;
                 const int row_base = b * S;
@@ -349,6 +358,14 @@ __global__ void __launch_bounds__(F6_THREADS, 4)
                 tma_load_2d(sQ, &tQ, q_full, h * FD, row_base + (t % nq) * FT);
                 for (int j = 0; j < nj; ++j, ++u) {
                     const int s = u % F6_NS;
+                    if (fa.mask && (j & 1) == 0) {  // keep bits of chunks j, j+1 for the tile's 128 rows
+                        const int ms = pp & 1;
+                        mbar_wait(&m_empty[ms], ((pp >> 1) & 1) ^ 1);
+                        mbar_expect_tx(&m_full[ms], F6_MASK_BYTES);
+                        tma_load_2d(sMk + ms * F6_MASK_BYTES, &tM, &m_full[ms], j * (KC6 / 32),
+                                    (b * fa.nh + h) * S + (t % nq) * FT);
+                        ++pp;
+                    }
                     mbar_wait(&kv_empty[s], ((u / F6_NS) & 1) ^ 1);
                     if (fa.dbg & 8) {  // debugging: no K/V traffic
                         mbar_arrive(&kv_full[s]);
@@ -405,17 +422,22 @@ __global__ void __launch_bounds__(F6_THREADS, 4)
             const long long qi = (long long)(t % nq) * FT + row;
             const int b = (int)(bh / fa.nh), h = (int)(bh % fa.nh);
             float m_used = 0.f, l = 0.f;
-            // keep bits of this row (natural layout: S/32 words per row), one chunk ahead
-            const uint2* mrow = fa.mask ? (const uint2*)(fa.mask + (bh * S + qi) * (S / 32)) : nullptr;
-            uint2 mw_next = mrow ? __ldg(mrow) : make_uint2(~0u, ~0u);
             for (int j = 0; j < nj; ++j, ++u) {
-                const uint2 mw = mw_next;
-                if (mrow && j + 1 < nj) mw_next = __ldg(mrow + j + 1);
+                // keep bits of chunk j (chunk pair u / 2 of this CTA's walk, staged by TMA)
+                uint2 mw = make_uint2(~0u, ~0u);
+                if (fa.mask) {
+                    const int pr = u >> 1, ms = pr & 1;
+                    mbar_wait(&m_full[ms], (pr >> 1) & 1);
+                    mw = *(const uint2*)(sMk + ms * F6_MASK_BYTES + row * 16 + (j & 1) * 8);
+                }
                 mbar_wait(s_full, u & 1);
                 fence_after();
                 if (fa.dbg & 1) {
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(p_full);
+                    if (lane == 0) {
+                        mbar_arrive(p_full);
+                        if (fa.mask && (j & 1)) mbar_arrive(&m_empty[(u >> 1) & 1]);
+                    }
                     l = 1.f;
                     continue;
                 }
@@ -472,7 +494,13 @@ __global__ void __launch_bounds__(F6_THREADS, 4)
                 tmem_st_wait();
                 fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(p_full);
+                if (lane == 0) {
+                    mbar_arrive(p_full);
+                    if (fa.mask && (j & 1)) {  // this warp is done with the chunk pair's keep bits
+                        fence_proxy_async();
+                        mbar_arrive(&m_empty[(u >> 1) & 1]);
+                    }
+                }
             }
             // ------------------------------------------------ epilogue
             mbar_wait(o_done, (u - 1) & 1);
@@ -1031,9 +1059,11 @@ bool attn_fwd_sm100_try(const Attn& a, cudaStream_t s) {
         k_fa5_fwd<NT><<<grid, FCfg<NT>::THREADS, FCfg<NT>::SMEM, s>>>(tq, tk, tv, tm, fa);
     };
     if (nt_env == 6) {
-        CUtensorMap tk6, tv6;
+        CUtensorMap tk6, tv6, tm6;
         if (!make_map_bf16(&tk6, a.k, cols, rows, a.ld_k, KC6) || !make_map_bf16(&tv6, a.v, cols, rows, a.ld_v, KC6))
             return false;
+        memset(&tm6, 0, sizeof(tm6));
+        if (a.thr && !make_map_u32(&tm6, a.mask, a.S / 32, a.B * a.nh * a.S, a.S / 32, 2 * KC6 / 32, FT)) return false;
         static bool attr6 = false;
         if (!attr6) {
             cudaFuncSetAttribute(k_fa6_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, F6_SMEM);
@@ -1043,7 +1073,7 @@ bool attn_fwd_sm100_try(const Attn& a, cudaStream_t s) {
         if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
         const long long ntiles = a.B * a.nh * (a.S / FT);
         const int grid = (int)std::min<long long>(ntiles, 4ll * sms);
-        k_fa6_fwd<<<grid, F6_THREADS, F6_SMEM, s>>>(tq, tk6, tv6, fa, (int)ntiles);
+        k_fa6_fwd<<<grid, F6_THREADS, F6_SMEM, s>>>(tq, tk6, tv6, tm6, fa, (int)ntiles);
     } else if (nt_env == 2) go(std::integral_constant<int, 2>{});
     else go(std::integral_constant<int, 1>{});
     SBK_CHECK_LAUNCH();
