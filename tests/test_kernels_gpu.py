@@ -172,6 +172,38 @@ def test_gemm_2sm_vs_1sm(layout, tile_n):
     assert (outs[0][0].float() - outs[1][0].float()).abs().max().item() <= 2e-2 * outs[1][0].float().abs().max().item()
 
 
+@pytest.mark.parametrize("layout", ["tn", "tn_bias", "nn", "nt_f32", "nt_f32_acc"])
+def test_gemm_4cta_multicast(layout):
+    """K >= 4096 with an even number of 256-wide N tiles takes the 4-CTA cluster variant
+    (two CTA pairs multicasting their shared A block): against the 1-SM kernel and torch."""
+    M, N, K = 1024, 1024, 4096
+    outs = {}
+    for cap in (0, 1):
+        g = torch.Generator(device="cuda").manual_seed(5)
+        rnd = lambda *sh: torch.randn(*sh, device="cuda", generator=g)  # noqa: E731
+        if layout.startswith("tn"):
+            x, w, b = rnd(M, K).bfloat16(), rnd(N, K).bfloat16(), rnd(N).bfloat16()
+            y = torch.zeros(M, N, device="cuda", dtype=torch.bfloat16)
+            e = _gemm_engine(cap, x, (K, 1), w, (1, K), y, M, N, K, bias=b if layout == "tn_bias" else None)
+            close(y, x.float() @ w.float().T + (b.float() if layout == "tn_bias" else 0))
+            outs[cap] = y
+        elif layout == "nn":
+            gy, w = rnd(M, K).bfloat16(), rnd(K, N).bfloat16()
+            dx = torch.zeros(M, N, device="cuda", dtype=torch.bfloat16)
+            e = _gemm_engine(cap, gy, (K, 1), w, (N, 1), dx, M, N, K)
+            close(dx, gy.float() @ w.float())
+            outs[cap] = dx
+        else:
+            gy, x = rnd(K, M).bfloat16(), rnd(K, N).bfloat16()
+            base = rnd(M, N)
+            dw = base.clone() if layout.endswith("acc") else torch.zeros(M, N, device="cuda")
+            e = _gemm_engine(cap, gy, (1, M), x, (N, 1), dw, M, N, K, acc=layout.endswith("acc"))
+            close(dw, (base if layout.endswith("acc") else 0) + gy.float().T @ x.float(), 1e-2)
+            outs[cap] = dw
+        assert e == (2 if cap == 0 else 1), (layout, cap, e)
+    assert (outs[0].float() - outs[1].float()).abs().max().item() <= 2e-2 * outs[1].float().abs().max().item()
+
+
 # ------------------------------------------------------------------ attention
 L.sb_attn_fwd.argtypes = [ctypes.c_void_p] * 4 + [ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p] + \
     [ctypes.c_int64] * 4 + [ctypes.c_float, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_double, ctypes.c_int,
