@@ -616,26 +616,42 @@ static sbk::Attn mk_attn(const void* q, const void* k, const void* v, void* o, i
     a.t = kdt(dtype);
     return a;
 }
+int sb_attn_fwd_ex(const void* q, const void* k, const void* v, void* o, int64_t ld_qkv, int64_t ld_o, float* lse,
+                   int64_t B, int64_t S, int64_t nh, int64_t hd, float scale, uint64_t es, uint64_t ns, double p, int dtype,
+                   const uint32_t* keep_bits, int flags, void* stream) {
+    return guard([&] {
+        if (flags & ~SB_ATTN_CAUSAL) throw Error("sb_attn_fwd_ex: unknown flags");
+        sbk::Attn a = mk_attn(q, k, v, o, ld_qkv, ld_o, lse, B, S, nh, hd, scale, es, ns, p, dtype);
+        a.mask = keep_bits;
+        a.causal = flags & SB_ATTN_CAUSAL;
+        sbk::attn_fwd(a, (cudaStream_t)stream);
+    });
+}
 int sb_attn_fwd(const void* q, const void* k, const void* v, void* o, int64_t ld_qkv, int64_t ld_o, float* lse, int64_t B,
                 int64_t S, int64_t nh, int64_t hd, float scale, uint64_t es, uint64_t ns, double p, int dtype,
                 const uint32_t* keep_bits, void* stream) {
+    return sb_attn_fwd_ex(q, k, v, o, ld_qkv, ld_o, lse, B, S, nh, hd, scale, es, ns, p, dtype, keep_bits, 0, stream);
+}
+int sb_attn_bwd_ex(const void* q, const void* k, const void* v, const void* o, int64_t ld_qkv, int64_t ld_o,
+                   const float* lse, const void* dout, void* dq, void* dk, void* dv, void* workspace, int64_t B, int64_t S,
+                   int64_t nh, int64_t hd, float scale, uint64_t es, uint64_t ns, double p, int dtype,
+                   const uint32_t* keep_bits, int acc_mask, int flags, void* stream) {
     return guard([&] {
-        sbk::Attn a = mk_attn(q, k, v, o, ld_qkv, ld_o, lse, B, S, nh, hd, scale, es, ns, p, dtype);
+        if (flags & ~SB_ATTN_CAUSAL) throw Error("sb_attn_bwd_ex: unknown flags");
+        sbk::Attn a = mk_attn(q, k, v, (void*)o, ld_qkv, ld_o, (float*)lse, B, S, nh, hd, scale, es, ns, p, dtype);
+        a.acc_mask = acc_mask;
         a.mask = keep_bits;
-        sbk::attn_fwd(a, (cudaStream_t)stream);
+        a.mask_t = keep_bits && S % 128 == 0 ? keep_bits + (B * nh * S * S) / 32 : nullptr;
+        a.causal = flags & SB_ATTN_CAUSAL;
+        sbk::attn_bwd(a, dout, ld_o, dq, dk, dv, ld_qkv, ld_qkv, ld_qkv, workspace, (cudaStream_t)stream);
     });
 }
 int sb_attn_bwd(const void* q, const void* k, const void* v, const void* o, int64_t ld_qkv, int64_t ld_o, const float* lse,
                 const void* dout, void* dq, void* dk, void* dv, void* workspace, int64_t B, int64_t S, int64_t nh, int64_t hd,
                 float scale, uint64_t es, uint64_t ns, double p, int dtype, const uint32_t* keep_bits, int acc_mask,
                 void* stream) {
-    return guard([&] {
-        sbk::Attn a = mk_attn(q, k, v, (void*)o, ld_qkv, ld_o, (float*)lse, B, S, nh, hd, scale, es, ns, p, dtype);
-        a.acc_mask = acc_mask;
-        a.mask = keep_bits;
-        a.mask_t = keep_bits && S % 128 == 0 ? keep_bits + (B * nh * S * S) / 32 : nullptr;
-        sbk::attn_bwd(a, dout, ld_o, dq, dk, dv, ld_qkv, ld_qkv, ld_qkv, workspace, (cudaStream_t)stream);
-    });
+    return sb_attn_bwd_ex(q, k, v, o, ld_qkv, ld_o, lse, dout, dq, dk, dv, workspace, B, S, nh, hd, scale, es, ns, p, dtype,
+                          keep_bits, acc_mask, 0, stream);
 }
 
 }  // extern "C"

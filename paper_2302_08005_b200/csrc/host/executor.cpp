@@ -965,6 +965,7 @@ public:
         a.t = cdt;
         a.mask = op.dropout ? (const uint32_t*)fp(r, op.out[2]) : nullptr;
         if (a.mask && a.S % 128 == 0) a.mask_t = a.mask + (a.B * a.nh * a.S * a.S) / 32;
+        a.causal = op.causal;
         return a;
     }
 

@@ -241,7 +241,7 @@ struct Lowerer {
         cur_region = r;
         Val out;
         if (m.kind == "EfficientAttention") {
-            Module ref = attention_reference_graph(m);
+            Module ref = composed_attention(m);
             out = eval_graph(*ref.forward, ref, path, args);
         } else if (m.composite()) {
             Val f;
@@ -327,7 +327,7 @@ struct Lowerer {
         if (k == "Embedding") return embedding(m, path, args[0].one());
         if (k == "EfficientAttention") {
             if (o.fused_kernels) return flash_attention(m, path, args);
-            Module ref = attention_reference_graph(m);
+            Module ref = composed_attention(m);
             return eval_graph(*ref.forward, ref, path, args);
         }
         throw Error("no executor semantics for module kind '" + k + "'");
@@ -422,6 +422,15 @@ struct Lowerer {
         return out;
     }
 
+    // the reference's composed attention graph (no mask op exists in its op set, so a causal
+    // EfficientAttention has no composed form: it needs the flash kernel's shapes)
+    static Module composed_attention(const Module& m) {
+        if (get_flag(m.attrs, "causal"))
+            throw Error("causal EfficientAttention runs only on the fused flash-attention path "
+                        "(rank-3 q/k/v of equal shape, hidden % head_dim == 0)");
+        return attention_reference_graph(m);
+    }
+
     Val flash_attention(const Module& m, const std::string& path, const std::vector<Val>& args) {
         i64 hd = get_int(m.attrs, "head_dim").value_or(0);
         if (hd <= 0) throw Error("EfficientAttention requires a positive head_dim attr");
@@ -432,7 +441,7 @@ struct Lowerer {
         auto& sh = V(q).shape;
         if (sh.size() != 3 || V(k).shape != sh || V(v).shape != sh || sh[2] % hd != 0) {
             // shapes the kernel does not cover: the reference graph, recomputed
-            Module ref = attention_reference_graph(m);
+            Module ref = composed_attention(m);
             return eval_graph(*ref.forward, ref, path, args);
         }
         if (p >= 1.0 && o.train) throw Error("dropout p must be < 1");
@@ -454,6 +463,7 @@ struct Lowerer {
         op.hd = hd;
         op.nh = nh;
         op.scale = scale;
+        op.causal = get_flag(m.attrs, "causal");
         op.p = p;
         op.dropout = o.train && p > 0.0;
         if (op.dropout) {

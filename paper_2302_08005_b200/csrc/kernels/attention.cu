@@ -49,7 +49,9 @@ __global__ void __launch_bounds__(kT) k_attn_fwd(Attn a) {
     }
     float m = -INFINITY, l = 0.f;
     float* srow = Ss + threadIdx.x * kT;
-    for (i64 j0 = 0; j0 < a.S; j0 += kT) {
+    // causal: key tiles past this block's last query are fully masked
+    const i64 jend = a.causal ? min(a.S, (i64)(blockIdx.x + 1) * kT) : a.S;
+    for (i64 j0 = 0; j0 < jend; j0 += kT) {
         __syncthreads();
         for (int e = threadIdx.x; e < kT * HD; e += kT) {
             int jj = e / HD, d = e % HD;
@@ -65,7 +67,7 @@ __global__ void __launch_bounds__(kT) k_attn_fwd(Attn a) {
             float s = 0.f;
 #pragma unroll
             for (int d = 0; d < HD; ++d) s = fmaf(q[d], Ks[jj * HD + d], s);
-            s *= a.scale;
+            s = (a.causal && j0 + jj > i) ? -INFINITY : s * a.scale;
             srow[jj] = s;
             tmax = fmaxf(tmax, s);
         }
@@ -123,7 +125,8 @@ __global__ void __launch_bounds__(kT) k_attn_dkdv(Attn a, const T* dout, i64 ld_
         v[d] = (valid && d < hd) ? to_f(((const T*)a.v)[(b * a.S + j) * a.ld_v + h * hd + d]) : 0.f;
         gk[d] = gv[d] = 0.f;
     }
-    for (i64 i0 = 0; i0 < a.S; i0 += kT) {
+    // causal: query tiles before this key block see none of its keys
+    for (i64 i0 = a.causal ? (i64)blockIdx.x * kT : 0; i0 < a.S; i0 += kT) {
         __syncthreads();
         for (int e = threadIdx.x; e < kT * HD; e += kT) {
             int ii = e / HD, d = e % HD;
@@ -147,7 +150,7 @@ __global__ void __launch_bounds__(kT) k_attn_dkdv(Attn a, const T* dout, i64 ld_
                 s = fmaf(Qs[ii * HD + d], k[d], s);
                 dpd = fmaf(Ds[ii * HD + d], v[d], dpd);
             }
-            float p = __expf(s * a.scale - Ls[ii]);
+            float p = (a.causal && j > i0 + ii) ? 0.f : __expf(s * a.scale - Ls[ii]);
             bool keep = !a.thr || d_keep(a.s1, drop_index(b, h, a.nh, a.S, i0 + ii, j), a.thr);
             float c = a.thr ? (keep ? a.dscale : 0.f) : 1.f;
             float pd = p * c;
@@ -184,7 +187,8 @@ __global__ void __launch_bounds__(kT) k_attn_dq(Attn a, const T* dout, i64 ld_do
         gq[d] = 0.f;
     }
     float L = valid ? a.lse[(b * a.nh + h) * a.S + i] : 0.f, E = valid ? delta[(b * a.nh + h) * a.S + i] : 0.f;
-    for (i64 j0 = 0; j0 < a.S; j0 += kT) {
+    const i64 jend = a.causal ? min(a.S, (i64)(blockIdx.x + 1) * kT) : a.S;
+    for (i64 j0 = 0; j0 < jend; j0 += kT) {
         __syncthreads();
         for (int e = threadIdx.x; e < kT * HD; e += kT) {
             int jj = e / HD, d = e % HD;
@@ -203,7 +207,7 @@ __global__ void __launch_bounds__(kT) k_attn_dq(Attn a, const T* dout, i64 ld_do
                 s = fmaf(q[d], Ks[jj * HD + d], s);
                 dpd = fmaf(g[d], Vs[jj * HD + d], dpd);
             }
-            float p = __expf(s * a.scale - L);
+            float p = (a.causal && j0 + jj > i) ? 0.f : __expf(s * a.scale - L);
             bool keep = !a.thr || d_keep(a.s1, drop_index(b, h, a.nh, a.S, i, j0 + jj), a.thr);
             float c = a.thr ? (keep ? a.dscale : 0.f) : 1.f;
             float ds = p * (c * dpd - E);
@@ -245,7 +249,7 @@ size_t attn_bwd_workspace(i64 B, i64 S, i64 nh, i64 hd) {
 int attn_last_engine(int bwd) { return bwd ? g_attn_last_bwd : g_attn_last_fwd; }
 
 void attn_fwd(const Attn& a, cudaStream_t s) {
-    if (g_attn_max_engine == 0 && attn_fwd_sm100_try(a, s)) {
+    if (g_attn_max_engine == 0 && !a.causal && attn_fwd_sm100_try(a, s)) {
         g_attn_last_fwd = 3;
         return;
     }
@@ -275,7 +279,7 @@ void attn_fwd(const Attn& a, cudaStream_t s) {
 void attn_bwd(const Attn& a, const void* dout, i64 ld_do, void* dq, void* dk, void* dv, i64 ld_dq, i64 ld_dk, i64 ld_dv,
               void* ws, cudaStream_t s) {
     float* delta = (float*)ws;
-    if (g_attn_max_engine == 0 && attn_bwd_sm100_try(a, dout, ld_do, dq, dk, dv, ld_dq, ld_dk, ld_dv, ws, s)) {
+    if (g_attn_max_engine == 0 && !a.causal && attn_bwd_sm100_try(a, dout, ld_do, dq, dk, dv, ld_dq, ld_dk, ld_dv, ws, s)) {
         g_attn_last_bwd = 3;
         return;
     }

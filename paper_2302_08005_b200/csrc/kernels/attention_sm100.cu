@@ -1036,7 +1036,7 @@ size_t carve(const Attn& a, void* base, BwdWs* w) {
 }  // namespace
 
 bool attn_fwd_sm100_try(const Attn& a, cudaStream_t s) {
-    if (!fwd_fits(a)) return false;
+    if (a.causal || !fwd_fits(a)) return false;
     CUtensorMap tq, tk, tv, tm;
     const long long rows = a.B * a.S, cols = a.nh * FD;
     if (!make_map_bf16(&tq, a.q, cols, rows, a.ld_q, FT) || !make_map_bf16(&tk, a.k, cols, rows, a.ld_k, FT) ||
@@ -1095,7 +1095,7 @@ size_t attn_bwd_sm100_workspace(i64 B, i64 S, i64 nh, i64 hd) {
 
 bool attn_bwd_sm100_try(const Attn& a, const void* dout, i64 ld_do, void* dq, void* dk, void* dv, i64 ld_dq, i64 ld_dk,
                         i64 ld_dv, void* ws, cudaStream_t s) {
-    if (!bwd_fits(a, dout, ld_do, ld_dq, ld_dk, ld_dv)) return false;
+    if (a.causal || !bwd_fits(a, dout, ld_do, ld_dq, ld_dk, ld_dv)) return false;
     CUtensorMap tq, tk, tv, tdo, tm;
     const long long rows = a.B * a.S, cols = a.nh * FD;
     if (!make_map_bf16(&tq, a.q, cols, rows, a.ld_q, FT) || !make_map_bf16(&tk, a.k, cols, rows, a.ld_k, FT) ||

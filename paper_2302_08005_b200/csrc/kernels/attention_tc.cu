@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(128, 4) k_fa_fwd(Attn a, MaskRef mk) {
     float o[D / 8][4] = {};
     float m[2] = {-INFINITY, -INFINITY}, l[2] = {0.f, 0.f};
     uint32_t qa[D / 16][4];
-    const int nblk = (int)(a.S / TB);
+    const int nblk = a.causal ? (int)blockIdx.x + 1 : (int)(a.S / TB);  // causal: stop at the diagonal block
     const int g = lane >> 2, t = lane & 3;
     for (int jb = 0; jb < nblk; ++jb) {
         int st = jb & 1;
@@ -166,6 +166,13 @@ __global__ void __launch_bounds__(128, 4) k_fa_fwd(Attn a, MaskRef mk) {
         if (jb == 0) load_a_frags<D>(qa, Qs, warp * 16, lane);
         float s[TB / 8][4] = {};
         mma_abt<D, TB / 8>(s, qa, Ks + st * TB * D, lane);
+        if (a.causal && jb == (int)blockIdx.x) {  // diagonal block: key > query -> -inf (the diagonal stays)
+#pragma unroll
+            for (int n = 0; n < TB / 8; ++n)
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                    if (n * 8 + 2 * t + (e & 1) > warp * 16 + g + 8 * (e >> 1)) s[n][e] = -INFINITY;
+        }
         // online softmax (rows g and g+8 of this warp's 16)
         float mx[2] = {m[0], m[1]};
 #pragma unroll
@@ -266,7 +273,8 @@ __global__ void __launch_bounds__(128) k_fa_dkdv(Attn a, MaskRef mk, const bf16*
             Ms[st * TB + tid] = mk.bits ? row_bits(mk, bh, (long long)ib * TB + tid, k0) : ~0ull;
         }
     };
-    load_q(0, 0);
+    const int ib0 = a.causal ? (int)blockIdx.x : 0;  // causal: earlier query blocks see none of these keys
+    load_q(ib0, ib0 & 1);
     cp_commit();
     cp_wait<0>();
     __syncthreads();
@@ -277,7 +285,7 @@ __global__ void __launch_bounds__(128) k_fa_dkdv(Attn a, MaskRef mk, const bf16*
     const float sl2 = a.scale * 1.4426950408889634f;
     const int nblk = (int)(a.S / TB);
     const long long j0 = k0 + warp * 16 + g;  // this thread's key rows: j0, j0+8
-    for (int ib = 0; ib < nblk; ++ib) {
+    for (int ib = ib0; ib < nblk; ++ib) {
         int st = ib & 1;
         if (ib + 1 < nblk) {
             __syncthreads();  // stage st^1 is free (consumed two iterations ago)
@@ -299,6 +307,7 @@ __global__ void __launch_bounds__(128) k_fa_dkdv(Attn a, MaskRef mk, const bf16*
             for (int e = 0; e < 4; ++e) {
                 int qi = n * 8 + 2 * t + (e & 1);  // query within the block
                 float p = ex2(s[n][e] * sl2 - Ls[st * TB + qi]);
+                if (a.causal && ib == (int)blockIdx.x && warp * 16 + g + 8 * (e >> 1) > qi) p = 0.f;
                 float c = mk.bits ? (((Ms[st * TB + qi] >> (warp * 16 + g + 8 * (e >> 1))) & 1) ? mk.scale : 0.f) : 1.f;
                 float dsv = p * (c * dp[n][e] - Es[st * TB + qi]);
                 s[n][e] = p * c;   // dropped probabilities for dV
@@ -350,7 +359,7 @@ __global__ void __launch_bounds__(128) k_fa_dq(Attn a, MaskRef mk, const bf16* d
     const float sl2 = a.scale * 1.4426950408889634f;
     uint32_t qa[D / 16][4], da[D / 16][4];
     float gq[D / 8][4] = {};
-    const int nblk = (int)(a.S / TB);
+    const int nblk = a.causal ? (int)blockIdx.x + 1 : (int)(a.S / TB);
     for (int jb = 0; jb < nblk; ++jb) {
         int st = jb & 1;
         if (jb + 1 < nblk) {
@@ -381,6 +390,7 @@ __global__ void __launch_bounds__(128) k_fa_dq(Attn a, MaskRef mk, const bf16* d
             for (int e = 0; e < 4; ++e) {
                 int r = e >> 1;
                 float p = ex2(s[n][e] * sl2 - L2[r]);
+                if (a.causal && jb == (int)blockIdx.x && n * 8 + 2 * t + (e & 1) > warp * 16 + g + 8 * r) p = 0.f;
                 float c = mk.bits ? (((mb[r] >> (n * 8 + 2 * t + (e & 1))) & 1) ? mk.scale : 0.f) : 1.f;
                 s[n][e] = p * (c * dp[n][e] - E[r]);  // dS
             }

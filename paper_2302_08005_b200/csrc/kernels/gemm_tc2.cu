@@ -45,7 +45,13 @@ template <int BN>
 struct Cfg {
     static constexpr int B_BYTES = (BN / 2) * G_BK * 2;
     static constexpr int STAGE = G_A + B_BYTES;
-    static constexpr int ST = BN == 256 ? 6 : 8;
+#ifndef G2_ST256
+#define G2_ST256 6
+#endif
+#ifndef G2_ST128
+#define G2_ST128 8
+#endif
+    static constexpr int ST = BN == 256 ? G2_ST256 : G2_ST128;
     static constexpr int SMEM = 1024 + ST * STAGE + 8 * G_EPI_BUF + 256;
 };
 

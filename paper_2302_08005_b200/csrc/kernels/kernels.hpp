@@ -167,6 +167,8 @@ struct Attn {
     const uint32_t* mask = nullptr;    // precomputed keep bits (dropout_mask); required by the tensor-core paths
     const uint32_t* mask_t = nullptr;  // transposed keep bits (dropout_mask_dual); required by the tcgen05 backward
     int acc_mask = 7;                // backward: bit0/1/2 = dq/dk/dv accumulate (else overwrite)
+    int causal = 0;                  // key j > query i masked out before the softmax (
+                                     // not in the reference's op set): SIMT and mma.sync engines only
 };
 void attn_fwd(const Attn& a, cudaStream_t s);
 // 0 = best available (tcgen05 > mma.sync > SIMT), 1 = at most mma.sync, 2 = SIMT only
