@@ -192,8 +192,7 @@ __global__ void __cluster_dims__(2 * PAIRS, 1, 1) __launch_bounds__(320, 1)
     uint64_t* empty = full + G_ST;
     uint64_t* tfull = empty + G_ST;   // [2]
     uint64_t* tempty = tfull + 2;     // [2]
-    uint64_t* auxbar = tempty + 2;    // [8] per epilogue warp: its dGeLU pre-activation chunk landed
-    uint32_t* tslot = (uint32_t*)(auxbar + 8);
+    uint32_t* tslot = (uint32_t*)(tempty + 2);
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const uint32_t crank = cluster_rank();
     const uint32_t rank = crank & 1u, pair = crank >> 1, lead_rank = crank & ~1u;  // rank in the pair
@@ -214,7 +213,6 @@ __global__ void __cluster_dims__(2 * PAIRS, 1, 1) __launch_bounds__(320, 1)
             mbar_init(&tfull[a], 1);
             mbar_init(&tempty[a], 16);
         }
-        for (int w = 0; w < 8; ++w) mbar_init(&auxbar[w], 1);
         fence_barrier_init();
     }
     if (warp == 1) {
@@ -307,22 +305,26 @@ __global__ void __cluster_dims__(2 * PAIRS, 1, 1) __launch_bounds__(320, 1)
         const int q = warp & 3, half = (warp - 2) / 4;
         uint8_t* mybuf = epi + (warp - 2) * G_EPI_BUF;
         const uint32_t tempty0 = mapa_shared(smem_u32(&tempty[0]), lead_rank);
-        int lt = 0, nst = 0, naux = 0;
-        uint64_t* abar = &auxbar[warp - 2];
-        // dGeLU epilogue: the pre-activation chunk (32 x 32 bf16) is TMA-loaded into the
-        // upper half of the staging slot ahead of its use
-        auto aux_load = [&](int col, long long row) {
-            if (lane == 0) {
-                mbar_expect_tx(abar, 2048);
-                tma_load_2d(mybuf + 2048, &tX, abar, col, (int)row);
-            }
+        int lt = 0, nst = 0;
+        // dGeLU epilogue: each lane's 64 B of the pre-activation (its row, the chunk's 32
+        // columns) loaded straight into registers two chunks ahead — the first two of a
+        // tile are issued before the accumulator wait, so their latency hides behind it
+        // (M and N are multiples of 256: no bounds checks)
+        uint4 axa[4], axb[4];
+        auto aux_ld = [&](uint4(&w)[4], long long row, long long col) {
+            const uint4* src = (const uint4*)(ep.aux + row * ep.ldc + col);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) w[j] = __ldg(src + j);
         };
         for (int tile = cluster; tile < ntiles; tile += nclusters, ++lt) {
             const int acc = lt & 1;
             int m0, n0, z;
             tile_coords(tile, m0, n0, z);
             const long long row0 = m0 + (long long)rank * G_BM + q * 32;  // first row of this warp
-            if (ep.gelu == 2) aux_load((int)(n0 + half * 32), row0);
+            if (ep.gelu == 2) {
+                aux_ld(axa, row0 + lane, n0 + half * 32);
+                if (half + 2 < G_BN / 32) aux_ld(axb, row0 + lane, n0 + (half + 2) * 32);
+            }
             mbar_wait(&tfull[acc], (lt >> 1) & 1);
             fence_after();
 #pragma unroll 1
@@ -375,22 +377,15 @@ __global__ void __cluster_dims__(2 * PAIRS, 1, 1) __launch_bounds__(320, 1)
 #pragma unroll
                     for (int j = 0; j < 32; ++j) v[j] = gelu_fast(v[j]);
                 } else if (ep.gelu == 2) {
-                    mbar_wait(abar, naux & 1);
-                    ++naux;
-                    uint4 w[4];
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) w[j] = *(const uint4*)(mybuf + 2048 + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4));
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {
-                        const bf16* e = (const bf16*)&w[j];
+                        const bf16* e = (const bf16*)&axa[j];
 #pragma unroll
                         for (int t = 0; t < 8; ++t) v[8 * j + t] *= gelu_grad_fast(__bfloat162float(e[t]));
                     }
-                    // every lane's generic reads of the aux slot are ordered before the next
-                    // chunk's TMA (async-proxy) write into it
-                    fence_proxy_async();
-                    __syncwarp();
-                    if (c + 2 < G_BN / 32) aux_load((int)(col + 64), row0);  // next chunk of this warp
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) axa[j] = axb[j];
+                    if (c + 4 < G_BN / 32) aux_ld(axb, row, col + 128);  // this warp's chunk after next
                 }
                 if (ep.accumulate) {
                     // C += v, direct read-modify-write of this thread's row
