@@ -100,6 +100,24 @@ def test_causal_attention_kernels(cap, engine, B, S, nh, hd, p):
         assert (o[:, 0].float() - v0).abs().max().item() < 1e-2
 
 
+@pytest.mark.parametrize("S,hd", [(100, 64), (72, 32)])
+def test_causal_ragged_sequence_uses_simt(S, hd):
+    """S % 64 != 0 (or head_dim outside {64, 128}): the tensor-core engines decline and the
+    SIMT kernels take the causal call, tile edges included."""
+    B, nh, H = 2, 2, 2 * hd
+    qkv, bits = _attn_case(B, S, nh, hd, 0.0, qscale=1.0)
+    do = (torch.randn(B, S, H, device="cuda", generator=torch.Generator(device="cuda").manual_seed(4)) * 0.5).bfloat16()
+    ref, lse_ref, grads = _causal_ref(qkv, bits, B, S, nh, hd, 0.0, do)
+    o, lse, used = _fwd(qkv, bits, B, S, nh, hd, 0.0, 0)
+    assert used == 1
+    close(o, ref)
+    assert (lse - lse_ref).abs().max().item() < 2e-3 * max(1.0, lse_ref.abs().max().item())
+    g, used = _bwd(qkv, o, lse, do, bits, B, S, nh, hd, 0.0, 0)
+    assert used == 1
+    for i in range(3):
+        close(g[..., i * H:(i + 1) * H], grads[i], 3e-2)
+
+
 def test_causal_flag_is_not_a_noop_and_bad_flags_fail():
     B, S, nh, hd = 1, 128, 2, 64
     qkv, bits = _attn_case(B, S, nh, hd, 0.0)
