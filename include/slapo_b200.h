@@ -198,8 +198,9 @@ int sb_attn_bwd(const void* q, const void* k, const void* v, const void* o, int6
 /* Causal attention core (SURVEY.md §8(f) f2 — C4's decoder blocks). Not in the reference's op set
  * (shape_inference.cpp:10-16 has no mask op), so this extends sb_attn_fwd / sb_attn_bwd rather than
  * replacing a reference interface: flags & SB_ATTN_CAUSAL masks key j > query i before the softmax
- * (the keep-bit indexing of dropout is unchanged). Causal calls run on the mma.sync engine (bf16,
- * head_dim 64/128, S % 64 == 0) or the SIMT engine; other flag bits are an error. */
+ * (the keep-bit indexing of dropout is unchanged). Causal forwards run on tcgen05 where the shape
+ * fits (bf16, head_dim 64, S % 128 == 0), causal backwards on mma.sync (bf16, head_dim 64/128,
+ * S % 64 == 0), anything else on the SIMT engine; other flag bits are an error. */
 #define SB_ATTN_CAUSAL 1
 int sb_attn_fwd_ex(const void* q, const void* k, const void* v, void* o, int64_t ld_qkv, int64_t ld_o, float* lse,
                    int64_t B, int64_t S, int64_t nh, int64_t hd, float scale, uint64_t exec_seed, uint64_t node_seed,

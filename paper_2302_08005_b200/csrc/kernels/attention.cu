@@ -249,7 +249,7 @@ size_t attn_bwd_workspace(i64 B, i64 S, i64 nh, i64 hd) {
 int attn_last_engine(int bwd) { return bwd ? g_attn_last_bwd : g_attn_last_fwd; }
 
 void attn_fwd(const Attn& a, cudaStream_t s) {
-    if (g_attn_max_engine == 0 && !a.causal && attn_fwd_sm100_try(a, s)) {
+    if (g_attn_max_engine == 0 && attn_fwd_sm100_try(a, s)) {
         g_attn_last_fwd = 3;
         return;
     }

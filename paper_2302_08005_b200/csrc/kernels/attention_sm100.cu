@@ -297,6 +297,7 @@ constexpr int F6_MASK_BYTES = 2048;         // keep bits of 128 query rows x 128
 constexpr int F6_SMEM = 1024 + F_TILE_BYTES + F6_NS * 2 * F6_KV_BYTES + 2 * F6_MASK_BYTES + 160;
 constexpr float kLazy6 = 8.f;                // lazy rescale threshold (log2 units)
 
+template <bool CAUSAL>
 __global__ void __launch_bounds__(F6_THREADS, 4)
     k_fa6_fwd(const __grid_constant__ CUtensorMap tQ, const __grid_constant__ CUtensorMap tK,
               const __grid_constant__ CUtensorMap tV, const __grid_constant__ CUtensorMap tM, FwdArgs fa,
@@ -321,7 +322,12 @@ __global__ void __launch_bounds__(F6_THREADS, 4)
     uint32_t* tslot = (uint32_t*)(m_empty + 2);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    const int S = fa.S, nj = S / KC6, nq = S / FT;
+    const int S = fa.S, nj = S / KC6, nq = S / FT, nbh = ntiles / nq;
+    // causal tiles differ in length (q-tile i has i+1 128-key spans), so they are walked
+    // heaviest q-tile first — the grid-stride walk then balances instead of handing every
+    // CTA the same q-tile (gridDim % nq == 0)
+    auto tile_qt = [&](int t) { return CAUSAL ? nq - 1 - t / nbh : t % nq; };
+    auto tile_bh = [&](int t) { return CAUSAL ? t % nbh : t / nq; };
 
     if (threadIdx.x == 0) {
         mbar_init(q_full, 1);
@@ -351,19 +357,20 @@ __global__ void __launch_bounds__(F6_THREADS, 4)
             // ------------------------------------------------ TMA producer
             int u = 0, n = 0, pp = 0;  // chunks / tiles / keep-bit chunk pairs loaded by this CTA
             for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++n) {
-                const int bh = t / nq, b = bh / fa.nh, h = bh % fa.nh;
+                const int bh = tile_bh(t), b = bh / fa.nh, h = bh % fa.nh;
                 const int row_base = b * S;
                 mbar_wait(q_empty, (n & 1) ^ 1);
                 mbar_expect_tx(q_full, F_TILE_BYTES);
-                tma_load_2d(sQ, &tQ, q_full, h * FD, row_base + (t % nq) * FT);
-                for (int j = 0; j < nj; ++j, ++u) {
+                tma_load_2d(sQ, &tQ, q_full, h * FD, row_base + tile_qt(t) * FT);
+                const int njt = CAUSAL ? (tile_qt(t) + 1) * (FT / KC6) : nj;  // causal: up to the diagonal
+                for (int j = 0; j < njt; ++j, ++u) {
                     const int s = u % F6_NS;
                     if (fa.mask && (j & 1) == 0) {  // keep bits of chunks j, j+1 for the tile's 128 rows
                         const int ms = pp & 1;
                         mbar_wait(&m_empty[ms], ((pp >> 1) & 1) ^ 1);
                         mbar_expect_tx(&m_full[ms], F6_MASK_BYTES);
                         tma_load_2d(sMk + ms * F6_MASK_BYTES, &tM, &m_full[ms], j * (KC6 / 32),
-                                    (b * fa.nh + h) * S + (t % nq) * FT);
+                                    (b * fa.nh + h) * S + tile_qt(t) * FT);
                         ++pp;
                     }
                     mbar_wait(&kv_empty[s], ((u / F6_NS) & 1) ^ 1);
@@ -386,7 +393,8 @@ __global__ void __launch_bounds__(F6_THREADS, 4)
             int u = 0, n = 0;
             for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++n) {
                 mbar_wait(q_full, n & 1);
-                for (int j = 0; j < nj; ++j, ++u) {
+                const int njt = CAUSAL ? (tile_qt(t) + 1) * (FT / KC6) : nj;
+                for (int j = 0; j < njt; ++j, ++u) {
                     const int s = u % F6_NS;
                     mbar_wait(&kv_full[s], (u / F6_NS) & 1);
                     fence_after();
@@ -398,7 +406,7 @@ __global__ void __launch_bounds__(F6_THREADS, 4)
                         for (int kk = 0; kk < FD / 16; ++kk)
                             mma_ss(tmem, desc_kmajor(a, kk), desc_kmajor(bk, kk), id_s, kk > 0);
                     mma_commit(s_full);
-                    if (j == nj - 1) mma_commit(q_empty);  // last read of this tile's Q
+                    if (j == njt - 1) mma_commit(q_empty);  // last read of this tile's Q
                     if (j == 0 && n > 0) mbar_wait(o_free, (n - 1) & 1);  // previous epilogue read O
                     mbar_wait(p_full, u & 1);
                     fence_after();
@@ -418,11 +426,15 @@ __global__ void __launch_bounds__(F6_THREADS, 4)
         const uint32_t t_row = tmem + ((uint32_t)(warp * 32) << 16);
         int u = 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-            const long long bh = t / nq;
-            const long long qi = (long long)(t % nq) * FT + row;
+            const long long bh = tile_bh(t);
+            const long long qi = (long long)tile_qt(t) * FT + row;
             const int b = (int)(bh / fa.nh), h = (int)(bh % fa.nh);
             float m_used = 0.f, l = 0.f;
-            for (int j = 0; j < nj; ++j, ++u) {
+            const int njt = CAUSAL ? (tile_qt(t) + 1) * (FT / KC6) : nj;
+            for (int j = 0; j < njt; ++j, ++u) {
+                // causal: in the diagonal chunks, keys past this row's query are masked (-inf);
+                // key 0 <= every query, so chunk 0 always sets a finite running max
+                const int kmax = CAUSAL ? (int)(qi - (long long)j * KC6) : KC6;  // keys [0, kmax] of the chunk kept
                 // keep bits of chunk j (chunk pair u / 2 of this CTA's walk, staged by TMA)
                 uint2 mw = make_uint2(~0u, ~0u);
                 if (fa.mask) {
@@ -448,6 +460,11 @@ __global__ void __launch_bounds__(F6_THREADS, 4)
                     uint32_t sv[32];
                     tmem_ld32_nowait(t_row + c * 32, sv);
                     tmem_ld_wait();
+                    if (kmax < KC6 - 1) {
+#pragma unroll
+                        for (int e = 0; e < 32; ++e)
+                            if (c * 32 + e > kmax) sv[e] = __float_as_uint(-INFINITY);
+                    }
 #pragma unroll
                     for (int e = 0; e < 32; ++e) mx = fmaxf(mx, __uint_as_float(sv[e]));
                 }
@@ -479,6 +496,11 @@ __global__ void __launch_bounds__(F6_THREADS, 4)
                     uint32_t sv[32], pk[16];
                     tmem_ld32_nowait(t_row + c * 32, sv);
                     tmem_ld_wait();
+                    if (kmax < KC6 - 1) {
+#pragma unroll
+                        for (int e = 0; e < 32; ++e)
+                            if (c * 32 + e > kmax) sv[e] = __float_as_uint(-INFINITY);
+                    }
 #pragma unroll
                     for (int e = 0; e < 16; ++e) {
                         float p0 = ex2f(fmaf(__uint_as_float(sv[2 * e]), fa.c, -m_used));
@@ -1036,7 +1058,8 @@ size_t carve(const Attn& a, void* base, BwdWs* w) {
 }  // namespace
 
 bool attn_fwd_sm100_try(const Attn& a, cudaStream_t s) {
-    if (a.causal || !fwd_fits(a)) return false;
+    static int nt_env = getenv("SB_ATTN_FWD_NT") ? atoi(getenv("SB_ATTN_FWD_NT")) : 6;
+    if ((a.causal && nt_env != 6) || !fwd_fits(a)) return false;  // causal: the 64-key-chunk kernel only
     CUtensorMap tq, tk, tv, tm;
     const long long rows = a.B * a.S, cols = a.nh * FD;
     if (!make_map_bf16(&tq, a.q, cols, rows, a.ld_q, FT) || !make_map_bf16(&tk, a.k, cols, rows, a.ld_k, FT) ||
@@ -1047,7 +1070,6 @@ bool attn_fwd_sm100_try(const Attn& a, cudaStream_t s) {
     FwdArgs fa{(bf16*)a.o, a.ld_o, a.lse, a.thr ? a.mask : nullptr, a.thr ? a.dscale : 1.f,
                a.scale * 1.4426950408889634f, (int)a.S, (int)a.nh, 0};
     if (const char* e = getenv("SB_ATTN_DBG")) fa.dbg = atoi(e);
-    static int nt_env = getenv("SB_ATTN_FWD_NT") ? atoi(getenv("SB_ATTN_FWD_NT")) : 6;
     auto go = [&](auto ntc) {
         constexpr int NT = decltype(ntc)::value;
         static bool attr = false;
@@ -1066,14 +1088,16 @@ bool attn_fwd_sm100_try(const Attn& a, cudaStream_t s) {
         if (a.thr && !make_map_u32(&tm6, a.mask, a.S / 32, a.B * a.nh * a.S, a.S / 32, 2 * KC6 / 32, FT)) return false;
         static bool attr6 = false;
         if (!attr6) {
-            cudaFuncSetAttribute(k_fa6_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, F6_SMEM);
+            cudaFuncSetAttribute(k_fa6_fwd<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, F6_SMEM);
+            cudaFuncSetAttribute(k_fa6_fwd<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, F6_SMEM);
             attr6 = true;
         }
         static int sms = 0;
         if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
         const long long ntiles = a.B * a.nh * (a.S / FT);
         const int grid = (int)std::min<long long>(ntiles, 4ll * sms);
-        k_fa6_fwd<<<grid, F6_THREADS, F6_SMEM, s>>>(tq, tk6, tv6, tm6, fa, (int)ntiles);
+        if (a.causal) k_fa6_fwd<true><<<grid, F6_THREADS, F6_SMEM, s>>>(tq, tk6, tv6, tm6, fa, (int)ntiles);
+        else k_fa6_fwd<false><<<grid, F6_THREADS, F6_SMEM, s>>>(tq, tk6, tv6, tm6, fa, (int)ntiles);
     } else if (nt_env == 2) go(std::integral_constant<int, 2>{});
     else go(std::integral_constant<int, 1>{});
     SBK_CHECK_LAUNCH();

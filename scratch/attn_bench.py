@@ -35,3 +35,11 @@ for eng in (0, 1):
     tb = t(bwd)
     print(f"engine cap {eng}: used {L.sb_attn_engine(1)} bwd {tb:.3f} ms ({5*unit/tb*1e3:.0f} TF/s model)")
 L.sb_attn_set_engine(0)
+L.sb_attn_set_engine(0)
+import tests.test_causal_gpu  # noqa: F401  (sets the _ex argtypes)
+def fwdc(): L.sb_attn_fwd_ex(P(q), P(k), P(v), P(o), 3*H, H, P(lse), B, S, nh, hd, hd**-0.5, 1, 2, p, 1, P(bits), 1, None)
+for eng in (0, 1):
+    L.sb_attn_set_engine(eng)
+    tf = t(fwdc)
+    print(f"causal engine cap {eng}: used {L.sb_attn_engine(0)} fwd {tf:.3f} ms ({unit/tf*1e3:.0f} TF/s useful)")
+L.sb_attn_set_engine(0)
