@@ -294,24 +294,30 @@ constexpr int F6_KV_BYTES = KC6 * FD * 2;    // 8 KB
 constexpr int F6_NS = 2;                     // K/V stages
 constexpr int F6_THREADS = 192;
 constexpr int F6_MASK_BYTES = 2048;         // keep bits of 128 query rows x 128 keys (two chunks)
-constexpr int F6_SMEM = 1024 + F_TILE_BYTES + F6_NS * 2 * F6_KV_BYTES + 2 * F6_MASK_BYTES + 160;
+#ifndef F6_CTAS
+#define F6_CTAS 4  // resident CTAs per SM
+#endif
+#ifndef F6_QBUF
+#define F6_QBUF 1  // Q tile buffers (2: the next tile's Q loads while this tile runs)
+#endif
+constexpr int F6_SMEM = 1024 + F6_QBUF * F_TILE_BYTES + F6_NS * 2 * F6_KV_BYTES + 2 * F6_MASK_BYTES + 160;
 constexpr float kLazy6 = 8.f;                // lazy rescale threshold (log2 units)
 
 template <bool CAUSAL>
-__global__ void __launch_bounds__(F6_THREADS, 4)
+__global__ void __launch_bounds__(F6_THREADS, F6_CTAS)
     k_fa6_fwd(const __grid_constant__ CUtensorMap tQ, const __grid_constant__ CUtensorMap tK,
               const __grid_constant__ CUtensorMap tV, const __grid_constant__ CUtensorMap tM, FwdArgs fa,
               int ntiles) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024 - (tc5::smem_u32(smem_raw) & 1023)) & 1023);
-    uint8_t* sQ = smem;                          // [FT][FD]
-    uint8_t* sK = sQ + F_TILE_BYTES;             // [F6_NS][KC6][FD]
+    uint8_t* sQ = smem;                          // [F6_QBUF][FT][FD]
+    uint8_t* sK = sQ + F6_QBUF * F_TILE_BYTES;   // [F6_NS][KC6][FD]
     uint8_t* sV = sK + F6_NS * F6_KV_BYTES;      // [F6_NS][KC6][FD]
     uint8_t* sMk = sV + F6_NS * F6_KV_BYTES;     // [2][128 rows][4 words]: keep bits of a chunk pair
     uint64_t* bars = (uint64_t*)(sMk + 2 * F6_MASK_BYTES);
-    uint64_t* q_full = bars;
-    uint64_t* q_empty = q_full + 1;
-    uint64_t* kv_full = q_empty + 1;        // [F6_NS]
+    uint64_t* q_full = bars;                // [F6_QBUF]
+    uint64_t* q_empty = q_full + F6_QBUF;   // [F6_QBUF]
+    uint64_t* kv_full = q_empty + F6_QBUF;  // [F6_NS]
     uint64_t* kv_empty = kv_full + F6_NS;   // [F6_NS]
     uint64_t* s_full = kv_empty + F6_NS;
     uint64_t* p_full = s_full + 1;
@@ -330,8 +336,10 @@ __global__ void __launch_bounds__(F6_THREADS, 4)
     auto tile_bh = [&](int t) { return CAUSAL ? t % nbh : t / nq; };
 
     if (threadIdx.x == 0) {
-        mbar_init(q_full, 1);
-        mbar_init(q_empty, 1);
+        for (int x = 0; x < F6_QBUF; ++x) {
+            mbar_init(&q_full[x], 1);
+            mbar_init(&q_empty[x], 1);
+        }
         for (int s = 0; s < F6_NS; ++s) {
             mbar_init(&kv_full[s], 1);
             mbar_init(&kv_empty[s], 1);
@@ -359,9 +367,10 @@ __global__ void __launch_bounds__(F6_THREADS, 4)
             for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++n) {
                 const int bh = tile_bh(t), b = bh / fa.nh, h = bh % fa.nh;
                 const int row_base = b * S;
-                mbar_wait(q_empty, (n & 1) ^ 1);
-                mbar_expect_tx(q_full, F_TILE_BYTES);
-                tma_load_2d(sQ, &tQ, q_full, h * FD, row_base + tile_qt(t) * FT);
+                const int qb = n % F6_QBUF;
+                mbar_wait(&q_empty[qb], ((n / F6_QBUF) & 1) ^ 1);
+                mbar_expect_tx(&q_full[qb], F_TILE_BYTES);
+                tma_load_2d(sQ + qb * F_TILE_BYTES, &tQ, &q_full[qb], h * FD, row_base + tile_qt(t) * FT);
                 const int njt = CAUSAL ? (tile_qt(t) + 1) * (FT / KC6) : nj;  // causal: up to the diagonal
                 for (int j = 0; j < njt; ++j, ++u) {
                     const int s = u % F6_NS;
@@ -389,10 +398,12 @@ __global__ void __launch_bounds__(F6_THREADS, 4)
             // ------------------------------------------------ MMA issuer
             constexpr uint32_t id_s = idesc_bf16(FT, KC6, false, false);  // S = Q K^T
             constexpr uint32_t id_o = idesc_bf16(FT, FD, false, true);    // O += P V (V MN-major)
-            const uint32_t a = smem_u32(sQ);
+            const uint32_t a0 = smem_u32(sQ);
             int u = 0, n = 0;
             for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++n) {
-                mbar_wait(q_full, n & 1);
+                const int qb = n % F6_QBUF;
+                const uint32_t a = a0 + qb * F_TILE_BYTES;
+                mbar_wait(&q_full[qb], (n / F6_QBUF) & 1);
                 const int njt = CAUSAL ? (tile_qt(t) + 1) * (FT / KC6) : nj;
                 for (int j = 0; j < njt; ++j, ++u) {
                     const int s = u % F6_NS;
@@ -406,7 +417,7 @@ __global__ void __launch_bounds__(F6_THREADS, 4)
                         for (int kk = 0; kk < FD / 16; ++kk)
                             mma_ss(tmem, desc_kmajor(a, kk), desc_kmajor(bk, kk), id_s, kk > 0);
                     mma_commit(s_full);
-                    if (j == njt - 1) mma_commit(q_empty);  // last read of this tile's Q
+                    if (j == njt - 1) mma_commit(&q_empty[qb]);  // last read of this tile's Q
                     if (j == 0 && n > 0) mbar_wait(o_free, (n - 1) & 1);  // previous epilogue read O
                     mbar_wait(p_full, u & 1);
                     fence_after();
@@ -1095,7 +1106,7 @@ bool attn_fwd_sm100_try(const Attn& a, cudaStream_t s) {
         static int sms = 0;
         if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
         const long long ntiles = a.B * a.nh * (a.S / FT);
-        const int grid = (int)std::min<long long>(ntiles, 4ll * sms);
+        const int grid = (int)std::min<long long>(ntiles, (long long)F6_CTAS * sms);
         if (a.causal) k_fa6_fwd<true><<<grid, F6_THREADS, F6_SMEM, s>>>(tq, tk6, tv6, tm6, fa, (int)ntiles);
         else k_fa6_fwd<false><<<grid, F6_THREADS, F6_SMEM, s>>>(tq, tk6, tv6, tm6, fa, (int)ntiles);
     } else if (nt_env == 2) go(std::integral_constant<int, 2>{});
