@@ -59,20 +59,32 @@ class ClockSampler:
                  "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
                  "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # nvidia-smi needs a moment before its first row: wait for it (the GPU idles for
+            # at most this long), then keep only rows taken inside the timed region
+            deadline = time.time() + 5.0
+            while not self.rows and time.time() < deadline and self.proc.poll() is None:
+                time.sleep(0.01)
         except Exception:
             self.proc = None
+        self.t0 = time.time()
         return self
 
     def _read(self):
         for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+            self.rows.append((time.time(), [x.strip() for x in line.split(",")]))
 
     def __exit__(self, *a):
+        self.t1 = time.time()
         if self.proc:
+            # a short region may fall between two 100 ms rows: wait for one more row
+            n = len(self.rows)
+            deadline = time.time() + 0.5
+            while len(self.rows) == n and time.time() < deadline:
+                time.sleep(0.01)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
@@ -80,8 +92,11 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        if not self.rows:
+        inside = [r for t, r in self.rows if self.t0 <= t <= self.t1]
+        rows = inside or [r for t, r in self.rows if t > self.t1][:1]  # the row right after a short region
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        self.rows = rows
         sm = sorted(float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit())
         mx = max(float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit())
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
