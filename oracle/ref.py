@@ -9,6 +9,7 @@ from __future__ import annotations
 
 import json
 import os
+import shutil
 import struct
 import subprocess
 import tempfile
@@ -49,9 +50,29 @@ def read_dump(path: str) -> Dict[str, np.ndarray]:
 
 
 class RefRun:
-    def __init__(self, outdir: str, meta: dict):
+    """Dumps of one oracle run. A temporary dump directory (no `outdir` given to
+    `run`) is owned by this object and removed with it (`close()` / GC / `with`):
+    full-width runs dump hundreds of MB (the embedding gradient alone is 250 MB at
+    BERT-large width), so nothing may accumulate under /tmp."""
+
+    def __init__(self, outdir: str, meta: dict, owned: bool = False):
         self.dir = outdir
         self.meta = meta
+        self._owned = owned
+
+    def close(self):
+        if self._owned and self.dir and os.path.isdir(self.dir):
+            shutil.rmtree(self.dir, ignore_errors=True)
+        self._owned = False
+
+    def __del__(self):
+        self.close()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
 
     def outputs(self, rank: int = 0):
         d = read_dump(os.path.join(self.dir, "outputs.bin"))
@@ -87,6 +108,7 @@ def run(model: str = "toy_bert", schedule: Optional[str] = None, outdir: Optiona
     backward, dump_params, tp_hidden, tp_inner, tp_batch, repeat, model_json (path)."""
     if not available():
         raise RuntimeError(f"oracle driver missing: build it with `make -C oracle` ({DRIVER})")
+    owned = outdir is None
     outdir = outdir or tempfile.mkdtemp(prefix="sbref_")
     args = [DRIVER, "--model", model, "--out", outdir]
     sched_file = None
@@ -100,16 +122,45 @@ def run(model: str = "toy_bert", schedule: Optional[str] = None, outdir: Optiona
         args += ["--schedule", sched_file]
     for k, v in kw.items():
         args += ["--" + k, str(v)]
+    try:
+        r = subprocess.run(args, capture_output=True, text=True, timeout=timeout)
+        if r.returncode != 0:
+            raise RuntimeError(f"oracle failed ({r.returncode}): {r.stderr.strip()}")
+        meta = json.loads(r.stdout.strip().splitlines()[-1])
+    except BaseException:
+        if owned:
+            shutil.rmtree(outdir, ignore_errors=True)
+        raise
+    return RefRun(outdir, meta, owned)
+
+
+def time_step(model: str = "toy_bert", schedule: Optional[str] = None, timeout: int = 3600, cpu: Optional[int] = None,
+              **kw) -> dict:
+    """One forward()+backward_all_ranks() of the reference executor WITHOUT any dump
+    (no --out: the driver writes nothing, ref_driver.cpp:289), optionally pinned to
+    host core `cpu` (the reference is single-threaded). Returns the driver's meta
+    line (fwd_s, bwd_s, collectives, ledger)."""
+    if not available():
+        raise RuntimeError(f"oracle driver missing: build it with `make -C oracle` ({DRIVER})")
+    args = [DRIVER, "--model", model]
+    if schedule:
+        if not os.path.exists(schedule):
+            raise ValueError("time_step takes a schedule file path")
+        args += ["--schedule", schedule]
+    for k, v in kw.items():
+        args += ["--" + k, str(v)]
+    if cpu is not None and shutil.which("taskset"):
+        args = ["taskset", "-c", str(cpu)] + args
     r = subprocess.run(args, capture_output=True, text=True, timeout=timeout)
     if r.returncode != 0:
         raise RuntimeError(f"oracle failed ({r.returncode}): {r.stderr.strip()}")
-    meta = json.loads(r.stdout.strip().splitlines()[-1])
-    return RefRun(outdir, meta)
+    return json.loads(r.stdout.strip().splitlines()[-1])
 
 
 def uniform01_probe(stream_seed: int, n: int) -> np.ndarray:
-    outdir = tempfile.mkdtemp(prefix="sbrng_")
-    r = subprocess.run([DRIVER, "--probe_rng", f"{stream_seed},{n}", "--out", outdir], capture_output=True, text=True)
-    if r.returncode != 0:
-        raise RuntimeError(r.stderr)
-    return read_dump(os.path.join(outdir, "rng.bin"))["uniform01"]
+    with tempfile.TemporaryDirectory(prefix="sbrng_") as outdir:
+        r = subprocess.run([DRIVER, "--probe_rng", f"{stream_seed},{n}", "--out", outdir], capture_output=True,
+                           text=True)
+        if r.returncode != 0:
+            raise RuntimeError(r.stderr)
+        return read_dump(os.path.join(outdir, "rng.bin"))["uniform01"]

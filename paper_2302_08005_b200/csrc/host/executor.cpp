@@ -759,7 +759,6 @@ public:
                     std::vector<char*> b;
                     for (auto& r : ranks) b.push_back(fp(r, r.P.fwd[(size_t)i].out[1]));
                     all_reduce(b, b, cdt, V(ranks[0], op0.out[1]).numel());
-                } else if (op0.allreduce == false && op0.k == K::FusedLinearResLN && false) {
                 }
                 for (auto& r : ranks) fused_res_ln_tail(r, r.P.fwd[(size_t)i]);
                 break;

@@ -1,0 +1,133 @@
+"""X1: parity at the benchmarked configuration (BASELINE.json configs[2], C3).
+
+The scheduled BERT-large recipe — FusedQKV, shard+sync, EfficientAttention, the
+all_reduce-including fusions, vocab-parallel embeddings, checkpoint — at full
+BERT-large width (H 1024, 16 heads, hd 64, F 4096, S 512, V 30528) in bf16 on
+the sm_100a kernels (2-SM tcgen05 GEMM, tcgen05 flash attention at S=512,
+vectorised fused LayerNorm, vocab-parallel embedding), against the reference
+executor itself (oracle/_ref/slapo_ref_driver: the reference's proj/src compiled
+by oracle/Makefile, f64) on the same seeds, inputs and schedule script.
+Reference entry points: Executor::forward + backward_all_ranks
+(proj/src/executor.cpp:285-381), run under run_sharded semantics for TP=2.
+
+Depth is what the CPU reference can afford (L <= 2 at this
+width, ~70 s per layer-step on one core); B=1 so the CPU runs finish in minutes.
+All reference runs of this module start together in a module fixture (one
+process per run, each single-threaded) and overlap each other.
+
+Checked per rank: every output, the loss (sum of outputs, executor.cpp:355-362)
+and every parameter gradient. Metric: relL2 per tensor (the
+analytically-zero key-bias gradient normalised by its QKV-bias group). The
+measured errors are written to $SB_PARITY_OUT (committed as
+profiles/r2_bf16_parity.json) and the tolerances below are derived from them
+(DESIGN.md §2).
+"""
+import json
+import os
+import subprocess
+import tempfile
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+import pytest
+
+import paper_2302_08005_b200 as sb
+from paper_2302_08005_b200 import recipes
+from oracle import ref
+from tests.helpers import BF16_GRAD_TOL, BF16_LOSS_TOL, BF16_OUT_TOL, group_scale, rel_err, rel_l2
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not ref.available(), reason="oracle not built")]
+
+C3W = dict(hidden=1024, heads=16, vocab=30528, batch=1, seq=512, p=0.1)
+# (layers, world, mode, checkpoint ratio)
+CASES = [(1, 1, "train", 1.0), (1, 2, "train", 1.0), (1, 1, "verify", 0.0), (1, 2, "verify", 0.0),
+         (2, 1, "train", 0.5), (2, 2, "train", 0.5), (2, 1, "verify", 0.0), (2, 2, "verify", 0.0)]
+
+
+
+def _name(c):
+    L, world, mode, ck = c
+    return f"L{L}_tp{world}_{mode}"
+
+
+def _script(c):
+    L, world, _, ck = c
+    return recipes.tp_script(L, world, ckpt_ratio=ck)
+
+
+@pytest.fixture(scope="module")
+def ref_runs():
+    tmp = tempfile.TemporaryDirectory(prefix="sb_c3ref_")
+
+    def one(c):
+        L, world, mode, _ = c
+        d = os.path.join(tmp.name, _name(c))
+        os.makedirs(d)
+        return _name(c), ref.run("toy_bert", schedule=_script(c), outdir=d, layers=L, world=world, mode=mode,
+                                 seed=123, input_seed=9, timeout=3000, **C3W)
+
+    with ThreadPoolExecutor(len(CASES)) as pool:
+        runs = dict(pool.map(one, CASES))
+    yield runs
+    tmp.cleanup()
+
+
+def _record(name, rec):
+    out = os.environ.get("SB_PARITY_OUT")
+    if not out:
+        return
+    os.makedirs(out, exist_ok=True)
+    with open(os.path.join(out, f"c3_{name}.json"), "w") as f:
+        json.dump(rec, f, indent=1, sort_keys=True)
+
+
+@pytest.mark.parametrize("case", CASES, ids=_name)
+def test_c3_width_bf16_vs_reference(case, ref_runs):
+    L, world, mode, _ = case
+    r = ref_runs[_name(case)]
+    m = sb.toy_bert(L, C3W["hidden"], C3W["heads"], C3W["vocab"], C3W["batch"], C3W["seq"], C3W["p"])
+    s = sb.create_schedule(m, world)
+    s.load_script(_script(case))
+    ex = sb.Executor(s.apply(), mode, 123, world, dtype="bf16")
+    ex.forward(m.random_inputs(9))
+    engines = dict(gemm=sb.lib().sb_gemm_engine(), attn_fwd=sb.lib().sb_attn_engine(0))
+    grads = ex.backward_all_ranks()
+    engines["attn_bwd"] = sb.lib().sb_attn_engine(1)
+    assert engines == dict(gemm=2, attn_fwd=3, attn_bwd=3), engines
+    assert ex.collective_invocations() == r.meta["collectives_total"]
+
+    rec = {"case": _name(case), "layers": L, "world": world, "mode": mode, **C3W, "ranks": []}
+    worst_out = worst_loss = 0.0
+    worst_grad = (0.0, None)
+    for rank in range(world):
+        outs = ex.outputs_of_rank(rank)
+        want = r.outputs(rank)
+        assert len(outs) == len(want)
+        e_out = max(rel_l2(g, w) for g, w in zip(outs, want))
+        e_out_inf = max(rel_err(g, w) for g, w in zip(outs, want))
+        loss_g = sum(float(np.asarray(o, dtype=np.float64).sum()) for o in outs)
+        loss_w = sum(float(w.sum()) for w in want)
+        e_loss = abs(loss_g - loss_w) / abs(loss_w)
+        gw = r.grads(rank)
+        got = grads[rank].params
+        assert set(got) == set(gw), sorted(set(got) ^ set(gw))
+        per = {}
+        for k, w in gw.items():
+            gs = group_scale(k, gw)
+            if gs is not None:
+                e = float(np.abs(np.asarray(got[k]).ravel() - np.asarray(w).ravel()).max() / gs)
+            else:
+                e = rel_l2(got[k], w)
+            per[k] = e
+            if e > worst_grad[0]:
+                worst_grad = (e, f"r{rank}:{k}")
+        rec["ranks"].append({"rank": rank, "out_rel_l2": e_out, "out_rel_inf": e_out_inf, "loss": loss_g,
+                             "loss_ref": loss_w, "loss_rel": e_loss, "grad_rel_l2": per})
+        worst_out = max(worst_out, e_out)
+        worst_loss = max(worst_loss, e_loss)
+    rec.update(worst_out=worst_out, worst_loss=worst_loss, worst_grad=worst_grad[0], worst_grad_name=worst_grad[1],
+               engines=engines)
+    _record(_name(case), rec)
+    assert worst_out <= BF16_OUT_TOL, f"output relL2 {worst_out:.3e}"
+    assert worst_loss <= BF16_LOSS_TOL, f"loss rel {worst_loss:.3e}"
+    assert worst_grad[0] <= BF16_GRAD_TOL, f"gradient {worst_grad[1]}: {worst_grad[0]:.3e}"
