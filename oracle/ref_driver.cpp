@@ -95,7 +95,8 @@ int main(int argc, char** argv) {
         {"backward", "1"}, {"dump_params", "0"}, {"probe_rng", ""}, {"model_json", ""},
         {"tp_hidden", "8"}, {"tp_inner", "16"}, {"tp_batch", "4"}, {"repeat", "1"}, {"cli_run", ""},
         {"estimate", ""}, {"est_batch", "0"}, {"est_mem", "17179869184"}, {"est_consts", ""}, {"ckpt_container", ""},
-        {"ckpt_ratio", "0"}, {"tune", ""}, {"tune_seed", "0"}, {"tune_restarts", "3"}, {"micro", "1"}};
+        {"ckpt_ratio", "0"}, {"tune", ""}, {"tune_seed", "0"}, {"tune_restarts", "3"}, {"micro", "1"},
+        {"cli_train", ""}};
     for (int i = 1; i + 1 < argc; i += 2) {
         std::string k = argv[i];
         if (k.rfind("--", 0) != 0) { std::cerr << "bad arg " << k << "\n"; return 2; }
@@ -249,6 +250,35 @@ int main(int argc, char** argv) {
             else outs = run_forward(res.model, ins, mode, derive_seed(seed, "run"));
             write_tensor_dump(a["cli_run"], outs);
             for (const auto& t : outs) std::cout << format_tensor_text(t) << "\n";
+            return 0;
+        }
+        if (!a["cli_train"].empty()) {
+            // the training-step reference for the B200 verifier's gradient mode
+            // (paper_2302_08005_b200/cli.py verify-train): `slapo run`'s inputs and seeds
+            // (slapo_main.cpp:69-82,168-199) through Executor::forward + backward_all_ranks
+            // (executor.cpp:285-381); per rank the outputs and every parameter gradient as
+            // the reference's SLD1 tensor dumps (dump.cpp:29) plus the gradient names.
+            auto specs = declared_input_specs(*model.forward);
+            std::vector<TensorValue> ins;
+            for (std::size_t i = 0; i < specs.size(); ++i)
+                ins.push_back(random_tensor(specs[i], derive_seed(seed, "cli-input"), static_cast<std::uint64_t>(i)));
+            const ModuleDef& target = a["schedule"].empty() ? model : res.model;
+            const int w = a["schedule"].empty() ? 1 : world;
+            Executor ex(target, mode, derive_seed(seed, "run"), w);
+            ex.forward(ins);
+            auto gm = ex.backward_all_ranks();
+            const std::string dir = a["cli_train"];
+            for (int r = 0; r < w; ++r) {
+                write_tensor_dump(dir + "/outputs.r" + std::to_string(r) + ".sld1", ex.outputs_of_rank(r));
+                std::vector<TensorValue> gs;
+                std::ofstream names(dir + "/grads.r" + std::to_string(r) + ".names");
+                for (auto& [k, v] : gm[(std::size_t)r].params) {
+                    gs.push_back(v);
+                    names << k << "\n";
+                }
+                write_tensor_dump(dir + "/grads.r" + std::to_string(r) + ".sld1", gs);
+            }
+            std::cout << "{\"world\": " << w << "}" << std::endl;
             return 0;
         }
         auto specs = declared_input_specs(*model.forward);

@@ -20,6 +20,7 @@ from __future__ import annotations
 import ctypes
 import json
 import os
+import sys
 from dataclasses import dataclass, field
 from typing import Dict, List, Optional, Sequence
 
@@ -396,6 +397,7 @@ class Executor:
             _check(_lib.sb_executor_create(model._h, train, seed, world, dt, int(fused), _c.byref(h)))
         else:
             rank, uid = nccl
+            _pin_nccl()
             ub = _c.create_string_buffer(bytes(uid), 128)
             _check(_lib.sb_executor_create_nccl(model._h, train, seed, world, rank, ub, dt, int(fused), _c.byref(h)))
             self.nccl_rank = rank
@@ -552,7 +554,25 @@ def plan_summary(model: Model, mode: str = "train", seed: int = 0, world: int = 
     return json.loads(buf.value.decode())
 
 
+def _pin_nccl() -> None:
+    """One NCCL per process: when torch (torch.distributed) is in this process, make
+    the executor dlopen the NCCL torch ships (nvidia/nccl/lib) instead of whatever
+    libnccl.so.2 the loader would find first (the system copy may be another version)."""
+    if os.environ.get("SB_NCCL_LIB") or "torch" not in sys.modules:
+        return
+    try:
+        import nvidia.nccl  # noqa: F401  (the wheel torch's libtorch_cuda links against)
+        for d in nvidia.nccl.__path__:
+            p = os.path.join(d, "lib", "libnccl.so.2")
+            if os.path.exists(p):
+                os.environ["SB_NCCL_LIB"] = p
+                return
+    except ImportError:
+        pass
+
+
 def nccl_unique_id() -> bytes:
+    _pin_nccl()
     buf = _c.create_string_buffer(128)
     _check(_lib.sb_nccl_unique_id(buf))
     return buf.raw

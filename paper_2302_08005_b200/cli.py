@@ -9,6 +9,8 @@ dumps (e.g. one written by the reference's `slapo run --dump`).
                                             [--mode verify|train] [--dump OUT.sld] [--dtype fp32|bf16]
     python -m paper_2302_08005_b200 verify  MODEL.json SCRIPT [--world-size N] [--seed S]
                                             [--trials T] [--atol A] [--rtol R]
+    python -m paper_2302_08005_b200 verify-train MODEL.json [SCRIPT] --reference DIR [--world-size N] [--seed S]
+                                            [--mode train|verify] [--dtype fp32|bf16] [--tol-out/--tol-loss/--tol-grad X]
     python -m paper_2302_08005_b200 estimate MODEL.json [SCRIPT] [--world-size N] [--batch B] [--b200]
     python -m paper_2302_08005_b200 diff    A.sld B.sld [--atol A] [--rtol R]
 
@@ -241,6 +243,79 @@ def cmd_verify(a) -> int:
     return EXIT_OK if ok else EXIT_NUMERIC
 
 
+def grad_error(name: str, got: np.ndarray, want: np.ndarray, grads: dict) -> float:
+    """Per-tensor normalised max error ||a-b||_inf / ||b||_inf (SURVEY.md Appendix A.5:
+    the verifier's elementwise max_rel breaks on gradients). An analytically-zero
+    gradient (the key-bias of a softmax attention: shift invariance) is normalised by
+    its layer's query-bias gradient instead of by its own round-off-sized norm."""
+    got = np.asarray(got, dtype=np.float64).ravel()
+    want = np.asarray(want, dtype=np.float64).ravel()
+    if got.shape != want.shape:
+        raise ValueError(f"gradient {name}: {got.size} vs {want.size} elements")
+    scale = float(np.abs(want).max(initial=0.0))
+    if name.endswith("key.bias"):
+        q = grads.get(name[: -len("key.bias")] + "query.bias")
+        if q is not None:
+            scale = float(np.abs(np.asarray(q)).max(initial=0.0))
+    return float(np.abs(got - want).max(initial=0.0)) / max(scale, 1e-30)
+
+
+def cmd_verify_train(a) -> int:
+    """The random-input verifier extended to one training step (SURVEY.md §2 item 12;
+    verify_end_to_end, proj/src/verifier.cpp:169-205, compares forward outputs only):
+    the scheduled model runs forward + backward_all_ranks on the GPU with `slapo run`'s
+    inputs and seeds (slapo_main.cpp:69-82: inputs random_tensor(spec_i,
+    derive_seed(seed, "cli-input"), i), executor seed derive_seed(seed, "run")), and
+    every rank's outputs, loss (sum of outputs, executor.cpp:355-362) and parameter
+    gradients are checked against the reference executor's dump of the same step
+    (--reference DIR: outputs.r<R>.sld1, grads.r<R>.sld1 + grads.r<R>.names, SLD1
+    tensor dumps written by the reference's write_tensor_dump, dump.cpp:29).
+    Metrics: per-tensor ||a-b||_inf/||b||_inf for outputs and gradients (Appendix A.5),
+    |loss - loss_ref| / |loss_ref| for the loss."""
+    import os
+    from . import Executor
+    model = _load_model(a.model)
+    target = _apply(model, a.script, a.world_size) if a.script else model
+    world = a.world_size if a.script else 1
+    inputs = cli_inputs(model, a.seed)
+    ex = Executor(target, mode=a.mode, seed=derive_seed(a.seed, "run"), world=world, dtype=a.dtype)
+    ex.forward(inputs)
+    gm = ex.backward_all_ranks()
+    worst_out = worst_loss = worst_grad = 0.0
+    worst_name = ""
+    n_grads = 0
+    for r in range(world):
+        want = [t for t, _ in _dump.read_tensor_dump(os.path.join(a.reference, "outputs.r%d.sld1" % r))]
+        got = ex.outputs_of_rank(r)
+        if len(want) != len(got):
+            raise ValueError("rank %d: %d outputs vs %d in the reference dump" % (r, len(got), len(want)))
+        for g, w in zip(got, want):
+            worst_out = max(worst_out, grad_error("", g, w, {}))
+        lg = sum(float(np.asarray(o, dtype=np.float64).sum()) for o in got)
+        lw = sum(float(np.asarray(w, dtype=np.float64).sum()) for w in want)
+        worst_loss = max(worst_loss, abs(lg - lw) / max(abs(lw), 1e-30))
+        names = _read(os.path.join(a.reference, "grads.r%d.names" % r)).split()
+        gw = [t for t, _ in _dump.read_tensor_dump(os.path.join(a.reference, "grads.r%d.sld1" % r))]
+        if len(names) != len(gw):
+            raise ValueError("rank %d: %d gradient names for %d tensors" % (r, len(names), len(gw)))
+        want_g = dict(zip(names, gw))
+        got_g = gm[r].params
+        if set(want_g) != set(got_g):
+            raise ValueError("rank %d: gradient sets differ: %s" % (r, sorted(set(want_g) ^ set(got_g))))
+        for k, w in want_g.items():
+            e = grad_error(k, got_g[k], w, want_g)
+            n_grads += 1
+            if e > worst_grad:
+                worst_grad, worst_name = e, "r%d:%s" % (r, k)
+    ok = worst_out <= a.tol_out and worst_loss <= a.tol_loss and worst_grad <= a.tol_grad
+    g = lambda v: "%g" % v  # noqa: E731 - ostream default formatting
+    print("ranks         %d\noutputs_err   %s\nloss_rel_err  %s\ngradients     %d\nworst_grad    %s %s\n"
+          "tol_out       %s\ntol_loss      %s\ntol_grad      %s\npass          %s\n" %
+          (world, g(worst_out), g(worst_loss), n_grads, g(worst_grad), worst_name or "-", g(a.tol_out),
+           g(a.tol_loss), g(a.tol_grad), "true" if ok else "false"), end="")
+    return EXIT_OK if ok else EXIT_NUMERIC
+
+
 def cmd_diff(a) -> int:
     ra = [t for t, _ in _dump.read_tensor_dump(a.a)]
     rb = [t for t, _ in _dump.read_tensor_dump(a.b)]
@@ -279,6 +354,18 @@ def main(argv: Optional[List[str]] = None) -> int:
     q.add_argument("--atol", type=float, default=1e-4)
     q.add_argument("--rtol", type=float, default=1e-3)
     q.add_argument("--dtype", choices=["fp32", "bf16"], default="fp32")
+    q = sp.add_parser("verify-train")
+    q.add_argument("model")
+    q.add_argument("script", nargs="?", default="")
+    q.add_argument("--reference", required=True, help="directory with the reference's per-rank SLD1 dumps")
+    q.add_argument("--world-size", type=int, default=1)
+    q.add_argument("--seed", type=int, default=0)
+    q.add_argument("--mode", choices=["verify", "train"], default="train")
+    q.add_argument("--dtype", choices=["fp32", "bf16"], default="fp32")
+    # defaults: the north star's fp32 bar; bf16 runs pass the stated bf16 tolerances
+    q.add_argument("--tol-out", type=float, default=1e-4)
+    q.add_argument("--tol-loss", type=float, default=1e-4)
+    q.add_argument("--tol-grad", type=float, default=1e-4)
     q = sp.add_parser("estimate")
     q.add_argument("model")
     q.add_argument("script", nargs="?", default="")
@@ -296,7 +383,7 @@ def main(argv: Optional[List[str]] = None) -> int:
         return EXIT_USAGE if e.code else EXIT_OK
     try:
         return {"inspect": cmd_inspect, "apply": cmd_apply, "run": cmd_run, "verify": cmd_verify,
-                "estimate": cmd_estimate, "diff": cmd_diff}[a.cmd](a)
+                "verify-train": cmd_verify_train, "estimate": cmd_estimate, "diff": cmd_diff}[a.cmd](a)
     except SystemExit:
         raise
     except Exception as e:  # noqa: BLE001 - the CLI's internal-error exit

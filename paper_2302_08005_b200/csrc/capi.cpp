@@ -302,7 +302,7 @@ int sb_executor_create(const sb_model* m, int train, uint64_t seed, int world, i
 }
 int sb_nccl_unique_id(void* out128) {
     return guard([&] {
-        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        void* h = sb::nccl_handle();
         if (!h) throw Error("NCCL not available");
         auto f = (ncclResult_t(*)(ncclUniqueId*))dlsym(h, "ncclGetUniqueId");
         ncclUniqueId id;

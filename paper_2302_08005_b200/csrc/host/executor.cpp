@@ -24,6 +24,20 @@ namespace sb {
     } while (0)
 
 // ------------------------------------------------------------------ NCCL (dlopen)
+// One NCCL per process: $SB_NCCL_LIB when set (the Python layer points it at the
+// NCCL torch.distributed already loaded), else whatever libnccl.so.2 is already
+// mapped (RTLD_NOLOAD), else the loader's libnccl.so.2.
+void* nccl_handle() {
+    static void* h = [] {
+        void* p = nullptr;
+        if (const char* e = getenv("SB_NCCL_LIB"); e && *e) p = dlopen(e, RTLD_NOW | RTLD_GLOBAL);
+        if (!p) p = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+        if (!p) p = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!p) p = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        return p;
+    }();
+    return h;
+}
 namespace {
 struct Nccl {
     void* h = nullptr;
@@ -34,10 +48,7 @@ struct Nccl {
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
     void load() {
         if (h) return;
-        for (const char* n : {"libnccl.so.2", "libnccl.so"}) {
-            h = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
-            if (h) break;
-        }
+        h = nccl_handle();
         if (!h) throw Error("NCCL not available: dlopen(libnccl.so.2) failed");
         CommInitRank = (decltype(CommInitRank))dlsym(h, "ncclCommInitRank");
         AllReduce = (decltype(AllReduce))dlsym(h, "ncclAllReduce");
@@ -117,6 +128,7 @@ public:
             lo.seed = seed;
             lo.cdt = cdt;
             lo.fused_kernels = fused;
+            lo.keep_collectives = comm.nccl;
             ranks[(size_t)i].P = lower(root, lo);
             if (i > 0 && ranks[(size_t)i].P.structure() != ranks[0].P.structure())
                 throw Error("per-rank plans differ structurally; lockstep execution impossible");
@@ -126,7 +138,7 @@ public:
         for (auto& r : ranks) allocate(r);
         init_mask_stream();
         init_early_allreduce();
-        if (comm.nccl && world > 1) {
+        if (comm.nccl) {
             nccl().load();
             ncclUniqueId id;
             if (comm.unique_id.size() != sizeof(id)) throw Error("nccl unique id must be 128 bytes");
@@ -143,6 +155,7 @@ public:
         for (auto& r : ranks)
             if (r.base) cudaFree(r.base);
         if (nan_flag) cudaFree(nan_flag);
+        if (nan_counts) cudaFree(nan_counts);
         if (ncomm && nccl().CommDestroy) nccl().CommDestroy(ncomm);
         for (auto e : mask_ev)
             if (e) cudaEventDestroy(e);
@@ -152,6 +165,8 @@ public:
             if (e) cudaEventDestroy(e);
         for (auto e : dgrad_ev)
             if (e) cudaEventDestroy(e);
+        for (auto e : far_gemm) cudaEventDestroy(e);
+        for (auto e : far_done) cudaEventDestroy(e);
         if (cstream) cudaStreamDestroy(cstream);
         if (fork_ev) cudaEventDestroy(fork_ev);
         if (mstream) cudaStreamDestroy(mstream);
@@ -631,7 +646,7 @@ public:
     void init_early_allreduce() {
         const Plan& P = ranks[0].P;
         early_ar.assign(P.fwd.size(), -1);
-        if (world <= 1) return;
+        if (world <= 1 && !comm.nccl) return;
         std::vector<int> pos(P.fwd.size(), -1);
         for (size_t k = 0; k < bsteps.size(); ++k)
             if (bsteps[k].kind == 0) pos[(size_t)bsteps[k].idx] = (int)k;
@@ -671,7 +686,7 @@ public:
                 CK(cudaEventCreateWithFlags(&ar_ev[(size_t)early_ar[k]], cudaEventDisableTiming));
                 any = true;
             }
-        if (any) {
+        if (any || world > 1 || comm.nccl) {
             int lo, hi;
             CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
             CK(cudaStreamCreateWithPriority(&cstream, cudaStreamNonBlocking, hi));  // communication first
@@ -706,6 +721,7 @@ public:
         all_reduce(b, b, cdt, V(ranks[0], ranks[0].P.fwd[(size_t)sidx].out[0]).numel(), cstream);
         CK(cudaEventRecord(ar_ev[(size_t)sidx], cstream));
         ar_pending[(size_t)sidx] = 1;
+        CommSmReserve keep_sms(*this);
         for (size_t k = 0; k < ranks.size(); ++k) linear_bwd(ranks[k], ranks[k].P.fwd[(size_t)i], g[k].first, g[k].second, 2);
     }
 
@@ -753,6 +769,10 @@ public:
                 break;
             }
             case K::FusedLinearResLN:
+                if (op0.allreduce && fwd_ar_chunks(ranks[0], op0) > 1) {
+                    fused_res_ln_overlapped(i, fwd_ar_chunks(ranks[0], op0));
+                    break;
+                }
                 for (auto& r : ranks) fused_res_ln_gemm(r, r.P.fwd[(size_t)i]);
                 if (op0.allreduce) {
                     ++collectives;
@@ -769,18 +789,121 @@ public:
         if (nan_guard) check_nan(i);
     }
 
+    // NaN guard (Executor::set_nan_guard, reference executor.cpp:308-316,845: the NaN check after
+    // every forward op): each op's outputs are counted into a per-op device counter
+    // (no host sync, so it also runs inside a captured graph); the counters are read
+    // once after the forward (eager) or after the graph replay, and the first op that
+    // produced a NaN is reported.
+    int* nan_counts = nullptr;
+    size_t nan_n = 0;
+    void nan_alloc() {  // (not inside a graph capture: set_nan_guard)
+        const size_t n = ranks[0].P.fwd.size() * ranks.size();
+        if (nan_n < n) {
+            if (nan_counts) cudaFree(nan_counts);
+            CK(cudaMalloc(&nan_counts, n * sizeof(int)));
+            nan_n = n;
+        }
+    }
+    void nan_reset() { CK(cudaMemsetAsync(nan_counts, 0, nan_n * sizeof(int), stream)); }
     void check_nan(int i) {
-        for (auto& r : ranks) {
+        for (size_t k = 0; k < ranks.size(); ++k) {
+            RankCtx& r = ranks[k];
             const Op& op = r.P.fwd[(size_t)i];
+            if (op.k == K::Cast) continue;  // input / dtype conversions are not reference ops
             for (int v : op.out) {
                 if (fdt(r, v) == sbk::F64 || r.P.st[(size_t)V(r, v).st].kind == SKind::Aux) continue;
-                CK(cudaMemsetAsync(nan_flag, 0, sizeof(int), stream));
-                sbk::count_nan(fp(r, v), fdt(r, v), V(r, v).numel(), nan_flag, stream);
-                int h = 0;
-                CK(cudaMemcpyAsync(&h, nan_flag, sizeof(int), cudaMemcpyDeviceToHost, stream));
-                CK(cudaStreamSynchronize(stream));
-                if (h) throw Error(std::string("NaN produced by op '") + k_str(op.k) + "' on rank " + std::to_string(r.P.rank));
+                sbk::count_nan(fp(r, v), fdt(r, v), V(r, v).numel(), nan_counts + k * ranks[0].P.fwd.size() + (size_t)i,
+                               stream);
             }
+        }
+    }
+    void nan_report() {
+        const size_t nf = ranks[0].P.fwd.size();
+        std::vector<int> h(nf * ranks.size());
+        CK(cudaMemcpyAsync(h.data(), nan_counts, h.size() * sizeof(int), cudaMemcpyDeviceToHost, stream));
+        CK(cudaStreamSynchronize(stream));
+        for (size_t i = 0; i < nf; ++i)
+            for (size_t k = 0; k < ranks.size(); ++k)
+                if (h[k * nf + i])
+                    throw Error(std::string("NaN produced by op '") + k_str(ranks[k].P.fwd[i].k) + "' on rank " +
+                                std::to_string(ranks[k].P.rank));
+    }
+
+    // ---------------------------------------- forward all-reduce overlap
+    // Row-parallel Linear (Megatron out.dense / dense2, sync forward) -> all_reduce ->
+    // bias+dropout+residual+LayerNorm: the rows are cut into chunks; the GEMM of chunk
+    // c+1 runs on the executor stream while chunk c is all-reduced on the
+    // communication stream, and each chunk's LayerNorm tail waits only for its own
+    // all-reduce. Every row's values are the unchunked ones (a row's GEMM, sum over
+    // ranks and LayerNorm do not depend on other rows; the keep bits are indexed by
+    // the global element index), so the semantics are the reference's
+    // (executor.cpp:812-820 all_reduce, schedule.cpp:205-309 sync forward).
+    std::vector<cudaEvent_t> far_gemm, far_done;  // per chunk (reused across ops)
+    // NCCL kernels need SMs of their own to run beside a persistent GEMM: while a
+    // collective is in flight on cstream, the 2-SM GEMM leaves $SB_COMM_SMS (16) SMs free
+    struct CommSmReserve {
+        explicit CommSmReserve(ExecutorImpl& e) {
+            if (!(e.comm.nccl && e.world > 1)) return;
+            static const int n = getenv("SB_COMM_SMS") ? atoi(getenv("SB_COMM_SMS")) : 16;
+            sbk::gemm_set_sm_reserve(n);
+            on = true;
+        }
+        ~CommSmReserve() {
+            if (on) sbk::gemm_set_sm_reserve(0);
+        }
+        bool on = false;
+    };
+    int fwd_ar_chunk_cap = -1;
+    int fwd_ar_chunks(RankCtx& r, const Op& op) {
+        if (fwd_ar_chunk_cap < 0) {
+            const char* e = getenv("SB_FWD_AR_CHUNKS");
+            fwd_ar_chunk_cap = e ? std::max(1, atoi(e)) : 4;
+        }
+        if (!cstream) return 1;
+        const View& y = V(r, op.out[0]);
+        const i64 rows = rows_of(y), n = cols_of(y);
+        if (op.dropout && !op.s1) return 1;
+        // chunks of >= 256 rows (whole 2-SM GEMM tiles) whose keep bits start on a word
+        int c = fwd_ar_chunk_cap;
+        while (c > 1 && (rows % c || (rows / c) % 256 || ((rows / c) * n) % 32)) --c;
+        return c;
+    }
+    void fused_res_ln_overlapped(int i, int nch) {
+        ++collectives;
+        while ((int)far_gemm.size() < nch) {
+            cudaEvent_t a, b;
+            CK(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+            far_gemm.push_back(a);
+            far_done.push_back(b);
+        }
+        const Op& op0 = ranks[0].P.fwd[(size_t)i];
+        const i64 rows = rows_of(V(ranks[0], op0.out[0])), cr = rows / nch;
+        const size_t eb = sbk::dt_bytes(cdt);
+        CommSmReserve keep_sms(*this);
+        for (int c = 0; c < nch; ++c) {
+            std::vector<char*> part;
+            for (auto& r : ranks) {
+                const Op& op = r.P.fwd[(size_t)i];
+                const View& x = V(r, op.in[0]);
+                const View& w = V(r, op.in[1]);
+                i64 xr, cols, ldx;
+                x.rowwise(xr, cols, ldx);
+                const i64 out_f = w.shape[0];
+                char* pc = fp(r, op.out[1]) + (size_t)(c * cr * out_f) * eb;
+                gemm_rowwise(r, fp(r, op.in[0]) + (size_t)(c * cr * ldx) * eb, ldx, false, fp(r, op.in[1]), cols, true,
+                             pc, out_f, cdt, cr, out_f, cols, false, nullptr);
+                ++launches;
+                part.push_back(pc);
+            }
+            CK(cudaEventRecord(far_gemm[(size_t)c], stream));
+            CK(cudaStreamWaitEvent(cstream, far_gemm[(size_t)c], 0));
+            all_reduce(part, part, cdt, cr * V(ranks[0], op0.out[1]).shape.back(), cstream);
+            CK(cudaEventRecord(far_done[(size_t)c], cstream));
+        }
+        for (int c = 0; c < nch; ++c) {
+            CK(cudaStreamWaitEvent(stream, far_done[(size_t)c], 0));
+            for (auto& r : ranks) fused_res_ln_tail(r, r.P.fwd[(size_t)i], c * cr, cr);
         }
     }
 
@@ -794,15 +917,19 @@ public:
                      out_f, cols, false, nullptr);
         ++launches;
     }
-    void fused_res_ln_tail(RankCtx& r, const Op& op) {
+    // rows [row0, row0 + nrows) (all rows when nrows < 0)
+    void fused_res_ln_tail(RankCtx& r, const Op& op, i64 row0 = 0, i64 nrows = -1) {
         const View& y = V(r, op.out[0]);
         i64 rows = rows_of(y), n = cols_of(y);
+        if (nrows >= 0) rows = nrows;
+        const size_t eo = (size_t)(row0 * n) * sbk::dt_bytes(cdt);
         const void* bias = op.has_bias && op.bias_on ? fp(r, op.in[5]) : nullptr;
-        sbk::bias_dropout_residual_ln_fwd(fp(r, op.out[1]), bias, fp(r, op.in[2]), fp(r, op.in[3]), fp(r, op.in[4]), cdt,
-                                          fp(r, op.out[2]), fp(r, op.out[0]), (float*)fp(r, op.out[3]),
-                                          (float*)fp(r, op.out[4]), cdt, rows, n, (float)op.eps, op.s1,
-                                          op.dropout ? op.thr : 0, (float)(1.0 / (1.0 - op.p)), stream,
-                                          op.dropout ? (const uint32_t*)fp(r, op.out[5]) : nullptr);
+        sbk::bias_dropout_residual_ln_fwd(fp(r, op.out[1]) + eo, bias, fp(r, op.in[2]) + eo, fp(r, op.in[3]), fp(r, op.in[4]),
+                                          cdt, fp(r, op.out[2]) + eo, fp(r, op.out[0]) + eo,
+                                          (float*)fp(r, op.out[3]) + row0, (float*)fp(r, op.out[4]) + row0, cdt, rows, n,
+                                          (float)op.eps, op.s1, op.dropout ? op.thr : 0, (float)(1.0 / (1.0 - op.p)),
+                                          stream,
+                                          op.dropout ? (const uint32_t*)fp(r, op.out[5]) + (row0 * n) / 32 : nullptr);
         ++launches;
     }
 
@@ -1030,7 +1157,7 @@ public:
                 if (ar_pending.size() > (size_t)i && ar_pending[(size_t)i]) {
                     CK(cudaStreamWaitEvent(stream, ar_ev[(size_t)i], 0));  // issued right after the dgrad
                     ar_pending[(size_t)i] = 0;
-                } else if (world > 1) {
+                } else if (world > 1 || comm.nccl) {
                     all_reduce(b, b, cdt, n);
                 }
                 for (auto& r : ranks) {
@@ -1409,6 +1536,11 @@ public:
     }
 
     void run_forward() {
+        if (nan_guard) nan_reset();
+        run_forward_ops();
+        if (nan_guard && !capturing()) nan_report();
+    }
+    void run_forward_ops() {
         if (mask_inline) {
             for (size_t i = 0; i < ranks[0].P.fwd.size(); ++i) {
                 if (mask_ev.size() > i && mask_ev[i]) gen_mask(i, stream);
@@ -1514,7 +1646,10 @@ public:
 Executor::Executor(const Module& root, bool train, u64 seed, int world, DT compute, const CommConfig& comm, bool fused)
     : impl_(std::make_unique<ExecutorImpl>(root, train, seed, world, compute, comm, fused)) {}
 Executor::~Executor() = default;
-void Executor::set_nan_guard(bool on) { impl_->nan_guard = on; }
+void Executor::set_nan_guard(bool on) {
+    if (on) impl_->nan_alloc();
+    impl_->nan_guard = on;
+}
 
 void Executor::upload_inputs(const std::vector<HostTensor>& inputs) {
     auto& I = *impl_;
@@ -1665,6 +1800,7 @@ void Executor::launch_graph() {
     auto& I = *impl_;
     if (!I.gexec) capture_graph();
     CK(cudaGraphLaunch(I.gexec, I.stream));
+    if (I.nan_guard) I.nan_report();
 }
 int Executor::kernel_launches_per_step() const {
     // exact: the kernel nodes of the captured fwd+bwd graph

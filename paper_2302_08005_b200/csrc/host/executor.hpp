@@ -21,6 +21,9 @@
 
 namespace sb {
 
+// the process's NCCL (dlopen handle; nullptr if none): executor.cpp
+void* nccl_handle();
+
 struct CommConfig {
     bool nccl = false;
     int rank = 0;                // nccl: this process's rank

@@ -192,7 +192,7 @@ struct Lowerer {
 
     // ---------------------------------------------------------- modules
     Val eval_module(const Module& m, const std::string& path, std::vector<Val> args) {
-        if (get_flag(m.attrs, "sync_backward") && o.world > 1 && !args.empty())
+        if (get_flag(m.attrs, "sync_backward") && o.collect() && !args.empty())
             args[0] = Val{{sync_grad(args[0].one())}, false};
         bool want_ckpt = (get_flag(m.attrs, "checkpoint") || m.kind == "EfficientAttention") && !in_ckpt;
         if (want_ckpt) {
@@ -500,7 +500,7 @@ struct Lowerer {
         // ---- Linear -> gelu
         if (core.size() == 2 && kind_of(core[1]) == "op:gelu" && core[1]->args[0] == core[0]->id && g.inputs.size() == 1) {
             int x = args[0].one();
-            if (get_flag(lin->attrs, "sync_backward") && o.world > 1) x = sync_grad(x);
+            if (get_flag(lin->attrs, "sync_backward") && o.collect()) x = sync_grad(x);
             return fused_linear_gelu(*lin, lpath, x, path, out);
         }
         // ---- Linear -> [all_reduce] -> [Dropout] -> add(., residual) -> LayerNorm
@@ -530,7 +530,7 @@ struct Lowerer {
         if (ar && ((wp->shard && wp->shard->axis != 1) || (bp && bp->shard))) return false;
         if (V(args[0].one()).shape.size() < 1) return false;
         int x = args[0].one();
-        if (get_flag(lin->attrs, "sync_backward") && o.world > 1) x = sync_grad(x);
+        if (get_flag(lin->attrs, "sync_backward") && o.collect()) x = sync_grad(x);
         int res = contig(args[1].one());
         x = rowwise(x);
         int w = param_view(*lin, lpath, "weight");
@@ -555,7 +555,7 @@ struct Lowerer {
         // rank; its gradient still lands on rank 0 only (executor.cpp:645,1146)
         op.bias_on = b >= 0 && (ar || !rank0_only || o.rank == 0);
         op.bias_grad = b >= 0 && (!rank0_only || o.rank == 0);
-        op.allreduce = ar && o.world > 1;
+        op.allreduce = ar && o.collect();
         op.out = {y, partial, sum, aux(rows), aux(rows)};
         op.eps = get_double(ln->attrs, "eps").value_or(1e-5);
         if (drop) {
@@ -632,7 +632,7 @@ struct Lowerer {
         if (opn == "all_reduce") {
             int x = arg(0);
             P.collectives_fwd += 1;
-            if (o.world == 1) {
+            if (!o.collect()) {
                 // one-rank sum: the value itself (the count still matches the reference)
                 Op op;
                 op.k = K::AllReduce;

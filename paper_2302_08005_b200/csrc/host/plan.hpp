@@ -126,6 +126,10 @@ struct LowerOptions {
     u64 seed = 0;
     DT cdt = sbk::F32;
     bool fused_kernels = true;  // lower recognised fused regions / EfficientAttention to fused kernels
+    // NCCL executor at world 1: keep the one-rank collectives (all_reduce, SyncGrad) as real
+    // NCCL calls so the communicator, the comm stream and graph capture of NCCL run
+    bool keep_collectives = false;
+    bool collect() const { return world > 1 || keep_collectives; }
 };
 
 Plan lower(const Module& root, const LowerOptions& o);

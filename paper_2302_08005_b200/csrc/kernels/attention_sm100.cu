@@ -624,7 +624,7 @@ __device__ __forceinline__ unsigned long long gtime() {
 
 // delta = rowsum(dO * O) and lse2 = lse * log2(e); 8 threads per (b, h, query) row
 __global__ void k_fa5_prep(const bf16* dout, long long ld_do, const bf16* o, long long ld_o, const float* lse,
-                           float* lse2, float* delta, long long BH, int S, int nh) {
+                           float* lse2, float* delta, long long BH, int S, int nh, float sgn) {
     const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     const long long idx = tid >> 3;
     const int part = (int)(tid & 7);
@@ -646,8 +646,8 @@ __global__ void k_fa5_prep(const bf16* dout, long long ld_do, const bf16* o, lon
     acc += __shfl_xor_sync(0xffffffffu, acc, 2);
     acc += __shfl_xor_sync(0xffffffffu, acc, 4);
     if (ok && part == 0) {
-        delta[idx] = acc;
-        lse2[idx] = lse[idx] * 1.4426950408889634f;
+        delta[idx] = sgn * acc;
+        lse2[idx] = sgn * lse[idx] * 1.4426950408889634f;
     }
 }
 
@@ -1037,6 +1037,486 @@ __global__ void __launch_bounds__(512, 1)
     }
 }
 
+
+// ---------------------------------------------------------------- backward v7
+// Same recurrence and CTA = (batch, head) sweep as k_fa5_bwd, re-laid-out so the
+// tensor pipe reads most operands from TMEM and twice as many warps run the
+// softmax (the round-2 timeline showed the fa5 step bound by 8 softmax warps and
+// by a pipeline drain at every key block):
+//   * K_j and V_j live in TMEM (cols [448,480) / [480,512), bf16 pairs, lane = key)
+//     as the A operand of S^T = K Q^T and dP^T = V dO^T (TS MMAs: only the 2 KB
+//     B slice per K16 step comes from shared memory); the softmax warps copy
+//     block j+1 into TMEM from shared memory as soon as block j's last S/dP MMAs
+//     completed, so the next block starts without a drain;
+//   * Z^T = keep/(1-p) P^T and dS^T overwrite the S^T columns they came from
+//     (bf16 pairs) and feed dV += Z^T dO and dK += dS^T Q as TS MMAs; dS^T also
+//     goes to shared memory (128B swizzle) for dQ = dS K (SS, MN-major A);
+//   * K is double-buffered in shared memory (dQ of block j reads K_j while K_{j+1}
+//     lands), V has one staging buffer (it only feeds the TMEM copy);
+//   * 16 softmax warps (lane quarter x 16-query column group), 4 dQ warps.
+// TMEM: S^T/Z^T/dS^T [0,128), dP^T [128,256), dV [256,320), dK [320,384),
+// dQ [384,448), K [448,480), V [480,512).
+constexpr int B7_NST = 2;
+constexpr int B7_STAGE = 2 * F_TILE_BYTES + 1024 + 2048;  // Q, dO, lse2[128], delta[128], keep bits [128][4]
+constexpr int B7_WARPS = 23;                              // 16 softmax, 4 dQ, producer, MMA, dQ-MMA
+// The single-thread roles get the highest warp ids: the warp schedulers favour
+// higher ids, and a starved MMA issuer stalls every other role.
+constexpr int W_PROD = 20, W_MMA = 21, W_DQMMA = 22;
+constexpr int B7_OUT = 2048;  // per-warp output staging: 32 rows x 32 bf16, row-major (TMA store box)
+constexpr int B7_SMEM = 1024 + 3 * F_TILE_BYTES + B7_NST * B7_STAGE + 4 * F_TILE_BYTES + 20 * B7_OUT + 256;
+
+__device__ __forceinline__ void store_row_bf16(bf16* dst, const float* f, int n16, float sc, bool acc) {
+    // n16 x 8 values of one row -> bf16 (x sc, += the existing values when acc), 16-byte stores
+    for (int c = 0; c < n16; ++c) {
+        float g[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) g[t] = f[c * 8 + t] * sc;
+        uint4* d = (uint4*)dst + c;
+        if (acc) {
+            const uint4 old = *d;
+            const __nv_bfloat162* po = (const __nv_bfloat162*)&old;
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                const float2 x = __bfloat1622float2(po[t]);
+                g[2 * t] += x.x;
+                g[2 * t + 1] += x.y;
+            }
+        }
+        *d = make_uint4(pack_bf16(g[0], g[1]), pack_bf16(g[2], g[3]), pack_bf16(g[4], g[5]), pack_bf16(g[6], g[7]));
+    }
+}
+
+// A warp's 32 rows (thread = row) x 32 fp32 -> bf16 (x sc) -> its staging slot (64B swizzle) ->
+// one TMA bulk-tensor store of the 32x32 box at (c0, r0): the global write is
+// coalesced by the TMA engine instead of 32 scattered 16-byte stores per instruction.
+__device__ __forceinline__ void warp_tile_tma(uint8_t* stage, const CUtensorMap* map, int c0, int r0, const float* f,
+                                              float sc, int lane) {
+    if (lane == 0) bulk_wait_read0();  // the previous store from this slot has read it
+    __syncwarp();
+    // 64-byte TMA swizzle: 16-byte chunk c of row r sits at chunk c ^ ((r >> 1) & 3)
+    // (conflict-free: the 8 lanes of a store phase hit 8 distinct bank groups)
+    uint4* row = (uint4*)(stage + lane * 64);
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+        row[c ^ ((lane >> 1) & 3)] = make_uint4(pack_bf16(f[8 * c] * sc, f[8 * c + 1] * sc), pack_bf16(f[8 * c + 2] * sc, f[8 * c + 3] * sc),
+                                                pack_bf16(f[8 * c + 4] * sc, f[8 * c + 5] * sc), pack_bf16(f[8 * c + 6] * sc, f[8 * c + 7] * sc));
+    fence_proxy_async();
+    __syncwarp();
+    if (lane == 0) {
+        tma_store_2d_cta(map, stage, c0, r0);
+        bulk_commit_group();
+    }
+}
+
+__global__ void __launch_bounds__(B7_WARPS * 32, 1)
+    k_fa7_bwd(const __grid_constant__ CUtensorMap tK, const __grid_constant__ CUtensorMap tV,
+              const __grid_constant__ CUtensorMap tQ, const __grid_constant__ CUtensorMap tdO,
+              const __grid_constant__ CUtensorMap tM, const __grid_constant__ CUtensorMap tdQ,
+              const __grid_constant__ CUtensorMap tdK, const __grid_constant__ CUtensorMap tdV, BwdArgs ba) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024 - (tc5::smem_u32(smem_raw) & 1023)) & 1023);
+    uint8_t* sK = smem;                              // [2] K_j (dQ's B operand; TMEM copy source)
+    uint8_t* sV = sK + 2 * F_TILE_BYTES;             // V_j staging (TMEM copy source)
+    uint8_t* sStage = sV + F_TILE_BYTES;             // [B7_NST][B7_STAGE]
+    uint8_t* sDS = sStage + B7_NST * B7_STAGE;       // [2] x dS^T [2 q-halves][128 keys][64 q] bf16, swizzled
+    uint8_t* sOut = sDS + 4 * F_TILE_BYTES;         // [20 warps][B7_OUT]
+    uint64_t* bars = (uint64_t*)(sOut + 20 * B7_OUT);
+    uint64_t* kv_full = bars;               // [2] K_j -> sK[j&1], V_j -> sV landed
+    uint64_t* k_empty = bars + 2;           // [2] sK[b] no longer read (dQ of its block done)
+    uint64_t* v_empty = bars + 4;           // sV copied into TMEM
+    uint64_t* kv_tmem = bars + 5;           // K_j / V_j in TMEM
+    uint64_t* st_full = bars + 6;           // [B7_NST]
+    uint64_t* st_empty = st_full + B7_NST;  // [B7_NST]
+    uint64_t* sdp_full = st_empty + B7_NST; // [2 halves]
+    uint64_t* sm_done = sdp_full + 2;       // [2 halves]
+    uint64_t* dq_full = sm_done + 2;
+    uint64_t* dq_free = dq_full + 1;
+    uint64_t* acc_full = dq_free + 1;
+    uint64_t* acc_free = acc_full + 1;
+    uint64_t* ds_free = acc_free + 1;       // [2] dS^T buffer b no longer read (its dQ MMAs done)
+    uint64_t* ds_full = ds_free + 2;        // [2] dS^T buffer b written (both halves)
+    uint32_t* tslot = (uint32_t*)(ds_full + 2);
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int S = ba.S, nj = S / FT, nsteps = nj * nj;
+    const int h = blockIdx.x, b = blockIdx.y;
+    const long long bh = (long long)b * ba.nh + h;
+    const int row_base = b * S;
+    const bool TS7 = ba.ts && blockIdx.x == 0 && blockIdx.y == 0;
+
+    if (threadIdx.x == 0) {
+        tma_prefetch(&tK);
+        tma_prefetch(&tV);
+        tma_prefetch(&tQ);
+        tma_prefetch(&tdO);
+        if (ba.mask_t) tma_prefetch(&tM);
+        for (int x = 0; x < 2; ++x) {
+            mbar_init(&kv_full[x], 1);
+            mbar_init(&k_empty[x], 1);
+            mbar_init(&sdp_full[x], 1);
+            mbar_init(&sm_done[x], 16);
+        }
+        mbar_init(v_empty, 8);
+        mbar_init(kv_tmem, 16);
+        for (int s = 0; s < B7_NST; ++s) {
+            mbar_init(&st_full[s], 1);
+            mbar_init(&st_empty[s], 1);
+        }
+        mbar_init(dq_full, 1);
+        mbar_init(dq_free, 4);
+        mbar_init(acc_full, 1);
+        mbar_init(acc_free, 16);
+        for (int x = 0; x < 2; ++x) {
+            mbar_init(&ds_free[x], 1);
+            mbar_init(&ds_full[x], 16);
+        }
+        fence_barrier_init();
+    }
+    if (warp == W_MMA) tmem_alloc<512>(tslot);
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem = *tslot;
+
+    if (warp == W_PROD) {
+        if (lane == 0) {
+            // ------------------------------------------------ TMA producer
+            auto load_kv = [&](int j) {
+                const int kb = j & 1;
+                if (j >= 2) mbar_wait(&k_empty[kb], ((j >> 1) & 1) ^ 1);
+                if (j >= 1) mbar_wait(v_empty, (j - 1) & 1);
+                mbar_expect_tx(&kv_full[kb], 2 * F_TILE_BYTES);
+                tma_load_2d(sK + kb * F_TILE_BYTES, &tK, &kv_full[kb], h * FD, row_base + j * FT);
+                tma_load_2d(sV, &tV, &kv_full[kb], h * FD, row_base + j * FT);
+            };
+            load_kv(0);
+            // K/V of block j+1 go out before the stage of step (j, min(2, nj-1)): late
+            // enough that V_j has been copied into TMEM (so the wait is short), early
+            // enough that block j+1 never waits for them
+            const int kv_at = nj > 2 ? 2 : nj - 1;
+            for (int u = 0; u < nsteps; ++u) {
+                const int j = u / nj, i = u % nj;
+                if (i == kv_at && j + 1 < nj) load_kv(j + 1);
+                const int s = u % B7_NST;
+                uint8_t* st = sStage + s * B7_STAGE;
+                if (TS7) ba.ts[14 * 64 + u] = gtime();
+                mbar_wait(&st_empty[s], ((u / B7_NST) & 1) ^ 1);
+                if (TS7) ba.ts[15 * 64 + u] = gtime();
+                mbar_expect_tx(&st_full[s], 2 * F_TILE_BYTES + 1024 + (ba.mask_t ? 2048 : 0));
+                tma_load_2d(st, &tQ, &st_full[s], h * FD, row_base + i * FT);
+                tma_load_2d(st + F_TILE_BYTES, &tdO, &st_full[s], h * FD, row_base + i * FT);
+                bulk_load(st + 2 * F_TILE_BYTES, ba.lse2 + bh * S + i * FT, 512, &st_full[s]);
+                bulk_load(st + 2 * F_TILE_BYTES + 512, ba.delta + bh * S + i * FT, 512, &st_full[s]);
+                if (ba.mask_t)
+                    tma_load_2d(st + 2 * F_TILE_BYTES + 1024, &tM, &st_full[s], i * (FT / 32), (int)(bh * S) + j * FT);
+            }
+        }
+    } else if (warp == W_MMA) {
+        // ------------------------------------------------ MMA issuer (whole warp, one
+        // elected lane issues: descriptors stay in uniform registers, each MMA is a
+        // couple of instructions; the 32-cycle M128 N64 K16 MMAs are issue-bound otherwise)
+        constexpr uint32_t id_s = idesc_bf16(FT, FT / 2, false, false);  // S^T / dP^T half: M128 N64
+        constexpr uint32_t id_kv = idesc_bf16(FT, FD, false, true);      // dV / dK: M128 N64, B MN-major
+        constexpr uint32_t id_q = idesc_bf16(FT, FD, true, true);        // dQ: A and B MN-major
+        const bool mm = !(ba.dbg & 4);
+        const uint32_t stage0 = smem_u32(sStage);
+        auto issue_sdp = [&](int u, int hh) {
+            const int j = u / nj, i = u % nj, s = u % B7_NST;
+            const uint32_t aQ = stage0 + s * B7_STAGE + hh * (F_TILE_BYTES / 2);
+            if (hh == 0) {
+                if (i == 0) mbar_wait(kv_tmem, j & 1);  // K_j / V_j in TMEM
+                mbar_wait(&st_full[s], (u / B7_NST) & 1);
+                fence_after();
+            }
+            if (mm) {
+                const uint64_t dq = desc_kmajor(aQ, 0), ddo = desc_kmajor(aQ + F_TILE_BYTES, 0);
+#pragma unroll
+                for (int kk = 0; kk < FD / 16; ++kk)  // S^T half = K Q_half^T
+                    mma_ts_w(tmem + hh * 64, tmem + 448 + kk * 8, dq + 2 * kk, id_s, kk);
+#pragma unroll
+                for (int kk = 0; kk < FD / 16; ++kk)  // dP^T half = V dO_half^T
+                    mma_ts_w(tmem + 128 + hh * 64, tmem + 480 + kk * 8, ddo + 2 * kk, id_s, kk);
+            }
+            mma_commit_w(&sdp_full[hh]);
+        };
+        issue_sdp(0, 0);
+        issue_sdp(0, 1);
+        for (int u = 0; u < nsteps; ++u) {
+            const int j = u / nj, i = u % nj, s = u % B7_NST;
+            const uint32_t aQ = stage0 + s * B7_STAGE, adO = aQ + F_TILE_BYTES;
+#pragma unroll 1
+            for (int hh = 0; hh < 2; ++hh) {
+                mbar_wait(&sm_done[hh], u & 1);
+                if (hh == 0 && i == 0 && j > 0) mbar_wait(acc_free, (j - 1) & 1);  // dK/dV of block j-1 drained
+                if (TS7 && lane == 0) ba.ts[hh * 64 + u] = gtime();
+                fence_after();
+                if (mm) {
+                    const uint64_t bdo = desc_mnmajor(adO, hh * 4), bq = desc_mnmajor(aQ, hh * 4);
+#pragma unroll
+                    for (int k4 = 0; k4 < 4; ++k4)  // dV += Z^T_half dO_half (Z^T: 8 cols per 16 queries)
+                        mma_ts_w(tmem + 256, tmem + hh * 64 + k4 * 16, bdo + 128 * k4, id_kv, i | hh | k4);
+#pragma unroll
+                    for (int k4 = 0; k4 < 4; ++k4)  // dK += dS^T_half Q_half
+                        mma_ts_w(tmem + 320, tmem + hh * 64 + k4 * 16 + 8, bq + 128 * k4, id_kv, i | hh | k4);
+                }
+                if (hh == 1) {
+                    mma_commit_w(&st_empty[s]);  // Q, dO, lse, delta, keep bits of this step are no longer read
+                    if (i == nj - 1) mma_commit_w(acc_full);
+                }
+                if (u + 1 < nsteps) issue_sdp(u + 1, hh);
+            }
+        }
+    } else if (warp == W_DQMMA) {
+        // ------------------------------------------------ dQ MMA issuer (a warp of its own:
+        // tcgen05.mma issue blocks while the tensor pipe drains, so these would otherwise
+        // delay the S/dP issue the softmax warps wait for)
+        constexpr uint32_t id_q = idesc_bf16(FT, FD, true, true);  // dQ: A and B MN-major
+        const bool mm = !(ba.dbg & 4);
+        const uint32_t ds0 = smem_u32(sDS), k0 = smem_u32(sK);
+        for (int u = 0; u < nsteps; ++u) {
+            const int j = u / nj, i = u % nj;
+            mbar_wait(&ds_full[u & 1], (u >> 1) & 1);  // dS^T(u) written (both halves)
+            if (u > 0) mbar_wait(dq_free, (u - 1) & 1);  // dQ of the previous step has left TMEM
+            if (TS7 && lane == 0) ba.ts[2 * 64 + u] = gtime();
+            fence_after();
+            if (mm) {
+                const uint64_t da = sdesc(ds0 + (u & 1) * 2 * F_TILE_BYTES, 16384 >> 4, 1024 >> 4),
+                               db = desc_mnmajor(k0 + (j & 1) * F_TILE_BYTES, 0);
+#pragma unroll
+                for (int kk = 0; kk < FT / 16; ++kk)  // dQ_ij = dS K
+                    mma_ss_w(tmem + 384, da + 128 * kk, db + 128 * kk, id_q, kk);
+            }
+            mma_commit_w(dq_full);
+            mma_commit_w(&ds_free[u & 1]);
+            if (i == nj - 1) mma_commit_w(&k_empty[j & 1]);  // K_j no longer read
+        }
+    } else if (warp < 16) {
+        // ------------------------------------------------------------------
+        // 16 softmax warps: lane quarter q4 (key rows), column group cg = 16 of
+        // the 64 queries of each half
+        const int q4 = warp & 3, cg = warp >> 2, k = q4 * 32 + lane;
+        const uint32_t t_lane = tmem + ((uint32_t)(q4 * 32) << 16);
+        // K_j (cg 0, 1) / V_j (cg 2, 3) rows -> TMEM (16 of their 32 bf16-pair columns each)
+        auto kv_to_tmem = [&](int j) {
+            mbar_wait(&kv_full[j & 1], (j >> 1) & 1);
+            const uint8_t* src = (cg < 2 ? sK + (j & 1) * F_TILE_BYTES : sV) + k * 128;
+            uint32_t r[16];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const uint4 x = *(const uint4*)(src + ((((cg & 1) * 4 + c) ^ (k & 7)) * 16));
+                r[4 * c] = x.x;
+                r[4 * c + 1] = x.y;
+                r[4 * c + 2] = x.z;
+                r[4 * c + 3] = x.w;
+            }
+            uint32_t r0[8], r1[8];
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+                r0[t] = r[t];
+                r1[t] = r[8 + t];
+            }
+            const uint32_t col = (cg < 2 ? 448 : 480) + (cg & 1) * 16;
+            tmem_st8(t_lane + col, r0);
+            tmem_st8(t_lane + col + 8, r1);
+            tmem_st_wait();
+            fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                mbar_arrive(kv_tmem);
+                if (cg >= 2) mbar_arrive(v_empty);
+            }
+        };
+        // dV_j (cg 0, 1) / dK_j (cg 2, 3): 32 of the 64 columns of this thread's key row
+        auto drain_kv = [&](int j) {
+            mbar_wait(acc_full, j & 1);
+            fence_after();
+            uint32_t r[32];
+            tmem_ld32_nowait(t_lane + 256 + cg * 32, r);
+            tmem_ld_wait();
+            fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(acc_free);
+            float f[32];
+#pragma unroll
+            for (int e = 0; e < 32; ++e) f[e] = __uint_as_float(r[e]);
+            const long long row = row_base + (long long)j * FT + k;
+            if (ba.dbg & 32) return;
+            const bool acc = cg >= 2 ? (ba.acc & 2) : (ba.acc & 4);
+            if (!acc)  // coalesced: staged tile + TMA store
+                warp_tile_tma(sOut + warp * B7_OUT, cg >= 2 ? &tdK : &tdV, h * FD + (cg & 1) * 32,
+                              row_base + j * FT + q4 * 32, f, cg >= 2 ? ba.scale : 1.f, lane);
+            else if (cg >= 2)
+                store_row_bf16(ba.dk + row * ba.ld_dk + (long long)h * FD + (cg & 1) * 32, f, 4, ba.scale, true);
+            else
+                store_row_bf16(ba.dv + row * ba.ld_dv + (long long)h * FD + (cg & 1) * 32, f, 4, 1.f, true);
+        };
+        kv_to_tmem(0);
+        for (int u = 0; u < nsteps; ++u) {
+            const int j = u / nj, i = u % nj, s = u % B7_NST;
+            const float* lse_s = (const float*)(sStage + s * B7_STAGE + 2 * F_TILE_BYTES);
+            const float* dl_s = lse_s + FT;
+            uint8_t* ds_buf = sDS + (u & 1) * 2 * F_TILE_BYTES;
+            mbar_wait(&st_full[s], (u / B7_NST) & 1);
+#pragma unroll 1
+            for (int hh = 0; hh < 2; ++hh) {
+                const int q0 = hh * 64 + cg * 16;  // first query (of the 128-query block) of this thread's columns
+                mbar_wait(&sdp_full[hh], u & 1);
+                if (TS7 && warp == 0 && lane == 0) ba.ts[(3 + 2 * hh) * 64 + u] = gtime();
+                if (TS7 && lane == 0 && u == 5) ba.ts[(12 + hh) * 64 + warp] = gtime();
+                fence_after();
+                if (hh == 1 && i == nj - 1 && j + 1 < nj) kv_to_tmem(j + 1);  // block j's S/dP all complete
+                uint32_t sv[16], dp[16];
+                if (!(ba.dbg & 8)) {
+                    tmem_ld16_nowait(t_lane + q0, sv);
+                    tmem_ld16_nowait(t_lane + 128 + q0, dp);
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) sv[e] = dp[e] = e;
+                }
+                const uint32_t mword =
+                    ba.mask_t ? *(const uint32_t*)(sStage + s * B7_STAGE + 2 * F_TILE_BYTES + 1024 + k * 16 + (q0 >> 5) * 4) >>
+                                    (q0 & 16)
+                              : 0xFFFFu;
+                tmem_ld_wait();
+                uint32_t zk[8], dk[8];
+#pragma unroll
+                for (int e4 = 0; e4 < 4; ++e4) {
+                    if (ba.dbg & 1) {
+                        zk[2 * e4] = zk[2 * e4 + 1] = dk[2 * e4] = dk[2 * e4 + 1] = sv[e4] ^ dp[e4];
+                        continue;
+                    }
+                    // (lse2 and delta are stored negated by the prep kernel)
+                    const float4 l4 = *(const float4*)(lse_s + q0 + e4 * 4);
+                    const float4 d4 = *(const float4*)(dl_s + q0 + e4 * 4);
+                    const float2 lv[2] = {make_float2(l4.x, l4.y), make_float2(l4.z, l4.w)};
+                    const float2 dv[2] = {make_float2(d4.x, d4.y), make_float2(d4.z, d4.w)};
+                    const float2 c2 = make_float2(ba.c, ba.c);
+#pragma unroll
+                    for (int e2 = 0; e2 < 2; ++e2) {  // element pairs on the packed-fp32 pipe
+                        const int e = e4 * 4 + e2 * 2;
+                        const float2 a = ffma2(make_float2(__uint_as_float(sv[e]), __uint_as_float(sv[e + 1])), c2, lv[e2]);
+                        const float2 p = make_float2(ex2f(a.x), ex2f(a.y));
+                        const float2 kd = make_float2(((mword >> e) & 1) ? ba.dscale : 0.f,
+                                                      ((mword >> (e + 1)) & 1) ? ba.dscale : 0.f);
+                        const float2 z = fmul2(p, kd);
+                        const float2 ds =
+                            fmul2(p, ffma2(kd, make_float2(__uint_as_float(dp[e]), __uint_as_float(dp[e + 1])), dv[e2]));
+                        zk[2 * e4 + e2] = pack_bf16(z.x, z.y);
+                        dk[2 * e4 + e2] = pack_bf16(ds.x, ds.y);
+                    }
+                }
+                if (!(ba.dbg & 64)) {
+                    tmem_st8(t_lane + q0, zk);      // Z^T over this group's S^T columns
+                    tmem_st8(t_lane + q0 + 8, dk);  // dS^T next to it
+                }
+                // dS^T row k, queries q0..q0+15 of half hh: 16-byte chunks cg*2, cg*2+1 of the 128 B row
+                if (hh == 0 && u >= 2) mbar_wait(&ds_free[u & 1], ((u >> 1) - 1) & 1);  // dQ(u-2) read this buffer
+                uint8_t* rowp = ds_buf + hh * 16384 + k * 128;
+                if (!(ba.dbg & 16)) {
+                    *(uint4*)(rowp + (((cg * 2) ^ (k & 7)) * 16)) = make_uint4(dk[0], dk[1], dk[2], dk[3]);
+                    *(uint4*)(rowp + (((cg * 2 + 1) ^ (k & 7)) * 16)) = make_uint4(dk[4], dk[5], dk[6], dk[7]);
+                }
+                tmem_st_wait();
+                fence_proxy_async();
+                fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    mbar_arrive(&sm_done[hh]);
+                    if (hh == 1) mbar_arrive(&ds_full[u & 1]);
+                }
+                if (TS7 && warp == 0 && lane == 0) ba.ts[(4 + 2 * hh) * 64 + u] = gtime();
+                if (TS7 && lane == 0 && u == 5) ba.ts[(8 + hh) * 64 + warp] = gtime();
+                if (TS7 && lane == 0 && u == 6) ba.ts[(10 + hh) * 64 + warp] = gtime();
+                if (hh == 0 && i == 0 && j > 0) drain_kv(j - 1);  // TMEM dK/dV free before dV/dK of block j start
+            }
+        }
+        drain_kv(nj - 1);
+    } else {
+        // ---------------------------------------------------- 4 dQ warps (thread = query row)
+        // dQ_ij leaves TMEM right away (dQ(u+1) waits for dq_free); the row's fp32
+        // partial sum over key blocks lives in this CTA's private L2-resident buffer:
+        // written at j = 0, then red.global.add (performed at L2, no read round trip;
+        // every address is only ever updated by this one thread, in program order, so
+        // the summation order — and the result — is fixed), read back at the last j.
+        const int q4 = warp & 3, r = q4 * 32 + lane;
+        const uint32_t t_row = tmem + ((uint32_t)(q4 * 32) << 16) + 384;
+        for (int u = 0; u < nsteps; ++u) {
+            const int j = u / nj, i = u % nj;
+            // thread-major: float4 v of query row r of block i at ((bh*nj + i)*16 + v)*128 + r
+            float4* acc = (float4*)ba.dqacc + ((bh * nj + i) * 16) * FT + r;
+            const bool last = j == nj - 1, dbg = ba.dbg & 2;
+            float f[32];
+            if (last && nj > 1 && !dbg) {  // the final partial sum's first half, before dQ(u) lands
+#pragma unroll
+                for (int v = 0; v < 8; ++v) {
+                    const float4 a4 = __ldcg(acc + v * FT);
+                    f[4 * v] = a4.x;
+                    f[4 * v + 1] = a4.y;
+                    f[4 * v + 2] = a4.z;
+                    f[4 * v + 3] = a4.w;
+                }
+            } else {
+#pragma unroll
+                for (int e = 0; e < 32; ++e) f[e] = 0.f;
+            }
+            mbar_wait(dq_full, u & 1);
+            if (TS7 && warp == 16 && lane == 0) ba.ts[7 * 64 + u] = gtime();
+            fence_after();
+            uint32_t d[32];
+#pragma unroll 1
+            for (int pss = 0; pss < 2; ++pss) {
+                tmem_ld32_nowait(t_row + pss * 32, d);
+                tmem_ld_wait();
+                if (pss == 1) {
+                    fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(dq_free);
+                }
+                if (dbg) continue;
+                if (!last) {
+#pragma unroll
+                    for (int v = 0; v < 8; ++v) {
+                        const float4 x = make_float4(__uint_as_float(d[4 * v]), __uint_as_float(d[4 * v + 1]),
+                                                     __uint_as_float(d[4 * v + 2]), __uint_as_float(d[4 * v + 3]));
+                        if (j == 0) __stcg(acc + (pss * 8 + v) * FT, x);
+                        else red_add_v4((float*)(acc + (pss * 8 + v) * FT), x);
+                    }
+                    continue;
+                }
+                if (pss == 1 && nj > 1) {
+#pragma unroll
+                    for (int v = 0; v < 8; ++v) {
+                        const float4 a4 = __ldcg(acc + (8 + v) * FT);
+                        f[4 * v] = a4.x;
+                        f[4 * v + 1] = a4.y;
+                        f[4 * v + 2] = a4.z;
+                        f[4 * v + 3] = a4.w;
+                    }
+                } else if (pss == 1) {
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) f[e] = 0.f;
+                }
+#pragma unroll
+                for (int e = 0; e < 32; ++e) f[e] += __uint_as_float(d[e]);
+                if (!(ba.acc & 1))
+                    warp_tile_tma(sOut + warp * B7_OUT, &tdQ, h * FD + pss * 32, row_base + i * FT + q4 * 32, f, ba.scale,
+                                  lane);
+                else {
+                    const long long row = row_base + (long long)i * FT + r;
+                    store_row_bf16(ba.dq + row * ba.ld_dq + (long long)h * FD + pss * 32, f, 4, ba.scale, true);
+                }
+            }
+        }
+    }
+    if (lane == 0) bulk_wait0();  // this warp's TMA stores have completed
+    fence_before();
+    __syncthreads();
+    if (warp == W_MMA) {
+        fence_after();
+        tmem_dealloc<512>(tmem);
+    }
+}
+
 bool bwd_fits(const Attn& a, const void* dout, i64 ld_do, i64 ld_dq, i64 ld_dk, i64 ld_dv) {
     if (!fwd_fits(a)) return false;
     if (a.thr && !a.mask_t) return false;
@@ -1142,8 +1622,11 @@ bool attn_bwd_sm100_try(const Attn& a, const void* dout, i64 ld_do, void* dq, vo
     carve(a, ws, &w);
     const long long BH = a.B * a.nh;
     const long long n = BH * a.S;
+    // SB_ATTN_BWD=5 selects the round-1 kernel (A/B runs); v7 reads lse2 and delta negated
+    static const int ver = getenv("SB_ATTN_BWD") ? atoi(getenv("SB_ATTN_BWD")) : 7;
     k_fa5_prep<<<(unsigned)((n * 8 + 255) / 256), 256, 0, s>>>((const bf16*)dout, ld_do, (const bf16*)a.o, a.ld_o, a.lse,
-                                                              w.lse2, w.delta, BH, (int)a.S, (int)a.nh);
+                                                              w.lse2, w.delta, BH, (int)a.S, (int)a.nh,
+                                                              ver == 5 ? 1.f : -1.f);
     SBK_CHECK_LAUNCH();
     BwdArgs ba{w.lse2, w.delta, w.dqacc, a.thr ? a.mask_t : nullptr, a.thr ? a.dscale : 1.f,
                a.scale * 1.4426950408889634f, a.scale, (bf16*)dq, (bf16*)dk, (bf16*)dv, ld_dq, ld_dk, ld_dv,
@@ -1152,26 +1635,56 @@ bool attn_bwd_sm100_try(const Attn& a, const void* dout, i64 ld_do, void* dq, vo
     ba.ts = nullptr;
     static unsigned long long* ts_buf = nullptr;
     if (getenv("SB_ATTN_TS")) {
-        if (!ts_buf) cudaMalloc(&ts_buf, 8 * 64 * 8);
-        cudaMemsetAsync(ts_buf, 0, 8 * 64 * 8, s);
+        if (!ts_buf) cudaMalloc(&ts_buf, 16 * 64 * 8);
+        cudaMemsetAsync(ts_buf, 0, 16 * 64 * 8, s);
         ba.ts = ts_buf;
     }
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k_fa5_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, B_SMEM);
+        cudaFuncSetAttribute(k_fa7_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, B7_SMEM);
         attr = true;
     }
     dim3 grid((unsigned)a.nh, (unsigned)a.B);
-    k_fa5_bwd<<<grid, 512, B_SMEM, s>>>(tk, tv, tq, tdo, tm, ba);
+    if (ver == 5) k_fa5_bwd<<<grid, 512, B_SMEM, s>>>(tk, tv, tq, tdo, tm, ba);
+    else {
+        CUtensorMap tdq, tdk, tdv;
+        if (!make_map_bf16_plain(&tdq, dq, cols, rows, ld_dq, 32, 32) || !make_map_bf16_plain(&tdk, dk, cols, rows, ld_dk, 32, 32) ||
+            !make_map_bf16_plain(&tdv, dv, cols, rows, ld_dv, 32, 32))
+            throw std::runtime_error("attention backward: output tensor maps rejected");
+        k_fa7_bwd<<<grid, B7_WARPS * 32, B7_SMEM, s>>>(tk, tv, tq, tdo, tm, tdq, tdk, tdv, ba);
+    }
     SBK_CHECK_LAUNCH();
     if (ba.ts) {
-        unsigned long long h_ts[8 * 64];
+        unsigned long long h_ts[16 * 64];
         cudaMemcpyAsync(h_ts, ba.ts, sizeof(h_ts), cudaMemcpyDeviceToHost, s);
         cudaStreamSynchronize(s);
-        unsigned long long t0 = h_ts[0];
-        const char* names[7] = {"prod st_empty ok", "mma sm_done_b ok", "mma sdp(u+1) issued", "mma dq_free ok",
-                                "smax sdp ok", "smax done", "dq dq_full ok"};
-        for (int r = 0; r < 7; ++r) {
+        unsigned long long t0 = ~0ull;
+        for (auto x : h_ts)
+            if (x && x < t0) t0 = x;
+        const char* names5[8] = {"prod st_empty ok", "mma sm_done_b ok", "mma sdp(u+1) issued", "mma dq_free ok",
+                                 "smax sdp ok", "smax done", "dq dq_full ok", ""};
+        const char* names7[8] = {"mma sm_done0 ok", "mma sm_done1 ok", "mma dq issue", "smax sdp0 ok",
+                                 "smax h0 done", "smax sdp1 ok", "smax h1 done", "dq dq_full ok"};
+        const char** names = ver == 5 ? names5 : names7;
+        if (ver != 5) {
+            const char* wn[6] = {"u5 h0 done by warp", "u5 h1 done by warp", "u6 h0 done by warp", "u6 h1 done by warp",
+                                 "u5 sdp0 ok by warp", "u5 sdp1 ok by warp"};
+            for (int r = 8; r < 14; ++r) {
+                fprintf(stderr, "%-22s", wn[r - 8]);
+                for (int w = 0; w < 16; ++w) fprintf(stderr, " %6lld", h_ts[r * 64 + w] ? (long long)(h_ts[r * 64 + w] - t0) : -1);
+                fprintf(stderr, "\n");
+            }
+        }
+        if (ver != 5) {
+            const char* pn[2] = {"prod wait st_empty", "prod st_empty ok"};
+            for (int r = 14; r < 16; ++r) {
+                fprintf(stderr, "%-22s", pn[r - 14]);
+                for (int u = 0; u < 16; ++u) fprintf(stderr, " %6lld", h_ts[r * 64 + u] ? (long long)(h_ts[r * 64 + u] - t0) : -1);
+                fprintf(stderr, "\n");
+            }
+        }
+        for (int r = 0; r < (ver == 5 ? 7 : 8); ++r) {
             fprintf(stderr, "%-22s", names[r]);
             for (int u = 0; u < 16; ++u) fprintf(stderr, " %6lld", h_ts[r * 64 + u] ? (long long)(h_ts[r * 64 + u] - t0) : -1);
             fprintf(stderr, "\n");

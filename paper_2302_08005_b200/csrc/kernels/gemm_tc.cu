@@ -427,6 +427,19 @@ bool tc5::make_map_bf16(CUtensorMap* m, const void* base, long long inner, long 
     return make_map(m, base, inner, outer, ld, box_outer);
 }
 
+bool tc5::make_map_bf16_plain(CUtensorMap* m, const void* base, long long inner, long long outer, long long ld,
+                              int box_inner, int box_outer) {
+    auto fn = encode_fn();
+    if (!fn || (ld * 2) % 16 || ((uintptr_t)base & 15)) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+    cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
+    cuuint32_t box[2] = {(cuuint32_t)box_inner, (cuuint32_t)box_outer};
+    cuuint32_t es[2] = {1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, box_inner * 2 == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_NONE,
+              CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 bool tc5::make_map_u32(CUtensorMap* m, const void* base, long long inner, long long outer, long long ld, int box_inner,
                        int box_outer) {
     auto fn = encode_fn();

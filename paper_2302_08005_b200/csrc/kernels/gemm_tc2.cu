@@ -487,6 +487,7 @@ bool make_store_map(CUtensorMap* m, const void* base, bool f32, long long cols, 
 }
 
 int g_sms2 = 0;
+int g_sm_reserve = 0;
 
 // co-resident clusters of the persistent kernel (GPCs need not split into whole 4-CTA clusters)
 template <int BN, bool A_MN, bool B_MN, int PAIRS>
@@ -523,12 +524,16 @@ void launch2(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc
         attr = true;
     }
     if (!g_sms2) cudaDeviceGetAttribute(&g_sms2, cudaDevAttrMultiProcessorCount, 0);
-    const int max_clusters = max_clusters2<BN, A_MN, B_MN, PAIRS>();
+    int max_clusters = max_clusters2<BN, A_MN, B_MN, PAIRS>();
+    // SMs left to a concurrent collective (gemm_set_sm_reserve)
+    if (g_sm_reserve > 0) max_clusters = std::max(1, std::min(max_clusters, (g_sms2 - g_sm_reserve) / (2 * PAIRS)));
     const int clusters = std::min(sc.tiles(), max_clusters);
     k<<<clusters * 2 * PAIRS, 320, Cfg<BN>::SMEM, s>>>(ta, tb, tc, tx, ep, sc);
 }
 
 }  // namespace
+
+void gemm_set_sm_reserve(int n) { g_sm_reserve = std::max(0, n); }
 
 bool g_tc2_disabled = false;
 int g_tc2_bn = 0;  // cluster tile N: 0 default (256), 128 or 256 forced (tests)

@@ -47,6 +47,9 @@ int gemm_last_engine();
 void gemm_set_engine(int e);
 // 2-SM kernel cluster tile N: 0 default (256), 128 or 256 forced
 void gemm2_set_tile_n(int bn);
+// SMs the persistent 2-SM GEMM leaves free (for an NCCL collective running
+// concurrently on another stream); 0 = use every SM.
+void gemm_set_sm_reserve(int n);
 // Force the SIMT engine (tests compare the tcgen05 kernel against it).
 void gemm_force_simt(bool on);
 // workspace the tcgen05 split-K path may use for an (M x N) fp32 output

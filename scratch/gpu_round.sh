@@ -1,13 +1,12 @@
 #!/bin/bash
-# one GPU session: tests, bench, launch list, ncu full of the hot kernels
-cd $GRAFT_REPO_ROOT
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/smi.txt 2>&1
-cp MEASURED_PEAKS.json gpurun_out/ 2>/dev/null
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?" >> gpurun_out/bench.err
-timeout 600 python bench.py --no-cpu-baseline --profile --steps 5 > gpurun_out/bench_prof.json 2> gpurun_out/bench_prof.err
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file gpurun_out/launches.csv \
-    python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-graph > gpurun_out/ncu_list.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on \
-    -k regex:"k_gemm_tc|k_fa_fwd|k_fa_dkdv|k_fa_dq|k_dropout_mask" -c 6 -o gpurun_out/prof python profiles/ncu_targets.py > gpurun_out/ncu_full.log 2>&1
-echo done
+# one GPU session: tests, smoke, the driver's two bench commands, launch list
+mkdir -p gpurun_out
+O=gpurun_out
+{ nvidia-smi; nproc; df -h /tmp .; } > $O/env.txt 2>&1
+SB_PARITY_OUT=$O/parity timeout 2400 python -m pytest tests -m gpu -x -q -p no:cacheprovider > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/smoke.log
+df -h /tmp . > $O/df_before.txt
+/usr/bin/time -v timeout 1800 python3 bench.py --impl reference --gpus 1 --steps 20 --warmup 5 > $O/ref1.out 2> $O/ref1.err; echo "rc=$?" >> $O/ref1.err
+df -h /tmp . > $O/df_mid.txt
+/usr/bin/time -v timeout 1800 python3 bench.py --gpus 1 --steps 20 --warmup 5 > $O/n1.out 2> $O/n1.err; echo "rc=$?" >> $O/n1.err
+df -h /tmp . > $O/df_after.txt

@@ -131,3 +131,46 @@ def test_c3_width_bf16_vs_reference(case, ref_runs):
     assert worst_out <= BF16_OUT_TOL, f"output relL2 {worst_out:.3e}"
     assert worst_loss <= BF16_LOSS_TOL, f"loss rel {worst_loss:.3e}"
     assert worst_grad[0] <= BF16_GRAD_TOL, f"gradient {worst_grad[1]}: {worst_grad[0]:.3e}"
+
+
+# ---------------------------------------------------------------- depth scaling
+# The CPU reference affords L <= 2 at this width, so the bf16 error's growth with
+# depth is measured against this repo's fp32 path (SIMT fp32 GEMMs / attention,
+# itself equal to the reference within 1e-6 relative at every size the reference
+# runs: tests/test_parity_gpu.py) on the full-width model at L = 2, 8 and 24. The
+# measured per-depth errors go to $SB_PARITY_OUT (profiles/r2_bf16_parity.json)
+# and set the stated depth rule in DESIGN.md §2.
+DEPTH_TOL = {2: (2e-2, 2e-3, 5e-2), 8: (4e-2, 5e-3, 1e-1), 24: (6e-2, 1e-2, 2e-1)}
+
+
+@pytest.mark.parametrize("layers", sorted(DEPTH_TOL))
+def test_c3_width_bf16_vs_fp32_by_depth(layers):
+    m = sb.toy_bert(layers, C3W["hidden"], C3W["heads"], C3W["vocab"], C3W["batch"], C3W["seq"], C3W["p"])
+    s = sb.create_schedule(m, 1)
+    s.load_script(recipes.tp_script(layers, 1, ckpt_ratio=0.25))
+    applied = s.apply()
+    x = m.random_inputs(9)
+    res = {}
+    for dt in ("fp32", "bf16"):
+        ex = sb.Executor(applied, "train", 123, 1, dtype=dt)
+        outs = ex.forward(x)
+        res[dt] = (outs, ex.backward().params)
+        del ex
+    (o32, g32), (o16, g16) = res["fp32"], res["bf16"]
+    e_out = max(rel_l2(a, b) for a, b in zip(o16, o32))
+    l32 = sum(float(np.asarray(o, dtype=np.float64).sum()) for o in o32)
+    l16 = sum(float(np.asarray(o, dtype=np.float64).sum()) for o in o16)
+    e_loss = abs(l16 - l32) / abs(l32)
+    per = {}
+    for k, w in g32.items():
+        gs = group_scale(k, g32)
+        per[k] = (float(np.abs(np.asarray(g16[k]).ravel() - np.asarray(w).ravel()).max() / gs) if gs is not None
+                  else rel_l2(g16[k], w))
+    worst = max(per.items(), key=lambda kv: kv[1])
+    _record(f"depth_L{layers}_bf16_vs_fp32", {"layers": layers, **C3W, "out_rel_l2": e_out, "loss_rel": e_loss,
+                                               "worst_grad": worst[1], "worst_grad_name": worst[0],
+                                               "grad_rel_l2": per})
+    t_out, t_loss, t_grad = DEPTH_TOL[layers]
+    assert e_out <= t_out, e_out
+    assert e_loss <= t_loss, e_loss
+    assert worst[1] <= t_grad, worst

@@ -172,3 +172,47 @@ def test_cli_estimate_matches_reference(tmp_path):
     got = _cli("estimate", model_json, sch, "--world-size", 2, "--batch", 8)
     assert got.returncode == 0, got.stderr
     assert got.stdout == want
+
+
+def _ref_cli_train(tmp, model_json, sch, world, seed, mode, name):
+    """The reference executor's training step with `slapo run`'s seeds, dumped per rank
+    as SLD1 outputs / gradients (oracle/ref_driver.cpp --cli_train)."""
+    out = os.path.join(tmp, name)
+    os.makedirs(out, exist_ok=True)
+    args = [ref.DRIVER, "--model_json", model_json, "--world", str(world), "--seed", str(seed), "--mode", mode,
+            "--cli_train", out]
+    if sch:
+        args += ["--schedule", sch]
+    r = subprocess.run(args, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr
+    return out
+
+
+@pytest.mark.gpu
+@needs_ref
+@pytest.mark.parametrize("world,mode,dtype", [(1, "train", "fp32"), (2, "train", "fp32"), (2, "verify", "fp32"),
+                                              (2, "train", "bf16")])
+def test_cli_verify_train_against_reference(tmp_path, world, mode, dtype):
+    """`verify-train`: one scheduled training step on the GPU — every rank's outputs,
+    loss and parameter gradients — against the reference executor's dump of the same
+    step. fp32 at the north star's 1e-4; bf16 at the stated bf16 tolerances."""
+    tmp = str(tmp_path)
+    model_json, sch = _ref_model(tmp, world=world, dtype="f32")
+    refdir = _ref_cli_train(tmp, model_json, sch, world, 23, mode, "ref_train")
+    tol = ["--tol-out", 2e-2, "--tol-loss", 2e-3, "--tol-grad", 5e-2] if dtype == "bf16" else []
+    r = _cli("verify-train", model_json, sch, "--reference", refdir, "--world-size", world, "--seed", 23, "--mode",
+             mode, "--dtype", dtype, *tol)
+    assert r.returncode == 0, r.stdout + r.stderr
+    rep = dict(ln.split(None, 1) for ln in r.stdout.splitlines())
+    assert rep["pass"].strip() == "true" and int(rep["ranks"]) == world and int(rep["gradients"]) > 10
+    # a corrupted reference gradient is caught (exit code 3, the numeric-failure code)
+    names = open(os.path.join(refdir, "grads.r0.names")).read().split()
+    gs = dump.read_tensor_dump(os.path.join(refdir, "grads.r0.sld1"))
+    k = names.index(next(n for n in names if n.endswith("dense.weight")))
+    bad = [(t.copy(), d) for t, d in gs]
+    bad[k][0].reshape(-1)[0] += 10 * np.abs(bad[k][0]).max()
+    dump.write_tensor_dump(os.path.join(refdir, "grads.r0.sld1"), bad)
+    r = _cli("verify-train", model_json, sch, "--reference", refdir, "--world-size", world, "--seed", 23, "--mode",
+             mode, "--dtype", dtype, *tol)
+    assert r.returncode == 3 and "pass          false" in r.stdout, r.stdout + r.stderr
+    assert names[k] in r.stdout
