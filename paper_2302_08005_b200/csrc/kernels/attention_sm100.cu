@@ -394,41 +394,40 @@ __global__ void __launch_bounds__(F6_THREADS, F6_CTAS)
             }
         }
     } else if (warp == 5) {
-        if (lane == 0) {
-            // ------------------------------------------------ MMA issuer
-            constexpr uint32_t id_s = idesc_bf16(FT, KC6, false, false);  // S = Q K^T
-            constexpr uint32_t id_o = idesc_bf16(FT, FD, false, true);    // O += P V (V MN-major)
-            const uint32_t a0 = smem_u32(sQ);
-            int u = 0, n = 0;
-            for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++n) {
-                const int qb = n % F6_QBUF;
-                const uint32_t a = a0 + qb * F_TILE_BYTES;
-                mbar_wait(&q_full[qb], (n / F6_QBUF) & 1);
-                const int njt = CAUSAL ? (tile_qt(t) + 1) * (FT / KC6) : nj;
-                for (int j = 0; j < njt; ++j, ++u) {
-                    const int s = u % F6_NS;
-                    mbar_wait(&kv_full[s], (u / F6_NS) & 1);
-                    fence_after();
-                    // S(j) overwrites P(j-1) in TMEM: tcgen05.mma executes in issue order, so
-                    // PV(j-1) (issued first) has read it (the CUTLASS Blackwell FMHA relies on the same)
-                    const uint32_t bk = smem_u32(sK + s * F6_KV_BYTES);
-                    if (!(fa.dbg & 4))
+        // ------------------------------------------------ MMA issuer (whole warp, one elected
+        // lane issues: descriptors in uniform registers, no per-MMA divergence loop)
+        constexpr uint32_t id_s = idesc_bf16(FT, KC6, false, false);  // S = Q K^T
+        constexpr uint32_t id_o = idesc_bf16(FT, FD, false, true);    // O += P V (V MN-major)
+        const uint32_t a0 = smem_u32(sQ), k0 = smem_u32(sK), v0 = smem_u32(sV);
+        int u = 0, n = 0;
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++n) {
+            const int qb = n % F6_QBUF;
+            const uint64_t dq = desc_kmajor(a0 + qb * F_TILE_BYTES, 0);
+            mbar_wait(&q_full[qb], (n / F6_QBUF) & 1);
+            const int njt = CAUSAL ? (tile_qt(t) + 1) * (FT / KC6) : nj;
+            for (int j = 0; j < njt; ++j, ++u) {
+                const int s = u % F6_NS;
+                mbar_wait(&kv_full[s], (u / F6_NS) & 1);
+                fence_after();
+                // S(j) overwrites P(j-1) in TMEM: tcgen05.mma executes in issue order, so
+                // PV(j-1) (issued first) has read it (the CUTLASS Blackwell FMHA relies on the same)
+                if (!(fa.dbg & 4)) {
+                    const uint64_t dk = desc_kmajor(k0 + s * F6_KV_BYTES, 0);
 #pragma unroll
-                        for (int kk = 0; kk < FD / 16; ++kk)
-                            mma_ss(tmem, desc_kmajor(a, kk), desc_kmajor(bk, kk), id_s, kk > 0);
-                    mma_commit(s_full);
-                    if (j == njt - 1) mma_commit(&q_empty[qb]);  // last read of this tile's Q
-                    if (j == 0 && n > 0) mbar_wait(o_free, (n - 1) & 1);  // previous epilogue read O
-                    mbar_wait(p_full, u & 1);
-                    fence_after();
-                    const uint32_t bv = smem_u32(sV + s * F6_KV_BYTES);
-                    if (!(fa.dbg & 4))
-#pragma unroll
-                        for (int kk = 0; kk < KC6 / 16; ++kk)
-                            mma_ts(tmem + 64, tmem + kk * 8, desc_mnmajor(bv, kk), id_o, (j | kk) != 0);
-                    mma_commit(o_done);
-                    mma_commit(&kv_empty[s]);
+                    for (int kk = 0; kk < FD / 16; ++kk) mma_ss_w(tmem, dq + 2 * kk, dk + 2 * kk, id_s, kk);
                 }
+                mma_commit_w(s_full);
+                if (j == njt - 1) mma_commit_w(&q_empty[qb]);  // last read of this tile's Q
+                if (j == 0 && n > 0) mbar_wait(o_free, (n - 1) & 1);  // previous epilogue read O
+                mbar_wait(p_full, u & 1);
+                fence_after();
+                if (!(fa.dbg & 4)) {
+                    const uint64_t dv = desc_mnmajor(v0 + s * F6_KV_BYTES, 0);
+#pragma unroll
+                    for (int kk = 0; kk < KC6 / 16; ++kk) mma_ts_w(tmem + 64, tmem + kk * 8, dv + 128 * kk, id_o, j | kk);
+                }
+                mma_commit_w(o_done);
+                mma_commit_w(&kv_empty[s]);
             }
         }
     } else {
@@ -477,7 +476,7 @@ __global__ void __launch_bounds__(F6_THREADS, F6_CTAS)
                             if (c * 32 + e > kmax) sv[e] = __float_as_uint(-INFINITY);
                     }
 #pragma unroll
-                    for (int e = 0; e < 32; ++e) mx = fmaxf(mx, __uint_as_float(sv[e]));
+                    for (int e = 0; e < 32; e += 2) mx = fmax3(mx, __uint_as_float(sv[e]), __uint_as_float(sv[e + 1]));
                 }
                 mx *= fa.c;
                 if (j == 0) m_used = mx;
@@ -500,7 +499,8 @@ __global__ void __launch_bounds__(F6_THREADS, F6_CTAS)
                     }
                 }
                 // pass 2: P = exp2(S*c - m_used) * keep -> TMEM (bf16 pairs over S's first 32 columns)
-                float lc = 0.f;
+                float2 lc2 = make_float2(0.f, 0.f);
+                const float2 c2 = make_float2(fa.c, fa.c), nm2 = make_float2(-m_used, -m_used);
 #pragma unroll
                 for (int c = 0; c < 2; ++c) {
                     const uint32_t mword = c == 0 ? mw.x : mw.y;
@@ -513,17 +513,18 @@ __global__ void __launch_bounds__(F6_THREADS, F6_CTAS)
                             if (c * 32 + e > kmax) sv[e] = __float_as_uint(-INFINITY);
                     }
 #pragma unroll
-                    for (int e = 0; e < 16; ++e) {
-                        float p0 = ex2f(fmaf(__uint_as_float(sv[2 * e]), fa.c, -m_used));
-                        float p1 = ex2f(fmaf(__uint_as_float(sv[2 * e + 1]), fa.c, -m_used));
-                        lc += p0 + p1;  // the normaliser counts every probability (dropout acts after softmax)
-                        p0 = ((mword >> (2 * e)) & 1) ? p0 : 0.f;
-                        p1 = ((mword >> (2 * e + 1)) & 1) ? p1 : 0.f;
-                        pk[e] = pack_bf16(p0, p1);
+                    for (int e = 0; e < 16; ++e) {  // element pairs on the packed-fp32 pipe
+                        const float2 a =
+                            ffma2(make_float2(__uint_as_float(sv[2 * e]), __uint_as_float(sv[2 * e + 1])), c2, nm2);
+                        float2 p = make_float2(ex2f(a.x), ex2f(a.y));
+                        lc2 = fadd2(lc2, p);  // the normaliser counts every probability (dropout acts after softmax)
+                        p.x = ((mword >> (2 * e)) & 1) ? p.x : 0.f;
+                        p.y = ((mword >> (2 * e + 1)) & 1) ? p.y : 0.f;
+                        pk[e] = pack_bf16(p.x, p.y);
                     }
                     tmem_st16(t_row + c * 16, pk);
                 }
-                l += lc;
+                l += lc2.x + lc2.y;
                 tmem_st_wait();
                 fence_before();
                 __syncwarp();

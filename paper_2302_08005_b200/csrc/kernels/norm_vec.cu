@@ -1,3 +1,4 @@
+#include <cstdlib>
 // Vectorised LayerNorm family for rows of n = 32 * VEC * CPL elements: one
 // warp per row, 16-byte loads/stores, the whole row in registers (single HBM
 // read of every input), fp32 statistics. Backward keeps the per-column
@@ -591,6 +592,11 @@ bool with_cpl(int n, F&& f) {
 }
 
 bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
+// SB_LN_NARROW=1: one warp per row everywhere (A/B and diagnostics)
+bool ln_narrow() {
+    static const bool on = getenv("SB_LN_NARROW") && atoi(getenv("SB_LN_NARROW"));
+    return on;
+}
 
 }  // namespace
 
@@ -626,7 +632,7 @@ bool bdrln_fwd_vec(const void* partial, const void* bias, const void* res, const
                 constexpr int CPL = decltype(cc)::value;
                 if constexpr (CPL % 4 == 0) {
                     // 4 warps per row, 16-warp blocks (4 rows per block)
-                    if (thr == 0 || keep) {
+                    if ((thr == 0 || keep) && !ln_narrow()) {
                         // 4 warps per row, persistent grid of two 16-warp blocks per SM (<= 64 registers)
                         const unsigned blocks = (unsigned)std::min<i64>(296, (rows + 3) / 4);
                         k_bdrln_fwd_w<T, CPL, 4, 1><<<blocks, 512, 0, s>>>(
@@ -667,7 +673,7 @@ bool ln_bwd_vec(int mode, const void* x, const float* mean, const float* rstd, c
                                                      ncol, gres_acc);
                 };
                 if constexpr (CPL % 4 == 0) {
-                  if (thr == 0 || keep) {
+                  if ((thr == 0 || keep) && !ln_narrow()) {
                     // 4 warps per row, 16-warp blocks, two blocks per SM
                     constexpr int WPR = 4;
                     const size_t sm2 = (size_t)16 * ncol * (n / WPR) * 4 + 2 * 16 * 2 * 4;

@@ -1,0 +1,16 @@
+import sys, os, numpy as np
+sys.path.insert(0, '.')
+import paper_2302_08005_b200 as sb
+from paper_2302_08005_b200 import recipes
+def rl2(a, b):
+    a = np.asarray(a, dtype=np.float64).ravel(); b = np.asarray(b, dtype=np.float64).ravel()
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+def run(L, H, heads, V, S, dt, mode="train", B=1):
+    m = sb.toy_bert(L, H, heads, V, B, S, 0.1)
+    s = sb.create_schedule(m, 1); s.load_script(recipes.tp_script(L, 1, ckpt_ratio=0.25))
+    ex = sb.Executor(s.apply(), mode, 123, 1, dtype=dt)
+    o = ex.forward(m.random_inputs(9))[0]
+    return o, ex.backward().params
+o32, g32 = run(4, 1024, 16, 30528, 512, "fp32")
+o16, g16 = run(4, 1024, 16, 30528, 512, "bf16")
+print(os.environ.get("SB_LN_NARROW"), "out", rl2(o16, o32), "emb", rl2(g16['embeddings.weight'], g32['embeddings.weight']), flush=True)
