@@ -279,7 +279,7 @@ void attn_fwd(const Attn& a, cudaStream_t s) {
 void attn_bwd(const Attn& a, const void* dout, i64 ld_do, void* dq, void* dk, void* dv, i64 ld_dq, i64 ld_dk, i64 ld_dv,
               void* ws, cudaStream_t s) {
     float* delta = (float*)ws;
-    if (g_attn_max_engine == 0 && !a.causal && attn_bwd_sm100_try(a, dout, ld_do, dq, dk, dv, ld_dq, ld_dk, ld_dv, ws, s)) {
+    if (g_attn_max_engine == 0 && attn_bwd_sm100_try(a, dout, ld_do, dq, dk, dv, ld_dq, ld_dk, ld_dv, ws, s)) {
         g_attn_last_bwd = 3;
         return;
     }

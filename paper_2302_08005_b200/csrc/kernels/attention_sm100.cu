@@ -1109,6 +1109,26 @@ __device__ __forceinline__ void warp_tile_tma(uint8_t* stage, const CUtensorMap*
     }
 }
 
+// step u -> (key block j, query block i): all nj x nj pairs, or for causal attention only
+// the i >= j ones (queries at or after the keys; the rest is masked out entirely)
+template <bool CAUSAL>
+__device__ __forceinline__ void step_ji(int u, int nj, int& j, int& i) {
+    if (!CAUSAL) {
+        j = u / nj;
+        i = u % nj;
+        return;
+    }
+    j = 0;
+    int cnt = nj;
+    while (u >= cnt) {
+        u -= cnt;
+        ++j;
+        --cnt;
+    }
+    i = j + u;
+}
+
+template <bool CAUSAL>
 __global__ void __launch_bounds__(B7_WARPS * 32, 1)
     k_fa7_bwd(const __grid_constant__ CUtensorMap tK, const __grid_constant__ CUtensorMap tV,
               const __grid_constant__ CUtensorMap tQ, const __grid_constant__ CUtensorMap tdO,
@@ -1139,7 +1159,8 @@ __global__ void __launch_bounds__(B7_WARPS * 32, 1)
     uint32_t* tslot = (uint32_t*)(ds_full + 2);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    const int S = ba.S, nj = S / FT, nsteps = nj * nj;
+    const int S = ba.S, nj = S / FT, nsteps = CAUSAL ? nj * (nj + 1) / 2 : nj * nj;
+    auto first_i = [&](int j) { return CAUSAL ? j : 0; };  // first query block of key block j
     const int h = blockIdx.x, b = blockIdx.y;
     const long long bh = (long long)b * ba.nh + h;
     const int row_base = b * S;
@@ -1194,10 +1215,11 @@ __global__ void __launch_bounds__(B7_WARPS * 32, 1)
             // K/V of block j+1 go out before the stage of step (j, min(2, nj-1)): late
             // enough that V_j has been copied into TMEM (so the wait is short), early
             // enough that block j+1 never waits for them
-            const int kv_at = nj > 2 ? 2 : nj - 1;
             for (int u = 0; u < nsteps; ++u) {
-                const int j = u / nj, i = u % nj;
-                if (i == kv_at && j + 1 < nj) load_kv(j + 1);
+                int j, i;
+                step_ji<CAUSAL>(u, nj, j, i);
+                const int bl = nj - first_i(j);  // steps of key block j
+                if (i - first_i(j) == (bl > 2 ? 2 : bl - 1) && j + 1 < nj) load_kv(j + 1);
                 const int s = u % B7_NST;
                 uint8_t* st = sStage + s * B7_STAGE;
                 if (TS7) ba.ts[14 * 64 + u] = gtime();
@@ -1222,10 +1244,12 @@ __global__ void __launch_bounds__(B7_WARPS * 32, 1)
         const bool mm = !(ba.dbg & 4);
         const uint32_t stage0 = smem_u32(sStage);
         auto issue_sdp = [&](int u, int hh) {
-            const int j = u / nj, i = u % nj, s = u % B7_NST;
+            int j, i;
+            step_ji<CAUSAL>(u, nj, j, i);
+            const int s = u % B7_NST;
             const uint32_t aQ = stage0 + s * B7_STAGE + hh * (F_TILE_BYTES / 2);
             if (hh == 0) {
-                if (i == 0) mbar_wait(kv_tmem, j & 1);  // K_j / V_j in TMEM
+                if (i == first_i(j)) mbar_wait(kv_tmem, j & 1);  // K_j / V_j in TMEM
                 mbar_wait(&st_full[s], (u / B7_NST) & 1);
                 fence_after();
             }
@@ -1243,22 +1267,25 @@ __global__ void __launch_bounds__(B7_WARPS * 32, 1)
         issue_sdp(0, 0);
         issue_sdp(0, 1);
         for (int u = 0; u < nsteps; ++u) {
-            const int j = u / nj, i = u % nj, s = u % B7_NST;
+            int j, i;
+            step_ji<CAUSAL>(u, nj, j, i);
+            const int s = u % B7_NST;
+            const int acc0 = i != first_i(j);  // dK / dV accumulate after the block's first step
             const uint32_t aQ = stage0 + s * B7_STAGE, adO = aQ + F_TILE_BYTES;
 #pragma unroll 1
             for (int hh = 0; hh < 2; ++hh) {
                 mbar_wait(&sm_done[hh], u & 1);
-                if (hh == 0 && i == 0 && j > 0) mbar_wait(acc_free, (j - 1) & 1);  // dK/dV of block j-1 drained
+                if (hh == 0 && i == first_i(j) && j > 0) mbar_wait(acc_free, (j - 1) & 1);  // dK/dV of block j-1 drained
                 if (TS7 && lane == 0) ba.ts[hh * 64 + u] = gtime();
                 fence_after();
                 if (mm) {
                     const uint64_t bdo = desc_mnmajor(adO, hh * 4), bq = desc_mnmajor(aQ, hh * 4);
 #pragma unroll
                     for (int k4 = 0; k4 < 4; ++k4)  // dV += Z^T_half dO_half (Z^T: 8 cols per 16 queries)
-                        mma_ts_w(tmem + 256, tmem + hh * 64 + k4 * 16, bdo + 128 * k4, id_kv, i | hh | k4);
+                        mma_ts_w(tmem + 256, tmem + hh * 64 + k4 * 16, bdo + 128 * k4, id_kv, acc0 | hh | k4);
 #pragma unroll
                     for (int k4 = 0; k4 < 4; ++k4)  // dK += dS^T_half Q_half
-                        mma_ts_w(tmem + 320, tmem + hh * 64 + k4 * 16 + 8, bq + 128 * k4, id_kv, i | hh | k4);
+                        mma_ts_w(tmem + 320, tmem + hh * 64 + k4 * 16 + 8, bq + 128 * k4, id_kv, acc0 | hh | k4);
                 }
                 if (hh == 1) {
                     mma_commit_w(&st_empty[s]);  // Q, dO, lse, delta, keep bits of this step are no longer read
@@ -1275,7 +1302,8 @@ __global__ void __launch_bounds__(B7_WARPS * 32, 1)
         const bool mm = !(ba.dbg & 4);
         const uint32_t ds0 = smem_u32(sDS), k0 = smem_u32(sK);
         for (int u = 0; u < nsteps; ++u) {
-            const int j = u / nj, i = u % nj;
+            int j, i;
+            step_ji<CAUSAL>(u, nj, j, i);
             mbar_wait(&ds_full[u & 1], (u >> 1) & 1);  // dS^T(u) written (both halves)
             if (u > 0) mbar_wait(dq_free, (u - 1) & 1);  // dQ of the previous step has left TMEM
             if (TS7 && lane == 0) ba.ts[2 * 64 + u] = gtime();
@@ -1353,7 +1381,9 @@ __global__ void __launch_bounds__(B7_WARPS * 32, 1)
         };
         kv_to_tmem(0);
         for (int u = 0; u < nsteps; ++u) {
-            const int j = u / nj, i = u % nj, s = u % B7_NST;
+            int j, i;
+            step_ji<CAUSAL>(u, nj, j, i);
+            const int s = u % B7_NST;
             const float* lse_s = (const float*)(sStage + s * B7_STAGE + 2 * F_TILE_BYTES);
             const float* dl_s = lse_s + FT;
             uint8_t* ds_buf = sDS + (u & 1) * 2 * F_TILE_BYTES;
@@ -1379,6 +1409,11 @@ __global__ void __launch_bounds__(B7_WARPS * 32, 1)
                                     (q0 & 16)
                               : 0xFFFFu;
                 tmem_ld_wait();
+                if (CAUSAL && i == j) {  // diagonal block: key k sees queries q >= k only
+#pragma unroll
+                    for (int e = 0; e < 16; ++e)
+                        if (q0 + e < k) sv[e] = __float_as_uint(-INFINITY);
+                }
                 uint32_t zk[8], dk[8];
 #pragma unroll
                 for (int e4 = 0; e4 < 4; ++e4) {
@@ -1428,7 +1463,7 @@ __global__ void __launch_bounds__(B7_WARPS * 32, 1)
                 if (TS7 && warp == 0 && lane == 0) ba.ts[(4 + 2 * hh) * 64 + u] = gtime();
                 if (TS7 && lane == 0 && u == 5) ba.ts[(8 + hh) * 64 + warp] = gtime();
                 if (TS7 && lane == 0 && u == 6) ba.ts[(10 + hh) * 64 + warp] = gtime();
-                if (hh == 0 && i == 0 && j > 0) drain_kv(j - 1);  // TMEM dK/dV free before dV/dK of block j start
+                if (hh == 0 && i == first_i(j) && j > 0) drain_kv(j - 1);  // TMEM dK/dV free before dV/dK of block j start
             }
         }
         drain_kv(nj - 1);
@@ -1442,12 +1477,13 @@ __global__ void __launch_bounds__(B7_WARPS * 32, 1)
         const int q4 = warp & 3, r = q4 * 32 + lane;
         const uint32_t t_row = tmem + ((uint32_t)(q4 * 32) << 16) + 384;
         for (int u = 0; u < nsteps; ++u) {
-            const int j = u / nj, i = u % nj;
+            int j, i;
+            step_ji<CAUSAL>(u, nj, j, i);
             // thread-major: float4 v of query row r of block i at ((bh*nj + i)*16 + v)*128 + r
             float4* acc = (float4*)ba.dqacc + ((bh * nj + i) * 16) * FT + r;
-            const bool last = j == nj - 1, dbg = ba.dbg & 2;
+            const bool last = j == (CAUSAL ? i : nj - 1), dbg = ba.dbg & 2;  // query block i's last key block
             float f[32];
-            if (last && nj > 1 && !dbg) {  // the final partial sum's first half, before dQ(u) lands
+            if (last && j > 0 && !dbg) {  // the final partial sum's first half, before dQ(u) lands
 #pragma unroll
                 for (int v = 0; v < 8; ++v) {
                     const float4 a4 = __ldcg(acc + v * FT);
@@ -1484,7 +1520,7 @@ __global__ void __launch_bounds__(B7_WARPS * 32, 1)
                     }
                     continue;
                 }
-                if (pss == 1 && nj > 1) {
+                if (pss == 1 && j > 0) {
 #pragma unroll
                     for (int v = 0; v < 8; ++v) {
                         const float4 a4 = __ldcg(acc + (8 + v) * FT);
@@ -1611,7 +1647,8 @@ size_t attn_bwd_sm100_workspace(i64 B, i64 S, i64 nh, i64 hd) {
 
 bool attn_bwd_sm100_try(const Attn& a, const void* dout, i64 ld_do, void* dq, void* dk, void* dv, i64 ld_dq, i64 ld_dk,
                         i64 ld_dv, void* ws, cudaStream_t s) {
-    if (a.causal || !bwd_fits(a, dout, ld_do, ld_dq, ld_dk, ld_dv)) return false;
+    if (!bwd_fits(a, dout, ld_do, ld_dq, ld_dk, ld_dv)) return false;
+    if (a.causal && getenv("SB_ATTN_BWD") && atoi(getenv("SB_ATTN_BWD")) == 5) return false;  // fa5: no causal
     CUtensorMap tq, tk, tv, tdo, tm;
     const long long rows = a.B * a.S, cols = a.nh * FD;
     if (!make_map_bf16(&tq, a.q, cols, rows, a.ld_q, FT) || !make_map_bf16(&tk, a.k, cols, rows, a.ld_k, FT) ||
@@ -1643,7 +1680,8 @@ bool attn_bwd_sm100_try(const Attn& a, const void* dout, i64 ld_do, void* dq, vo
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k_fa5_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, B_SMEM);
-        cudaFuncSetAttribute(k_fa7_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, B7_SMEM);
+        cudaFuncSetAttribute(k_fa7_bwd<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, B7_SMEM);
+        cudaFuncSetAttribute(k_fa7_bwd<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, B7_SMEM);
         attr = true;
     }
     dim3 grid((unsigned)a.nh, (unsigned)a.B);
@@ -1653,7 +1691,8 @@ bool attn_bwd_sm100_try(const Attn& a, const void* dout, i64 ld_do, void* dq, vo
         if (!make_map_bf16_plain(&tdq, dq, cols, rows, ld_dq, 32, 32) || !make_map_bf16_plain(&tdk, dk, cols, rows, ld_dk, 32, 32) ||
             !make_map_bf16_plain(&tdv, dv, cols, rows, ld_dv, 32, 32))
             throw std::runtime_error("attention backward: output tensor maps rejected");
-        k_fa7_bwd<<<grid, B7_WARPS * 32, B7_SMEM, s>>>(tk, tv, tq, tdo, tm, tdq, tdk, tdv, ba);
+        if (a.causal) k_fa7_bwd<true><<<grid, B7_WARPS * 32, B7_SMEM, s>>>(tk, tv, tq, tdo, tm, tdq, tdk, tdv, ba);
+        else k_fa7_bwd<false><<<grid, B7_WARPS * 32, B7_SMEM, s>>>(tk, tv, tq, tdo, tm, tdq, tdk, tdv, ba);
     }
     SBK_CHECK_LAUNCH();
     if (ba.ts) {

@@ -43,3 +43,10 @@ for eng in (0, 1):
     tf = t(fwdc)
     print(f"causal engine cap {eng}: used {L.sb_attn_engine(0)} fwd {tf:.3f} ms ({unit/tf*1e3:.0f} TF/s useful)")
 L.sb_attn_set_engine(0)
+def bwdc(): L.sb_attn_bwd_ex(P(q), P(k), P(v), P(o), 3*H, H, P(lse), P(do), P(g[..., :H]), P(g[..., H:2*H]), P(g[..., 2*H:]), P(delta), B, S, nh, hd, hd**-0.5, 1, 2, p, 1, P(bits), 0, 1, None)
+fwdc()
+for eng in (0, 1):
+    L.sb_attn_set_engine(eng)
+    tb = t(bwdc)
+    print(f"causal engine cap {eng}: used {L.sb_attn_engine(1)} bwd {tb:.3f} ms ({2.5*unit/tb*1e3:.0f} TF/s useful)")
+L.sb_attn_set_engine(0)

@@ -2,7 +2,7 @@ import os, sys, torch
 sys.path.insert(0, '.')
 exec(open('scratch/attn_bench.py').read().split("def t(")[0])
 fwd(); torch.cuda.synchronize()
-for d in ("0", "1", "4", "5", "7", "13", "21", "37", "69", "127", "2", "8", "16", "32", "64"):
+for d in ("127", "0"):
     os.environ["SB_ATTN_DBG"] = d
     bwd(); torch.cuda.synchronize()
     a, b = torch.cuda.Event(True), torch.cuda.Event(True)
