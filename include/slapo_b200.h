@@ -34,6 +34,11 @@ int sb_version(void);
 int sb_model_toy_bert(int layers, int64_t hidden, int64_t heads, int64_t vocab, int64_t batch, int64_t seq,
                       double dropout_p, sb_model** out);
 int sb_model_tp_two_linear(int64_t hidden, int64_t inner, int64_t batch, sb_model** out);
+/* f2 (no reference fixture): GPT-Neo-style pre-LN causal decoder in the reference's module
+   vocabulary (csrc/host/model_io.cpp gpt_neo); its oracle is the documented extension
+   oracle/causal_ext.py (a `causal` attr on softmax, proj/src/executor.cpp:907-916) */
+int sb_model_gpt_neo(int layers, int64_t hidden, int64_t heads, int64_t vocab, int64_t batch, int64_t seq,
+                     double dropout_p, sb_model** out);
 int sb_model_fig3c(sb_model** out);
 int sb_model_ffn_stack(int n, int64_t hidden, int64_t batch, sb_model** out);
 /* load_model / save_model — proj/include/slapo/model_io.hpp:16-23 */

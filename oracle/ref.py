@@ -19,6 +19,9 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 DRIVER = os.path.join(HERE, "_ref", "slapo_ref_driver")
+# the documented causal extension (oracle/causal_ext.py): the reference executor with a
+# `causal` attr on softmax; identical to DRIVER on models without that attr
+DRIVER_CAUSAL = os.path.join(HERE, "_ref", "slapo_ref_driver_causal")
 
 
 def available() -> bool:
@@ -103,14 +106,16 @@ class RefRun:
 
 
 def run(model: str = "toy_bert", schedule: Optional[str] = None, outdir: Optional[str] = None, timeout: int = 600,
-        **kw) -> RefRun:
+        causal: bool = False, **kw) -> RefRun:
     """kw: layers, hidden, heads, vocab, batch, seq, p, dtype, world, mode, seed, input_seed,
-    backward, dump_params, tp_hidden, tp_inner, tp_batch, repeat, model_json (path)."""
-    if not available():
-        raise RuntimeError(f"oracle driver missing: build it with `make -C oracle` ({DRIVER})")
+    backward, dump_params, tp_hidden, tp_inner, tp_batch, repeat, model_json (path).
+    causal=True runs the causal extension's driver (needed for decoder models)."""
+    drv = DRIVER_CAUSAL if causal else DRIVER
+    if not os.path.exists(drv):
+        raise RuntimeError(f"oracle driver missing: build it with `make -C oracle` ({drv})")
     owned = outdir is None
     outdir = outdir or tempfile.mkdtemp(prefix="sbref_")
-    args = [DRIVER, "--model", model, "--out", outdir]
+    args = [drv, "--model", model, "--out", outdir]
     sched_file = None
     if schedule:
         if os.path.exists(schedule):

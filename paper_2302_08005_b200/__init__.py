@@ -3,7 +3,7 @@
 Python mirror of the reference's C++ interface, bound to the C ABI of
 ``libslapo_b200.so`` (include/slapo_b200.h):
 
-* models: ``toy_bert``, ``tp_two_linear``, ``fig3c_exact``, ``ffn_stack``
+* models: ``toy_bert``, ``gpt_neo`` (f2), ``tp_two_linear``, ``fig3c_exact``, ``ffn_stack``
   (proj/tests/support/fixtures.hpp:21-38), ``Model.from_json`` (model_io.hpp:16);
 * ``create_schedule`` / ``Schedule`` with ``at``, ``trace``, ``replace``, ``shard``,
   ``sync``, ``checkpoint``, ``define_pattern``, ``fuse``, ``pipeline_split``,
@@ -53,6 +53,7 @@ def _sig(name, *argtypes):
 _lib.sb_last_error.restype = _c.c_char_p
 for _n, _a in {
     "sb_model_toy_bert": (_c.c_int, _i64, _i64, _i64, _i64, _i64, _c.c_double, _c.POINTER(_P)),
+    "sb_model_gpt_neo": (_c.c_int, _i64, _i64, _i64, _i64, _i64, _c.c_double, _c.POINTER(_P)),
     "sb_model_tp_two_linear": (_i64, _i64, _i64, _c.POINTER(_P)),
     "sb_model_fig3c": (_c.POINTER(_P),),
     "sb_model_ffn_stack": (_c.c_int, _i64, _i64, _c.POINTER(_P)),
@@ -232,6 +233,12 @@ class Model:
 
 def toy_bert(layers=24, hidden=8, heads=2, vocab=28, batch=4, seq=4, dropout_p=0.1) -> Model:
     return Model._make(_lib.sb_model_toy_bert, layers, hidden, heads, vocab, batch, seq, dropout_p)
+
+
+def gpt_neo(layers=24, hidden=8, heads=2, vocab=28, batch=4, seq=4, dropout_p=0.1) -> Model:
+    """GPT-Neo-style pre-LN causal decoder (f2, BASELINE.json configs[3]); no reference
+    fixture exists — its oracle is the documented causal extension (oracle/causal_ext.py)."""
+    return Model._make(_lib.sb_model_gpt_neo, layers, hidden, heads, vocab, batch, seq, dropout_p)
 
 
 def tp_two_linear(hidden=8, inner=16, batch=4) -> Model:

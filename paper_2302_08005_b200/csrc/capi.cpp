@@ -108,6 +108,20 @@ int sb_model_toy_bert(int layers, int64_t hidden, int64_t heads, int64_t vocab, 
         *out = new sb_model{toy_bert(c)};
     });
 }
+int sb_model_gpt_neo(int layers, int64_t hidden, int64_t heads, int64_t vocab, int64_t batch, int64_t seq, double p,
+                     sb_model** out) {
+    return guard([&] {
+        DecoderConfig c;
+        c.layers = layers;
+        c.hidden = hidden;
+        c.heads = heads;
+        c.vocab = vocab;
+        c.batch = batch;
+        c.seq = seq;
+        c.dropout_p = p;
+        *out = new sb_model{gpt_neo(c)};
+    });
+}
 int sb_model_tp_two_linear(int64_t hidden, int64_t inner, int64_t batch, sb_model** out) {
     return guard([&] { *out = new sb_model{tp_two_linear(hidden, inner, batch)}; });
 }

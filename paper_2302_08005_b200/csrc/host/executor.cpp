@@ -984,7 +984,8 @@ public:
             case K::Softmax: {
                 i64 outer, n, inner;
                 axis_split(V(r, op.in[0]), op.axis, outer, n, inner);
-                sbk::softmax_fwd(fp(r, op.in[0]), fp(r, op.out[0]), cdt, outer, n, inner, stream);
+                sbk::softmax_fwd(fp(r, op.in[0]), fp(r, op.out[0]), cdt, outer, n, inner, stream,
+                                 op.causal ? V(r, op.in[0]).shape[V(r, op.in[0]).shape.size() - 2] : 0);
                 break;
             }
             case K::Matmul: {

@@ -422,14 +422,9 @@ struct Lowerer {
         return out;
     }
 
-    // the reference's composed attention graph (no mask op exists in its op set, so a causal
-    // EfficientAttention has no composed form: it needs the flash kernel's shapes)
-    static Module composed_attention(const Module& m) {
-        if (get_flag(m.attrs, "causal"))
-            throw Error("causal EfficientAttention runs only on the fused flash-attention path "
-                        "(rank-3 q/k/v of equal shape, hidden % head_dim == 0)");
-        return attention_reference_graph(m);
-    }
+    // the reference's composed attention graph (a causal EfficientAttention keeps its mask as
+    // the softmax's causal attr, as in the oracle extension)
+    static Module composed_attention(const Module& m) { return attention_reference_graph(m); }
 
     Val flash_attention(const Module& m, const std::string& path, const std::vector<Val>& args) {
         i64 hd = get_int(m.attrs, "head_dim").value_or(0);
@@ -712,6 +707,9 @@ struct Lowerer {
             op.in = {x};
             op.out = {y};
             op.axis = (int)(ax < 0 ? ax + r : ax);
+            // the oracle extension's causal softmax (oracle/causal_ext.py): keys k <= q + (Sk - Sq)
+            op.causal = get_flag(at, "causal");
+            if (op.causal && (op.axis != r - 1 || r < 2)) throw Error("causal softmax must run over the last axis of a rank >= 2 input");
             emit(op);
             return Val{{y}, false};
         }

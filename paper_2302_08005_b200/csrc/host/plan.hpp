@@ -85,7 +85,7 @@ struct Op {
     double p = 0, scale = 1, eps = 1e-5;
     u64 s1 = 0, thr = 0;  // dropout: s1 = hash_combine(hash_combine(seed, node_seed), 0xd0)
     bool dropout = false, bias_on = true, bias_grad = true, has_bias = false, qkv = false, allreduce = false;
-    bool causal = false;  // FlashAttn: EfficientAttention attr "causal" (f2; not in the reference op set)
+    bool causal = false;  // FlashAttn / Softmax: attr "causal" (f2; the oracle extension oracle/causal_ext.py)
     bool affine = true;
     int axis = -1;
     std::vector<int> perm;

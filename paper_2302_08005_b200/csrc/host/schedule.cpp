@@ -294,11 +294,14 @@ std::vector<Match> find_module_calls(const Graph& g, const std::string& glob) {
 }
 
 // ===================================================================== library
-Module make_attention_core(i64 hd, double p, u64 seed) {
+Module make_attention_core(i64 hd, double p, u64 seed, bool causal) {
     Module core;
     core.attrs["head_dim"] = hd;
     core.attrs["p"] = p;
     core.attrs["seed"] = (i64)seed;
+    // f2 (decoder): the oracle extension's causal softmax (oracle/causal_ext.py), also
+    // carried by an EfficientAttention that replaces this core (attrs are copied)
+    if (causal) core.attrs["causal"] = (i64)1;
     double scale = 1.0 / std::sqrt((double)hd);
     GB b;
     int q = b.input(), k = b.input(), v = b.input();
@@ -310,7 +313,9 @@ Module make_attention_core(i64 hd, double p, u64 seed) {
     int kt = b.op("transpose", {kh}, {{"axes", std::vector<i64>{-2, -1}}});
     int s = b.op("matmul", {qh, kt});
     int sc = b.op("scale", {s}, {{"factor", scale}});
-    int a = b.op("softmax", {sc}, {{"axis", (i64)-1}});
+    Attrs smx{{"axis", (i64)-1}};
+    if (causal) smx["causal"] = (i64)1;
+    int a = b.op("softmax", {sc}, smx);
     int d = b.op("dropout", {a}, {{"p", p}, {"seed", (i64)seed}});
     int c = b.op("matmul", {d, vh});
     int back = b.op("transpose", {c}, {{"perm", std::vector<i64>{0, 2, 1, 3}}});
@@ -324,7 +329,7 @@ Module attention_reference_graph(const Module& ea) {
     if (hd <= 0) throw Error("EfficientAttention requires a positive head_dim attr");
     double p = get_double(ea.attrs, "p").value_or(0.0);
     i64 seed = get_int(ea.attrs, "seed").value_or(0);
-    Module m = make_attention_core(hd, p, (u64)seed);
+    Module m = make_attention_core(hd, p, (u64)seed, get_int(ea.attrs, "causal").value_or(0) != 0);
     if (auto sc = get_double(ea.attrs, "scale")) {
         for (auto& n : m.forward->nodes)
             if (n.kind == NK::CallOp && n.op == "scale") n.attrs["factor"] = *sc;

@@ -34,7 +34,7 @@ std::vector<int> escaping_values(const Graph& g, const std::vector<int>& nodes);
 void validate_pattern(const Graph& p);
 
 // --------------------------------------------------------------- library
-Module make_attention_core(i64 head_dim, double p, u64 seed);
+Module make_attention_core(i64 head_dim, double p, u64 seed, bool causal = false);
 Module make_qkv_composite(i64 hidden, u64 seed);
 Module build_fused_qkv(const Module& old_qkv);
 bool has_library_module(const std::string& n);
@@ -127,6 +127,14 @@ struct BertConfig {
     double dropout_p = 0.1;
 };
 Module toy_bert(const BertConfig& c);
+// f2: a GPT-Neo-style pre-LN decoder (causal attention) in the
+// reference's module vocabulary, runnable by the oracle extension (oracle/causal_ext.py)
+struct DecoderConfig {
+    int layers = 2;
+    i64 hidden = 8, heads = 2, vocab = 28, batch = 4, seq = 4;
+    double dropout_p = 0.1;
+};
+Module gpt_neo(const DecoderConfig& c);
 Module tp_two_linear(i64 hidden, i64 inner, i64 batch);
 Module fig3c_exact();
 Module ffn_stack(int n, i64 hidden, i64 batch);

@@ -289,31 +289,48 @@ __global__ void __launch_bounds__(FCfg<NT>::THREADS, NT == 1 ? 2 : 1)
 // (in-order tcgen05.mma execution); the next tile's first S overlaps this
 // tile's epilogue, and its first PV waits until the epilogue has read O.
 // Keep bits are read per row from the natural-layout mask one chunk ahead.
+// Head dim D = 64 or 128 (template): a D = 128 row is two 64-column (128-byte)
+// swizzle panels, each its own TMA box; S = Q K^T takes its 8 K16 steps across
+// both panels, O += P V is one M128 N128 MMA per K16 step (the two V panels are
+// the two MN atoms of the B descriptor, LBO = one panel). TMEM S [0,64) + O
+// [64, 64 + D): 128 columns (four CTAs per SM) at D = 64, 256 (two) at D = 128 —
+// at D = 128 the chunk's MMA time (512 cycles) matches its exp2 time.
 constexpr int KC6 = 64;                      // keys per chunk
-constexpr int F6_KV_BYTES = KC6 * FD * 2;    // 8 KB
 constexpr int F6_NS = 2;                     // K/V stages
 constexpr int F6_THREADS = 192;
 constexpr int F6_MASK_BYTES = 2048;         // keep bits of 128 query rows x 128 keys (two chunks)
 #ifndef F6_CTAS
-#define F6_CTAS 4  // resident CTAs per SM
+#define F6_CTAS 4  // resident CTAs per SM (head dim 64)
 #endif
 #ifndef F6_QBUF
 #define F6_QBUF 1  // Q tile buffers (2: the next tile's Q loads while this tile runs)
 #endif
-constexpr int F6_SMEM = 1024 + F6_QBUF * F_TILE_BYTES + F6_NS * 2 * F6_KV_BYTES + 2 * F6_MASK_BYTES + 160;
+template <int D>
+struct F6 {
+    static constexpr int PANELS = D / 64;
+    static constexpr int Q_BYTES = FT * D * 2;      // 16 / 32 KB
+    static constexpr int KV_BYTES = KC6 * D * 2;    // 8 / 16 KB
+    static constexpr int Q_PANEL = FT * 128, KV_PANEL = KC6 * 128;
+    static constexpr int CTAS = D == 64 ? F6_CTAS : 2;
+    static constexpr uint32_t TCOLS = D == 64 ? 128 : 256;
+    static constexpr int SMEM = 1024 + F6_QBUF * Q_BYTES + F6_NS * 2 * KV_BYTES + 2 * F6_MASK_BYTES + 160;
+};
+constexpr int F6_KV_BYTES = F6<64>::KV_BYTES;
+constexpr int F6_SMEM = F6<64>::SMEM;
 constexpr float kLazy6 = 8.f;                // lazy rescale threshold (log2 units)
 
-template <bool CAUSAL>
-__global__ void __launch_bounds__(F6_THREADS, F6_CTAS)
+template <bool CAUSAL, int D = 64>
+__global__ void __launch_bounds__(F6_THREADS, F6<D>::CTAS)
     k_fa6_fwd(const __grid_constant__ CUtensorMap tQ, const __grid_constant__ CUtensorMap tK,
               const __grid_constant__ CUtensorMap tV, const __grid_constant__ CUtensorMap tM, FwdArgs fa,
               int ntiles) {
+    using C = F6<D>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024 - (tc5::smem_u32(smem_raw) & 1023)) & 1023);
-    uint8_t* sQ = smem;                          // [F6_QBUF][FT][FD]
-    uint8_t* sK = sQ + F6_QBUF * F_TILE_BYTES;   // [F6_NS][KC6][FD]
-    uint8_t* sV = sK + F6_NS * F6_KV_BYTES;      // [F6_NS][KC6][FD]
-    uint8_t* sMk = sV + F6_NS * F6_KV_BYTES;     // [2][128 rows][4 words]: keep bits of a chunk pair
+    uint8_t* sQ = smem;                          // [F6_QBUF][panel][FT][64]
+    uint8_t* sK = sQ + F6_QBUF * C::Q_BYTES;     // [F6_NS][panel][KC6][64]
+    uint8_t* sV = sK + F6_NS * C::KV_BYTES;      // [F6_NS][panel][KC6][64]
+    uint8_t* sMk = sV + F6_NS * C::KV_BYTES;     // [2][128 rows][4 words]: keep bits of a chunk pair
     uint64_t* bars = (uint64_t*)(sMk + 2 * F6_MASK_BYTES);
     uint64_t* q_full = bars;                // [F6_QBUF]
     uint64_t* q_empty = q_full + F6_QBUF;   // [F6_QBUF]
@@ -354,7 +371,7 @@ __global__ void __launch_bounds__(F6_THREADS, F6_CTAS)
         }
         fence_barrier_init();
     }
-    if (warp == 5) tmem_alloc<128>(tslot);
+    if (warp == 5) tmem_alloc<C::TCOLS>(tslot);
     fence_before();
     __syncthreads();
     fence_after();
@@ -369,8 +386,11 @@ __global__ void __launch_bounds__(F6_THREADS, F6_CTAS)
                 const int row_base = b * S;
                 const int qb = n % F6_QBUF;
                 mbar_wait(&q_empty[qb], ((n / F6_QBUF) & 1) ^ 1);
-                mbar_expect_tx(&q_full[qb], F_TILE_BYTES);
-                tma_load_2d(sQ + qb * F_TILE_BYTES, &tQ, &q_full[qb], h * FD, row_base + tile_qt(t) * FT);
+                mbar_expect_tx(&q_full[qb], C::Q_BYTES);
+#pragma unroll
+                for (int pn = 0; pn < C::PANELS; ++pn)
+                    tma_load_2d(sQ + qb * C::Q_BYTES + pn * C::Q_PANEL, &tQ, &q_full[qb], h * D + 64 * pn,
+                                row_base + tile_qt(t) * FT);
                 const int njt = CAUSAL ? (tile_qt(t) + 1) * (FT / KC6) : nj;  // causal: up to the diagonal
                 for (int j = 0; j < njt; ++j, ++u) {
                     const int s = u % F6_NS;
@@ -387,9 +407,14 @@ __global__ void __launch_bounds__(F6_THREADS, F6_CTAS)
                         mbar_arrive(&kv_full[s]);
                         continue;
                     }
-                    mbar_expect_tx(&kv_full[s], 2 * F6_KV_BYTES);
-                    tma_load_2d(sK + s * F6_KV_BYTES, &tK, &kv_full[s], h * FD, row_base + j * KC6);
-                    tma_load_2d(sV + s * F6_KV_BYTES, &tV, &kv_full[s], h * FD, row_base + j * KC6);
+                    mbar_expect_tx(&kv_full[s], 2 * C::KV_BYTES);
+#pragma unroll
+                    for (int pn = 0; pn < C::PANELS; ++pn) {
+                        tma_load_2d(sK + s * C::KV_BYTES + pn * C::KV_PANEL, &tK, &kv_full[s], h * D + 64 * pn,
+                                    row_base + j * KC6);
+                        tma_load_2d(sV + s * C::KV_BYTES + pn * C::KV_PANEL, &tV, &kv_full[s], h * D + 64 * pn,
+                                    row_base + j * KC6);
+                    }
                 }
             }
         }
@@ -397,12 +422,12 @@ __global__ void __launch_bounds__(F6_THREADS, F6_CTAS)
         // ------------------------------------------------ MMA issuer (whole warp, one elected
         // lane issues: descriptors in uniform registers, no per-MMA divergence loop)
         constexpr uint32_t id_s = idesc_bf16(FT, KC6, false, false);  // S = Q K^T
-        constexpr uint32_t id_o = idesc_bf16(FT, FD, false, true);    // O += P V (V MN-major)
+        constexpr uint32_t id_o = idesc_bf16(FT, D, false, true);     // O += P V (V MN-major)
         const uint32_t a0 = smem_u32(sQ), k0 = smem_u32(sK), v0 = smem_u32(sV);
         int u = 0, n = 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++n) {
             const int qb = n % F6_QBUF;
-            const uint64_t dq = desc_kmajor(a0 + qb * F_TILE_BYTES, 0);
+            const uint32_t aq = a0 + qb * C::Q_BYTES;
             mbar_wait(&q_full[qb], (n / F6_QBUF) & 1);
             const int njt = CAUSAL ? (tile_qt(t) + 1) * (FT / KC6) : nj;
             for (int j = 0; j < njt; ++j, ++u) {
@@ -412,9 +437,11 @@ __global__ void __launch_bounds__(F6_THREADS, F6_CTAS)
                 // S(j) overwrites P(j-1) in TMEM: tcgen05.mma executes in issue order, so
                 // PV(j-1) (issued first) has read it (the CUTLASS Blackwell FMHA relies on the same)
                 if (!(fa.dbg & 4)) {
-                    const uint64_t dk = desc_kmajor(k0 + s * F6_KV_BYTES, 0);
+                    const uint32_t ak = k0 + s * C::KV_BYTES;
 #pragma unroll
-                    for (int kk = 0; kk < FD / 16; ++kk) mma_ss_w(tmem, dq + 2 * kk, dk + 2 * kk, id_s, kk);
+                    for (int kk = 0; kk < D / 16; ++kk)  // K16 step kk: panel kk / 4, 32-byte column kk % 4
+                        mma_ss_w(tmem, desc_kmajor(aq + (kk >> 2) * C::Q_PANEL, kk & 3),
+                                 desc_kmajor(ak + (kk >> 2) * C::KV_PANEL, kk & 3), id_s, kk);
                 }
                 mma_commit_w(s_full);
                 if (j == njt - 1) mma_commit_w(&q_empty[qb]);  // last read of this tile's Q
@@ -422,7 +449,9 @@ __global__ void __launch_bounds__(F6_THREADS, F6_CTAS)
                 mbar_wait(p_full, u & 1);
                 fence_after();
                 if (!(fa.dbg & 4)) {
-                    const uint64_t dv = desc_mnmajor(v0 + s * F6_KV_BYTES, 0);
+                    // (desc_mnmajor's LBO is 8 KB = one V panel: the second 64 columns of N)
+                    static_assert(C::KV_PANEL == 8192, "V panel must match desc_mnmajor's LBO");
+                    const uint64_t dv = desc_mnmajor(v0 + s * C::KV_BYTES, 0);
 #pragma unroll
                     for (int kk = 0; kk < KC6 / 16; ++kk) mma_ts_w(tmem + 64, tmem + kk * 8, dv + 128 * kk, id_o, j | kk);
                 }
@@ -489,7 +518,7 @@ __global__ void __launch_bounds__(F6_THREADS, F6_CTAS)
                     mbar_wait(o_done, (u - 1) & 1);
                     fence_after();
 #pragma unroll
-                    for (int c = 0; c < 2; ++c) {
+                    for (int c = 0; c < D / 32; ++c) {
                         uint32_t o[32];
                         tmem_ld32_nowait(t_row + 64 + c * 32, o);
                         tmem_ld_wait();
@@ -539,26 +568,31 @@ __global__ void __launch_bounds__(F6_THREADS, F6_CTAS)
             // ------------------------------------------------ epilogue
             mbar_wait(o_done, (u - 1) & 1);
             fence_after();
-            uint32_t o[2][32];
-            tmem_ld32_nowait(t_row + 64, o[0]);
-            tmem_ld32_nowait(t_row + 96, o[1]);
-            tmem_ld_wait();
-            fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(o_free);  // O may be overwritten by the next tile's PV
             const float inv = fa.dscale / l;
-            bf16* orow = fa.o + (long long)(b * S + qi) * fa.ld_o + (long long)h * FD;
+            bf16* orow = fa.o + (long long)(b * S + qi) * fa.ld_o + (long long)h * D;
 #pragma unroll
-            for (int c = 0; c < 2; ++c)
-#pragma unroll
-                for (int v = 0; v < 4; ++v) {
-                    uint4 w;
-                    w.x = pack_bf16(__uint_as_float(o[c][8 * v + 0]) * inv, __uint_as_float(o[c][8 * v + 1]) * inv);
-                    w.y = pack_bf16(__uint_as_float(o[c][8 * v + 2]) * inv, __uint_as_float(o[c][8 * v + 3]) * inv);
-                    w.z = pack_bf16(__uint_as_float(o[c][8 * v + 4]) * inv, __uint_as_float(o[c][8 * v + 5]) * inv);
-                    w.w = pack_bf16(__uint_as_float(o[c][8 * v + 6]) * inv, __uint_as_float(o[c][8 * v + 7]) * inv);
-                    *(uint4*)(orow + c * 32 + v * 8) = w;
+            for (int half = 0; half < D / 64; ++half) {  // 64 columns of O at a time (registers)
+                uint32_t o[2][32];
+                tmem_ld32_nowait(t_row + 64 + half * 64, o[0]);
+                tmem_ld32_nowait(t_row + 96 + half * 64, o[1]);
+                tmem_ld_wait();
+                if (half == D / 64 - 1) {
+                    fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(o_free);  // O may be overwritten by the next tile's PV
                 }
+#pragma unroll
+                for (int c = 0; c < 2; ++c)
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) {
+                        uint4 w;
+                        w.x = pack_bf16(__uint_as_float(o[c][8 * v + 0]) * inv, __uint_as_float(o[c][8 * v + 1]) * inv);
+                        w.y = pack_bf16(__uint_as_float(o[c][8 * v + 2]) * inv, __uint_as_float(o[c][8 * v + 3]) * inv);
+                        w.z = pack_bf16(__uint_as_float(o[c][8 * v + 4]) * inv, __uint_as_float(o[c][8 * v + 5]) * inv);
+                        w.w = pack_bf16(__uint_as_float(o[c][8 * v + 6]) * inv, __uint_as_float(o[c][8 * v + 7]) * inv);
+                        *(uint4*)(orow + half * 64 + c * 32 + v * 8) = w;
+                    }
+            }
             fa.lse[bh * S + qi] = (m_used + __log2f(l)) * 0.6931471805599453f;  // natural log
         }
     }
@@ -566,17 +600,17 @@ __global__ void __launch_bounds__(F6_THREADS, F6_CTAS)
     __syncthreads();
     if (warp == 5) {
         fence_after();
-        tmem_dealloc<128>(tmem);
+        tmem_dealloc<C::TCOLS>(tmem);
     }
 }
 
-bool fwd_fits(const Attn& a) {
-    if (a.t != BF16 || a.hd != FD || a.S % FT || a.S < FT) return false;
+bool fwd_fits(const Attn& a, int hd = FD) {
+    if (a.t != BF16 || a.hd != hd || a.S % FT || a.S < FT) return false;
     if (a.thr && !a.mask) return false;
     auto al = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
     if (!al(a.q) || !al(a.k) || !al(a.v) || !al(a.o) || a.ld_o % 8) return false;
     if (a.ld_q % 8 || a.ld_k % 8 || a.ld_v % 8) return false;
-    if (a.B * a.S > (1ll << 31) || a.nh * FD > a.ld_q) return false;
+    if (a.B * a.S > (1ll << 31) || a.nh * hd > a.ld_q) return false;
     return true;
 }
 
@@ -1587,6 +1621,33 @@ size_t carve(const Attn& a, void* base, BwdWs* w) {
 
 bool attn_fwd_sm100_try(const Attn& a, cudaStream_t s) {
     static int nt_env = getenv("SB_ATTN_FWD_NT") ? atoi(getenv("SB_ATTN_FWD_NT")) : 6;
+    if (a.hd == 128) {  // head dim 128 (GPT-Neo, C4): the 64-key-chunk kernel, two CTAs per SM
+        if (!fwd_fits(a, 128)) return false;
+        CUtensorMap tq, tk6, tv6, tm6;
+        const long long rows = a.B * a.S, cols = a.nh * 128;
+        if (!make_map_bf16(&tq, a.q, cols, rows, a.ld_q, FT) || !make_map_bf16(&tk6, a.k, cols, rows, a.ld_k, KC6) ||
+            !make_map_bf16(&tv6, a.v, cols, rows, a.ld_v, KC6))
+            return false;
+        memset(&tm6, 0, sizeof(tm6));
+        if (a.thr && !make_map_u32(&tm6, a.mask, a.S / 32, a.B * a.nh * a.S, a.S / 32, 2 * KC6 / 32, FT)) return false;
+        FwdArgs fa{(bf16*)a.o, a.ld_o, a.lse, a.thr ? a.mask : nullptr, a.thr ? a.dscale : 1.f,
+                   a.scale * 1.4426950408889634f, (int)a.S, (int)a.nh, 0};
+        if (const char* e = getenv("SB_ATTN_DBG")) fa.dbg = atoi(e);
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(k_fa6_fwd<false, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, F6<128>::SMEM);
+            cudaFuncSetAttribute(k_fa6_fwd<true, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, F6<128>::SMEM);
+            attr = true;
+        }
+        static int sms = 0;
+        if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+        const long long ntiles = a.B * a.nh * (a.S / FT);
+        const int grid = (int)std::min<long long>(ntiles, (long long)F6<128>::CTAS * sms);
+        if (a.causal) k_fa6_fwd<true, 128><<<grid, F6_THREADS, F6<128>::SMEM, s>>>(tq, tk6, tv6, tm6, fa, (int)ntiles);
+        else k_fa6_fwd<false, 128><<<grid, F6_THREADS, F6<128>::SMEM, s>>>(tq, tk6, tv6, tm6, fa, (int)ntiles);
+        SBK_CHECK_LAUNCH();
+        return true;
+    }
     if ((a.causal && nt_env != 6) || !fwd_fits(a)) return false;  // causal: the 64-key-chunk kernel only
     CUtensorMap tq, tk, tv, tm;
     const long long rows = a.B * a.S, cols = a.nh * FD;

@@ -103,7 +103,9 @@ void strided_copy(const void* src, DT ts, const i64* src_strides, void* dst, DT 
 
 // ------------------------------------------------------ norms / softmax
 // Row-wise over (outer, n, inner) layout: element (o, j, i) at o*n*inner + j*inner + i.
-void softmax_fwd(const void* x, void* y, DT t, i64 outer, i64 n, i64 inner, cudaStream_t s);
+// causal_nq > 0 (rows layout only): row r is query q = r % causal_nq and covers keys
+// [0, min(n, q + 1 + n - causal_nq)); the rest are written as 0 (oracle/causal_ext.py)
+void softmax_fwd(const void* x, void* y, DT t, i64 outer, i64 n, i64 inner, cudaStream_t s, i64 causal_nq = 0);
 void softmax_bwd(const void* y, const void* g, void* gx, DT t, DT tg, i64 outer, i64 n, i64 inner, cudaStream_t s);
 // LayerNorm over the last dim: y = gamma*(x-mu)*rstd + beta; gamma/beta may be null.
 void layernorm_fwd(const void* x, const void* gamma, const void* beta, DT tp, void* y, float* mean, float* rstd,

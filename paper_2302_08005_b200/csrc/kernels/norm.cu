@@ -26,20 +26,22 @@ static int vec_blocks(i64 rows) { return (int)std::min<i64>(296, std::max<i64>(1
 
 // ------------------------------------------------------------------ softmax
 template <class T>
-__global__ void k_softmax_rows(const T* x, T* y, i64 rows, i64 n) {
+__global__ void k_softmax_rows(const T* x, T* y, i64 rows, i64 n, i64 nq) {
     i64 row = blockIdx.x * (i64)kWarps + threadIdx.x / 32;
     int lane = threadIdx.x & 31;
     if (row >= rows) return;
     const T* px = x + row * n;
     T* py = y + row * n;
+    i64 lim = n;
+    if (nq > 0) lim = max((i64)1, min(n, row % nq + 1 + n - nq));  // causal (oracle/causal_ext.py)
     float mx = -INFINITY;
-    for (i64 i = lane; i < n; i += 32) mx = fmaxf(mx, to_f(px[i]));
+    for (i64 i = lane; i < lim; i += 32) mx = fmaxf(mx, to_f(px[i]));
     mx = warp_max(mx);
     float s = 0.f;
-    for (i64 i = lane; i < n; i += 32) s += __expf(to_f(px[i]) - mx);
+    for (i64 i = lane; i < lim; i += 32) s += __expf(to_f(px[i]) - mx);
     s = warp_sum(s);
     float inv = 1.f / s;
-    for (i64 i = lane; i < n; i += 32) py[i] = from_f<T>(__expf(to_f(px[i]) - mx) * inv);
+    for (i64 i = lane; i < n; i += 32) py[i] = i < lim ? from_f<T>(__expf(to_f(px[i]) - mx) * inv) : from_f<T>(0.f);
 }
 template <class T>
 __global__ void k_softmax_cols(const T* x, T* y, i64 outer, i64 n, i64 inner) {
@@ -54,11 +56,13 @@ __global__ void k_softmax_cols(const T* x, T* y, i64 outer, i64 n, i64 inner) {
         for (i64 j = 0; j < n; ++j) py[j * inner] = from_f<T>(__expf(to_f(px[j * inner]) - mx) / s);
     }
 }
-void softmax_fwd(const void* x, void* y, DT t, i64 outer, i64 n, i64 inner, cudaStream_t s) {
+void softmax_fwd(const void* x, void* y, DT t, i64 outer, i64 n, i64 inner, cudaStream_t s, i64 causal_nq) {
+    if (causal_nq > 0 && inner != 1) throw std::runtime_error("softmax_fwd: causal needs the last axis");
     dispatch(t, [&](auto* p) {
         using T = std::remove_pointer_t<decltype(p)>;
         if (inner == 1)
-            k_softmax_rows<T><<<(unsigned)((outer + kWarps - 1) / kWarps), 32 * kWarps, 0, s>>>((const T*)x, (T*)y, outer, n);
+            k_softmax_rows<T><<<(unsigned)((outer + kWarps - 1) / kWarps), 32 * kWarps, 0, s>>>((const T*)x, (T*)y, outer, n,
+                                                                                               causal_nq);
         else
             k_softmax_cols<T><<<grid_for(outer * inner, 256), 256, 0, s>>>((const T*)x, (T*)y, outer, n, inner);
     });

@@ -99,3 +99,39 @@ def tp_script(layers: int, world: int, fuse: bool = True, flash: bool = True, ck
     for i in range(int(ckpt_ratio * layers)):
         s += f"checkpoint encoder.layer.{i}\n"
     return s
+
+
+def neo_script(layers: int, world: int = 1, flash: bool = True, fuse: bool = True, fused_qkv: bool = True,
+               checkpoint_layers=(), shard_embeddings: bool = True) -> str:
+    """The decoder recipe (f2, BASELINE.json configs[3]) for ``gpt_neo``: FusedQKV
+    (bias-free, sharded blockwise on axis 0 + sync backward), out_proj axis 1 + sync
+    forward, mlp.c_fc axis 0 + sync backward, mlp.c_proj axis 1 + sync forward,
+    vocab-parallel wte + sync both; the causal core replaced by EfficientAttention
+    (its ``causal`` attr is copied, library.cpp:106-113); bias+GeLU fused in the MLP;
+    selective checkpointing of ``checkpoint_layers``."""
+    s = f"# GPT-Neo-style decoder recipe, TP={world}\n"
+    for i in range(layers):
+        lp = f"h.{i}"
+        if fused_qkv:
+            s += f"replace {lp}.attn.qkv with FusedQKV\n"
+        if world > 1:
+            if fused_qkv:
+                s += f"shard {lp}.attn.qkv weight axis=0\n"
+                s += f"sync {lp}.attn.qkv type=backward\n"
+            s += f"shard {lp}.attn.out_proj weight,bias axis=1\n"
+            s += f"sync {lp}.attn.out_proj type=forward\n"
+            s += f"shard {lp}.mlp.c_fc weight,bias axis=0\n"
+            s += f"sync {lp}.mlp.c_fc type=backward\n"
+            s += f"shard {lp}.mlp.c_proj weight,bias axis=1\n"
+            s += f"sync {lp}.mlp.c_proj type=forward\n"
+        if flash:
+            s += f"replace {lp}.attn.core with EfficientAttention\n"
+    if fuse:
+        s += _pattern_block("bias_gelu", pattern_linear_gelu())
+        for i in range(layers):
+            s += f"trace h.{i}.mlp flatten=true\n"
+            s += f"fuse h.{i}.mlp at bias_gelu backend=composed\n"
+    if world > 1 and shard_embeddings:
+        s += "shard wte weight axis=0\nsync wte type=both\n"
+    s += "".join(f"checkpoint h.{i}\n" for i in checkpoint_layers)
+    return s

@@ -1,8 +1,10 @@
-import ctypes, sys, torch
+import ctypes, os, sys, torch
 sys.path.insert(0, '.')
 import paper_2302_08005_b200 as sb
 from tests.test_kernels_gpu import L, P
-B, S, nh, hd, p = 32, 512, 16, 64, 0.1
+B, S, nh, hd = (int(x) for x in os.environ.get("ATTN_CFG", "32,512,16,64").split(","))
+p = 0.1
+print('B,S,nh,hd', B, S, nh, hd)
 H = nh * hd
 qkv = (torch.randn(B, S, 3 * H, device="cuda") * 0.5).bfloat16()
 q, k, v = qkv[..., :H], qkv[..., H:2*H], qkv[..., 2*H:]

@@ -1,7 +1,8 @@
 """Causal attention core (the first piece of C4's decoder blocks).
 
-The reference's op set has no mask op (proj/src/shape_inference.cpp:10-16), so there is
-no reference output to pin against: **parity unpinned** (DESIGN.md §8). The checks are
+The reference's op set has no mask op (proj/src/shape_inference.cpp:10-16); causal
+parity is pinned end to end against the documented oracle extension (oracle/causal_ext.py,
+tests/test_decoder_gpu.py, tests/test_causal_oracle_cpu.py). The checks here are
 (1) the kernels through the C ABI (`sb_attn_fwd_ex` / `sb_attn_bwd_ex`, SB_ATTN_CAUSAL)
 against a torch fp32 causal reference with the same keep bits, on both engines that take
 the flag (mma.sync, SIMT), and (2) at the executor level, the defining property of a
@@ -15,6 +16,7 @@ import pytest
 
 import paper_2302_08005_b200 as sb
 from paper_2302_08005_b200 import recipes
+from tests.helpers import compare_grads
 from tests.test_kernels_gpu import ES, NS, L, P, _attn_case, _keep, close
 
 pytestmark = pytest.mark.gpu
@@ -90,7 +92,7 @@ def test_causal_attention_kernels(cap, engine, B, S, nh, hd, p):
     do = (torch.randn(B, S, H, device="cuda", generator=torch.Generator(device="cuda").manual_seed(3)) * 0.5).bfloat16()
     ref, lse_ref, grads = _causal_ref(qkv, bits, B, S, nh, hd, p, do)
     o, lse, used = _fwd(qkv, bits, B, S, nh, hd, p, cap)
-    assert used == (3 if cap == 0 and hd == 64 else engine)
+    assert used == (3 if cap == 0 else engine)  # tcgen05 forward: k_fa6_fwd<causal, hd>
     close(o, ref)
     assert (lse - lse_ref).abs().max().item() < 2e-3 * max(1.0, lse_ref.abs().max().item())
     g, used = _bwd(qkv, o, lse, do, bits, B, S, nh, hd, p, cap)
@@ -181,7 +183,16 @@ def test_causal_executor_prefix_property(dtype, hidden, heads, seq):
     assert all(np.isfinite(v).all() for v in g.params.values())
 
 
-def test_causal_needs_the_fused_path():
+def test_causal_composed_path_matches_fused():
+    """fused=False runs a causal EfficientAttention as the reference graph with the
+    oracle extension's causal softmax; it agrees with the flash path (fp32, train)."""
     m, cm = _causal_model(32, 4, 16, 2, 0.1)
-    with pytest.raises(sb.SlapoError, match="causal"):
-        sb.Executor(cm, "verify", 123, 1, dtype="fp32", fused=False).forward(m.random_inputs(5))
+    x = m.random_inputs(5)
+    res = []
+    for fused in (False, True):
+        ex = sb.Executor(cm, "train", 123, 1, dtype="fp32", fused=fused)
+        out = ex.forward(x)[0]
+        res.append((out, ex.backward().params))
+    (o0, g0), (o1, g1) = res
+    assert np.abs(o0 - o1).max() <= 1e-4 * np.abs(o1).max()
+    compare_grads(g0, g1, 1e-4)  # (the analytically-zero key bias normalised by its QKV-bias group)

@@ -1,0 +1,91 @@
+"""GPU parity of the decoder model family (f2, BASELINE.json configs[3]):
+``gpt_neo`` (pre-LN blocks, causal self-attention) through the B200 executor
+(C ABI) against the documented causal oracle extension (oracle/causal_ext.py:
+the reference executor with a `causal` softmax attr, pinned against a numpy
+restatement in tests/test_causal_oracle_cpu.py), same seeds / inputs / schedule.
+
+Tolerances as for the encoder: fp32 1e-4 per tensor
+(||a-b||_inf/||b||_inf) on outputs, loss and every gradient; bf16 relL2 2e-2
+outputs, 5e-2 gradients, and 2e-3 on the loss taken relative to sum|logits|
+(the logits have both signs, so their plain sum cancels; the condition number
+sum|o| / |sum o| is recorded with the errors).
+"""
+import os
+
+import numpy as np
+import pytest
+
+import paper_2302_08005_b200 as sb
+from paper_2302_08005_b200 import recipes
+from oracle import ref
+from tests.helpers import BF16_GRAD_TOL, BF16_LOSS_TOL, BF16_OUT_TOL, rel_l2
+from tests.test_parity_gpu import check
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not os.path.exists(ref.DRIVER_CAUSAL), reason="causal oracle not built")]
+
+
+def run_both(tmp, cfg, script, world, mode="train", dtype="fp32", seed=123, input_seed=9):
+    m = sb.gpt_neo(cfg["layers"], cfg["hidden"], cfg["heads"], cfg["vocab"], cfg["batch"], cfg["seq"], cfg["p"])
+    mj = os.path.join(tmp, "neo.json")
+    with open(mj, "w") as f:
+        f.write(m.to_json())
+    s = sb.create_schedule(m, world)
+    if script:
+        s.load_script(script)
+    ex = sb.Executor(s.apply(), mode, seed, world, dtype=dtype)
+    ex.forward(m.random_inputs(input_seed))
+    outs = [ex.outputs_of_rank(r) for r in range(world)]
+    grads = ex.backward_all_ranks()
+    r = ref.run(model_json=mj, causal=True, schedule=script or None, world=world, mode=mode, seed=seed,
+                input_seed=input_seed)
+    return ex, outs, grads, r
+
+
+SMALL = dict(layers=2, hidden=32, heads=2, vocab=32, batch=2, seq=16, p=0.1)
+
+
+@pytest.mark.parametrize("mode", ["train", "verify"])
+def test_decoder_unscheduled_fp32(tmp_path, mode):
+    """the composed causal attention core (causal softmax kernel) and pre-LN blocks"""
+    _, outs, grads, r = run_both(str(tmp_path), SMALL, "", 1, mode)
+    check(outs, grads, r, 1, 1e-4, 1e-4)
+
+
+@pytest.mark.parametrize("world", [1, 2])
+def test_decoder_recipe_fp32(tmp_path, world):
+    """FusedQKV (bias-free) + TP shard/sync + causal EfficientAttention + bias+GeLU
+    fusion + a checkpointed block, at TP 1 and 2 (local placement)"""
+    script = recipes.neo_script(SMALL["layers"], world, checkpoint_layers=[1])
+    ex, outs, grads, r = run_both(str(tmp_path), SMALL, script, world)
+    check(outs, grads, r, world, 1e-4, 1e-4)
+    assert ex.collective_invocations() == r.meta["collectives_total"]
+
+
+@pytest.mark.parametrize("heads,seq", [(4, 128), (2, 128), (4, 256)])
+def test_decoder_recipe_bf16(tmp_path, heads, seq):
+    """bf16 on the tensor-core paths: head_dim 64 runs the tcgen05 causal flash
+    attention (k_fa6_fwd<true> / k_fa7_bwd<true>), head_dim 128 the mma.sync one"""
+    cfg = dict(layers=2, hidden=256, heads=heads, vocab=64, batch=2, seq=seq, p=0.1)
+    script = recipes.neo_script(2, 1, checkpoint_layers=[0])
+    _, outs, grads, r = run_both(str(tmp_path), cfg, script, 1, dtype="bf16")
+    check(outs, grads, r, 1, BF16_OUT_TOL, BF16_GRAD_TOL, metric=rel_l2, tol_loss=BF16_LOSS_TOL,
+          record=f"decoder_bf16_h256_nh{heads}_s{seq}", loss_l1=True)
+    if heads == 4:
+        assert sb.lib().sb_attn_engine(0) == 3 and sb.lib().sb_attn_engine(1) == 3
+
+
+def test_decoder_prefix_independence(tmp_path):
+    """causality end to end: outputs of the first S/2 positions do not change when
+    the second half of every sequence changes (verify mode, bf16 tcgen05 path)"""
+    cfg = dict(layers=2, hidden=256, heads=4, vocab=64, batch=2, seq=128, p=0.0)
+    m = sb.gpt_neo(cfg["layers"], cfg["hidden"], cfg["heads"], cfg["vocab"], cfg["batch"], cfg["seq"], cfg["p"])
+    s = sb.create_schedule(m, 1)
+    s.load_script(recipes.neo_script(2, 1))
+    ex = sb.Executor(s.apply(), "verify", 5, 1, dtype="bf16")
+    ids = m.random_inputs(3)[0]
+    a = ex.forward([ids])[0]
+    ids2 = ids.copy()
+    ids2[:, 64:] = np.random.default_rng(0).normal(size=ids2[:, 64:].shape)
+    b = ex.forward([ids2])[0]
+    assert np.array_equal(a[:, :64], b[:, :64])
+    assert not np.array_equal(a[:, 64:], b[:, 64:])

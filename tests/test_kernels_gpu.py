@@ -320,10 +320,14 @@ def test_flash_attention_tensor_core(B, S, nh, hd, p):
 
 @pytest.mark.parametrize("B,S,nh,hd,p,qscale", [(2, 128, 4, 64, 0.0, 0.5), (2, 256, 2, 64, 0.1, 0.5),
                                                  (1, 384, 2, 64, 0.1, 0.5), (2, 512, 16, 64, 0.1, 0.5),
-                                                 (1, 512, 2, 64, 0.1, 4.0), (1, 1024, 2, 64, 0.0, 3.0)])
+                                                 (1, 512, 2, 64, 0.1, 4.0), (1, 1024, 2, 64, 0.0, 3.0),
+                                                 (2, 128, 2, 128, 0.0, 0.5), (2, 256, 4, 128, 0.1, 0.5),
+                                                 (1, 1024, 16, 128, 0.1, 3.0)])
 def test_flash_attention_tcgen05_forward(B, S, nh, hd, p, qscale):
-    """tcgen05/TMEM forward (engine 3) vs a torch fp32 reference and vs the mma.sync kernel;
-    qscale > 1 makes logits large enough to exercise the lazy running-max rescale."""
+    """tcgen05/TMEM forward (engine 3; head_dim 64: four CTAs per SM, 128: two, with
+    two-panel Q/K/V tiles and M128 N128 PV MMAs) vs a torch fp32 reference and vs the
+    mma.sync kernel; qscale > 1 makes logits large enough to exercise the lazy
+    running-max rescale."""
     qkv, bits = _attn_case(B, S, nh, hd, p, qscale)
     o5, lse5, used = _attn_fwd(qkv, bits, B, S, nh, hd, p, 0)
     assert used == 3, "tcgen05 attention path not taken"

@@ -46,10 +46,13 @@ def run_both(cfg, script, world, mode="train", dtype="fp32", fused=True, seed=12
     return ex, outs, grads, r
 
 
-def check(outs, grads, r, world, tol_out, tol_grad, metric=rel_err, tol_loss=None, record=None):
+def check(outs, grads, r, world, tol_out, tol_grad, metric=rel_err, tol_loss=None, record=None, loss_l1=False):
     """Per rank: every output (metric <= tol_out), the loss = sum of outputs
     (|loss - loss_ref| <= tol_loss * |loss_ref|; tol_loss defaults to tol_out, i.e.
-    1e-4 relative on the fp32 path) and every gradient (compare_grads)."""
+    1e-4 relative on the fp32 path) and every gradient (compare_grads).
+    loss_l1: the loss error is taken relative to sum(|outputs_ref|) instead — for
+    outputs of both signs (decoder logits) the sum cancels, and its relative error is
+    the outputs' error times the condition number sum|o| / |sum o| (recorded)."""
     tol_loss = tol_out if tol_loss is None else tol_loss
     rec = []
     for rank in range(world):
@@ -62,10 +65,12 @@ def check(outs, grads, r, world, tol_out, tol_grad, metric=rel_err, tol_loss=Non
             assert e <= tol_out, f"rank {rank} output err {e:.3e}"
         loss_g = sum(float(np.asarray(o, dtype=np.float64).sum()) for o in outs[rank])
         loss_w = sum(float(w.sum()) for w in want)
-        e_loss = abs(loss_g - loss_w) / max(abs(loss_w), 1e-30)
+        l1 = sum(float(np.abs(w).sum()) for w in want)
+        e_loss = abs(loss_g - loss_w) / max(l1 if loss_l1 else abs(loss_w), 1e-30)
         assert e_loss <= tol_loss, (rank, loss_g, loss_w, e_loss)
         worst = compare_grads(grads[rank].params, r.grads(rank), tol_grad, metric)
-        rec.append({"rank": rank, "out": e_out, "loss_rel": e_loss, "worst_grad": worst[0],
+        rec.append({"rank": rank, "out": e_out, "loss_rel": e_loss, "loss_metric": "l1" if loss_l1 else "rel",
+                    "loss_cond": l1 / max(abs(loss_w), 1e-30), "worst_grad": worst[0],
                     "worst_grad_name": worst[1]})
     if record:
         _record(record, rec)
