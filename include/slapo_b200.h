@@ -96,6 +96,28 @@ int sb_pipeline_num_stages(const sb_pipeline* p, int* n);
 int sb_pipeline_stage(const sb_pipeline* p, int i, sb_model** out);
 int sb_pipeline_stage_io(const sb_pipeline* p, int i, int which, char* buf, size_t cap, size_t* needed);
 int sb_pipeline_free(sb_pipeline* p);
+/* Pipeline-parallel training step over the stages of a pipeline_split plan (f1): GPipe with
+   re-materialisation, one Executor per stage on its own device (devices: one per stage, NULL:
+   the current device), stage-boundary values stashed per micro-batch (peer copies between
+   devices), backward seeded with the consumers' input gradients, parameter gradients summed
+   over micro-batches. Extends run_pipeline (proj/src/executor.cpp:1531-1579; forward only in
+   the reference) to a training step; per-micro-batch semantics as run_pipeline. */
+typedef struct sb_pipeline_executor sb_pipeline_executor;
+int sb_pipeline_executor_create(const sb_pipeline* p, int micro_batches, int train, uint64_t seed, int dtype,
+                                const int* devices, int fused, sb_pipeline_executor** out);
+int sb_pipeline_executor_forward(sb_pipeline_executor* e, const double* const* inputs, int n);
+int sb_pipeline_executor_num_outputs(sb_pipeline_executor* e, int* n);
+int sb_pipeline_executor_output(sb_pipeline_executor* e, int idx, double* out, size_t cap, size_t* n, int64_t* dims,
+                                int* ndims);
+int sb_pipeline_executor_backward(sb_pipeline_executor* e);
+int sb_pipeline_executor_num_grads(sb_pipeline_executor* e, int stage, int* n);
+int sb_pipeline_executor_grad_name(sb_pipeline_executor* e, int stage, int idx, char* buf, size_t cap);
+int sb_pipeline_executor_grad(sb_pipeline_executor* e, int stage, const char* dotted, double* out, size_t cap,
+                              size_t* n);
+int sb_pipeline_executor_num_input_grads(sb_pipeline_executor* e, int stage, int* n);
+int sb_pipeline_executor_input_grad(sb_pipeline_executor* e, int stage, int idx, double* out, size_t cap, size_t* n);
+int sb_pipeline_executor_time_steps(sb_pipeline_executor* e, int steps, float* ms);
+int sb_pipeline_executor_free(sb_pipeline_executor* e);
 int sb_schedule_free(sb_schedule* s);
 
 /* -------------------------------------------------------------- executor */

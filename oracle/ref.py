@@ -52,6 +52,17 @@ def read_dump(path: str) -> Dict[str, np.ndarray]:
     return out
 
 
+def write_dump(path: str, tensors) -> None:
+    """SBT1 (ref_driver.cpp write_dump): [(name, array)], f64."""
+    with open(path, "wb") as f:
+        f.write(b"SBT1" + struct.pack("<I", len(tensors)))
+        for name, a in tensors:
+            a = np.ascontiguousarray(np.asarray(a, dtype="<f8"))
+            nb = name.encode()
+            f.write(struct.pack("<I", len(nb)) + nb + struct.pack("<I", a.ndim) + struct.pack("<%dq" % a.ndim, *a.shape))
+            f.write(a.tobytes())
+
+
 class RefRun:
     """Dumps of one oracle run. A temporary dump directory (no `outdir` given to
     `run`) is owned by this object and removed with it (`close()` / GC / `with`):
@@ -106,10 +117,11 @@ class RefRun:
 
 
 def run(model: str = "toy_bert", schedule: Optional[str] = None, outdir: Optional[str] = None, timeout: int = 600,
-        causal: bool = False, **kw) -> RefRun:
+        causal: bool = False, inputs=None, **kw) -> RefRun:
     """kw: layers, hidden, heads, vocab, batch, seq, p, dtype, world, mode, seed, input_seed,
     backward, dump_params, tp_hidden, tp_inner, tp_batch, repeat, model_json (path).
-    causal=True runs the causal extension's driver (needed for decoder models)."""
+    causal=True runs the causal extension's driver (needed for decoder models);
+    inputs: explicit model inputs (arrays in declared order) instead of random_tensor ones."""
     drv = DRIVER_CAUSAL if causal else DRIVER
     if not os.path.exists(drv):
         raise RuntimeError(f"oracle driver missing: build it with `make -C oracle` ({drv})")
@@ -127,6 +139,10 @@ def run(model: str = "toy_bert", schedule: Optional[str] = None, outdir: Optiona
         args += ["--schedule", sched_file]
     for k, v in kw.items():
         args += ["--" + k, str(v)]
+    if inputs is not None:
+        ipath = os.path.join(outdir, "given_inputs.bin")
+        write_dump(ipath, [(f"input{i}", a) for i, a in enumerate(inputs)])
+        args += ["--inputs", ipath]
     try:
         r = subprocess.run(args, capture_output=True, text=True, timeout=timeout)
         if r.returncode != 0:

@@ -63,6 +63,36 @@ void write_dump(const std::string& path, const std::vector<std::pair<std::string
     }
 }
 
+// the inverse of write_dump: tensors in file order (used for --inputs)
+std::vector<TensorValue> read_dump_values(const std::string& path) {
+    std::ifstream in(path, std::ios::binary);
+    if (!in) throw Error("cannot read " + path);
+    char magic[4];
+    in.read(magic, 4);
+    if (std::string(magic, 4) != "SBT1") throw Error("not an SBT1 dump: " + path);
+    std::uint32_t n = 0;
+    in.read(reinterpret_cast<char*>(&n), 4);
+    std::vector<TensorValue> res;
+    for (std::uint32_t k = 0; k < n; ++k) {
+        std::uint32_t len = 0, rank = 0;
+        in.read(reinterpret_cast<char*>(&len), 4);
+        std::string name(len, '\0');
+        in.read(name.data(), len);
+        in.read(reinterpret_cast<char*>(&rank), 4);
+        TensorSpec spec;
+        spec.dtype = Dtype::F64;
+        for (std::uint32_t r = 0; r < rank; ++r) {
+            std::int64_t d = 0;
+            in.read(reinterpret_cast<char*>(&d), 8);
+            spec.shape.push_back(d);
+        }
+        TensorValue t(spec);
+        in.read(reinterpret_cast<char*>(t.data.data()), static_cast<std::streamsize>(t.data.size() * 8));
+        res.push_back(std::move(t));
+    }
+    return res;
+}
+
 std::string read_file(const std::string& p) {
     std::ifstream in(p, std::ios::binary);
     if (!in) throw Error("cannot read " + p);
@@ -96,7 +126,7 @@ int main(int argc, char** argv) {
         {"tp_hidden", "8"}, {"tp_inner", "16"}, {"tp_batch", "4"}, {"repeat", "1"}, {"cli_run", ""},
         {"estimate", ""}, {"est_batch", "0"}, {"est_mem", "17179869184"}, {"est_consts", ""}, {"ckpt_container", ""},
         {"ckpt_ratio", "0"}, {"tune", ""}, {"tune_seed", "0"}, {"tune_restarts", "3"}, {"micro", "1"},
-        {"cli_train", ""}};
+        {"cli_train", ""}, {"inputs", ""}};
     for (int i = 1; i + 1 < argc; i += 2) {
         std::string k = argv[i];
         if (k.rfind("--", 0) != 0) { std::cerr << "bad arg " << k << "\n"; return 2; }
@@ -283,8 +313,19 @@ int main(int argc, char** argv) {
         }
         auto specs = declared_input_specs(*model.forward);
         std::vector<TensorValue> inputs;
-        for (std::size_t i = 0; i < specs.size(); ++i)
-            inputs.push_back(random_tensor(specs[i], std::stoull(a["input_seed"]), i));
+        if (!a["inputs"].empty()) {  // explicit inputs (SBT1 dump, declared order), e.g. one micro-batch
+            inputs = read_dump_values(a["inputs"]);
+            if (inputs.size() != specs.size()) throw Error("--inputs: wrong number of tensors");
+            for (std::size_t i = 0; i < specs.size(); ++i) {
+                if (inputs[i].data.size() != static_cast<std::size_t>(specs[i].element_count()))
+                    throw Error("--inputs: tensor " + std::to_string(i) + " does not match the declared shape");
+                inputs[i].spec = specs[i];
+                inputs[i].quantize();
+            }
+        } else {
+            for (std::size_t i = 0; i < specs.size(); ++i)
+                inputs.push_back(random_tensor(specs[i], std::stoull(a["input_seed"]), i));
+        }
 
         int repeat = std::stoi(a["repeat"]);
         double fwd_s = 0, bwd_s = 0;

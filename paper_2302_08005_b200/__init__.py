@@ -19,6 +19,7 @@ from __future__ import annotations
 
 import ctypes
 import json
+import weakref
 import os
 import sys
 from dataclasses import dataclass, field
@@ -54,6 +55,20 @@ _lib.sb_last_error.restype = _c.c_char_p
 for _n, _a in {
     "sb_model_toy_bert": (_c.c_int, _i64, _i64, _i64, _i64, _i64, _c.c_double, _c.POINTER(_P)),
     "sb_model_gpt_neo": (_c.c_int, _i64, _i64, _i64, _i64, _i64, _c.c_double, _c.POINTER(_P)),
+    "sb_pipeline_executor_create": (_P, _c.c_int, _c.c_int, _u64, _c.c_int, _c.POINTER(_c.c_int), _c.c_int,
+                                    _c.POINTER(_P)),
+    "sb_pipeline_executor_forward": (_P, _c.POINTER(_dp), _c.c_int),
+    "sb_pipeline_executor_num_outputs": (_P, _c.POINTER(_c.c_int)),
+    "sb_pipeline_executor_output": (_P, _c.c_int, _dp, _c.c_size_t, _c.POINTER(_c.c_size_t), _c.POINTER(_i64),
+                                    _c.POINTER(_c.c_int)),
+    "sb_pipeline_executor_backward": (_P,),
+    "sb_pipeline_executor_num_grads": (_P, _c.c_int, _c.POINTER(_c.c_int)),
+    "sb_pipeline_executor_grad_name": (_P, _c.c_int, _c.c_int, _c.c_char_p, _c.c_size_t),
+    "sb_pipeline_executor_grad": (_P, _c.c_int, _c.c_char_p, _dp, _c.c_size_t, _c.POINTER(_c.c_size_t)),
+    "sb_pipeline_executor_num_input_grads": (_P, _c.c_int, _c.POINTER(_c.c_int)),
+    "sb_pipeline_executor_input_grad": (_P, _c.c_int, _c.c_int, _dp, _c.c_size_t, _c.POINTER(_c.c_size_t)),
+    "sb_pipeline_executor_time_steps": (_P, _c.c_int, _c.POINTER(_c.c_float)),
+    "sb_pipeline_executor_free": (_P,),
     "sb_model_tp_two_linear": (_i64, _i64, _i64, _c.POINTER(_P)),
     "sb_model_fig3c": (_c.POINTER(_P),),
     "sb_model_ffn_stack": (_c.c_int, _i64, _i64, _c.POINTER(_P)),
@@ -336,9 +351,13 @@ class Schedule:
                 mh = _P()
                 _check(_lib.sb_pipeline_stage(h, i, _c.byref(mh)))
                 stages.append(PipelineStage(Model(mh), names(i, 0), names(i, 1)))
-            return PipelinePlan(stages, names(-1, 0), names(-1, 1))
-        finally:
+            plan = PipelinePlan(stages, names(-1, 0), names(-1, 1))
+        except BaseException:
             _lib.sb_pipeline_free(h)
+            raise
+        plan._h = h  # kept for PipelineExecutor; freed with the plan
+        weakref.finalize(plan, _lib.sb_pipeline_free, h)
+        return plan
 
     def apply(self) -> Model:
         h = _P()
@@ -359,6 +378,7 @@ class PipelinePlan:
     stages: List[PipelineStage]
     model_inputs: List[str]
     model_outputs: List[str]
+    _h: object = field(default=None, repr=False, compare=False)
 
 
 def create_schedule(model: Model, world_size: int = 1) -> Schedule:
@@ -652,3 +672,83 @@ def run_pipeline(plan: PipelinePlan, inputs, micro_batches: int = 1, mode: str =
     if micro_batches == 1:
         return chunks[0]
     return [np.concatenate([ch[o] for ch in chunks], axis=0) for o in range(len(plan.model_outputs))]
+
+
+class PipelineExecutor:
+    """Pipeline-parallel training step over a stage plan (f1; csrc/host/pipeline_exec.hpp):
+    GPipe with re-materialisation, one executor per stage on `devices[stage]` (default:
+    the current device), stage-boundary values stashed per micro-batch and moved
+    device-to-device (peer copies over NVLink between devices), the backward of
+    sum(outputs) seeded stage by stage with the consumers' input gradients, parameter
+    gradients summed over micro-batches. The forward is run_pipeline's (proj/src/
+    executor.cpp:1531-1579): every micro-batch of a stage runs with the executor seed
+    on micro-batch-shaped tensors."""
+
+    def __init__(self, plan: PipelinePlan, micro_batches: int = 1, mode: str = "train", seed: int = 0,
+                 dtype: str = "fp32", devices: Optional[Sequence[int]] = None, fused: bool = True):
+        if plan._h is None:
+            raise SlapoError("PipelineExecutor needs a plan from Schedule.apply_pipeline()")
+        self._plan = plan
+        self.micro_batches = micro_batches
+        devs = None
+        if devices is not None:
+            if len(devices) != len(plan.stages):
+                raise SlapoError("one device per stage")
+            devs = (_c.c_int * len(devices))(*devices)
+        h = _P()
+        _check(_lib.sb_pipeline_executor_create(plan._h, micro_batches, int(mode == "train"), seed, _DTYPES[dtype],
+                                                devs, int(fused), _c.byref(h)))
+        self._h = h
+        weakref.finalize(self, _lib.sb_pipeline_executor_free, h)
+
+    def forward(self, inputs: Sequence[np.ndarray]) -> List[np.ndarray]:
+        arrs = [np.ascontiguousarray(np.asarray(x, dtype=np.float64)) for x in inputs]
+        ptrs = (_dp * len(arrs))(*[a.ctypes.data_as(_dp) for a in arrs])
+        _check(_lib.sb_pipeline_executor_forward(self._h, ptrs, len(arrs)))
+        n = _c.c_int()
+        _check(_lib.sb_pipeline_executor_num_outputs(self._h, _c.byref(n)))
+        outs = []
+        for i in range(n.value):
+            nn = _c.c_size_t()
+            dims = (_i64 * 16)()
+            nd = _c.c_int(16)
+            _check(_lib.sb_pipeline_executor_output(self._h, i, None, 0, _c.byref(nn), dims, _c.byref(nd)))
+            a = np.empty(nn.value, dtype=np.float64)
+            _check(_lib.sb_pipeline_executor_output(self._h, i, a.ctypes.data_as(_dp), nn.value, _c.byref(nn), dims,
+                                                    _c.byref(nd)))
+            outs.append(a.reshape([dims[k] for k in range(nd.value)]))
+        return outs
+
+    def backward(self) -> List[GradientMap]:
+        """Per stage: parameter gradients (stage-local names) and the gradients of the
+        model inputs the stage consumes."""
+        _check(_lib.sb_pipeline_executor_backward(self._h))
+        res = []
+        buf = _c.create_string_buffer(4096)
+        for st in range(len(self._plan.stages)):
+            gm = GradientMap()
+            n = _c.c_int()
+            _check(_lib.sb_pipeline_executor_num_grads(self._h, st, _c.byref(n)))
+            for i in range(n.value):
+                _check(_lib.sb_pipeline_executor_grad_name(self._h, st, i, buf, 4096))
+                name = buf.value
+                nn = _c.c_size_t()
+                _check(_lib.sb_pipeline_executor_grad(self._h, st, name, None, 0, _c.byref(nn)))
+                a = np.empty(nn.value, dtype=np.float64)
+                _check(_lib.sb_pipeline_executor_grad(self._h, st, name, a.ctypes.data_as(_dp), nn.value, _c.byref(nn)))
+                gm.params[name.decode()] = a
+            _check(_lib.sb_pipeline_executor_num_input_grads(self._h, st, _c.byref(n)))
+            for i in range(n.value):
+                nn = _c.c_size_t()
+                _check(_lib.sb_pipeline_executor_input_grad(self._h, st, i, None, 0, _c.byref(nn)))
+                a = np.empty(nn.value, dtype=np.float64)
+                _check(_lib.sb_pipeline_executor_input_grad(self._h, st, i, a.ctypes.data_as(_dp), nn.value,
+                                                            _c.byref(nn)))
+                gm.inputs.append(a)
+            res.append(gm)
+        return res
+
+    def time_steps(self, steps: int) -> float:
+        ms = _c.c_float()
+        _check(_lib.sb_pipeline_executor_time_steps(self._h, steps, _c.byref(ms)))
+        return ms.value

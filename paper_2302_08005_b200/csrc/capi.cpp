@@ -13,6 +13,7 @@
 #include "host/rng.hpp"
 #include "host/schedule.hpp"
 #include "host/stages.hpp"
+#include "host/pipeline_exec.hpp"
 #include "host/step_model.hpp"
 
 using namespace sb;
@@ -25,6 +26,11 @@ struct sb_schedule {
 };
 struct sb_pipeline {
     StagePlan p;
+};
+struct sb_pipeline_executor {
+    std::unique_ptr<PipelineExecutor> ex;
+    std::vector<HostTensor> outs;
+    std::vector<GradMap> grads;  // per stage
 };
 struct sb_executor {
     std::unique_ptr<Executor> ex;
@@ -668,4 +674,82 @@ int sb_attn_bwd(const void* q, const void* k, const void* v, const void* o, int6
                           keep_bits, acc_mask, 0, stream);
 }
 
+}  // extern "C"
+
+// ------------------------------------------------------- pipeline executor (f1)
+extern "C" {
+int sb_pipeline_executor_create(const sb_pipeline* p, int micro_batches, int train, uint64_t seed, int dtype,
+                                const int* devices, int fused, sb_pipeline_executor** out) {
+    return guard([&] {
+        std::vector<int> devs;
+        if (devices) devs.assign(devices, devices + p->p.stages.size());
+        auto* e = new sb_pipeline_executor;
+        e->ex = std::make_unique<PipelineExecutor>(p->p, micro_batches, train != 0, seed, dtype ? sbk::BF16 : sbk::F32,
+                                                   devs, fused != 0);
+        *out = e;
+    });
+}
+int sb_pipeline_executor_forward(sb_pipeline_executor* e, const double* const* inputs, int n) {
+    return guard([&] {
+        e->grads.clear();
+        e->outs = e->ex->forward_raw(inputs, n);
+    });
+}
+int sb_pipeline_executor_num_outputs(sb_pipeline_executor* e, int* n) {
+    return guard([&] { *n = (int)e->outs.size(); });
+}
+int sb_pipeline_executor_output(sb_pipeline_executor* e, int idx, double* out, size_t cap, size_t* n, int64_t* dims,
+                                int* ndims) {
+    return guard([&] {
+        auto& t = e->outs.at((size_t)idx);
+        if (dims && ndims) {
+            if (*ndims < (int)t.spec.shape.size()) throw Error("dims buffer too small");
+            for (size_t i = 0; i < t.spec.shape.size(); ++i) dims[i] = t.spec.shape[i];
+            *ndims = (int)t.spec.shape.size();
+        }
+        copy_out(t.data, out, cap, n);
+    });
+}
+int sb_pipeline_executor_backward(sb_pipeline_executor* e) {
+    return guard([&] { e->grads = e->ex->backward(); });
+}
+static GradMap& pgmap(sb_pipeline_executor* e, int stage) {
+    if (e->grads.empty()) throw Error("no gradients: call backward first");
+    if (stage < 0 || stage >= (int)e->grads.size()) throw Error("stage index out of range");
+    return e->grads[(size_t)stage];
+}
+int sb_pipeline_executor_num_grads(sb_pipeline_executor* e, int stage, int* n) {
+    return guard([&] { *n = (int)pgmap(e, stage).params.size(); });
+}
+int sb_pipeline_executor_grad_name(sb_pipeline_executor* e, int stage, int idx, char* buf, size_t cap) {
+    return guard([&] {
+        auto& g = pgmap(e, stage);
+        if (idx < 0 || idx >= (int)g.params.size()) throw Error("grad index out of range");
+        auto it = g.params.begin();
+        std::advance(it, idx);
+        if (cap < it->first.size() + 1) throw Error("name buffer too small");
+        std::memcpy(buf, it->first.c_str(), it->first.size() + 1);
+    });
+}
+int sb_pipeline_executor_grad(sb_pipeline_executor* e, int stage, const char* dotted, double* out, size_t cap, size_t* n) {
+    return guard([&] {
+        auto& g = pgmap(e, stage);
+        auto it = g.params.find(dotted);
+        if (it == g.params.end()) throw Error(std::string("no gradient for '") + dotted + "'");
+        copy_out(it->second.data, out, cap, n);
+    });
+}
+int sb_pipeline_executor_num_input_grads(sb_pipeline_executor* e, int stage, int* n) {
+    return guard([&] { *n = (int)pgmap(e, stage).inputs.size(); });
+}
+int sb_pipeline_executor_input_grad(sb_pipeline_executor* e, int stage, int idx, double* out, size_t cap, size_t* n) {
+    return guard([&] { copy_out(pgmap(e, stage).inputs.at((size_t)idx).data, out, cap, n); });
+}
+int sb_pipeline_executor_time_steps(sb_pipeline_executor* e, int steps, float* ms) {
+    return guard([&] { *ms = e->ex->time_steps(steps); });
+}
+int sb_pipeline_executor_free(sb_pipeline_executor* e) {
+    delete e;
+    return 0;
+}
 }  // extern "C"

@@ -104,6 +104,11 @@ public:
     ncclComm_t ncomm = nullptr;
     i64 collectives = 0;
     bool ran_forward = false;
+    // pipeline stages (f1): parameter gradients accumulate across backward calls
+    // (micro-batches) instead of being overwritten, and output gradients can be
+    // seeded from device buffers (the next stage's input gradients) instead of ones
+    bool accum_params = false;
+    std::vector<std::pair<const void*, DT>> out_seed;
     cudaGraphExec_t gexec = nullptr;
     cudaGraph_t graph = nullptr;
     int launches = 0;
@@ -346,6 +351,15 @@ public:
         const Plan& P = ranks[0].P;
         std::map<int, std::vector<Span>> written;
         std::vector<char> need(P.st.size(), 0);
+        std::set<int> param_gst;
+        for (auto& pv : P.params) param_gst.insert(P.views[(size_t)pv.second].gst);
+        if (accum_params)  // every parameter-gradient write accumulates onto the previous micro-batches'
+            for (int g : param_gst) {
+                Span full{};
+                full.hi = P.st[(size_t)g].numel;
+                full.n = P.st[(size_t)g].numel;
+                written[g].push_back(full);
+            }
         auto covered = [&](int gst, const Span& r) {
             auto& w = written[gst];
             for (auto& s : w)
@@ -393,7 +407,7 @@ public:
         zero_gst.clear();
         region_zero.assign(P.regions.size(), 0);
         for (size_t g = 0; g < P.st.size(); ++g) {
-            if (!need[g]) continue;
+            if (!need[g] || (accum_params && param_gst.count((int)g))) continue;  // (zeroed by zero_param_grads)
             if (P.st[g].region >= 0) region_zero[(size_t)P.st[g].region] = 1;
             else zero_gst.push_back((int)g);
         }
@@ -1573,9 +1587,15 @@ public:
             // zero only what is read/accumulated before being fully written (analyze_writes)
             for (auto& [off, bytes] : zero_ranges(r)) CK(cudaMemsetAsync(r.base + off, 0, bytes, stream));
             // loss = sum of outputs: seed ones (executor.cpp:355-362)
-            for (int v : r.P.outputs) {
+            for (size_t k = 0; k < r.P.outputs.size(); ++k) {
+                const int v = r.P.outputs[k];
                 if (!V(r, v).g_contiguous()) throw Error("internal: strided model output gradient");
-                if (seed_ow.count(v) && seed_ow[v]) sbk::fill(gp(r, v), gdt(r, v), V(r, v).numel(), 1.f, stream);
+                const bool ow = seed_ow.count(v) && seed_ow[v];
+                if (k < out_seed.size() && out_seed[k].first) {  // seeded by the caller (pipeline stage)
+                    const i64 n = V(r, v).numel(), one = 1;
+                    sbk::strided_copy(out_seed[k].first, out_seed[k].second, &one, gp(r, v), gdt(r, v), &one, &n, 1, !ow,
+                                      stream);
+                } else if (ow) sbk::fill(gp(r, v), gdt(r, v), V(r, v).numel(), 1.f, stream);
                 else sbk::add_scalar(gp(r, v), gdt(r, v), V(r, v).numel(), 1.f, nullptr, stream);
                 ++launches;
             }
@@ -1769,6 +1789,70 @@ std::vector<GradMap> Executor::backward_all_ranks() {
 GradMap Executor::backward() { return backward_all_ranks()[0]; }
 i64 Executor::ledger_bytes() const { return impl_->ranks[0].P.ledger_bytes; }
 i64 Executor::collective_invocations() const { return impl_->collectives; }
+
+// ---- pipeline-stage hooks (csrc/host/pipeline_exec.cpp) ----
+void Executor::set_accumulate_param_grads(bool on) {
+    auto& I = *impl_;
+    if (I.accum_params == on) return;
+    if (I.gexec) throw Error("set_accumulate_param_grads: the step graph is already captured");
+    I.accum_params = on;
+    I.analyze_writes();
+}
+void Executor::zero_param_grads() {
+    auto& I = *impl_;
+    for (auto& r : I.ranks) {
+        std::set<int> done;
+        for (auto& pv : r.P.params) {
+            const int g = r.P.views[(size_t)pv.second].gst;
+            if (!done.insert(g).second || !r.gptr[(size_t)g]) continue;
+            CK(cudaMemsetAsync(r.gptr[(size_t)g], 0, (size_t)r.P.st[(size_t)g].numel * sbk::dt_bytes(r.P.st[(size_t)g].gdt),
+                               I.stream));
+        }
+    }
+}
+void Executor::set_output_grad_seed(int idx, const void* dptr, DT dt) {
+    auto& I = *impl_;
+    if (idx < 0 || idx >= (int)I.ranks[0].P.outputs.size()) throw Error("set_output_grad_seed: output index out of range");
+    if (I.world > 1 && !I.comm.nccl) throw Error("set_output_grad_seed: one rank per executor only");
+    if (I.out_seed.size() < I.ranks[0].P.outputs.size()) I.out_seed.resize(I.ranks[0].P.outputs.size(), {nullptr, sbk::F32});
+    I.out_seed[(size_t)idx] = {dptr, dt};
+}
+DeviceTensor Executor::output_device(int idx) const {
+    auto& I = *impl_;
+    RankCtx& r = I.ranks[0];
+    if (idx < 0 || idx >= (int)r.P.outputs.size()) throw Error("output index out of range");
+    const int v = r.P.outputs[(size_t)idx];
+    if (!I.V(r, v).contiguous()) throw Error("internal: strided output");
+    return {I.fp(r, v), I.fdt(r, v), I.V(r, v).numel(), I.V(r, v).shape};
+}
+DeviceTensor Executor::input_grad_device(int idx) const {
+    auto& I = *impl_;
+    RankCtx& r = I.ranks[0];
+    if (idx < 0 || idx >= (int)r.P.inputs.size()) throw Error("input index out of range");
+    const int v = r.P.inputs[(size_t)idx];
+    if (!I.V(r, v).g_contiguous()) throw Error("internal: strided input gradient");
+    return {I.gp(r, v), I.gdt(r, v), I.V(r, v).numel(), I.V(r, v).shape};
+}
+void Executor::set_input_from_device(int idx, const void* src, DT dt) {
+    auto& I = *impl_;
+    for (auto& r : I.ranks) {
+        const int v = r.P.inputs[(size_t)idx];
+        const i64 n = I.V(r, v).numel(), one = 1;
+        sbk::strided_copy(src, dt, &one, I.fp(r, v), I.fdt(r, v), &one, &n, 1, false, I.stream);
+    }
+}
+std::vector<GradMap> Executor::grads_all_ranks() {
+    auto& I = *impl_;
+    synchronize();
+    std::vector<GradMap> maps;
+    for (auto& r : I.ranks) {
+        GradMap m;
+        for (auto& [name, v] : r.P.params) m.params[name] = download(I, r, v, true);
+        for (int v : r.P.inputs) m.inputs.push_back(download(I, r, v, true));
+        maps.push_back(std::move(m));
+    }
+    return maps;
+}
 
 void Executor::enqueue_loss(float* dloss) {
     auto& I = *impl_;

@@ -37,6 +37,14 @@ struct GradMap {
 
 class ExecutorImpl;
 
+// a device-resident tensor of an executor (contiguous)
+struct DeviceTensor {
+    void* ptr;
+    DT dt;
+    i64 numel;
+    std::vector<i64> shape;
+};
+
 class Executor {
 public:
     Executor(const Module& root, bool train, u64 seed, int world, DT compute, const CommConfig& comm = {},
@@ -72,6 +80,15 @@ public:
     // kernel-level timing of one op kind (bench roofline): returns the ms of
     // all launches of op kind `k` inside one forward+backward, measured with events.
     std::vector<std::pair<std::string, float>> profile_step();
+
+    // ---- pipeline-stage hooks (f1, csrc/host/pipeline_exec.cpp) ----
+    void set_accumulate_param_grads(bool on);  // parameter gradients += across backward calls
+    void zero_param_grads();                   // (enqueued)
+    void set_output_grad_seed(int idx, const void* dptr, DT dt);  // backward seeds output idx from dptr (nullptr: ones)
+    DeviceTensor output_device(int idx) const;
+    DeviceTensor input_grad_device(int idx) const;
+    void set_input_from_device(int idx, const void* src, DT dt);  // (enqueued) cast into input idx
+    std::vector<GradMap> grads_all_ranks();                        // download the current gradients
 
 private:
     std::unique_ptr<ExecutorImpl> impl_;

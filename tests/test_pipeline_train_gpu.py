@@ -1,0 +1,126 @@
+"""Pipeline-parallel training step (f1; csrc/host/pipeline_exec.cpp) against the
+reference executor.
+
+The reference's run_pipeline (proj/src/executor.cpp:1531-1579) is forward-only;
+its training-step semantics follow from it: micro-batch m of every stage runs
+the stage module with the executor seed on micro-batch-shaped tensors, and the
+loss is the sum of all outputs. So
+  * verify mode (no dropout): the pipelined gradients equal the reference's
+    full-batch gradients of the unsplit model (sum over micro-batches of a
+    per-sample model);
+  * train mode: they equal the sum over micro-batches of the reference's
+    gradients of the unsplit model run on that micro-batch (same seed, same
+    micro-batch-local dropout indices as run_pipeline's stages).
+Stage parameters carry the partitioner's names (encoder_p0.layer_p0.0...); they
+map back to the model's by dropping the _p<k> suffixes.
+"""
+import re
+
+import numpy as np
+import pytest
+
+import paper_2302_08005_b200 as sb
+from paper_2302_08005_b200 import recipes
+from oracle import ref
+from tests.helpers import BF16_GRAD_TOL, BF16_OUT_TOL, compare_grads, rel_err, rel_l2
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not ref.available(), reason="oracle not built")]
+
+SPLIT1 = "trace encoder.layer\npipeline_split encoder.layer after=1\n"
+SPLIT02 = "trace encoder.layer\npipeline_split encoder.layer after=0\npipeline_split encoder.layer after=2\n"
+
+
+def _plan(cfg, script):
+    m = sb.toy_bert(cfg["layers"], cfg["hidden"], cfg["heads"], cfg["vocab"], cfg["batch"], cfg["seq"], cfg["p"])
+    s = sb.create_schedule(m, 2)  # pipeline_split needs a distributed world (R2); stages run at world 1
+    s.load_script(script)
+    return m, s.apply_pipeline()
+
+
+def _merged(stage_grads):
+    out = {}
+    for g in stage_grads:
+        for k, v in g.params.items():
+            name = re.sub(r"_p\d+(?=\.|$)", "", k)
+            assert name not in out, name
+            out[name] = v
+    return out
+
+
+def _ref_grads(cfg, mode, seed, input_seed, micro=1, x=None, dtype="f64", schedule=None):
+    """reference gradients of the unsplit model: full batch (micro=1) or the sum over
+    micro-batches of runs on each micro-batch's inputs"""
+    if micro == 1:
+        with ref.run("toy_bert", schedule=schedule, mode=mode, seed=seed, input_seed=input_seed, dtype=dtype,
+                     **cfg) as r:
+            return r.outputs(0), r.grads(0)
+    per = cfg["batch"] // micro
+    tot, outs = None, []
+    for mb in range(micro):
+        c = dict(cfg, batch=per)
+        with ref.run("toy_bert", mode=mode, seed=seed, inputs=[x[mb * per:(mb + 1) * per]], dtype=dtype, **c) as r:
+            g = r.grads(0)
+            outs.append(r.outputs(0)[0])
+        tot = g if tot is None else {k: tot[k] + g[k] for k in tot}
+    return [np.concatenate(outs, 0)], tot
+
+
+CFG = dict(layers=4, hidden=32, heads=4, vocab=32, batch=4, seq=8, p=0.1)
+
+
+@pytest.mark.parametrize("script,micro", [(SPLIT1, 1), (SPLIT1, 2), (SPLIT02, 4)])
+def test_pipeline_step_verify_equals_full_batch(script, micro):
+    m, plan = _plan(CFG, script)
+    x = m.random_inputs(9)
+    pe = sb.PipelineExecutor(plan, micro, "verify", 123, "fp32")
+    out = pe.forward(x)
+    grads = _merged(pe.backward())
+    want_out, want = _ref_grads(CFG, "verify", 123, 9)
+    assert rel_err(out[0], want_out[0]) <= 1e-4
+    compare_grads(grads, {k: v.ravel() for k, v in want.items()}, 1e-4)
+
+
+@pytest.mark.parametrize("micro", [1, 2])
+def test_pipeline_step_train_equals_micro_batch_sum(micro):
+    m, plan = _plan(CFG, SPLIT1)
+    x = m.random_inputs(9)
+    pe = sb.PipelineExecutor(plan, micro, "train", 123, "fp32")
+    out = pe.forward(x)
+    grads = _merged(pe.backward())
+    want_out, want = _ref_grads(CFG, "train", 123, 9, micro, x[0])
+    assert rel_err(out[0], want_out[0]) <= 1e-4
+    compare_grads(grads, {k: v.ravel() for k, v in want.items()}, 1e-4)
+    # a second step (stashes, seeds and accumulators reused) gives the same gradients
+    pe.forward(x)
+    again = _merged(pe.backward())
+    for k in grads:
+        assert np.array_equal(grads[k], again[k]), k
+
+
+def test_pipeline_step_bf16_tcgen05():
+    """C2's fused + flash-attention schedule split in two stages, bf16 on the tcgen05
+    kernels, 2 micro-batches, verify mode vs the reference's full batch"""
+    cfg = dict(layers=2, hidden=256, heads=4, vocab=64, batch=8, seq=128, p=0.1)
+    m, plan = _plan(cfg, recipes.c2_script(2) + SPLIT1.replace("after=1", "after=0"))
+    x = m.random_inputs(9)
+    pe = sb.PipelineExecutor(plan, 2, "verify", 123, "bf16")
+    out = pe.forward(x)
+    grads = _merged(pe.backward())
+    assert sb.lib().sb_attn_engine(1) == 3 and sb.lib().sb_gemm_engine() == 2
+    want_out, want = _ref_grads(cfg, "verify", 123, 9, schedule=recipes.c2_script(2))  # (fused module names)
+    assert rel_l2(out[0], want_out[0]) <= BF16_OUT_TOL
+    compare_grads(grads, {k: v.ravel() for k, v in want.items()}, BF16_GRAD_TOL, rel_l2)
+
+
+def test_pipeline_timing_and_errors():
+    m, plan = _plan(CFG, SPLIT02)
+    pe = sb.PipelineExecutor(plan, 2, "train", 1, "fp32")
+    with pytest.raises(sb.SlapoError):
+        pe.backward()  # before any forward
+    pe.forward(m.random_inputs(3))
+    ms = pe.time_steps(3)
+    assert ms > 0
+    with pytest.raises(sb.SlapoError, match="micro-batches"):
+        sb.PipelineExecutor(plan, 3, "train", 1, "fp32")  # batch 4 is not divisible by 3
+    with pytest.raises(sb.SlapoError, match="one device per stage"):
+        sb.PipelineExecutor(plan, 2, "train", 1, "fp32", devices=[0])
