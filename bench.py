@@ -314,7 +314,7 @@ def main():
                      "achieved": achieved, "peak": sustained, "unit": "TFLOP/s", "frac": achieved / sustained,
                      "peak_source": f"bf16_tflops_sustained ({src})", "traffic": traffic,
                      "traffic_unit": "DRAM bytes per step of all GEMM launches (ncu, profiles/r1_gemm_traffic.json)",
-                     "algorithmic_flop_per_byte": (gemm_tflop * 1e12 / traffic) if traffic else None,
+                     "flop_per_dram_byte": (gemm_tflop * 1e12 / traffic) if traffic else None,
                      "gemm_ms_per_step": gemm_ms, "gemm_tflop_per_step": gemm_tflop},
         "model_tflops": model_tflops, "model_flops_frac": model_tflops / sustained,
         "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": int(host_ids.nbytes),

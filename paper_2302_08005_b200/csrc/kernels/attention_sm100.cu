@@ -657,18 +657,20 @@ __device__ __forceinline__ unsigned long long gtime() {
     return t;
 }
 
-// delta = rowsum(dO * O) and lse2 = lse * log2(e); 8 threads per (b, h, query) row
+// delta = rowsum(dO * O) and lse2 = lse * log2(e); D/8 threads per (b, h, query) row
+template <int D = FD>
 __global__ void k_fa5_prep(const bf16* dout, long long ld_do, const bf16* o, long long ld_o, const float* lse,
                            float* lse2, float* delta, long long BH, int S, int nh, float sgn) {
+    constexpr int TPR = D / 8;
     const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    const long long idx = tid >> 3;
-    const int part = (int)(tid & 7);
+    const long long idx = tid / TPR;
+    const int part = (int)(tid % TPR);
     const bool ok = idx < BH * S;
     float acc = 0.f;
     if (ok) {
         const long long bh = idx / S, q = idx % S, b = bh / nh, h = bh % nh;
-        const uint4 a = *((const uint4*)(dout + (b * S + q) * ld_do + h * FD) + part);
-        const uint4 c = *((const uint4*)(o + (b * S + q) * ld_o + h * FD) + part);
+        const uint4 a = *((const uint4*)(dout + (b * S + q) * ld_do + h * D) + part);
+        const uint4 c = *((const uint4*)(o + (b * S + q) * ld_o + h * D) + part);
         const __nv_bfloat162* pa = (const __nv_bfloat162*)&a;
         const __nv_bfloat162* pc = (const __nv_bfloat162*)&c;
 #pragma unroll
@@ -677,9 +679,8 @@ __global__ void k_fa5_prep(const bf16* dout, long long ld_do, const bf16* o, lon
             acc = fmaf(fa.x, fc.x, fmaf(fa.y, fc.y, acc));
         }
     }
-    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-    acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+#pragma unroll
+    for (int m = 1; m < TPR; m <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m);
     if (ok && part == 0) {
         delta[idx] = sgn * acc;
         lse2[idx] = sgn * lse[idx] * 1.4426950408889634f;
@@ -1588,6 +1589,400 @@ __global__ void __launch_bounds__(B7_WARPS * 32, 1)
     }
 }
 
+// ------------------------------------------------------- backward, head_dim 128
+// The v7 recurrence re-laid-out for head_dim 128 (GPT-Neo, BASELINE.json C4),
+// where dV, dK (128 keys x 128 fp32 each) and dQ leave no TMEM for K/V operands:
+//   * CTA = (batch, head); key blocks j of 128 (outer), query blocks i of 64
+//     (inner), each in two halves of 32 queries (one half's softmax overlaps the
+//     other half's MMAs);
+//   * S^T = K Q^T and dP^T = V dO^T are SS MMAs (M128 N32, K = 128 over the two
+//     64-column panels of K / V and of the Q / dO stage);
+//   * Z^T and dS^T overwrite the S^T columns they came from (bf16 pairs) and feed
+//     dV += Z^T dO and dK += dS^T Q as TS MMAs (M128 N128, B MN-major over both
+//     panels: LBO = one panel);
+//   * dQ^T = K^T dS^T (M128 = head dims, N64 = queries, SS: K read MN-major,
+//     LBO = one K panel; dS^T from shared memory) by its own issuer warp; 4 dQ
+//     warps (thread = head dim) add it into the CTA's private fp32 accumulator
+//     (stored at a query block's first key block, red.global.add after, read back
+//     at the last: every address has one writer in program order — deterministic);
+//   * K double-buffered, V single-buffered (the next V loads after the block's
+//     last dP^T MMA), dK / dV drained by the softmax warps while the next key
+//     block starts.
+// TMEM: S^T [0,64), dP^T [64,128), dV [128,256), dK [256,384), dQ^T [384,448).
+constexpr int B8_D = 128, B8_QT = 64;                          // head dim, queries per step
+constexpr int B8_KV = FT * B8_D * 2;                           // 32 KB: K or V tile (2 panels of 16 KB)
+constexpr int B8_QP = B8_QT * 128;                             // 8 KB: one 64-column panel of a Q / dO stage
+// Q, dO, lse2[64], delta[64], keep bits [128 keys][4 words]: the 128-query word span holding this
+// block's 64 (a TMA box row must be a multiple of 16 bytes)
+constexpr int B8_STAGE_RAW = 4 * B8_QP + 2 * B8_QT * 4 + FT * 16;
+constexpr int B8_STAGE = (B8_STAGE_RAW + 1023) & ~1023;
+constexpr int B8_NST = 2;
+constexpr int B8_DS = FT * B8_QT * 2;                          // 16 KB: dS^T [128 keys][64 queries] bf16
+constexpr int B8_SMEM = 1024 + 2 * B8_KV + B8_KV + B8_NST * B8_STAGE + 2 * B8_DS + 256;
+constexpr int B8_WARPS = 15;                                   // 8 softmax, 4 dQ, producer, MMA, dQ-MMA
+constexpr int W8_PROD = 12, W8_MMA = 13, W8_DQMMA = 14;
+
+// step u -> (key block j of 128, query block i of 64): all pairs, or for causal
+// attention the i >= 2j ones (the block's last query is at or after its first key)
+template <bool CAUSAL>
+__device__ __forceinline__ void step_ji8(int u, int nj, int nq, int& j, int& i) {
+    if (!CAUSAL) {
+        j = u / nq;
+        i = u % nq;
+        return;
+    }
+    j = 0;
+    int cnt = nq;
+    while (u >= cnt) {
+        u -= cnt;
+        ++j;
+        cnt -= 2;
+    }
+    i = 2 * j + u;
+}
+
+template <bool CAUSAL>
+__global__ void __launch_bounds__(B8_WARPS * 32, 1)
+    k_fa8_bwd(const __grid_constant__ CUtensorMap tK, const __grid_constant__ CUtensorMap tV,
+              const __grid_constant__ CUtensorMap tQ, const __grid_constant__ CUtensorMap tdO,
+              const __grid_constant__ CUtensorMap tM, BwdArgs ba) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024 - (tc5::smem_u32(smem_raw) & 1023)) & 1023);
+    uint8_t* sK = smem;                      // [2] K_j: 2 panels [128 keys][64 dims]
+    uint8_t* sV = sK + 2 * B8_KV;            // V_j
+    uint8_t* sStage = sV + B8_KV;            // [B8_NST][B8_STAGE]
+    uint8_t* sDS = sStage + B8_NST * B8_STAGE;  // [2] dS^T
+    uint64_t* bars = (uint64_t*)(sDS + 2 * B8_DS);
+    uint64_t* k_full = bars;                 // [2]
+    uint64_t* k_empty = bars + 2;            // [2] (dQ of its block done)
+    uint64_t* v_full = bars + 4;
+    uint64_t* v_empty = bars + 5;            // the block's last dP^T MMA done
+    uint64_t* st_full = bars + 6;            // [B8_NST]
+    uint64_t* st_empty = st_full + B8_NST;   // [B8_NST]
+    uint64_t* sdp_full = st_empty + B8_NST;  // [2 halves]
+    uint64_t* sm_done = sdp_full + 2;        // [2 halves]
+    uint64_t* dq_full = sm_done + 2;
+    uint64_t* dq_free = dq_full + 1;
+    uint64_t* acc_full = dq_free + 1;
+    uint64_t* acc_free = acc_full + 1;
+    uint64_t* ds_free = acc_free + 1;        // [2]
+    uint64_t* ds_full = ds_free + 2;         // [2]
+    uint32_t* tslot = (uint32_t*)(ds_full + 2);
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int S = ba.S, nj = S / FT, nq = S / B8_QT;
+    int nsteps = nj * nq;
+    if (CAUSAL) {
+        nsteps = 0;
+        for (int j = 0; j < nj; ++j) nsteps += nq - 2 * j;
+    }
+    auto first_i = [&](int j) { return CAUSAL ? 2 * j : 0; };
+    const int h = blockIdx.x, b = blockIdx.y;
+    const long long bh = (long long)b * ba.nh + h;
+    const int row_base = b * S;
+
+    if (threadIdx.x == 0) {
+        for (int x = 0; x < 2; ++x) {
+            mbar_init(&k_full[x], 1);
+            mbar_init(&k_empty[x], 1);
+            mbar_init(&sdp_full[x], 1);
+            mbar_init(&sm_done[x], 8);
+            mbar_init(&ds_free[x], 1);
+            mbar_init(&ds_full[x], 8);
+        }
+        mbar_init(v_full, 1);
+        mbar_init(v_empty, 1);
+        for (int s = 0; s < B8_NST; ++s) {
+            mbar_init(&st_full[s], 1);
+            mbar_init(&st_empty[s], 1);
+        }
+        mbar_init(dq_full, 1);
+        mbar_init(dq_free, 4);
+        mbar_init(acc_full, 1);
+        mbar_init(acc_free, 8);
+        fence_barrier_init();
+    }
+    if (warp == W8_MMA) tmem_alloc<512>(tslot);
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem = *tslot;
+
+    if (warp == W8_PROD) {
+        if (lane == 0) {
+            // ------------------------------------------------ TMA producer
+            auto load_k = [&](int j) {
+                const int kb = j & 1;
+                if (j >= 2) mbar_wait(&k_empty[kb], ((j >> 1) - 1) & 1);
+                mbar_expect_tx(&k_full[kb], B8_KV);
+                for (int p = 0; p < 2; ++p)
+                    tma_load_2d(sK + kb * B8_KV + p * (B8_KV / 2), &tK, &k_full[kb], h * B8_D + 64 * p, row_base + j * FT);
+            };
+            auto load_v = [&](int j) {
+                if (j >= 1) mbar_wait(v_empty, (j - 1) & 1);
+                mbar_expect_tx(v_full, B8_KV);
+                for (int p = 0; p < 2; ++p)
+                    tma_load_2d(sV + p * (B8_KV / 2), &tV, v_full, h * B8_D + 64 * p, row_base + j * FT);
+            };
+            load_k(0);
+            load_v(0);
+            for (int u = 0; u < nsteps; ++u) {
+                int j, i;
+                step_ji8<CAUSAL>(u, nj, nq, j, i);
+                const int s = u % B8_NST;
+                uint8_t* st = sStage + s * B8_STAGE;
+                mbar_wait(&st_empty[s], ((u / B8_NST) & 1) ^ 1);
+                mbar_expect_tx(&st_full[s], 4 * B8_QP + 2 * B8_QT * 4 + (ba.mask_t ? FT * 16 : 0));
+                for (int p = 0; p < 2; ++p) {
+                    tma_load_2d(st + p * B8_QP, &tQ, &st_full[s], h * B8_D + 64 * p, row_base + i * B8_QT);
+                    tma_load_2d(st + (2 + p) * B8_QP, &tdO, &st_full[s], h * B8_D + 64 * p, row_base + i * B8_QT);
+                }
+                bulk_load(st + 4 * B8_QP, ba.lse2 + bh * S + i * B8_QT, B8_QT * 4, &st_full[s]);
+                bulk_load(st + 4 * B8_QP + B8_QT * 4, ba.delta + bh * S + i * B8_QT, B8_QT * 4, &st_full[s]);
+                if (ba.mask_t)
+                    tma_load_2d(st + 4 * B8_QP + 2 * B8_QT * 4, &tM, &st_full[s], (i >> 1) * 4, (int)(bh * S) + j * FT);
+                // K_{j+1} into the other buffer once block j is under way (its previous user,
+                // block j-1, releases it with its last dQ); V_{j+1} after block j's last stage
+                if (j + 1 < nj && i == first_i(j) + (nq - first_i(j) > 1 ? 1 : 0)) load_k(j + 1);
+                if (i == nq - 1 && j + 1 < nj) load_v(j + 1);
+            }
+        }
+    } else if (warp == W8_MMA) {
+        // ------------------------------------------------ MMA issuer (elected lane)
+        constexpr uint32_t id_s = idesc_bf16(FT, 32, false, false);   // S^T / dP^T half: M128 N32
+        constexpr uint32_t id_kv = idesc_bf16(FT, B8_D, false, true);  // dV / dK: M128 N128, B MN-major
+        const bool mm = !(ba.dbg & 4);
+        const uint32_t stage0 = smem_u32(sStage), k0 = smem_u32(sK), v0 = smem_u32(sV);
+        auto issue_sdp = [&](int u, int hh) {
+            int j, i;
+            step_ji8<CAUSAL>(u, nj, nq, j, i);
+            const int s = u % B8_NST;
+            const uint32_t aQ = stage0 + s * B8_STAGE, adO = aQ + 2 * B8_QP;
+            if (hh == 0) {
+                if (i == first_i(j)) {
+                    mbar_wait(&k_full[j & 1], (j >> 1) & 1);
+                    mbar_wait(v_full, j & 1);
+                }
+                mbar_wait(&st_full[s], (u / B8_NST) & 1);
+                fence_after();
+            }
+            if (mm) {
+                const uint32_t ak = k0 + (j & 1) * B8_KV;
+#pragma unroll
+                for (int kk = 0; kk < B8_D / 16; ++kk)  // S^T half = K Q_half^T
+                    mma_ss_w(tmem + hh * 32, desc_kmajor(ak + (kk >> 2) * (B8_KV / 2), kk & 3),
+                             desc_kmajor(aQ + (kk >> 2) * B8_QP + hh * 4096, kk & 3), id_s, kk);
+#pragma unroll
+                for (int kk = 0; kk < B8_D / 16; ++kk)  // dP^T half = V dO_half^T
+                    mma_ss_w(tmem + 64 + hh * 32, desc_kmajor(v0 + (kk >> 2) * (B8_KV / 2), kk & 3),
+                             desc_kmajor(adO + (kk >> 2) * B8_QP + hh * 4096, kk & 3), id_s, kk);
+            }
+            mma_commit_w(&sdp_full[hh]);
+            if (hh == 1 && i == nq - 1) mma_commit_w(v_empty);  // V_j read for the last time
+        };
+        issue_sdp(0, 0);
+        issue_sdp(0, 1);
+        for (int u = 0; u < nsteps; ++u) {
+            int j, i;
+            step_ji8<CAUSAL>(u, nj, nq, j, i);
+            const int s = u % B8_NST;
+            const int acc0 = i != first_i(j);
+            const uint32_t aQ = stage0 + s * B8_STAGE, adO = aQ + 2 * B8_QP;
+#pragma unroll 1
+            for (int hh = 0; hh < 2; ++hh) {
+                mbar_wait(&sm_done[hh], u & 1);
+                if (hh == 0 && i == first_i(j) && j > 0) mbar_wait(acc_free, (j - 1) & 1);
+                fence_after();
+                if (mm) {
+#pragma unroll
+                    for (int k2 = 0; k2 < 2; ++k2)  // dV += Z^T_half dO_half (Z^T: 8 cols per 16 queries)
+                        mma_ts_w(tmem + 128, tmem + hh * 32 + k2 * 16, desc_mnmajor(adO, 2 * hh + k2), id_kv,
+                                 acc0 | hh | k2);
+#pragma unroll
+                    for (int k2 = 0; k2 < 2; ++k2)  // dK += dS^T_half Q_half
+                        mma_ts_w(tmem + 256, tmem + hh * 32 + k2 * 16 + 8, desc_mnmajor(aQ, 2 * hh + k2), id_kv,
+                                 acc0 | hh | k2);
+                }
+                if (hh == 1) {
+                    mma_commit_w(&st_empty[s]);
+                    if (i == nq - 1) mma_commit_w(acc_full);
+                }
+                if (u + 1 < nsteps) issue_sdp(u + 1, hh);
+            }
+        }
+    } else if (warp == W8_DQMMA) {
+        // ------------------------------------------------ dQ^T = K^T dS^T issuer
+        constexpr uint32_t id_q = idesc_bf16(FT, B8_QT, true, true);  // M128 (dims) N64 (queries), both MN-major
+        const bool mm = !(ba.dbg & 4);
+        const uint32_t ds0 = smem_u32(sDS), k0 = smem_u32(sK);
+        for (int u = 0; u < nsteps; ++u) {
+            int j, i;
+            step_ji8<CAUSAL>(u, nj, nq, j, i);
+            mbar_wait(&ds_full[u & 1], (u >> 1) & 1);
+            if (u > 0) mbar_wait(dq_free, (u - 1) & 1);
+            fence_after();
+            if (mm) {
+                const uint32_t ak = k0 + (j & 1) * B8_KV, ad = ds0 + (u & 1) * B8_DS;
+#pragma unroll
+                for (int kk = 0; kk < FT / 16; ++kk)  // 16 keys per step: 16 rows of 128 B
+                    mma_ss_w(tmem + 384, sdesc(ak + kk * 2048, (B8_KV / 2) >> 4, 1024 >> 4), desc_mnmajor(ad, kk), id_q,
+                             kk);
+            }
+            mma_commit_w(dq_full);
+            mma_commit_w(&ds_free[u & 1]);
+            if (i == nq - 1) mma_commit_w(&k_empty[j & 1]);
+        }
+    } else if (warp < 8) {
+        // ------------------------------------------------ 8 softmax warps: lane quarter q4
+        // (key rows), column group cg = 16 of the 32 queries of each half
+        const int q4 = warp & 3, cg = warp >> 2, k = q4 * 32 + lane;
+        const uint32_t t_lane = tmem + ((uint32_t)(q4 * 32) << 16);
+        // dV_j (cg 0) / dK_j (cg 1): this thread's key row, 128 columns in four chunks
+        auto drain_kv = [&](int j) {
+            mbar_wait(acc_full, j & 1);
+            fence_after();
+            const long long row = row_base + (long long)j * FT + k;
+            const bool acc = cg == 1 ? (ba.acc & 2) : (ba.acc & 4);
+            bf16* dst = cg == 1 ? ba.dk + row * ba.ld_dk + (long long)h * B8_D : ba.dv + row * ba.ld_dv + (long long)h * B8_D;
+            const float sc = cg == 1 ? ba.scale : 1.f;
+#pragma unroll 1
+            for (int c = 0; c < 4; ++c) {
+                uint32_t r[32];
+                tmem_ld32_nowait(t_lane + 128 + cg * 128 + c * 32, r);
+                tmem_ld_wait();
+                if (c == 3) {
+                    fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(acc_free);
+                }
+                float f[32];
+#pragma unroll
+                for (int e = 0; e < 32; ++e) f[e] = __uint_as_float(r[e]);
+                if (!(ba.dbg & 32)) store_row_bf16(dst + c * 32, f, 4, sc, acc);
+            }
+        };
+        for (int u = 0; u < nsteps; ++u) {
+            int j, i;
+            step_ji8<CAUSAL>(u, nj, nq, j, i);
+            const int s = u % B8_NST;
+            const uint8_t* st = sStage + s * B8_STAGE;
+            const float* lse_s = (const float*)(st + 4 * B8_QP);
+            const float* dl_s = lse_s + B8_QT;
+            uint8_t* ds_buf = sDS + (u & 1) * B8_DS;
+            mbar_wait(&st_full[s], (u / B8_NST) & 1);
+#pragma unroll 1
+            for (int hh = 0; hh < 2; ++hh) {
+                const int q0 = hh * 32 + cg * 16;  // first query (of the 64) of this thread's columns
+                mbar_wait(&sdp_full[hh], u & 1);
+                fence_after();
+                uint32_t sv[16], dp[16];
+                tmem_ld16_nowait(t_lane + q0, sv);
+                tmem_ld16_nowait(t_lane + 64 + q0, dp);
+                const uint32_t mword =
+                    ba.mask_t ? *(const uint32_t*)(st + 4 * B8_QP + 2 * B8_QT * 4 + k * 16 + ((i & 1) * 2 + hh) * 4) >> (cg * 16)
+                              : 0xFFFFu;
+                tmem_ld_wait();
+                if (CAUSAL && i <= 2 * j + 1) {  // diagonal blocks: key k sees queries at or after it
+                    const int qd = i * B8_QT + q0 - j * FT - k;  // (query - key) of element 0
+#pragma unroll
+                    for (int e = 0; e < 16; ++e)
+                        if (qd + e < 0) sv[e] = __float_as_uint(-INFINITY);
+                }
+                uint32_t zk[8], dk[8];
+#pragma unroll
+                for (int e4 = 0; e4 < 4; ++e4) {
+                    const float4 l4 = *(const float4*)(lse_s + q0 + e4 * 4);  // (negated by the prep kernel)
+                    const float4 d4 = *(const float4*)(dl_s + q0 + e4 * 4);
+                    const float2 lv[2] = {make_float2(l4.x, l4.y), make_float2(l4.z, l4.w)};
+                    const float2 dv[2] = {make_float2(d4.x, d4.y), make_float2(d4.z, d4.w)};
+                    const float2 c2 = make_float2(ba.c, ba.c);
+#pragma unroll
+                    for (int e2 = 0; e2 < 2; ++e2) {
+                        const int e = e4 * 4 + e2 * 2;
+                        const float2 a = ffma2(make_float2(__uint_as_float(sv[e]), __uint_as_float(sv[e + 1])), c2, lv[e2]);
+                        const float2 p = make_float2(ex2f(a.x), ex2f(a.y));
+                        const float2 kd = make_float2(((mword >> e) & 1) ? ba.dscale : 0.f,
+                                                      ((mword >> (e + 1)) & 1) ? ba.dscale : 0.f);
+                        const float2 z = fmul2(p, kd);
+                        const float2 ds =
+                            fmul2(p, ffma2(kd, make_float2(__uint_as_float(dp[e]), __uint_as_float(dp[e + 1])), dv[e2]));
+                        zk[2 * e4 + e2] = pack_bf16(z.x, z.y);
+                        dk[2 * e4 + e2] = pack_bf16(ds.x, ds.y);
+                    }
+                }
+                tmem_st8(t_lane + q0, zk);      // Z^T over this group's S^T columns
+                tmem_st8(t_lane + q0 + 8, dk);  // dS^T next to it
+                // dS^T row k, queries q0..q0+15: 16-byte chunks q0/8, q0/8+1 of the 128 B row (128B swizzle)
+                if (hh == 0 && u >= 2) mbar_wait(&ds_free[u & 1], ((u >> 1) - 1) & 1);
+                uint8_t* rowp = ds_buf + k * 128;
+                const int c0 = q0 >> 3;
+                *(uint4*)(rowp + ((c0 ^ (k & 7)) * 16)) = make_uint4(dk[0], dk[1], dk[2], dk[3]);
+                *(uint4*)(rowp + (((c0 + 1) ^ (k & 7)) * 16)) = make_uint4(dk[4], dk[5], dk[6], dk[7]);
+                tmem_st_wait();
+                fence_proxy_async();
+                fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    mbar_arrive(&sm_done[hh]);
+                    if (hh == 1) mbar_arrive(&ds_full[u & 1]);
+                }
+                if (hh == 0 && i == first_i(j) && j > 0) drain_kv(j - 1);
+            }
+        }
+        drain_kv(nj - 1);
+    } else {
+        // ------------------------------------------------ 4 dQ warps (thread = head dim d)
+        const int d = (warp - 8) * 32 + lane;
+        const uint32_t t_row = tmem + ((uint32_t)((warp - 8) * 32) << 16) + 384;
+        for (int u = 0; u < nsteps; ++u) {
+            int j, i;
+            step_ji8<CAUSAL>(u, nj, nq, j, i);
+            const bool last = j == (CAUSAL ? i / 2 : nj - 1), dbg = ba.dbg & 2;
+            float* acc = ba.dqacc + ((bh * S) + (long long)i * B8_QT) * B8_D + d;  // [query][dim] of this block
+            mbar_wait(dq_full, u & 1);
+            fence_after();
+#pragma unroll 1
+            for (int pss = 0; pss < 2; ++pss) {
+                uint32_t r[32];
+                tmem_ld32_nowait(t_row + pss * 32, r);
+                tmem_ld_wait();
+                if (pss == 1) {
+                    fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(dq_free);
+                }
+                if (dbg) continue;
+                if (!last) {
+#pragma unroll
+                    for (int c = 0; c < 32; ++c) {
+                        float* p = acc + (long long)(pss * 32 + c) * B8_D;
+                        if (j == 0) __stcg(p, __uint_as_float(r[c]));
+                        else atomicAdd(p, __uint_as_float(r[c]));  // (one writer per address: ordered)
+                    }
+                    continue;
+                }
+                float f[32];
+#pragma unroll
+                for (int c = 0; c < 32; ++c) f[c] = j > 0 ? __ldcg(acc + (long long)(pss * 32 + c) * B8_D) : 0.f;
+#pragma unroll
+                for (int c = 0; c < 32; ++c) {
+                    const long long q = row_base + (long long)i * B8_QT + pss * 32 + c;
+                    bf16* o = ba.dq + q * ba.ld_dq + (long long)h * B8_D + d;
+                    float v = (f[c] + __uint_as_float(r[c])) * ba.scale;
+                    if (ba.acc & 1) v += __bfloat162float(*o);
+                    *o = __float2bfloat16_rn(v);
+                }
+            }
+        }
+    }
+    fence_before();
+    __syncthreads();
+    if (warp == W8_MMA) {
+        fence_after();
+        tmem_dealloc<512>(tmem);
+    }
+}
+
 bool bwd_fits(const Attn& a, const void* dout, i64 ld_do, i64 ld_dq, i64 ld_dk, i64 ld_dv) {
     if (!fwd_fits(a)) return false;
     if (a.thr && !a.mask_t) return false;
@@ -1609,7 +2004,7 @@ size_t carve(const Attn& a, void* base, BwdWs* w) {
         off += (bytes + 255) & ~(size_t)255;
         return o;
     };
-    size_t o_l = take(rows * 4), o_d = take(rows * 4), o_q = take(rows * FD * 4);
+    size_t o_l = take(rows * 4), o_d = take(rows * 4), o_q = take(rows * (size_t)std::max<i64>(a.hd, FD) * 4);
     if (w) {
         char* c = (char*)base;
         *w = BwdWs{(float*)(c + o_l), (float*)(c + o_d), (float*)(c + o_q)};
@@ -1706,8 +2101,47 @@ size_t attn_bwd_sm100_workspace(i64 B, i64 S, i64 nh, i64 hd) {
     return carve(a, nullptr, nullptr);
 }
 
+static bool attn_bwd_hd128(const Attn& a, const void* dout, i64 ld_do, void* dq, void* dk, void* dv, i64 ld_dq,
+                           i64 ld_dk, i64 ld_dv, void* ws, cudaStream_t s) {
+    if (!fwd_fits(a, 128) || (a.thr && !a.mask_t)) return false;
+    auto al = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
+    if (!al(dout) || ld_do % 8 || ((uintptr_t)dq & 1) || ((uintptr_t)dk & 15) || ((uintptr_t)dv & 15) || ld_dk % 8 ||
+        ld_dv % 8)
+        return false;
+    CUtensorMap tq, tk, tv, tdo, tm;
+    const long long rows = a.B * a.S, cols = a.nh * 128;
+    if (!make_map_bf16(&tq, a.q, cols, rows, a.ld_q, B8_QT) || !make_map_bf16(&tk, a.k, cols, rows, a.ld_k, FT) ||
+        !make_map_bf16(&tv, a.v, cols, rows, a.ld_v, FT) || !make_map_bf16(&tdo, dout, cols, rows, ld_do, B8_QT))
+        return false;
+    memset(&tm, 0, sizeof(tm));
+    if (a.thr && !make_map_u32(&tm, a.mask_t, a.S / 32, a.B * a.nh * a.S, a.S / 32, 4, FT)) return false;
+    BwdWs w;
+    carve(a, ws, &w);
+    const long long BH = a.B * a.nh, n = BH * a.S;
+    k_fa5_prep<128><<<(unsigned)((n * 16 + 255) / 256), 256, 0, s>>>((const bf16*)dout, ld_do, (const bf16*)a.o, a.ld_o,
+                                                                    a.lse, w.lse2, w.delta, BH, (int)a.S, (int)a.nh, -1.f);
+    SBK_CHECK_LAUNCH();
+    BwdArgs ba{w.lse2, w.delta, w.dqacc, a.thr ? a.mask_t : nullptr, a.thr ? a.dscale : 1.f,
+               a.scale * 1.4426950408889634f, a.scale, (bf16*)dq, (bf16*)dk, (bf16*)dv, ld_dq, ld_dk, ld_dv,
+               (int)a.S, (int)a.nh, a.acc_mask, 0};
+    if (const char* e = getenv("SB_ATTN_DBG")) ba.dbg = atoi(e);
+    ba.ts = nullptr;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_fa8_bwd<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, B8_SMEM);
+        cudaFuncSetAttribute(k_fa8_bwd<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, B8_SMEM);
+        attr = true;
+    }
+    dim3 grid((unsigned)a.nh, (unsigned)a.B);
+    if (a.causal) k_fa8_bwd<true><<<grid, B8_WARPS * 32, B8_SMEM, s>>>(tk, tv, tq, tdo, tm, ba);
+    else k_fa8_bwd<false><<<grid, B8_WARPS * 32, B8_SMEM, s>>>(tk, tv, tq, tdo, tm, ba);
+    SBK_CHECK_LAUNCH();
+    return true;
+}
+
 bool attn_bwd_sm100_try(const Attn& a, const void* dout, i64 ld_do, void* dq, void* dk, void* dv, i64 ld_dq, i64 ld_dk,
                         i64 ld_dv, void* ws, cudaStream_t s) {
+    if (a.hd == 128) return attn_bwd_hd128(a, dout, ld_do, dq, dk, dv, ld_dq, ld_dk, ld_dv, ws, s);
     if (!bwd_fits(a, dout, ld_do, ld_dq, ld_dk, ld_dv)) return false;
     if (a.causal && getenv("SB_ATTN_BWD") && atoi(getenv("SB_ATTN_BWD")) == 5) return false;  // fa5: no causal
     CUtensorMap tq, tk, tv, tdo, tm;
@@ -1723,7 +2157,7 @@ bool attn_bwd_sm100_try(const Attn& a, const void* dout, i64 ld_do, void* dq, vo
     const long long n = BH * a.S;
     // SB_ATTN_BWD=5 selects the round-1 kernel (A/B runs); v7 reads lse2 and delta negated
     static const int ver = getenv("SB_ATTN_BWD") ? atoi(getenv("SB_ATTN_BWD")) : 7;
-    k_fa5_prep<<<(unsigned)((n * 8 + 255) / 256), 256, 0, s>>>((const bf16*)dout, ld_do, (const bf16*)a.o, a.ld_o, a.lse,
+    k_fa5_prep<FD><<<(unsigned)((n * 8 + 255) / 256), 256, 0, s>>>((const bf16*)dout, ld_do, (const bf16*)a.o, a.ld_o, a.lse,
                                                               w.lse2, w.delta, BH, (int)a.S, (int)a.nh,
                                                               ver == 5 ? 1.f : -1.f);
     SBK_CHECK_LAUNCH();

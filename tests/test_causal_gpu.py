@@ -82,7 +82,7 @@ def _causal_ref(qkv, bits, B, S, nh, hd, p, do):
 
 @pytest.mark.parametrize("cap,engine", [(0, 2), (1, 2), (2, 1)])
 @pytest.mark.parametrize("B,S,nh,hd,p", [(2, 128, 2, 64, 0.0), (1, 256, 2, 64, 0.1), (1, 256, 2, 128, 0.1),
-                                         (2, 512, 4, 64, 0.1)])
+                                         (2, 512, 4, 64, 0.1), (1, 128, 2, 128, 0.0), (2, 512, 2, 128, 0.1)])
 def test_causal_attention_kernels(cap, engine, B, S, nh, hd, p):
     """cap 0 (best available): the tcgen05 forward (k_fa6_fwd: diagonal chunks masked, later
     chunks skipped) and backward (k_fa7_bwd<true>: key block j visits query blocks i >= j only,
@@ -96,7 +96,7 @@ def test_causal_attention_kernels(cap, engine, B, S, nh, hd, p):
     close(o, ref)
     assert (lse - lse_ref).abs().max().item() < 2e-3 * max(1.0, lse_ref.abs().max().item())
     g, used = _bwd(qkv, o, lse, do, bits, B, S, nh, hd, p, cap)
-    assert used == (3 if cap == 0 and hd == 64 else engine)  # tcgen05 backward: k_fa7_bwd<causal>
+    assert used == (3 if cap == 0 else engine)  # tcgen05 backward: k_fa7_bwd<causal> (hd 64) / k_fa8_bwd (128)
     for i in range(3):
         close(g[..., i * H:(i + 1) * H], grads[i], 3e-2)
     # the first query row attends to key 0 alone: o[:, 0] = v[:, 0] (x keep / (1-p))

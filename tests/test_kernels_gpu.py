@@ -341,7 +341,8 @@ def test_flash_attention_tcgen05_forward(B, S, nh, hd, p, qscale):
 
 @pytest.mark.parametrize("B,S,nh,hd,p,qscale", [(2, 128, 4, 64, 0.0, 0.5), (2, 256, 2, 64, 0.1, 0.5),
                                                  (1, 384, 2, 64, 0.1, 0.5), (2, 512, 16, 64, 0.1, 0.5),
-                                                 (1, 512, 2, 64, 0.1, 3.0)])
+                                                 (1, 512, 2, 64, 0.1, 3.0), (1, 128, 2, 128, 0.0, 0.5),
+                                                 (2, 256, 2, 128, 0.1, 0.5), (1, 1024, 4, 128, 0.1, 3.0)])
 def test_flash_attention_tcgen05_backward(B, S, nh, hd, p, qscale):
     """tcgen05 backward (engine 3: TS/SS MMAs, ordered fp32 dQ accumulation) vs torch autograd
     of the fp32 reference, vs the mma.sync backward, accumulate mode, and run-to-run bitwise equality."""
