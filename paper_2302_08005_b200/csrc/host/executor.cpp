@@ -78,6 +78,7 @@ struct RankCtx {
     std::vector<char*> fptr, gptr;  // per storage
     char* ws = nullptr;             // workspace
     size_t ws_bytes = 0;
+    char* ws2 = nullptr;            // workspace of the side-stream weight gradients (ws_bytes)
     char* tmp = nullptr;            // grad-conversion temp
     size_t tmp_bytes = 0;
     size_t scratch_grad_bytes = 0;
@@ -119,10 +120,73 @@ public:
 
     int my_rank(int idx) const { return comm.nccl ? comm.rank : idx; }
 
+    // ------------------------------------------ weight gradients on a side stream
+    // The weight / bias gradients of a Linear (dW = g^T x, db = colsum g) feed nothing
+    // else in the backward, so they are enqueued on a low-priority stream that forks
+    // right before the layer's dgrad: the dgrad (critical path) keeps its SMs and the
+    // weight-gradient CTAs fill the SMs its last wave, the attention backward's last
+    // wave and the small reduction kernels leave idle. Joined before any checkpoint
+    // region is recomputed (its scratch is reused) and at the end of the backward.
+    // Only parameters whose gradient storage has a single backward writer move, so the
+    // first-writer overwrite/accumulate order is unchanged.
+    cudaStream_t wstream = nullptr;
+    bool wside = false, wside_pending = false;
+    std::set<int> wside_ok;  // gradient storages (weights / biases) with one backward writer
+    std::vector<cudaEvent_t> wfork;
+    size_t wfork_next = 0;
+    cudaEvent_t wjoin_ev = nullptr;
+    void init_wside() {
+        // opt-in (SB_WGRAD_SIDE=1): measured neutral at C3 on one power-capped B200
+        // (648.6-653.2 vs 648.6-650.7 samples/s, profiles/r2/summary.md §3)
+        const char* e = getenv("SB_WGRAD_SIDE");
+        wside = e && atoi(e) != 0 && !comm.nccl && world == 1;
+        if (!wside) return;
+        const Plan& P = ranks[0].P;
+        std::map<int, int> writers;
+        for (auto& st : bsteps)
+            if (st.kind == 0)
+                for (int g : grad_writes(P, P.fwd[(size_t)st.idx])) ++writers[g];
+        for (auto& pv : P.params) {
+            const int g = P.views[(size_t)pv.second].gst;
+            if (writers[g] == 1 && P.st[(size_t)g].region < 0) wside_ok.insert(g);
+        }
+        int lo, hi;
+        CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        CK(cudaStreamCreateWithPriority(&wstream, cudaStreamNonBlocking, lo));
+        CK(cudaEventCreateWithFlags(&wjoin_ev, cudaEventDisableTiming));
+    }
+    bool wside_eligible(RankCtx& r, const Op& op) const {
+        if (!wside) return false;
+        if (!wside_ok.count(r.P.views[(size_t)op.in[1]].gst)) return false;
+        if (op.has_bias && op.bias_grad && !wside_ok.count(r.P.views[(size_t)op.in[2]].gst)) return false;
+        return true;
+    }
+    cudaEvent_t next_fork() {
+        if (wfork_next == wfork.size()) {
+            cudaEvent_t e;
+            CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            wfork.push_back(e);
+        }
+        return wfork[wfork_next++];
+    }
+    void wside_join() {
+        if (!wside_pending) return;
+        CK(cudaEventRecord(wjoin_ev, wstream));
+        CK(cudaStreamWaitEvent(stream, wjoin_ev, 0));
+        wside_pending = false;
+    }
+
     ExecutorImpl(const Module& root, bool tr, u64 sd, int w, DT c, const CommConfig& cc, bool fused)
         : train(tr), seed(sd), world(w), cdt(c), comm(cc) {
         if (world < 1) throw Error("world_size must be >= 1");
-        CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+        {
+            // SB_MAIN_PRIO=1: the executor stream above the side streams (keep bits, weight
+            // gradients), below the communication stream (measured neutral, default off)
+            int lo, hi;
+            CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+            static const int raise = getenv("SB_MAIN_PRIO") ? atoi(getenv("SB_MAIN_PRIO")) : 0;
+            CK(cudaStreamCreateWithPriority(&stream, cudaStreamNonBlocking, raise && hi < lo ? std::min(lo, hi + 1) : lo));
+        }
         int nr = comm.nccl ? 1 : world;
         ranks.resize((size_t)nr);
         for (int i = 0; i < nr; ++i) {
@@ -143,6 +207,11 @@ public:
         for (auto& r : ranks) allocate(r);
         init_mask_stream();
         init_early_allreduce();
+        init_wside();
+        if (wside)
+            for (auto& r : ranks) {
+                CK(cudaMalloc(&r.ws2, r.ws_bytes));
+            }
         if (comm.nccl) {
             nccl().load();
             ncclUniqueId id;
@@ -157,8 +226,13 @@ public:
     ~ExecutorImpl() {
         if (gexec) cudaGraphExecDestroy(gexec);
         if (graph) cudaGraphDestroy(graph);
-        for (auto& r : ranks)
+        for (auto& r : ranks) {
             if (r.base) cudaFree(r.base);
+            if (r.ws2) cudaFree(r.ws2);
+        }
+        for (auto e : wfork) cudaEventDestroy(e);
+        if (wjoin_ev) cudaEventDestroy(wjoin_ev);
+        if (wstream) cudaStreamDestroy(wstream);
         if (nan_flag) cudaFree(nan_flag);
         if (nan_counts) cudaFree(nan_counts);
         if (ncomm && nccl().CommDestroy) nccl().CommDestroy(ncomm);
@@ -592,18 +666,21 @@ public:
     // every GEMM of the step goes through here: profiling tags them "gemm" and
     // counts their flops (the roofline of the dominant kernel in bench.py)
     double gemm_flops = 0;
-    void run_gemm(const sbk::Gemm& g) {
-        if (profiling) {
+    void run_gemm(const sbk::Gemm& g, cudaStream_t st = nullptr) {
+        if (!st) st = stream;
+        const bool prof = profiling;
+        if (prof) {
             prof_begin("gemm");
             gemm_flops += 2.0 * (double)g.M * (double)g.N * (double)g.K * (double)g.batch;
         }
-        sbk::gemm(g, stream);
-        if (profiling) prof_end();
+        sbk::gemm(g, st);
+        if (prof) prof_end();
         ++launches;
     }
 
     void gemm_rowwise(RankCtx& r, const void* A, i64 lda, bool a_t, const void* B, i64 ldb, bool b_t, void* C, i64 ldc,
-                      DT tc, i64 M, i64 N, i64 K, bool acc, const void* bias, int epi = 0, void* aux = nullptr) {
+                      DT tc, i64 M, i64 N, i64 K, bool acc, const void* bias, int epi = 0, void* aux = nullptr,
+                      cudaStream_t st = nullptr) {
         // A(m,k): a_t ? A[k*lda + m] : A[m*lda + k];  B(k,n): b_t ? B[n*ldb + k] : B[k*ldb + n]
         sbk::Gemm g;
         g.A = A;
@@ -626,9 +703,9 @@ public:
         g.tbias = cdt;
         g.epilogue = epi;
         g.aux = aux;
-        g.ws = r.ws;
+        g.ws = st && st == wstream ? r.ws2 : r.ws;
         g.ws_bytes = r.ws_bytes;
-        run_gemm(g);
+        run_gemm(g, st);
     }
 
     // ------------------------------------------------------- collectives
@@ -1127,6 +1204,13 @@ public:
         i64 rows, cols, ldx, gr, gc, ldgx;
         x.rowwise(rows, cols, ldx);
         i64 out_f = w.shape[0];
+        const bool side = part == 3 && wside_eligible(r, op);
+        if (side) {  // fork before the dgrad: everything g and x depend on is enqueued
+            cudaEvent_t f = next_fork();
+            CK(cudaEventRecord(f, stream));
+            CK(cudaStreamWaitEvent(wstream, f, 0));
+            wside_pending = true;
+        }
         if (!(part & 1)) {
         } else if (op.dgelu_pre >= 0) {
             // dx lands directly as the producing GeLU's input gradient: gelu'(pre) * (g W)
@@ -1144,11 +1228,13 @@ public:
             ++launches;
             return;
         }
+        cudaStream_t ws = side ? wstream : stream;
         gemm_rowwise(r, g, ldg, true, fp(r, op.in[0]), ldx, false, gp(r, op.in[1]), cols, gdt(r, op.in[1]), out_f, cols,
-                     rows, !OW(op.in[1]), nullptr);
+                     rows, !OW(op.in[1]), nullptr, 0, nullptr, ws);
         launches += (part & 1) ? 2 : 1;
         if (op.has_bias && op.bias_grad) {
-            sbk::bias_grad(g, cdt, ldg, rows, out_f, (float*)gp(r, op.in[2]), (float*)r.ws, stream, !OW(op.in[2]));
+            sbk::bias_grad(g, cdt, ldg, rows, out_f, (float*)gp(r, op.in[2]), (float*)(side ? r.ws2 : r.ws), ws,
+                           !OW(op.in[2]));
             ++launches;
         }
     }
@@ -1604,6 +1690,7 @@ public:
         cudaEvent_t last = nullptr;
         for (size_t si = 0; si < bsteps.size(); ++si) {
             const Step& s = bsteps[si];
+            if (s.kind != 0) wside_join();  // a region's recompute / gradient scratch reuses memory
             if (s.kind == 2) {
                 if (region_zero[(size_t)s.idx])
                     for (auto& r : ranks)
@@ -1624,6 +1711,8 @@ public:
                 }
             }
         }
+        wside_join();
+        wfork_next = 0;
         if (cap && last) CK(cudaStreamWaitEvent(stream, last, 0));  // join the side stream into the graph
     }
 
@@ -1994,6 +2083,9 @@ std::vector<std::pair<std::string, float>> Executor::profile_step() {
     I.profiling = true;
     I.prof.clear();
     I.gemm_flops = 0;
+    // per-kind times need one stream: the side-stream weight gradients run inline here
+    const bool wside = I.wside;
+    I.wside = false;
     cudaEvent_t s0, s1;
     cudaEventCreate(&s0);
     cudaEventCreate(&s1);
@@ -2002,6 +2094,7 @@ std::vector<std::pair<std::string, float>> Executor::profile_step() {
     I.run_backward();
     cudaEventRecord(s1, I.stream);
     I.profiling = false;
+    I.wside = wside;
     synchronize();
     std::map<std::string, float> acc;
     float total = 0;

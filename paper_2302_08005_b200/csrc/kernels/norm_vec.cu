@@ -684,12 +684,8 @@ bool ln_bwd_vec(int mode, const void* x, const float* mean, const float* rstd, c
                     return;
                   }
                 }
-                if (false) {
-                } else if (mode == 0) {
-                    launch(k_ln_bwd_v<T, CPL, 0>);
-                } else {
-                    launch(k_ln_bwd_v<T, CPL, 1>);
-                }
+                if (mode == 0) launch(k_ln_bwd_v<T, CPL, 0>);
+                else launch(k_ln_bwd_v<T, CPL, 1>);
             });
         }
     });
