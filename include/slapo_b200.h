@@ -202,6 +202,40 @@ int sb_bias_dropout_residual_ln_fwd(const void* partial, const void* bias, const
                                     const void* beta, void* sum, void* y, float* mean, float* rstd, int dtype,
                                     int64_t rows, int64_t n, float eps, uint64_t exec_seed, uint64_t node_seed,
                                     double p, void* stream);
+/* backward_layernorm_mod (proj/src/executor.cpp:1158-1197): gx (+)= d LN / dx . g; dgamma/dbeta
+ * overwritten with the column sums (fp32; may be NULL). workspace: sb_layernorm_bwd_workspace bytes */
+int sb_layernorm_bwd(const void* x, const float* mean, const float* rstd, const void* gamma, const void* g, void* gx,
+                     float* dgamma, float* dbeta, int dtype, int64_t rows, int64_t n, int gx_accumulate, void* workspace,
+                     void* stream);
+size_t sb_layernorm_bwd_workspace(int64_t rows, int64_t n);
+/* backward of the fused bias+dropout+residual+LayerNorm block: g_res = g_sum (the LN input gradient),
+ * g_partial = dropout_bwd(g_sum) (the Linear output gradient), dbias / dgamma / dbeta column sums */
+int sb_bias_dropout_residual_ln_bwd(const void* sum, const float* mean, const float* rstd, const void* gamma,
+                                    const void* g, void* g_res, void* g_partial, float* dbias, float* dgamma,
+                                    float* dbeta, int dtype, int64_t rows, int64_t n, uint64_t exec_seed,
+                                    uint64_t node_seed, double p, void* workspace, void* stream);
+size_t sb_bias_dropout_residual_ln_bwd_workspace(int64_t rows, int64_t n);
+/* the .fuse'd Linear->gelu region outside a GEMM (executor.cpp:901-906,1306-1312; the product folds it
+ * into the tcgen05 GEMM epilogue, sb_gemm epilogue 1 / 2): pre = x + bias, y = gelu(pre);
+ * backward gx = g * gelu'(pre), dbias = column sums of gx (fp32, may be NULL) */
+int sb_bias_gelu_fwd(const void* x, const void* bias, void* y, void* pre, int dtype, int64_t rows, int64_t n,
+                     void* stream);
+int sb_bias_gelu_bwd(const void* pre, const void* g, void* gx, float* dbias, int dtype, int64_t rows, int64_t n,
+                     void* workspace, void* stream);
+size_t sb_bias_gelu_bwd_workspace(int64_t rows, int64_t n);
+/* eval_embedding / backward (executor.cpp:749-784,1199-1219): row = llround(id) mod vocab; a
+ * vocab-parallel shard owns rows [row0, row0 + local_rows) and writes zeros elsewhere; the backward is
+ * a deterministic sorted scatter-add into the fp32 shard gradient */
+int sb_embedding_fwd(const double* ids, int64_t n_ids, const void* table, int dtype, int64_t dim, int64_t vocab,
+                     int64_t row0, int64_t local_rows, void* out, void* stream);
+int sb_embedding_bwd(const double* ids, int64_t n_ids, const void* g, int dtype, int64_t dim, int64_t vocab,
+                     int64_t row0, int64_t local_rows, float* gtable, void* workspace, void* stream);
+size_t sb_embedding_bwd_workspace(int64_t n_ids, int64_t dim);
+/* all_reduce (executor.cpp:812-820): rank-ascending sum of `ranks` device buffers on one device (the
+ * lockstep simulator's semantics); sb_executor_allreduce: in place over an NCCL executor's ranks */
+int sb_allreduce_local(const void* const* srcs, void* const* dsts, int ranks, int dtype, int64_t n, int accumulate,
+                       void* stream);
+int sb_executor_allreduce(sb_executor* e, void* buf, int64_t n, int dtype, void* stream);
 /* attention keep bits in both layouts (S % 128 == 0): words [0, W) natural (bit e%32 of word e/32
  * for element e = ((b*nh + h)*S + i)*S + j, exactly sb_dropout_mask's bits), words [W, 2W)
  * transposed (element ((b*nh + h)*S + j)*S + i), W = B*nh*S*S/32 */

@@ -614,6 +614,64 @@ int sb_bias_dropout_residual_ln_fwd(const void* partial, const void* bias, const
                                           rows, n, eps, s1, thr, (float)(1.0 / (1.0 - p)), (cudaStream_t)stream);
     });
 }
+int sb_layernorm_bwd(const void* x, const float* mean, const float* rstd, const void* gamma, const void* g, void* gx,
+                     float* dgamma, float* dbeta, int dtype, int64_t rows, int64_t n, int gx_accumulate, void* workspace,
+                     void* stream) {
+    return guard([&] {
+        sbk::layernorm_bwd(x, mean, rstd, gamma, kdt(dtype), g, kdt(dtype), gx, dgamma, dbeta, kdt(dtype), rows, n,
+                           (float*)workspace, (cudaStream_t)stream, gx_accumulate != 0, false);
+    });
+}
+size_t sb_layernorm_bwd_workspace(int64_t rows, int64_t n) {
+    return std::max(sbk::layernorm_bwd_workspace(rows, n), (size_t)296 * 3 * (size_t)n * 4);
+}
+int sb_bias_dropout_residual_ln_bwd(const void* sum, const float* mean, const float* rstd, const void* gamma,
+                                    const void* g, void* g_res, void* g_partial, float* dbias, float* dgamma,
+                                    float* dbeta, int dtype, int64_t rows, int64_t n, uint64_t exec_seed,
+                                    uint64_t node_seed, double p, void* workspace, void* stream) {
+    return guard([&] {
+        u64 s1 = hash_combine(hash_combine(exec_seed, node_seed), 0xd0);
+        u64 thr = p > 0 ? dropout_threshold(p) : 0;
+        sbk::bias_dropout_residual_ln_bwd(sum, mean, rstd, gamma, kdt(dtype), g, g_res, g_partial, false, dbias, dgamma,
+                                          dbeta, kdt(dtype), rows, n, s1, thr, (float)(1.0 / (1.0 - p)),
+                                          (float*)workspace, (cudaStream_t)stream, false, false);
+    });
+}
+size_t sb_bias_dropout_residual_ln_bwd_workspace(int64_t rows, int64_t n) {
+    return std::max(sbk::bdrln_bwd_workspace(rows, n), (size_t)296 * 3 * (size_t)n * 4);
+}
+int sb_bias_gelu_fwd(const void* x, const void* bias, void* y, void* pre, int dtype, int64_t rows, int64_t n,
+                     void* stream) {
+    return guard([&] { sbk::bias_gelu_fwd(x, bias, y, pre, kdt(dtype), rows, n, (cudaStream_t)stream); });
+}
+int sb_bias_gelu_bwd(const void* pre, const void* g, void* gx, float* dbias, int dtype, int64_t rows, int64_t n,
+                     void* workspace, void* stream) {
+    return guard([&] {
+        sbk::bias_gelu_bwd(pre, g, gx, dbias, kdt(dtype), rows, n, (float*)workspace, (cudaStream_t)stream);
+    });
+}
+size_t sb_bias_gelu_bwd_workspace(int64_t rows, int64_t n) { return sbk::bias_grad_workspace(rows, n); }
+int sb_embedding_fwd(const double* ids, int64_t n_ids, const void* table, int dtype, int64_t dim, int64_t vocab,
+                     int64_t row0, int64_t local_rows, void* out, void* stream) {
+    return guard([&] {
+        sbk::embedding_fwd(ids, n_ids, table, kdt(dtype), dim, vocab, row0, local_rows, out, (cudaStream_t)stream);
+    });
+}
+int sb_embedding_bwd(const double* ids, int64_t n_ids, const void* g, int dtype, int64_t dim, int64_t vocab,
+                     int64_t row0, int64_t local_rows, float* gtable, void* workspace, void* stream) {
+    return guard([&] {
+        sbk::embedding_bwd(ids, n_ids, g, kdt(dtype), dim, vocab, row0, local_rows, gtable, workspace,
+                           (cudaStream_t)stream);
+    });
+}
+size_t sb_embedding_bwd_workspace(int64_t n_ids, int64_t dim) { return sbk::embedding_bwd_workspace(n_ids, dim); }
+int sb_allreduce_local(const void* const* srcs, void* const* dsts, int ranks, int dtype, int64_t n, int accumulate,
+                       void* stream) {
+    return guard([&] {
+        if (ranks < 1 || ranks > 16) throw Error("sb_allreduce_local: 1..16 ranks");
+        sbk::sum_ranks(srcs, dsts, ranks, kdt(dtype), n, accumulate != 0, (cudaStream_t)stream);
+    });
+}
 static sbk::Attn mk_attn(const void* q, const void* k, const void* v, void* o, int64_t ld_qkv, int64_t ld_o, float* lse,
                          int64_t B, int64_t S, int64_t nh, int64_t hd, float scale, uint64_t es, uint64_t ns, double p,
                          int dtype) {
@@ -747,6 +805,9 @@ int sb_pipeline_executor_input_grad(sb_pipeline_executor* e, int stage, int idx,
 }
 int sb_pipeline_executor_time_steps(sb_pipeline_executor* e, int steps, float* ms) {
     return guard([&] { *ms = e->ex->time_steps(steps); });
+}
+int sb_executor_allreduce(sb_executor* e, void* buf, int64_t n, int dtype, void* stream) {
+    return guard([&] { e->ex->all_reduce_device(buf, n, kdt(dtype), stream); });
 }
 int sb_pipeline_executor_free(sb_pipeline_executor* e) {
     delete e;

@@ -1943,6 +1943,17 @@ std::vector<GradMap> Executor::grads_all_ranks() {
     return maps;
 }
 
+void Executor::all_reduce_device(void* buf, i64 n, DT dt, void* st) {
+    auto& I = *impl_;
+    if (I.comm.nccl) {
+        nccl().check(nccl().AllReduce(buf, buf, (size_t)n, nccl_dt(dt), ncclSum, I.ncomm,
+                                          st ? (cudaStream_t)st : I.stream),
+                       "ncclAllReduce");
+        return;
+    }
+    if (I.world != 1) throw Error("all_reduce_device: a lockstep multi-rank executor has no communicator");
+}
+
 void Executor::enqueue_loss(float* dloss) {
     auto& I = *impl_;
     RankCtx& r = I.ranks[0];

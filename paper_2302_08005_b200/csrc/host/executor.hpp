@@ -89,6 +89,8 @@ public:
     DeviceTensor input_grad_device(int idx) const;
     void set_input_from_device(int idx, const void* src, DT dt);  // (enqueued) cast into input idx
     std::vector<GradMap> grads_all_ranks();                        // download the current gradients
+    // in-place sum over the executor's ranks on `stream` (NCCL executors; identity at world 1)
+    void all_reduce_device(void* buf, i64 n, DT dt, void* stream);
 
 private:
     std::unique_ptr<ExecutorImpl> impl_;

@@ -651,4 +651,43 @@ void bias_grad(const void* g, DT tg, i64 ld, i64 rows, i64 cols, float* db, floa
     SBK_CHECK_LAUNCH();
 }
 
+// ------------------------------------------------- bias + GeLU (standalone)
+// The .fuse'd Linear->gelu region outside a GEMM (the product path folds it into
+// the tcgen05 GEMM epilogue): pre = x + b[col], y = gelu(pre); backward
+// gx = g * gelu'(pre) (db = column sums of gx via bias_grad).
+template <class T>
+__global__ void k_bias_gelu_fwd(const T* x, const T* b, T* y, T* pre, i64 rows, i64 n) {
+    for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < rows * n; i += (i64)gridDim.x * blockDim.x) {
+        const float v = to_f(x[i]) + (b ? to_f(b[i % n]) : 0.f);
+        if (pre) pre[i] = from_f<T>(v);
+        y[i] = from_f<T>(gelu_f(v));
+    }
+}
+template <class T>
+__global__ void k_bias_gelu_bwd(const T* pre, const T* g, T* gx, i64 total) {
+    for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < total; i += (i64)gridDim.x * blockDim.x)
+        gx[i] = from_f<T>(to_f(g[i]) * gelu_grad_f(to_f(pre[i])));
+}
+void bias_gelu_fwd(const void* x, const void* b, void* y, void* pre, DT t, i64 rows, i64 n, cudaStream_t s) {
+    dispatch(t, [&](auto* p) {
+        using T = std::remove_pointer_t<decltype(p)>;
+        if constexpr (!std::is_same_v<T, double>)
+            k_bias_gelu_fwd<T><<<grid_for(rows * n, 256), 256, 0, s>>>((const T*)x, (const T*)b, (T*)y, (T*)pre, rows, n);
+        else
+            throw std::runtime_error("bias_gelu: f64 unsupported");
+    });
+    SBK_CHECK_LAUNCH();
+}
+void bias_gelu_bwd(const void* pre, const void* g, void* gx, float* db, DT t, i64 rows, i64 n, float* ws, cudaStream_t s) {
+    dispatch(t, [&](auto* p) {
+        using T = std::remove_pointer_t<decltype(p)>;
+        if constexpr (!std::is_same_v<T, double>)
+            k_bias_gelu_bwd<T><<<grid_for(rows * n, 256), 256, 0, s>>>((const T*)pre, (const T*)g, (T*)gx, rows * n);
+        else
+            throw std::runtime_error("bias_gelu: f64 unsupported");
+    });
+    SBK_CHECK_LAUNCH();
+    if (db) bias_grad(gx, t, n, rows, n, db, ws, s, false);
+}
+
 }  // namespace sbk

@@ -137,6 +137,10 @@ size_t bdrln_bwd_workspace(i64 rows, i64 n);
 void bias_grad(const void* g, DT tg, i64 ld, i64 rows, i64 cols, float* db, float* workspace, cudaStream_t s,
                bool acc = true);
 size_t bias_grad_workspace(i64 rows, i64 cols);
+// standalone bias + GeLU (the product folds it into the GEMM epilogue): pre = x + b, y = gelu(pre);
+// backward gx = g * gelu'(pre), db = column sums of gx (overwritten; workspace bias_grad_workspace)
+void bias_gelu_fwd(const void* x, const void* b, void* y, void* pre, DT t, i64 rows, i64 n, cudaStream_t s);
+void bias_gelu_bwd(const void* pre, const void* g, void* gx, float* db, DT t, i64 rows, i64 n, float* ws, cudaStream_t s);
 
 // ---------------------------------------------------------- embedding
 void embedding_fwd(const double* ids, i64 n_ids, const void* table, DT t, i64 dim, i64 full_rows, i64 row0,
