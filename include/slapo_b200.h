@@ -105,6 +105,10 @@ int sb_pipeline_free(sb_pipeline* p);
 typedef struct sb_pipeline_executor sb_pipeline_executor;
 int sb_pipeline_executor_create(const sb_pipeline* p, int micro_batches, int train, uint64_t seed, int dtype,
                                 const int* devices, int fused, sb_pipeline_executor** out);
+/* tp > 1: each stage's (sharded) module runs on tp lockstep ranks of its device; the gradient
+   functions below then take a slot = stage * tp + rank */
+int sb_pipeline_executor_create_tp(const sb_pipeline* p, int micro_batches, int tp, int train, uint64_t seed,
+                                   int dtype, const int* devices, int fused, sb_pipeline_executor** out);
 int sb_pipeline_executor_forward(sb_pipeline_executor* e, const double* const* inputs, int n);
 int sb_pipeline_executor_num_outputs(sb_pipeline_executor* e, int* n);
 int sb_pipeline_executor_output(sb_pipeline_executor* e, int idx, double* out, size_t cap, size_t* n, int64_t* dims,

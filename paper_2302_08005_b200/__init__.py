@@ -57,6 +57,8 @@ for _n, _a in {
     "sb_model_gpt_neo": (_c.c_int, _i64, _i64, _i64, _i64, _i64, _c.c_double, _c.POINTER(_P)),
     "sb_pipeline_executor_create": (_P, _c.c_int, _c.c_int, _u64, _c.c_int, _c.POINTER(_c.c_int), _c.c_int,
                                     _c.POINTER(_P)),
+    "sb_pipeline_executor_create_tp": (_P, _c.c_int, _c.c_int, _c.c_int, _u64, _c.c_int, _c.POINTER(_c.c_int),
+                                       _c.c_int, _c.POINTER(_P)),
     "sb_pipeline_executor_forward": (_P, _c.POINTER(_dp), _c.c_int),
     "sb_pipeline_executor_num_outputs": (_P, _c.POINTER(_c.c_int)),
     "sb_pipeline_executor_output": (_P, _c.c_int, _dp, _c.c_size_t, _c.POINTER(_c.c_size_t), _c.POINTER(_i64),
@@ -685,7 +687,7 @@ class PipelineExecutor:
     on micro-batch-shaped tensors."""
 
     def __init__(self, plan: PipelinePlan, micro_batches: int = 1, mode: str = "train", seed: int = 0,
-                 dtype: str = "fp32", devices: Optional[Sequence[int]] = None, fused: bool = True):
+                 dtype: str = "fp32", devices: Optional[Sequence[int]] = None, fused: bool = True, tp: int = 1):
         if plan._h is None:
             raise SlapoError("PipelineExecutor needs a plan from Schedule.apply_pipeline()")
         self._plan = plan
@@ -696,8 +698,9 @@ class PipelineExecutor:
                 raise SlapoError("one device per stage")
             devs = (_c.c_int * len(devices))(*devices)
         h = _P()
-        _check(_lib.sb_pipeline_executor_create(plan._h, micro_batches, int(mode == "train"), seed, _DTYPES[dtype],
-                                                devs, int(fused), _c.byref(h)))
+        _check(_lib.sb_pipeline_executor_create_tp(plan._h, micro_batches, tp, int(mode == "train"), seed,
+                                                   _DTYPES[dtype], devs, int(fused), _c.byref(h)))
+        self.tp = tp
         self._h = h
         weakref.finalize(self, _lib.sb_pipeline_executor_free, h)
 
@@ -720,12 +723,13 @@ class PipelineExecutor:
         return outs
 
     def backward(self) -> List[GradientMap]:
-        """Per stage: parameter gradients (stage-local names) and the gradients of the
-        model inputs the stage consumes."""
+        """Per stage (and tensor-parallel rank: slot stage * tp + rank): parameter
+        gradients (stage-local names) and the gradients of the model inputs the stage
+        consumes."""
         _check(_lib.sb_pipeline_executor_backward(self._h))
         res = []
         buf = _c.create_string_buffer(4096)
-        for st in range(len(self._plan.stages)):
+        for st in range(len(self._plan.stages) * self.tp):
             gm = GradientMap()
             n = _c.c_int()
             _check(_lib.sb_pipeline_executor_num_grads(self._h, st, _c.byref(n)))

@@ -736,16 +736,20 @@ int sb_attn_bwd(const void* q, const void* k, const void* v, const void* o, int6
 
 // ------------------------------------------------------- pipeline executor (f1)
 extern "C" {
-int sb_pipeline_executor_create(const sb_pipeline* p, int micro_batches, int train, uint64_t seed, int dtype,
-                                const int* devices, int fused, sb_pipeline_executor** out) {
+int sb_pipeline_executor_create_tp(const sb_pipeline* p, int micro_batches, int tp, int train, uint64_t seed,
+                                   int dtype, const int* devices, int fused, sb_pipeline_executor** out) {
     return guard([&] {
         std::vector<int> devs;
         if (devices) devs.assign(devices, devices + p->p.stages.size());
         auto* e = new sb_pipeline_executor;
         e->ex = std::make_unique<PipelineExecutor>(p->p, micro_batches, train != 0, seed, dtype ? sbk::BF16 : sbk::F32,
-                                                   devs, fused != 0);
+                                                   devs, fused != 0, tp);
         *out = e;
     });
+}
+int sb_pipeline_executor_create(const sb_pipeline* p, int micro_batches, int train, uint64_t seed, int dtype,
+                                const int* devices, int fused, sb_pipeline_executor** out) {
+    return sb_pipeline_executor_create_tp(p, micro_batches, 1, train, seed, dtype, devices, fused, out);
 }
 int sb_pipeline_executor_forward(sb_pipeline_executor* e, const double* const* inputs, int n) {
     return guard([&] {
@@ -773,7 +777,7 @@ int sb_pipeline_executor_backward(sb_pipeline_executor* e) {
 }
 static GradMap& pgmap(sb_pipeline_executor* e, int stage) {
     if (e->grads.empty()) throw Error("no gradients: call backward first");
-    if (stage < 0 || stage >= (int)e->grads.size()) throw Error("stage index out of range");
+    if (stage < 0 || stage >= (int)e->grads.size()) throw Error("stage slot out of range (stage * tp + rank)");
     return e->grads[(size_t)stage];
 }
 int sb_pipeline_executor_num_grads(sb_pipeline_executor* e, int stage, int* n) {

@@ -1902,7 +1902,8 @@ void Executor::zero_param_grads() {
 void Executor::set_output_grad_seed(int idx, const void* dptr, DT dt) {
     auto& I = *impl_;
     if (idx < 0 || idx >= (int)I.ranks[0].P.outputs.size()) throw Error("set_output_grad_seed: output index out of range");
-    if (I.world > 1 && !I.comm.nccl) throw Error("set_output_grad_seed: one rank per executor only");
+    // (lockstep ranks: every rank's output is seeded from the same buffer — stage-boundary
+    // values are replicated across tensor-parallel ranks)
     if (I.out_seed.size() < I.ranks[0].P.outputs.size()) I.out_seed.resize(I.ranks[0].P.outputs.size(), {nullptr, sbk::F32});
     I.out_seed[(size_t)idx] = {dptr, dt};
 }

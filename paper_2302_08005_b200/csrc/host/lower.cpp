@@ -193,7 +193,7 @@ struct Lowerer {
     // ---------------------------------------------------------- modules
     Val eval_module(const Module& m, const std::string& path, std::vector<Val> args) {
         if (get_flag(m.attrs, "sync_backward") && o.collect() && !args.empty())
-            args[0] = Val{{sync_grad(args[0].one())}, false};
+            args[0] = Val{{sync_grad(args[0].one(), m.kind == "Embedding")}, false};
         bool want_ckpt = (get_flag(m.attrs, "checkpoint") || m.kind == "EfficientAttention") && !in_ckpt;
         if (want_ckpt) {
             if (m.kind == "EfficientAttention" && o.fused_kernels) {
@@ -214,7 +214,10 @@ struct Lowerer {
         return eval_builtin(m, path, args);
     }
 
-    int sync_grad(int in) {
+    // index_input: the synced value is an Embedding's id tensor, whose gradient is zero by
+    // definition (executor.cpp:1216-1217): the SyncGrad still counts but sums nothing. Any
+    // other input — a stage-boundary activation of a pipeline stage included — is summed.
+    int sync_grad(int in, bool index_input = false) {
         View nv = V(in);
         int gst = new_storage(nv.numel(), o.cdt, SKind::Act, "syncgrad");
         P.st[(size_t)gst].has_fwd = false;
@@ -227,7 +230,7 @@ struct Lowerer {
         op.k = K::SyncGrad;
         op.in = {in};
         op.out = {out};
-        op.ids_input = P.st[(size_t)V(in).st].kind == SKind::Input;
+        op.ids_input = index_input;
         emit(op);
         return out;
     }

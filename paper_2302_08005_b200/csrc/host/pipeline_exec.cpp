@@ -71,7 +71,7 @@ void* dev_alloc(int dev, size_t bytes) {
 }  // namespace
 
 struct PipelineExecutor::Impl {
-    int M = 1;
+    int M = 1, tp = 1;
     std::vector<StageRt> stages;
     std::vector<Value> values;  // model inputs first, then produced values
     std::vector<int> model_out_val;
@@ -207,10 +207,12 @@ struct PipelineExecutor::Impl {
 };
 
 PipelineExecutor::PipelineExecutor(const StagePlan& plan, int micro, bool train, u64 seed, DT compute,
-                                   std::vector<int> devices, bool fused)
+                                   std::vector<int> devices, bool fused, int tp)
     : impl_(std::make_unique<Impl>()) {
     auto& I = *impl_;
     if (micro < 1) throw Error("micro_batches must be >= 1");
+    if (tp < 1) throw Error("pipeline: tp must be >= 1");
+    I.tp = tp;
     if (plan.stages.empty()) throw Error("pipeline: empty stage plan");
     if (devices.empty()) {
         int d = 0;
@@ -233,7 +235,7 @@ PipelineExecutor::PipelineExecutor(const StagePlan& plan, int micro, bool train,
         StageRt s;
         s.dev = devices[si];
         PCK(cudaSetDevice(s.dev));
-        s.ex = std::make_unique<Executor>(micro_module(st.module, micro), train, seed, 1, compute, CommConfig{}, fused);
+        s.ex = std::make_unique<Executor>(micro_module(st.module, micro), train, seed, tp, compute, CommConfig{}, fused);
         s.ex->set_accumulate_param_grads(true);
         s.st = (cudaStream_t)s.ex->stream();
         for (size_t i = 0; i < st.consumes.size(); ++i) {
@@ -374,7 +376,7 @@ std::vector<GradMap> PipelineExecutor::backward() {
     std::vector<GradMap> res;
     for (auto& s : I.stages) {
         PCK(cudaSetDevice(s.dev));
-        GradMap g = s.ex->grads_all_ranks()[0];
+        std::vector<GradMap> per_rank = s.ex->grads_all_ranks();
         // model-input gradients concatenated over micro-batches; produced-value inputs: none
         std::vector<HostTensor> ins;
         for (size_t i = 0; i < s.in_val.size(); ++i) {
@@ -391,11 +393,14 @@ std::vector<GradMap> PipelineExecutor::backward() {
             }
             ins.push_back(std::move(t));
         }
-        g.inputs = std::move(ins);
-        res.push_back(std::move(g));
+        for (auto& g : per_rank) {
+            g.inputs = ins;  // (replicated across the stage's ranks)
+            res.push_back(std::move(g));
+        }
     }
     return res;
 }
+int PipelineExecutor::tp() const { return impl_->tp; }
 
 float PipelineExecutor::time_steps(int steps) {
     auto& I = *impl_;

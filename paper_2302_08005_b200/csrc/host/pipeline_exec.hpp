@@ -33,17 +33,21 @@ namespace sb {
 
 class PipelineExecutor {
 public:
+    // tp > 1: every stage runs its (sharded) module on tp lockstep ranks of its device
+    // (tensor parallelism inside the stage; stage-boundary values are replicated)
     PipelineExecutor(const StagePlan& plan, int micro_batches, bool train, u64 seed, DT compute,
-                     std::vector<int> devices = {}, bool fused_kernels = true);
+                     std::vector<int> devices = {}, bool fused_kernels = true, int tp = 1);
     ~PipelineExecutor();
 
     // GPipe forward of every micro-batch; the model outputs concatenated along dim 0
     std::vector<HostTensor> forward(const std::vector<HostTensor>& inputs);
     std::vector<HostTensor> forward_raw(const double* const* inputs, int n);  // full-batch f64 inputs
-    // backward of sum(outputs) over all micro-batches (requires forward): per stage,
-    // its parameter gradients summed over micro-batches (stage-local names) and the
-    // gradients of the model inputs it consumes (concatenated over micro-batches)
+    // backward of sum(outputs) over all micro-batches (requires forward): per stage and
+    // tensor-parallel rank (slot stage * tp + rank), its parameter gradients summed over
+    // micro-batches (stage-local names) and the gradients of the model inputs it consumes
+    // (concatenated over micro-batches)
     std::vector<GradMap> backward();
+    int tp() const;
     // device ms of `steps` full training steps (forward + backward of every
     // micro-batch) on already-uploaded inputs (the last forward's)
     float time_steps(int steps);

@@ -124,3 +124,36 @@ def test_pipeline_timing_and_errors():
         sb.PipelineExecutor(plan, 3, "train", 1, "fp32")  # batch 4 is not divisible by 3
     with pytest.raises(sb.SlapoError, match="one device per stage"):
         sb.PipelineExecutor(plan, 2, "train", 1, "fp32", devices=[0])
+
+
+@pytest.mark.parametrize("mode", ["verify", "train"])
+def test_pipeline_with_tensor_parallel_stages(mode):
+    """C5's TP x PP shape on one GPU ('pin each stage's TP with
+    run_sharded, and the composition at world 1, separately'): the TP=2 recipe split into
+    2 stages, each on 2 lockstep tensor-parallel ranks, 2 micro-batches. Per rank, the
+    gradients equal the unsplit TP=2 executor's (pinned against the reference's
+    run_sharded by tests/test_parity_gpu.py): verify — on the full batch; train — summed
+    over unsplit runs on each micro-batch (run_pipeline's per-chunk semantics)."""
+    cfg = dict(layers=4, hidden=32, heads=4, vocab=32, batch=4, seq=8, p=0.1)
+    script = recipes.tp_script(4, 2, ckpt_ratio=0.25)
+    m, plan = _plan(cfg, script + SPLIT1)
+    x = m.random_inputs(9)
+    pe = sb.PipelineExecutor(plan, 2, mode, 123, "fp32", tp=2)
+    out = pe.forward(x)
+    g = pe.backward()
+    assert len(g) == 2 * 2
+    got = [_merged([g[st * 2 + r] for st in range(2)]) for r in range(2)]
+    micro = 1 if mode == "verify" else 2
+    per = cfg["batch"] // micro
+    want, wout = None, []
+    for mb in range(micro):
+        mm = sb.toy_bert(cfg["layers"], cfg["hidden"], cfg["heads"], cfg["vocab"], per, cfg["seq"], cfg["p"])
+        s = sb.create_schedule(mm, 2)
+        s.load_script(script)
+        ex = sb.Executor(s.apply(), mode, 123, 2)
+        wout.append(ex.forward([x[0][mb * per:(mb + 1) * per]])[0])
+        gm = [r.params for r in ex.backward_all_ranks()]
+        want = gm if want is None else [{k: a[k] + b[k] for k in a} for a, b in zip(want, gm)]
+    assert rel_err(out[0], np.concatenate(wout, 0)) <= 1e-4
+    for r in range(2):
+        compare_grads(got[r], want[r], 1e-4)
