@@ -109,6 +109,17 @@ int sb_pipeline_executor_create(const sb_pipeline* p, int micro_batches, int tra
    functions below then take a slot = stage * tp + rank */
 int sb_pipeline_executor_create_tp(const sb_pipeline* p, int micro_batches, int tp, int train, uint64_t seed,
                                    int dtype, const int* devices, int fused, sb_pipeline_executor** out);
+/* one process per (stage, tp rank): rank = stage * tp + tp_rank of world = stages * tp; stage I/O by
+   ncclSend / ncclRecv over a pipeline communicator (pp_uid, broadcast from rank 0), the stage's own TP
+   over an NCCL communicator of its tp ranks (tp_uid, one per stage; NULL when tp == 1). forward returns
+   only the model outputs this rank's stage produces (others: empty); gradients: this rank's only. */
+int sb_pipeline_executor_create_dist(const sb_pipeline* p, int micro_batches, int tp, int train, uint64_t seed,
+                                     int dtype, int fused, int rank, int world, const void* pp_uid128,
+                                     const void* tp_uid128, sb_pipeline_executor** out);
+/* the transfer program of one rank (lines "kind m idx peer value numel", kind in fwd_recv / fwd_run /
+   fwd_send / bwd_recv / bwd_run / bwd_send): what a distributed rank executes, for host-side checks */
+int sb_pipeline_program(const sb_pipeline* p, int micro_batches, int tp, int rank, char* buf, size_t cap,
+                        size_t* needed);
 int sb_pipeline_executor_forward(sb_pipeline_executor* e, const double* const* inputs, int n);
 int sb_pipeline_executor_num_outputs(sb_pipeline_executor* e, int* n);
 int sb_pipeline_executor_output(sb_pipeline_executor* e, int idx, double* out, size_t cap, size_t* n, int64_t* dims,

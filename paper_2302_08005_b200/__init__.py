@@ -59,6 +59,9 @@ for _n, _a in {
                                     _c.POINTER(_P)),
     "sb_pipeline_executor_create_tp": (_P, _c.c_int, _c.c_int, _c.c_int, _u64, _c.c_int, _c.POINTER(_c.c_int),
                                        _c.c_int, _c.POINTER(_P)),
+    "sb_pipeline_executor_create_dist": (_P, _c.c_int, _c.c_int, _c.c_int, _u64, _c.c_int, _c.c_int, _c.c_int,
+                                         _c.c_int, _c.c_char_p, _c.c_char_p, _c.POINTER(_P)),
+    "sb_pipeline_program": (_P, _c.c_int, _c.c_int, _c.c_int, _c.c_char_p, _c.c_size_t, _c.POINTER(_c.c_size_t)),
     "sb_pipeline_executor_forward": (_P, _c.POINTER(_dp), _c.c_int),
     "sb_pipeline_executor_num_outputs": (_P, _c.POINTER(_c.c_int)),
     "sb_pipeline_executor_output": (_P, _c.c_int, _dp, _c.c_size_t, _c.POINTER(_c.c_size_t), _c.POINTER(_i64),
@@ -687,7 +690,11 @@ class PipelineExecutor:
     on micro-batch-shaped tensors."""
 
     def __init__(self, plan: PipelinePlan, micro_batches: int = 1, mode: str = "train", seed: int = 0,
-                 dtype: str = "fp32", devices: Optional[Sequence[int]] = None, fused: bool = True, tp: int = 1):
+                 dtype: str = "fp32", devices: Optional[Sequence[int]] = None, fused: bool = True, tp: int = 1,
+                 dist: Optional[tuple] = None):
+        """dist = (rank, world, pp_uid, tp_uid): one process per (stage, tp rank), rank = stage * tp +
+        tp_rank, world = stages * tp; pp_uid (128 bytes, the same on every rank) names the pipeline
+        communicator, tp_uid (the same on the tp ranks of one stage; None for tp == 1) the stage's."""
         if plan._h is None:
             raise SlapoError("PipelineExecutor needs a plan from Schedule.apply_pipeline()")
         self._plan = plan
@@ -698,8 +705,16 @@ class PipelineExecutor:
                 raise SlapoError("one device per stage")
             devs = (_c.c_int * len(devices))(*devices)
         h = _P()
-        _check(_lib.sb_pipeline_executor_create_tp(plan._h, micro_batches, tp, int(mode == "train"), seed,
-                                                   _DTYPES[dtype], devs, int(fused), _c.byref(h)))
+        self.dist = dist
+        if dist is not None:
+            _pin_nccl()
+            rank, world, pp_uid, tp_uid = dist
+            _check(_lib.sb_pipeline_executor_create_dist(plan._h, micro_batches, tp, int(mode == "train"), seed,
+                                                         _DTYPES[dtype], int(fused), rank, world, pp_uid, tp_uid,
+                                                         _c.byref(h)))
+        else:
+            _check(_lib.sb_pipeline_executor_create_tp(plan._h, micro_batches, tp, int(mode == "train"), seed,
+                                                       _DTYPES[dtype], devs, int(fused), _c.byref(h)))
         self.tp = tp
         self._h = h
         weakref.finalize(self, _lib.sb_pipeline_executor_free, h)
@@ -729,7 +744,7 @@ class PipelineExecutor:
         _check(_lib.sb_pipeline_executor_backward(self._h))
         res = []
         buf = _c.create_string_buffer(4096)
-        for st in range(len(self._plan.stages) * self.tp):
+        for st in range(1 if self.dist is not None else len(self._plan.stages) * self.tp):
             gm = GradientMap()
             n = _c.c_int()
             _check(_lib.sb_pipeline_executor_num_grads(self._h, st, _c.byref(n)))
@@ -756,3 +771,19 @@ class PipelineExecutor:
         ms = _c.c_float()
         _check(_lib.sb_pipeline_executor_time_steps(self._h, steps, _c.byref(ms)))
         return ms.value
+
+
+def pipeline_program(plan: PipelinePlan, micro_batches: int, tp: int, rank: int):
+    """The transfer program a distributed pipeline rank executes (csrc/host/pipeline_exec.hpp
+    pipe_program): [(kind, micro_batch, index, peer, value, numel)]."""
+    if plan._h is None:
+        raise SlapoError("pipeline_program needs a plan from Schedule.apply_pipeline()")
+    need = _c.c_size_t()
+    _check(_lib.sb_pipeline_program(plan._h, micro_batches, tp, rank, None, 0, _c.byref(need)))
+    buf = _c.create_string_buffer(need.value)
+    _check(_lib.sb_pipeline_program(plan._h, micro_batches, tp, rank, buf, need.value, _c.byref(need)))
+    out = []
+    for ln in buf.value.decode().splitlines():
+        k, m, i, p, v, n = ln.split()
+        out.append((k, int(m), int(i), int(p), v, int(n)))
+    return out

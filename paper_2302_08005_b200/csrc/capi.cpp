@@ -5,6 +5,7 @@
 #include <nccl.h>
 
 #include <cstring>
+#include <map>
 #include <dlfcn.h>
 #include <sstream>
 
@@ -745,6 +746,48 @@ int sb_pipeline_executor_create_tp(const sb_pipeline* p, int micro_batches, int 
         e->ex = std::make_unique<PipelineExecutor>(p->p, micro_batches, train != 0, seed, dtype ? sbk::BF16 : sbk::F32,
                                                    devs, fused != 0, tp);
         *out = e;
+    });
+}
+int sb_pipeline_executor_create_dist(const sb_pipeline* p, int micro_batches, int tp, int train, uint64_t seed,
+                                     int dtype, int fused, int rank, int world, const void* pp_uid128,
+                                     const void* tp_uid128, sb_pipeline_executor** out) {
+    return guard([&] {
+        PipeDist d;
+        d.rank = rank;
+        d.world = world;
+        d.pp_uid.assign((const char*)pp_uid128, (const char*)pp_uid128 + 128);
+        if (tp > 1) {
+            if (!tp_uid128) throw Error("tp > 1 needs the stage's tensor-parallel unique id");
+            d.tp_uid.assign((const char*)tp_uid128, (const char*)tp_uid128 + 128);
+        }
+        auto* e = new sb_pipeline_executor;
+        e->ex = std::make_unique<PipelineExecutor>(p->p, micro_batches, train != 0, seed, dtype ? sbk::BF16 : sbk::F32,
+                                                   std::vector<int>{}, fused != 0, tp, &d);
+        *out = e;
+    });
+}
+int sb_pipeline_program(const sb_pipeline* p, int micro_batches, int tp, int rank, char* buf, size_t cap,
+                        size_t* needed) {
+    return guard([&] {
+        // element count of every stage-boundary value per micro-batch, from a consumer's declared input shape
+        std::map<std::string, long long> numel;
+        for (auto& st : p->p.stages)
+            for (size_t i = 0; i < st.consumes.size(); ++i) {
+                const auto& at = st.module.forward->at(st.module.forward->inputs[i]).attrs;
+                auto it = at.find("shape");
+                if (it == at.end()) continue;
+                long long n = 1;
+                for (auto d : std::get<std::vector<i64>>(it->second)) n *= d;
+                numel[st.consumes[i]] = n / micro_batches;
+            }
+        static const char* kinds[] = {"fwd_recv", "fwd_run", "fwd_send", "bwd_recv", "bwd_run", "bwd_send"};
+        std::ostringstream o;
+        for (auto& st : pipe_program(p->p, micro_batches, tp, rank))
+            o << kinds[(int)st.kind] << " " << st.m << " " << st.idx << " " << st.peer << " "
+              << (st.value.empty() ? "-" : st.value) << " " << (st.value.empty() ? 0 : numel[st.value]) << "\n";
+        const std::string t = o.str();
+        *needed = t.size() + 1;
+        if (buf && cap >= t.size() + 1) std::memcpy(buf, t.c_str(), t.size() + 1);
     });
 }
 int sb_pipeline_executor_create(const sb_pipeline* p, int micro_batches, int train, uint64_t seed, int dtype,

@@ -45,6 +45,8 @@ struct Nccl {
     ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
     void load() {
         if (h) return;
@@ -54,6 +56,8 @@ struct Nccl {
         AllReduce = (decltype(AllReduce))dlsym(h, "ncclAllReduce");
         AllGather = (decltype(AllGather))dlsym(h, "ncclAllGather");
         CommDestroy = (decltype(CommDestroy))dlsym(h, "ncclCommDestroy");
+        Send = (decltype(Send))dlsym(h, "ncclSend");
+        Recv = (decltype(Recv))dlsym(h, "ncclRecv");
         GetErrorString = (decltype(GetErrorString))dlsym(h, "ncclGetErrorString");
         if (!CommInitRank || !AllReduce || !AllGather) throw Error("NCCL symbols missing");
     }
@@ -69,6 +73,27 @@ ncclDataType_t nccl_dt(DT t) { return t == sbk::F32 ? ncclFloat32 : t == sbk::BF
 
 size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 }  // namespace
+
+// ---- point-to-point transport of the pipeline executor (pipeline_exec.cpp) ----
+void* p2p_comm_create(int world, int rank, const std::vector<char>& uid) {
+    nccl().load();
+    if (!nccl().Send || !nccl().Recv) throw Error("NCCL without ncclSend/ncclRecv");
+    ncclUniqueId id;
+    if (uid.size() != sizeof(id)) throw Error("nccl unique id must be 128 bytes");
+    std::memcpy(&id, uid.data(), sizeof(id));
+    ncclComm_t c = nullptr;
+    nccl().check(nccl().CommInitRank(&c, world, id, rank), "ncclCommInitRank (pipeline)");
+    return c;
+}
+void p2p_comm_destroy(void* c) {
+    if (c && nccl().CommDestroy) nccl().CommDestroy((ncclComm_t)c);
+}
+void p2p_send(void* c, const void* buf, i64 n, DT dt, int peer, cudaStream_t st) {
+    nccl().check(nccl().Send(buf, (size_t)n, nccl_dt(dt), peer, (ncclComm_t)c, st), "ncclSend");
+}
+void p2p_recv(void* c, void* buf, i64 n, DT dt, int peer, cudaStream_t st) {
+    nccl().check(nccl().Recv(buf, (size_t)n, nccl_dt(dt), peer, (ncclComm_t)c, st), "ncclRecv");
+}
 
 // ------------------------------------------------------------------ per rank
 struct RankCtx {

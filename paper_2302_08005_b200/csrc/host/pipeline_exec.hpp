@@ -31,12 +31,38 @@
 
 namespace sb {
 
+// One process per (stage, tensor-parallel rank): rank = stage * tp + tp_rank of `world` =
+// stages * tp processes. Stage-boundary values move with ncclSend / ncclRecv on a
+// pipeline communicator (pp_uid) between ranks of equal tp_rank; the stage's own
+// tensor parallelism runs on an NCCL communicator of its tp ranks (tp_uid, one per stage).
+struct PipeDist {
+    int rank = -1, world = 0;
+    std::vector<char> pp_uid, tp_uid;
+};
+
+// The per-rank transfer program of a distributed pipeline step (pure function of the plan):
+// forward, micro-batch m ascending: receive the remote inputs (sorted by producer stage,
+// output index), run, send each output to each remote consumer (stage order); backward,
+// m descending: receive the consumers' input gradients of each output (output index,
+// consumer stage order), run, send the remote inputs' gradients to their producers (sorted
+// as the forward receives). A pair of ranks thus posts matching transfers in the same
+// order in both directions; tests/test_pipeline_program_cpu.py checks matching and
+// deadlock freedom under rendezvous semantics over gloo and in simulation.
+struct PipeStep {
+    enum Kind : int { FwdRecv = 0, FwdRun = 1, FwdSend = 2, BwdRecv = 3, BwdRun = 4, BwdSend = 5 };
+    Kind kind;
+    int m, idx, peer;  // idx: the stage's input (Recv / BwdSend) or output (Send / BwdRecv) index
+    std::string value;
+};
+std::vector<PipeStep> pipe_program(const StagePlan& plan, int micro, int tp, int rank);
+
 class PipelineExecutor {
 public:
     // tp > 1: every stage runs its (sharded) module on tp lockstep ranks of its device
     // (tensor parallelism inside the stage; stage-boundary values are replicated)
     PipelineExecutor(const StagePlan& plan, int micro_batches, bool train, u64 seed, DT compute,
-                     std::vector<int> devices = {}, bool fused_kernels = true, int tp = 1);
+                     std::vector<int> devices = {}, bool fused_kernels = true, int tp = 1,
+                     const PipeDist* dist = nullptr);
     ~PipelineExecutor();
 
     // GPipe forward of every micro-batch; the model outputs concatenated along dim 0
