@@ -74,6 +74,7 @@ for _n, _a in {
     "sb_pipeline_executor_input_grad": (_P, _c.c_int, _c.c_int, _dp, _c.c_size_t, _c.POINTER(_c.c_size_t)),
     "sb_pipeline_executor_time_steps": (_P, _c.c_int, _c.POINTER(_c.c_float)),
     "sb_pipeline_executor_free": (_P,),
+    "sb_model_t5": (_c.c_int, _c.c_int, _i64, _i64, _i64, _i64, _i64, _i64, _c.c_double, _c.POINTER(_P)),
     "sb_model_tp_two_linear": (_i64, _i64, _i64, _c.POINTER(_P)),
     "sb_model_fig3c": (_c.POINTER(_P),),
     "sb_model_ffn_stack": (_c.c_int, _i64, _i64, _c.POINTER(_P)),
@@ -259,6 +260,14 @@ def gpt_neo(layers=24, hidden=8, heads=2, vocab=28, batch=4, seq=4, dropout_p=0.
     """GPT-Neo-style pre-LN causal decoder (f2, BASELINE.json configs[3]); no reference
     fixture exists — its oracle is the documented causal extension (oracle/causal_ext.py)."""
     return Model._make(_lib.sb_model_gpt_neo, layers, hidden, heads, vocab, batch, seq, dropout_p)
+
+
+def t5(enc_layers=2, dec_layers=2, hidden=8, heads=2, vocab=28, batch=4, enc_seq=4, dec_seq=4,
+       dropout_p=0.1) -> Model:
+    """T5-style encoder-decoder with cross-attention (f2, BASELINE.json configs[4]); two id
+    inputs (encoder, decoder); oracle: the causal extension (oracle/causal_ext.py)."""
+    return Model._make(_lib.sb_model_t5, enc_layers, dec_layers, hidden, heads, vocab, batch, enc_seq, dec_seq,
+                       dropout_p)
 
 
 def tp_two_linear(hidden=8, inner=16, batch=4) -> Model:

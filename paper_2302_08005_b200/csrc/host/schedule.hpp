@@ -135,6 +135,13 @@ struct DecoderConfig {
     double dropout_p = 0.1;
 };
 Module gpt_neo(const DecoderConfig& c);
+// f2: a T5-style encoder-decoder with cross-attention (BASELINE.json configs[4])
+struct T5Config {
+    int enc_layers = 2, dec_layers = 2;
+    i64 hidden = 8, heads = 2, vocab = 28, batch = 4, enc_seq = 4, dec_seq = 4;
+    double dropout_p = 0.1;
+};
+Module t5(const T5Config& c);
 Module tp_two_linear(i64 hidden, i64 inner, i64 batch);
 Module fig3c_exact();
 Module ffn_stack(int n, i64 hidden, i64 batch);

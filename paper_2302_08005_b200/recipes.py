@@ -135,3 +135,51 @@ def neo_script(layers: int, world: int = 1, flash: bool = True, fuse: bool = Tru
         s += "shard wte weight axis=0\nsync wte type=both\n"
     s += "".join(f"checkpoint h.{i}\n" for i in checkpoint_layers)
     return s
+
+
+def t5_script(enc_layers: int, dec_layers: int, world: int = 1, flash: bool = True, fused_qkv: bool = True,
+              checkpoint=(), shard_embeddings: bool = True) -> str:
+    """The encoder-decoder recipe (f2, BASELINE.json configs[4]) for ``t5``: self-attention
+    as FusedQKV (sharded blockwise on axis 0 + sync backward), cross-attention query / key /
+    value Linears sharded on axis 0 with sync backward (the key / value SyncGrads sum the
+    encoder output's gradient contributions), out_proj / mlp.wo row-parallel + sync forward,
+    mlp.wi column-parallel + sync backward, the shared vocab-parallel embedding + sync both;
+    every self-attention core replaced by EfficientAttention (the decoder's keeps its causal
+    attr; the cross-attention core cannot be — rule R4, q and k/v shapes differ — and runs as
+    the composed reference graph); checkpointing of the listed blocks ("encoder.block.0", ...)."""
+    s = f"# T5-style encoder-decoder recipe, TP={world}\n"
+
+    def self_attn(p):
+        nonlocal s
+        if fused_qkv:
+            s += f"replace {p}.qkv with FusedQKV\n"
+        if world > 1:
+            if fused_qkv:
+                s += f"shard {p}.qkv weight axis=0\nsync {p}.qkv type=backward\n"
+            s += f"shard {p}.out_proj weight,bias axis=1\nsync {p}.out_proj type=forward\n"
+        if flash:
+            s += f"replace {p}.core with EfficientAttention\n"
+
+    def mlp(p):
+        nonlocal s
+        if world > 1:
+            s += f"shard {p}.wi weight,bias axis=0\nsync {p}.wi type=backward\n"
+            s += f"shard {p}.wo weight,bias axis=1\nsync {p}.wo type=forward\n"
+
+    for i in range(enc_layers):
+        self_attn(f"encoder.block.{i}.attn")
+        mlp(f"encoder.block.{i}.mlp")
+    for i in range(dec_layers):
+        p = f"decoder.block.{i}"
+        self_attn(f"{p}.self_attn")
+        if world > 1:
+            for n in ("query", "key", "value"):
+                s += f"shard {p}.cross_attn.{n} weight axis=0\nsync {p}.cross_attn.{n} type=backward\n"
+            s += f"shard {p}.cross_attn.out_proj weight,bias axis=1\nsync {p}.cross_attn.out_proj type=forward\n"
+        # (the cross-attention core stays the composed reference graph: replacing it with
+        # EfficientAttention violates rule R4 — its q and k/v specs differ, S_dec vs S_enc)
+        mlp(f"{p}.mlp")
+    if world > 1 and shard_embeddings:
+        s += "shard shared weight axis=0\nsync shared type=both\n"
+    s += "".join(f"checkpoint {c}\n" for c in checkpoint)
+    return s

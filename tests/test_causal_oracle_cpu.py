@@ -171,3 +171,37 @@ def test_decoder_recipe_applies_identically(tmp_path, world):
     mine = s.apply().to_json()
     assert mine == open(os.path.join(out, "model.json")).read()
     assert '"causal": 1' in mine and "EfficientAttention" in mine
+
+
+T5 = dict(enc_layers=2, dec_layers=2, hidden=32, heads=4, vocab=32, batch=2, enc_seq=12, dec_seq=8, p=0.1)
+
+
+def _t5():
+    c = T5
+    return sb.t5(c["enc_layers"], c["dec_layers"], c["hidden"], c["heads"], c["vocab"], c["batch"], c["enc_seq"],
+                 c["dec_seq"], c["p"])
+
+
+@pytest.mark.parametrize("world", [1, 2])
+def test_t5_recipe_applies_identically(tmp_path, world):
+    """the encoder-decoder (cross-attention, shared embedding, two id inputs) loads into
+    the reference and its recipe applies to byte-identical JSON; replacing the
+    cross-attention core violates R4 on both sides (q and k/v shapes differ)"""
+    tmp = str(tmp_path)
+    m = _t5()
+    mj = _write(tmp, "t5.json", m.to_json())
+    script = recipes.t5_script(2, 2, world, checkpoint=["encoder.block.0", "decoder.block.1"])
+    sch = _write(tmp, "t5.sch", script)
+    out = os.path.join(tmp, "ref")
+    os.makedirs(out)
+    ref.run(model_json=mj, causal=True, schedule=sch, world=world, outdir=out, backward=0, mode="verify").close()
+    s = sb.create_schedule(m, world)
+    s.load_script(script)
+    assert s.apply().to_json() == open(os.path.join(out, "model.json")).read()
+    bad = _write(tmp, "bad.sch", "replace decoder.block.0.cross_attn.core with EfficientAttention\n")
+    with pytest.raises(RuntimeError, match="R4"):
+        ref.run(model_json=mj, causal=True, schedule=bad, outdir=out, backward=0, mode="verify")
+    s = sb.create_schedule(m, 1)
+    s.load_script(open(bad).read())
+    with pytest.raises(sb.SlapoError, match="R4"):
+        s.apply()

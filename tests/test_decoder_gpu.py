@@ -89,3 +89,48 @@ def test_decoder_prefix_independence(tmp_path):
     b = ex.forward([ids2])[0]
     assert np.array_equal(a[:, :64], b[:, :64])
     assert not np.array_equal(a[:, 64:], b[:, 64:])
+
+
+T5 = dict(enc_layers=2, dec_layers=2, hidden=32, heads=4, vocab=32, batch=2, enc_seq=24, dec_seq=16, p=0.1)
+
+
+def run_t5(tmp, cfg, script, world, mode="train", dtype="fp32", seed=123, input_seed=9):
+    m = sb.t5(cfg["enc_layers"], cfg["dec_layers"], cfg["hidden"], cfg["heads"], cfg["vocab"], cfg["batch"],
+              cfg["enc_seq"], cfg["dec_seq"], cfg["p"])
+    mj = os.path.join(tmp, "t5.json")
+    with open(mj, "w") as f:
+        f.write(m.to_json())
+    s = sb.create_schedule(m, world)
+    if script:
+        s.load_script(script)
+    ex = sb.Executor(s.apply(), mode, seed, world, dtype=dtype)
+    ex.forward(m.random_inputs(input_seed))
+    outs = [ex.outputs_of_rank(r) for r in range(world)]
+    grads = ex.backward_all_ranks()
+    r = ref.run(model_json=mj, causal=True, schedule=script or None, world=world, mode=mode, seed=seed,
+                input_seed=input_seed)
+    return ex, outs, grads, r
+
+
+@pytest.mark.parametrize("mode", ["train", "verify"])
+def test_t5_unscheduled_fp32(tmp_path, mode):
+    """encoder-decoder with cross-attention (S_dec x S_enc scores), causal decoder
+    self-attention, a shared embedding used twice, two id inputs"""
+    _, outs, grads, r = run_t5(str(tmp_path), T5, "", 1, mode)
+    check(outs, grads, r, 1, 1e-4, 1e-4)
+
+
+@pytest.mark.parametrize("world", [1, 2])
+def test_t5_recipe_fp32(tmp_path, world):
+    script = recipes.t5_script(2, 2, world, checkpoint=["encoder.block.0", "decoder.block.1"])
+    ex, outs, grads, r = run_t5(str(tmp_path), T5, script, world)
+    check(outs, grads, r, world, 1e-4, 1e-4)
+    assert ex.collective_invocations() == r.meta["collectives_total"]
+
+
+def test_t5_recipe_bf16(tmp_path):
+    cfg = dict(T5, hidden=256, heads=4, vocab=64, enc_seq=256, dec_seq=128)
+    script = recipes.t5_script(2, 2, 1, checkpoint=["decoder.block.0"])
+    _, outs, grads, r = run_t5(str(tmp_path), cfg, script, 1, dtype="bf16")
+    check(outs, grads, r, 1, BF16_OUT_TOL, BF16_GRAD_TOL, metric=rel_l2, tol_loss=BF16_LOSS_TOL,
+          record="t5_bf16_h256_enc256_dec128", loss_l1=True)
