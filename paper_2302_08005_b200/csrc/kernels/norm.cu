@@ -198,21 +198,33 @@ __global__ void k_ln_bwd(const T* x, const float* mean, const float* rstd, const
         ws[(i64)blockIdx.x * ncol * n + i] = acc;
     }
 }
-// block = 32 columns x 8 warps: warp w sums partial rows w, w+8, ... of its lane's
-// column, then warp 0 adds the 8 sums in warp order (fixed order: deterministic)
-__global__ void k_col_final(const float* ws, int blocks, i64 ncoln, float* o0, float* o1, float* o2, i64 n, bool accum) {
-    __shared__ float part[8][32];
+// block = 32 columns x 32 warps: warp w sums partial rows w, w+32, ... of its lane's
+// column with 8 loads in flight (the partials are L2-resident; a serial walk over the
+// ~300 block partials was latency-bound at ~9 us), then warp 0 adds the 32 sums in
+// warp order (fixed order: deterministic)
+__global__ void __launch_bounds__(1024) k_col_final(const float* ws, int blocks, i64 ncoln, float* o0, float* o1, float* o2,
+                                                    i64 n, bool accum) {
+    __shared__ float part[32][33];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const i64 i = blockIdx.x * 32ll + lane;
     float acc = 0.f;
-    if (i < ncoln)
-        for (int b = warp; b < blocks; b += 8) acc += ws[(i64)b * ncoln + i];
+    if (i < ncoln) {
+        int b = warp;
+        for (; b + 7 * 32 < blocks; b += 8 * 32) {
+            float a[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) a[u] = __ldcg(ws + (i64)(b + u * 32) * ncoln + i);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) acc += a[u];
+        }
+        for (; b < blocks; b += 32) acc += __ldcg(ws + (i64)b * ncoln + i);
+    }
     part[warp][lane] = acc;
     __syncthreads();
     if (warp == 0 && i < ncoln) {
         float t = 0.f;
 #pragma unroll
-        for (int w = 0; w < 8; ++w) t += part[w][lane];
+        for (int w = 0; w < 32; ++w) t += part[w][lane];
         int k = (int)(i / n);
         float* o = k == 0 ? o0 : k == 1 ? o1 : o2;
         if (o) o[i % n] = accum ? o[i % n] + t : t;
@@ -236,7 +248,7 @@ void layernorm_bwd(const void* x, const float* mean, const float* rstd, const vo
     int ncol = (dgamma || dbeta) ? 2 : 0;
     int vb = vec_blocks(rows);
     if (ln_bwd_vec(0, x, mean, rstd, gamma, g, gx, nullptr, gx_acc, true, t, rows, n, 0, 0, 1.f, nullptr, ws, ncol, vb, s)) {
-        if (ncol) k_col_final<<<col_final_grid(2 * n), 256, 0, s>>>(ws, vb, 2 * n, dgamma, dbeta, nullptr, n, col_acc);
+        if (ncol) k_col_final<<<col_final_grid(2 * n), 1024, 0, s>>>(ws, vb, 2 * n, dgamma, dbeta, nullptr, n, col_acc);
         SBK_CHECK_LAUNCH();
         return;
     }
@@ -249,7 +261,7 @@ void layernorm_bwd(const void* x, const float* mean, const float* rstd, const vo
         k<<<nb, 32 * kWarps, smem, s>>>((const T*)x, mean, rstd, (const T*)gamma, (const T*)g, (T*)gx, nullptr, gx_acc,
                                         rows, n, 0, 0, 1.f, ws, ncol, true);
     });
-    if (ncol) k_col_final<<<col_final_grid(2 * n), 256, 0, s>>>(ws, nb, 2 * n, dgamma, dbeta, nullptr, n, col_acc);
+    if (ncol) k_col_final<<<col_final_grid(2 * n), 1024, 0, s>>>(ws, nb, 2 * n, dgamma, dbeta, nullptr, n, col_acc);
     SBK_CHECK_LAUNCH();
 }
 
@@ -305,7 +317,7 @@ void bias_dropout_residual_ln_bwd(const void* sum, const float* mean, const floa
     int vb = vec_blocks(rows);
     if (ln_bwd_vec(1, sum, mean, rstd, gamma, g, g_partial, g_res, g_partial_acc, gres_acc, t, rows, n, s1, thr, dscale,
                    keep, ws, ncol, vb, s)) {
-        k_col_final<<<col_final_grid(3 * n), 256, 0, s>>>(ws, vb, 3 * n, dgamma, dbeta, dbias, n, col_acc);
+        k_col_final<<<col_final_grid(3 * n), 1024, 0, s>>>(ws, vb, 3 * n, dgamma, dbeta, dbias, n, col_acc);
         SBK_CHECK_LAUNCH();
         return;
     }
@@ -318,7 +330,7 @@ void bias_dropout_residual_ln_bwd(const void* sum, const float* mean, const floa
         k<<<nb, 32 * kWarps, smem, s>>>((const T*)sum, mean, rstd, (const T*)gamma, (const T*)g, (T*)g_partial, (T*)g_res,
                                         g_partial_acc, rows, n, s1, thr, dscale, ws, ncol, gres_acc);
     });
-    k_col_final<<<col_final_grid(3 * n), 256, 0, s>>>(ws, nb, 3 * n, dgamma, dbeta, dbias, n, col_acc);
+    k_col_final<<<col_final_grid(3 * n), 1024, 0, s>>>(ws, nb, 3 * n, dgamma, dbeta, dbias, n, col_acc);
     SBK_CHECK_LAUNCH();
 }
 

@@ -674,8 +674,10 @@ bool ln_bwd_vec(int mode, const void* x, const float* mean, const float* rstd, c
                 };
                 if constexpr (CPL % 4 == 0) {
                   if ((thr == 0 || keep) && !ln_narrow()) {
-                    // 4 warps per row, 16-warp blocks, two blocks per SM
-                    constexpr int WPR = 4;
+                    // 4 warps per row (8 at CPL 8: a 2048-wide bf16 row would otherwise hold two
+                    // chunks of column partials per thread and spill under the 64-register cap),
+                    // 16-warp blocks, two blocks per SM
+                    constexpr int WPR = CPL >= 8 ? 8 : 4;
                     const size_t sm2 = (size_t)16 * ncol * (n / WPR) * 4 + 2 * 16 * 2 * 4;
                     auto k = mode == 0 ? k_ln_bwd_w<T, CPL, 0, WPR> : k_ln_bwd_w<T, CPL, 1, WPR>;
                     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
