@@ -14,6 +14,7 @@
 #include <sstream>
 
 #include "rng.hpp"
+#include <nvtx3/nvToolsExt.h>
 
 namespace sb {
 
@@ -72,6 +73,25 @@ Nccl& nccl() {
 ncclDataType_t nccl_dt(DT t) { return t == sbk::F32 ? ncclFloat32 : t == sbk::BF16 ? ncclBfloat16 : ncclFloat64; }
 
 size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+
+// NVTX ranges per plan op (SB_NVTX=1; header-only NVTX v3, no-ops without a tool attached):
+// "<op kind>[ (bwd)| (re)] <module path>" around each op's launches — eager steps only (a
+// captured CUDA graph replays kernels, not host ranges)
+struct NvtxRange {
+    bool on;
+    NvtxRange(const char* kind, const char* tag, const std::string& path) : on(enabled()) {
+        if (!on) return;
+        std::string n = std::string(kind) + tag + " " + path;
+        nvtxRangePushA(n.c_str());
+    }
+    ~NvtxRange() {
+        if (on) nvtxRangePop();
+    }
+    static bool enabled() {
+        static const bool e = getenv("SB_NVTX") && atoi(getenv("SB_NVTX"));
+        return e;
+    }
+};
 }  // namespace
 
 // ---- point-to-point transport of the pipeline executor (pipeline_exec.cpp) ----
@@ -844,6 +864,7 @@ public:
     // ------------------------------------------------------- forward op
     void fwd_op(int i, bool recompute = false) {
         const Op& op0 = ranks[0].P.fwd[(size_t)i];
+        NvtxRange trace(k_str(op0.k), recompute ? " (re)" : "", op0.path);
         if (profiling) prof_begin(std::string(k_str(op0.k)) + (recompute ? "(re)" : ""));
         switch (op0.k) {
             case K::AllReduce: {
@@ -1266,6 +1287,7 @@ public:
 
     void bwd_op(int i) {
         const Op& op0 = ranks[0].P.fwd[(size_t)i];
+        NvtxRange trace(k_str(op0.k), " (bwd)", op0.path);
         if (profiling) prof_begin(std::string(k_str(op0.k)) + "(bwd)");
         if (early_ar.size() > (size_t)i && early_ar[(size_t)i] >= 0) {
             linear_bwd_overlapped(i);

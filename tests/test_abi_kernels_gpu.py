@@ -171,3 +171,21 @@ def test_allreduce_local():
     for o in outs:
         close(o, want, 1e-6)
         assert torch.equal(o, outs[0])
+
+
+def test_nvtx_tracing_runs(tmp_path):
+    """SB_NVTX=1 wraps every plan op in an NVTX range (no tool attached: no-ops); the step's
+    results are unchanged"""
+    import os
+    import subprocess
+    import sys
+    code = ("import sys, numpy as np; sys.path.insert(0, %r)\n"
+            "import paper_2302_08005_b200 as sb\n"
+            "m = sb.toy_bert(2, 32, 4, 32, 2, 8, 0.1); ex = sb.Executor(m, 'train', 1, 1)\n"
+            "o = ex.forward(m.random_inputs(3))[0]; g = ex.backward().params\n"
+            "print(float(np.abs(o).sum()) + sum(float(np.abs(v).sum()) for v in g.values()))\n") % os.path.dirname(
+        os.path.dirname(os.path.abspath(__file__)))
+    out = [subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300,
+                          env=dict(os.environ, SB_NVTX=v)) for v in ("0", "1")]
+    assert all(r.returncode == 0 for r in out), [r.stderr for r in out]
+    assert out[0].stdout == out[1].stdout
