@@ -1,6 +1,9 @@
-cd $GRAFT_REPO_ROOT
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/smi.txt 2>&1
-timeout 1200 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_gpu.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/smoke.log 2>&1; echo "rc=$?" >> gpurun_out/smoke.log
-timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?" >> gpurun_out/bench.err
-timeout 600 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
+#!/bin/bash
+# full GPU check of the committed tree: tests, smoke, the driver's bench sequence, launch list
+mkdir -p gpurun_out; O=gpurun_out
+SB_PARITY_OUT=$O/parity timeout 2400 python -m pytest tests -m gpu -q -p no:cacheprovider > $O/final_pytest.log 2>&1; echo "pytest rc=$?" >> $O/final_pytest.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/final_smoke.log 2>&1; echo "smoke rc=$?" >> $O/final_smoke.log
+timeout 1800 python3 bench.py --impl reference --gpus 1 --steps 20 --warmup 5 > $O/final_ref.out 2> $O/final_ref.err
+timeout 1800 python3 bench.py --gpus 1 --steps 20 --warmup 5 > $O/final_n1.out 2> $O/final_n1.err
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -s 2262 -c 754 --csv --log-file $O/final_launches.csv \
+    python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-graph > $O/final_ncu_list.log 2>&1
