@@ -1220,6 +1220,7 @@ public:
         a.lse = (float*)fp(r, op.out[1]);
         a.B = q.shape[0];
         a.S = q.shape[1];
+        a.Sk = V(r, op.in[1]).shape[1] != a.S ? V(r, op.in[1]).shape[1] : 0;  // cross-attention keys
         a.nh = op.nh;
         a.hd = op.hd;
         a.scale = (float)op.scale;
@@ -1228,7 +1229,7 @@ public:
         a.dscale = (float)(1.0 / (1.0 - op.p));
         a.t = cdt;
         a.mask = op.dropout ? (const uint32_t*)fp(r, op.out[2]) : nullptr;
-        if (a.mask && a.S % 128 == 0) a.mask_t = a.mask + (a.B * a.nh * a.S * a.S) / 32;
+        if (a.mask && a.S % 128 == 0 && a.keys() % 128 == 0) a.mask_t = a.mask + (a.B * a.nh * a.S * a.keys()) / 32;
         a.causal = op.causal;
         return a;
     }
@@ -1663,10 +1664,10 @@ public:
                 continue;
             }
             sbk::Attn a = attn_args(r, op);
-            if (a.S % 128 == 0)
-                sbk::dropout_mask_dual((uint32_t*)fp(r, op.out[2]), a.B * a.nh, a.S, op.s1, op.thr, ms);
+            if (a.S % 128 == 0 && a.keys() % 128 == 0)
+                sbk::dropout_mask_dual((uint32_t*)fp(r, op.out[2]), a.B * a.nh, a.S, op.s1, op.thr, ms, a.keys());
             else
-                sbk::dropout_mask((uint32_t*)fp(r, op.out[2]), a.B * a.nh * a.S * a.S, op.s1, op.thr, ms);
+                sbk::dropout_mask((uint32_t*)fp(r, op.out[2]), a.B * a.nh * a.S * a.keys(), op.s1, op.thr, ms);
         }
         if (!side) return;
         CK(cudaEventRecord(mask_ev[i], mstream));

@@ -209,9 +209,72 @@ struct Lowerer {
         if (m.composite()) {
             Val out;
             if (o.fused_kernels && get_flag(m.attrs, "fused") && try_fused(m, path, args, out)) return out;
+            if (o.fused_kernels && try_cross_core(m, path, args, out)) return out;
             return eval_graph(*m.forward, m, path, args);
         }
         return eval_builtin(m, path, args);
+    }
+
+    // A cross-attention core (queries of one length, keys / values of another) left in its
+    // composed form — the reference's rule R4 forbids replacing it with EfficientAttention —
+    // is recognised by its graph (library.cpp:9-34's op sequence) and lowered to the flash
+    // kernels: the same math and the same dropout draws (flat index over the (B, nh, Sq, Sk)
+    // probabilities), only the (B, nh, Sq, Sk) intermediates are never stored. The activation
+    // ledger still counts the composed graph's outputs (the reference's accounting rule).
+    // SB_ATTN_CORE_FLASH=0 keeps the composed path.
+    bool try_cross_core(const Module& m, const std::string& path, const std::vector<Val>& args, Val& out) {
+        static const bool on = !(getenv("SB_ATTN_CORE_FLASH") && atoi(getenv("SB_ATTN_CORE_FLASH")) == 0);
+        if (!on || !m.forward || args.size() != 3 || !m.children.empty()) return false;
+        const Graph& g = *m.forward;
+        std::vector<const Node*> ops;
+        for (auto& n : g.nodes) {
+            if (n.kind == NK::Input || n.kind == NK::Output) continue;
+            if (n.kind != NK::CallOp) return false;
+            ops.push_back(&n);
+        }
+        static const char* seq[] = {"reshape", "transpose", "reshape", "transpose", "reshape", "transpose", "transpose",
+                                    "matmul",  "scale",     "softmax", "dropout", "matmul",    "transpose", "reshape"};
+        if (ops.size() != 14 || g.inputs.size() != 3) return false;
+        for (size_t i = 0; i < ops.size(); ++i)
+            if (ops[i]->op != seq[i]) return false;
+        // wiring: heads(q), heads(k), heads(v); k^T; scores; ...
+        auto arg = [&](int i, int k) { return ops[(size_t)i]->args.at((size_t)k); };
+        auto id = [&](int i) { return ops[(size_t)i]->id; };
+        if (arg(0, 0) != g.inputs[0] || arg(1, 0) != id(0) || arg(2, 0) != g.inputs[1] || arg(3, 0) != id(2) ||
+            arg(4, 0) != g.inputs[2] || arg(5, 0) != id(4) || arg(6, 0) != id(3) || arg(7, 0) != id(1) ||
+            arg(7, 1) != id(6) || arg(8, 0) != id(7) || arg(9, 0) != id(8) || arg(10, 0) != id(9) ||
+            arg(11, 0) != id(10) || arg(11, 1) != id(5) || arg(12, 0) != id(11) || arg(13, 0) != id(12) ||
+            g.out_node().args.size() != 1 || g.out_node().args[0] != id(13))
+            return false;
+        const i64 hd = get_int(ops[0]->attrs, "factor").value_or(0);
+        if (hd <= 0 || get_int(ops[9]->attrs, "axis").value_or(-1) != -1) return false;
+        if (get_int(ops[2]->attrs, "factor").value_or(0) != hd || get_int(ops[4]->attrs, "factor").value_or(0) != hd)
+            return false;
+        for (int i : {0, 2, 4})
+            if (get_int(ops[(size_t)i]->attrs, "split_axis").value_or(-1) != 2) return false;
+        const View& q = V(args[0].one());
+        const View& k = V(args[1].one());
+        const View& v = V(args[2].one());
+        if (q.shape.size() != 3 || k.shape != v.shape || k.shape.size() != 3 || k.shape[0] != q.shape[0] ||
+            k.shape[2] != q.shape[2] || k.shape[1] == q.shape[1])  // (equal lengths: the schedule's EfficientAttention)
+            return false;
+        if (get_flag(ops[9]->attrs, "causal")) return false;  // (causal cross-attention: composed)
+        Module ea;
+        ea.kind = "EfficientAttention";
+        ea.attrs["head_dim"] = hd;
+        ea.attrs["p"] = get_double(ops[10]->attrs, "p").value_or(0.0);
+        ea.attrs["seed"] = get_int(ops[10]->attrs, "seed").value_or(0);
+        ea.attrs["scale"] = get_double(ops[8]->attrs, "factor").value_or(1.0);
+        const bool led = ledger_on;
+        ledger_on = false;  // the composed graph's ledger below
+        out = flash_attention(ea, path, args);
+        ledger_on = led;
+        if (ledger_on) {
+            const i64 B = q.shape[0], Sq = q.shape[1], Sk = k.shape[1], H = q.shape[2], nh = H / hd;
+            const i64 elems = 5 * B * Sq * H + 5 * B * Sk * H + 4 * B * nh * Sq * Sk;
+            P.ledger_bytes += elems * dtype_bytes(q.rdt);
+        }
+        return true;
     }
 
     // index_input: the synced value is an Embedding's id tensor, whose gradient is zero by
@@ -437,13 +500,16 @@ struct Lowerer {
         double scale = get_double(m.attrs, "scale").value_or(1.0 / std::sqrt((double)hd));
         int q = rowwise(args[0].one()), k = rowwise(args[1].one()), v = rowwise(args[2].one());
         auto& sh = V(q).shape;
-        if (sh.size() != 3 || V(k).shape != sh || V(v).shape != sh || sh[2] % hd != 0) {
+        const auto& ksh = V(k).shape;
+        const bool cross = ksh.size() == 3 && sh.size() == 3 && ksh[1] != sh[1];  // Sk != Sq (keys, values alike)
+        if (sh.size() != 3 || V(v).shape != ksh || ksh.size() != 3 || ksh[0] != sh[0] || ksh[2] != sh[2] ||
+            sh[2] % hd != 0 || (cross && get_flag(m.attrs, "causal"))) {
             // shapes the kernel does not cover: the reference graph, recomputed
             Module ref = composed_attention(m);
             return eval_graph(*ref.forward, ref, path, args);
         }
         if (p >= 1.0 && o.train) throw Error("dropout p must be < 1");
-        i64 B = sh[0], S = sh[1], nh = sh[2] / hd;
+        i64 B = sh[0], S = sh[1], Sk = ksh[1], nh = sh[2] / hd;
         int out = fresh(sh, V(q).rdt);
         Op op;
         op.k = K::FlashAttn;
@@ -453,8 +519,8 @@ struct Lowerer {
             // 1-bit keep mask, persistent even inside a checkpoint region: it is a
             // pure function of the seeds, so recompute re-reads it
             // (both layouts when S % 128 == 0: natural for the forward, transposed for the backward)
-            const i64 words = (B * nh * S * S + 31) / 32;
-            int mv = aux(S % 128 == 0 ? 2 * words : words);
+            const i64 words = (B * nh * S * Sk + 31) / 32;
+            int mv = aux(S % 128 == 0 && Sk % 128 == 0 ? 2 * words : words);
             P.st[(size_t)V(mv).st].region = -1;
             op.out.push_back(mv);
         }

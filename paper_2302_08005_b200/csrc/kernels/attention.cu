@@ -25,8 +25,9 @@ bool attn_bwd_tc_try(const Attn& a, const void* dout, i64 ld_do, void* dq, void*
 namespace {
 constexpr int kT = 64;  // rows per block / keys per tile
 
-__device__ __forceinline__ uint64_t drop_index(i64 b, i64 h, i64 nh, i64 S, i64 i, i64 j) {
-    return (uint64_t)(((b * nh + h) * S + i) * S + j);
+// the reference's flat index of probability (b, h, query i, key j) in a (B, nh, Sq, Sk) tensor
+__device__ __forceinline__ uint64_t drop_index(i64 b, i64 h, i64 nh, i64 Sq, i64 Sk, i64 i, i64 j) {
+    return (uint64_t)(((b * nh + h) * Sq + i) * Sk + j);
 }
 
 template <class T, int HD>
@@ -37,6 +38,7 @@ __global__ void __launch_bounds__(kT) k_attn_fwd(Attn a) {
     float* Ss = Vs + kT * HD;       // [kT threads][kT]
     const int hd = (int)a.hd;
     i64 b = blockIdx.z, h = blockIdx.y, i = (i64)blockIdx.x * kT + threadIdx.x;
+    const i64 Sk = a.keys();
     const T* Q = (const T*)a.q;
     const T* Kg = (const T*)a.k;
     const T* Vg = (const T*)a.v;
@@ -50,18 +52,18 @@ __global__ void __launch_bounds__(kT) k_attn_fwd(Attn a) {
     float m = -INFINITY, l = 0.f;
     float* srow = Ss + threadIdx.x * kT;
     // causal: key tiles past this block's last query are fully masked
-    const i64 jend = a.causal ? min(a.S, (i64)(blockIdx.x + 1) * kT) : a.S;
+    const i64 jend = a.causal ? min(Sk, (i64)(blockIdx.x + 1) * kT) : Sk;
     for (i64 j0 = 0; j0 < jend; j0 += kT) {
         __syncthreads();
         for (int e = threadIdx.x; e < kT * HD; e += kT) {
             int jj = e / HD, d = e % HD;
             i64 j = j0 + jj;
-            bool ok = j < a.S && d < hd;
-            Ks[e] = ok ? to_f(Kg[(b * a.S + j) * a.ld_k + h * hd + d]) : 0.f;
-            Vs[e] = ok ? to_f(Vg[(b * a.S + j) * a.ld_v + h * hd + d]) : 0.f;
+            bool ok = j < Sk && d < hd;
+            Ks[e] = ok ? to_f(Kg[(b * Sk + j) * a.ld_k + h * hd + d]) : 0.f;
+            Vs[e] = ok ? to_f(Vg[(b * Sk + j) * a.ld_v + h * hd + d]) : 0.f;
         }
         __syncthreads();
-        int nj = (int)min((i64)kT, a.S - j0);
+        int nj = (int)min((i64)kT, Sk - j0);
         float tmax = -INFINITY;
         for (int jj = 0; jj < nj; ++jj) {
             float s = 0.f;
@@ -79,7 +81,7 @@ __global__ void __launch_bounds__(kT) k_attn_fwd(Attn a) {
         for (int jj = 0; jj < nj; ++jj) {
             float p = __expf(srow[jj] - mn);
             l += p;
-            if (a.thr && !d_keep(a.s1, drop_index(b, h, a.nh, a.S, i, j0 + jj), a.thr)) continue;
+            if (a.thr && !d_keep(a.s1, drop_index(b, h, a.nh, a.S, Sk, i, j0 + jj), a.thr)) continue;
             float w = a.thr ? p * a.dscale : p;
 #pragma unroll
             for (int d = 0; d < HD; ++d) o[d] = fmaf(w, Vs[jj * HD + d], o[d]);
@@ -117,12 +119,13 @@ __global__ void __launch_bounds__(kT) k_attn_dkdv(Attn a, const T* dout, i64 ld_
     float* Es = Ls + kT;         // delta
     const int hd = (int)a.hd;
     i64 b = blockIdx.z, h = blockIdx.y, j = (i64)blockIdx.x * kT + threadIdx.x;
-    bool valid = j < a.S;
+    const i64 Sk = a.keys();
+    bool valid = j < Sk;
     float k[HD], v[HD], gk[HD], gv[HD];
 #pragma unroll
     for (int d = 0; d < HD; ++d) {
-        k[d] = (valid && d < hd) ? to_f(((const T*)a.k)[(b * a.S + j) * a.ld_k + h * hd + d]) : 0.f;
-        v[d] = (valid && d < hd) ? to_f(((const T*)a.v)[(b * a.S + j) * a.ld_v + h * hd + d]) : 0.f;
+        k[d] = (valid && d < hd) ? to_f(((const T*)a.k)[(b * Sk + j) * a.ld_k + h * hd + d]) : 0.f;
+        v[d] = (valid && d < hd) ? to_f(((const T*)a.v)[(b * Sk + j) * a.ld_v + h * hd + d]) : 0.f;
         gk[d] = gv[d] = 0.f;
     }
     // causal: query tiles before this key block see none of its keys
@@ -151,7 +154,7 @@ __global__ void __launch_bounds__(kT) k_attn_dkdv(Attn a, const T* dout, i64 ld_
                 dpd = fmaf(Ds[ii * HD + d], v[d], dpd);
             }
             float p = (a.causal && j > i0 + ii) ? 0.f : __expf(s * a.scale - Ls[ii]);
-            bool keep = !a.thr || d_keep(a.s1, drop_index(b, h, a.nh, a.S, i0 + ii, j), a.thr);
+            bool keep = !a.thr || d_keep(a.s1, drop_index(b, h, a.nh, a.S, Sk, i0 + ii, j), a.thr);
             float c = a.thr ? (keep ? a.dscale : 0.f) : 1.f;
             float pd = p * c;
             float ds = p * (c * dpd - Es[ii]);
@@ -164,7 +167,7 @@ __global__ void __launch_bounds__(kT) k_attn_dkdv(Attn a, const T* dout, i64 ld_
     }
     if (!valid) return;
     for (int d = 0; d < hd; ++d) {
-        i64 ik = (b * a.S + j) * ld_dk + h * hd + d, iv = (b * a.S + j) * ld_dv + h * hd + d;
+        i64 ik = (b * Sk + j) * ld_dk + h * hd + d, iv = (b * Sk + j) * ld_dv + h * hd + d;
         dk[ik] = from_f<T>(((a.acc_mask & 2) ? to_f(dk[ik]) : 0.f) + a.scale * gk[d]);
         dv[iv] = from_f<T>(((a.acc_mask & 4) ? to_f(dv[iv]) : 0.f) + gv[d]);
     }
@@ -178,6 +181,7 @@ __global__ void __launch_bounds__(kT) k_attn_dq(Attn a, const T* dout, i64 ld_do
     float* Vs = Ks + kT * HD;
     const int hd = (int)a.hd;
     i64 b = blockIdx.z, h = blockIdx.y, i = (i64)blockIdx.x * kT + threadIdx.x;
+    const i64 Sk = a.keys();
     bool valid = i < a.S;
     float q[HD], g[HD], gq[HD];
 #pragma unroll
@@ -187,19 +191,19 @@ __global__ void __launch_bounds__(kT) k_attn_dq(Attn a, const T* dout, i64 ld_do
         gq[d] = 0.f;
     }
     float L = valid ? a.lse[(b * a.nh + h) * a.S + i] : 0.f, E = valid ? delta[(b * a.nh + h) * a.S + i] : 0.f;
-    const i64 jend = a.causal ? min(a.S, (i64)(blockIdx.x + 1) * kT) : a.S;
+    const i64 jend = a.causal ? min(Sk, (i64)(blockIdx.x + 1) * kT) : Sk;
     for (i64 j0 = 0; j0 < jend; j0 += kT) {
         __syncthreads();
         for (int e = threadIdx.x; e < kT * HD; e += kT) {
             int jj = e / HD, d = e % HD;
             i64 j = j0 + jj;
-            bool ok = j < a.S && d < hd;
-            Ks[e] = ok ? to_f(((const T*)a.k)[(b * a.S + j) * a.ld_k + h * hd + d]) : 0.f;
-            Vs[e] = ok ? to_f(((const T*)a.v)[(b * a.S + j) * a.ld_v + h * hd + d]) : 0.f;
+            bool ok = j < Sk && d < hd;
+            Ks[e] = ok ? to_f(((const T*)a.k)[(b * Sk + j) * a.ld_k + h * hd + d]) : 0.f;
+            Vs[e] = ok ? to_f(((const T*)a.v)[(b * Sk + j) * a.ld_v + h * hd + d]) : 0.f;
         }
         __syncthreads();
         if (!valid) continue;
-        int nj = (int)min((i64)kT, a.S - j0);
+        int nj = (int)min((i64)kT, Sk - j0);
         for (int jj = 0; jj < nj; ++jj) {
             float s = 0.f, dpd = 0.f;
 #pragma unroll
@@ -208,7 +212,7 @@ __global__ void __launch_bounds__(kT) k_attn_dq(Attn a, const T* dout, i64 ld_do
                 dpd = fmaf(g[d], Vs[jj * HD + d], dpd);
             }
             float p = (a.causal && j0 + jj > i) ? 0.f : __expf(s * a.scale - L);
-            bool keep = !a.thr || d_keep(a.s1, drop_index(b, h, a.nh, a.S, i, j0 + jj), a.thr);
+            bool keep = !a.thr || d_keep(a.s1, drop_index(b, h, a.nh, a.S, Sk, i, j0 + jj), a.thr);
             float c = a.thr ? (keep ? a.dscale : 0.f) : 1.f;
             float ds = p * (c * dpd - E);
 #pragma unroll
@@ -249,6 +253,7 @@ size_t attn_bwd_workspace(i64 B, i64 S, i64 nh, i64 hd) {
 int attn_last_engine(int bwd) { return bwd ? g_attn_last_bwd : g_attn_last_fwd; }
 
 void attn_fwd(const Attn& a, cudaStream_t s) {
+    if (a.causal && a.keys() != a.S) throw std::runtime_error("attention: causal needs as many keys as queries");
     if (g_attn_max_engine == 0 && attn_fwd_sm100_try(a, s)) {
         g_attn_last_fwd = 3;
         return;
@@ -278,6 +283,7 @@ void attn_fwd(const Attn& a, cudaStream_t s) {
 
 void attn_bwd(const Attn& a, const void* dout, i64 ld_do, void* dq, void* dk, void* dv, i64 ld_dq, i64 ld_dk, i64 ld_dv,
               void* ws, cudaStream_t s) {
+    if (a.causal && a.keys() != a.S) throw std::runtime_error("attention: causal needs as many keys as queries");
     float* delta = (float*)ws;
     if (g_attn_max_engine == 0 && attn_bwd_sm100_try(a, dout, ld_do, dq, dk, dv, ld_dq, ld_dk, ld_dv, ws, s)) {
         g_attn_last_bwd = 3;
@@ -302,7 +308,8 @@ void attn_bwd(const Attn& a, const void* dout, i64 ld_do, void* dq, void* dk, vo
                 auto k2 = k_attn_dq<T, HD>;
                 smem_attr(k1, s1);
                 smem_attr(k2, s2);
-                k1<<<grid, kT, s1, s>>>(a, (const T*)dout, ld_do, (T*)dk, (T*)dv, ld_dk, ld_dv, delta);
+                const dim3 gk((unsigned)((a.keys() + kT - 1) / kT), (unsigned)a.nh, (unsigned)a.B);  // one thread per key
+                k1<<<gk, kT, s1, s>>>(a, (const T*)dout, ld_do, (T*)dk, (T*)dv, ld_dk, ld_dv, delta);
                 k2<<<grid, kT, s2, s>>>(a, (const T*)dout, ld_do, (T*)dq, ld_dq, delta);
             });
         } else {

@@ -54,6 +54,7 @@ struct FwdArgs {
     float c;               // scale * log2(e)
     int S, nh;
     int dbg;               // debugging switches (SB_ATTN_DBG): 1 skip softmax math, 4 skip MMAs
+    int Sk = 0;            // keys per sequence (cross-attention, k_fa6_fwd<false, D> only); 0: S
 };
 
 template <int NT>
@@ -345,7 +346,7 @@ __global__ void __launch_bounds__(F6_THREADS, F6<D>::CTAS)
     uint32_t* tslot = (uint32_t*)(m_empty + 2);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    const int S = fa.S, nj = S / KC6, nq = S / FT, nbh = ntiles / nq;
+    const int S = fa.S, Sk = fa.Sk ? fa.Sk : S, nj = Sk / KC6, nq = S / FT, nbh = ntiles / nq;
     // causal tiles differ in length (q-tile i has i+1 128-key spans), so they are walked
     // heaviest q-tile first — the grid-stride walk then balances instead of handing every
     // CTA the same q-tile (gridDim % nq == 0)
@@ -383,7 +384,7 @@ __global__ void __launch_bounds__(F6_THREADS, F6<D>::CTAS)
             int u = 0, n = 0, pp = 0;  // chunks / tiles / keep-bit chunk pairs loaded by this CTA
             for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++n) {
                 const int bh = tile_bh(t), b = bh / fa.nh, h = bh % fa.nh;
-                const int row_base = b * S;
+                const int row_base = b * S, kv_base = b * Sk;  // (query rows / key rows)
                 const int qb = n % F6_QBUF;
                 mbar_wait(&q_empty[qb], ((n / F6_QBUF) & 1) ^ 1);
                 mbar_expect_tx(&q_full[qb], C::Q_BYTES);
@@ -411,9 +412,9 @@ __global__ void __launch_bounds__(F6_THREADS, F6<D>::CTAS)
 #pragma unroll
                     for (int pn = 0; pn < C::PANELS; ++pn) {
                         tma_load_2d(sK + s * C::KV_BYTES + pn * C::KV_PANEL, &tK, &kv_full[s], h * D + 64 * pn,
-                                    row_base + j * KC6);
+                                    kv_base + j * KC6);
                         tma_load_2d(sV + s * C::KV_BYTES + pn * C::KV_PANEL, &tV, &kv_full[s], h * D + 64 * pn,
-                                    row_base + j * KC6);
+                                    kv_base + j * KC6);
                     }
                 }
             }
@@ -605,6 +606,8 @@ __global__ void __launch_bounds__(F6_THREADS, F6<D>::CTAS)
 }
 
 bool fwd_fits(const Attn& a, int hd = FD) {
+    // cross-attention (keys != queries): non-causal, whole 128-key blocks
+    if (a.keys() != a.S && (a.causal || a.keys() % FT || a.keys() < FT)) return false;
     if (a.t != BF16 || a.hd != hd || a.S % FT || a.S < FT) return false;
     if (a.thr && !a.mask) return false;
     auto al = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
@@ -650,6 +653,7 @@ struct BwdArgs {
     int S, nh, acc;
     int dbg;  // debugging switches (SB_ATTN_DBG): 1 skip softmax math, 2 skip dQ accumulation, 4 skip MMAs
     unsigned long long* ts;  // debugging timeline (SB_ATTN_TS): [role][event], CTA (0,0) only
+    int Sk = 0;  // keys per sequence (cross-attention, non-causal k_fa7_bwd / k_fa8_bwd); 0: S
 };
 __device__ __forceinline__ unsigned long long gtime() {
     unsigned long long t;
@@ -1147,10 +1151,11 @@ __device__ __forceinline__ void warp_tile_tma(uint8_t* stage, const CUtensorMap*
 // step u -> (key block j, query block i): all nj x nj pairs, or for causal attention only
 // the i >= j ones (queries at or after the keys; the rest is masked out entirely)
 template <bool CAUSAL>
-__device__ __forceinline__ void step_ji(int u, int nj, int& j, int& i) {
-    if (!CAUSAL) {
-        j = u / nj;
-        i = u % nj;
+__device__ __forceinline__ void step_ji(int u, int nj, int& j, int& i, int nq = 0) {
+    if (!CAUSAL) {  // nq query blocks per key block (cross-attention: nq != nj)
+        if (!nq) nq = nj;
+        j = u / nq;
+        i = u % nq;
         return;
     }
     j = 0;
@@ -1194,11 +1199,13 @@ __global__ void __launch_bounds__(B7_WARPS * 32, 1)
     uint32_t* tslot = (uint32_t*)(ds_full + 2);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    const int S = ba.S, nj = S / FT, nsteps = CAUSAL ? nj * (nj + 1) / 2 : nj * nj;
+    // nj key blocks (outer) x nq query blocks (inner); cross-attention (Sk != S) is non-causal
+    const int S = ba.S, Sk = ba.Sk ? ba.Sk : S, nj = Sk / FT, nq = S / FT;
+    const int nsteps = CAUSAL ? nj * (nj + 1) / 2 : nj * nq;
     auto first_i = [&](int j) { return CAUSAL ? j : 0; };  // first query block of key block j
     const int h = blockIdx.x, b = blockIdx.y;
     const long long bh = (long long)b * ba.nh + h;
-    const int row_base = b * S;
+    const int row_base = b * S, kv_base = b * Sk;  // (query rows / key rows)
     const bool TS7 = ba.ts && blockIdx.x == 0 && blockIdx.y == 0;
 
     if (threadIdx.x == 0) {
@@ -1243,8 +1250,8 @@ __global__ void __launch_bounds__(B7_WARPS * 32, 1)
                 if (j >= 2) mbar_wait(&k_empty[kb], ((j >> 1) & 1) ^ 1);
                 if (j >= 1) mbar_wait(v_empty, (j - 1) & 1);
                 mbar_expect_tx(&kv_full[kb], 2 * F_TILE_BYTES);
-                tma_load_2d(sK + kb * F_TILE_BYTES, &tK, &kv_full[kb], h * FD, row_base + j * FT);
-                tma_load_2d(sV, &tV, &kv_full[kb], h * FD, row_base + j * FT);
+                tma_load_2d(sK + kb * F_TILE_BYTES, &tK, &kv_full[kb], h * FD, kv_base + j * FT);
+                tma_load_2d(sV, &tV, &kv_full[kb], h * FD, kv_base + j * FT);
             };
             load_kv(0);
             // K/V of block j+1 go out before the stage of step (j, min(2, nj-1)): late
@@ -1252,8 +1259,8 @@ __global__ void __launch_bounds__(B7_WARPS * 32, 1)
             // enough that block j+1 never waits for them
             for (int u = 0; u < nsteps; ++u) {
                 int j, i;
-                step_ji<CAUSAL>(u, nj, j, i);
-                const int bl = nj - first_i(j);  // steps of key block j
+                step_ji<CAUSAL>(u, nj, j, i, nq);
+                const int bl = (CAUSAL ? nj : nq) - first_i(j);  // steps of key block j
                 if (i - first_i(j) == (bl > 2 ? 2 : bl - 1) && j + 1 < nj) load_kv(j + 1);
                 const int s = u % B7_NST;
                 uint8_t* st = sStage + s * B7_STAGE;
@@ -1266,7 +1273,7 @@ __global__ void __launch_bounds__(B7_WARPS * 32, 1)
                 bulk_load(st + 2 * F_TILE_BYTES, ba.lse2 + bh * S + i * FT, 512, &st_full[s]);
                 bulk_load(st + 2 * F_TILE_BYTES + 512, ba.delta + bh * S + i * FT, 512, &st_full[s]);
                 if (ba.mask_t)
-                    tma_load_2d(st + 2 * F_TILE_BYTES + 1024, &tM, &st_full[s], i * (FT / 32), (int)(bh * S) + j * FT);
+                    tma_load_2d(st + 2 * F_TILE_BYTES + 1024, &tM, &st_full[s], i * (FT / 32), (int)(bh * Sk) + j * FT);
             }
         }
     } else if (warp == W_MMA) {
@@ -1280,7 +1287,7 @@ __global__ void __launch_bounds__(B7_WARPS * 32, 1)
         const uint32_t stage0 = smem_u32(sStage);
         auto issue_sdp = [&](int u, int hh) {
             int j, i;
-            step_ji<CAUSAL>(u, nj, j, i);
+            step_ji<CAUSAL>(u, nj, j, i, nq);
             const int s = u % B7_NST;
             const uint32_t aQ = stage0 + s * B7_STAGE + hh * (F_TILE_BYTES / 2);
             if (hh == 0) {
@@ -1303,7 +1310,7 @@ __global__ void __launch_bounds__(B7_WARPS * 32, 1)
         issue_sdp(0, 1);
         for (int u = 0; u < nsteps; ++u) {
             int j, i;
-            step_ji<CAUSAL>(u, nj, j, i);
+            step_ji<CAUSAL>(u, nj, j, i, nq);
             const int s = u % B7_NST;
             const int acc0 = i != first_i(j);  // dK / dV accumulate after the block's first step
             const uint32_t aQ = stage0 + s * B7_STAGE, adO = aQ + F_TILE_BYTES;
@@ -1324,7 +1331,7 @@ __global__ void __launch_bounds__(B7_WARPS * 32, 1)
                 }
                 if (hh == 1) {
                     mma_commit_w(&st_empty[s]);  // Q, dO, lse, delta, keep bits of this step are no longer read
-                    if (i == nj - 1) mma_commit_w(acc_full);
+                    if (i == nq - 1) mma_commit_w(acc_full);
                 }
                 if (u + 1 < nsteps) issue_sdp(u + 1, hh);
             }
@@ -1338,7 +1345,7 @@ __global__ void __launch_bounds__(B7_WARPS * 32, 1)
         const uint32_t ds0 = smem_u32(sDS), k0 = smem_u32(sK);
         for (int u = 0; u < nsteps; ++u) {
             int j, i;
-            step_ji<CAUSAL>(u, nj, j, i);
+            step_ji<CAUSAL>(u, nj, j, i, nq);
             mbar_wait(&ds_full[u & 1], (u >> 1) & 1);  // dS^T(u) written (both halves)
             if (u > 0) mbar_wait(dq_free, (u - 1) & 1);  // dQ of the previous step has left TMEM
             if (TS7 && lane == 0) ba.ts[2 * 64 + u] = gtime();
@@ -1352,7 +1359,7 @@ __global__ void __launch_bounds__(B7_WARPS * 32, 1)
             }
             mma_commit_w(dq_full);
             mma_commit_w(&ds_free[u & 1]);
-            if (i == nj - 1) mma_commit_w(&k_empty[j & 1]);  // K_j no longer read
+            if (i == nq - 1) mma_commit_w(&k_empty[j & 1]);  // K_j no longer read
         }
     } else if (warp < 16) {
         // ------------------------------------------------------------------
@@ -1403,12 +1410,12 @@ __global__ void __launch_bounds__(B7_WARPS * 32, 1)
             float f[32];
 #pragma unroll
             for (int e = 0; e < 32; ++e) f[e] = __uint_as_float(r[e]);
-            const long long row = row_base + (long long)j * FT + k;
+            const long long row = kv_base + (long long)j * FT + k;
             if (ba.dbg & 32) return;
             const bool acc = cg >= 2 ? (ba.acc & 2) : (ba.acc & 4);
             if (!acc)  // coalesced: staged tile + TMA store
                 warp_tile_tma(sOut + warp * B7_OUT, cg >= 2 ? &tdK : &tdV, h * FD + (cg & 1) * 32,
-                              row_base + j * FT + q4 * 32, f, cg >= 2 ? ba.scale : 1.f, lane);
+                              kv_base + j * FT + q4 * 32, f, cg >= 2 ? ba.scale : 1.f, lane);
             else if (cg >= 2)
                 store_row_bf16(ba.dk + row * ba.ld_dk + (long long)h * FD + (cg & 1) * 32, f, 4, ba.scale, true);
             else
@@ -1417,7 +1424,7 @@ __global__ void __launch_bounds__(B7_WARPS * 32, 1)
         kv_to_tmem(0);
         for (int u = 0; u < nsteps; ++u) {
             int j, i;
-            step_ji<CAUSAL>(u, nj, j, i);
+            step_ji<CAUSAL>(u, nj, j, i, nq);
             const int s = u % B7_NST;
             const float* lse_s = (const float*)(sStage + s * B7_STAGE + 2 * F_TILE_BYTES);
             const float* dl_s = lse_s + FT;
@@ -1430,7 +1437,7 @@ __global__ void __launch_bounds__(B7_WARPS * 32, 1)
                 if (TS7 && warp == 0 && lane == 0) ba.ts[(3 + 2 * hh) * 64 + u] = gtime();
                 if (TS7 && lane == 0 && u == 5) ba.ts[(12 + hh) * 64 + warp] = gtime();
                 fence_after();
-                if (hh == 1 && i == nj - 1 && j + 1 < nj) kv_to_tmem(j + 1);  // block j's S/dP all complete
+                if (hh == 1 && i == nq - 1 && j + 1 < nj) kv_to_tmem(j + 1);  // block j's S/dP all complete
                 uint32_t sv[16], dp[16];
                 if (!(ba.dbg & 8)) {
                     tmem_ld16_nowait(t_lane + q0, sv);
@@ -1513,9 +1520,9 @@ __global__ void __launch_bounds__(B7_WARPS * 32, 1)
         const uint32_t t_row = tmem + ((uint32_t)(q4 * 32) << 16) + 384;
         for (int u = 0; u < nsteps; ++u) {
             int j, i;
-            step_ji<CAUSAL>(u, nj, j, i);
-            // thread-major: float4 v of query row r of block i at ((bh*nj + i)*16 + v)*128 + r
-            float4* acc = (float4*)ba.dqacc + ((bh * nj + i) * 16) * FT + r;
+            step_ji<CAUSAL>(u, nj, j, i, nq);
+            // thread-major: float4 v of query row r of block i at ((bh*nq + i)*16 + v)*128 + r
+            float4* acc = (float4*)ba.dqacc + ((bh * nq + i) * 16) * FT + r;
             const bool last = j == (CAUSAL ? i : nj - 1), dbg = ba.dbg & 2;  // query block i's last key block
             float f[32];
             if (last && j > 0 && !dbg) {  // the final partial sum's first half, before dQ(u) lands
@@ -1670,7 +1677,7 @@ __global__ void __launch_bounds__(B8_WARPS * 32, 1)
     uint32_t* tslot = (uint32_t*)(ds_full + 2);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    const int S = ba.S, nj = S / FT, nq = S / B8_QT;
+    const int S = ba.S, Sk = ba.Sk ? ba.Sk : S, nj = Sk / FT, nq = S / B8_QT;  // (cross-attention: Sk != S)
     int nsteps = nj * nq;
     if (CAUSAL) {
         nsteps = 0;
@@ -1679,7 +1686,7 @@ __global__ void __launch_bounds__(B8_WARPS * 32, 1)
     auto first_i = [&](int j) { return CAUSAL ? 2 * j : 0; };
     const int h = blockIdx.x, b = blockIdx.y;
     const long long bh = (long long)b * ba.nh + h;
-    const int row_base = b * S;
+    const int row_base = b * S, kv_base = b * Sk;  // (query rows / key rows)
 
     if (threadIdx.x == 0) {
         for (int x = 0; x < 2; ++x) {
@@ -1716,13 +1723,13 @@ __global__ void __launch_bounds__(B8_WARPS * 32, 1)
                 if (j >= 2) mbar_wait(&k_empty[kb], ((j >> 1) - 1) & 1);
                 mbar_expect_tx(&k_full[kb], B8_KV);
                 for (int p = 0; p < 2; ++p)
-                    tma_load_2d(sK + kb * B8_KV + p * (B8_KV / 2), &tK, &k_full[kb], h * B8_D + 64 * p, row_base + j * FT);
+                    tma_load_2d(sK + kb * B8_KV + p * (B8_KV / 2), &tK, &k_full[kb], h * B8_D + 64 * p, kv_base + j * FT);
             };
             auto load_v = [&](int j) {
                 if (j >= 1) mbar_wait(v_empty, (j - 1) & 1);
                 mbar_expect_tx(v_full, B8_KV);
                 for (int p = 0; p < 2; ++p)
-                    tma_load_2d(sV + p * (B8_KV / 2), &tV, v_full, h * B8_D + 64 * p, row_base + j * FT);
+                    tma_load_2d(sV + p * (B8_KV / 2), &tV, v_full, h * B8_D + 64 * p, kv_base + j * FT);
             };
             load_k(0);
             load_v(0);
@@ -1740,7 +1747,7 @@ __global__ void __launch_bounds__(B8_WARPS * 32, 1)
                 bulk_load(st + 4 * B8_QP, ba.lse2 + bh * S + i * B8_QT, B8_QT * 4, &st_full[s]);
                 bulk_load(st + 4 * B8_QP + B8_QT * 4, ba.delta + bh * S + i * B8_QT, B8_QT * 4, &st_full[s]);
                 if (ba.mask_t)
-                    tma_load_2d(st + 4 * B8_QP + 2 * B8_QT * 4, &tM, &st_full[s], (i >> 1) * 4, (int)(bh * S) + j * FT);
+                    tma_load_2d(st + 4 * B8_QP + 2 * B8_QT * 4, &tM, &st_full[s], (i >> 1) * 4, (int)(bh * Sk) + j * FT);
                 // K_{j+1} into the other buffer once block j is under way (its previous user,
                 // block j-1, releases it with its last dQ); V_{j+1} after block j's last stage
                 if (j + 1 < nj && i == first_i(j) + (nq - first_i(j) > 1 ? 1 : 0)) load_k(j + 1);
@@ -1841,7 +1848,7 @@ __global__ void __launch_bounds__(B8_WARPS * 32, 1)
         auto drain_kv = [&](int j) {
             mbar_wait(acc_full, j & 1);
             fence_after();
-            const long long row = row_base + (long long)j * FT + k;
+            const long long row = kv_base + (long long)j * FT + k;
             const bool acc = cg == 1 ? (ba.acc & 2) : (ba.acc & 4);
             bf16* dst = cg == 1 ? ba.dk + row * ba.ld_dk + (long long)h * B8_D : ba.dv + row * ba.ld_dv + (long long)h * B8_D;
             const float sc = cg == 1 ? ba.scale : 1.f;
@@ -2019,14 +2026,16 @@ bool attn_fwd_sm100_try(const Attn& a, cudaStream_t s) {
     if (a.hd == 128) {  // head dim 128 (GPT-Neo, C4): the 64-key-chunk kernel, two CTAs per SM
         if (!fwd_fits(a, 128)) return false;
         CUtensorMap tq, tk6, tv6, tm6;
-        const long long rows = a.B * a.S, cols = a.nh * 128;
-        if (!make_map_bf16(&tq, a.q, cols, rows, a.ld_q, FT) || !make_map_bf16(&tk6, a.k, cols, rows, a.ld_k, KC6) ||
-            !make_map_bf16(&tv6, a.v, cols, rows, a.ld_v, KC6))
+        const long long rows = a.B * a.S, krows = a.B * a.keys(), cols = a.nh * 128;
+        if (!make_map_bf16(&tq, a.q, cols, rows, a.ld_q, FT) || !make_map_bf16(&tk6, a.k, cols, krows, a.ld_k, KC6) ||
+            !make_map_bf16(&tv6, a.v, cols, krows, a.ld_v, KC6))
             return false;
         memset(&tm6, 0, sizeof(tm6));
-        if (a.thr && !make_map_u32(&tm6, a.mask, a.S / 32, a.B * a.nh * a.S, a.S / 32, 2 * KC6 / 32, FT)) return false;
+        if (a.thr && !make_map_u32(&tm6, a.mask, a.keys() / 32, a.B * a.nh * a.S, a.keys() / 32, 2 * KC6 / 32, FT))
+            return false;
         FwdArgs fa{(bf16*)a.o, a.ld_o, a.lse, a.thr ? a.mask : nullptr, a.thr ? a.dscale : 1.f,
                    a.scale * 1.4426950408889634f, (int)a.S, (int)a.nh, 0};
+        fa.Sk = (int)a.keys();
         if (const char* e = getenv("SB_ATTN_DBG")) fa.dbg = atoi(e);
         static bool attr = false;
         if (!attr) {
@@ -2044,6 +2053,7 @@ bool attn_fwd_sm100_try(const Attn& a, cudaStream_t s) {
         return true;
     }
     if ((a.causal && nt_env != 6) || !fwd_fits(a)) return false;  // causal: the 64-key-chunk kernel only
+    if (a.keys() != a.S && nt_env != 6) return false;               // cross-attention likewise
     CUtensorMap tq, tk, tv, tm;
     const long long rows = a.B * a.S, cols = a.nh * FD;
     if (!make_map_bf16(&tq, a.q, cols, rows, a.ld_q, FT) || !make_map_bf16(&tk, a.k, cols, rows, a.ld_k, FT) ||
@@ -2066,10 +2076,13 @@ bool attn_fwd_sm100_try(const Attn& a, cudaStream_t s) {
     };
     if (nt_env == 6) {
         CUtensorMap tk6, tv6, tm6;
-        if (!make_map_bf16(&tk6, a.k, cols, rows, a.ld_k, KC6) || !make_map_bf16(&tv6, a.v, cols, rows, a.ld_v, KC6))
+        const long long krows = a.B * a.keys();
+        if (!make_map_bf16(&tk6, a.k, cols, krows, a.ld_k, KC6) || !make_map_bf16(&tv6, a.v, cols, krows, a.ld_v, KC6))
             return false;
         memset(&tm6, 0, sizeof(tm6));
-        if (a.thr && !make_map_u32(&tm6, a.mask, a.S / 32, a.B * a.nh * a.S, a.S / 32, 2 * KC6 / 32, FT)) return false;
+        if (a.thr && !make_map_u32(&tm6, a.mask, a.keys() / 32, a.B * a.nh * a.S, a.keys() / 32, 2 * KC6 / 32, FT))
+            return false;
+        fa.Sk = (int)a.keys();
         static bool attr6 = false;
         if (!attr6) {
             cudaFuncSetAttribute(k_fa6_fwd<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, F6_SMEM);
@@ -2109,12 +2122,13 @@ static bool attn_bwd_hd128(const Attn& a, const void* dout, i64 ld_do, void* dq,
         ld_dv % 8)
         return false;
     CUtensorMap tq, tk, tv, tdo, tm;
-    const long long rows = a.B * a.S, cols = a.nh * 128;
-    if (!make_map_bf16(&tq, a.q, cols, rows, a.ld_q, B8_QT) || !make_map_bf16(&tk, a.k, cols, rows, a.ld_k, FT) ||
-        !make_map_bf16(&tv, a.v, cols, rows, a.ld_v, FT) || !make_map_bf16(&tdo, dout, cols, rows, ld_do, B8_QT))
+    const long long rows = a.B * a.S, krows = a.B * a.keys(), cols = a.nh * 128;
+    if (!make_map_bf16(&tq, a.q, cols, rows, a.ld_q, B8_QT) || !make_map_bf16(&tk, a.k, cols, krows, a.ld_k, FT) ||
+        !make_map_bf16(&tv, a.v, cols, krows, a.ld_v, FT) || !make_map_bf16(&tdo, dout, cols, rows, ld_do, B8_QT))
         return false;
     memset(&tm, 0, sizeof(tm));
-    if (a.thr && !make_map_u32(&tm, a.mask_t, a.S / 32, a.B * a.nh * a.S, a.S / 32, 4, FT)) return false;
+    // transposed keep bits: a row per key, words over the queries
+    if (a.thr && !make_map_u32(&tm, a.mask_t, a.S / 32, a.B * a.nh * a.keys(), a.S / 32, 4, FT)) return false;
     BwdWs w;
     carve(a, ws, &w);
     const long long BH = a.B * a.nh, n = BH * a.S;
@@ -2124,6 +2138,7 @@ static bool attn_bwd_hd128(const Attn& a, const void* dout, i64 ld_do, void* dq,
     BwdArgs ba{w.lse2, w.delta, w.dqacc, a.thr ? a.mask_t : nullptr, a.thr ? a.dscale : 1.f,
                a.scale * 1.4426950408889634f, a.scale, (bf16*)dq, (bf16*)dk, (bf16*)dv, ld_dq, ld_dk, ld_dv,
                (int)a.S, (int)a.nh, a.acc_mask, 0};
+    ba.Sk = (int)a.keys();
     if (const char* e = getenv("SB_ATTN_DBG")) ba.dbg = atoi(e);
     ba.ts = nullptr;
     static bool attr = false;
@@ -2143,14 +2158,16 @@ bool attn_bwd_sm100_try(const Attn& a, const void* dout, i64 ld_do, void* dq, vo
                         i64 ld_dv, void* ws, cudaStream_t s) {
     if (a.hd == 128) return attn_bwd_hd128(a, dout, ld_do, dq, dk, dv, ld_dq, ld_dk, ld_dv, ws, s);
     if (!bwd_fits(a, dout, ld_do, ld_dq, ld_dk, ld_dv)) return false;
-    if (a.causal && getenv("SB_ATTN_BWD") && atoi(getenv("SB_ATTN_BWD")) == 5) return false;  // fa5: no causal
+    // fa5 (A/B only): neither causal nor cross-attention
+    if ((a.causal || a.keys() != a.S) && getenv("SB_ATTN_BWD") && atoi(getenv("SB_ATTN_BWD")) == 5) return false;
     CUtensorMap tq, tk, tv, tdo, tm;
-    const long long rows = a.B * a.S, cols = a.nh * FD;
-    if (!make_map_bf16(&tq, a.q, cols, rows, a.ld_q, FT) || !make_map_bf16(&tk, a.k, cols, rows, a.ld_k, FT) ||
-        !make_map_bf16(&tv, a.v, cols, rows, a.ld_v, FT) || !make_map_bf16(&tdo, dout, cols, rows, ld_do, FT))
+    const long long rows = a.B * a.S, krows = a.B * a.keys(), cols = a.nh * FD;
+    if (!make_map_bf16(&tq, a.q, cols, rows, a.ld_q, FT) || !make_map_bf16(&tk, a.k, cols, krows, a.ld_k, FT) ||
+        !make_map_bf16(&tv, a.v, cols, krows, a.ld_v, FT) || !make_map_bf16(&tdo, dout, cols, rows, ld_do, FT))
         return false;
     memset(&tm, 0, sizeof(tm));
-    if (a.thr && !make_map_u32(&tm, a.mask_t, a.S / 32, a.B * a.nh * a.S, a.S / 32, FT / 32, FT)) return false;
+    // transposed keep bits: a row per key, words over the queries
+    if (a.thr && !make_map_u32(&tm, a.mask_t, a.S / 32, a.B * a.nh * a.keys(), a.S / 32, FT / 32, FT)) return false;
     BwdWs w;
     carve(a, ws, &w);
     const long long BH = a.B * a.nh;
@@ -2164,6 +2181,7 @@ bool attn_bwd_sm100_try(const Attn& a, const void* dout, i64 ld_do, void* dq, vo
     BwdArgs ba{w.lse2, w.delta, w.dqacc, a.thr ? a.mask_t : nullptr, a.thr ? a.dscale : 1.f,
                a.scale * 1.4426950408889634f, a.scale, (bf16*)dq, (bf16*)dk, (bf16*)dv, ld_dq, ld_dk, ld_dv,
                (int)a.S, (int)a.nh, a.acc_mask, 0};
+    ba.Sk = (int)a.keys();
     if (const char* e = getenv("SB_ATTN_DBG")) ba.dbg = atoi(e);
     ba.ts = nullptr;
     static unsigned long long* ts_buf = nullptr;
@@ -2183,8 +2201,8 @@ bool attn_bwd_sm100_try(const Attn& a, const void* dout, i64 ld_do, void* dq, vo
     if (ver == 5) k_fa5_bwd<<<grid, 512, B_SMEM, s>>>(tk, tv, tq, tdo, tm, ba);
     else {
         CUtensorMap tdq, tdk, tdv;
-        if (!make_map_bf16_plain(&tdq, dq, cols, rows, ld_dq, 32, 32) || !make_map_bf16_plain(&tdk, dk, cols, rows, ld_dk, 32, 32) ||
-            !make_map_bf16_plain(&tdv, dv, cols, rows, ld_dv, 32, 32))
+        if (!make_map_bf16_plain(&tdq, dq, cols, rows, ld_dq, 32, 32) || !make_map_bf16_plain(&tdk, dk, cols, krows, ld_dk, 32, 32) ||
+            !make_map_bf16_plain(&tdv, dv, cols, krows, ld_dv, 32, 32))
             throw std::runtime_error("attention backward: output tensor maps rejected");
         if (a.causal) k_fa7_bwd<true><<<grid, B7_WARPS * 32, B7_SMEM, s>>>(tk, tv, tq, tdo, tm, tdq, tdk, tdv, ba);
         else k_fa7_bwd<false><<<grid, B7_WARPS * 32, B7_SMEM, s>>>(tk, tv, tq, tdo, tm, tdq, tdk, tdv, ba);

@@ -410,6 +410,7 @@ __global__ void __launch_bounds__(128) k_fa_dq(Attn a, MaskRef mk, const bf16* d
 }
 
 bool fits(const Attn& a) {
+    if (a.keys() != a.S) return false;  // (cross-attention: the SIMT and tcgen05 engines)
     if (a.t != BF16 || (a.hd != 64 && a.hd != 128) || a.S % TB || a.S < TB) return false;
     auto al = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
     if (!al(a.q) || !al(a.k) || !al(a.v) || !al(a.o)) return false;

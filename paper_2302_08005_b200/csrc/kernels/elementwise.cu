@@ -361,18 +361,18 @@ __global__ void k_dropout_mask(uint32_t* bits, i64 n, uint64_t s1, uint64_t thr,
 // thread) and transposed (bit i of key row j, read by the backward, one key per
 // thread). A warp owns a 32x32 (query, key) block: lane = query row computes
 // its 32 keep bits, and 32 ballots transpose the block.
-__global__ void k_dropout_mask_dual(uint32_t* bits, uint32_t* bits_t, int S, long long BH, uint64_t s1, uint64_t thr,
-                                    uint32_t one) {
+__global__ void k_dropout_mask_dual(uint32_t* bits, uint32_t* bits_t, int S, int Sk, long long BH, uint64_t s1,
+                                    uint64_t thr, uint32_t one) {
     // grid-stride over 32x32 (query, key) blocks, one per warp: a small persistent grid
     // (g_mask_blocks blocks of 4 warps) co-resides with the GEMM / attention CTAs and
     // uses their idle issue slots without crowding out their producer / MMA warps
     const int lane = threadIdx.x & 31;
-    const int nb = S / 32;
-    const long long nblk = BH * nb * nb;
+    const int nb = S / 32, nbk = Sk / 32;  // query / key blocks of 32 (Sk != S: cross-attention)
+    const long long nblk = BH * nb * nbk;
     for (long long w = (long long)blockIdx.x * 4 + (threadIdx.x >> 5); w < nblk; w += (long long)gridDim.x * 4) {
-        const int kb = (int)(w % nb), qb = (int)((w / nb) % nb);
-        const long long bh = w / ((long long)nb * nb);
-        const long long e0 = (bh * S + qb * 32 + lane) * S + kb * 32;  // flat index of (query qb*32+lane, key kb*32)
+        const int kb = (int)(w % nbk), qb = (int)((w / nbk) % nb);
+        const long long bh = w / ((long long)nb * nbk);
+        const long long e0 = (bh * S + qb * 32 + lane) * Sk + kb * 32;  // flat index of (query qb*32+lane, key kb*32)
         const uint32_t m = d_keep_word_fast(s1, (uint64_t)e0 + d_keep_key(s1), thr << 11, one);
         bits[e0 >> 5] = m;
         // 32x32 bit-matrix transpose across the warp (lane = row -> lane = column):
@@ -385,7 +385,7 @@ __global__ void k_dropout_mask_dual(uint32_t* bits, uint32_t* bits_t, int S, lon
             const uint32_t y = __shfl_xor_sync(0xffffffffu, t, j);
             t = (lane & j) ? (t & ~msk) | ((y >> j) & msk) : (t & msk) | ((y & msk) << j);
         }
-        bits_t[((bh * S + kb * 32 + lane) * S + qb * 32) >> 5] = t;
+        bits_t[((bh * Sk + kb * 32 + lane) * S + qb * 32) >> 5] = t;
     }
 }
 int g_mask_blocks = 0;  // grid of the keep-bit kernels: 0 full grid (measured best), -1 one block per SM, n > 0 n blocks
@@ -397,10 +397,11 @@ static unsigned mask_grid(long long work_blocks) {
     if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     return (unsigned)sms;
 }
-void dropout_mask_dual(uint32_t* bits, i64 BH, i64 S, u64 s1, u64 thr, cudaStream_t s) {
-    if (S % 32) throw std::runtime_error("dropout_mask_dual: S % 32 != 0");
-    const i64 words = BH * S * S / 32;
-    const i64 nblk = BH * (S / 32) * (S / 32);
+void dropout_mask_dual(uint32_t* bits, i64 BH, i64 S, u64 s1, u64 thr, cudaStream_t s, i64 Sk) {
+    if (!Sk) Sk = S;
+    if (S % 32 || Sk % 32) throw std::runtime_error("dropout_mask_dual: S % 32 != 0");
+    const i64 words = BH * S * Sk / 32;
+    const i64 nblk = BH * (S / 32) * (Sk / 32);
     const unsigned grid = mask_grid((nblk + 3) / 4);
     static bool attr = false;
     if (!attr) {
@@ -409,7 +410,7 @@ void dropout_mask_dual(uint32_t* bits, i64 BH, i64 S, u64 s1, u64 thr, cudaStrea
         cudaFuncSetAttribute(k_dropout_mask_dual, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         attr = true;
     }
-    k_dropout_mask_dual<<<grid, 128, 0, s>>>(bits, bits + words, (int)S, BH, s1, thr, 1u);
+    k_dropout_mask_dual<<<grid, 128, 0, s>>>(bits, bits + words, (int)S, (int)Sk, BH, s1, thr, 1u);
     SBK_CHECK_LAUNCH();
 }
 void dropout_mask(uint32_t* bits, i64 n, u64 s1, u64 thr, cudaStream_t s) {

@@ -93,7 +93,8 @@ void dropout_mask(uint32_t* bits, i64 n, u64 s1, u64 thr, cudaStream_t s);
 // attention keep bits, both layouts: bits[0, W) natural (element ((bh*S+i)*S+j)
 // at bit e%32 of word e/32), bits[W, 2W) transposed (element ((bh*S+j)*S+i)),
 // W = BH*S*S/32; S % 128 == 0
-void dropout_mask_dual(uint32_t* bits, i64 BH, i64 S, u64 s1, u64 thr, cudaStream_t s);
+// natural (B*nh, S, Sk) + transposed (B*nh, Sk, S) keep bits; Sk = 0: S
+void dropout_mask_dual(uint32_t* bits, i64 BH, i64 S, u64 s1, u64 thr, cudaStream_t s, i64 Sk = 0);
 void set_mask_blocks(int n);  // experiments: persistent grid size of the keep-bit kernel (0 = full grid)
 
 // --------------------------------------------------------- strided copy
@@ -168,7 +169,12 @@ struct Attn {
     void* o;
     i64 ld_q, ld_k, ld_v, ld_o;
     float* lse;
-    i64 B, S, nh, hd;
+    i64 B, S, nh, hd;  // S: queries per sequence
+    i64 Sk = 0;        // keys per sequence (cross-attention); 0: S
+#ifdef __CUDACC__
+    __host__ __device__
+#endif
+    i64 keys() const { return Sk ? Sk : S; }
     float scale;
     u64 s1 = 0, thr = 0;
     float dscale = 1.f;

@@ -122,10 +122,38 @@ def test_t5_unscheduled_fp32(tmp_path, mode):
 
 @pytest.mark.parametrize("world", [1, 2])
 def test_t5_recipe_fp32(tmp_path, world):
+    """the cross-attention cores stay composed in the schedule (R4) and are lowered to the
+    flash kernels by their graph (S_dec != S_enc); the activation ledger still follows the
+    reference's accounting of the composed graph"""
     script = recipes.t5_script(2, 2, world, checkpoint=["encoder.block.0", "decoder.block.1"])
     ex, outs, grads, r = run_t5(str(tmp_path), T5, script, world)
     check(outs, grads, r, world, 1e-4, 1e-4)
     assert ex.collective_invocations() == r.meta["collectives_total"]
+    assert ex.ledger() == r.meta["ledger_bytes"]
+    assert ex.describe()["kinds"].get("FlashAttn", 0) == 2 + 2 + 2  # encoder self, decoder self and cross cores
+
+
+def test_t5_cross_core_composed_switch(tmp_path):
+    """SB_ATTN_CORE_FLASH=0 keeps the composed cross-attention graph; both agree"""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import sys, numpy as np; sys.path.insert(0, %r)\n"
+            "import paper_2302_08005_b200 as sb\n"
+            "m = sb.t5(2, 2, 32, 4, 32, 2, 24, 16, 0.1); ex = sb.Executor(m, 'train', 5, 1)\n"
+            "o = ex.forward(m.random_inputs(3))[0]; g = ex.backward().params\n"
+            "np.save(sys.argv[1], np.concatenate([o.ravel()] + [g[k].ravel() for k in sorted(g)]))\n"
+            "print(ex.ledger())\n") % root
+    res = []
+    for v in ("1", "0"):
+        f = str(tmp_path / f"r{v}.npy")
+        r = subprocess.run([sys.executable, "-c", code, f], capture_output=True, text=True, timeout=300,
+                           env=dict(os.environ, SB_ATTN_CORE_FLASH=v))
+        assert r.returncode == 0, r.stderr
+        res.append((np.load(f), r.stdout.strip()))
+    (a, la), (b, lb) = res
+    assert la == lb  # same ledger
+    assert np.abs(a - b).max() <= 1e-5 * np.abs(b).max()
 
 
 def test_t5_recipe_bf16(tmp_path):
