@@ -39,6 +39,10 @@ int sb_model_tp_two_linear(int64_t hidden, int64_t inner, int64_t batch, sb_mode
    two id inputs (B, enc_seq) and (B, dec_seq) (csrc/host/model_io.cpp t5) */
 int sb_model_t5(int enc_layers, int dec_layers, int64_t hidden, int64_t heads, int64_t vocab, int64_t batch,
                 int64_t enc_seq, int64_t dec_seq, double dropout_p, sb_model** out);
+/* tie_embeddings = 0: separate encoder / decoder tables (enc_embed, dec_embed) — a tied table
+   cannot be cut by pipeline_split (used by two segments) */
+int sb_model_t5_ex(int enc_layers, int dec_layers, int64_t hidden, int64_t heads, int64_t vocab, int64_t batch,
+                   int64_t enc_seq, int64_t dec_seq, double dropout_p, int tie_embeddings, sb_model** out);
 /* f2 (no reference fixture): GPT-Neo-style pre-LN causal decoder in the reference's module
    vocabulary (csrc/host/model_io.cpp gpt_neo); its oracle is the documented extension
    oracle/causal_ext.py (a `causal` attr on softmax, proj/src/executor.cpp:907-916) */

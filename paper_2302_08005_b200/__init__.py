@@ -75,6 +75,8 @@ for _n, _a in {
     "sb_pipeline_executor_time_steps": (_P, _c.c_int, _c.POINTER(_c.c_float)),
     "sb_pipeline_executor_free": (_P,),
     "sb_model_t5": (_c.c_int, _c.c_int, _i64, _i64, _i64, _i64, _i64, _i64, _c.c_double, _c.POINTER(_P)),
+    "sb_model_t5_ex": (_c.c_int, _c.c_int, _i64, _i64, _i64, _i64, _i64, _i64, _c.c_double, _c.c_int,
+                       _c.POINTER(_P)),
     "sb_model_tp_two_linear": (_i64, _i64, _i64, _c.POINTER(_P)),
     "sb_model_fig3c": (_c.POINTER(_P),),
     "sb_model_ffn_stack": (_c.c_int, _i64, _i64, _c.POINTER(_P)),
@@ -263,11 +265,12 @@ def gpt_neo(layers=24, hidden=8, heads=2, vocab=28, batch=4, seq=4, dropout_p=0.
 
 
 def t5(enc_layers=2, dec_layers=2, hidden=8, heads=2, vocab=28, batch=4, enc_seq=4, dec_seq=4,
-       dropout_p=0.1) -> Model:
+       dropout_p=0.1, tie_embeddings=True) -> Model:
     """T5-style encoder-decoder with cross-attention (f2, BASELINE.json configs[4]); two id
-    inputs (encoder, decoder); oracle: the causal extension (oracle/causal_ext.py)."""
-    return Model._make(_lib.sb_model_t5, enc_layers, dec_layers, hidden, heads, vocab, batch, enc_seq, dec_seq,
-                       dropout_p)
+    inputs (encoder, decoder); oracle: the causal extension (oracle/causal_ext.py).
+    tie_embeddings=False: separate encoder / decoder tables (needed to pipeline_split it)."""
+    return Model._make(_lib.sb_model_t5_ex, enc_layers, dec_layers, hidden, heads, vocab, batch, enc_seq, dec_seq,
+                       dropout_p, int(tie_embeddings))
 
 
 def tp_two_linear(hidden=8, inner=16, batch=4) -> Model:

@@ -129,10 +129,11 @@ int sb_model_gpt_neo(int layers, int64_t hidden, int64_t heads, int64_t vocab, i
         *out = new sb_model{gpt_neo(c)};
     });
 }
-int sb_model_t5(int enc_layers, int dec_layers, int64_t hidden, int64_t heads, int64_t vocab, int64_t batch,
-                int64_t enc_seq, int64_t dec_seq, double p, sb_model** out) {
+int sb_model_t5_ex(int enc_layers, int dec_layers, int64_t hidden, int64_t heads, int64_t vocab, int64_t batch,
+                   int64_t enc_seq, int64_t dec_seq, double p, int tie_embeddings, sb_model** out) {
     return guard([&] {
         T5Config c;
+        c.tie_embeddings = tie_embeddings != 0;
         c.enc_layers = enc_layers;
         c.dec_layers = dec_layers;
         c.hidden = hidden;
@@ -144,6 +145,10 @@ int sb_model_t5(int enc_layers, int dec_layers, int64_t hidden, int64_t heads, i
         c.dropout_p = p;
         *out = new sb_model{t5(c)};
     });
+}
+int sb_model_t5(int enc_layers, int dec_layers, int64_t hidden, int64_t heads, int64_t vocab, int64_t batch,
+                int64_t enc_seq, int64_t dec_seq, double p, sb_model** out) {
+    return sb_model_t5_ex(enc_layers, dec_layers, hidden, heads, vocab, batch, enc_seq, dec_seq, p, 1, out);
 }
 int sb_model_tp_two_linear(int64_t hidden, int64_t inner, int64_t batch, sb_model** out) {
     return guard([&] { *out = new sb_model{tp_two_linear(hidden, inner, batch)}; });

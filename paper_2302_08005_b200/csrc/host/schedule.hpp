@@ -140,6 +140,7 @@ struct T5Config {
     int enc_layers = 2, dec_layers = 2;
     i64 hidden = 8, heads = 2, vocab = 28, batch = 4, enc_seq = 4, dec_seq = 4;
     double dropout_p = 0.1;
+    bool tie_embeddings = true;  // one table for both id inputs (T5); false: enc_embed / dec_embed
 };
 Module t5(const T5Config& c);
 Module tp_two_linear(i64 hidden, i64 inner, i64 batch);

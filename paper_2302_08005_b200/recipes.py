@@ -138,7 +138,7 @@ def neo_script(layers: int, world: int = 1, flash: bool = True, fuse: bool = Tru
 
 
 def t5_script(enc_layers: int, dec_layers: int, world: int = 1, flash: bool = True, fused_qkv: bool = True,
-              checkpoint=(), shard_embeddings: bool = True) -> str:
+              checkpoint=(), shard_embeddings: bool = True, tied: bool = True) -> str:
     """The encoder-decoder recipe (f2, BASELINE.json configs[4]) for ``t5``: self-attention
     as FusedQKV (sharded blockwise on axis 0 + sync backward), cross-attention query / key /
     value Linears sharded on axis 0 with sync backward (the key / value SyncGrads sum the
@@ -180,6 +180,7 @@ def t5_script(enc_layers: int, dec_layers: int, world: int = 1, flash: bool = Tr
         # EfficientAttention violates rule R4 — its q and k/v specs differ, S_dec vs S_enc)
         mlp(f"{p}.mlp")
     if world > 1 and shard_embeddings:
-        s += "shard shared weight axis=0\nsync shared type=both\n"
+        for e in (("shared",) if tied else ("enc_embed", "dec_embed")):
+            s += f"shard {e} weight axis=0\nsync {e} type=both\n"
     s += "".join(f"checkpoint {c}\n" for c in checkpoint)
     return s
