@@ -435,6 +435,7 @@ public:
     }
     std::vector<int> grad_reads(const Op& op) const {
         if (op.k == K::FusedLinearGelu && op.dgelu_fused) return {op.out[1]};
+        if (op.k == K::FusedLinearResLN && op.sum_ext) return {op.out[0], op.out[2]};
         if (op.k == K::SyncGrad && op.ids_input) return {};
         return {op.out[0]};
     }
@@ -1327,7 +1328,8 @@ public:
                         op.has_bias && op.bias_grad ? (float*)gp(r, op.in[5]) : nullptr, (float*)gp(r, op.in[3]),
                         (float*)gp(r, op.in[4]), cdt, rows, n, op.s1, op.dropout ? op.thr : 0,
                         (float)(1.0 / (1.0 - op.p)), (float*)r.ws, stream, gres.temp || !OW(op.in[2]), !OW(op.in[3]),
-                        op.dropout ? (const uint32_t*)fp(r, op.out[5]) : nullptr);
+                        op.dropout ? (const uint32_t*)fp(r, op.out[5]) : nullptr,
+                        op.sum_ext ? gp(r, op.out[2]) : nullptr);  // (pre-LN: the residual stream's gradient)
                     flush(r, gres);
                     ++launches;
                     // the in-region all_reduce backpropagates as identity (executor.cpp:1227-1233)

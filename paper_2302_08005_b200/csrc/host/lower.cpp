@@ -900,6 +900,141 @@ struct Lowerer {
 
 }  // namespace
 
+// Residual-stream fusion (pre-LN blocks: GPT-Neo, T5). A `.fuse` region may have only one
+// escaping value (schedule.cpp:63-66), so the pre-LN chain
+//     y_L = Linear(x) -> [all_reduce] -> [Dropout] -> r = add(., res) -> LayerNorm(r)
+// whose sum r is also the next residual cannot be fused by the schedule. On the plan it
+// is one FusedLinearResLN op — the GEMM, then dropout + residual + LayerNorm in one pass
+// writing both r and LN(r) — whose backward adds r's gradient from its other readers
+// (sum_ext). Same math, same dropout draws (flat index over the (T, H) tensor); placed at
+// the LayerNorm's position, with no reader of r in between. SB_RESLN_FUSE=0 disables it.
+static void fuse_residual_stream(Plan& P, const LowerOptions& o) {
+    static const bool on = !(getenv("SB_RESLN_FUSE") && atoi(getenv("SB_RESLN_FUSE")) == 0);
+    if (!on || !o.fused_kernels) return;
+    const size_t n = P.fwd.size();
+    std::map<int, std::vector<int>> readers, producer_of;  // storage -> reading ops / producing ops
+    for (size_t i = 0; i < n; ++i) {
+        for (int v : P.fwd[i].in) readers[P.views[(size_t)v].st].push_back((int)i);
+        for (int v : P.fwd[i].out) producer_of[P.views[(size_t)v].st].push_back((int)i);
+    }
+    for (int v : P.outputs) readers[P.views[(size_t)v].st].push_back(1 << 30);
+    auto st = [&](int v) { return P.views[(size_t)v].st; };
+    auto sole_reader = [&](int v, int op) { auto& r = readers[st(v)]; return r.size() == 1 && r[0] == op; };
+    auto produced_by = [&](int v) -> int {  // the single op writing storage st(v), or -1
+        auto it = producer_of.find(st(v));
+        return it != producer_of.end() && it->second.size() == 1 ? it->second[0] : -1;
+    };
+    auto plain = [&](int v) {
+        const View& w = P.views[(size_t)v];
+        return w.off == 0 && w.contiguous() && w.g_contiguous() && w.st == w.gst;
+    };
+    std::vector<char> dead(n, 0);
+    for (size_t ia = 0; ia < n; ++ia) {
+        const Op& A = P.fwd[ia];
+        if (A.k != K::Add || dead[ia] || A.in.size() != 2) continue;
+        for (int side = 0; side < 2; ++side) {
+            const int dv = A.in[(size_t)side], rv = A.in[(size_t)(1 - side)];
+            if (P.views[(size_t)dv].shape != P.views[(size_t)rv].shape || !plain(dv) || !plain(rv)) continue;
+            // [Dropout] <- [AllReduce] <- Linear
+            int id = produced_by(dv), iar = -1, il = -1;
+            if (id < 0 || !sole_reader(dv, (int)ia)) continue;
+            int lin_out = dv;
+            if (P.fwd[(size_t)id].k == K::Dropout) {
+                lin_out = P.fwd[(size_t)id].in[0];
+            } else {
+                id = -1;
+            }
+            int prod = produced_by(lin_out);
+            if (prod >= 0 && P.fwd[(size_t)prod].k == K::AllReduce) {
+                if (!P.fwd[(size_t)prod].allreduce) continue;  // (an identity all_reduce still counts; keep it)
+                iar = prod;
+                if (!sole_reader(lin_out, id >= 0 ? id : (int)ia)) continue;
+                lin_out = P.fwd[(size_t)iar].in[0];
+                prod = produced_by(lin_out);
+            }
+            if (prod < 0 || P.fwd[(size_t)prod].k != K::Linear) continue;
+            il = prod;
+            const int next_reader = iar >= 0 ? iar : id >= 0 ? id : (int)ia;
+            if (!sole_reader(lin_out, next_reader) || !plain(lin_out) || P.fwd[(size_t)il].qkv) continue;
+            if (id >= 0 && (!sole_reader(P.fwd[(size_t)id].in[0], id) || !plain(P.fwd[(size_t)id].in[0]))) continue;
+            // the LayerNorm reading r = A.out, with no other reader of r before it
+            const int rout = A.out[0];
+            int in_ = -1;
+            for (int rd : readers[st(rout)])
+                if (rd > (int)ia && rd < (1 << 30) && P.fwd[(size_t)rd].k == K::LayerNorm && P.fwd[(size_t)rd].affine &&
+                    P.fwd[(size_t)rd].in[0] == rout && (in_ < 0 || rd < in_))
+                    in_ = rd;
+            if (in_ < 0 || !plain(rout)) continue;
+            bool early = false, ext = false;
+            for (int rd : readers[st(rout)]) {
+                if (rd == in_) continue;
+                ext = true;
+                early |= rd < in_;
+            }
+            const int reg = P.fwd[(size_t)il].region;
+            bool same_region = P.fwd[ia].region == reg && P.fwd[(size_t)in_].region == reg &&
+                               (id < 0 || P.fwd[(size_t)id].region == reg) && (iar < 0 || P.fwd[(size_t)iar].region == reg);
+            if (early || !same_region) continue;
+            const Op& L = P.fwd[(size_t)il];
+            const Op& N = P.fwd[(size_t)in_];
+            const View& y = P.views[(size_t)rout];
+            Op F;
+            F.k = K::FusedLinearResLN;
+            F.in = {L.in[0], L.in[1], rv, N.in[1], N.in[2]};
+            F.has_bias = L.has_bias;
+            if (L.has_bias) F.in.push_back(L.in[2]);
+            F.bias_on = L.bias_on;
+            F.bias_grad = L.bias_grad;
+            F.allreduce = iar >= 0 && P.fwd[(size_t)iar].allreduce;
+            F.out = {N.out[0], lin_out, rout, N.out[1], N.out[2]};
+            F.eps = N.eps;
+            if (id >= 0) {
+                const Op& D = P.fwd[(size_t)id];
+                F.dropout = true;
+                F.p = D.p;
+                F.s1 = D.s1;
+                F.thr = D.thr;
+                // persistent keep bits (bit row * n + col), like the scheduled fusion's
+                const i64 words = (y.numel() + 31) / 32;
+                Storage kb;
+                kb.numel = words;
+                kb.dt = kb.gdt = sbk::F32;
+                kb.kind = SKind::Aux;
+                kb.region = -1;
+                kb.name = "keep";
+                P.st.push_back(kb);
+                View kv;
+                kv.st = kv.gst = (int)P.st.size() - 1;
+                kv.shape = {words};
+                kv.strides = kv.gstrides = {1};
+                kv.rdt = Dtype::F32;
+                P.views.push_back(kv);
+                F.out.push_back((int)P.views.size() - 1);
+            }
+            F.sum_ext = ext;
+            F.region = reg;
+            F.path = L.path;
+            P.fwd[(size_t)in_] = F;
+            dead[(size_t)il] = dead[ia] = 1;
+            if (id >= 0) dead[(size_t)id] = 1;
+            if (iar >= 0) dead[(size_t)iar] = 1;
+            break;
+        }
+    }
+    std::vector<Op> kept;
+    for (size_t i = 0; i < n; ++i)
+        if (!dead[i]) kept.push_back(std::move(P.fwd[i]));
+    P.fwd = std::move(kept);
+    for (auto& R : P.regions) R.first_op = R.last_op = -1;
+    for (size_t i = 0; i < P.fwd.size(); ++i) {
+        const int r = P.fwd[i].region;
+        if (r < 0) continue;
+        Region& R = P.regions[(size_t)r];
+        if (R.first_op < 0) R.first_op = (int)i;
+        R.last_op = (int)i;
+    }
+}
+
 Plan lower(const Module& root, const LowerOptions& o) {
     Plan P;
     P.rank = o.rank;
@@ -909,6 +1044,7 @@ Plan lower(const Module& root, const LowerOptions& o) {
     if (o.world < 1) throw Error("world_size must be >= 1");
     Lowerer L(P, root, o);
     L.run();
+    fuse_residual_stream(P, o);
     // Drop empty regions; keep region-internal storages in scratch only when
     // nothing outside the region reads them.
     std::vector<Region> keep;

@@ -97,6 +97,10 @@ struct Op {
     // gradient of view `dgelu_pre` (the producing FusedLinearGelu's pre-activation)
     int dgelu_pre = -1;
     bool dgelu_fused = false;  // FusedLinearGelu whose GeLU backward was folded into its consumer
+    // FusedLinearResLN whose pre-LN sum (out[2]) is also read by other ops (the residual
+    // stream of a pre-LN block): its backward adds that sum's gradient (lower.cpp
+    // fuse_residual_stream)
+    bool sum_ext = false;
 };
 
 struct Region {

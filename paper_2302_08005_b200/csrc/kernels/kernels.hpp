@@ -126,12 +126,13 @@ void bias_dropout_residual_ln_fwd(const void* partial, const void* bias, const v
                                   const void* beta, DT tp, void* sum, void* y, float* mean, float* rstd, DT t,
                                   i64 rows, i64 n, float eps, u64 s1, u64 thr, float dscale, cudaStream_t s,
                                   const uint32_t* keep = nullptr);
-// g_sum = LNbwd(g); g_res += g_sum; g_partial (+)= dropout_bwd(g_sum); dbias/dgamma/dbeta (+)=
+// g_sum = LNbwd(g) (+ g_sum_extra: the sum's gradient from other consumers); g_res += g_sum;
+// g_partial (+)= dropout_bwd(g_sum); dbias/dgamma/dbeta (+)=
 void bias_dropout_residual_ln_bwd(const void* sum, const float* mean, const float* rstd, const void* gamma, DT tp,
                                   const void* g, void* g_res, void* g_partial, bool g_partial_accumulate,
                                   float* dbias, float* dgamma, float* dbeta, DT t, i64 rows, i64 n, u64 s1,
                                   u64 thr, float dscale, float* workspace, cudaStream_t s, bool gres_acc = true,
-                                  bool col_acc = true, const uint32_t* keep = nullptr);
+                                  bool col_acc = true, const uint32_t* keep = nullptr, const void* g_sum_extra = nullptr);
 size_t bdrln_bwd_workspace(i64 rows, i64 n);
 
 // column sums of g (rows x cols) into fp32 db (+=)

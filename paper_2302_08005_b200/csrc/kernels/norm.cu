@@ -21,7 +21,7 @@ bool bdrln_fwd_vec(const void* partial, const void* bias, const void* res, const
                    const uint32_t* keep, cudaStream_t s);
 bool ln_bwd_vec(int mode, const void* x, const float* mean, const float* rstd, const void* gamma, const void* g, void* gx,
                 void* gres, bool gx_acc, bool gres_acc, DT t, i64 rows, i64 n, u64 s1, u64 thr, float dscale,
-                const uint32_t* keep, float* ws, int ncol, int nblocks, cudaStream_t s);
+                const uint32_t* keep, float* ws, int ncol, int nblocks, cudaStream_t s, const void* gext = nullptr);
 static int vec_blocks(i64 rows) { return (int)std::min<i64>(296, std::max<i64>(1, (rows + kWarps - 1) / kWarps)); }
 
 // ------------------------------------------------------------------ softmax
@@ -150,7 +150,7 @@ void layernorm_fwd(const void* x, const void* gamma, const void* beta, DT tp, vo
 template <class T, class P, int MODE>  // MODE 0: LayerNorm, 1: bias+dropout+residual+LN
 __global__ void k_ln_bwd(const T* x, const float* mean, const float* rstd, const P* gamma, const T* g, T* gx, T* gres,
                          bool gx_acc, i64 rows, i64 n, uint64_t s1, uint64_t thr, float dscale, float* ws, int ncol,
-                         bool gres_acc) {
+                         bool gres_acc, const T* gext) {
     extern __shared__ float sh[];  // [kWarps][ncol][n]
     int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
     float* mine = sh + (size_t)warp * ncol * n;
@@ -179,6 +179,7 @@ __global__ void k_ln_bwd(const T* x, const float* mean, const float* rstd, const
             float gh = gamma ? gv * to_f(gamma[i]) : gv;
             float d = rs * (gh - a - xh * b);
             i64 k = row * n + i;
+            if (MODE == 1 && gext) d += to_f(gext[k]);  // the sum's gradient from its other consumers
             if (MODE == 0) {
                 gx[k] = from_f<T>(gx_acc ? to_f(gx[k]) + d : d);
             } else {
@@ -259,7 +260,7 @@ void layernorm_bwd(const void* x, const float* mean, const float* rstd, const vo
         auto k = k_ln_bwd<T, T, 0>;
         set_smem(k, smem);
         k<<<nb, 32 * kWarps, smem, s>>>((const T*)x, mean, rstd, (const T*)gamma, (const T*)g, (T*)gx, nullptr, gx_acc,
-                                        rows, n, 0, 0, 1.f, ws, ncol, true);
+                                        rows, n, 0, 0, 1.f, ws, ncol, true, nullptr);
     });
     if (ncol) k_col_final<<<col_final_grid(2 * n), 1024, 0, s>>>(ws, nb, 2 * n, dgamma, dbeta, nullptr, n, col_acc);
     SBK_CHECK_LAUNCH();
@@ -311,12 +312,13 @@ void bias_dropout_residual_ln_fwd(const void* partial, const void* bias, const v
 void bias_dropout_residual_ln_bwd(const void* sum, const float* mean, const float* rstd, const void* gamma, DT tp,
                                   const void* g, void* g_res, void* g_partial, bool g_partial_acc, float* dbias,
                                   float* dgamma, float* dbeta, DT t, i64 rows, i64 n, u64 s1, u64 thr, float dscale,
-                                  float* ws, cudaStream_t s, bool gres_acc, bool col_acc, const uint32_t* keep) {
+                                  float* ws, cudaStream_t s, bool gres_acc, bool col_acc, const uint32_t* keep,
+                                  const void* gext) {
     (void)tp;
     int ncol = 3;
     int vb = vec_blocks(rows);
     if (ln_bwd_vec(1, sum, mean, rstd, gamma, g, g_partial, g_res, g_partial_acc, gres_acc, t, rows, n, s1, thr, dscale,
-                   keep, ws, ncol, vb, s)) {
+                   keep, ws, ncol, vb, s, gext)) {
         k_col_final<<<col_final_grid(3 * n), 1024, 0, s>>>(ws, vb, 3 * n, dgamma, dbeta, dbias, n, col_acc);
         SBK_CHECK_LAUNCH();
         return;
@@ -328,7 +330,7 @@ void bias_dropout_residual_ln_bwd(const void* sum, const float* mean, const floa
         auto k = k_ln_bwd<T, T, 1>;
         set_smem(k, smem);
         k<<<nb, 32 * kWarps, smem, s>>>((const T*)sum, mean, rstd, (const T*)gamma, (const T*)g, (T*)g_partial, (T*)g_res,
-                                        g_partial_acc, rows, n, s1, thr, dscale, ws, ncol, gres_acc);
+                                        g_partial_acc, rows, n, s1, thr, dscale, ws, ncol, gres_acc, (const T*)gext);
     });
     k_col_final<<<col_final_grid(3 * n), 1024, 0, s>>>(ws, nb, 3 * n, dgamma, dbeta, dbias, n, col_acc);
     SBK_CHECK_LAUNCH();

@@ -325,7 +325,7 @@ template <class T, int CPL, int MODE>
 __global__ void __launch_bounds__(32 * kW, 1)
     k_ln_bwd_v(const T* x, const float* mean, const float* rstd, const T* gamma, const T* g, T* gx, T* gres, bool gx_acc,
                i64 rows, int n, uint64_t s1, uint64_t thr, float dscale, const uint32_t* keep, float* ws, int ncol,
-               bool gres_acc) {
+               bool gres_acc, const T* gext) {
     constexpr int VN = Vec<T>::N;
     extern __shared__ float sh[];  // [kW][ncol][n]
     int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
@@ -359,6 +359,14 @@ __global__ void __launch_bounds__(32 * kW, 1)
                 float gh = gamma ? gv[c][e] * gm[c][e] : gv[c][e];
                 gv[c][e] = rs * (gh - a - xv[c][e] * b);  // d(sum) / dx
             }
+        if (MODE == 1 && gext) {  // + the sum's gradient from its other consumers (pre-LN residual stream)
+            float ex[CPL][VN];
+            load_row<T, CPL>(gext + row * n, lane, ex);
+#pragma unroll
+            for (int c = 0; c < CPL; ++c)
+#pragma unroll
+                for (int e = 0; e < VN; ++e) gv[c][e] += ex[c][e];
+        }
         if (MODE == 0) {
             float o[CPL][VN] = {};
             if (gx_acc) load_row<T, CPL>(gx + row * n, lane, o);
@@ -431,7 +439,7 @@ template <class T, int CPL, int MODE, int WPR>
 __global__ void __launch_bounds__(512, 2)
     k_ln_bwd_w(const T* x, const float* mean, const float* rstd, const T* gamma, const T* g, T* gx, T* gres, bool gx_acc,
                i64 rows, int n, uint64_t s1, uint64_t thr, float dscale, const uint32_t* keep, float* ws, int ncol,
-               bool gres_acc) {
+               bool gres_acc, const T* gext) {
     constexpr int VN = Vec<T>::N, CW = CPL / WPR, RPB = 16 / WPR;  // chunks per warp, rows per block pass
     extern __shared__ float sh[];  // [16 warps][ncol][CW*32*VN] column partials | red[2][16][2]
     float* red = sh + (size_t)16 * ncol * (CW * 32 * VN);
@@ -530,6 +538,11 @@ __global__ void __launch_bounds__(512, 2)
             for (int c = 0; c < CW; ++c) {
                 const int ch = (part * CW + c) * 32 + lane;
                 float o[VN];
+                if (gext) {  // + the sum's gradient from its other consumers (pre-LN residual stream)
+                    V::unpack(((const typename V::R*)(gext + row * n))[ch], o);
+#pragma unroll
+                    for (int e = 0; e < VN; ++e) gv[c][e] += o[e];
+                }
                 if (gres_acc) V::unpack(grr[ch], o);
 #pragma unroll
                 for (int e = 0; e < VN; ++e) o[e] = (gres_acc ? o[e] : 0.f) + gv[c][e];
@@ -654,7 +667,8 @@ bool bdrln_fwd_vec(const void* partial, const void* bias, const void* res, const
 // partials per block to ws (the caller finishes with the fixed-order column sum).
 bool ln_bwd_vec(int mode, const void* x, const float* mean, const float* rstd, const void* gamma, const void* g, void* gx,
                 void* gres, bool gx_acc, bool gres_acc, DT t, i64 rows, i64 n, u64 s1, u64 thr, float dscale,
-                const uint32_t* keep, float* ws, int ncol, int nblocks, cudaStream_t s) {
+                const uint32_t* keep, float* ws, int ncol, int nblocks, cudaStream_t s, const void* gext) {
+    if (gext && !aligned16(gext)) return false;
     for (const void* p : {x, g, (const void*)gx})
         if (!aligned16(p)) return false;
     if (t == F64 || (gamma && !aligned16(gamma)) || (gres && !aligned16(gres))) return false;
@@ -670,7 +684,7 @@ bool ln_bwd_vec(int mode, const void* x, const float* mean, const float* rstd, c
                     if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
                     k<<<nblocks, 32 * kW, smem, s>>>((const T*)x, mean, rstd, (const T*)gamma, (const T*)g, (T*)gx,
                                                      (T*)gres, gx_acc, rows, (int)n, s1, thr, dscale, keep, ws,
-                                                     ncol, gres_acc);
+                                                     ncol, gres_acc, (const T*)gext);
                 };
                 if constexpr (CPL % 4 == 0) {
                   if ((thr == 0 || keep) && !ln_narrow()) {
@@ -682,7 +696,8 @@ bool ln_bwd_vec(int mode, const void* x, const float* mean, const float* rstd, c
                     auto k = mode == 0 ? k_ln_bwd_w<T, CPL, 0, WPR> : k_ln_bwd_w<T, CPL, 1, WPR>;
                     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
                     k<<<nblocks, 512, sm2, s>>>((const T*)x, mean, rstd, (const T*)gamma, (const T*)g, (T*)gx, (T*)gres,
-                                                 gx_acc, rows, (int)n, s1, thr, dscale, keep, ws, ncol, gres_acc);
+                                                 gx_acc, rows, (int)n, s1, thr, dscale, keep, ws, ncol, gres_acc,
+                                                 (const T*)gext);
                     return;
                   }
                 }

@@ -10,6 +10,7 @@ outputs, 5e-2 gradients, and 2e-3 on the loss taken relative to sum|logits|
 (the logits have both signs, so their plain sum cancels; the condition number
 sum|o| / |sum o| is recorded with the errors).
 """
+import json
 import os
 
 import numpy as np
@@ -162,3 +163,29 @@ def test_t5_recipe_bf16(tmp_path):
     _, outs, grads, r = run_t5(str(tmp_path), cfg, script, 1, dtype="bf16")
     check(outs, grads, r, 1, BF16_OUT_TOL, BF16_GRAD_TOL, metric=rel_l2, tol_loss=BF16_LOSS_TOL,
           record="t5_bf16_h256_enc256_dec128", loss_l1=True)
+
+
+def test_residual_stream_fusion(tmp_path):
+    """pre-LN blocks: out_proj / mlp.c_proj -> dropout -> residual add -> next LayerNorm run as
+    one FusedLinearResLN whose sum is also the residual stream (lower.cpp
+    fuse_residual_stream); SB_RESLN_FUSE=0 keeps the separate ops — same results"""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import sys, json, numpy as np; sys.path.insert(0, %r)\\n"
+            "import paper_2302_08005_b200 as sb\\n"
+            "m = sb.gpt_neo(2, 32, 2, 32, 2, 16, 0.1); ex = sb.Executor(m, 'train', 5, 1)\\n"
+            "o = ex.forward(m.random_inputs(3))[0]; g = ex.backward().params\\n"
+            "np.save(sys.argv[1], np.concatenate([o.ravel()] + [g[k].ravel() for k in sorted(g)]))\\n"
+            "print(json.dumps(ex.describe()['kinds']))\\n") % root
+    res = []
+    for v in ("1", "0"):
+        f = str(tmp_path / f"r{v}.npy")
+        r = subprocess.run([sys.executable, "-c", code, f], capture_output=True, text=True, timeout=300,
+                           env=dict(os.environ, SB_RESLN_FUSE=v))
+        assert r.returncode == 0, r.stderr
+        res.append((np.load(f), json.loads(r.stdout.strip().splitlines()[-1])))
+    (a, ka), (b, kb) = res
+    # per block: attention out_proj + ln_2, and block 0's mlp c_proj + block 1's ln_1
+    assert ka.get("FusedLinearResLN", 0) == 3 and kb.get("FusedLinearResLN", 0) == 0, (ka, kb)
+    assert np.abs(a - b).max() <= 1e-5 * np.abs(b).max()
