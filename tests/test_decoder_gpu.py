@@ -172,12 +172,12 @@ def test_residual_stream_fusion(tmp_path):
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    code = ("import sys, json, numpy as np; sys.path.insert(0, %r)\\n"
-            "import paper_2302_08005_b200 as sb\\n"
-            "m = sb.gpt_neo(2, 32, 2, 32, 2, 16, 0.1); ex = sb.Executor(m, 'train', 5, 1)\\n"
-            "o = ex.forward(m.random_inputs(3))[0]; g = ex.backward().params\\n"
-            "np.save(sys.argv[1], np.concatenate([o.ravel()] + [g[k].ravel() for k in sorted(g)]))\\n"
-            "print(json.dumps(ex.describe()['kinds']))\\n") % root
+    code = ("import sys, json, numpy as np; sys.path.insert(0, %r)\n"
+            "import paper_2302_08005_b200 as sb\n"
+            "m = sb.gpt_neo(2, 32, 2, 32, 2, 16, 0.1); ex = sb.Executor(m, 'train', 5, 1)\n"
+            "o = ex.forward(m.random_inputs(3))[0]; g = ex.backward().params\n"
+            "np.save(sys.argv[1], np.concatenate([o.ravel()] + [g[k].ravel() for k in sorted(g)]))\n"
+            "print(json.dumps(ex.describe()['kinds']))\n") % root
     res = []
     for v in ("1", "0"):
         f = str(tmp_path / f"r{v}.npy")
@@ -186,6 +186,6 @@ def test_residual_stream_fusion(tmp_path):
         assert r.returncode == 0, r.stderr
         res.append((np.load(f), json.loads(r.stdout.strip().splitlines()[-1])))
     (a, ka), (b, kb) = res
-    # per block: attention out_proj + ln_2, and block 0's mlp c_proj + block 1's ln_1
-    assert ka.get("FusedLinearResLN", 0) == 3 and kb.get("FusedLinearResLN", 0) == 0, (ka, kb)
+    # per block: attn.out_proj + ln_2 and mlp.c_proj + the next LayerNorm (block 1's ln_1, then ln_f)
+    assert ka.get("FusedLinearResLN", 0) == 4 and kb.get("FusedLinearResLN", 0) == 0, (ka, kb)
     assert np.abs(a - b).max() <= 1e-5 * np.abs(b).max()
