@@ -140,7 +140,8 @@ int sb_pipeline_executor_grad(sb_pipeline_executor* e, int stage, const char* do
                               size_t* n);
 int sb_pipeline_executor_num_input_grads(sb_pipeline_executor* e, int stage, int* n);
 int sb_pipeline_executor_input_grad(sb_pipeline_executor* e, int stage, int idx, double* out, size_t cap, size_t* n);
-int sb_pipeline_executor_time_steps(sb_pipeline_executor* e, int steps, float* ms);
+int sb_pipeline_executor_time_steps(sb_pipeline_executor* e, int steps, float* ms); /* CUDA graph replay */
+int sb_pipeline_executor_time_steps_ex(sb_pipeline_executor* e, int steps, int use_graph, float* ms);
 int sb_pipeline_executor_free(sb_pipeline_executor* e);
 int sb_schedule_free(sb_schedule* s);
 

@@ -73,6 +73,7 @@ for _n, _a in {
     "sb_pipeline_executor_num_input_grads": (_P, _c.c_int, _c.POINTER(_c.c_int)),
     "sb_pipeline_executor_input_grad": (_P, _c.c_int, _c.c_int, _dp, _c.c_size_t, _c.POINTER(_c.c_size_t)),
     "sb_pipeline_executor_time_steps": (_P, _c.c_int, _c.POINTER(_c.c_float)),
+    "sb_pipeline_executor_time_steps_ex": (_P, _c.c_int, _c.c_int, _c.POINTER(_c.c_float)),
     "sb_pipeline_executor_free": (_P,),
     "sb_model_t5": (_c.c_int, _c.c_int, _i64, _i64, _i64, _i64, _i64, _i64, _c.c_double, _c.POINTER(_P)),
     "sb_model_t5_ex": (_c.c_int, _c.c_int, _i64, _i64, _i64, _i64, _i64, _i64, _c.c_double, _c.c_int,
@@ -779,9 +780,11 @@ class PipelineExecutor:
             res.append(gm)
         return res
 
-    def time_steps(self, steps: int) -> float:
+    def time_steps(self, steps: int, use_graph: bool = True) -> float:
+        """device ms of `steps` training steps; use_graph: captured once into a CUDA graph
+        (stages on one device) and replayed"""
         ms = _c.c_float()
-        _check(_lib.sb_pipeline_executor_time_steps(self._h, steps, _c.byref(ms)))
+        _check(_lib.sb_pipeline_executor_time_steps_ex(self._h, steps, int(use_graph), _c.byref(ms)))
         return ms.value
 
 

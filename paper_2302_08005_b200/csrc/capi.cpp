@@ -874,6 +874,9 @@ int sb_pipeline_executor_input_grad(sb_pipeline_executor* e, int stage, int idx,
 int sb_pipeline_executor_time_steps(sb_pipeline_executor* e, int steps, float* ms) {
     return guard([&] { *ms = e->ex->time_steps(steps); });
 }
+int sb_pipeline_executor_time_steps_ex(sb_pipeline_executor* e, int steps, int use_graph, float* ms) {
+    return guard([&] { *ms = e->ex->time_steps(steps, use_graph != 0); });
+}
 int sb_executor_allreduce(sb_executor* e, void* buf, int64_t n, int dtype, void* stream) {
     return guard([&] { e->ex->all_reduce_device(buf, n, kdt(dtype), stream); });
 }

@@ -152,8 +152,14 @@ struct PipelineExecutor::Impl {
     std::vector<std::vector<void*>> in_host_dev;  // [m][model input]: uploaded f64 slices (value buffers)
     bool ran_forward = false;
     int dev0 = 0;
+    // the whole step (every micro-batch's forward and backward over all stage streams)
+    // captured once into a CUDA graph when every local stage shares one device
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t gexec = nullptr;
 
     ~Impl() {
+        if (gexec) cudaGraphExecDestroy(gexec);
+        if (graph) cudaGraphDestroy(graph);
         for (auto& [k, p] : rtmp) cudaFree(p);
         for (auto& [k, p] : stmp) cudaFree(p);
         if (pcomm) p2p_comm_destroy(pcomm);
@@ -614,7 +620,7 @@ std::vector<GradMap> PipelineExecutor::backward() {
 }
 int PipelineExecutor::tp() const { return impl_->tp; }
 
-float PipelineExecutor::time_steps(int steps) {
+float PipelineExecutor::time_steps(int steps, bool use_graph) {
     auto& I = *impl_;
     if (!I.ran_forward) throw Error("time_steps: run forward() once first (uploads the inputs)");
     PCK(cudaSetDevice(I.dev0));
@@ -624,22 +630,41 @@ float PipelineExecutor::time_steps(int steps) {
     I.sync_all();
     PCK(cudaSetDevice(I.dev0));
     cudaStream_t s0 = I.stages[I.dist ? (size_t)I.lstage : 0].st;
-    PCK(cudaEventRecord(a, s0));
+    bool one_dev = true;
     for (auto& s : I.stages)
-        if (s.ex && s.st != s0) PCK(cudaStreamWaitEvent(s.st, a, 0));
-    for (int k = 0; k < steps; ++k) {
+        if (s.ex) one_dev &= s.dev == I.dev0;
+    // one step on the stage streams, forked from and joined into s0
+    cudaEvent_t fork;
+    PCK(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+    auto enqueue_step = [&]() {
+        PCK(cudaEventRecord(fork, s0));
+        for (auto& s : I.stages)
+            if (s.ex && s.st != s0) PCK(cudaStreamWaitEvent(s.st, fork, 0));
         I.forward_all();
         I.backward_all();
+        PCK(cudaSetDevice(I.dev0));
+        for (auto& s : I.stages)
+            if (s.ex && s.st != s0) PCK(cudaStreamWaitEvent(s0, s.ev_bwd[0], 0));
+    };
+    if (use_graph && one_dev && !I.gexec) {
+        PCK(cudaStreamBeginCapture(s0, cudaStreamCaptureModeThreadLocal));
+        enqueue_step();
+        PCK(cudaStreamEndCapture(s0, &I.graph));
+        PCK(cudaGraphInstantiate(&I.gexec, I.graph, 0));
     }
-    PCK(cudaSetDevice(I.dev0));
-    for (auto& s : I.stages)
-        if (s.ex && s.st != s0) PCK(cudaStreamWaitEvent(s0, s.ev_bwd[0], 0));
+    const bool graph = use_graph && I.gexec;
+    PCK(cudaEventRecord(a, s0));
+    for (int k = 0; k < steps; ++k) {
+        if (graph) PCK(cudaGraphLaunch(I.gexec, s0));
+        else enqueue_step();
+    }
     PCK(cudaEventRecord(b, s0));
     PCK(cudaEventSynchronize(b));
     float ms = 0;
     PCK(cudaEventElapsedTime(&ms, a, b));
     cudaEventDestroy(a);
     cudaEventDestroy(b);
+    cudaEventDestroy(fork);
     I.sync_all();
     return ms;
 }

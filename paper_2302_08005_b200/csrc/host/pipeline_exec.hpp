@@ -75,8 +75,9 @@ public:
     std::vector<GradMap> backward();
     int tp() const;
     // device ms of `steps` full training steps (forward + backward of every
-    // micro-batch) on already-uploaded inputs (the last forward's)
-    float time_steps(int steps);
+    // micro-batch) on already-uploaded inputs (the last forward's); use_graph: the step is
+    // captured once into a CUDA graph (stages on one device) and replayed
+    float time_steps(int steps, bool use_graph = true);
     int num_stages() const;
     int micro_batches() const;
 

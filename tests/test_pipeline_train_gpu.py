@@ -117,9 +117,15 @@ def test_pipeline_timing_and_errors():
     pe = sb.PipelineExecutor(plan, 2, "train", 1, "fp32")
     with pytest.raises(sb.SlapoError):
         pe.backward()  # before any forward
-    pe.forward(m.random_inputs(3))
-    ms = pe.time_steps(3)
-    assert ms > 0
+    x = m.random_inputs(3)
+    pe.forward(x)
+    g0 = _merged(pe.backward())
+    assert pe.time_steps(2, use_graph=False) > 0
+    assert pe.time_steps(3) > 0  # the step captured into a CUDA graph and replayed
+    pe.forward(x)  # eager again after the replays: identical gradients
+    g1 = _merged(pe.backward())
+    for k in g0:
+        assert np.array_equal(g0[k], g1[k]), k
     with pytest.raises(sb.SlapoError, match="micro-batches"):
         sb.PipelineExecutor(plan, 3, "train", 1, "fp32")  # batch 4 is not divisible by 3
     with pytest.raises(sb.SlapoError, match="one device per stage"):
