@@ -436,7 +436,7 @@ __global__ void __launch_bounds__(32 * kW, 1)
 // co-reside with other work. The two row sums are combined across the WPR warps
 // through shared memory in a fixed order (deterministic).
 template <class T, int CPL, int MODE, int WPR>
-__global__ void __launch_bounds__(512, 2)
+__global__ void __launch_bounds__(512, WPR >= 4 ? 2 : 1)
     k_ln_bwd_w(const T* x, const float* mean, const float* rstd, const T* gamma, const T* g, T* gx, T* gres, bool gx_acc,
                i64 rows, int n, uint64_t s1, uint64_t thr, float dscale, const uint32_t* keep, float* ws, int ncol,
                bool gres_acc, const T* gext) {
@@ -691,13 +691,28 @@ bool ln_bwd_vec(int mode, const void* x, const float* mean, const float* rstd, c
                     // 4 warps per row (8 at CPL 8: a 2048-wide bf16 row would otherwise hold two
                     // chunks of column partials per thread and spill under the 64-register cap),
                     // 16-warp blocks, two blocks per SM
-                    constexpr int WPR = CPL >= 8 ? 8 : 4;
-                    const size_t sm2 = (size_t)16 * ncol * (n / WPR) * 4 + 2 * 16 * 2 * 4;
-                    auto k = mode == 0 ? k_ln_bwd_w<T, CPL, 0, WPR> : k_ln_bwd_w<T, CPL, 1, WPR>;
-                    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
-                    k<<<nblocks, 512, sm2, s>>>((const T*)x, mean, rstd, (const T*)gamma, (const T*)g, (T*)gx, (T*)gres,
-                                                 gx_acc, rows, (int)n, s1, thr, dscale, keep, ws, ncol, gres_acc,
-                                                 (const T*)gext);
+                    // SB_LN_WPR=2 / 4 forces 2 / 4 warps per row (2: one 16-warp block per SM, <= 128 registers)
+                    static const int wpr_env = getenv("SB_LN_WPR") ? atoi(getenv("SB_LN_WPR")) : 0;
+                    auto go = [&](auto wc) {
+                        constexpr int WPR = decltype(wc)::value;
+                        const size_t sm2 = (size_t)16 * ncol * (n / WPR) * 4 + 2 * 16 * 2 * 4;
+                        auto k = mode == 0 ? k_ln_bwd_w<T, CPL, 0, WPR> : k_ln_bwd_w<T, CPL, 1, WPR>;
+                        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+                        const int nb = nblocks;  // (the column finish reads one partial row per block)
+                        k<<<nb, 512, sm2, s>>>((const T*)x, mean, rstd, (const T*)gamma, (const T*)g, (T*)gx, (T*)gres,
+                                               gx_acc, rows, (int)n, s1, thr, dscale, keep, ws, ncol, gres_acc,
+                                               (const T*)gext);
+                        return nb;
+                    };
+                    if constexpr (CPL >= 8) {
+                        go(std::integral_constant<int, 8>{});
+                    } else {
+                        // the plain LayerNorm backward (mode 0) runs faster with 2 warps per row at
+                        // one block per SM (41.2 -> 33.0 us at 16384 x 1024); the fused one does not
+                        // (41.2 either way: it spills more) — profiles/r2/ln_wpr.log
+                        if (wpr_env == 2 || (wpr_env == 0 && mode == 0)) go(std::integral_constant<int, 2>{});
+                        else go(std::integral_constant<int, 4>{});
+                    }
                     return;
                   }
                 }
