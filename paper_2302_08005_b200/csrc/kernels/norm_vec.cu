@@ -435,8 +435,8 @@ __global__ void __launch_bounds__(32 * kW, 1)
 // per-column dgamma/dbeta/dbias partials dominate), so 16-warp blocks fit and
 // co-reside with other work. The two row sums are combined across the WPR warps
 // through shared memory in a fixed order (deterministic).
-template <class T, int CPL, int MODE, int WPR>
-__global__ void __launch_bounds__(512, WPR >= 4 ? 2 : 1)
+template <class T, int CPL, int MODE, int WPR, int MINB = (WPR >= 8 ? 2 : 1)>
+__global__ void __launch_bounds__(512, MINB)
     k_ln_bwd_w(const T* x, const float* mean, const float* rstd, const T* gamma, const T* g, T* gx, T* gres, bool gx_acc,
                i64 rows, int n, uint64_t s1, uint64_t thr, float dscale, const uint32_t* keep, float* ws, int ncol,
                bool gres_acc, const T* gext) {
@@ -688,10 +688,8 @@ bool ln_bwd_vec(int mode, const void* x, const float* mean, const float* rstd, c
                 };
                 if constexpr (CPL % 4 == 0) {
                   if ((thr == 0 || keep) && !ln_narrow()) {
-                    // 4 warps per row (8 at CPL 8: a 2048-wide bf16 row would otherwise hold two
-                    // chunks of column partials per thread and spill under the 64-register cap),
-                    // 16-warp blocks, two blocks per SM
-                    // SB_LN_WPR=2 / 4 forces 2 / 4 warps per row (2: one 16-warp block per SM, <= 128 registers)
+                    // 2 or 4 warps per row, one 16-warp block per SM (<= 128 registers); SB_LN_WPR=2 / 4
+                    // forces 2 / 4 warps per row at CPL 4, SB_LN_WPR=8 forces 8 (two blocks per SM) at CPL 8
                     static const int wpr_env = getenv("SB_LN_WPR") ? atoi(getenv("SB_LN_WPR")) : 0;
                     auto go = [&](auto wc) {
                         constexpr int WPR = decltype(wc)::value;
@@ -705,11 +703,15 @@ bool ln_bwd_vec(int mode, const void* x, const float* mean, const float* rstd, c
                         return nb;
                     };
                     if constexpr (CPL >= 8) {
-                        go(std::integral_constant<int, 8>{});
+                        // (2048-wide bf16 rows: 4 warps per row at one block per SM beat 8 at two,
+                        // 45.1 -> 35.0 us plain and 53.1 -> 45.2 us fused at 8192 rows — ln_minb2.log)
+                        if (wpr_env == 8) go(std::integral_constant<int, 8>{});
+                        else go(std::integral_constant<int, 4>{});
                     } else {
-                        // the plain LayerNorm backward (mode 0) runs faster with 2 warps per row at
-                        // one block per SM (41.2 -> 33.0 us at 16384 x 1024); the fused one does not
-                        // (41.2 either way: it spills more) — profiles/r2/ln_wpr.log
+                        // one 16-warp block per SM (<= 128 registers, no spills): the plain LayerNorm
+                        // backward with 2 warps per row (41.2 -> 33.0 us at 16384 x 1024), the fused
+                        // one with 4 (41.4 -> 37.1 us; at 2 it keeps more live state and spills) —
+                        // profiles/r2/ln_wpr.log, ln_minb.log
                         if (wpr_env == 2 || (wpr_env == 0 && mode == 0)) go(std::integral_constant<int, 2>{});
                         else go(std::integral_constant<int, 4>{});
                     }
