@@ -1207,6 +1207,7 @@ __global__ void __launch_bounds__(B7_WARPS * 32, 1)
     const long long bh = (long long)b * ba.nh + h;
     const int row_base = b * S, kv_base = b * Sk;  // (query rows / key rows)
     const bool TS7 = ba.ts && blockIdx.x == 0 && blockIdx.y == 0;
+    if (TS7 && threadIdx.x == 0) ba.ts[14 * 64 + 63] = gtime();
 
     if (threadIdx.x == 0) {
         tma_prefetch(&tK);
@@ -1267,6 +1268,10 @@ __global__ void __launch_bounds__(B7_WARPS * 32, 1)
                 if (TS7) ba.ts[14 * 64 + u] = gtime();
                 mbar_wait(&st_empty[s], ((u / B7_NST) & 1) ^ 1);
                 if (TS7) ba.ts[15 * 64 + u] = gtime();
+                if (ba.dbg & 128) {  // debugging: no per-step loads
+                    mbar_arrive(&st_full[s]);
+                    continue;
+                }
                 mbar_expect_tx(&st_full[s], 2 * F_TILE_BYTES + 1024 + (ba.mask_t ? 2048 : 0));
                 tma_load_2d(st, &tQ, &st_full[s], h * FD, row_base + i * FT);
                 tma_load_2d(st + F_TILE_BYTES, &tdO, &st_full[s], h * FD, row_base + i * FT);
@@ -1590,6 +1595,7 @@ __global__ void __launch_bounds__(B7_WARPS * 32, 1)
     if (lane == 0) bulk_wait0();  // this warp's TMA stores have completed
     fence_before();
     __syncthreads();
+    if (TS7 && threadIdx.x == 0) ba.ts[15 * 64 + 63] = gtime();
     if (warp == W_MMA) {
         fence_after();
         tmem_dealloc<512>(tmem);
@@ -2234,6 +2240,7 @@ bool attn_bwd_sm100_try(const Attn& a, const void* dout, i64 ld_do, void* dq, vo
             for (int r = 14; r < 16; ++r) {
                 fprintf(stderr, "%-22s", pn[r - 14]);
                 for (int u = 0; u < 16; ++u) fprintf(stderr, " %6lld", h_ts[r * 64 + u] ? (long long)(h_ts[r * 64 + u] - t0) : -1);
+                fprintf(stderr, "  cta %s %lld", r == 14 ? "start" : "end", (long long)(h_ts[r * 64 + 63] - t0));
                 fprintf(stderr, "\n");
             }
         }

@@ -308,8 +308,10 @@ __global__ void __cluster_dims__(2 * PAIRS, 1, 1) __launch_bounds__(320, 1)
         int lt = 0, nst = 0;
         // dGeLU epilogue: each lane's 64 B of the pre-activation (its row, the chunk's 32
         // columns) loaded straight into registers two chunks ahead — the first two of a
-        // tile are issued before the accumulator wait, so their latency hides behind it
-        // (M and N are multiples of 256: no bounds checks)
+        // tile are issued before the accumulator wait, so their latency hides behind it.
+        // Ragged edges (M, N multiples of 32, not of the tile): the TMA loads zero-fill
+        // beyond M / N and the TMA stores clip, so only the direct global accesses (bias,
+        // pre-activation, accumulate, split-K rows) skip a warp's chunks past the edge.
         uint4 axa[4], axb[4];
         auto aux_ld = [&](uint4(&w)[4], long long row, long long col) {
             const uint4* src = (const uint4*)(ep.aux + row * ep.ldc + col);
@@ -321,9 +323,10 @@ __global__ void __cluster_dims__(2 * PAIRS, 1, 1) __launch_bounds__(320, 1)
             int m0, n0, z;
             tile_coords(tile, m0, n0, z);
             const long long row0 = m0 + (long long)rank * G_BM + q * 32;  // first row of this warp
-            if (ep.gelu == 2) {
-                aux_ld(axa, row0 + lane, n0 + half * 32);
-                if (half + 2 < G_BN / 32) aux_ld(axb, row0 + lane, n0 + (half + 2) * 32);
+            const bool row_ok = row0 < ep.M;
+            if (ep.gelu == 2 && row_ok) {
+                if (n0 + half * 32 < ep.N) aux_ld(axa, row0 + lane, n0 + half * 32);
+                if (half + 2 < G_BN / 32 && n0 + (half + 2) * 32 < ep.N) aux_ld(axb, row0 + lane, n0 + (half + 2) * 32);
             }
             mbar_wait(&tfull[acc], (lt >> 1) & 1);
             fence_after();
@@ -338,6 +341,7 @@ __global__ void __cluster_dims__(2 * PAIRS, 1, 1) __launch_bounds__(320, 1)
                     if (lane == 0) mbar_arrive_cluster(tempty0 + acc * 8);
                 }
                 const long long col = n0 + c * 32;
+                if (!row_ok || col >= ep.N) continue;  // past the ragged edge (later chunks too)
                 float v[32];
 #pragma unroll
                 for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * ep.alpha;
@@ -385,7 +389,7 @@ __global__ void __cluster_dims__(2 * PAIRS, 1, 1) __launch_bounds__(320, 1)
                     }
 #pragma unroll
                     for (int j = 0; j < 4; ++j) axa[j] = axb[j];
-                    if (c + 4 < G_BN / 32) aux_ld(axb, row, col + 128);  // this warp's chunk after next
+                    if (c + 4 < G_BN / 32 && col + 128 < ep.N) aux_ld(axb, row, col + 128);  // this warp's chunk after next
                 }
                 if (ep.accumulate) {
                     // C += v, direct read-modify-write of this thread's row
@@ -553,7 +557,8 @@ bool gemm_tc2_try(const Gemm& g, cudaStream_t s) {
     const bool a_k = g.sAk == 1 && !a_mn, b_k = g.sBk == 1 && !b_mn;
     if (!(a_mn || a_k) || !(b_mn || b_k)) return false;
     const long long M = g.M, N = g.N, K = g.K;
-    if (M % 256 || N % 256 || K % G_BK || M <= 0 || N <= 0 || K <= 0) return false;
+    // M, N multiples of 32 (a warp's epilogue chunk): ragged last tiles (TMA zero-fill / clip)
+    if (M % 32 || N % 32 || K % G_BK || M <= 0 || N <= 0 || K <= 0) return false;
     const long long lda = a_mn ? g.sAk : g.sAm, ldb = b_mn ? g.sBk : g.sBn, ldc = g.sCm;
     auto al16 = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
     if (lda % 8 || ldb % 8 || ldc % 8 || !al16(g.A) || !al16(g.B) || !al16(g.C)) return false;
@@ -570,7 +575,8 @@ bool gemm_tc2_try(const Gemm& g, cudaStream_t s) {
     // stage, but 4-CTA clusters fit only 33 per chip (132 SMs): measured +2-3% on
     // K = 4096 / 16384, -3-6% on the K = 1024 GEMMs with GeLU / dGeLU / bias epilogues
     static const int pairs_env = getenv("SB_GEMM_PAIRS") ? atoi(getenv("SB_GEMM_PAIRS")) : 0;
-    const int pairs = (N / G_BN) % 2 ? 1 : pairs_env ? pairs_env : (K >= 4096 ? 2 : 1);
+    const long long m_blks = (M + 255) / 256, n_blks = (N + G_BN - 1) / G_BN;
+    const int pairs = n_blks % 2 ? 1 : pairs_env ? pairs_env : (K >= 4096 ? 2 : 1);
     // pair slots of the persistent grid (the split-K model below counts waves in them)
     const int clusters = pairs == 2 ? 2 * (G_BN == 256 ? max_clusters2<256, false, false, 2>()
                                                        : max_clusters2<128, false, false, 2>())
@@ -579,7 +585,7 @@ bool gemm_tc2_try(const Gemm& g, cudaStream_t s) {
         return false;
     if (!(b_mn ? make_map_bf16(&tb, g.B, N, K, ldb, 64) : make_map_bf16(&tb, g.B, K, N, ldb, G_BN / 2))) return false;
     const int kblocks = (int)(K / G_BK);
-    const long long tiles = (M / 256) * (N / G_BN);  // pair tiles
+    const long long tiles = m_blks * n_blks;  // pair tiles
     int splits = 1;
     // long-K, few-tile problems (the weight gradients) -> deterministic split-K, with the
     // split count from a wave model: ceil(tiles * s / clusters) waves of kblocks / s
@@ -621,7 +627,7 @@ bool gemm_tc2_try(const Gemm& g, cudaStream_t s) {
     if (g.epilogue && splits == 1) {  // GeLU: pre-activation store map; dGeLU: pre-activation load map
         if (!make_store_map(&tx, g.aux, false, N, M, ldc)) return false;
     }
-    Sched2 sc{(int)(M / 256), (int)(N / G_BN), splits, kblocks / splits, pairs};
+    Sched2 sc{(int)m_blks, (int)n_blks, splits, kblocks / splits, pairs};
     static unsigned long long* ts_buf = nullptr;
     ep.ts = nullptr;
     if (getenv("SB_GEMM_TS")) {

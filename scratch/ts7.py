@@ -2,7 +2,7 @@ import os, sys, torch
 sys.path.insert(0, '.')
 exec(open('scratch/attn_bench.py').read().split("def t(")[0])
 fwd(); torch.cuda.synchronize()
-for d in ("127",):
+for d in os.environ.get("DBGS", "0,255").split(","):
     os.environ["SB_ATTN_DBG"] = d
     bwd(); torch.cuda.synchronize()
     a, b = torch.cuda.Event(True), torch.cuda.Event(True)

@@ -204,6 +204,62 @@ def test_gemm_4cta_multicast(layout):
     assert (outs[0].float() - outs[1].float()).abs().max().item() <= 2e-2 * outs[1].float().abs().max().item()
 
 
+@pytest.mark.parametrize("M,N,K", [(1056, 800, 512), (1152, 640, 256), (544, 800, 4096)])
+@pytest.mark.parametrize("layout", ["tn_bias", "tn_gelu", "nn_acc", "nn_dgelu", "nt_f32", "nt_f32_acc", "nt_splitk"])
+def test_gemm_2sm_ragged_tiles(layout, M, N, K):
+    """M, N multiples of 32 but not of the 256-wide tile (GPT-Neo's vocab 50304, T5's 32128): the
+    2-SM kernel's last tiles are ragged (TMA zero-fill on loads, clipped stores, the direct bias /
+    pre-activation / accumulate / split-K accesses skip the chunks past the edge) — against fp32
+    torch, with guard bands around C checking nothing is written past the edge"""
+    if layout == "nt_splitk":
+        M, N, K = min(M, 288), 160, 4096  # few tiles, long K: split-K partials
+    g = torch.Generator(device="cuda").manual_seed(11)
+    rnd = lambda *sh: torch.randn(*sh, device="cuda", generator=g)  # noqa: E731
+    f32 = layout.startswith("nt")
+    # C inside a larger buffer (row stride N + 64, 32 extra rows): the band must stay untouched
+    big = torch.full((M + 32, N + 64), 7.0, device="cuda", dtype=torch.float32 if f32 else torch.bfloat16)
+    C = big[:M, :N]
+    if layout.startswith("tn"):
+        x, w, b = rnd(M, K).bfloat16(), rnd(N, K).bfloat16(), rnd(N).bfloat16()
+        C.zero_()
+        # (the pre-activation shares C's row stride)
+        pre = torch.zeros(M + 32, N + 64, device="cuda", dtype=torch.bfloat16)[:M, :N] if layout == "tn_gelu" else None
+        e = gemm(x, (K, 1), w, (1, K), C, M, N, K, bias=b, gelu=layout == "tn_gelu", aux=pre)
+        ref = x.float() @ w.float().T + b.float()
+        if pre is not None:
+            close(pre, ref)
+            ref = torch.nn.functional.gelu(ref, approximate="tanh")
+    elif layout.startswith("nn"):
+        gy, w = rnd(M, K).bfloat16(), rnd(K, N).bfloat16()
+        if layout == "nn_acc":
+            C.copy_(rnd(M, N).bfloat16())
+            base = C.float().clone()
+            e = gemm(gy, (K, 1), w, (N, 1), C, M, N, K, acc=True)
+            ref = base + gy.float() @ w.float()
+        else:
+            C.zero_()
+            aux = torch.zeros(M + 32, N + 64, device="cuda", dtype=torch.bfloat16)[:M, :N]
+            aux.copy_(rnd(M, N).bfloat16())
+            e = gemm(gy, (K, 1), w, (N, 1), C, M, N, K, epi=2, aux=aux)
+            a = aux.float()
+            t = torch.tanh(0.7978845608028654 * (a + 0.044715 * a ** 3))
+            ref = (gy.float() @ w.float()) * (0.5 * (1 + t) + 0.5 * a * (1 - t * t) * 0.7978845608028654 *
+                                              (1 + 3 * 0.044715 * a * a))
+    else:
+        gy, x = rnd(K, M).bfloat16(), rnd(K, N).bfloat16()
+        acc = layout == "nt_f32_acc"
+        if acc:
+            C.copy_(rnd(M, N))
+        else:
+            C.zero_()
+        base = C.clone()
+        e = gemm(gy, (1, M), x, (N, 1), C, M, N, K, acc=acc)
+        ref = (base if acc else 0) + gy.float().T @ x.float()
+    assert e == 2, (layout, M, N, K, e)
+    close(C, ref, 1e-2 if f32 else 2e-2)
+    assert bool((big[M:] == 7).all()) and bool((big[:, N:] == 7).all()), "written past the ragged edge"
+
+
 # ------------------------------------------------------------------ attention
 L.sb_attn_fwd.argtypes = [ctypes.c_void_p] * 4 + [ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p] + \
     [ctypes.c_int64] * 4 + [ctypes.c_float, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_double, ctypes.c_int,
