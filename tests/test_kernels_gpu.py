@@ -204,7 +204,7 @@ def test_gemm_4cta_multicast(layout):
     assert (outs[0].float() - outs[1].float()).abs().max().item() <= 2e-2 * outs[1].float().abs().max().item()
 
 
-@pytest.mark.parametrize("M,N,K", [(1056, 800, 512), (1152, 640, 256), (544, 800, 4096)])
+@pytest.mark.parametrize("M,N,K", [(1056, 800, 512), (1152, 640, 256), (544, 800, 4096), (32, 96, 128)])
 @pytest.mark.parametrize("layout", ["tn_bias", "tn_gelu", "nn_acc", "nn_dgelu", "nt_f32", "nt_f32_acc", "nt_splitk"])
 def test_gemm_2sm_ragged_tiles(layout, M, N, K):
     """M, N multiples of 32 but not of the 256-wide tile (GPT-Neo's vocab 50304, T5's 32128): the
