@@ -306,6 +306,12 @@ constexpr int F6_MASK_BYTES = 2048;         // keep bits of 128 query rows x 128
 #ifndef F6_QBUF
 #define F6_QBUF 1  // Q tile buffers (2: the next tile's Q loads while this tile runs)
 #endif
+#ifndef F6_ONEPASS
+// S read from TMEM once (64 registers per row: max, then exp2 from registers) instead of
+// twice: 0 never, 1 always, 2 for causal tiles and head dim 128 (fa_ab.log: 67.9 -> 64.0 us
+// causal hd 128, 57.7 -> 56.3 us causal hd 64; the non-causal hd-64 tile runs 68.1 -> 70.5)
+#define F6_ONEPASS 2
+#endif
 template <int D>
 struct F6 {
     static constexpr int PANELS = D / 64;
@@ -495,53 +501,57 @@ __global__ void __launch_bounds__(F6_THREADS, F6<D>::CTAS)
                 }
                 // pass 1: row max of S (P overwrites S in place, so the max comes first)
                 float mx = -INFINITY;
-#pragma unroll
-                for (int c = 0; c < 2; ++c) {
-                    uint32_t sv[32];
-                    tmem_ld32_nowait(t_row + c * 32, sv);
+                constexpr bool ONEPASS = F6_ONEPASS == 1 || (F6_ONEPASS == 2 && (CAUSAL || D == 128));
+                uint32_t s0[32], s1[32];
+                if constexpr (ONEPASS) {
+                    tmem_ld32_nowait(t_row, s0);
+                    tmem_ld32_nowait(t_row + 32, s1);
                     tmem_ld_wait();
                     if (kmax < KC6 - 1) {
 #pragma unroll
-                        for (int e = 0; e < 32; ++e)
-                            if (c * 32 + e > kmax) sv[e] = __float_as_uint(-INFINITY);
+                        for (int e = 0; e < 32; ++e) {
+                            if (e > kmax) s0[e] = __float_as_uint(-INFINITY);
+                            if (32 + e > kmax) s1[e] = __float_as_uint(-INFINITY);
+                        }
                     }
 #pragma unroll
-                    for (int e = 0; e < 32; e += 2) mx = fmax3(mx, __uint_as_float(sv[e]), __uint_as_float(sv[e + 1]));
+                    for (int e = 0; e < 32; e += 2) {
+                        mx = fmax3(mx, __uint_as_float(s0[e]), __uint_as_float(s0[e + 1]));
+                        mx = fmax3(mx, __uint_as_float(s1[e]), __uint_as_float(s1[e + 1]));
+                    }
+                } else {
+#pragma unroll
+                    for (int c = 0; c < 2; ++c) {
+                        uint32_t sv[32];
+                        tmem_ld32_nowait(t_row + c * 32, sv);
+                        tmem_ld_wait();
+                        if (kmax < KC6 - 1) {
+#pragma unroll
+                            for (int e = 0; e < 32; ++e)
+                                if (c * 32 + e > kmax) sv[e] = __float_as_uint(-INFINITY);
+                        }
+#pragma unroll
+                        for (int e = 0; e < 32; e += 2) mx = fmax3(mx, __uint_as_float(sv[e]), __uint_as_float(sv[e + 1]));
+                    }
                 }
                 mx *= fa.c;
                 if (j == 0) m_used = mx;
-                if (__any_sync(0xffffffffu, mx > m_used + kLazy6)) {
-                    // rare: the running max grew by > 2^kLazy6 -> rescale O (after PV(j-1)) and l
+                // rare: the running max grew by > 2^kLazy6 -> rescale l now and O once P is out
+                // (S(j) completing implies PV(j-1) did: in-order MMAs, so O is final until PV(j))
+                float f_res = 0.f;
+                const bool rescale = __any_sync(0xffffffffu, mx > m_used + kLazy6);
+                if (rescale) {
                     const float m_new = fmaxf(m_used, mx);
-                    const float f = ex2f(m_used - m_new);
-                    l *= f;
+                    f_res = ex2f(m_used - m_new);
+                    l *= f_res;
                     m_used = m_new;
-                    mbar_wait(o_done, (u - 1) & 1);
-                    fence_after();
-#pragma unroll
-                    for (int c = 0; c < D / 32; ++c) {
-                        uint32_t o[32];
-                        tmem_ld32_nowait(t_row + 64 + c * 32, o);
-                        tmem_ld_wait();
-#pragma unroll
-                        for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * f);
-                        tmem_st32(t_row + 64 + c * 32, o);
-                    }
                 }
                 // pass 2: P = exp2(S*c - m_used) * keep -> TMEM (bf16 pairs over S's first 32 columns)
                 float2 lc2 = make_float2(0.f, 0.f);
                 const float2 c2 = make_float2(fa.c, fa.c), nm2 = make_float2(-m_used, -m_used);
-#pragma unroll
-                for (int c = 0; c < 2; ++c) {
-                    const uint32_t mword = c == 0 ? mw.x : mw.y;
-                    uint32_t sv[32], pk[16];
-                    tmem_ld32_nowait(t_row + c * 32, sv);
-                    tmem_ld_wait();
-                    if (kmax < KC6 - 1) {
-#pragma unroll
-                        for (int e = 0; e < 32; ++e)
-                            if (c * 32 + e > kmax) sv[e] = __float_as_uint(-INFINITY);
-                    }
+                // 32 columns of S (registers) -> P bf16 pairs -> TMEM columns [c * 16, c * 16 + 16)
+                auto p_half = [&](const uint32_t(&sv)[32], uint32_t mword, int c) {
+                    uint32_t pk[16];
 #pragma unroll
                     for (int e = 0; e < 16; ++e) {  // element pairs on the packed-fp32 pipe
                         const float2 a =
@@ -553,8 +563,38 @@ __global__ void __launch_bounds__(F6_THREADS, F6<D>::CTAS)
                         pk[e] = pack_bf16(p.x, p.y);
                     }
                     tmem_st16(t_row + c * 16, pk);
+                };
+                if constexpr (ONEPASS) {
+                    p_half(s0, mw.x, 0);
+                    p_half(s1, mw.y, 1);
+                } else {
+#pragma unroll
+                    for (int c = 0; c < 2; ++c) {
+                        uint32_t sv[32];
+                        tmem_ld32_nowait(t_row + c * 32, sv);
+                        tmem_ld_wait();
+                        if (kmax < KC6 - 1) {
+#pragma unroll
+                            for (int e = 0; e < 32; ++e)
+                                if (c * 32 + e > kmax) sv[e] = __float_as_uint(-INFINITY);
+                        }
+                        p_half(sv, c == 0 ? mw.x : mw.y, c);
+                    }
                 }
                 l += lc2.x + lc2.y;
+                if (rescale) {
+                    mbar_wait(o_done, (u - 1) & 1);
+                    fence_after();
+#pragma unroll
+                    for (int c = 0; c < D / 32; ++c) {
+                        uint32_t o[32];
+                        tmem_ld32_nowait(t_row + 64 + c * 32, o);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * f_res);
+                        tmem_st32(t_row + 64 + c * 32, o);
+                    }
+                }
                 tmem_st_wait();
                 fence_before();
                 __syncwarp();
