@@ -129,6 +129,11 @@ struct RankCtx {
     size_t scratch_grad_bytes = 0;
     char* scratch_grad = nullptr;
     std::vector<std::pair<size_t, size_t>> region_grad_span;  // per region: offset,bytes in grad scratch
+    // FusedLinearGelu op -> its bias gradient's column partials ([rows/32][out] fp32), written
+    // by the consuming Linear's dGeLU dgrad epilogue (2-SM GEMM) instead of re-reading the
+    // pre-activation gradient; colsum_ready: written during this backward
+    std::map<int, float*> colsum;
+    std::set<int> colsum_ready;
 };
 
 struct Step {
@@ -625,6 +630,17 @@ public:
         r.tmp_bytes = align_up(tmp);
         size_t tmp_off = off;
         off += r.tmp_bytes;
+        std::vector<std::pair<int, size_t>> cs_off;
+        const char* bias_epi = getenv("SB_BIAS_EPI");  // 0: bias gradients by the separate column-sum pass (A/B)
+        if (cdt == sbk::BF16 && !(bias_epi && atoi(bias_epi) == 0))
+            for (size_t i = 0; i < P.fwd.size(); ++i) {
+                const Op& op = P.fwd[i];
+                if (op.k != K::FusedLinearGelu || !op.dgelu_fused || !op.has_bias || !op.bias_grad) continue;
+                const View& y = P.views[(size_t)op.out[0]];
+                if (rows_of(y) % 32) continue;
+                cs_off.push_back({(int)i, off});
+                off += align_up((size_t)(rows_of(y) / 32) * (size_t)cols_of(y) * 4);
+            }
         r.total = off;
         CK(cudaMalloc(&r.base, r.total));
         // on our (non-blocking) stream: a legacy-stream memset would race the
@@ -645,6 +661,8 @@ public:
         }
         r.ws = r.base + ws_off;
         r.tmp = r.base + tmp_off;
+        r.colsum.clear();
+        for (auto& [i, o] : cs_off) r.colsum[i] = (float*)(r.base + o);
         r.scratch_grad = r.base + sg_off;
         r.region_grad_span.clear();
         for (size_t k = 0; k < P.regions.size(); ++k) r.region_grad_span.push_back({sg_off, rg[k]});
@@ -726,7 +744,7 @@ public:
 
     void gemm_rowwise(RankCtx& r, const void* A, i64 lda, bool a_t, const void* B, i64 ldb, bool b_t, void* C, i64 ldc,
                       DT tc, i64 M, i64 N, i64 K, bool acc, const void* bias, int epi = 0, void* aux = nullptr,
-                      cudaStream_t st = nullptr) {
+                      cudaStream_t st = nullptr, float* colsum = nullptr) {
         // A(m,k): a_t ? A[k*lda + m] : A[m*lda + k];  B(k,n): b_t ? B[n*ldb + k] : B[k*ldb + n]
         sbk::Gemm g;
         g.A = A;
@@ -751,6 +769,7 @@ public:
         g.aux = aux;
         g.ws = st && st == wstream ? r.ws2 : r.ws;
         g.ws_bytes = r.ws_bytes;
+        g.colsum = colsum;
         run_gemm(g, st);
     }
 
@@ -1261,9 +1280,16 @@ public:
         }
         if (!(part & 1)) {
         } else if (op.dgelu_pre >= 0) {
-            // dx lands directly as the producing GeLU's input gradient: gelu'(pre) * (g W)
+            // dx lands directly as the producing GeLU's input gradient: gelu'(pre) * (g W);
+            // the epilogue also leaves the column partials of the producer's bias gradient
+            int fi = -1;
+            for (size_t k = 0; k < r.P.fwd.size(); ++k)
+                if (r.P.fwd[k].k == K::FusedLinearGelu && r.P.fwd[k].out[1] == op.dgelu_pre) fi = (int)k;
+            auto cs = r.colsum.find(fi);
+            float* csp = cs != r.colsum.end() && OW(op.dgelu_pre) ? cs->second : nullptr;
             gemm_rowwise(r, g, ldg, false, fp(r, op.in[1]), cols, false, gp(r, op.dgelu_pre), cols, cdt, rows, cols,
-                         out_f, !OW(op.dgelu_pre), nullptr, 2, fp(r, op.dgelu_pre));
+                         out_f, !OW(op.dgelu_pre), nullptr, 2, fp(r, op.dgelu_pre), nullptr, csp);
+            if (csp && sbk::gemm_last_colsum()) r.colsum_ready.insert(fi);
         } else {
             GT gx = gtarget(r, op.in[0]);
             if (gx.temp) ldgx = cols;
@@ -1281,8 +1307,12 @@ public:
                      rows, !OW(op.in[1]), nullptr, 0, nullptr, ws);
         launches += (part & 1) ? 2 : 1;
         if (op.has_bias && op.bias_grad) {
-            sbk::bias_grad(g, cdt, ldg, rows, out_f, (float*)gp(r, op.in[2]), (float*)(side ? r.ws2 : r.ws), ws,
-                           !OW(op.in[2]));
+            const int oi = (int)(&op - r.P.fwd.data());
+            if (r.colsum_ready.erase(oi))  // partials from the consumer's dgrad epilogue
+                sbk::bias_grad_partials(r.colsum.at(oi), rows / 32, out_f, (float*)gp(r, op.in[2]), ws, !OW(op.in[2]));
+            else
+                sbk::bias_grad(g, cdt, ldg, rows, out_f, (float*)gp(r, op.in[2]), (float*)(side ? r.ws2 : r.ws), ws,
+                               !OW(op.in[2]));
             ++launches;
         }
     }

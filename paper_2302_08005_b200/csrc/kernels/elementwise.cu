@@ -634,6 +634,10 @@ __global__ void __launch_bounds__(1024) k_bias_final(const float* part, i64 chun
         db[c] = accum ? db[c] + t : t;
     }
 }
+void bias_grad_partials(const float* partials, i64 chunks, i64 cols, float* db, cudaStream_t s, bool accum) {
+    k_bias_final<<<(unsigned)((cols + 31) / 32), 1024, 0, s>>>(partials, chunks, cols, db, accum);
+    SBK_CHECK_LAUNCH();
+}
 size_t bias_grad_workspace(i64 rows, i64 cols) { return (size_t)((rows + kBiasChunkV - 1) / kBiasChunkV) * cols * 4; }
 void bias_grad(const void* g, DT tg, i64 ld, i64 rows, i64 cols, float* db, float* ws, cudaStream_t s, bool accum) {
     i64 chunks = (rows + kBiasChunk - 1) / kBiasChunk;

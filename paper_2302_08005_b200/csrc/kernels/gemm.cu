@@ -84,7 +84,10 @@ int gemm_last_engine() { return g_last_engine; }
 void gemm_force_simt(bool on) { g_force_simt = on; }
 void gemm_set_engine(int e) { g_gemm_max_engine = e; }
 
+extern bool g_tc2_colsum_done;
+bool gemm_last_colsum() { return g_tc2_colsum_done; }
 void gemm(const Gemm& g, cudaStream_t s) {
+    g_tc2_colsum_done = false;
     if (g.M == 0 || g.N == 0) return;
     if (!g_force_simt && g_gemm_max_engine == 0 && gemm_tc2_try(g, s)) {
         g_last_engine = 2;

@@ -163,6 +163,7 @@ struct Epi2 {
     int partial;  // split-K: fp32 partials through tC at row z*M + m
     long long M, N;
     unsigned long long* ts;  // debugging timeline (SB_GEMM_TS): cluster 0, [role][k-block]
+    float* colsum;           // column sums of the output per 32 rows ([M/32][N]) or null
 };
 __device__ __forceinline__ unsigned long long gtime2() {
     unsigned long long t;
@@ -418,6 +419,35 @@ __global__ void __cluster_dims__(2 * PAIRS, 1, 1) __launch_bounds__(320, 1)
                     }
                     continue;
                 }
+                if (ep.colsum) {
+                    // this warp's 32 rows summed per column (a bias gradient's partial): a
+                    // reduce-scatter across the lanes, halving the columns each level, ends
+                    // with lane L holding column L (fixed order: deterministic)
+                    float t16[16], t8[8], t4[4], t2[2];
+#pragma unroll
+                    for (int c = 0; c < 16; ++c) {
+                        const bool up = lane & 16;
+                        t16[c] = (up ? v[c + 16] : v[c]) + __shfl_xor_sync(0xffffffffu, up ? v[c] : v[c + 16], 16);
+                    }
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        const bool up = lane & 8;
+                        t8[c] = (up ? t16[c + 8] : t16[c]) + __shfl_xor_sync(0xffffffffu, up ? t16[c] : t16[c + 8], 8);
+                    }
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        const bool up = lane & 4;
+                        t4[c] = (up ? t8[c + 4] : t8[c]) + __shfl_xor_sync(0xffffffffu, up ? t8[c] : t8[c + 4], 4);
+                    }
+#pragma unroll
+                    for (int c = 0; c < 2; ++c) {
+                        const bool up = lane & 2;
+                        t2[c] = (up ? t4[c + 2] : t4[c]) + __shfl_xor_sync(0xffffffffu, up ? t4[c] : t4[c + 2], 2);
+                    }
+                    const bool up = lane & 1;
+                    const float t1 = (up ? t2[1] : t2[0]) + __shfl_xor_sync(0xffffffffu, up ? t2[0] : t2[1], 1);
+                    ep.colsum[(row0 >> 5) * ep.N + col + lane] = t1;
+                }
                 uint8_t* buf = mybuf;
                 if (nst >= 1 && lane == 0) bulk_wait_read<0>();
                 __syncwarp();
@@ -540,6 +570,7 @@ void launch2(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc
 void gemm_set_sm_reserve(int n) { g_sm_reserve = std::max(0, n); }
 
 bool g_tc2_disabled = false;
+bool g_tc2_colsum_done = false;
 int g_tc2_bn = 0;  // cluster tile N: 0 default (256), 128 or 256 forced (tests)
 void gemm2_set_tile_n(int bn) { g_tc2_bn = bn; }
 
@@ -619,6 +650,7 @@ bool gemm_tc2_try(const Gemm& g, cudaStream_t s) {
     ep.partial = splits > 1;
     ep.M = M;
     ep.N = N;
+    ep.colsum = splits == 1 && !ep.accumulate ? g.colsum : nullptr;
     if (splits > 1) {
         if (!make_store_map(&tc, g.ws, true, N, (long long)splits * M, N)) return false;
     } else if (!ep.accumulate) {
@@ -661,6 +693,7 @@ bool gemm_tc2_try(const Gemm& g, cudaStream_t s) {
             fprintf(stderr, "\n");
         }
     }
+    g_tc2_colsum_done = ep.colsum != nullptr;
     if (splits > 1)
         splitk_reduce_launch((const float*)g.ws, splits, M, N, g.C, g.tc, ldc, g.bias, g.accumulate, s);
     return true;

@@ -39,8 +39,13 @@ struct Gemm {
     void* aux = nullptr;  // pre-activation (same layout as C) when epilogue == gelu
     void* ws = nullptr;   // scratch for deterministic split-K partials (optional)
     size_t ws_bytes = 0;
+    // optional: fp32 column sums of the output, one row per 32 output rows ([M/32][N]) —
+    // produced by the 2-SM kernel's epilogue when it can (gemm_last_colsum() reports it)
+    float* colsum = nullptr;
 };
 void gemm(const Gemm& g, cudaStream_t s);
+// whether the last gemm() call wrote g.colsum
+bool gemm_last_colsum();
 // Which engine the last gemm() call used: 0 SIMT, 1 tcgen05 1-SM, 2 tcgen05 2-SM (tests/bench).
 int gemm_last_engine();
 // engine cap: 0 best available, 1 at most the 1-SM tcgen05 kernel, 2 SIMT only
@@ -136,6 +141,8 @@ void bias_dropout_residual_ln_bwd(const void* sum, const float* mean, const floa
 size_t bdrln_bwd_workspace(i64 rows, i64 n);
 
 // column sums of g (rows x cols) into fp32 db (+=)
+// db (+)= the fixed-order sum of `chunks` rows of fp32 column partials ([chunks][cols])
+void bias_grad_partials(const float* partials, i64 chunks, i64 cols, float* db, cudaStream_t s, bool accum);
 void bias_grad(const void* g, DT tg, i64 ld, i64 rows, i64 cols, float* db, float* workspace, cudaStream_t s,
                bool acc = true);
 size_t bias_grad_workspace(i64 rows, i64 cols);

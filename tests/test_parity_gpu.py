@@ -218,6 +218,31 @@ def test_ledger_matches_reference():
         assert ex.ledger() == r.meta["ledger_bytes"]
 
 
+def test_bias_grad_from_dgrad_epilogue(monkeypatch):
+    """The FFN's first bias gradient comes from column partials the consuming dGeLU dgrad
+    GEMM's epilogue writes (fp32, per 32 rows) instead of a second pass over the
+    pre-activation gradient: only that gradient changes (summation order), every other
+    one is bitwise the same as with the separate pass (SB_BIAS_EPI=0), and both stay
+    within the stated tolerance of the reference."""
+    cfg = dict(layers=2, hidden=256, heads=4, vocab=32, batch=8, seq=128, p=0.1)
+    script = recipes.c2_script(2, checkpoint_layers=[1])
+    m, applied = build(cfg, script, 1)
+    x = m.random_inputs(9)
+    res = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("SB_BIAS_EPI", flag)
+        ex = sb.Executor(applied, "train", 123, 1, dtype="bf16")
+        ex.forward(x)
+        res[flag] = ex.backward().params
+    changed = [k for k in res["1"] if res["1"][k].tobytes() != res["0"][k].tobytes()]
+    assert changed and all(k.endswith("dense1.bias") for k in changed), changed  # (the FFN's first Linear)
+    for k in changed:
+        assert rel_l2(res["1"][k], res["0"][k]) <= 1e-3, k
+    with ref.run("toy_bert", schedule=script, mode="train", seed=123, input_seed=9, **cfg) as r:
+        want = r.grads(0)
+    compare_grads(res["1"], {k: v.ravel() for k, v in want.items()}, BF16_GRAD_TOL, rel_l2)
+
+
 def test_determinism_bitwise():
     m, applied = build(TOY, recipes.c2_script(2), 1)
     x = m.random_inputs(9)
