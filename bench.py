@@ -289,9 +289,12 @@ def main():
     if rank != 0:
         return
     burst, sustained, hbm, src = peaks()
-    traffic = None
+    traffic, tf = None, None
     try:  # DRAM bytes of the step's GEMM launches from the committed ncu capture (profiles/README.md)
-        with open(os.path.join(ROOT, "profiles", "r1_gemm_traffic.json")) as f:
+        tf = os.path.join(ROOT, "profiles", "r2", "gemm_traffic.json")
+        if not os.path.exists(tf):
+            tf = os.path.join(ROOT, "profiles", "r1_gemm_traffic.json")
+        with open(tf) as f:
             tr = json.load(f)
         if world == 1 and cfg["layers"] == CFG["layers"] and cfg["batch"] == CFG["batch"]:
             traffic = tr["dram_read_bytes_per_step"] + tr["dram_write_bytes_per_step"]
@@ -313,7 +316,7 @@ def main():
         "roofline": {"bound": "tensor", "kernel": "tcgen05 GEMMs (all Linear fwd/dgrad/wgrad of the step)",
                      "achieved": achieved, "peak": sustained, "unit": "TFLOP/s", "frac": achieved / sustained,
                      "peak_source": f"bf16_tflops_sustained ({src})", "traffic": traffic,
-                     "traffic_unit": "DRAM bytes per step of all GEMM launches (ncu, profiles/r1_gemm_traffic.json)",
+                     "traffic_unit": f"DRAM bytes per step of all GEMM launches (ncu, {os.path.relpath(tf, ROOT) if traffic and tf else 'n/a'})",
                      "flop_per_dram_byte": (gemm_tflop * 1e12 / traffic) if traffic else None,
                      "gemm_ms_per_step": gemm_ms, "gemm_tflop_per_step": gemm_tflop},
         "model_tflops": model_tflops, "model_flops_frac": model_tflops / sustained,
