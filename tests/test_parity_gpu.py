@@ -243,6 +243,26 @@ def test_bias_grad_from_dgrad_epilogue(monkeypatch):
     compare_grads(res["1"], {k: v.ravel() for k, v in want.items()}, BF16_GRAD_TOL, rel_l2)
 
 
+def test_bias_grad_from_dgrad_epilogue_tp2(monkeypatch):
+    """The same fold under tensor parallelism (tp_script at world 2, lockstep ranks): per rank
+    only the column-parallel dense1 bias gradient changes, within 1e-3 of the separate pass."""
+    cfg = dict(layers=2, hidden=256, heads=4, vocab=32, batch=8, seq=128, p=0.1)
+    m, applied = build(cfg, recipes.tp_script(2, 2), 2)
+    x = m.random_inputs(9)
+    res = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("SB_BIAS_EPI", flag)
+        ex = sb.Executor(applied, "train", 123, 2, dtype="bf16")
+        ex.forward(x)
+        res[flag] = [g.params for g in ex.backward_all_ranks()]
+    for rank in range(2):
+        a, b = res["1"][rank], res["0"][rank]
+        changed = [k for k in a if a[k].tobytes() != b[k].tobytes()]
+        assert changed and all(k.endswith("dense1.bias") for k in changed), (rank, changed)
+        for k in changed:
+            assert rel_l2(a[k], b[k]) <= 1e-3, (rank, k)
+
+
 def test_determinism_bitwise():
     m, applied = build(TOY, recipes.c2_script(2), 1)
     x = m.random_inputs(9)
