@@ -184,8 +184,8 @@ __global__ void __launch_bounds__(32 * kW) k_bdrln_fwd_v(const T* partial, const
 // loads issued before any math: bytes in flight for HBM): few registers, 16-warp
 // blocks; the row mean and variance are combined across the WPR warps through
 // shared memory in a fixed order.
-template <class T, int CPL, int WPR, int NR>
-__global__ void __launch_bounds__(512, 2) k_bdrln_fwd_w(const T* partial, const T* bias, const T* res, const T* gamma,
+template <class T, int CPL, int WPR, int NR, int MINB = 2>
+__global__ void __launch_bounds__(512, MINB) k_bdrln_fwd_w(const T* partial, const T* bias, const T* res, const T* gamma,
                                                      const T* beta, T* sum, T* y, float* mean, float* rstd, i64 rows,
                                                      int n, float eps, uint64_t s1, uint64_t thr, float dscale,
                                                      const uint32_t* keep) {
@@ -646,11 +646,22 @@ bool bdrln_fwd_vec(const void* partial, const void* bias, const void* res, const
                 if constexpr (CPL % 4 == 0) {
                     // 4 warps per row, 16-warp blocks (4 rows per block)
                     if ((thr == 0 || keep) && !ln_narrow()) {
-                        // 4 warps per row, persistent grid of two 16-warp blocks per SM (<= 64 registers)
-                        const unsigned blocks = (unsigned)std::min<i64>(296, (rows + 3) / 4);
-                        k_bdrln_fwd_w<T, CPL, 4, 1><<<blocks, 512, 0, s>>>(
-                            (const T*)partial, (const T*)bias, (const T*)res, (const T*)gamma, (const T*)beta, (T*)sum,
-                            (T*)y, mean, rstd, rows, (int)n, eps, s1, thr, dscale, keep);
+                        // 4 warps per row, persistent grid of two 16-warp blocks per SM (<= 64 registers);
+                        // 2048-wide bf16 rows (CPL 8): one block per SM (<= 128 registers: 292 B of
+                        // spills at 64)
+                        static int sms = 0;
+                        if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+                        if constexpr (CPL >= 8) {
+                            const unsigned blocks = (unsigned)std::min<i64>(sms, (rows + 3) / 4);
+                            k_bdrln_fwd_w<T, CPL, 4, 1, 1><<<blocks, 512, 0, s>>>(
+                                (const T*)partial, (const T*)bias, (const T*)res, (const T*)gamma, (const T*)beta, (T*)sum,
+                                (T*)y, mean, rstd, rows, (int)n, eps, s1, thr, dscale, keep);
+                        } else {
+                            const unsigned blocks = (unsigned)std::min<i64>(2 * sms, (rows + 3) / 4);
+                            k_bdrln_fwd_w<T, CPL, 4, 1><<<blocks, 512, 0, s>>>(
+                                (const T*)partial, (const T*)bias, (const T*)res, (const T*)gamma, (const T*)beta, (T*)sum,
+                                (T*)y, mean, rstd, rows, (int)n, eps, s1, thr, dscale, keep);
+                        }
                         return;
                     }
                 }
