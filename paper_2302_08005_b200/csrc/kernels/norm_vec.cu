@@ -665,6 +665,18 @@ bool bdrln_fwd_vec(const void* partial, const void* bias, const void* res, const
                         return;
                     }
                 }
+                if constexpr (CPL == 3) {
+                    // 768-wide bf16 rows (T5-base): 3 warps per row, 15-warp blocks (5 rows), two per SM
+                    if ((thr == 0 || keep) && !ln_narrow()) {
+                        static int sms3 = 0;
+                        if (!sms3) cudaDeviceGetAttribute(&sms3, cudaDevAttrMultiProcessorCount, 0);
+                        const unsigned blocks = (unsigned)std::min<i64>(2 * sms3, (rows + 4) / 5);
+                        k_bdrln_fwd_w<T, 3, 3, 1><<<blocks, 480, 0, s>>>(
+                            (const T*)partial, (const T*)bias, (const T*)res, (const T*)gamma, (const T*)beta, (T*)sum,
+                            (T*)y, mean, rstd, rows, (int)n, eps, s1, thr, dscale, keep);
+                        return;
+                    }
+                }
                 k_bdrln_fwd_v<T, CPL><<<(unsigned)((rows + kW - 1) / kW), 32 * kW, 0, s>>>(
                     (const T*)partial, (const T*)bias, (const T*)res, (const T*)gamma, (const T*)beta, (T*)sum, (T*)y,
                     mean, rstd, rows, (int)n, eps, s1, thr, dscale, keep);
@@ -728,6 +740,19 @@ bool ln_bwd_vec(int mode, const void* x, const float* mean, const float* rstd, c
                     }
                     return;
                   }
+                }
+                if constexpr (CPL == 3) {
+                    // 768-wide bf16 rows (T5-base): 3 warps per row (one chunk each), 15-warp
+                    // blocks (5 rows), one per SM
+                    if ((thr == 0 || keep) && !ln_narrow()) {
+                        const size_t sm2 = (size_t)16 * ncol * (n / 3) * 4 + 2 * 16 * 2 * 4;
+                        auto k = mode == 0 ? k_ln_bwd_w<T, 3, 0, 3> : k_ln_bwd_w<T, 3, 1, 3>;
+                        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+                        k<<<nblocks, 480, sm2, s>>>((const T*)x, mean, rstd, (const T*)gamma, (const T*)g, (T*)gx,
+                                                    (T*)gres, gx_acc, rows, (int)n, s1, thr, dscale, keep, ws, ncol,
+                                                    gres_acc, (const T*)gext);
+                        return;
+                    }
                 }
                 if (mode == 0) launch(k_ln_bwd_v<T, CPL, 0>);
                 else launch(k_ln_bwd_v<T, CPL, 1>);

@@ -6,7 +6,7 @@ ref = {}
 for name in sys.argv[1:]:
     L = c.CDLL(name)
     L.sb_bias_dropout_residual_ln_fwd.argtypes = [vp] * 9 + [c.c_int, i64, i64, c.c_float, c.c_uint64, c.c_uint64, c.c_double, vp]
-    for rows, n in [(16384, 1024), (8192, 2048)]:
+    for rows, n in [(16384, 1024), (8192, 2048), (16384, 768), (4096, 768)]:
         g0 = torch.Generator(device="cuda").manual_seed(5)
         x = torch.randn(rows, n, device="cuda", generator=g0).bfloat16(); r = torch.randn(rows, n, device="cuda", generator=g0).bfloat16()
         bias = torch.randn(n, device="cuda", generator=g0).bfloat16()
@@ -25,5 +25,5 @@ for name in sys.argv[1:]:
         if key not in ref:
             ref[key] = out; cmp = "reference"
         else:
-            cmp = "bitwise " + str([bool(torch.equal(p, q)) for p, q in zip(out, ref[key])])
+            cmp = "bitwise " + str([bool(torch.equal(p, q)) for p, q in zip(out, ref[key])]) + " relL2 " + str(["%.1e" % ((p - q).norm() / q.norm()).item() for p, q in zip(out, ref[key])])
         print(f"{name.split('/')[-1]:10s} rows {rows} n {n}: {us:6.1f} us  {rows*n*2*4/us/1e6:.2f} TB/s  {cmp}", flush=True)

@@ -7,7 +7,7 @@ for name in sys.argv[1:]:
     L.sb_layernorm_bwd.argtypes = [vp] * 8 + [c.c_int, i64, i64, c.c_int, vp, vp]
     L.sb_bias_dropout_residual_ln_fwd.argtypes = [vp] * 9 + [c.c_int, i64, i64, c.c_float, c.c_uint64, c.c_uint64, c.c_double, vp]
     L.sb_bias_dropout_residual_ln_bwd.argtypes = [vp] * 10 + [c.c_int, i64, i64, c.c_uint64, c.c_uint64, c.c_double, vp, vp]
-    for rows, n, mode in [(16384, 1024, 1), (16384, 1024, 0), (8192, 2048, 0), (8192, 2048, 1)]:
+    for rows, n, mode in [(16384, 1024, 1), (16384, 1024, 0), (8192, 2048, 0), (8192, 2048, 1), (16384, 768, 1), (16384, 768, 0)]:
         x = torch.randn(rows, n, device="cuda").bfloat16(); g = torch.randn_like(x)
         gam = torch.ones(n, device="cuda").bfloat16(); bet = torch.zeros_like(gam)
         y, s = torch.empty_like(x), torch.empty_like(x)

@@ -9,7 +9,7 @@ for name in sys.argv[1:]:
     L.sb_layernorm_bwd.argtypes = [vp] * 8 + [c.c_int, i64, i64, c.c_int, vp, vp]
     L.sb_bias_dropout_residual_ln_fwd.argtypes = [vp] * 9 + [c.c_int, i64, i64, c.c_float, c.c_uint64, c.c_uint64, c.c_double, vp]
     L.sb_bias_dropout_residual_ln_bwd.argtypes = [vp] * 10 + [c.c_int, i64, i64, c.c_uint64, c.c_uint64, c.c_double, vp, vp]
-    for rows, n, mode in [(16384, 1024, 1), (16384, 1024, 0), (8192, 2048, 0), (8192, 2048, 1)]:
+    for rows, n, mode in [(16384, 1024, 1), (16384, 1024, 0), (8192, 2048, 0), (8192, 2048, 1), (16384, 768, 1), (16384, 768, 0), (4096, 768, 1)]:
         g0 = torch.Generator(device="cuda").manual_seed(5)
         x = torch.randn(rows, n, device="cuda", generator=g0).bfloat16(); g = torch.randn(rows, n, device="cuda", generator=g0).bfloat16()
         gam = (1 + 0.1 * torch.randn(n, device="cuda", generator=g0)).bfloat16(); bet = torch.zeros_like(gam)
