@@ -435,7 +435,7 @@ __global__ void __launch_bounds__(32 * kW, 1)
 // per-column dgamma/dbeta/dbias partials dominate), so 16-warp blocks fit and
 // co-reside with other work. The two row sums are combined across the WPR warps
 // through shared memory in a fixed order (deterministic).
-template <class T, int CPL, int MODE, int WPR, int MINB = (WPR >= 8 ? 2 : 1)>
+template <class T, int CPL, int MODE, int WPR, int MINB = 1>
 __global__ void __launch_bounds__(512, MINB)
     k_ln_bwd_w(const T* x, const float* mean, const float* rstd, const T* gamma, const T* g, T* gx, T* gres, bool gx_acc,
                i64 rows, int n, uint64_t s1, uint64_t thr, float dscale, const uint32_t* keep, float* ws, int ncol,
@@ -711,8 +711,8 @@ bool ln_bwd_vec(int mode, const void* x, const float* mean, const float* rstd, c
                 };
                 if constexpr (CPL % 4 == 0) {
                   if ((thr == 0 || keep) && !ln_narrow()) {
-                    // 2 or 4 warps per row, one 16-warp block per SM (<= 128 registers); SB_LN_WPR=2 / 4
-                    // forces 2 / 4 warps per row at CPL 4, SB_LN_WPR=8 forces 8 (two blocks per SM) at CPL 8
+                    // 2, 4 or 8 warps per row, one 16-warp block per SM (<= 128 registers); SB_LN_WPR=2 / 4
+                    // forces 2 / 4 warps per row at CPL 4, SB_LN_WPR=4 / 8 forces 4 / 8 at CPL 8
                     static const int wpr_env = getenv("SB_LN_WPR") ? atoi(getenv("SB_LN_WPR")) : 0;
                     auto go = [&](auto wc) {
                         constexpr int WPR = decltype(wc)::value;
@@ -726,9 +726,10 @@ bool ln_bwd_vec(int mode, const void* x, const float* mean, const float* rstd, c
                         return nb;
                     };
                     if constexpr (CPL >= 8) {
-                        // (2048-wide bf16 rows: 4 warps per row at one block per SM beat 8 at two,
-                        // 45.1 -> 35.0 us plain and 53.1 -> 45.2 us fused at 8192 rows — ln_minb2.log)
-                        if (wpr_env == 8) go(std::integral_constant<int, 8>{});
+                        // 2048-wide bf16 rows, one block per SM: the plain backward with 4 warps per
+                        // row (35.0 us at 8192 rows), the fused one with 8 (41.3 us; 45.0 with 4,
+                        // which spills) — ln_minb2.log, ln_wpr8.log
+                        if (wpr_env == 8 || (wpr_env == 0 && mode == 1)) go(std::integral_constant<int, 8>{});
                         else go(std::integral_constant<int, 4>{});
                     } else {
                         // one 16-warp block per SM (<= 128 registers, no spills): the plain LayerNorm
