@@ -1103,7 +1103,7 @@ public:
                 x.rowwise(rows, cols, ldx);
                 i64 out_f = w.shape[0];
                 gemm_rowwise(r, fp(r, op.in[0]), ldx, false, fp(r, op.in[1]), cols, true, fp(r, op.out[0]), out_f, cdt, rows,
-                             out_f, cols, false, op.bias_on ? fp(r, op.in[2]) : nullptr);
+                             out_f, cols, false, op.bias_on ? fp(r, op.in[2]) : nullptr, op.act ? 3 : 0);
                 break;
             }
             case K::FusedLinearGelu: {
@@ -1290,6 +1290,10 @@ public:
             gemm_rowwise(r, g, ldg, false, fp(r, op.in[1]), cols, false, gp(r, op.dgelu_pre), cols, cdt, rows, cols,
                          out_f, !OW(op.dgelu_pre), nullptr, 2, fp(r, op.dgelu_pre), nullptr, csp);
             if (csp && sbk::gemm_last_colsum()) r.colsum_ready.insert(fi);
+        } else if (op.drelu) {
+            // dx lands as the gradient at the folded ReLU's input: (g W) * (x > 0), x this op's input
+            gemm_rowwise(r, g, ldg, false, fp(r, op.in[1]), cols, false, gp(r, op.in[0]), cols, cdt, rows, cols, out_f,
+                         !OW(op.in[0]), nullptr, 4, fp(r, op.in[0]));
         } else {
             GT gx = gtarget(r, op.in[0]);
             if (gx.temp) ldgx = cols;

@@ -1035,6 +1035,67 @@ static void fuse_residual_stream(Plan& P, const LowerOptions& o) {
     }
 }
 
+// Linear -> ReLU -> one Linear-like consumer (T5's feed-forward: wi -> relu -> wo): the ReLU
+// runs in the first GEMM's epilogue and its backward in the consumer's dgrad epilogue (the
+// mask from the consumer's own input: relu(z) > 0 <=> z > 0), so neither the pre-activation
+// nor its gradient is materialised (SB_RELU_FUSE=0 keeps the separate op). Same values: the
+// epilogue computes max(z, 0) on the fp32 accumulator, then rounds once.
+static void fuse_linear_relu(Plan& P, const LowerOptions& o) {
+    static const bool on = !(getenv("SB_RELU_FUSE") && atoi(getenv("SB_RELU_FUSE")) == 0);
+    if (!on || !o.fused_kernels) return;
+    const size_t n = P.fwd.size();
+    std::map<int, std::vector<int>> readers, producer_of;
+    for (size_t i = 0; i < n; ++i) {
+        for (int v : P.fwd[i].in) readers[P.views[(size_t)v].st].push_back((int)i);
+        for (int v : P.fwd[i].out) producer_of[P.views[(size_t)v].st].push_back((int)i);
+    }
+    for (int v : P.outputs) readers[P.views[(size_t)v].st].push_back(1 << 30);
+    auto st = [&](int v) { return P.views[(size_t)v].st; };
+    auto plain = [&](int v) {
+        const View& w = P.views[(size_t)v];
+        return w.off == 0 && w.contiguous() && w.g_contiguous() && w.st == w.gst;
+    };
+    std::vector<char> dead(n, 0);
+    for (size_t ir = 0; ir < n; ++ir) {
+        const Op& R = P.fwd[ir];
+        if (R.k != K::Relu || R.in.size() != 1 || R.out.size() != 1) continue;
+        const int pre = R.in[0], y = R.out[0];
+        auto pp = producer_of.find(st(pre));
+        if (pp == producer_of.end() || pp->second.size() != 1) continue;
+        const int il = pp->second[0];
+        Op& L = P.fwd[(size_t)il];
+        if (L.k != K::Linear || L.allreduce || L.qkv || L.act || L.out.size() != 1 || L.out[0] != pre) continue;
+        auto& rp = readers[st(pre)];
+        auto& ry = readers[st(y)];
+        if (rp.size() != 1 || rp[0] != (int)ir || ry.size() != 1 || ry[0] >= (1 << 30)) continue;
+        if (!plain(pre) || !plain(y) || P.views[(size_t)pre].shape != P.views[(size_t)y].shape) continue;
+        // (the consumer's dgrad epilogue writes the gradient storage directly)
+        if (P.st[(size_t)P.views[(size_t)y].gst].gdt != P.cdt || P.st[(size_t)P.views[(size_t)y].st].dt != P.cdt) continue;
+        Op& C = P.fwd[(size_t)ry[0]];
+        if ((C.k != K::Linear && C.k != K::FusedLinearGelu && C.k != K::FusedLinearResLN) || C.in[0] != y || C.drelu)
+            continue;
+        bool other_use = false;
+        for (size_t k = 1; k < C.in.size(); ++k) other_use |= C.in[k] == y;
+        if (other_use || L.region != R.region || C.region != R.region) continue;
+        L.out[0] = y;
+        L.act = 1;
+        C.drelu = true;
+        dead[ir] = 1;
+    }
+    std::vector<Op> kept;
+    for (size_t i = 0; i < n; ++i)
+        if (!dead[i]) kept.push_back(std::move(P.fwd[i]));
+    P.fwd = std::move(kept);
+    for (auto& R : P.regions) R.first_op = R.last_op = -1;
+    for (size_t i = 0; i < P.fwd.size(); ++i) {
+        const int r = P.fwd[i].region;
+        if (r < 0) continue;
+        Region& R = P.regions[(size_t)r];
+        if (R.first_op < 0) R.first_op = (int)i;
+        R.last_op = (int)i;
+    }
+}
+
 Plan lower(const Module& root, const LowerOptions& o) {
     Plan P;
     P.rank = o.rank;
@@ -1045,6 +1106,7 @@ Plan lower(const Module& root, const LowerOptions& o) {
     Lowerer L(P, root, o);
     L.run();
     fuse_residual_stream(P, o);
+    fuse_linear_relu(P, o);
     // Drop empty regions; keep region-internal storages in scratch only when
     // nothing outside the region reads them.
     std::vector<Region> keep;

@@ -97,6 +97,12 @@ struct Op {
     // gradient of view `dgelu_pre` (the producing FusedLinearGelu's pre-activation)
     int dgelu_pre = -1;
     bool dgelu_fused = false;  // FusedLinearGelu whose GeLU backward was folded into its consumer
+    // Linear -> ReLU folded (lower.cpp fuse_linear_relu): act = 1 on the Linear (its out[0] is
+    // the ReLU's output, applied in the GEMM epilogue); drelu on the sole consumer of that
+    // output, whose dgrad epilogue multiplies by (x > 0) — x its own input — so the gradient
+    // it leaves is the one at the Linear's pre-activation
+    int act = 0;
+    bool drelu = false;
     // FusedLinearResLN whose pre-LN sum (out[2]) is also read by other ops (the residual
     // stream of a pre-LN block): its backward adds that sum's gradient (lower.cpp
     // fuse_residual_stream)

@@ -71,6 +71,10 @@ __global__ void __launch_bounds__(256) k_gemm_simt(Gemm g) {
                 v = gelu_f(v);
             } else if (g.epilogue == 2) {
                 v *= gelu_grad_f(to_f(X[ci]));  // dgrad straight into a GeLU input's gradient
+            } else if (g.epilogue == 3) {
+                v = fmaxf(v, 0.f);  // ReLU
+            } else if (g.epilogue == 4) {
+                v = to_f(X[ci]) > 0.f ? v : 0.f;  // dgrad times the ReLU mask of the activation X
             }
             if (g.accumulate) v += to_f(C[ci]);
             C[ci] = from_f<TC>(v);

@@ -165,15 +165,21 @@ __device__ __forceinline__ void epilogue_chunk(const Epi& ep, int z, long long r
         }
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = gelu_fast(v[j]);
-    } else if (ep.gelu == 2) {
+    } else if (ep.gelu == 2 || ep.gelu == 4) {
         const uint4* ax = (const uint4*)(ep.aux + row * ep.ldc + col);
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             uint4 w = ax[j];
             const bf16* e = (const bf16*)&w;
 #pragma unroll
-            for (int t = 0; t < 8; ++t) v[8 * j + t] *= gelu_grad_fast(__bfloat162float(e[t]));
+            for (int t = 0; t < 8; ++t) {
+                const float a = __bfloat162float(e[t]);
+                v[8 * j + t] = ep.gelu == 2 ? v[8 * j + t] * gelu_grad_fast(a) : (a > 0.f ? v[8 * j + t] : 0.f);
+            }
         }
+    } else if (ep.gelu == 3) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j], 0.f);
     }
     if (ep.c_f32) {
         float4* dst = (float4*)((float*)ep.C + row * ep.ldc + col);
@@ -457,7 +463,7 @@ bool gemm_tc_try(const Gemm& g, cudaStream_t s) {
     if (g_tc_disabled) return false;
     if (g.ta != BF16 || g.tb != BF16 || g.batch != 1 || g.sCn != 1) return false;
     if (g.tc != BF16 && g.tc != F32) return false;
-    if (g.epilogue && (g.tc != BF16 || !g.aux)) return false;
+    if (g.epilogue && (g.tc != BF16 || (g.epilogue != 3 && !g.aux))) return false;
     if (g.bias && g.tbias != BF16) return false;
     const bool a_mn = g.sAm == 1 && g.sAk != 1, b_mn = g.sBn == 1 && g.sBk != 1;
     const bool a_k = g.sAk == 1 && !a_mn, b_k = g.sBk == 1 && !b_mn;

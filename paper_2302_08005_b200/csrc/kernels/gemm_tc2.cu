@@ -205,7 +205,7 @@ __global__ void __cluster_dims__(2 * PAIRS, 1, 1) __launch_bounds__(320, 1)
         tma_prefetch(&tA);
         tma_prefetch(&tB);
         if (!ep.accumulate) tma_prefetch(&tC);
-        if (ep.gelu) tma_prefetch(&tX);
+        if (ep.gelu == 1) tma_prefetch(&tX);
         for (int s = 0; s < G_ST; ++s) {
             mbar_init(&full[s], 2);
             mbar_init(&empty[s], PAIRS);  // freed by every pair's MMA commit
@@ -325,7 +325,7 @@ __global__ void __cluster_dims__(2 * PAIRS, 1, 1) __launch_bounds__(320, 1)
             tile_coords(tile, m0, n0, z);
             const long long row0 = m0 + (long long)rank * G_BM + q * 32;  // first row of this warp
             const bool row_ok = row0 < ep.M;
-            if (ep.gelu == 2 && row_ok) {
+            if ((ep.gelu == 2 || ep.gelu == 4) && row_ok) {
                 if (n0 + half * 32 < ep.N) aux_ld(axa, row0 + lane, n0 + half * 32);
                 if (half + 2 < G_BN / 32 && n0 + (half + 2) * 32 < ep.N) aux_ld(axb, row0 + lane, n0 + (half + 2) * 32);
             }
@@ -381,12 +381,18 @@ __global__ void __cluster_dims__(2 * PAIRS, 1, 1) __launch_bounds__(320, 1)
                     for (int j = 0; j < 16; ++j) pre[j] = pack_bf16(v[2 * j], v[2 * j + 1]);
 #pragma unroll
                     for (int j = 0; j < 32; ++j) v[j] = gelu_fast(v[j]);
-                } else if (ep.gelu == 2) {
+                } else if (ep.gelu == 3) {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j], 0.f);
+                } else if (ep.gelu == 2 || ep.gelu == 4) {
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {
                         const bf16* e = (const bf16*)&axa[j];
 #pragma unroll
-                        for (int t = 0; t < 8; ++t) v[8 * j + t] *= gelu_grad_fast(__bfloat162float(e[t]));
+                        for (int t = 0; t < 8; ++t) {
+                            const float a = __bfloat162float(e[t]);
+                            v[8 * j + t] = ep.gelu == 2 ? v[8 * j + t] * gelu_grad_fast(a) : (a > 0.f ? v[8 * j + t] : 0.f);
+                        }
                     }
 #pragma unroll
                     for (int j = 0; j < 4; ++j) axa[j] = axb[j];
@@ -582,7 +588,7 @@ bool gemm_tc2_try(const Gemm& g, cudaStream_t s) {
     if (g_tc2_disabled) return false;
     if (g.ta != BF16 || g.tb != BF16 || g.batch != 1 || g.sCn != 1) return false;
     if (g.tc != BF16 && g.tc != F32) return false;
-    if (g.epilogue && (g.tc != BF16 || !g.aux)) return false;
+    if (g.epilogue && (g.tc != BF16 || (g.epilogue != 3 && !g.aux))) return false;
     if (g.bias && g.tbias != BF16) return false;
     const bool a_mn = g.sAm == 1 && g.sAk != 1, b_mn = g.sBn == 1 && g.sBk != 1;
     const bool a_k = g.sAk == 1 && !a_mn, b_k = g.sBk == 1 && !b_mn;
@@ -656,7 +662,7 @@ bool gemm_tc2_try(const Gemm& g, cudaStream_t s) {
     } else if (!ep.accumulate) {
         if (!make_store_map(&tc, g.C, ep.c_f32, N, M, ldc)) return false;
     }
-    if (g.epilogue && splits == 1) {  // GeLU: pre-activation store map; dGeLU: pre-activation load map
+    if (g.epilogue == 1 && splits == 1) {  // GeLU: pre-activation store map
         if (!make_store_map(&tx, g.aux, false, N, M, ldc)) return false;
     }
     Sched2 sc{(int)m_blks, (int)n_blks, splits, kblocks / splits, pairs};

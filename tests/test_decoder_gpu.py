@@ -189,3 +189,28 @@ def test_residual_stream_fusion(tmp_path):
     # per block: attn.out_proj + ln_2 and mlp.c_proj + the next LayerNorm (block 1's ln_1, then ln_f)
     assert ka.get("FusedLinearResLN", 0) == 4 and kb.get("FusedLinearResLN", 0) == 0, (ka, kb)
     assert np.abs(a - b).max() <= 1e-5 * np.abs(b).max()
+
+
+def test_t5_relu_fold(tmp_path):
+    """T5's feed-forward wi -> relu -> wo: the ReLU runs in wi's GEMM epilogue and its backward
+    in wo's dgrad epilogue (lower.cpp fuse_linear_relu); SB_RELU_FUSE=0 keeps the separate op —
+    fp32: the same outputs and gradients up to rounding; no Relu op left in the fused plan."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import sys, json, numpy as np; sys.path.insert(0, %r)\n"
+            "import paper_2302_08005_b200 as sb\n"
+            "m = sb.t5(2, 2, 32, 4, 32, 2, 24, 16, 0.1); ex = sb.Executor(m, 'train', 5, 1)\n"
+            "o = ex.forward(m.random_inputs(3))[0]; g = ex.backward().params\n"
+            "np.save(sys.argv[1], np.concatenate([o.ravel()] + [g[k].ravel() for k in sorted(g)]))\n"
+            "print(json.dumps(ex.describe()['kinds']))\n") % root
+    res = []
+    for v in ("1", "0"):
+        f = str(tmp_path / f"r{v}.npy")
+        r = subprocess.run([sys.executable, "-c", code, f], capture_output=True, text=True, timeout=300,
+                           env=dict(os.environ, SB_RELU_FUSE=v))
+        assert r.returncode == 0, r.stderr
+        res.append((np.load(f), json.loads(r.stdout.strip().splitlines()[-1])))
+    (a, ka), (b, kb) = res
+    assert ka.get("Relu", 0) == 0 and kb.get("Relu", 0) == 4, (ka, kb)  # 2 encoder + 2 decoder blocks
+    assert np.abs(a - b).max() <= 1e-5 * np.abs(b).max()

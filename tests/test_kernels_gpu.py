@@ -260,6 +260,31 @@ def test_gemm_2sm_ragged_tiles(layout, M, N, K):
     assert bool((big[M:] == 7).all()) and bool((big[:, N:] == 7).all()), "written past the ragged edge"
 
 
+@pytest.mark.parametrize("cap", [0, 1, 2])
+def test_gemm_relu_epilogues(cap):
+    """The folded ReLU (T5's wi -> relu -> wo, lower.cpp fuse_linear_relu): epilogue 3 writes
+    max(x W^T + b, 0); epilogue 4 writes (g W) * (a > 0) for the activation a — on the 2-SM,
+    1-SM and SIMT engines, against fp32 torch."""
+    M, N, K = 512, 768, 256
+    g = torch.Generator(device="cuda").manual_seed(13)
+    x, w, b = (torch.randn(M, K, device="cuda", generator=g).bfloat16(), torch.randn(N, K, device="cuda", generator=g).bfloat16(),
+               torch.randn(N, device="cuda", generator=g).bfloat16())
+    y = torch.zeros(M, N, device="cuda", dtype=torch.bfloat16)
+    if cap == 2:
+        L.sb_gemm_force_simt(1)
+    try:
+        e = gemm(x, (K, 1), w, (1, K), y, M, N, K, bias=b, epi=3, cap=min(cap, 1))
+        close(y, torch.relu(x.float() @ w.float().T + b.float()))
+        gy, w2 = torch.randn(M, K, device="cuda", generator=g).bfloat16(), torch.randn(K, N, device="cuda", generator=g).bfloat16()
+        a = torch.randn(M, N, device="cuda", generator=g).bfloat16()
+        dx = torch.zeros(M, N, device="cuda", dtype=torch.bfloat16)
+        e2 = gemm(gy, (K, 1), w2, (N, 1), dx, M, N, K, epi=4, aux=a, cap=min(cap, 1))
+        close(dx, (gy.float() @ w2.float()) * (a.float() > 0))
+    finally:
+        L.sb_gemm_force_simt(0)
+    assert e == e2 == (2 - cap), (e, e2)
+
+
 # ------------------------------------------------------------------ attention
 L.sb_attn_fwd.argtypes = [ctypes.c_void_p] * 4 + [ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p] + \
     [ctypes.c_int64] * 4 + [ctypes.c_float, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_double, ctypes.c_int,
