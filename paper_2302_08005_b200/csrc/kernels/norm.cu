@@ -21,7 +21,7 @@ bool bdrln_fwd_vec(const void* partial, const void* bias, const void* res, const
                    const uint32_t* keep, cudaStream_t s);
 bool ln_bwd_vec(int mode, const void* x, const float* mean, const float* rstd, const void* gamma, const void* g, void* gx,
                 void* gres, bool gx_acc, bool gres_acc, DT t, i64 rows, i64 n, u64 s1, u64 thr, float dscale,
-                const uint32_t* keep, float* ws, int ncol, int nblocks, cudaStream_t s, const void* gext = nullptr);
+                const uint32_t* keep, float* ws, int ncol, int& nblocks, cudaStream_t s, const void* gext = nullptr);
 static int vec_blocks(i64 rows) { return (int)std::min<i64>(296, std::max<i64>(1, (rows + kWarps - 1) / kWarps)); }
 
 // ------------------------------------------------------------------ softmax

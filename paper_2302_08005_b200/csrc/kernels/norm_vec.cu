@@ -690,7 +690,7 @@ bool bdrln_fwd_vec(const void* partial, const void* bias, const void* res, const
 // partials per block to ws (the caller finishes with the fixed-order column sum).
 bool ln_bwd_vec(int mode, const void* x, const float* mean, const float* rstd, const void* gamma, const void* g, void* gx,
                 void* gres, bool gx_acc, bool gres_acc, DT t, i64 rows, i64 n, u64 s1, u64 thr, float dscale,
-                const uint32_t* keep, float* ws, int ncol, int nblocks, cudaStream_t s, const void* gext) {
+                const uint32_t* keep, float* ws, int ncol, int& nblocks, cudaStream_t s, const void* gext) {
     if (gext && !aligned16(gext)) return false;
     for (const void* p : {x, g, (const void*)gx})
         if (!aligned16(p)) return false;
@@ -719,7 +719,11 @@ bool ln_bwd_vec(int mode, const void* x, const float* mean, const float* rstd, c
                         const size_t sm2 = (size_t)16 * ncol * (n / WPR) * 4 + 2 * 16 * 2 * 4;
                         auto k = mode == 0 ? k_ln_bwd_w<T, CPL, 0, WPR> : k_ln_bwd_w<T, CPL, 1, WPR>;
                         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
-                        const int nb = nblocks;  // (the column finish reads one partial row per block)
+                        // one persistent block per SM (the column finish then sums one partial row per SM)
+                        static int sms_w = 0;
+                        if (!sms_w) cudaDeviceGetAttribute(&sms_w, cudaDevAttrMultiProcessorCount, 0);
+                        if (!getenv("SB_LN_TWO_WAVES")) nblocks = std::min(nblocks, sms_w);
+                        const int nb = nblocks;
                         k<<<nb, 512, sm2, s>>>((const T*)x, mean, rstd, (const T*)gamma, (const T*)g, (T*)gx, (T*)gres,
                                                gx_acc, rows, (int)n, s1, thr, dscale, keep, ws, ncol, gres_acc,
                                                (const T*)gext);
@@ -749,6 +753,9 @@ bool ln_bwd_vec(int mode, const void* x, const float* mean, const float* rstd, c
                         const size_t sm2 = (size_t)16 * ncol * (n / 3) * 4 + 2 * 16 * 2 * 4;
                         auto k = mode == 0 ? k_ln_bwd_w<T, 3, 0, 3> : k_ln_bwd_w<T, 3, 1, 3>;
                         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+                        static int sms_3 = 0;
+                        if (!sms_3) cudaDeviceGetAttribute(&sms_3, cudaDevAttrMultiProcessorCount, 0);
+                        if (!getenv("SB_LN_TWO_WAVES")) nblocks = std::min(nblocks, sms_3);
                         k<<<nblocks, 480, sm2, s>>>((const T*)x, mean, rstd, (const T*)gamma, (const T*)g, (T*)gx,
                                                     (T*)gres, gx_acc, rows, (int)n, s1, thr, dscale, keep, ws, ncol,
                                                     gres_acc, (const T*)gext);
