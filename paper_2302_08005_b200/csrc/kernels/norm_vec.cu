@@ -435,7 +435,7 @@ __global__ void __launch_bounds__(32 * kW, 1)
 // per-column dgamma/dbeta/dbias partials dominate), so 16-warp blocks fit and
 // co-reside with other work. The two row sums are combined across the WPR warps
 // through shared memory in a fixed order (deterministic).
-template <class T, int CPL, int MODE, int WPR, int MINB = 1>
+template <class T, int CPL, int MODE, int WPR, int MINB = 1, bool PF2 = (CPL >= 8 && CPL / WPR == 1)>
 __global__ void __launch_bounds__(512, MINB)
     k_ln_bwd_w(const T* x, const float* mean, const float* rstd, const T* gamma, const T* g, T* gx, T* gres, bool gx_acc,
                i64 rows, int n, uint64_t s1, uint64_t thr, float dscale, const uint32_t* keep, float* ws, int ncol,
@@ -454,19 +454,23 @@ __global__ void __launch_bounds__(512, MINB)
     // software pipeline: the next row's x / g / statistics are loaded while this row is processed
     const i64 rstep = (i64)gridDim.x * RPB;
     i64 row = (i64)blockIdx.x * RPB + slot;
-    typename V::R xn[CW], gn[CW];
-    float mun = 0.f, rsn = 0.f;
-    auto prefetch = [&](i64 r) {
+    // rows in flight: the next one (PF2: the next two — 2048-wide rows at one chunk per warp,
+    // 37.2 -> 35.3 us; no gain at 1024 / 768 — profiles/r2/ln_bwd_pf2_ab.log) loaded while this
+    // one is processed
+    typename V::R xn[CW], gn[CW], xn2[CW], gn2[CW];
+    float mun = 0.f, rsn = 0.f, mun2 = 0.f, rsn2 = 0.f;
+    auto load = [&](i64 r, typename V::R(&xd)[CW], typename V::R(&gd)[CW], float& mu_d, float& rs_d) {
         if (r >= rows) return;
 #pragma unroll
         for (int c = 0; c < CW; ++c) {
-            xn[c] = __ldcs((const typename V::R*)(x + r * n) + (part * CW + c) * 32 + lane);
-            gn[c] = __ldcs((const typename V::R*)(g + r * n) + (part * CW + c) * 32 + lane);
+            xd[c] = __ldcs((const typename V::R*)(x + r * n) + (part * CW + c) * 32 + lane);
+            gd[c] = __ldcs((const typename V::R*)(g + r * n) + (part * CW + c) * 32 + lane);
         }
-        mun = mean[r];
-        rsn = rstd[r];
+        mu_d = mean[r];
+        rs_d = rstd[r];
     };
-    prefetch(row);
+    load(row, xn, gn, mun, rsn);
+    if (PF2) load(row + rstep, xn2, gn2, mun2, rsn2);
     for (; row < rows; row += rstep, ++it) {
         float xv[CW][VN], gv[CW][VN];
 #pragma unroll
@@ -475,7 +479,18 @@ __global__ void __launch_bounds__(512, MINB)
             V::unpack(gn[c], gv[c]);
         }
         const float mu = mun, rs = rsn;
-        prefetch(row + rstep);
+        if (PF2) {
+#pragma unroll
+            for (int c = 0; c < CW; ++c) {
+                xn[c] = xn2[c];
+                gn[c] = gn2[c];
+            }
+            mun = mun2;
+            rsn = rsn2;
+            load(row + 2 * rstep, xn2, gn2, mun2, rsn2);
+        } else {
+            load(row + rstep, xn, gn, mun, rsn);
+        }
         float a = 0.f, b = 0.f;
 #pragma unroll
         for (int c = 0; c < CW; ++c) {
