@@ -198,7 +198,10 @@ int sb_executor_device_bytes(sb_executor* e, int64_t* bytes);
 
 /* ------------------------------------------------------- device kernels */
 /* dtype codes: 0 f32, 1 bf16, 2 f64. */
-/* linear_fwd / linear_dx / linear_dw / matmul_fwd — proj/src/executor.cpp:38-133 */
+/* linear_fwd / linear_dx / linear_dw / matmul_fwd — proj/src/executor.cpp:38-133.
+ * epilogue: 0 none; 1 C = gelu(v), aux = v (pre-activation); 2 C = gelu'(aux) * v (dgrad into a
+ * GeLU input); 3 C = max(v, 0); 4 C = v * (aux > 0) (dgrad through a ReLU whose output is aux);
+ * v = alpha * A B + bias. aux shares C's row stride. */
 int sb_gemm(const void* A, int ta, int64_t sAb, int64_t sAm, int64_t sAk, const void* B, int tb, int64_t sBb,
             int64_t sBk, int64_t sBn, void* C, int tc, int64_t sCb, int64_t sCm, int64_t sCn, int64_t batch, int64_t M,
             int64_t N, int64_t K, float alpha, int accumulate, const void* bias, int epilogue, void* aux, void* stream);
